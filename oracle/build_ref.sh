@@ -22,6 +22,16 @@ if [[ ! -f "$REF/include/dctplus/fast_transform.hpp" ]]; then
     echo "build_ref: reference not present at $REF; using prebuilt oracle/_ref if any"
     exit 0
 fi
+DEPS=("$HERE/ref_driver.cpp" "$HERE/fftw_shim/fftw3.h" "$ROOT/paper_2409_08970_b200/csrc/host/r2r.hpp" "$HERE/build_ref.sh")
+fresh=1
+for f in "$OUT/libdctref.so" "$OUT/acceptance"; do
+    [[ -f "$f" ]] || fresh=0
+    for d in "${DEPS[@]}"; do [[ -f "$f" && "$d" -nt "$f" ]] && fresh=0; done
+done
+if [[ $fresh == 1 && "${1:-}" != "--force" ]]; then
+    echo "build_ref: oracle/_ref is up to date"
+    exit 0
+fi
 mkdir -p "$OUT/include/dctplus"
 python3 - "$REF/include/dctplus/graph.hpp" "$OUT/include/dctplus/graph.hpp" <<'EOF'
 import sys

@@ -1,0 +1,783 @@
+// C ABI (include/dctplus_b200.h): plan construction on the host, constants
+// uploaded once per plan, batched apply through the sm_100a kernels.
+//
+// Compiled with -ffp-contract=off: the setup (host/setup.hpp) must reproduce
+// the reference's floating-point operations bit for bit.
+#include "dctplus_b200.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numbers>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime_api.h>
+
+#include "host/setup.hpp"
+#include "host/signal.hpp"
+#include "kernels/launch.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw CudaError(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return DCTP_OK;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return DCTP_INVALID_ARGUMENT;
+    } catch (const std::domain_error& e) {
+        g_last_error = e.what();
+        return DCTP_DOMAIN_ERROR;
+    } catch (const std::logic_error& e) {
+        g_last_error = e.what();
+        return DCTP_LOGIC_ERROR;
+    } catch (const CudaError& e) {
+        g_last_error = e.what();
+        return DCTP_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return DCTP_RUNTIME_ERROR;
+    } catch (...) {
+        g_last_error = "unknown error";
+        return DCTP_RUNTIME_ERROR;
+    }
+}
+
+/// Makes `device` current for the scope and restores the previous device.
+class DeviceScope {
+  public:
+    explicit DeviceScope(int device) {
+        cuda_check(cudaGetDevice(&prev_), "cudaGetDevice");
+        if (prev_ != device) cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        changed_ = prev_ != device;
+    }
+    ~DeviceScope() {
+        if (changed_) cudaSetDevice(prev_);
+    }
+
+  private:
+    int prev_ = 0;
+    bool changed_ = false;
+};
+
+void prepare_pool(int device) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(done.begin(), done.end(), device) != done.end()) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        std::uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done.push_back(device);
+}
+
+/// Packs host arrays into one device allocation (256-byte aligned pieces).
+class Blob {
+  public:
+    template <class T>
+    std::size_t add(const std::vector<T>& v) {
+        const std::size_t off = (bytes_.size() + 255) / 256 * 256;
+        bytes_.resize(off + std::max<std::size_t>(v.size() * sizeof(T), 1));
+        if (!v.empty()) std::memcpy(bytes_.data() + off, v.data(), v.size() * sizeof(T));
+        return off;
+    }
+    void* upload() {
+        void* d = nullptr;
+        cuda_check(cudaMalloc(&d, bytes_.size()), "cudaMalloc(plan constants)");
+        cuda_check(cudaMemcpy(d, bytes_.data(), bytes_.size(), cudaMemcpyHostToDevice), "cudaMemcpy(plan constants)");
+        return d;
+    }
+
+  private:
+    std::vector<unsigned char> bytes_;
+};
+
+template <class T>
+const T* at(void* base, std::size_t off) {
+    return reinterpret_cast<const T*>(static_cast<const unsigned char*>(base) + off);
+}
+
+/// Twiddle tables of length n in fp64 (exact index angles) and fp32.
+struct TwiddleOffsets {
+    std::size_t fft = 0, split = 0, rot = 0, cos4n = 0;
+};
+
+template <class T>
+TwiddleOffsets add_twiddles(Blob& blob, std::size_t n) {
+    const double pi = std::numbers::pi;
+    const std::size_t N = std::max<std::size_t>(n / 2, 1);
+    std::vector<T> fft(2 * std::max<std::size_t>(N / 2, 1)), split(2 * N), rot(2 * (N + 1)), c4(4 * n);
+    for (std::size_t k = 0; k < fft.size() / 2; ++k) {
+        const double a = 2.0 * pi * static_cast<double>(k) / static_cast<double>(N);
+        fft[2 * k] = static_cast<T>(std::cos(a));
+        fft[2 * k + 1] = static_cast<T>(-std::sin(a));
+    }
+    for (std::size_t k = 0; k < N; ++k) {
+        const double a = 2.0 * pi * static_cast<double>(k) / static_cast<double>(n);
+        split[2 * k] = static_cast<T>(std::cos(a));
+        split[2 * k + 1] = static_cast<T>(-std::sin(a));
+    }
+    for (std::size_t k = 0; k <= N; ++k) {
+        const double a = pi * static_cast<double>(k) / (2.0 * static_cast<double>(n));
+        rot[2 * k] = static_cast<T>(std::cos(a));
+        rot[2 * k + 1] = static_cast<T>(-std::sin(a));
+    }
+    for (std::size_t m = 0; m < 4 * n; ++m)
+        c4[m] = static_cast<T>(std::cos(pi * static_cast<double>(m) / (2.0 * static_cast<double>(n))));
+    TwiddleOffsets o;
+    o.fft = blob.add(fft);
+    o.split = blob.add(split);
+    o.rot = blob.add(rot);
+    o.cos4n = blob.add(c4);
+    return o;
+}
+
+template <class T>
+dctp::dev::Twiddles<T> twiddles_at(void* base, const TwiddleOffsets& o) {
+    return {at<T>(base, o.fft), at<T>(base, o.split), at<T>(base, o.rot), at<T>(base, o.cos4n)};
+}
+
+/// Device-side description of one Cauchy stage in both precisions.
+struct StageOffsets {
+    std::size_t src, x, rscale64, rscale32, dst, y, cscale64, cscale32;
+    int rows, cols;
+};
+
+dctp::dev::CauchyStage stage_at(void* base, const StageOffsets& s, bool f32, std::int64_t out_offset) {
+    return {at<int>(base, s.src), at<double>(base, s.x),
+            f32 ? static_cast<const void*>(at<float>(base, s.rscale32)) : at<double>(base, s.rscale64),
+            at<int>(base, s.dst), at<double>(base, s.y),
+            f32 ? static_cast<const void*>(at<float>(base, s.cscale32)) : at<double>(base, s.cscale64),
+            s.rows, s.cols, out_offset};
+}
+
+template <class T>
+std::vector<float> to_f32(const std::vector<T>& v) {
+    return std::vector<float>(v.begin(), v.end());
+}
+
+/// Host-side apply tables derived from a setup (fast_transform.hpp:94-125
+/// restated for the direct Cauchy route).
+struct ApplyTables {
+    std::vector<int> kept_idx, act_slot, pass_slot, pass_src;
+    std::vector<double> lam_kept, z_kept, neg_z_kept, nu, act_scale, pass_sign;
+};
+
+ApplyTables make_tables(const dctp::host::Setup& st) {
+    ApplyTables t;
+    for (std::size_t j : st.kept) {
+        t.kept_idx.push_back(static_cast<int>(j));
+        t.lam_kept.push_back(st.lambda[j]);
+        t.z_kept.push_back(st.z[j]);
+        t.neg_z_kept.push_back(-st.z[j]);
+    }
+    t.act_slot.assign(st.sub_mu.size(), -1);
+    t.nu = st.sub_mu;
+    t.act_scale.assign(st.sub_mu.size(), 0.0);
+    for (std::size_t s = 0; s < st.slots.size(); ++s) {
+        const auto& sl = st.slots[s];
+        if (sl.passthrough) {
+            t.pass_slot.push_back(static_cast<int>(s));
+            t.pass_src.push_back(static_cast<int>(sl.idx));
+            t.pass_sign.push_back(st.sigma[s]);
+        } else {
+            t.act_slot[sl.idx] = static_cast<int>(s);
+            // out_s = sigma_s a_s sum_j z_j shat_j / (lambda_j - nu)
+            t.act_scale[sl.idx] = st.sigma[s] * st.a[s];
+        }
+    }
+    return t;
+}
+
+template <class T>
+struct Scratch {
+    T* ptr = nullptr;
+    cudaStream_t stream = nullptr;
+    Scratch(std::size_t count, cudaStream_t s) : stream(s) {
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&ptr), std::max<std::size_t>(count, 1) * sizeof(T), s),
+                   "cudaMallocAsync(scratch)");
+    }
+    ~Scratch() {
+        if (ptr) cudaFreeAsync(ptr, stream);
+    }
+};
+
+} // namespace
+
+// ---------------------------------------------------------------------------
+
+struct dctp_plan {
+    dctp::host::Setup st;
+    dctp::host::Update update;
+    int device = 0;
+    void* blob = nullptr;
+    int* flag = nullptr;
+    TwiddleOffsets tw64, tw32;
+    StageOffsets fwd{}, inv{};
+    std::size_t pass_slot = 0, pass_src = 0, pass_sign64 = 0, pass_sign32 = 0;
+    std::size_t stage_desc = 0; // 4 CauchyStage descriptors: fwd64, fwd32, inv64, inv32
+    int n_pass = 0;
+
+    ~dctp_plan() {
+        if (blob) {
+            int prev = 0;
+            cudaGetDevice(&prev);
+            cudaSetDevice(device);
+            cudaFree(blob);
+            cudaFree(flag);
+            cudaSetDevice(prev);
+        }
+    }
+
+    const dctp::dev::CauchyStage* stage_dev(int which) const {
+        return at<dctp::dev::CauchyStage>(blob, stage_desc) + which;
+    }
+    template <class T>
+    dctp::dev::Twiddles<T> tw() const {
+        if constexpr (std::is_same_v<T, double>)
+            return twiddles_at<double>(blob, tw64);
+        else
+            return twiddles_at<float>(blob, tw32);
+    }
+    template <class T>
+    dctp::dev::Emit<T> emit_fwd() const {
+        const T* sign;
+        if constexpr (std::is_same_v<T, double>)
+            sign = at<double>(blob, pass_sign64);
+        else
+            sign = at<float>(blob, pass_sign32);
+        return {at<int>(blob, pass_slot), at<int>(blob, pass_src), sign, n_pass};
+    }
+    template <class T>
+    dctp::dev::Emit<T> emit_inv() const {
+        dctp::dev::Emit<T> e = emit_fwd<T>();
+        std::swap(e.to, e.from);
+        return e;
+    }
+};
+
+static void upload_plan(dctp_plan& p) {
+    const auto& st = p.st;
+    const ApplyTables t = make_tables(st);
+    Blob blob;
+    p.tw64 = add_twiddles<double>(blob, st.n);
+    p.tw32 = add_twiddles<float>(blob, st.n);
+    const std::size_t kept_idx = blob.add(t.kept_idx), lam = blob.add(t.lam_kept);
+    const std::size_t z64 = blob.add(t.z_kept), z32 = blob.add(to_f32(t.z_kept));
+    const std::size_t nz64 = blob.add(t.neg_z_kept), nz32 = blob.add(to_f32(t.neg_z_kept));
+    const std::size_t act = blob.add(t.act_slot), nu = blob.add(t.nu);
+    const std::size_t sc64 = blob.add(t.act_scale), sc32 = blob.add(to_f32(t.act_scale));
+    p.pass_slot = blob.add(t.pass_slot);
+    p.pass_src = blob.add(t.pass_src);
+    p.pass_sign64 = blob.add(t.pass_sign);
+    p.pass_sign32 = blob.add(to_f32(t.pass_sign));
+    p.n_pass = static_cast<int>(t.pass_slot.size());
+    const int K = static_cast<int>(t.kept_idx.size()), A = static_cast<int>(t.nu.size());
+    p.fwd = {kept_idx, lam, z64, z32, act, nu, sc64, sc32, K, A};
+    p.inv = {act, nu, sc64, sc32, kept_idx, lam, nz64, nz32, A, K};
+    // Stage descriptors hold device pointers: reserve, upload, then patch.
+    p.stage_desc = blob.add(std::vector<dctp::dev::CauchyStage>(4));
+    p.blob = blob.upload();
+    const dctp::dev::CauchyStage desc[4] = {stage_at(p.blob, p.fwd, false, 0), stage_at(p.blob, p.fwd, true, 0),
+                                            stage_at(p.blob, p.inv, false, 0), stage_at(p.blob, p.inv, true, 0)};
+    cuda_check(cudaMemcpy(static_cast<unsigned char*>(p.blob) + p.stage_desc, desc, sizeof(desc),
+                          cudaMemcpyHostToDevice),
+               "cudaMemcpy(stage descriptors)");
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.flag), sizeof(int)), "cudaMalloc(flag)");
+    cuda_check(cudaMemset(p.flag, 0, sizeof(int)), "cudaMemset(flag)");
+}
+
+static dctp::host::Update make_update(int kind, std::size_t i, std::size_t j, double rho, const double* v,
+                                      std::size_t n) {
+    switch (kind) {
+        case DCTP_SELF_LOOP: return dctp::host::Update::self_loop(i, rho);
+        case DCTP_EDGE_DELTA: return dctp::host::Update::edge_delta(i, j, rho);
+        case DCTP_GENERAL:
+            if (!v) throw std::invalid_argument("RankOneUpdate: general update needs a direction");
+            return dctp::host::Update::general(std::vector<double>(v, v + n), rho);
+        default: throw std::invalid_argument("RankOneUpdate: unknown update kind");
+    }
+}
+
+static std::unique_ptr<dctp_plan> build_plan(std::size_t n, const dctp::host::Update& u, double eps, double tau,
+                                             int device) {
+    auto p = std::make_unique<dctp_plan>();
+    p->update = u;
+    p->device = device;
+    p->st = dctp::host::build_setup(n, u, eps, tau);
+    if (device < 0) return p; // host-only plan: setup vectors, no device constants
+    DeviceScope scope(device);
+    prepare_pool(device);
+    upload_plan(*p);
+    return p;
+}
+
+template <class T>
+static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s) {
+    if (!p) throw std::invalid_argument("dctp_forward: null plan");
+    if (!p->blob) throw std::invalid_argument("DctPlusPlan: host-only plan (created with device < 0)");
+    if (batch == 0) return;
+    if (!in || !out) throw std::invalid_argument("dctp_forward: null buffer");
+    if (static_cast<const void*>(in) == static_cast<const void*>(out))
+        throw std::invalid_argument("dctp_forward: in and out must not alias");
+    const std::size_t n = p->st.n;
+    DeviceScope scope(p->device);
+    Scratch<T> hat(batch * n, s);
+    cuda_check(dctp::dev::dct2_rows<T>(in, n, hat.ptr, n, out, n, p->emit_fwd<T>(), n, batch, p->tw<T>(), p->flag, s),
+               "dct2 kernel");
+    if (p->fwd.cols > 0)
+        cuda_check(dctp::dev::cauchy_rows<T>(hat.ptr, n, out, n, p->stage_dev(std::is_same_v<T, float> ? 1 : 0), 1,
+                                             p->fwd.rows, p->fwd.cols, batch, p->flag, s),
+                   "cauchy kernel");
+}
+
+template <class T>
+static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s) {
+    if (!p) throw std::invalid_argument("dctp_inverse: null plan");
+    if (!p->blob) throw std::invalid_argument("DctPlusPlan: host-only plan (created with device < 0)");
+    if (batch == 0) return;
+    if (!in || !out) throw std::invalid_argument("dctp_inverse: null buffer");
+    if (static_cast<const void*>(in) == static_cast<const void*>(out))
+        throw std::invalid_argument("dctp_inverse: in and out must not alias");
+    const std::size_t n = p->st.n;
+    DeviceScope scope(p->device);
+    Scratch<T> d(batch * n, s);
+    if (p->inv.cols > 0)
+        cuda_check(dctp::dev::cauchy_rows<T>(in, n, d.ptr, n, p->stage_dev(std::is_same_v<T, float> ? 3 : 2), 1,
+                                             p->inv.rows, p->inv.cols, batch, p->flag, s),
+                   "cauchy kernel");
+    cuda_check(dctp::dev::idct_rows<T>(d.ptr, n, in, n, p->emit_inv<T>(), out, n, n, batch, p->tw<T>(), p->flag, s),
+               "idct kernel");
+}
+
+static void sync_check(int device, int* flag, cudaStream_t s) {
+    DeviceScope scope(device);
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    int h = 0;
+    cuda_check(cudaMemcpy(&h, flag, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(flag)");
+    if (h != 0) {
+        cuda_check(cudaMemset(flag, 0, sizeof(int)), "cudaMemset(flag)");
+        throw std::domain_error("DctPlusPlan: non-finite input sample");
+    }
+}
+
+template <class T, class F>
+static void host_roundtrip(int device, std::size_t in_count, std::size_t out_count, const T* h_in, T* h_out, F&& run) {
+    if (!h_in || !h_out) throw std::invalid_argument("host buffer is null");
+    DeviceScope scope(device);
+    cudaStream_t s;
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { cudaStreamDestroy(s); }
+    } guard{s};
+    {
+        Scratch<T> din(in_count, s), dout(out_count, s);
+        cuda_check(cudaMemcpyAsync(din.ptr, h_in, in_count * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+        run(din.ptr, dout.ptr, s);
+        cuda_check(cudaMemcpyAsync(h_out, dout.ptr, out_count * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+    }
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
+
+// --- ensemble ------------------------------------------------------------------
+
+struct dctp_ensemble {
+    std::size_t n = 0, cp = 0;
+    double threshold = 0.0;
+    int device = 0;
+    std::vector<std::unique_ptr<dctp_plan>> members;
+    void* blob = nullptr;
+    int* flag = nullptr;
+    TwiddleOffsets tw64, tw32;
+    std::size_t to = 0, from = 0, sign64 = 0, sign32 = 0, desc64 = 0, desc32 = 0;
+    int n_emit = 0, max_rows = 0, max_cols = 0;
+
+    ~dctp_ensemble() {
+        if (blob) {
+            int prev = 0;
+            cudaGetDevice(&prev);
+            cudaSetDevice(device);
+            cudaFree(blob);
+            cudaFree(flag);
+            cudaSetDevice(prev);
+        }
+    }
+};
+
+template <class T>
+static void ensemble_forward(const dctp_ensemble* e, const T* in, T* out, std::size_t batch, cudaStream_t s) {
+    if (!e) throw std::invalid_argument("dctp_ensemble_forward_all: null ensemble");
+    if (!e->blob) throw std::invalid_argument("PrunedEnsemblePlan: host-only plan (created with device < 0)");
+    if (batch == 0) return;
+    if (!in || !out) throw std::invalid_argument("dctp_ensemble_forward_all: null buffer");
+    const std::size_t n = e->n, sets = e->members.size() + 1, ld = sets * n;
+    DeviceScope scope(e->device);
+    constexpr bool f32 = std::is_same_v<T, float>;
+    dctp::dev::Emit<T> emit{at<int>(e->blob, e->to), at<int>(e->blob, e->from), nullptr, e->n_emit};
+    dctp::dev::Twiddles<T> tw;
+    if constexpr (f32) {
+        emit.sign = at<float>(e->blob, e->sign32);
+        tw = twiddles_at<float>(e->blob, e->tw32);
+    } else {
+        emit.sign = at<double>(e->blob, e->sign64);
+        tw = twiddles_at<double>(e->blob, e->tw64);
+    }
+    // Set 0 (the shared DCT, fast_transform.hpp:401-403) is written in place
+    // and is the Cauchy stages' input; sets 1..K follow in each row.
+    cuda_check(dctp::dev::dct2_rows<T>(in, n, out, ld, out, ld, emit, n, batch, tw, e->flag, s), "dct2 kernel");
+    if (!e->members.empty() && e->max_cols > 0)
+        cuda_check(dctp::dev::cauchy_rows<T>(out, ld, out, ld,
+                                             at<dctp::dev::CauchyStage>(e->blob, f32 ? e->desc32 : e->desc64),
+                                             static_cast<int>(e->members.size()), e->max_rows, e->max_cols, batch,
+                                             e->flag, s),
+                   "cauchy kernel");
+}
+
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+const char* dctp_last_error(void) { return g_last_error.c_str(); }
+
+const char* dctp_version(void) { return "dctplus_b200 0.1 (sm_100a)"; }
+
+int dctp_plan_create(size_t n, int kind, size_t i, size_t j, double rho, const double* v, double epsilon,
+                     double tau, int device, dctp_plan** out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("dctp_plan_create: null output");
+        *out = nullptr;
+        if (n < 2) throw std::invalid_argument("DctPlusPlan: need n >= 2");
+        *out = build_plan(n, make_update(kind, i, j, rho, v, n), epsilon, tau, device).release();
+    });
+}
+
+int dctp_plan_destroy(dctp_plan* plan) {
+    return guarded([&] { delete plan; });
+}
+
+int dctp_plan_info(const dctp_plan* p, size_t* n, double* epsilon, int* slow_path, size_t* n_kept,
+                   size_t* n_active, int* device) {
+    return guarded([&] {
+        if (!p) throw std::invalid_argument("dctp_plan_info: null plan");
+        if (n) *n = p->st.n;
+        if (epsilon) *epsilon = p->st.epsilon;
+        if (slow_path) *slow_path = p->st.slow_path ? 1 : 0;
+        if (n_kept) *n_kept = p->st.kept.size();
+        if (n_active) *n_active = p->st.sub_mu.size();
+        if (device) *device = p->device;
+    });
+}
+
+int dctp_plan_setup(const dctp_plan* p, double* lambda, double* mu, double* z, double* a, double* sigma) {
+    return guarded([&] {
+        if (!p) throw std::invalid_argument("dctp_plan_setup: null plan");
+        const auto& st = p->st;
+        if (lambda) std::copy(st.lambda.begin(), st.lambda.end(), lambda);
+        if (mu) std::copy(st.mu.begin(), st.mu.end(), mu);
+        if (z) std::copy(st.z.begin(), st.z.end(), z);
+        if (a) std::copy(st.a.begin(), st.a.end(), a);
+        if (sigma) std::copy(st.sigma.begin(), st.sigma.end(), sigma);
+    });
+}
+
+int dctp_plan_slots(const dctp_plan* p, int* passthrough, int64_t* idx) {
+    return guarded([&] {
+        if (!p) throw std::invalid_argument("dctp_plan_slots: null plan");
+        for (std::size_t s = 0; s < p->st.slots.size(); ++s) {
+            if (passthrough) passthrough[s] = p->st.slots[s].passthrough ? 1 : 0;
+            if (idx) idx[s] = static_cast<int64_t>(p->st.slots[s].idx);
+        }
+    });
+}
+
+int dctp_plan_basis(const dctp_plan* p, double* x) {
+    return guarded([&] {
+        if (!p || !x) throw std::invalid_argument("dctp_plan_basis: null argument");
+        const auto& st = p->st;
+        const std::size_t n = st.n;
+        const dctp::host::Trig idct(dctp::host::Trig::Kind::idct2, n);
+        dctp::host::parallel_for(n, [&](std::size_t s) {
+            std::vector<double> buf(2 * n + idct.scratch_size() + 1);
+            double* y = buf.data();
+            double* col = y + n;
+            dctp::host::basis_coefficients(st, s, y);
+            idct.execute(y, col, col + n);
+            for (std::size_t i = 0; i < n; ++i) x[i * n + s] = st.sigma[s] < 0.0 ? -col[i] : col[i];
+        }, 4);
+    });
+}
+
+int dctp_forward_f64(const dctp_plan* p, const double* in, double* out, size_t batch, void* stream) {
+    return guarded([&] { plan_forward<double>(p, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_forward_f32(const dctp_plan* p, const float* in, float* out, size_t batch, void* stream) {
+    return guarded([&] { plan_forward<float>(p, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_inverse_f64(const dctp_plan* p, const double* in, double* out, size_t batch, void* stream) {
+    return guarded([&] { plan_inverse<double>(p, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_inverse_f32(const dctp_plan* p, const float* in, float* out, size_t batch, void* stream) {
+    return guarded([&] { plan_inverse<float>(p, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+
+int dctp_plan_sync_check(const dctp_plan* p, void* stream) {
+    return guarded([&] {
+        if (!p) throw std::invalid_argument("dctp_plan_sync_check: null plan");
+        sync_check(p->device, p->flag, static_cast<cudaStream_t>(stream));
+    });
+}
+
+#define DCTP_HOST_ENTRY(NAME, T, FN)                                                                  \
+    int NAME(const dctp_plan* p, const T* h_in, T* h_out, size_t batch) {                             \
+        return guarded([&] {                                                                          \
+            if (!p) throw std::invalid_argument(#NAME ": null plan");                                 \
+            if (!p->blob) throw std::invalid_argument("DctPlusPlan: host-only plan (created with device < 0)"); \
+            if (batch == 0) return;                                                                   \
+            const std::size_t cnt = batch * p->st.n;                                                  \
+            host_roundtrip<T>(p->device, cnt, cnt, h_in, h_out,                                       \
+                              [&](const T* din, T* dout, cudaStream_t s) { FN<T>(p, din, dout, batch, s); }); \
+            sync_check(p->device, p->flag, nullptr);                                                  \
+        });                                                                                           \
+    }
+DCTP_HOST_ENTRY(dctp_forward_host_f64, double, plan_forward)
+DCTP_HOST_ENTRY(dctp_forward_host_f32, float, plan_forward)
+DCTP_HOST_ENTRY(dctp_inverse_host_f64, double, plan_inverse)
+DCTP_HOST_ENTRY(dctp_inverse_host_f32, float, plan_inverse)
+#undef DCTP_HOST_ENTRY
+
+int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is, const size_t* js, const double* rhos,
+                         const double* vs, size_t cp, double threshold, double epsilon, int device,
+                         dctp_ensemble** out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("dctp_ensemble_create: null output");
+        *out = nullptr;
+        if (cp < 1 || cp > n) throw std::invalid_argument("PrunedEnsemblePlan: need 1 <= c_p <= n");
+        if (cp != n)
+            throw std::invalid_argument("PrunedEnsemblePlan: the GPU path implements the progressive mode c_p = n only");
+        if (k > 0 && (!kinds || !is || !js || !rhos)) throw std::invalid_argument("dctp_ensemble_create: null update arrays");
+        auto e = std::make_unique<dctp_ensemble>();
+        e->n = n;
+        e->cp = cp;
+        e->threshold = threshold;
+        e->device = device;
+        for (std::size_t r = 0; r < k; ++r)
+            e->members.push_back(build_plan(
+                n, make_update(kinds[r], is[r], js[r], rhos[r], vs ? vs + r * n : nullptr, n), epsilon, 1e-12, device));
+        // Twiddles, the merged pass-through emit list and one stage per member.
+        Blob blob;
+        e->tw64 = add_twiddles<double>(blob, n);
+        e->tw32 = add_twiddles<float>(blob, n);
+        std::vector<int> to, from;
+        std::vector<double> sign;
+        std::vector<ApplyTables> tabs;
+        for (std::size_t r = 0; r < k; ++r) {
+            tabs.push_back(make_tables(e->members[r]->st));
+            const auto& t = tabs.back();
+            for (std::size_t q = 0; q < t.pass_slot.size(); ++q) {
+                to.push_back(static_cast<int>((r + 1) * n) + t.pass_slot[q]);
+                from.push_back(t.pass_src[q]);
+                sign.push_back(t.pass_sign[q]);
+            }
+        }
+        e->to = blob.add(to);
+        e->from = blob.add(from);
+        e->sign64 = blob.add(sign);
+        e->sign32 = blob.add(to_f32(sign));
+        e->n_emit = static_cast<int>(to.size());
+        std::vector<StageOffsets> st(k);
+        for (std::size_t r = 0; r < k; ++r) {
+            const auto& t = tabs[r];
+            st[r] = {blob.add(t.kept_idx), blob.add(t.lam_kept), blob.add(t.z_kept), blob.add(to_f32(t.z_kept)),
+                     blob.add(t.act_slot), blob.add(t.nu), blob.add(t.act_scale), blob.add(to_f32(t.act_scale)),
+                     static_cast<int>(t.kept_idx.size()), static_cast<int>(t.nu.size())};
+            e->max_rows = std::max(e->max_rows, st[r].rows);
+            e->max_cols = std::max(e->max_cols, st[r].cols);
+        }
+        e->desc64 = blob.add(std::vector<dctp::dev::CauchyStage>(k));
+        e->desc32 = blob.add(std::vector<dctp::dev::CauchyStage>(k));
+        if (device < 0) {
+            *out = e.release();
+            return;
+        }
+        DeviceScope scope(device);
+        e->blob = blob.upload();
+        std::vector<dctp::dev::CauchyStage> d64, d32;
+        for (std::size_t r = 0; r < k; ++r) {
+            d64.push_back(stage_at(e->blob, st[r], false, static_cast<std::int64_t>((r + 1) * n)));
+            d32.push_back(stage_at(e->blob, st[r], true, static_cast<std::int64_t>((r + 1) * n)));
+        }
+        if (k > 0) {
+            cuda_check(cudaMemcpy(static_cast<unsigned char*>(e->blob) + e->desc64, d64.data(),
+                                  k * sizeof(dctp::dev::CauchyStage), cudaMemcpyHostToDevice),
+                       "cudaMemcpy(stages)");
+            cuda_check(cudaMemcpy(static_cast<unsigned char*>(e->blob) + e->desc32, d32.data(),
+                                  k * sizeof(dctp::dev::CauchyStage), cudaMemcpyHostToDevice),
+                       "cudaMemcpy(stages)");
+        }
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&e->flag), sizeof(int)), "cudaMalloc(flag)");
+        cuda_check(cudaMemset(e->flag, 0, sizeof(int)), "cudaMemset(flag)");
+        *out = e.release();
+    });
+}
+
+int dctp_ensemble_destroy(dctp_ensemble* e) {
+    return guarded([&] { delete e; });
+}
+
+int dctp_ensemble_info(const dctp_ensemble* e, size_t* n, size_t* ensemble_size) {
+    return guarded([&] {
+        if (!e) throw std::invalid_argument("dctp_ensemble_info: null ensemble");
+        if (n) *n = e->n;
+        if (ensemble_size) *ensemble_size = e->members.size() + 1;
+    });
+}
+
+int dctp_ensemble_member(const dctp_ensemble* e, size_t r, const dctp_plan** member) {
+    return guarded([&] {
+        if (!e || !member) throw std::invalid_argument("dctp_ensemble_member: null argument");
+        if (r < 1 || r > e->members.size()) throw std::out_of_range("PrunedEnsemblePlan::member: index out of range");
+        *member = e->members[r - 1].get();
+    });
+}
+
+int dctp_ensemble_forward_all_f64(const dctp_ensemble* e, const double* in, double* out, size_t batch, void* stream) {
+    return guarded([&] { ensemble_forward<double>(e, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_ensemble_forward_all_f32(const dctp_ensemble* e, const float* in, float* out, size_t batch, void* stream) {
+    return guarded([&] { ensemble_forward<float>(e, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_ensemble_sync_check(const dctp_ensemble* e, void* stream) {
+    return guarded([&] {
+        if (!e) throw std::invalid_argument("dctp_ensemble_sync_check: null ensemble");
+        sync_check(e->device, e->flag, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int dctp_ensemble_forward_all_host_f32(const dctp_ensemble* e, const float* h_in, float* h_out, size_t batch) {
+    return guarded([&] {
+        if (!e) throw std::invalid_argument("null ensemble");
+        if (!e->blob) throw std::invalid_argument("PrunedEnsemblePlan: host-only plan (created with device < 0)");
+        if (batch == 0) return;
+        const std::size_t sets = e->members.size() + 1;
+        host_roundtrip<float>(e->device, batch * e->n, batch * sets * e->n, h_in, h_out,
+                              [&](const float* din, float* dout, cudaStream_t s) {
+                                  ensemble_forward<float>(e, din, dout, batch, s);
+                              });
+        sync_check(e->device, e->flag, nullptr);
+    });
+}
+int dctp_ensemble_forward_all_host_f64(const dctp_ensemble* e, const double* h_in, double* h_out, size_t batch) {
+    return guarded([&] {
+        if (!e) throw std::invalid_argument("null ensemble");
+        if (!e->blob) throw std::invalid_argument("PrunedEnsemblePlan: host-only plan (created with device < 0)");
+        if (batch == 0) return;
+        const std::size_t sets = e->members.size() + 1;
+        host_roundtrip<double>(e->device, batch * e->n, batch * sets * e->n, h_in, h_out,
+                               [&](const double* din, double* dout, cudaStream_t s) {
+                                   ensemble_forward<double>(e, din, dout, batch, s);
+                               });
+        sync_check(e->device, e->flag, nullptr);
+    });
+}
+
+// --- bare trig kernels ------------------------------------------------------------
+
+} // extern "C"
+
+namespace {
+struct TrigCache {
+    std::mutex mu;
+    struct Entry {
+        int device;
+        std::size_t n;
+        void* blob;
+        TwiddleOffsets t64, t32;
+        int* flag;
+    };
+    std::vector<Entry> entries;
+    Entry get(int device, std::size_t n) {
+        std::lock_guard<std::mutex> lock(mu);
+        for (auto& e : entries)
+            if (e.device == device && e.n == n) return e;
+        Blob blob;
+        Entry e{device, n, nullptr, add_twiddles<double>(blob, n), add_twiddles<float>(blob, n), nullptr};
+        e.blob = blob.upload();
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&e.flag), sizeof(int)), "cudaMalloc(flag)");
+        cuda_check(cudaMemset(e.flag, 0, sizeof(int)), "cudaMemset(flag)");
+        entries.push_back(e);
+        return e;
+    }
+};
+TrigCache& trig_cache() {
+    static TrigCache* c = new TrigCache; // never destroyed: outlives the CUDA context teardown
+    return *c;
+}
+
+template <class T>
+void trig_run(bool inverse, std::size_t n, const T* in, T* out, std::size_t batch, int device, cudaStream_t s) {
+    if (n < 1) throw std::invalid_argument("TrigPlan: length must be positive");
+    if (batch == 0) return;
+    if (!in || !out) throw std::invalid_argument("trig: null buffer");
+    DeviceScope scope(device);
+    const auto e = trig_cache().get(device, n);
+    dctp::dev::Twiddles<T> tw;
+    if constexpr (std::is_same_v<T, double>)
+        tw = twiddles_at<double>(e.blob, e.t64);
+    else
+        tw = twiddles_at<float>(e.blob, e.t32);
+    const dctp::dev::Emit<T> none{};
+    if (!inverse)
+        cuda_check(dctp::dev::dct2_rows<T>(in, n, out, n, out, n, none, n, batch, tw, e.flag, s), "dct2 kernel");
+    else
+        cuda_check(dctp::dev::idct_rows<T>(in, n, in, n, none, out, n, n, batch, tw, e.flag, s), "idct kernel");
+}
+} // namespace
+
+extern "C" {
+
+int dctp_dct2_f64(size_t n, const double* in, double* out, size_t batch, int device, void* stream) {
+    return guarded([&] { trig_run<double>(false, n, in, out, batch, device, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_idct2_f64(size_t n, const double* in, double* out, size_t batch, int device, void* stream) {
+    return guarded([&] { trig_run<double>(true, n, in, out, batch, device, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_dct2_f32(size_t n, const float* in, float* out, size_t batch, int device, void* stream) {
+    return guarded([&] { trig_run<float>(false, n, in, out, batch, device, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_idct2_f32(size_t n, const float* in, float* out, size_t batch, int device, void* stream) {
+    return guarded([&] { trig_run<float>(true, n, in, out, batch, device, static_cast<cudaStream_t>(stream)); });
+}
+
+uint64_t dctp_mix_seed(uint64_t seed, size_t size, size_t kind) { return dctp::host::mix_seed(seed, size, kind); }
+
+int dctp_fill_signals(uint64_t seed, int dist, double r, size_t n, size_t rows, double* out) {
+    return guarded([&] {
+        if (!out && n * rows > 0) throw std::invalid_argument("dctp_fill_signals: null output");
+        if (dist < 0 || dist > 4) throw std::invalid_argument("dctp_fill_signals: unknown distribution");
+        dctp::host::fill_signals(seed, static_cast<dctp::host::Dist>(dist), r, n, rows, out);
+    });
+}
+
+} // extern "C"

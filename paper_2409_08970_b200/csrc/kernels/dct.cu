@@ -1,0 +1,324 @@
+// Batched orthonormal DCT-II / DCT-III (the U^T s and U d stages of DCT+),
+// sm_100a.  Replaces the reference's per-signal FFTW REDFT10/REDFT01 calls
+// (proj/include/dctplus/trig.hpp:95-110) for a whole batch per launch.
+//
+// Power-of-two n: Makhoul's reordering turns the length-n DCT into one
+// length-n/2 complex FFT of the packed real sequence, run in shared memory
+// (bit-reversed load, radix-2 stages, one CTA processes rows_per_cta signals
+// at once), followed by the real-split and the e^{-i pi k/2n} rotation.  The
+// epilogue stages the coefficients in shared memory and writes them with
+// coalesced row stores plus an optional scattered "emit" list (pass-through
+// slots of the DCT+ output), so the pass-through never needs its own launch.
+// Other n: a direct O(n^2) kernel over a cos(pi m / 2n) table.
+#include <algorithm>
+#include <cmath>
+
+#include "kernels/common.cuh"
+#include "kernels/launch.hpp"
+
+namespace dctp::dev {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kTileElems = 2048; // signal samples staged per CTA
+
+template <class T, bool Inverse>
+__device__ __forceinline__ void fft_radix2(cplx_t<T>* buf, int rows, int N, int logN,
+                                           const T* __restrict__ tw) {
+    const int halfN = N >> 1;
+    const int total = rows * halfN;
+    for (int s = 1; s <= logN; ++s) {
+        const int half = 1 << (s - 1);
+        const int stride_shift = logN - s; // twiddle index = j << stride_shift
+        for (int t = threadIdx.x; t < total; t += blockDim.x) {
+            const int row = t >> (logN - 1);
+            const int bidx = t & (halfN - 1);
+            const int j = bidx & (half - 1);
+            const int i0 = row * N + ((bidx >> (s - 1)) << s) + j;
+            const int i1 = i0 + half;
+            const int widx = j << stride_shift;
+            const T wr = __ldg(tw + 2 * widx);
+            const T wi = Inverse ? -__ldg(tw + 2 * widx + 1) : __ldg(tw + 2 * widx + 1);
+            const cplx_t<T> a = buf[i0];
+            const cplx_t<T> b = buf[i1];
+            const T tr = b.x * wr - b.y * wi;
+            const T ti = b.x * wi + b.y * wr;
+            buf[i1] = {a.x - tr, a.y - ti};
+            buf[i0] = {a.x + tr, a.y + ti};
+        }
+        __syncthreads();
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads)
+dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat, std::size_t ld_hat,
+                T* __restrict__ out, std::size_t ld_out, Emit<T> emit, int n, int logn,
+                int rows_per_cta, std::size_t batch, Twiddles<T> tw, int* flag) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int N = n >> 1, logN = logn - 1;
+    cplx_t<T>* cbuf = reinterpret_cast<cplx_t<T>*>(smem_raw);
+    T* sh = reinterpret_cast<T*>(cbuf + rows_per_cta * N);
+    const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * rows_per_cta;
+    const int rows = static_cast<int>(min(static_cast<std::size_t>(rows_per_cta), batch - b0));
+
+    // Load with Makhoul's permutation v = (x0, x2, ..., x3, x1), packed as
+    // w_m = v_{2m} + i v_{2m+1}, stored bit-reversed for the DIT stages.
+    bool bad = false;
+    for (int t = threadIdx.x; t < rows * n; t += blockDim.x) {
+        const int r = t >> logn, j = t & (n - 1);
+        const T x = in[(b0 + r) * ld_in + j];
+        bad |= !finite_val(x);
+        const int p = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
+        T* slot = reinterpret_cast<T*>(&cbuf[r * N + bit_reverse(static_cast<unsigned>(p >> 1), logN)]);
+        slot[p & 1] = x;
+    }
+    if (bad) atomicOr(flag, 1);
+    __syncthreads();
+
+    fft_radix2<T, false>(cbuf, rows, N, logN, tw.fft);
+
+    // Real split V_k = E_k - i e^{-2 pi i k/n} O_k, then Y_k = Re(e^{-i pi k/2n} V_k),
+    // Y_{n-k} = -Im(...); orthonormal scale sqrt(2/n), DC gets 1/sqrt(2) more.
+    const T scale = static_cast<T>(sqrt(2.0 / n));
+    const T dc_scale = static_cast<T>(1.0 / sqrt(static_cast<double>(n)));
+    const T half = static_cast<T>(0.5);
+    for (int t = threadIdx.x; t < rows * N; t += blockDim.x) {
+        const int r = t >> logN, k = t & (N - 1);
+        const cplx_t<T>* row = cbuf + r * N;
+        T* o = sh + r * n;
+        if (k == 0) {
+            const cplx_t<T> w0 = row[0];
+            o[0] = (w0.x + w0.y) * dc_scale;
+            o[N] = (w0.x - w0.y) * __ldg(tw.rot + 2 * N) * scale;
+            continue;
+        }
+        const cplx_t<T> wk = row[k];
+        const cplx_t<T> wc = row[N - k];
+        const T er = half * (wk.x + wc.x), ei = half * (wk.y - wc.y);
+        const T orr = half * (wk.x - wc.x), oi = half * (wk.y + wc.y);
+        const T sr = __ldg(tw.split + 2 * k), si = __ldg(tw.split + 2 * k + 1);
+        const T qr = sr * orr - si * oi, qi = sr * oi + si * orr;
+        const T vr = er + qi, vi = ei - qr;
+        const T cr = __ldg(tw.rot + 2 * k), ci = __ldg(tw.rot + 2 * k + 1);
+        o[k] = (vr * cr - vi * ci) * scale;
+        o[n - k] = -(vr * ci + vi * cr) * scale;
+    }
+    __syncthreads();
+
+    if (hat != nullptr)
+        for (int t = threadIdx.x; t < rows * n; t += blockDim.x) {
+            const int r = t >> logn, k = t & (n - 1);
+            hat[(b0 + r) * ld_hat + k] = sh[t];
+        }
+    for (int t = threadIdx.x; t < rows * emit.count; t += blockDim.x) {
+        const int r = t / emit.count, e = t - r * emit.count;
+        out[(b0 + r) * ld_out + emit.to[e]] = emit.sign[e] * sh[r * n + emit.from[e]];
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads)
+idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__ p, std::size_t ld_p,
+                Emit<T> emit, T* __restrict__ out, std::size_t ld_out, int n, int logn,
+                int rows_per_cta, std::size_t batch, Twiddles<T> tw, int* flag) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int N = n >> 1, logN = logn - 1;
+    cplx_t<T>* cbuf = reinterpret_cast<cplx_t<T>*>(smem_raw);
+    T* sh = reinterpret_cast<T*>(cbuf + rows_per_cta * N);
+    const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * rows_per_cta;
+    const int rows = static_cast<int>(min(static_cast<std::size_t>(rows_per_cta), batch - b0));
+
+    // X_k = sqrt(2/n) c_k d_k, with X_0 doubled (the REDFT01 convention).
+    const T scale = static_cast<T>(sqrt(2.0 / n));
+    const T dc_scale = static_cast<T>(2.0 / sqrt(static_cast<double>(n)));
+    for (int t = threadIdx.x; t < rows * n; t += blockDim.x) {
+        const int r = t >> logn, k = t & (n - 1);
+        sh[t] = d[(b0 + r) * ld_d + k];
+    }
+    __syncthreads();
+    bool bad = false;
+    for (int t = threadIdx.x; t < rows * emit.count; t += blockDim.x) {
+        const int r = t / emit.count, e = t - r * emit.count;
+        const T v = p[(b0 + r) * ld_p + emit.from[e]];
+        bad |= !finite_val(v);
+        sh[r * n + emit.to[e]] = emit.sign[e] * v;
+    }
+    if (bad) atomicOr(flag, 1);
+    __syncthreads();
+    for (int t = threadIdx.x; t < rows * n; t += blockDim.x) sh[t] *= ((t & (n - 1)) == 0) ? dc_scale : scale;
+    __syncthreads();
+
+    // V_k = e^{i pi k/2n} (X_k - i X_{n-k}); Z_k = (V_k + V_{k+N} + i e^{2 pi i k/n}(V_k - V_{k+N}))/2.
+    const T half = static_cast<T>(0.5);
+    const T r2 = static_cast<T>(0.70710678118654752440);
+    for (int t = threadIdx.x; t < rows * N; t += blockDim.x) {
+        const int r = t >> logN, k = t & (N - 1);
+        const T* x = sh + r * n;
+        const T cr = __ldg(tw.rot + 2 * k), ci = -__ldg(tw.rot + 2 * k + 1); // e^{+i pi k/2n}
+        const T ar = x[k], ai = (k == 0) ? T(0) : -x[n - k];
+        const T v1r = ar * cr - ai * ci, v1i = ar * ci + ai * cr;
+        // e^{i pi (k+N)/2n} = e^{i pi/4} e^{i pi k/2n}
+        const T c2r = r2 * (cr - ci), c2i = r2 * (cr + ci);
+        const T br = x[k + N], bi = -x[N - k];
+        const T v2r = br * c2r - bi * c2i, v2i = br * c2i + bi * c2r;
+        const T sr = __ldg(tw.split + 2 * k), si = -__ldg(tw.split + 2 * k + 1); // e^{+2 pi i k/n}
+        const T dr = v1r - v2r, di = v1i - v2i;
+        const T qr = sr * dr - si * di, qi = sr * di + si * dr;
+        cbuf[r * N + bit_reverse(static_cast<unsigned>(k), logN)] = {half * (v1r + v2r - qi),
+                                                                     half * (v1i + v2i + qr)};
+    }
+    __syncthreads();
+
+    fft_radix2<T, true>(cbuf, rows, N, logN, tw.fft);
+
+    for (int t = threadIdx.x; t < rows * n; t += blockDim.x) {
+        const int r = t >> logn, j = t & (n - 1);
+        const int pidx = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
+        const cplx_t<T> w = cbuf[r * N + (pidx >> 1)];
+        out[(b0 + r) * ld_out + j] = (pidx & 1) ? w.y : w.x;
+    }
+}
+
+// --- any n: direct O(n^2) over the cos(pi m / 2n) table ------------------------
+
+template <class T>
+__global__ void __launch_bounds__(kThreads)
+dct2_direct_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat, std::size_t ld_hat,
+                   T* __restrict__ out, std::size_t ld_out, Emit<T> emit, int n, std::size_t batch,
+                   Twiddles<T> tw, int* flag) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* x = reinterpret_cast<T*>(smem_raw);
+    T* o = x + n;
+    const std::size_t b = blockIdx.x;
+    bool bad = false;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        x[j] = in[b * ld_in + j];
+        bad |= !finite_val(x[j]);
+    }
+    if (bad) atomicOr(flag, 1);
+    __syncthreads();
+    const int m4 = 4 * n;
+    const T scale = static_cast<T>(sqrt(2.0 / n));
+    const T dc_scale = static_cast<T>(1.0 / sqrt(static_cast<double>(n)));
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        T acc = 0;
+        int idx = k % m4, inc = (2 * k) % m4;
+        for (int j = 0; j < n; ++j) {
+            acc += x[j] * __ldg(tw.cos4n + idx);
+            idx += inc;
+            if (idx >= m4) idx -= m4;
+        }
+        o[k] = acc * (k == 0 ? dc_scale : scale);
+    }
+    __syncthreads();
+    if (hat != nullptr)
+        for (int k = threadIdx.x; k < n; k += blockDim.x) hat[b * ld_hat + k] = o[k];
+    for (int e = threadIdx.x; e < emit.count; e += blockDim.x)
+        out[b * ld_out + emit.to[e]] = emit.sign[e] * o[emit.from[e]];
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads)
+idct_direct_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__ p, std::size_t ld_p,
+                   Emit<T> emit, T* __restrict__ out, std::size_t ld_out, int n, std::size_t batch,
+                   Twiddles<T> tw, int* flag) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* x = reinterpret_cast<T*>(smem_raw);
+    const std::size_t b = blockIdx.x;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) x[k] = d[b * ld_d + k];
+    __syncthreads();
+    bool bad = false;
+    for (int e = threadIdx.x; e < emit.count; e += blockDim.x) {
+        const T v = p[b * ld_p + emit.from[e]];
+        bad |= !finite_val(v);
+        x[emit.to[e]] = emit.sign[e] * v;
+    }
+    if (bad) atomicOr(flag, 1);
+    __syncthreads();
+    const int m4 = 4 * n;
+    const T scale = static_cast<T>(sqrt(2.0 / n));
+    const T dc_scale = static_cast<T>(1.0 / sqrt(static_cast<double>(n)));
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        T acc = x[0] * dc_scale;
+        const int inc = (2 * j + 1) % m4;
+        int idx = inc;
+        for (int k = 1; k < n; ++k) {
+            acc += x[k] * scale * __ldg(tw.cos4n + idx);
+            idx += inc;
+            if (idx >= m4) idx -= m4;
+        }
+        out[b * ld_out + j] = acc;
+    }
+}
+
+template <class T>
+int rows_per_cta_for(std::size_t n) {
+    return static_cast<int>(std::max<std::size_t>(1, kTileElems / n));
+}
+
+} // namespace
+
+template <class T>
+cudaError_t dct2_rows(const T* in, std::size_t ld_in, T* hat, std::size_t ld_hat, T* out,
+                      std::size_t ld_out, Emit<T> emit, std::size_t n, std::size_t batch,
+                      Twiddles<T> tw, int* flag, cudaStream_t stream) {
+    if (batch == 0) return cudaSuccess;
+    if (is_pow2(n) && n >= 2) {
+        const int rows = rows_per_cta_for<T>(n);
+        const std::size_t smem = static_cast<std::size_t>(rows) * n * (sizeof(T) * 2);
+        auto kern = dct2_fft_kernel<T>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        const unsigned grid = static_cast<unsigned>((batch + rows - 1) / rows);
+        kern<<<grid, kThreads, smem, stream>>>(in, ld_in, hat, ld_hat, out, ld_out, emit,
+                                              static_cast<int>(n), ilog2(n), rows, batch, tw, flag);
+        return cudaGetLastError();
+    }
+    const std::size_t smem = 2 * n * sizeof(T);
+    auto kern = dct2_direct_kernel<T>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<static_cast<unsigned>(batch), kThreads, smem, stream>>>(in, ld_in, hat, ld_hat, out, ld_out, emit,
+                                                                 static_cast<int>(n), batch, tw, flag);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t idct_rows(const T* d, std::size_t ld_d, const T* p, std::size_t ld_p, Emit<T> emit,
+                      T* out, std::size_t ld_out, std::size_t n, std::size_t batch,
+                      Twiddles<T> tw, int* flag, cudaStream_t stream) {
+    if (batch == 0) return cudaSuccess;
+    if (is_pow2(n) && n >= 2) {
+        const int rows = rows_per_cta_for<T>(n);
+        const std::size_t smem = static_cast<std::size_t>(rows) * n * (sizeof(T) * 2);
+        auto kern = idct_fft_kernel<T>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        const unsigned grid = static_cast<unsigned>((batch + rows - 1) / rows);
+        kern<<<grid, kThreads, smem, stream>>>(d, ld_d, p, ld_p, emit, out, ld_out, static_cast<int>(n),
+                                              ilog2(n), rows, batch, tw, flag);
+        return cudaGetLastError();
+    }
+    const std::size_t smem = n * sizeof(T);
+    auto kern = idct_direct_kernel<T>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<static_cast<unsigned>(batch), kThreads, smem, stream>>>(d, ld_d, p, ld_p, emit, out, ld_out,
+                                                                 static_cast<int>(n), batch, tw, flag);
+    return cudaGetLastError();
+}
+
+template cudaError_t dct2_rows<double>(const double*, std::size_t, double*, std::size_t, double*, std::size_t,
+                                       Emit<double>, std::size_t, std::size_t, Twiddles<double>, int*, cudaStream_t);
+template cudaError_t dct2_rows<float>(const float*, std::size_t, float*, std::size_t, float*, std::size_t,
+                                      Emit<float>, std::size_t, std::size_t, Twiddles<float>, int*, cudaStream_t);
+template cudaError_t idct_rows<double>(const double*, std::size_t, const double*, std::size_t, Emit<double>,
+                                       double*, std::size_t, std::size_t, std::size_t, Twiddles<double>, int*,
+                                       cudaStream_t);
+template cudaError_t idct_rows<float>(const float*, std::size_t, const float*, std::size_t, Emit<float>, float*,
+                                      std::size_t, std::size_t, std::size_t, Twiddles<float>, int*, cudaStream_t);
+
+} // namespace dctp::dev

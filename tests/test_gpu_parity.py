@@ -1,0 +1,207 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+goldens and the C restatement, on every BASELINE config and the reference
+tests' edge cases.
+
+Tolerances (north star / BASELINE.md section 3), norm-wise per signal,
+e = max_i |y_i - r_i| / max_i |r_i|, max over the batch:
+    fp64 <= 1e-10,  fp32 <= 1e-4 (against the fp64 reference).
+Full-size batches are checked through size-independent properties
+(orthogonality: Parseval and inverse(forward(s)) == s).
+"""
+import numpy as np
+import pytest
+
+from oracle import checkers as O
+from tests.golden_io import kat_cases, load_golden, setup_of
+
+pytestmark = pytest.mark.gpu
+
+TOL64, TOL32 = 1e-10, 1e-4
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2409_08970_b200 as P
+
+    return P
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    torch.cuda.init()
+    return torch
+
+
+def upd(P, u: O.Update):
+    if u.kind == 0:
+        return P.RankOneUpdate.self_loop(u.i, u.rho)
+    if u.kind == 1:
+        return P.RankOneUpdate.edge_delta(u.i, u.j, u.rho)
+    return P.RankOneUpdate.general(u.v, u.rho)
+
+
+_plans = {}
+
+
+def plan_for(P, cid):
+    if cid not in _plans:
+        cfg = O.config(cid)
+        if cfg.progressive:
+            _plans[cid] = P.PrunedEnsemblePlan(cfg.n, [upd(P, u) for u in cfg.updates], cfg.n, 1.7e308)
+        else:
+            _plans[cid] = P.DctPlusPlan(cfg.n, upd(P, cfg.updates[0]), 1e-12)
+    return _plans[cid]
+
+
+def dev(torch, a, dtype):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 5])
+def test_forward_matches_reference_goldens_fp64(P, torch, cid):
+    g = load_golden(f"c{cid}")
+    plan = plan_for(P, cid)
+    y = plan.forward(dev(torch, g["signals"], torch.float64)).cpu().numpy()
+    assert O.parity(y, g["forward"]) <= TOL64
+
+
+def test_forward_c3_fp32_against_fp64_reference(P, torch):
+    g = load_golden("c3")
+    y = plan_for(P, 3).forward(dev(torch, g["signals"], torch.float32)).cpu().numpy()
+    assert O.parity(y, g["forward"]) <= TOL32
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", TOL64), ("float32", TOL32)])
+def test_inverse_c3(P, torch, dtype, tol):
+    g = load_golden("c3")
+    t = getattr(torch, dtype)
+    plan = plan_for(P, 3)
+    y = plan.inverse(dev(torch, g["p"], t)).cpu().numpy()
+    assert O.parity(y, g["inverse"]) <= tol
+    rt = plan.inverse(plan.forward(dev(torch, g["signals"], t))).cpu().numpy()
+    assert O.parity(rt, g["signals"]) <= tol
+
+
+@pytest.mark.parametrize("dtype,tol", [("float32", TOL32), ("float64", TOL64)])
+def test_progressive_c4_matches_reference_forward_all(P, torch, dtype, tol):
+    g = load_golden("c4")
+    ens = plan_for(P, 4)
+    y = ens.forward_all_batch(dev(torch, g["signals"], getattr(torch, dtype))).cpu().numpy()
+    assert y.shape == g["forward_all"].shape
+    for r in range(17):
+        assert O.parity(y[:, r, :], g["forward_all"][:, r, :]) <= tol, r
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+def test_full_batch_against_restatement(P, torch, restatement, cid):
+    """Whole BASELINE batch (C1: 4096, C2: first 8192 of 65536) vs the C
+    restatement applied to the reference's setup."""
+    cfg = O.config(cid)
+    g = load_golden(f"c{cid}")
+    rows = min(cfg.batch, 8192)
+    s = restatement.signals(cfg, rows)
+    y = plan_for(P, cid).forward(dev(torch, s, torch.float64)).cpu().numpy()
+    assert O.parity(y, restatement.forward(setup_of(g), s)) <= TOL64
+
+
+@pytest.mark.parametrize("cid,dtype", [(1, "float64"), (2, "float64"), (3, "float64"), (3, "float32"),
+                                       (5, "float64")])
+def test_full_size_orthogonality(P, torch, restatement, cid, dtype):
+    """Size-independent properties at the BASELINE batch: Parseval and
+    inverse(forward(s)) == s (X is orthogonal)."""
+    cfg = O.config(cid)
+    t = getattr(torch, dtype)
+    s = dev(torch, restatement.signals(cfg, cfg.batch), t)
+    plan = plan_for(P, cid)
+    y = plan.forward(s)
+    tol = TOL32 if dtype == "float32" else (1e-8 if cid == 5 else TOL64)
+    ns, ny = torch.linalg.vector_norm(s.double(), dim=1), torch.linalg.vector_norm(y.double(), dim=1)
+    assert float(((ny - ns).abs() / ns).max()) <= tol
+    back = plan.inverse(y)
+    err = ((back - s).abs().amax(dim=1) / s.abs().amax(dim=1)).max()
+    assert float(err) <= tol
+
+
+def test_progressive_full_batch_properties(P, torch, restatement):
+    cfg = O.config(4)
+    s = dev(torch, restatement.signals(cfg, cfg.batch), torch.float32)
+    y = plan_for(P, 4).forward_all_batch(s)
+    assert y.shape == (cfg.batch, 17, 128)
+    ns = torch.linalg.vector_norm(s.double(), dim=1)
+    for r in (0, 1, 8, 16):
+        nr = torch.linalg.vector_norm(y[:, r, :].double(), dim=1)
+        assert float(((nr - ns).abs() / ns).max()) <= 1e-5
+    # set 0 is the plain orthonormal DCT-II
+    import paper_2409_08970_b200 as P_
+
+    assert float((y[:, 0, :] - P_.dct2(s)).abs().max()) == 0.0
+
+
+def test_reference_edge_cases(P, torch):
+    """n = 2, 3, 4, 8, 12 (non-power-of-two DCT kernel), 16, 33, 64, 100; rho < 0;
+    deflating updates; a slow-path plan (test_fast_transform.cpp:197-278)."""
+    for case in kat_cases():
+        kind, rho, i, j = case["update"]
+        u = O.Update(int(kind), float(rho), int(i), int(j))
+        plan = P.DctPlusPlan(int(case["n"]), upd(P, u), 1e-12)
+        s = dev(torch, case["signals"], torch.float64)
+        y = plan.forward(s).cpu().numpy()
+        assert O.parity(y, case["forward"]) <= TOL64, case["name"]
+        back = plan.inverse(torch.as_tensor(y, device="cuda")).cpu().numpy()
+        assert O.parity(back, case["signals"]) <= 1e-9, case["name"]
+        y32 = plan.forward(s.float()).cpu().numpy()
+        assert O.parity(y32, case["forward"]) <= TOL32, case["name"]
+
+
+def test_trig_kernels_match_reference_trigplan(P, torch):
+    g = load_golden("kat")
+    for n in (2, 4, 8, 12, 16, 17, 64):
+        x = dev(torch, g[f"trig/in_{n}"], torch.float64)
+        assert float((P.dct2(x).cpu() - torch.as_tensor(g[f"trig/dct2_{n}"])).abs().max()) <= 1e-13
+        assert float((P.idct2(x).cpu() - torch.as_tensor(g[f"trig/idct2_{n}"])).abs().max()) <= 1e-13
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 64, 96, 256, 1024, 2048, 8192])
+def test_dct_sizes_against_direct_sum(P, torch, restatement, n):
+    x = np.random.default_rng(n).standard_normal((5, n))
+    y = P.dct2(dev(torch, x, torch.float64)).cpu().numpy()
+    assert O.parity(y, restatement.dct2(x)) <= 1e-13
+    back = P.idct2(torch.as_tensor(y, device="cuda")).cpu().numpy()
+    assert O.parity(back, x) <= 1e-13
+
+
+def test_non_finite_input_raises_domain_error(P, torch):
+    plan = plan_for(P, 1)
+    s = torch.zeros((3, 64), dtype=torch.float64, device="cuda")
+    s[1, 5] = float("nan")
+    with pytest.raises(P.DomainError):
+        plan.forward(s)
+    plan.forward(torch.zeros((3, 64), dtype=torch.float64, device="cuda"))  # flag was cleared
+    s[1, 5] = float("inf")
+    with pytest.raises(P.DomainError):
+        plan.inverse(s)
+    with pytest.raises(P.DomainError):
+        plan.forward(np.full(64, np.inf))
+
+
+def test_shapes_and_empty_batch(P, torch):
+    plan = plan_for(P, 1)
+    assert plan.forward(torch.zeros((0, 64), dtype=torch.float64, device="cuda")).shape == (0, 64)
+    with pytest.raises(P.InvalidArgument):
+        plan.forward(torch.zeros((2, 63), dtype=torch.float64, device="cuda"))
+    one = plan.forward(torch.ones(64, dtype=torch.float64, device="cuda"))
+    assert one.shape == (64,)
+
+
+def test_host_entry_points_match_device(P, torch, restatement):
+    cfg = O.config(2)
+    s = restatement.signals(cfg, 257)  # ragged batch (not a multiple of any tile)
+    plan = plan_for(P, 2)
+    a = plan.forward(s)
+    b = plan.forward(dev(torch, s, torch.float64)).cpu().numpy()
+    assert np.array_equal(a, b)
+    assert np.array_equal(plan.inverse(a), plan.inverse(torch.as_tensor(a, device="cuda")).cpu().numpy())
+    res = plan_for(P, 4).forward_all(s[0, :128])
+    assert len(res.coeffs) == 17 and res.bounds == [0.0] * 17

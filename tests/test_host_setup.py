@@ -1,0 +1,140 @@
+"""CPU tests of the product's host side: the per-graph setup (host-only plans,
+device = -1) is bit-identical to the reference's, the API
+mirrors the reference's argument checks and exception classes, and the seeded
+signal sources reproduce the reference's Rng."""
+import numpy as np
+import pytest
+
+import paper_2409_08970_b200 as P
+from oracle import checkers as O
+from tests.golden_io import kat_cases, load_golden, setup_of
+
+BITWISE = ("lambda", "mu", "z", "a", "sigma", "slot_pass", "slot_idx")
+
+
+def product_update(u: O.Update):
+    if u.kind == 0:
+        return P.RankOneUpdate.self_loop(u.i, u.rho)
+    if u.kind == 1:
+        return P.RankOneUpdate.edge_delta(u.i, u.j, u.rho)
+    return P.RankOneUpdate.general(u.v, u.rho)
+
+
+def assert_setup_bitwise(plan, ref: dict, what: str):
+    st = plan.setup()
+    for k in BITWISE:
+        assert np.array_equal(np.asarray(st[k]), np.asarray(ref[k]).astype(np.asarray(st[k]).dtype)), (what, k)
+    assert plan.slow_path() == bool(ref["slow_path"]), what
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4])
+def test_setup_bitwise_equal_to_reference(cid):
+    cfg = O.config(cid)
+    g = load_golden(f"c{cid}")
+    if cfg.progressive:
+        for r, u in enumerate(cfg.updates, start=1):
+            plan = P.DctPlusPlan(cfg.n, product_update(u), 1e-12, device=-1)
+            assert_setup_bitwise(plan, setup_of(g, f"m{r}_"), f"C{cid} member {r}")
+    else:
+        plan = P.DctPlusPlan(cfg.n, product_update(cfg.updates[0]), 1e-12, device=-1)
+        assert_setup_bitwise(plan, setup_of(g), f"C{cid}")
+
+
+@pytest.mark.slow
+def test_setup_bitwise_equal_to_reference_c5():
+    cfg = O.config(5)
+    g = load_golden("c5")
+    assert np.array_equal(np.asarray(cfg.updates[0].v), g["v"])
+    plan = P.DctPlusPlan(cfg.n, product_update(cfg.updates[0]), 1e-12, device=-1)
+    assert_setup_bitwise(plan, setup_of(g), "C5")
+
+
+def test_setup_bitwise_on_reference_kat_cases():
+    for case in kat_cases():
+        kind, rho, i, j = case["update"]
+        u = O.Update(int(kind), float(rho), int(i), int(j))
+        plan = P.DctPlusPlan(int(case["n"]), product_update(u), 1e-12, device=-1)
+        assert_setup_bitwise(plan, case, case["name"])
+
+
+def test_basis_is_orthonormal_and_signed():
+    plan = P.DctPlusPlan(32, P.RankOneUpdate.edge_delta(3, 5, 1.5), 1e-12, device=-1)
+    x = plan.basis()
+    assert np.abs(x.T @ x - np.eye(32)).max() < 1e-10  # acceptance.cpp criterion 3
+    # largest-magnitude entry of every column is positive (spectral.hpp:30-37)
+    idx = np.abs(x).argmax(axis=0)
+    assert np.all(x[idx, np.arange(32)] > 0)
+
+
+def test_general_update_matches_edge_update():
+    n = 16
+    v = np.zeros(n)
+    v[2], v[4] = 1.0, -1.0
+    a = P.DctPlusPlan(n, P.RankOneUpdate.general(v, 1.5), 1e-12, device=-1).setup()
+    b = P.DctPlusPlan(n, P.RankOneUpdate.edge_delta(3, 5, 1.5), 1e-12, device=-1).setup()
+    for k in BITWISE:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_argument_errors_mirror_reference():
+    # fast_transform.hpp:52-53, :266-269; graph.hpp:95-108
+    with pytest.raises(P.InvalidArgument):
+        P.DctPlusPlan(1, P.RankOneUpdate.self_loop(1, 1.0), 1e-12, device=-1)
+    with pytest.raises(P.InvalidArgument):
+        P.DctPlusPlan(8, P.RankOneUpdate.self_loop(1, 1.0), 2.0, device=-1)
+    with pytest.raises(P.InvalidArgument):
+        P.DctPlusPlan(8, P.RankOneUpdate.self_loop(1, 1.0), 0.0, device=-1)
+    with pytest.raises(P.InvalidArgument):
+        P.DctPlusPlan(8, P.RankOneUpdate.self_loop(9, 1.0), 1e-12, device=-1)
+    with pytest.raises(P.InvalidArgument):
+        P.RankOneUpdate.self_loop(0, 1.0)
+    with pytest.raises(P.InvalidArgument):
+        P.RankOneUpdate.edge_delta(3, 3, 1.0)
+    with pytest.raises(P.InvalidArgument):
+        P.RankOneUpdate.edge_delta(1, 2, 0.0)
+    with pytest.raises(P.InvalidArgument):
+        P.DctPlusPlan(8, P.RankOneUpdate.general(np.ones(7), 1.0), 1e-12, device=-1)
+    with pytest.raises(ValueError):  # InvalidArgument is a ValueError
+        P.DctPlusPlan(8, P.RankOneUpdate.edge_delta(1, 9, 1.0), 1e-12, device=-1)
+    plan = P.DctPlusPlan(8, P.RankOneUpdate.self_loop(1, 1.0), 1e-12, device=-1)
+    with pytest.raises(P.InvalidArgument):  # host-only plan cannot apply
+        plan.forward(np.zeros(8))
+    with pytest.raises(P.InvalidArgument):
+        P.PrunedEnsemblePlan(8, [P.RankOneUpdate.self_loop(1, 1.0)], 0, 1.0, device=-1)
+    with pytest.raises(P.InvalidArgument):
+        P.PrunedEnsemblePlan(8, [P.RankOneUpdate.self_loop(1, 1.0)], 9, 1.0, device=-1)
+
+
+def test_disconnecting_edge_takes_slow_path_like_reference():
+    # test_fast_transform.cpp:259-278: removing an edge of the path trips the guard
+    case = next(c for c in kat_cases() if c["name"] == "disconnect_n16")
+    plan = P.DctPlusPlan(16, P.RankOneUpdate.edge_delta(8, 9, -1.0), 1e-12, device=-1)
+    assert plan.slow_path() == bool(case["slow_path"]) == True  # noqa: E712
+
+
+def test_ensemble_members_host_only():
+    ws = [0.05 + k * (1.95 / 15.0) for k in range(16)]
+    ens = P.PrunedEnsemblePlan(128, [P.RankOneUpdate.self_loop(1, w) for w in ws], 128, 1e300, device=-1)
+    assert ens.ensemble_size() == 17 and ens.size() == 128 and ens.keep_count() == 128
+    g = load_golden("c4")
+    for r in (1, 8, 16):
+        assert_setup_bitwise(ens.member(r), setup_of(g, f"m{r}_"), f"member {r}")
+    with pytest.raises(P.LogicError):
+        ens.member(0)
+    with pytest.raises(P.LogicError):
+        ens.member(17)
+
+
+@pytest.mark.parametrize("dist,r", [(0, 0.0), (1, 0.0), (2, 0.95), (3, 0.0), (4, 0.9)])
+def test_signal_sources_match_oracle(restatement, dist, r):
+    a = P.fill_signals(77, dist, 128, 300, r)
+    b = restatement.fill_signals(77, dist, 128, 300, r)
+    assert np.array_equal(a, b)
+
+
+def test_signal_sources_match_reference_goldens():
+    for cid in (1, 2, 3, 4):
+        g = load_golden(f"c{cid}")
+        s = P.fill_signals(int(g["seed"]), int(g["dist"]), int(g["n"]), g["signals"].shape[0], float(g["r"]))
+        assert np.array_equal(s, g["signals"])
+    assert P.mix_seed(2409, 1024, 3) == O.mix_seed(2409, 1024, 3)

@@ -136,6 +136,14 @@ int dctp_idct2_f64(size_t n, const double* d_in, double* d_out, size_t batch, in
 int dctp_dct2_f32(size_t n, const float* d_in, float* d_out, size_t batch, int device, void* stream);
 int dctp_idct2_f32(size_t n, const float* d_in, float* d_out, size_t batch, int device, void* stream);
 
+/* --- profiling: CUDA-event timing of every kernel launch ---------------- */
+/* When enabled, each kernel the library launches is bracketed by two CUDA
+ * events on its stream.  dctp_profile_summary() waits for them and writes
+ * {"kernel": [launches, total_ms], ...} as JSON into buf. */
+int dctp_profile_enable(int on);
+int dctp_profile_reset(void);
+int dctp_profile_summary(char* buf, size_t len);
+
 /* --- seeded inputs: signal.hpp Rng / gen_ar_signal, bench.hpp mix_seed ---- */
 uint64_t dctp_mix_seed(uint64_t seed, size_t size, size_t kind);
 /* dist 0: Rng::gaussian(), 1: Rng::uniform(), 2: rows of gen_ar_signal(n, r),

@@ -59,6 +59,9 @@ SIGNATURES = {
     "dctp_idct2_f64": (C.c_int, [_sz, _p, _p, _sz, C.c_int, _p]),
     "dctp_dct2_f32": (C.c_int, [_sz, _p, _p, _sz, C.c_int, _p]),
     "dctp_idct2_f32": (C.c_int, [_sz, _p, _p, _sz, C.c_int, _p]),
+    "dctp_profile_enable": (C.c_int, [C.c_int]),
+    "dctp_profile_reset": (C.c_int, []),
+    "dctp_profile_summary": (C.c_int, [C.c_char_p, _sz]),
     "dctp_mix_seed": (C.c_uint64, [C.c_uint64, _sz, _sz]),
     "dctp_fill_signals": (C.c_int, [C.c_uint64, C.c_int, C.c_double, _sz, _sz, _p]),
 }

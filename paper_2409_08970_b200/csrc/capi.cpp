@@ -10,6 +10,9 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <atomic>
+#include <cstdio>
+#include <map>
 #include <mutex>
 #include <numbers>
 #include <stdexcept>
@@ -223,6 +226,82 @@ struct Scratch {
     }
 };
 
+/// Optional per-launch CUDA-event timing of every kernel the library issues
+/// (bench.py's roofline and launch count); off unless dctp_profile_enable(1).
+class Profiler {
+  public:
+    static Profiler& get() {
+        static Profiler* p = new Profiler;
+        return *p;
+    }
+    bool on() const { return on_; }
+    void enable(bool on) { on_ = on; }
+    template <class F>
+    cudaError_t run(const char* name, cudaStream_t s, F&& launch) {
+        if (!on_) return launch();
+        cudaEvent_t a = take(), b = take();
+        cudaEventRecord(a, s);
+        const cudaError_t e = launch();
+        cudaEventRecord(b, s);
+        std::lock_guard<std::mutex> lock(mu_);
+        pending_.push_back({name, a, b});
+        return e;
+    }
+    std::string summary() {
+        std::lock_guard<std::mutex> lock(mu_);
+        for (auto& p : pending_) {
+            cudaEventSynchronize(p.b);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, p.a, p.b);
+            auto& acc = totals_[p.name];
+            acc.first += 1;
+            acc.second += ms;
+            free_.push_back(p.a);
+            free_.push_back(p.b);
+        }
+        pending_.clear();
+        std::string out = "{";
+        bool first = true;
+        for (auto& [name, acc] : totals_) {
+            char buf[160];
+            std::snprintf(buf, sizeof buf, "%s\"%s\": [%ld, %.6f]", first ? "" : ", ", name.c_str(), acc.first,
+                          acc.second);
+            out += buf;
+            first = false;
+        }
+        return out + "}";
+    }
+    void reset() {
+        summary();
+        std::lock_guard<std::mutex> lock(mu_);
+        totals_.clear();
+    }
+
+  private:
+    cudaEvent_t take() {
+        std::lock_guard<std::mutex> lock(mu_);
+        if (!free_.empty()) {
+            cudaEvent_t e = free_.back();
+            free_.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    struct Pending {
+        std::string name;
+        cudaEvent_t a, b;
+    };
+    std::atomic<bool> on_{false};
+    std::mutex mu_;
+    std::vector<Pending> pending_;
+    std::vector<cudaEvent_t> free_;
+    std::map<std::string, std::pair<long, double>> totals_;
+};
+
+#define DCTP_LAUNCH(name, stream, call) Profiler::get().run(name, stream, [&] { return (call); })
+
 } // namespace
 
 // ---------------------------------------------------------------------------
@@ -344,11 +423,13 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
     const std::size_t n = p->st.n;
     DeviceScope scope(p->device);
     Scratch<T> hat(batch * n, s);
-    cuda_check(dctp::dev::dct2_rows<T>(in, n, hat.ptr, n, out, n, p->emit_fwd<T>(), n, batch, p->tw<T>(), p->flag, s),
+    cuda_check(DCTP_LAUNCH("dct2", s, dctp::dev::dct2_rows<T>(in, n, hat.ptr, n, out, n, p->emit_fwd<T>(), n, batch,
+                                                             p->tw<T>(), p->flag, s)),
                "dct2 kernel");
     if (p->fwd.cols > 0)
-        cuda_check(dctp::dev::cauchy_rows<T>(hat.ptr, n, out, n, p->stage_dev(std::is_same_v<T, float> ? 1 : 0), 1,
-                                             p->fwd.rows, p->fwd.cols, batch, p->flag, s),
+        cuda_check(DCTP_LAUNCH("cauchy", s,
+                               dctp::dev::cauchy_rows<T>(hat.ptr, n, out, n, p->stage_dev(std::is_same_v<T, float> ? 1 : 0),
+                                                         1, p->fwd.rows, p->fwd.cols, batch, p->flag, s)),
                    "cauchy kernel");
 }
 
@@ -364,10 +445,13 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
     DeviceScope scope(p->device);
     Scratch<T> d(batch * n, s);
     if (p->inv.cols > 0)
-        cuda_check(dctp::dev::cauchy_rows<T>(in, n, d.ptr, n, p->stage_dev(std::is_same_v<T, float> ? 3 : 2), 1,
-                                             p->inv.rows, p->inv.cols, batch, p->flag, s),
+        cuda_check(DCTP_LAUNCH("cauchy_inv", s,
+                               dctp::dev::cauchy_rows<T>(in, n, d.ptr, n, p->stage_dev(std::is_same_v<T, float> ? 3 : 2),
+                                                         1, p->inv.rows, p->inv.cols, batch, p->flag, s)),
                    "cauchy kernel");
-    cuda_check(dctp::dev::idct_rows<T>(d.ptr, n, in, n, p->emit_inv<T>(), out, n, n, batch, p->tw<T>(), p->flag, s),
+    cuda_check(DCTP_LAUNCH("idct", s,
+                           dctp::dev::idct_rows<T>(d.ptr, n, in, n, p->emit_inv<T>(), out, n, n, batch, p->tw<T>(),
+                                                   p->flag, s)),
                "idct kernel");
 }
 
@@ -446,12 +530,14 @@ static void ensemble_forward(const dctp_ensemble* e, const T* in, T* out, std::s
     }
     // Set 0 (the shared DCT, fast_transform.hpp:401-403) is written in place
     // and is the Cauchy stages' input; sets 1..K follow in each row.
-    cuda_check(dctp::dev::dct2_rows<T>(in, n, out, ld, out, ld, emit, n, batch, tw, e->flag, s), "dct2 kernel");
+    cuda_check(DCTP_LAUNCH("dct2", s, dctp::dev::dct2_rows<T>(in, n, out, ld, out, ld, emit, n, batch, tw, e->flag, s)),
+               "dct2 kernel");
     if (!e->members.empty() && e->max_cols > 0)
-        cuda_check(dctp::dev::cauchy_rows<T>(out, ld, out, ld,
-                                             at<dctp::dev::CauchyStage>(e->blob, f32 ? e->desc32 : e->desc64),
-                                             static_cast<int>(e->members.size()), e->max_rows, e->max_cols, batch,
-                                             e->flag, s),
+        cuda_check(DCTP_LAUNCH("cauchy_progressive", s,
+                               dctp::dev::cauchy_rows<T>(out, ld, out, ld,
+                                                         at<dctp::dev::CauchyStage>(e->blob, f32 ? e->desc32 : e->desc64),
+                                                         static_cast<int>(e->members.size()), e->max_rows, e->max_cols,
+                                                         batch, e->flag, s)),
                    "cauchy kernel");
 }
 
@@ -768,6 +854,22 @@ int dctp_dct2_f32(size_t n, const float* in, float* out, size_t batch, int devic
 }
 int dctp_idct2_f32(size_t n, const float* in, float* out, size_t batch, int device, void* stream) {
     return guarded([&] { trig_run<float>(true, n, in, out, batch, device, static_cast<cudaStream_t>(stream)); });
+}
+
+int dctp_profile_enable(int on) {
+    return guarded([&] { Profiler::get().enable(on != 0); });
+}
+
+int dctp_profile_reset(void) {
+    return guarded([&] { Profiler::get().reset(); });
+}
+
+int dctp_profile_summary(char* buf, size_t len) {
+    return guarded([&] {
+        const std::string s = Profiler::get().summary();
+        if (!buf || len <= s.size()) throw std::invalid_argument("dctp_profile_summary: buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
 }
 
 uint64_t dctp_mix_seed(uint64_t seed, size_t size, size_t kind) { return dctp::host::mix_seed(seed, size, kind); }

@@ -418,3 +418,22 @@ def fill_signals(seed: int, dist: int, n: int, rows: int, r: float = 0.0) -> np.
     out = np.empty((rows, n))
     check(lib.dctp_fill_signals(seed, dist, float(r), n, rows, out.ctypes.data_as(C.c_void_p)))
     return out
+
+
+# --- kernel profiling (CUDA events around every launch; bench.py) ---------------------
+
+def profile_enable(on: bool = True) -> None:
+    check(lib.dctp_profile_enable(1 if on else 0))
+
+
+def profile_reset() -> None:
+    check(lib.dctp_profile_reset())
+
+
+def profile_summary() -> dict:
+    """{kernel: (launches, total_ms)} since the last reset (waits for the events)."""
+    import json
+
+    buf = C.create_string_buffer(1 << 16)
+    check(lib.dctp_profile_summary(buf, len(buf)))
+    return {k: (int(v[0]), float(v[1])) for k, v in json.loads(buf.value.decode()).items()}

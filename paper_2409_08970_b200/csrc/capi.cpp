@@ -317,6 +317,9 @@ struct dctp_plan {
     std::size_t pass_slot = 0, pass_src = 0, pass_sign64 = 0, pass_sign32 = 0;
     std::size_t stage_desc = 0; // 4 CauchyStage descriptors: fwd64, fwd32, inv64, inv32
     int n_pass = 0;
+    bool small = false;         // fused small-plan forward kernel eligible
+    std::size_t route = 0, fft_full = 0, act_scale64 = 0, z64 = 0, lam = 0, nu = 0, act_slot = 0;
+    int num_sms = 0;
 
     ~dctp_plan() {
         if (blob) {
@@ -369,6 +372,29 @@ static void upload_plan(dctp_plan& p) {
     const std::size_t sc64 = blob.add(t.act_scale), sc32 = blob.add(to_f32(t.act_scale));
     p.pass_slot = blob.add(t.pass_slot);
     p.pass_src = blob.add(t.pass_src);
+    p.act_scale64 = sc64;
+    p.z64 = z64;
+    p.lam = lam;
+    p.nu = nu;
+    p.act_slot = act;
+    p.small = dctp::dev::fused_small_supported(st.n, static_cast<int>(t.kept_idx.size()),
+                                               static_cast<int>(t.nu.size()));
+    if (p.small) {
+        // route[j]: kept position, or the signed pass-through slot (fused_small.cu)
+        std::vector<int> route(st.n, 0);
+        for (std::size_t k = 0; k < t.kept_idx.size(); ++k) route[t.kept_idx[k]] = static_cast<int>(k);
+        for (std::size_t q = 0; q < t.pass_slot.size(); ++q)
+            route[t.pass_src[q]] = -(2 * t.pass_slot[q] + (t.pass_sign[q] < 0.0 ? 1 : 0)) - 1;
+        p.route = blob.add(route);
+        const std::size_t N = st.n / 2;
+        std::vector<double> fftN(2 * N);
+        for (std::size_t m = 0; m < N; ++m) {
+            const double a = 2.0 * std::numbers::pi * static_cast<double>(m) / static_cast<double>(N);
+            fftN[2 * m] = std::cos(a);
+            fftN[2 * m + 1] = -std::sin(a);
+        }
+        p.fft_full = blob.add(fftN);
+    }
     p.pass_sign64 = blob.add(t.pass_sign);
     p.pass_sign32 = blob.add(to_f32(t.pass_sign));
     p.n_pass = static_cast<int>(t.pass_slot.size());
@@ -385,6 +411,7 @@ static void upload_plan(dctp_plan& p) {
                "cudaMemcpy(stage descriptors)");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.flag), sizeof(int)), "cudaMalloc(flag)");
     cuda_check(cudaMemset(p.flag, 0, sizeof(int)), "cudaMemset(flag)");
+    cuda_check(cudaDeviceGetAttribute(&p.num_sms, cudaDevAttrMultiProcessorCount, p.device), "cudaDeviceGetAttribute");
 }
 
 static dctp::host::Update make_update(int kind, std::size_t i, std::size_t j, double rho, const double* v,
@@ -422,6 +449,20 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
         throw std::invalid_argument("dctp_forward: in and out must not alias");
     const std::size_t n = p->st.n;
     DeviceScope scope(p->device);
+    if constexpr (std::is_same_v<T, double>) {
+        if (p->small) {
+            const dctp::dev::SmallPlanDev sp{at<double>(p->blob, p->lam), at<double>(p->blob, p->z64),
+                                             at<double>(p->blob, p->nu), at<double>(p->blob, p->act_scale64),
+                                             at<int>(p->blob, p->act_slot), at<int>(p->blob, p->route),
+                                             at<double>(p->blob, p->fft_full), at<double>(p->blob, p->tw64.split),
+                                             at<double>(p->blob, p->tw64.rot), static_cast<int>(n), p->fwd.rows,
+                                             p->fwd.cols};
+            cuda_check(DCTP_LAUNCH("fused_small_fwd", s,
+                                   dctp::dev::fused_small_forward(in, out, batch, sp, p->flag, p->num_sms, s)),
+                       "fused small forward kernel");
+            return;
+        }
+    }
     Scratch<T> hat(batch * n, s);
     cuda_check(DCTP_LAUNCH("dct2", s, dctp::dev::dct2_rows<T>(in, n, hat.ptr, n, out, n, p->emit_fwd<T>(), n, batch,
                                                              p->tw<T>(), p->flag, s)),

@@ -63,4 +63,22 @@ cudaError_t cauchy_rows(const T* in, std::size_t ld_in, T* out, std::size_t ld_o
                         const CauchyStage* stages_dev, int num_stages, int max_rows, int max_cols,
                         std::size_t batch, int* flag, cudaStream_t stream);
 
+/// Constants of the fused small-plan forward kernel (fused_small.cu).
+struct SmallPlanDev {
+    const double* lam_kept;  // K
+    const double* z_kept;    // K
+    const double* nu;        // A (secular roots, ascending)
+    const double* act_scale; // A (sigma * a of the root's slot)
+    const int* act_slot;     // A
+    const int* route;        // n: kept position (>= 0) or -(2*slot + negative) - 1
+    const double* fft_tw;    // N = n/2 complex e^{-2 pi i m / N}
+    const double* split_tw;  // N complex e^{-2 pi i k / n}
+    const double* rot_tw;    // N+1 complex e^{-i pi k / 2n}
+    int n, K, A;
+};
+
+bool fused_small_supported(std::size_t n, int K, int A);
+cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
+                                int num_sms, cudaStream_t stream);
+
 } // namespace dctp::dev

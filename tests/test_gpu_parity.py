@@ -205,3 +205,21 @@ def test_host_entry_points_match_device(P, torch, restatement):
     assert np.array_equal(plan.inverse(a), plan.inverse(torch.as_tensor(a, device="cuda")).cpu().numpy())
     res = plan_for(P, 4).forward_all(s[0, :128])
     assert len(res.coeffs) == 17 and res.bounds == [0.0] * 17
+
+
+@pytest.mark.parametrize("n", [16, 32, 64, 128, 256, 512])
+@pytest.mark.parametrize("kind", ["self_loop", "edge", "edge_center", "neg"])
+def test_small_plans_fused_path_against_restatement(P, torch, restatement, n, kind):
+    """The fused persistent kernel (pow2 n <= 512, <= 128 kept / active) on
+    ragged batches, deflating and non-deflating updates, rho of both signs."""
+    u = {"self_loop": P.RankOneUpdate.self_loop(3, 0.8),
+         "edge": P.RankOneUpdate.edge_delta(2, n // 2 + 1, 1.3),
+         "edge_center": P.RankOneUpdate.edge_delta(n // 2, n // 2 + 1, -0.7),
+         "neg": P.RankOneUpdate.self_loop(n, -0.4)}[kind]
+    plan = P.DctPlusPlan(n, u, 1e-12)
+    st = plan.setup()
+    st["sub_mu"] = np.array(sorted(st["mu"][st["slot_pass"] == 0]))
+    for batch in (1, 17, 16 * 148 + 5):
+        s = restatement.fill_signals(O.mix_seed(O.SEED, n, batch), 0, n, batch)
+        y = plan.forward(dev(torch, s, torch.float64)).cpu().numpy()
+        assert O.parity(y, restatement.forward(st, s)) <= TOL64, (n, kind, batch)

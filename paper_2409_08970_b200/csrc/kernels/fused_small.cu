@@ -14,7 +14,7 @@
 //      T[k, c] = sigma_c a_c z_k / (lambda_k - mu_c) (the reference's dense
 //      T_r of fast_transform.hpp:355-366, transposed) held in REGISTERS as
 //      m8n8k4 B fragments for the whole kernel (K x A <= 128 x 128 fp64 =
-//      128 KB spread over 8 warps)
+//      128 KB spread over 16 warps, one 8-column N-tile each)
 //   -> the assembled output tile leaves with one TMA 1-D bulk store.
 // HBM traffic is the algorithmic minimum (read s once, write the coefficients
 // once); the Cauchy matrix is generated once per CTA from fp64 gaps.
@@ -26,8 +26,8 @@
 namespace dctp::dev {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32; // one 8-slot N-tile of the Cauchy product per warp: A <= 128
 constexpr int KTMAX = 32;            // k-tiles of 4: K <= 128
 constexpr int LDA = KTMAX * 4 + 4;   // A-tile row stride (doubles): +4 staggers the 8 fragment rows over banks
 
@@ -127,7 +127,7 @@ __device__ __forceinline__ double2* fft_rows(const double* x, double2* a, double
     return src;
 }
 
-template <int LOGN, int NTW, int TS>
+template <int LOGN, int KT, int TS>
 __global__ void __launch_bounds__(kThreads, 1)
 fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, std::size_t batch, SmallPlanDev P,
                        int* flag) {
@@ -157,27 +157,25 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
         ptx::fence_mbar_init();
     }
 
-    // Cauchy fragments, resident for the whole kernel: B[k][c] = T[k][c].
-    double bf[KTMAX][NTW];
+    // Cauchy fragments, resident for the whole kernel: B[k][c] = T[k][c] for
+    // this warp's 8 output columns c and all K (zero-padded to 4*KT) kept rows.
+    double bf[KT];
+    {
+        const int c = warp * 8 + (lane >> 2);
 #pragma unroll
-    for (int kt = 0; kt < KTMAX; ++kt)
-#pragma unroll
-        for (int nt = 0; nt < NTW; ++nt) {
+        for (int kt = 0; kt < KT; ++kt) {
             const int k = kt * 4 + (lane & 3);
-            const int c = (warp * NTW + nt) * 8 + (lane >> 2);
             double v = 0.0;
             if (k < P.K && c < P.A) v = P.act_scale[c] * (P.z_kept[k] / (P.lam_kept[k] - P.nu[c]));
-            bf[kt][nt] = v;
+            bf[kt] = v;
         }
-    int slot[NTW][2];
+    }
+    int slot[2];
 #pragma unroll
-    for (int nt = 0; nt < NTW; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int c = (warp * NTW + nt) * 8 + 2 * (lane & 3) + e;
-            slot[nt][e] = c < P.A ? P.act_slot[c] : -1;
-        }
-    const int kt_count = (P.K + 3) / 4;
+    for (int e = 0; e < 2; ++e) {
+        const int c = warp * 8 + 2 * (lane & 3) + e;
+        slot[e] = c < P.A ? P.act_slot[c] : -1;
+    }
     __syncthreads();
 
     const std::size_t ntiles = (batch + TS - 1) / TS;
@@ -236,32 +234,24 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
         __syncthreads();
 
         // Cauchy stage: D[s, c] += A[s, k] * B[k, c] on DMMA, 8 x 8 x 4 at a time.
-        double acc[MT][NTW][2];
+        double acc[MT][2];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < NTW; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
         const double* arow = atile + (lane >> 2) * LDA + (lane & 3);
 #pragma unroll
-        for (int kt = 0; kt < KTMAX; ++kt) {
-            if (kt < kt_count) {
-                double a[MT];
+        for (int kt = 0; kt < KT; ++kt) {
+            double a[MT];
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt) a[mt] = arow[mt * 8 * LDA + kt * 4];
+            for (int mt = 0; mt < MT; ++mt) a[mt] = arow[mt * 8 * LDA + kt * 4];
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                    for (int nt = 0; nt < NTW; ++nt) ptx::dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[kt][nt]);
-            }
+            for (int mt = 0; mt < MT; ++mt) ptx::dmma_8x8x4(acc[mt][0], acc[mt][1], a[mt], bf[kt]);
         }
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
             const int r = mt * 8 + (lane >> 2);
 #pragma unroll
-            for (int nt = 0; nt < NTW; ++nt)
-#pragma unroll
-                for (int e = 0; e < 2; ++e)
-                    if (slot[nt][e] >= 0) x[r * n + slot[nt][e]] = acc[mt][nt][e];
+            for (int e = 0; e < 2; ++e)
+                if (slot[e] >= 0) x[r * n + slot[e]] = acc[mt][e];
         }
         ptx::fence_proxy_async();
         __syncthreads();
@@ -286,12 +276,12 @@ constexpr std::size_t smem_bytes() {
            (3 * N + 1) * sizeof(double2) + n * sizeof(int) + 2 * sizeof(uint64_t);
 }
 
-template <int LOGN, int NTW>
+template <int LOGN, int KT>
 cudaError_t launch_small(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
                          int num_sms, cudaStream_t stream) {
     constexpr int TS = LOGN >= 9 ? 8 : 16;
     constexpr std::size_t smem = smem_bytes<LOGN, TS>();
-    auto kern = fused_small_fwd_kernel<LOGN, NTW, TS>;
+    auto kern = fused_small_fwd_kernel<LOGN, KT, TS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const std::size_t ntiles = (batch + TS - 1) / TS;
@@ -300,29 +290,36 @@ cudaError_t launch_small(const double* in, double* out, std::size_t batch, const
     return cudaGetLastError();
 }
 
+/// K is padded up to 4*KT with KT in {4, 8, 16, 32} (never above n/4).
 template <int LOGN>
-cudaError_t dispatch_ntw(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
-                         int num_sms, cudaStream_t stream) {
-    if (P.A <= 8 * kWarps) return launch_small<LOGN, 1>(in, out, batch, P, flag, num_sms, stream);
-    return launch_small<LOGN, 2>(in, out, batch, P, flag, num_sms, stream);
+cudaError_t dispatch_kt(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
+                        int num_sms, cudaStream_t stream) {
+    constexpr int n = 1 << LOGN;
+    if (P.K <= 16 || n <= 16) return launch_small<LOGN, 4>(in, out, batch, P, flag, num_sms, stream);
+    if constexpr (n >= 32)
+        if (P.K <= 32 || n <= 32) return launch_small<LOGN, 8>(in, out, batch, P, flag, num_sms, stream);
+    if constexpr (n >= 64)
+        if (P.K <= 64 || n <= 64) return launch_small<LOGN, 16>(in, out, batch, P, flag, num_sms, stream);
+    if constexpr (n >= 128) return launch_small<LOGN, 32>(in, out, batch, P, flag, num_sms, stream);
+    return cudaErrorInvalidValue;
 }
 
 } // namespace
 
 bool fused_small_supported(std::size_t n, int K, int A) {
-    return is_pow2(n) && n >= 16 && n <= 512 && K <= 4 * KTMAX && A <= 16 * kWarps;
+    return is_pow2(n) && n >= 16 && n <= 512 && K <= 4 * KTMAX && A <= 8 * kWarps;
 }
 
 cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
                                 int num_sms, cudaStream_t stream) {
     if (batch == 0) return cudaSuccess;
     switch (P.n) {
-        case 16: return dispatch_ntw<4>(in, out, batch, P, flag, num_sms, stream);
-        case 32: return dispatch_ntw<5>(in, out, batch, P, flag, num_sms, stream);
-        case 64: return dispatch_ntw<6>(in, out, batch, P, flag, num_sms, stream);
-        case 128: return dispatch_ntw<7>(in, out, batch, P, flag, num_sms, stream);
-        case 256: return dispatch_ntw<8>(in, out, batch, P, flag, num_sms, stream);
-        case 512: return dispatch_ntw<9>(in, out, batch, P, flag, num_sms, stream);
+        case 16: return dispatch_kt<4>(in, out, batch, P, flag, num_sms, stream);
+        case 32: return dispatch_kt<5>(in, out, batch, P, flag, num_sms, stream);
+        case 64: return dispatch_kt<6>(in, out, batch, P, flag, num_sms, stream);
+        case 128: return dispatch_kt<7>(in, out, batch, P, flag, num_sms, stream);
+        case 256: return dispatch_kt<8>(in, out, batch, P, flag, num_sms, stream);
+        case 512: return dispatch_kt<9>(in, out, batch, P, flag, num_sms, stream);
         default: return cudaErrorInvalidValue;
     }
 }

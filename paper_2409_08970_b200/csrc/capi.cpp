@@ -318,7 +318,7 @@ struct dctp_plan {
     std::size_t stage_desc = 0; // 4 CauchyStage descriptors: fwd64, fwd32, inv64, inv32
     int n_pass = 0;
     bool small = false;         // fused small-plan forward kernel eligible
-    std::size_t route = 0, fft_full = 0, act_scale64 = 0, z64 = 0, lam = 0, nu = 0, act_slot = 0;
+    std::size_t pass_neg = 0, fft_full = 0, act_scale64 = 0, z64 = 0, lam = 0, nu = 0, act_slot = 0, kept = 0;
     int num_sms = 0;
 
     ~dctp_plan() {
@@ -377,15 +377,13 @@ static void upload_plan(dctp_plan& p) {
     p.lam = lam;
     p.nu = nu;
     p.act_slot = act;
+    p.kept = kept_idx;
     p.small = dctp::dev::fused_small_supported(st.n, static_cast<int>(t.kept_idx.size()),
                                                static_cast<int>(t.nu.size()));
     if (p.small) {
-        // route[j]: kept position, or the signed pass-through slot (fused_small.cu)
-        std::vector<int> route(st.n, 0);
-        for (std::size_t k = 0; k < t.kept_idx.size(); ++k) route[t.kept_idx[k]] = static_cast<int>(k);
-        for (std::size_t q = 0; q < t.pass_slot.size(); ++q)
-            route[t.pass_src[q]] = -(2 * t.pass_slot[q] + (t.pass_sign[q] < 0.0 ? 1 : 0)) - 1;
-        p.route = blob.add(route);
+        std::vector<int> neg(t.pass_sign.size());
+        for (std::size_t q = 0; q < neg.size(); ++q) neg[q] = t.pass_sign[q] < 0.0 ? 1 : 0;
+        p.pass_neg = blob.add(neg);
         const std::size_t N = st.n / 2;
         std::vector<double> fftN(2 * N);
         for (std::size_t m = 0; m < N; ++m) {
@@ -453,7 +451,9 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
         if (p->small) {
             const dctp::dev::SmallPlanDev sp{at<double>(p->blob, p->lam), at<double>(p->blob, p->z64),
                                              at<double>(p->blob, p->nu), at<double>(p->blob, p->act_scale64),
-                                             at<int>(p->blob, p->act_slot), at<int>(p->blob, p->route),
+                                             at<int>(p->blob, p->act_slot), at<int>(p->blob, p->kept),
+                                             at<int>(p->blob, p->pass_src), at<int>(p->blob, p->pass_slot),
+                                             at<int>(p->blob, p->pass_neg),
                                              at<double>(p->blob, p->fft_full), at<double>(p->blob, p->tw64.split),
                                              at<double>(p->blob, p->tw64.rot), static_cast<int>(n), p->fwd.rows,
                                              p->fwd.cols};

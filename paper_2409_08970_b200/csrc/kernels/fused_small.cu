@@ -1,23 +1,26 @@
 // Fused persistent forward DCT+ for small plans (power-of-two n <= 512, at
 // most 128 kept DCT indices and 128 secular roots), fp64, sm_100a.
 //
-// One CTA per SM loops over tiles of TS signals:
-//   TMA 1-D bulk load of the tile (double-buffered, mbarrier completion)
-//   -> orthonormal DCT-II of every row in shared memory: Makhoul packing fused
-//      into the first Stockham pass of an n/2-point complex FFT (radix-2/4,
-//      natural order), then the real split and e^{-i pi k/2n} rotation
-//   -> each coefficient is routed once: kept indices into the A tile of the
-//      Cauchy product, pass-through indices (signed) straight into their
-//      output slot (fast_transform.hpp:171)
-//   -> Cauchy stage on the fp64 tensor cores (mma.sync m8n8k4 DMMA):
-//      out[s, slot_c] = sum_k shat[s, kept_k] * T[k, c] with
-//      T[k, c] = sigma_c a_c z_k / (lambda_k - mu_c) (the reference's dense
-//      T_r of fast_transform.hpp:355-366, transposed) held in REGISTERS as
-//      m8n8k4 B fragments for the whole kernel (K x A <= 128 x 128 fp64 =
-//      128 KB spread over 16 warps, one 8-column N-tile each)
-//   -> the assembled output tile leaves with one TMA 1-D bulk store.
-// HBM traffic is the algorithmic minimum (read s once, write the coefficients
-// once); the Cauchy matrix is generated once per CTA from fp64 gaps.
+// Warp-specialised, one CTA per SM, three warpgroups:
+//   producer (warpgroup 0): TMA 1-D bulk loads of signal tiles (double-
+//     buffered, mbarrier completion) -> orthonormal DCT-II of every row in
+//     shared memory (Makhoul packing fused into the first Stockham pass of an
+//     n/2-point complex FFT with compile-time radix-2/4 passes and per-pass
+//     twiddle tables; real split + e^{-i pi k/2n} rotation) -> uniform gathers:
+//     kept coefficients into the A tile of the Cauchy product, pass-through
+//     coefficients (signed) straight into their output slots
+//     (fast_transform.hpp:171);
+//   consumers (warpgroups 1-2): the Cauchy stage on the fp64 tensor cores
+//     (mma.sync m8n8k4 DMMA), out[s, slot_c] = sum_k shat[s, kept_k] T[k, c],
+//     T[k, c] = sigma_c a_c z_k / (lambda_k - mu_c) (the reference's dense T_r,
+//     fast_transform.hpp:355-366, transposed) held in REGISTERS as m8n8k4 B
+//     fragments for the whole kernel (K x A <= 128 x 128 fp64 over 8 warps),
+//     then the epilogue writes the active slots and one consumer thread sends
+//     the assembled tile out with a TMA 1-D bulk store.
+// Producer and consumers run one tile apart, synchronised by mbarriers, so
+// the DCT of tile i+1 overlaps the DMMA work of tile i.  HBM traffic is the
+// algorithmic minimum: every signal is read once and every coefficient
+// written once.
 #include <algorithm>
 
 #include "kernels/common.cuh"
@@ -26,10 +29,11 @@
 namespace dctp::dev {
 namespace {
 
-constexpr int kThreads = 512;
-constexpr int kWarps = kThreads / 32; // one 8-slot N-tile of the Cauchy product per warp: A <= 128
-constexpr int KTMAX = 32;            // k-tiles of 4: K <= 128
-constexpr int LDA = KTMAX * 4 + 4;   // A-tile row stride (doubles): +4 staggers the 8 fragment rows over banks
+constexpr int kProducerThreads = 128;
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = kProducerThreads + 32 * kConsumerWarps;
+constexpr int KTMAX = 32;          // k-tiles of 4: K <= 128
+constexpr int LDA = KTMAX * 4 + 4; // A-tile row stride (doubles): +4 staggers the 8 fragment rows over banks
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -58,24 +62,50 @@ __device__ __forceinline__ void butterfly<4>(double2 (&v)[4]) {
     v[3] = make_double2(a1.x - a3.x, a1.y - a3.y);
 }
 
-/// One Stockham (autosort) pass of radix R over TS rows of N points:
-/// NS = size of the sub-transforms already done (log2 in lns).  FIRST: the
-/// source is the real signal tile, packed on the fly (Makhoul:
-/// w_m = v_{2m} + i v_{2m+1}, v = (x0, x2, ..., x3, x1)).
-template <int N, int TS, int R, bool FIRST>
+__device__ __forceinline__ void producer_sync() {
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kProducerThreads) : "memory");
+}
+
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 2, %0;\n" ::"n"(32 * kConsumerWarps) : "memory");
+}
+
+/// Stockham pass layout for an N-point FFT: the first pass is radix-2 when
+/// log2 N is odd, every other pass radix-4.  Pass p has sub-transform size
+/// NS = 2^lns_of(p) and radix_of(p); its twiddles e^{-2 pi i r jm/(NS R)}
+/// (jm < NS, 1 <= r < R) live at twiddle_offset(p) in the per-pass table.
+template <int N>
+struct Passes {
+    static constexpr int LOG = __builtin_ctz(N);
+    static constexpr int FIRST_R = (LOG % 2) ? 2 : 4;
+    static constexpr int COUNT = (LOG % 2) ? 1 + (LOG - 1) / 2 : LOG / 2;
+    static constexpr int radix(int p) { return p == 0 ? FIRST_R : 4; }
+    static constexpr int lns(int p) { return p == 0 ? 0 : (FIRST_R == 2 ? 1 : 2) + 2 * (p - 1); }
+    static constexpr int twiddle_offset(int p) {
+        int off = 0;
+        for (int q = 1; q < p; ++q) off += (1 << lns(q)) * (radix(q) - 1);
+        return off;
+    }
+    static constexpr int TWIDDLES = twiddle_offset(COUNT);
+};
+
+/// One Stockham (autosort) pass over TS rows.  P == 0 reads the real signal
+/// tile with Makhoul's packing w_m = v_{2m} + i v_{2m+1}, v = (x0, x2, ..., x3, x1).
+template <int N, int TS, int P>
 __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, const double* __restrict__ x,
-                                              double2* __restrict__ dst, const double2* __restrict__ tw, int lns,
+                                              double2* __restrict__ dst, const double2* __restrict__ ptw, int ptid,
                                               int rows, bool& bad) {
-    constexpr int M = N / R;
-    constexpr int n = 2 * N;
-    const int ns = 1 << lns;
-    for (int t = threadIdx.x; t < TS * M; t += kThreads) {
+    constexpr int R = Passes<N>::radix(P), LNS = Passes<N>::lns(P), NS = 1 << LNS;
+    constexpr int M = N / R, n = 2 * N;
+    constexpr int TWO = Passes<N>::twiddle_offset(P);
+#pragma unroll
+    for (int t = ptid; t < TS * M; t += kProducerThreads) {
         const int sig = t / M, j = t % M;
         double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int m = j + r * M;
-            if constexpr (FIRST) {
+            if constexpr (P == 0) {
                 const double* xr = x + sig * n;
                 const int p0 = 2 * m, p1 = 2 * m + 1;
                 const double e0 = (p0 < N) ? xr[2 * p0] : xr[2 * (n - 1 - p0) + 1];
@@ -86,202 +116,266 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, c
                 v[r] = src[sig * N + m];
             }
         }
-        const int jm = j & (ns - 1);
-        if (!FIRST || ns > 1) {
+        const int jm = j & (NS - 1);
+        if constexpr (P > 0) {
 #pragma unroll
-            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[(r * jm * (N >> lns)) / R]);
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], ptw[TWO + jm * (R - 1) + (r - 1)]);
         }
         butterfly<R>(v);
-        const int d = ((j >> lns) << lns) * R + jm;
+        const int d = (j >> LNS) * (NS * R) + jm;
 #pragma unroll
-        for (int r = 0; r < R; ++r) dst[sig * N + d + r * ns] = v[r];
+        for (int r = 0; r < R; ++r) dst[sig * N + d + r * NS] = v[r];
     }
 }
 
-/// The full n/2-point FFT of every row; returns the buffer holding the result.
-template <int N, int TS>
-__device__ __forceinline__ double2* fft_rows(const double* x, double2* a, double2* b, const double2* tw, int rows,
-                                             bool& bad) {
-    constexpr int LOGN = __builtin_ctz(N);
-    int lns = 0;
-    double2* src = nullptr;
-    double2* dst = a;
-    if constexpr (LOGN % 2 == 1) {
-        stockham_pass<N, TS, 2, true>(nullptr, x, dst, tw, 0, rows, bad);
-        lns = 1;
+/// Runs passes P.. of the FFT, ping-ponging between a and b; returns the
+/// buffer that holds the final (natural-order) spectrum.
+template <int N, int TS, int P>
+__device__ __forceinline__ double2* fft_passes(const double* x, double2* a, double2* b, const double2* ptw, int ptid,
+                                               int rows, bool& bad) {
+    if constexpr (P == Passes<N>::COUNT) {
+        return a; // `a` holds the output of the last pass
     } else {
-        stockham_pass<N, TS, 4, true>(nullptr, x, dst, tw, 0, rows, bad);
-        lns = 2;
+        stockham_pass<N, TS, P>(a, x, b, ptw, ptid, rows, bad);
+        producer_sync();
+        return fft_passes<N, TS, P + 1>(x, b, a, ptw, ptid, rows, bad);
     }
-    __syncthreads();
-    src = dst;
-    dst = b;
-#pragma unroll 1
-    for (; lns < LOGN; lns += 2) {
-        stockham_pass<N, TS, 4, false>(src, nullptr, dst, tw, lns, rows, bad);
-        __syncthreads();
-        double2* t = src;
-        src = dst;
-        dst = t;
-    }
-    return src;
 }
 
-template <int LOGN, int KT, int TS>
+template <int LOGN, int NTW, int KT, int TS>
 __global__ void __launch_bounds__(kThreads, 1)
 fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, std::size_t batch, SmallPlanDev P,
                        int* flag) {
     constexpr int n = 1 << LOGN, N = n / 2, MT = TS / 8;
+    constexpr int TILE = TS * n; // doubles per signal tile (== TS*N complex)
+    using PS = Passes<N>;
     extern __shared__ __align__(128) unsigned char smem[];
-    double* xbuf = reinterpret_cast<double*>(smem);
-    double2* ca = reinterpret_cast<double2*>(xbuf + 2 * TS * n);
-    double2* cb = ca + TS * N;
-    double* atile = reinterpret_cast<double*>(cb + TS * N);
-    double2* tw = reinterpret_cast<double2*>(atile + TS * LDA);
-    double2* sp = tw + N;
+    double* xin = reinterpret_cast<double*>(smem);            // 2 x TILE: TMA-loaded input tiles
+    double* xout = xin + 2 * TILE;                             // 2 x TILE: assembled output tiles
+    double2* cw = reinterpret_cast<double2*>(xout + 2 * TILE); // TILE/2 complex: FFT ping-pong partner
+    double* atile = reinterpret_cast<double*>(cw + TILE / 2);  // 2 x TS x LDA: Cauchy A operand
+    double2* ptw = reinterpret_cast<double2*>(atile + 2 * TS * LDA);
+    double2* sp = ptw + (PS::TWIDDLES > 0 ? PS::TWIDDLES : 1);
     double2* rt = sp + N;
-    int* route = reinterpret_cast<int*>(rt + N + 1);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(route + n);
+    int* kept_idx = reinterpret_cast<int*>(rt + N + 1); // KT*4
+    int* pass_src = kept_idx + 4 * KT;                   // n (used: P.n - P.K)
+    int* pass_dst = pass_src + n;                        // n: slot, with the sign in bit 30
+    uint64_t* bars = reinterpret_cast<uint64_t*>(pass_dst + n);
+    uint64_t* xfull = bars;       // [2] TMA load landed
+    uint64_t* afull = bars + 2;   // [2] producer -> consumers: A tile + pass-through written
+    uint64_t* aempty = bars + 4;  // [2] consumers -> producer: A tile consumed
+    uint64_t* xofree = bars + 6;  // [2] output tile's TMA store has read it
 
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int i = tid; i < N; i += kThreads) {
-        tw[i] = reinterpret_cast<const double2*>(P.fft_tw)[i];
-        sp[i] = reinterpret_cast<const double2*>(P.split_tw)[i];
-    }
-    for (int i = tid; i <= N; i += kThreads) rt[i] = reinterpret_cast<const double2*>(P.rot_tw)[i];
-    for (int i = tid; i < n; i += kThreads) route[i] = P.route[i];
-    for (int i = tid; i < TS * LDA; i += kThreads) atile[i] = 0.0;
-    if (tid == 0) {
-        ptx::mbar_init(&mbar[0], 1);
-        ptx::mbar_init(&mbar[1], 1);
-        ptx::fence_mbar_init();
-    }
+    const int tid = threadIdx.x;
+    const int n_pass = P.n - P.K;
 
-    // Cauchy fragments, resident for the whole kernel: B[k][c] = T[k][c] for
-    // this warp's 8 output columns c and all K (zero-padded to 4*KT) kept rows.
-    double bf[KT];
+    // ---- prologue: tables, barriers ---------------------------------------------
     {
-        const int c = warp * 8 + (lane >> 2);
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-            const int k = kt * 4 + (lane & 3);
-            double v = 0.0;
-            if (k < P.K && c < P.A) v = P.act_scale[c] * (P.z_kept[k] / (P.lam_kept[k] - P.nu[c]));
-            bf[kt] = v;
+        const double2* fft = reinterpret_cast<const double2*>(P.fft_tw);
+#pragma unroll 1
+        for (int p = 1; p < PS::COUNT; ++p) {
+            const int R = PS::radix(p), ns = 1 << PS::lns(p), off = PS::twiddle_offset(p);
+            for (int i = tid; i < ns * (R - 1); i += kThreads) {
+                const int jm = i / (R - 1), r = i % (R - 1) + 1;
+                ptw[off + i] = fft[(r * jm * (N / ns)) / R];
+            }
         }
-    }
-    int slot[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const int c = warp * 8 + 2 * (lane & 3) + e;
-        slot[e] = c < P.A ? P.act_slot[c] : -1;
+        for (int i = tid; i < N; i += kThreads) sp[i] = reinterpret_cast<const double2*>(P.split_tw)[i];
+        for (int i = tid; i <= N; i += kThreads) rt[i] = reinterpret_cast<const double2*>(P.rot_tw)[i];
+        for (int i = tid; i < 4 * KT; i += kThreads) kept_idx[i] = i < P.K ? P.kept_idx[i] : -1;
+        for (int i = tid; i < n_pass; i += kThreads) {
+            pass_src[i] = P.pass_src[i];
+            pass_dst[i] = P.pass_slot[i] | (P.pass_neg[i] ? (1 << 30) : 0);
+        }
+        for (int i = tid; i < 2 * TS * LDA; i += kThreads) atile[i] = 0.0;
+        if (tid == 0) {
+            for (int b = 0; b < 2; ++b) {
+                ptx::mbar_init(&xfull[b], 1);
+                ptx::mbar_init(&afull[b], kProducerThreads);
+                ptx::mbar_init(&aempty[b], 32 * kConsumerWarps);
+                ptx::mbar_init(&xofree[b], 1);
+            }
+            ptx::fence_mbar_init();
+        }
     }
     __syncthreads();
 
     const std::size_t ntiles = (batch + TS - 1) / TS;
-    auto issue = [&](std::size_t tile, int b) {
-        const std::size_t rows = min(static_cast<std::size_t>(TS), batch - tile * TS);
-        const uint32_t bytes = static_cast<uint32_t>(rows * n * sizeof(double));
-        ptx::mbar_expect_tx(&mbar[b], bytes);
-        ptx::bulk_load(xbuf + b * TS * n, in + tile * TS * n, bytes, &mbar[b]);
-    };
-    if (tid == 0) {
-        if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
-        if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
-    }
+    const std::size_t grid = gridDim.x;
+    auto rows_of = [&](std::size_t tile) { return static_cast<int>(min(static_cast<std::size_t>(TS), batch - tile * TS)); };
 
-    const double scale = sqrt(2.0 / n);
-    const double dc_scale = 1.0 / sqrt(static_cast<double>(n));
-    bool bad = false;
-    int it = 0;
-    for (std::size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int b = it & 1;
-        double* x = xbuf + b * TS * n;
-        const int rows = static_cast<int>(min(static_cast<std::size_t>(TS), batch - tile * TS));
-        ptx::mbar_wait(&mbar[b], (it >> 1) & 1);
-
-        const double2* F = fft_rows<N, TS>(x, ca, cb, tw, rows, bad);
-
-        // split + rotate + scale, then route every coefficient once
-        auto put = [&](int r, int j, double v) {
-            const int d = route[j];
-            if (d >= 0) {
-                atile[r * LDA + d] = v;
-            } else {
-                const int p = -d - 1;
-                x[r * n + (p >> 1)] = (p & 1) ? -v : v;
-            }
+    if (tid < kProducerThreads) {
+        // =============================== producer ===================================
+        const int ptid = tid;
+        auto issue = [&](std::size_t tile, int b) {
+            const uint32_t bytes = static_cast<uint32_t>(rows_of(tile) * n * sizeof(double));
+            ptx::mbar_expect_tx(&xfull[b], bytes);
+            ptx::bulk_load(xin + b * TILE, in + tile * TS * n, bytes, &xfull[b]);
         };
-        for (int t = tid; t < TS * N; t += kThreads) {
-            const int r = t / N, k = t % N;
-            const double2* row = F + r * N;
-            if (k == 0) {
-                const double2 w0 = row[0];
-                put(r, 0, (w0.x + w0.y) * dc_scale);
-                put(r, N, (w0.x - w0.y) * rt[N].x * scale);
-                continue;
-            }
-            const double2 wk = row[k], wc = row[N - k];
-            const double er = 0.5 * (wk.x + wc.x), ei = 0.5 * (wk.y - wc.y);
-            const double orr = 0.5 * (wk.x - wc.x), oi = 0.5 * (wk.y + wc.y);
-            const double2 s2 = sp[k];
-            const double qr = s2.x * orr - s2.y * oi, qi = s2.x * oi + s2.y * orr;
-            const double vr = er + qi, vi = ei - qr;
-            const double2 c2 = rt[k];
-            put(r, k, (vr * c2.x - vi * c2.y) * scale);
-            put(r, n - k, -(vr * c2.y + vi * c2.x) * scale);
+        if (ptid == 0) {
+            if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+            if (blockIdx.x + grid < ntiles) issue(blockIdx.x + grid, 1);
         }
-        __syncthreads();
+        const double scale = sqrt(2.0 / n);
+        const double dc_scale = 1.0 / sqrt(static_cast<double>(n));
+        bool bad = false;
+        int it = 0;
+        for (std::size_t tile = blockIdx.x; tile < ntiles; tile += grid, ++it) {
+            const int b = it & 1;
+            const uint32_t ph = (it >> 1) & 1;
+            const int rows = rows_of(tile);
+            double* x = xin + b * TILE;
+            ptx::mbar_wait(&xfull[b], ph);
 
-        // Cauchy stage: D[s, c] += A[s, k] * B[k, c] on DMMA, 8 x 8 x 4 at a time.
-        double acc[MT][2];
+            // FFT: pass 0 reads x (real) -> cw; then ping-pong cw <-> x (as complex)
+            double2* xc = reinterpret_cast<double2*>(x);
+            double2* F;
+            stockham_pass<N, TS, 0>(nullptr, x, cw, ptw, ptid, rows, bad);
+            producer_sync();
+            F = fft_passes<N, TS, 1>(nullptr, cw, xc, ptw, ptid, rows, bad);
+            // real split + rotation: shat into the buffer F does not occupy
+            double* S = reinterpret_cast<double*>(F == cw ? xc : cw);
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
-        const double* arow = atile + (lane >> 2) * LDA + (lane & 3);
+            for (int t = ptid; t < TS * (N / 2 + 1); t += kProducerThreads) {
+                const int r = t / (N / 2 + 1), k = t % (N / 2 + 1);
+                const double2* row = F + r * N;
+                double* o = S + r * n;
+                if (k == 0) {
+                    const double2 w0 = row[0];
+                    o[0] = (w0.x + w0.y) * dc_scale;
+                    o[N] = (w0.x - w0.y) * rt[N].x * scale;
+                    continue;
+                }
+                // k and N - k together: both read W_k and W_{N-k}
+                const double2 wk = row[k], wc = row[N - k];
 #pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-            double a[MT];
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) a[mt] = arow[mt * 8 * LDA + kt * 4];
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) ptx::dmma_8x8x4(acc[mt][0], acc[mt][1], a[mt], bf[kt]);
+                for (int h = 0; h < 2; ++h) {
+                    const int kk = h == 0 ? k : N - k;
+                    if (h == 1 && kk == k) break;
+                    const double2 a = h == 0 ? wk : wc, c = h == 0 ? wc : wk;
+                    const double er = 0.5 * (a.x + c.x), ei = 0.5 * (a.y - c.y);
+                    const double orr = 0.5 * (a.x - c.x), oi = 0.5 * (a.y + c.y);
+                    const double2 s2 = sp[kk];
+                    const double qr = s2.x * orr - s2.y * oi, qi = s2.x * oi + s2.y * orr;
+                    const double vr = er + qi, vi = ei - qr;
+                    const double2 c2 = rt[kk];
+                    o[kk] = (vr * c2.x - vi * c2.y) * scale;
+                    o[n - kk] = -(vr * c2.y + vi * c2.x) * scale;
+                }
+            }
+            producer_sync();
+            // the output tile and the A tile of this buffer must be free again
+            if (it >= 2) {
+                ptx::mbar_wait(&xofree[b], ((it - 2) >> 1) & 1);
+                ptx::mbar_wait(&aempty[b], ((it - 2) >> 1) & 1);
+            }
+            double* ob = xout + b * TILE;
+            double* ab = atile + b * TS * LDA;
+#pragma unroll 4
+            for (int t = ptid; t < TS * 4 * KT; t += kProducerThreads) {
+                const int r = t / (4 * KT), k = t % (4 * KT);
+                const int j = kept_idx[k];
+                if (j >= 0) ab[r * LDA + k] = S[r * n + j];
+            }
+#pragma unroll 4
+            for (int t = ptid; t < TS * n_pass; t += kProducerThreads) {
+                const int r = t / n_pass, q = t - r * n_pass;
+                const int d = pass_dst[q];
+                const double v = S[r * n + pass_src[q]];
+                ob[r * n + (d & 0xffff)] = (d >> 30) ? -v : v;
+            }
+            ptx::fence_proxy_async(); // pass-through writes -> visible to the consumers' TMA store
+            ptx::mbar_arrive(&afull[b]);
+            producer_sync(); // every read of x / cw for this tile is done
+            if (ptid == 0 && tile + 2 * grid < ntiles) issue(tile + 2 * grid, b);
         }
+        if (bad) atomicOr(flag, 1);
+    } else {
+        // =============================== consumers ==================================
+        const int ctid = tid - kProducerThreads;
+        const int warp = ctid >> 5, lane = ctid & 31;
+        // Cauchy fragments, resident for the whole kernel: B[k][c] = T[k][c] for
+        // this warp's NTW x 8 output columns c and all 4*KT (zero-padded) kept rows.
+        double bf[KT][NTW];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-            const int r = mt * 8 + (lane >> 2);
+        for (int kt = 0; kt < KT; ++kt)
 #pragma unroll
-            for (int e = 0; e < 2; ++e)
-                if (slot[e] >= 0) x[r * n + slot[e]] = acc[mt][e];
-        }
-        ptx::fence_proxy_async();
-        __syncthreads();
-        if (tid == 0) {
-            ptx::bulk_store(out + tile * TS * n, x, static_cast<uint32_t>(rows * n * sizeof(double)));
-            ptx::bulk_commit();
-            const std::size_t next = tile + 2 * static_cast<std::size_t>(gridDim.x);
-            if (next < ntiles) {
+            for (int nt = 0; nt < NTW; ++nt) {
+                const int k = kt * 4 + (lane & 3);
+                const int c = (warp * NTW + nt) * 8 + (lane >> 2);
+                double v = 0.0;
+                if (k < P.K && c < P.A) v = P.act_scale[c] * (P.z_kept[k] / (P.lam_kept[k] - P.nu[c]));
+                bf[kt][nt] = v;
+            }
+        int slot[NTW][2];
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int c = (warp * NTW + nt) * 8 + 2 * (lane & 3) + e;
+                slot[nt][e] = c < P.A ? P.act_slot[c] : -1;
+            }
+        int it = 0;
+        for (std::size_t tile = blockIdx.x; tile < ntiles; tile += grid, ++it) {
+            const int b = it & 1;
+            const int rows = rows_of(tile);
+            ptx::mbar_wait(&afull[b], (it >> 1) & 1);
+            const double* arow = atile + b * TS * LDA + (lane >> 2) * LDA + (lane & 3);
+            double acc[MT][NTW][2];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < NTW; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt) {
+                double a[MT];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) a[mt] = arow[mt * 8 * LDA + kt * 4];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < NTW; ++nt)
+                        ptx::dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[kt][nt]);
+            }
+            ptx::mbar_arrive(&aempty[b]);
+            double* ob = xout + b * TILE;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const int r = mt * 8 + (lane >> 2);
+#pragma unroll
+                for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        if (slot[nt][e] >= 0) ob[r * n + slot[nt][e]] = acc[mt][nt][e];
+            }
+            ptx::fence_proxy_async();
+            consumer_sync();
+            if (ctid == 0) {
+                ptx::bulk_store(out + tile * TS * n, ob, static_cast<uint32_t>(rows * n * sizeof(double)));
+                ptx::bulk_commit();
                 ptx::bulk_wait_read_all();
-                issue(next, b);
+                ptx::mbar_arrive(&xofree[b]);
             }
         }
+        if (ctid == 0) ptx::bulk_wait_all();
     }
-    if (bad) atomicOr(flag, 1);
-    if (tid == 0) ptx::bulk_wait_all();
 }
 
-template <int LOGN, int TS>
+template <int LOGN, int KT, int TS>
 constexpr std::size_t smem_bytes() {
-    constexpr int n = 1 << LOGN, N = n / 2;
-    return 2 * TS * n * sizeof(double) + 2 * TS * N * sizeof(double2) + TS * LDA * sizeof(double) +
-           (3 * N + 1) * sizeof(double2) + n * sizeof(int) + 2 * sizeof(uint64_t);
+    constexpr int n = 1 << LOGN, N = n / 2, TILE = TS * n;
+    constexpr int tw = Passes<N>::TWIDDLES > 0 ? Passes<N>::TWIDDLES : 1;
+    return 4 * TILE * sizeof(double) + (TILE / 2) * sizeof(double2) + 2 * TS * LDA * sizeof(double) +
+           (tw + 2 * N + 1) * sizeof(double2) + (4 * KT + 2 * n) * sizeof(int) + 8 * sizeof(uint64_t);
 }
 
-template <int LOGN, int KT>
+template <int LOGN, int NTW, int KT>
 cudaError_t launch_small(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
                          int num_sms, cudaStream_t stream) {
     constexpr int TS = LOGN >= 9 ? 8 : 16;
-    constexpr std::size_t smem = smem_bytes<LOGN, TS>();
-    auto kern = fused_small_fwd_kernel<LOGN, KT, TS>;
+    constexpr std::size_t smem = smem_bytes<LOGN, KT, TS>();
+    static_assert(smem <= 227 * 1024, "fused small kernel exceeds shared memory");
+    auto kern = fused_small_fwd_kernel<LOGN, NTW, KT, TS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const std::size_t ntiles = (batch + TS - 1) / TS;
@@ -290,24 +384,31 @@ cudaError_t launch_small(const double* in, double* out, std::size_t batch, const
     return cudaGetLastError();
 }
 
+template <int LOGN, int KT>
+cudaError_t dispatch_ntw(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
+                         int num_sms, cudaStream_t stream) {
+    if (P.A <= 8 * kConsumerWarps) return launch_small<LOGN, 1, KT>(in, out, batch, P, flag, num_sms, stream);
+    return launch_small<LOGN, 2, KT>(in, out, batch, P, flag, num_sms, stream);
+}
+
 /// K is padded up to 4*KT with KT in {4, 8, 16, 32} (never above n/4).
 template <int LOGN>
 cudaError_t dispatch_kt(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
                         int num_sms, cudaStream_t stream) {
     constexpr int n = 1 << LOGN;
-    if (P.K <= 16 || n <= 16) return launch_small<LOGN, 4>(in, out, batch, P, flag, num_sms, stream);
+    if (P.K <= 16 || n <= 16) return dispatch_ntw<LOGN, 4>(in, out, batch, P, flag, num_sms, stream);
     if constexpr (n >= 32)
-        if (P.K <= 32 || n <= 32) return launch_small<LOGN, 8>(in, out, batch, P, flag, num_sms, stream);
+        if (P.K <= 32 || n <= 32) return dispatch_ntw<LOGN, 8>(in, out, batch, P, flag, num_sms, stream);
     if constexpr (n >= 64)
-        if (P.K <= 64 || n <= 64) return launch_small<LOGN, 16>(in, out, batch, P, flag, num_sms, stream);
-    if constexpr (n >= 128) return launch_small<LOGN, 32>(in, out, batch, P, flag, num_sms, stream);
+        if (P.K <= 64 || n <= 64) return dispatch_ntw<LOGN, 16>(in, out, batch, P, flag, num_sms, stream);
+    if constexpr (n >= 128) return dispatch_ntw<LOGN, 32>(in, out, batch, P, flag, num_sms, stream);
     return cudaErrorInvalidValue;
 }
 
 } // namespace
 
 bool fused_small_supported(std::size_t n, int K, int A) {
-    return is_pow2(n) && n >= 16 && n <= 512 && K <= 4 * KTMAX && A <= 8 * kWarps;
+    return is_pow2(n) && n >= 16 && n <= 512 && K <= 4 * KTMAX && A <= 16 * kConsumerWarps;
 }
 
 cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,

@@ -70,7 +70,10 @@ struct SmallPlanDev {
     const double* nu;        // A (secular roots, ascending)
     const double* act_scale; // A (sigma * a of the root's slot)
     const int* act_slot;     // A
-    const int* route;        // n: kept position (>= 0) or -(2*slot + negative) - 1
+    const int* kept_idx;     // K: DCT index of each kept coefficient
+    const int* pass_src;     // n - K: DCT index of each pass-through coefficient
+    const int* pass_slot;    // n - K: its output slot
+    const int* pass_neg;     // n - K: 1 if sigma of that slot is -1
     const double* fft_tw;    // N = n/2 complex e^{-2 pi i m / N}
     const double* split_tw;  // N complex e^{-2 pi i k / n}
     const double* rot_tw;    // N+1 complex e^{-i pi k / 2n}

@@ -318,7 +318,7 @@ struct dctp_plan {
     std::size_t stage_desc = 0; // 4 CauchyStage descriptors: fwd64, fwd32, inv64, inv32
     int n_pass = 0;
     bool small = false;         // fused small-plan forward kernel eligible
-    std::size_t pass_neg = 0, fft_full = 0, act_scale64 = 0, z64 = 0, lam = 0, nu = 0, act_slot = 0, kept = 0;
+    std::size_t pass_neg = 0, tmat = 0, fft_full = 0, act_scale64 = 0, z64 = 0, lam = 0, nu = 0, act_slot = 0, kept = 0;
     int num_sms = 0;
 
     ~dctp_plan() {
@@ -384,6 +384,13 @@ static void upload_plan(dctp_plan& p) {
         std::vector<int> neg(t.pass_sign.size());
         for (std::size_t q = 0; q < neg.size(); ++q) neg[q] = t.pass_sign[q] < 0.0 ? 1 : 0;
         p.pass_neg = blob.add(neg);
+        // T[c][k] = sigma_c a_c z_k / (lambda_k - mu_c): the reference's dense T
+        // (fast_transform.hpp:355-366, row = slot) restricted to active x kept.
+        const std::size_t K = t.kept_idx.size(), A = t.nu.size();
+        std::vector<double> tm(A * K);
+        for (std::size_t c = 0; c < A; ++c)
+            for (std::size_t k = 0; k < K; ++k) tm[c * K + k] = t.act_scale[c] * (t.z_kept[k] / (t.lam_kept[k] - t.nu[c]));
+        p.tmat = blob.add(tm);
         const std::size_t N = st.n / 2;
         std::vector<double> fftN(2 * N);
         for (std::size_t m = 0; m < N; ++m) {
@@ -451,7 +458,8 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
         if (p->small) {
             const dctp::dev::SmallPlanDev sp{at<double>(p->blob, p->lam), at<double>(p->blob, p->z64),
                                              at<double>(p->blob, p->nu), at<double>(p->blob, p->act_scale64),
-                                             at<int>(p->blob, p->act_slot), at<int>(p->blob, p->kept),
+                                             at<int>(p->blob, p->act_slot), at<double>(p->blob, p->tmat),
+                                             at<int>(p->blob, p->kept),
                                              at<int>(p->blob, p->pass_src), at<int>(p->blob, p->pass_slot),
                                              at<int>(p->blob, p->pass_neg),
                                              at<double>(p->blob, p->fft_full), at<double>(p->blob, p->tw64.split),

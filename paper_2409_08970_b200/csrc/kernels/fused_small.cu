@@ -29,8 +29,8 @@
 namespace dctp::dev {
 namespace {
 
-constexpr int kProducerThreads = 128;
-constexpr int kConsumerWarps = 8;
+constexpr int kProducerThreads = 256; // warpgroups 0-1: TMA + DCT (setmaxnreg 88)
+constexpr int kConsumerWarps = 8;     // warpgroups 2-3: DMMA Cauchy stage (setmaxnreg 168)
 constexpr int kThreads = kProducerThreads + 32 * kConsumerWarps;
 constexpr int KTMAX = 32;          // k-tiles of 4: K <= 128
 constexpr int LDA = KTMAX * 4 + 4; // A-tile row stride (doubles): +4 staggers the 8 fragment rows over banks
@@ -89,38 +89,22 @@ struct Passes {
     static constexpr int TWIDDLES = twiddle_offset(COUNT);
 };
 
-/// One Stockham (autosort) pass over TS rows.  P == 0 reads the real signal
-/// tile with Makhoul's packing w_m = v_{2m} + i v_{2m+1}, v = (x0, x2, ..., x3, x1).
+/// One Stockham (autosort) pass over TS rows (P >= 1).
 template <int N, int TS, int P>
-__device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, const double* __restrict__ x,
-                                              double2* __restrict__ dst, const double2* __restrict__ ptw, int ptid,
-                                              int rows, bool& bad) {
+__device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, double2* __restrict__ dst,
+                                              const double2* __restrict__ ptw, int ptid) {
     constexpr int R = Passes<N>::radix(P), LNS = Passes<N>::lns(P), NS = 1 << LNS;
-    constexpr int M = N / R, n = 2 * N;
+    constexpr int M = N / R;
     constexpr int TWO = Passes<N>::twiddle_offset(P);
 #pragma unroll
     for (int t = ptid; t < TS * M; t += kProducerThreads) {
         const int sig = t / M, j = t % M;
         double2 v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int m = j + r * M;
-            if constexpr (P == 0) {
-                const double* xr = x + sig * n;
-                const int p0 = 2 * m, p1 = 2 * m + 1;
-                const double e0 = (p0 < N) ? xr[2 * p0] : xr[2 * (n - 1 - p0) + 1];
-                const double e1 = (p1 < N) ? xr[2 * p1] : xr[2 * (n - 1 - p1) + 1];
-                if (sig < rows) bad |= !isfinite(e0) || !isfinite(e1);
-                v[r] = make_double2(e0, e1);
-            } else {
-                v[r] = src[sig * N + m];
-            }
-        }
+        for (int r = 0; r < R; ++r) v[r] = src[sig * N + j + r * M];
         const int jm = j & (NS - 1);
-        if constexpr (P > 0) {
 #pragma unroll
-            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], ptw[TWO + jm * (R - 1) + (r - 1)]);
-        }
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], ptw[TWO + jm * (R - 1) + (r - 1)]);
         butterfly<R>(v);
         const int d = (j >> LNS) * (NS * R) + jm;
 #pragma unroll
@@ -128,17 +112,55 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, c
     }
 }
 
+/// Pass 0 straight from the real signal tile.  Makhoul's packing
+/// w_m = v_{2m} + i v_{2m+1}, v = (x0, x2, ..., x3, x1), means every block of
+/// four samples x[4b..4b+3] (b < N/2) holds w_b = (x[4b], x[4b+2]) and
+/// w_{N-1-b} = (x[4b+3], x[4b+1]).  Butterflies j and j' = M-1-j of a radix-R
+/// pass (M = N/R) together need exactly the blocks j + rM and j' + rM for
+/// r < R/2, so each task loads R contiguous 32-byte blocks and runs both.
+template <int N, int TS>
+__device__ __forceinline__ void stockham_first(const double* __restrict__ x, double2* __restrict__ dst, int ptid,
+                                               int rows, bool& bad) {
+    constexpr int R = Passes<N>::FIRST_R, M = N / R, n = 2 * N;
+#pragma unroll
+    for (int t = ptid; t < TS * (M / 2); t += kProducerThreads) {
+        const int sig = t / (M / 2), j = t % (M / 2), jp = M - 1 - j;
+        const double* xr = x + sig * n;
+        double2 a[R], c[R]; // butterflies j and j'
+#pragma unroll
+        for (int r = 0; r < R / 2; ++r) {
+            const double2 b0 = *reinterpret_cast<const double2*>(xr + 4 * (j + r * M));
+            const double2 b1 = *reinterpret_cast<const double2*>(xr + 4 * (j + r * M) + 2);
+            const double2 e0 = *reinterpret_cast<const double2*>(xr + 4 * (jp + r * M));
+            const double2 e1 = *reinterpret_cast<const double2*>(xr + 4 * (jp + r * M) + 2);
+            if (sig < rows)
+                bad |= !isfinite(b0.x) || !isfinite(b0.y) || !isfinite(b1.x) || !isfinite(b1.y) ||
+                       !isfinite(e0.x) || !isfinite(e0.y) || !isfinite(e1.x) || !isfinite(e1.y);
+            a[r] = make_double2(b0.x, b1.x);
+            c[R - 1 - r] = make_double2(b1.y, b0.y);
+            c[r] = make_double2(e0.x, e1.x);
+            a[R - 1 - r] = make_double2(e1.y, e0.y);
+        }
+        butterfly<R>(a);
+        butterfly<R>(c);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            dst[sig * N + j * R + r] = a[r];
+            dst[sig * N + jp * R + r] = c[r];
+        }
+    }
+}
+
 /// Runs passes P.. of the FFT, ping-ponging between a and b; returns the
 /// buffer that holds the final (natural-order) spectrum.
 template <int N, int TS, int P>
-__device__ __forceinline__ double2* fft_passes(const double* x, double2* a, double2* b, const double2* ptw, int ptid,
-                                               int rows, bool& bad) {
+__device__ __forceinline__ double2* fft_passes(double2* a, double2* b, const double2* ptw, int ptid) {
     if constexpr (P == Passes<N>::COUNT) {
         return a; // `a` holds the output of the last pass
     } else {
-        stockham_pass<N, TS, P>(a, x, b, ptw, ptid, rows, bad);
+        stockham_pass<N, TS, P>(a, b, ptw, ptid);
         producer_sync();
-        return fft_passes<N, TS, P + 1>(x, b, a, ptw, ptid, rows, bad);
+        return fft_passes<N, TS, P + 1>(b, a, ptw, ptid);
     }
 }
 
@@ -168,6 +190,7 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
 
     const int tid = threadIdx.x;
     const int n_pass = P.n - P.K;
+    static_assert(kThreads == 512, "register split 256 x 88 + 256 x 168 assumes 512 threads");
 
     // ---- prologue: tables, barriers ---------------------------------------------
     {
@@ -206,6 +229,7 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
 
     if (tid < kProducerThreads) {
         // =============================== producer ===================================
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
         const int ptid = tid;
         auto issue = [&](std::size_t tile, int b) {
             const uint32_t bytes = static_cast<uint32_t>(rows_of(tile) * n * sizeof(double));
@@ -230,9 +254,9 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
             // FFT: pass 0 reads x (real) -> cw; then ping-pong cw <-> x (as complex)
             double2* xc = reinterpret_cast<double2*>(x);
             double2* F;
-            stockham_pass<N, TS, 0>(nullptr, x, cw, ptw, ptid, rows, bad);
+            stockham_first<N, TS>(x, cw, ptid, rows, bad);
             producer_sync();
-            F = fft_passes<N, TS, 1>(nullptr, cw, xc, ptw, ptid, rows, bad);
+            F = fft_passes<N, TS, 1>(cw, xc, ptw, ptid);
             // real split + rotation: shat into the buffer F does not occupy
             double* S = reinterpret_cast<double*>(F == cw ? xc : cw);
 #pragma unroll
@@ -277,12 +301,15 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
                 const int j = kept_idx[k];
                 if (j >= 0) ab[r * LDA + k] = S[r * n + j];
             }
+            for (int q = ptid; q < n_pass; q += kProducerThreads) {
+                const int d = pass_dst[q], src = pass_src[q];
+                const int slotq = d & 0xffff;
+                const bool neg = (d >> 30) != 0;
 #pragma unroll 4
-            for (int t = ptid; t < TS * n_pass; t += kProducerThreads) {
-                const int r = t / n_pass, q = t - r * n_pass;
-                const int d = pass_dst[q];
-                const double v = S[r * n + pass_src[q]];
-                ob[r * n + (d & 0xffff)] = (d >> 30) ? -v : v;
+                for (int r = 0; r < TS; ++r) {
+                    const double v = S[r * n + src];
+                    ob[r * n + slotq] = neg ? -v : v;
+                }
             }
             ptx::fence_proxy_async(); // pass-through writes -> visible to the consumers' TMA store
             ptx::mbar_arrive(&afull[b]);
@@ -292,10 +319,12 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
         if (bad) atomicOr(flag, 1);
     } else {
         // =============================== consumers ==================================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n" ::: "memory");
         const int ctid = tid - kProducerThreads;
         const int warp = ctid >> 5, lane = ctid & 31;
         // Cauchy fragments, resident for the whole kernel: B[k][c] = T[k][c] for
-        // this warp's NTW x 8 output columns c and all 4*KT (zero-padded) kept rows.
+        // this warp's NTW x 8 output columns c and all 4*KT (zero-padded) kept
+        // rows, from the plan's precomputed T (row c, K contiguous).
         double bf[KT][NTW];
 #pragma unroll
         for (int kt = 0; kt < KT; ++kt)
@@ -303,9 +332,7 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
             for (int nt = 0; nt < NTW; ++nt) {
                 const int k = kt * 4 + (lane & 3);
                 const int c = (warp * NTW + nt) * 8 + (lane >> 2);
-                double v = 0.0;
-                if (k < P.K && c < P.A) v = P.act_scale[c] * (P.z_kept[k] / (P.lam_kept[k] - P.nu[c]));
-                bf[kt][nt] = v;
+                bf[kt][nt] = (k < P.K && c < P.A) ? P.tmat[static_cast<std::size_t>(c) * P.K + k] : 0.0;
             }
         int slot[NTW][2];
 #pragma unroll

@@ -70,6 +70,7 @@ struct SmallPlanDev {
     const double* nu;        // A (secular roots, ascending)
     const double* act_scale; // A (sigma * a of the root's slot)
     const int* act_slot;     // A
+    const double* tmat;      // A x K: T[c][k] = sigma_c a_c z_k / (lambda_k - mu_c)
     const int* kept_idx;     // K: DCT index of each kept coefficient
     const int* pass_src;     // n - K: DCT index of each pass-through coefficient
     const int* pass_slot;    // n - K: its output slot

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <atomic>
@@ -359,6 +360,16 @@ struct dctp_plan {
     }
 };
 
+/// Development knob for profiling the fused kernel's phases in isolation
+/// (DCTP_DEBUG_MODE=1: DCT work skipped, =2: DMMA work skipped); 0 otherwise.
+static int debug_mode() {
+    static const int mode = [] {
+        const char* e = std::getenv("DCTP_DEBUG_MODE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return mode;
+}
+
 static void upload_plan(dctp_plan& p) {
     const auto& st = p.st;
     const ApplyTables t = make_tables(st);
@@ -464,7 +475,7 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
                                              at<int>(p->blob, p->pass_neg),
                                              at<double>(p->blob, p->fft_full), at<double>(p->blob, p->tw64.split),
                                              at<double>(p->blob, p->tw64.rot), static_cast<int>(n), p->fwd.rows,
-                                             p->fwd.cols};
+                                             p->fwd.cols, debug_mode()};
             cuda_check(DCTP_LAUNCH("fused_small_fwd", s,
                                    dctp::dev::fused_small_forward(in, out, batch, sp, p->flag, p->num_sms, s)),
                        "fused small forward kernel");

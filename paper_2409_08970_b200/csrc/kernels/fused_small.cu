@@ -89,15 +89,20 @@ struct Passes {
     static constexpr int TWIDDLES = twiddle_offset(COUNT);
 };
 
-/// One Stockham (autosort) pass over TS rows (P >= 1).
-template <int N, int TS, int P>
+__device__ __forceinline__ bool non_finite(double v) {
+    return ((__double_as_longlong(v) >> 52) & 0x7ff) == 0x7ff; // integer test: keeps the fp64 pipe free
+}
+
+/// One Stockham (autosort) pass (P >= 1) over the SPW signals one producer
+/// warp owns; lanes stride over the butterflies, the SPW rows interleave.
+template <int N, int SPW, int P>
 __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, double2* __restrict__ dst,
-                                              const double2* __restrict__ ptw, int ptid) {
+                                              const double2* __restrict__ ptw, int lane) {
     constexpr int R = Passes<N>::radix(P), LNS = Passes<N>::lns(P), NS = 1 << LNS;
     constexpr int M = N / R;
     constexpr int TWO = Passes<N>::twiddle_offset(P);
 #pragma unroll
-    for (int t = ptid; t < TS * M; t += kProducerThreads) {
+    for (int t = lane; t < SPW * M; t += 32) {
         const int sig = t / M, j = t % M;
         double2 v[R];
 #pragma unroll
@@ -112,18 +117,18 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
     }
 }
 
-/// Pass 0 straight from the real signal tile.  Makhoul's packing
+/// Pass 0 straight from the real signal rows.  Makhoul's packing
 /// w_m = v_{2m} + i v_{2m+1}, v = (x0, x2, ..., x3, x1), means every block of
 /// four samples x[4b..4b+3] (b < N/2) holds w_b = (x[4b], x[4b+2]) and
 /// w_{N-1-b} = (x[4b+3], x[4b+1]).  Butterflies j and j' = M-1-j of a radix-R
 /// pass (M = N/R) together need exactly the blocks j + rM and j' + rM for
 /// r < R/2, so each task loads R contiguous 32-byte blocks and runs both.
-template <int N, int TS>
-__device__ __forceinline__ void stockham_first(const double* __restrict__ x, double2* __restrict__ dst, int ptid,
-                                               int rows, bool& bad) {
+template <int N, int SPW>
+__device__ __forceinline__ void stockham_first(const double* __restrict__ x, double2* __restrict__ dst, int lane,
+                                               int valid_rows, bool& bad) {
     constexpr int R = Passes<N>::FIRST_R, M = N / R, n = 2 * N;
 #pragma unroll
-    for (int t = ptid; t < TS * (M / 2); t += kProducerThreads) {
+    for (int t = lane; t < SPW * (M / 2); t += 32) {
         const int sig = t / (M / 2), j = t % (M / 2), jp = M - 1 - j;
         const double* xr = x + sig * n;
         double2 a[R], c[R]; // butterflies j and j'
@@ -133,9 +138,9 @@ __device__ __forceinline__ void stockham_first(const double* __restrict__ x, dou
             const double2 b1 = *reinterpret_cast<const double2*>(xr + 4 * (j + r * M) + 2);
             const double2 e0 = *reinterpret_cast<const double2*>(xr + 4 * (jp + r * M));
             const double2 e1 = *reinterpret_cast<const double2*>(xr + 4 * (jp + r * M) + 2);
-            if (sig < rows)
-                bad |= !isfinite(b0.x) || !isfinite(b0.y) || !isfinite(b1.x) || !isfinite(b1.y) ||
-                       !isfinite(e0.x) || !isfinite(e0.y) || !isfinite(e1.x) || !isfinite(e1.y);
+            if (sig < valid_rows)
+                bad |= non_finite(b0.x) | non_finite(b0.y) | non_finite(b1.x) | non_finite(b1.y) |
+                       non_finite(e0.x) | non_finite(e0.y) | non_finite(e1.x) | non_finite(e1.y);
             a[r] = make_double2(b0.x, b1.x);
             c[R - 1 - r] = make_double2(b1.y, b0.y);
             c[r] = make_double2(e0.x, e1.x);
@@ -151,16 +156,16 @@ __device__ __forceinline__ void stockham_first(const double* __restrict__ x, dou
     }
 }
 
-/// Runs passes P.. of the FFT, ping-ponging between a and b; returns the
-/// buffer that holds the final (natural-order) spectrum.
-template <int N, int TS, int P>
-__device__ __forceinline__ double2* fft_passes(double2* a, double2* b, const double2* ptw, int ptid) {
+/// Runs passes P.. of the FFT for one warp's rows, ping-ponging between a and
+/// b (warp-synchronous: no CTA barrier); returns the buffer with the result.
+template <int N, int SPW, int P>
+__device__ __forceinline__ double2* fft_passes(double2* a, double2* b, const double2* ptw, int lane) {
     if constexpr (P == Passes<N>::COUNT) {
         return a; // `a` holds the output of the last pass
     } else {
-        stockham_pass<N, TS, P>(a, b, ptw, ptid);
-        producer_sync();
-        return fft_passes<N, TS, P + 1>(b, a, ptw, ptid);
+        stockham_pass<N, SPW, P>(a, b, ptw, lane);
+        __syncwarp();
+        return fft_passes<N, SPW, P + 1>(b, a, ptw, lane);
     }
 }
 
@@ -179,7 +184,8 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
     double2* ptw = reinterpret_cast<double2*>(atile + 2 * TS * LDA);
     double2* sp = ptw + (PS::TWIDDLES > 0 ? PS::TWIDDLES : 1);
     double2* rt = sp + N;
-    int* kept_idx = reinterpret_cast<int*>(rt + N + 1); // KT*4
+    double2* rt2 = rt + N + 1;                           // rt * sqrt(2/n) / 2
+    int* kept_idx = reinterpret_cast<int*>(rt2 + N + 1); // KT*4
     int* pass_src = kept_idx + 4 * KT;                   // n (used: P.n - P.K)
     int* pass_dst = pass_src + n;                        // n: slot, with the sign in bit 30
     uint64_t* bars = reinterpret_cast<uint64_t*>(pass_dst + n);
@@ -187,6 +193,7 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
     uint64_t* afull = bars + 2;   // [2] producer -> consumers: A tile + pass-through written
     uint64_t* aempty = bars + 4;  // [2] consumers -> producer: A tile consumed
     uint64_t* xofree = bars + 6;  // [2] output tile's TMA store has read it
+    uint64_t* xempty = bars + 8;  // [2] every producer warp is done reading xin[b]
 
     const int tid = threadIdx.x;
     const int n_pass = P.n - P.K;
@@ -204,7 +211,12 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
             }
         }
         for (int i = tid; i < N; i += kThreads) sp[i] = reinterpret_cast<const double2*>(P.split_tw)[i];
-        for (int i = tid; i <= N; i += kThreads) rt[i] = reinterpret_cast<const double2*>(P.rot_tw)[i];
+        for (int i = tid; i <= N; i += kThreads) {
+            const double2 r = reinterpret_cast<const double2*>(P.rot_tw)[i];
+            const double h = 0.5 * sqrt(2.0 / n);
+            rt[i] = r;
+            rt2[i] = make_double2(r.x * h, r.y * h);
+        }
         for (int i = tid; i < 4 * KT; i += kThreads) kept_idx[i] = i < P.K ? P.kept_idx[i] : -1;
         for (int i = tid; i < n_pass; i += kThreads) {
             pass_src[i] = P.pass_src[i];
@@ -217,6 +229,7 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
                 ptx::mbar_init(&afull[b], kProducerThreads);
                 ptx::mbar_init(&aempty[b], 32 * kConsumerWarps);
                 ptx::mbar_init(&xofree[b], 1);
+                ptx::mbar_init(&xempty[b], kProducerThreads);
             }
             ptx::fence_mbar_init();
         }
@@ -229,8 +242,11 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
 
     if (tid < kProducerThreads) {
         // =============================== producer ===================================
+        // Each producer warp owns SPW = TS/8 rows of every tile and runs their
+        // whole DCT warp-synchronously; the warps only meet at the mbarriers.
         asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
-        const int ptid = tid;
+        constexpr int SPW = TS / (kProducerThreads / 32);
+        const int ptid = tid, pw = ptid >> 5, lane = ptid & 31;
         auto issue = [&](std::size_t tile, int b) {
             const uint32_t bytes = static_cast<uint32_t>(rows_of(tile) * n * sizeof(double));
             ptx::mbar_expect_tx(&xfull[b], bytes);
@@ -242,79 +258,84 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
         }
         const double scale = sqrt(2.0 / n);
         const double dc_scale = 1.0 / sqrt(static_cast<double>(n));
+        const double y_n = rt[N].x * scale;
         bool bad = false;
         int it = 0;
         for (std::size_t tile = blockIdx.x; tile < ntiles; tile += grid, ++it) {
             const int b = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            const int rows = rows_of(tile);
-            double* x = xin + b * TILE;
-            ptx::mbar_wait(&xfull[b], ph);
-
-            // FFT: pass 0 reads x (real) -> cw; then ping-pong cw <-> x (as complex)
+            const int valid = rows_of(tile) - pw * SPW; // rows of this warp holding real signals
+            double* x = xin + b * TILE + pw * SPW * n;
             double2* xc = reinterpret_cast<double2*>(x);
-            double2* F;
-            stockham_first<N, TS>(x, cw, ptid, rows, bad);
-            producer_sync();
-            F = fft_passes<N, TS, 1>(cw, xc, ptw, ptid);
-            // real split + rotation: shat into the buffer F does not occupy
-            double* S = reinterpret_cast<double*>(F == cw ? xc : cw);
+            double2* cwp = cw + pw * SPW * N;
+            ptx::mbar_wait(&xfull[b], ph);
+            if (P.debug != 1) {
+                stockham_first<N, SPW>(x, cwp, lane, valid, bad);
+                __syncwarp();
+                double2* F = fft_passes<N, SPW, 1>(cwp, xc, ptw, lane);
+                // real split + rotation (rt2 = e^{-i pi k/2n} sqrt(2/n)/2): shat into the free buffer
+                double* S = reinterpret_cast<double*>(F == cwp ? xc : cwp);
 #pragma unroll
-            for (int t = ptid; t < TS * (N / 2 + 1); t += kProducerThreads) {
-                const int r = t / (N / 2 + 1), k = t % (N / 2 + 1);
-                const double2* row = F + r * N;
-                double* o = S + r * n;
-                if (k == 0) {
-                    const double2 w0 = row[0];
-                    o[0] = (w0.x + w0.y) * dc_scale;
-                    o[N] = (w0.x - w0.y) * rt[N].x * scale;
-                    continue;
-                }
-                // k and N - k together: both read W_k and W_{N-k}
-                const double2 wk = row[k], wc = row[N - k];
+                for (int t = lane; t < SPW * (N / 2 + 1); t += 32) {
+                    const int r = t / (N / 2 + 1), k = t % (N / 2 + 1);
+                    const double2* row = F + r * N;
+                    double* o = S + r * n;
+                    if (k == 0) {
+                        const double2 w0 = row[0];
+                        o[0] = (w0.x + w0.y) * dc_scale;
+                        o[N] = (w0.x - w0.y) * y_n;
+                        continue;
+                    }
+                    const double2 wk = row[k], wc = row[N - k];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int kk = h == 0 ? k : N - k;
-                    if (h == 1 && kk == k) break;
-                    const double2 a = h == 0 ? wk : wc, c = h == 0 ? wc : wk;
-                    const double er = 0.5 * (a.x + c.x), ei = 0.5 * (a.y - c.y);
-                    const double orr = 0.5 * (a.x - c.x), oi = 0.5 * (a.y + c.y);
-                    const double2 s2 = sp[kk];
-                    const double qr = s2.x * orr - s2.y * oi, qi = s2.x * oi + s2.y * orr;
-                    const double vr = er + qi, vi = ei - qr;
-                    const double2 c2 = rt[kk];
-                    o[kk] = (vr * c2.x - vi * c2.y) * scale;
-                    o[n - kk] = -(vr * c2.y + vi * c2.x) * scale;
+                    for (int h = 0; h < 2; ++h) {
+                        const int kk = h == 0 ? k : N - k;
+                        if (h == 1 && kk == k) break;
+                        const double2 a = h == 0 ? wk : wc, c = h == 0 ? wc : wk;
+                        const double sr = a.x + c.x, si = a.y - c.y; // a + conj(c)
+                        const double dr = a.x - c.x, di = a.y + c.y; // a - conj(c)
+                        const double2 s2 = sp[kk];
+                        const double qr = s2.x * dr - s2.y * di, qi = s2.x * di + s2.y * dr;
+                        const double vr = sr + qi, vi = si - qr; // 2 V_kk
+                        const double2 c2 = rt2[kk];
+                        o[kk] = vr * c2.x - vi * c2.y;
+                        o[n - kk] = -(vr * c2.y + vi * c2.x);
+                    }
                 }
-            }
-            producer_sync();
-            // the output tile and the A tile of this buffer must be free again
-            if (it >= 2) {
+                __syncwarp();
+                if (it >= 2) {
+                    ptx::mbar_wait(&xofree[b], ((it - 2) >> 1) & 1);
+                    ptx::mbar_wait(&aempty[b], ((it - 2) >> 1) & 1);
+                }
+                double* ob = xout + b * TILE + pw * SPW * n;
+                double* ab = atile + b * TS * LDA + pw * SPW * LDA;
+#pragma unroll
+                for (int t = lane; t < SPW * 4 * KT; t += 32) {
+                    const int r = t / (4 * KT), k = t % (4 * KT);
+                    const int j = kept_idx[k];
+                    if (j >= 0) ab[r * LDA + k] = S[r * n + j];
+                }
+                for (int q = lane; q < n_pass; q += 32) {
+                    const int d = pass_dst[q], src = pass_src[q];
+                    const int slotq = d & 0xffff;
+                    const bool neg = (d >> 30) != 0;
+#pragma unroll
+                    for (int r = 0; r < SPW; ++r) {
+                        const double v = S[r * n + src];
+                        ob[r * n + slotq] = neg ? -v : v;
+                    }
+                }
+                ptx::fence_proxy_async(); // pass-through writes -> visible to the consumers' TMA store
+            } else if (it >= 2) {
                 ptx::mbar_wait(&xofree[b], ((it - 2) >> 1) & 1);
                 ptx::mbar_wait(&aempty[b], ((it - 2) >> 1) & 1);
             }
-            double* ob = xout + b * TILE;
-            double* ab = atile + b * TS * LDA;
-#pragma unroll 4
-            for (int t = ptid; t < TS * 4 * KT; t += kProducerThreads) {
-                const int r = t / (4 * KT), k = t % (4 * KT);
-                const int j = kept_idx[k];
-                if (j >= 0) ab[r * LDA + k] = S[r * n + j];
-            }
-            for (int q = ptid; q < n_pass; q += kProducerThreads) {
-                const int d = pass_dst[q], src = pass_src[q];
-                const int slotq = d & 0xffff;
-                const bool neg = (d >> 30) != 0;
-#pragma unroll 4
-                for (int r = 0; r < TS; ++r) {
-                    const double v = S[r * n + src];
-                    ob[r * n + slotq] = neg ? -v : v;
-                }
-            }
-            ptx::fence_proxy_async(); // pass-through writes -> visible to the consumers' TMA store
             ptx::mbar_arrive(&afull[b]);
-            producer_sync(); // every read of x / cw for this tile is done
-            if (ptid == 0 && tile + 2 * grid < ntiles) issue(tile + 2 * grid, b);
+            ptx::mbar_arrive(&xempty[b]); // this warp is done with xin[b] (and its cw rows)
+            if (ptid == 0 && tile + 2 * grid < ntiles) {
+                ptx::mbar_wait(&xempty[b], ph);
+                issue(tile + 2 * grid, b);
+            }
         }
         if (bad) atomicOr(flag, 1);
     } else {
@@ -355,6 +376,7 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
                 for (int nt = 0; nt < NTW; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 #pragma unroll
             for (int kt = 0; kt < KT; ++kt) {
+                if (P.debug == 2) break;
                 double a[MT];
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) a[mt] = arow[mt * 8 * LDA + kt * 4];
@@ -393,7 +415,7 @@ constexpr std::size_t smem_bytes() {
     constexpr int n = 1 << LOGN, N = n / 2, TILE = TS * n;
     constexpr int tw = Passes<N>::TWIDDLES > 0 ? Passes<N>::TWIDDLES : 1;
     return 4 * TILE * sizeof(double) + (TILE / 2) * sizeof(double2) + 2 * TS * LDA * sizeof(double) +
-           (tw + 2 * N + 1) * sizeof(double2) + (4 * KT + 2 * n) * sizeof(int) + 8 * sizeof(uint64_t);
+           (tw + 3 * N + 2) * sizeof(double2) + (4 * KT + 2 * n) * sizeof(int) + 10 * sizeof(uint64_t);
 }
 
 template <int LOGN, int NTW, int KT>

@@ -79,6 +79,7 @@ struct SmallPlanDev {
     const double* split_tw;  // N complex e^{-2 pi i k / n}
     const double* rot_tw;    // N+1 complex e^{-i pi k / 2n}
     int n, K, A;
+    int debug; // development knob (DCTP_DEBUG_MODE): 1 = skip the DCT work, 2 = skip the DMMA work
 };
 
 bool fused_small_supported(std::size_t n, int K, int A);

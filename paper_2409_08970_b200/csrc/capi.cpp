@@ -319,7 +319,12 @@ struct dctp_plan {
     std::size_t stage_desc = 0; // 4 CauchyStage descriptors: fwd64, fwd32, inv64, inv32
     int n_pass = 0;
     bool small = false;         // fused small-plan forward kernel eligible
-    std::size_t pass_neg = 0, tmat = 0, fft_full = 0, act_scale64 = 0, z64 = 0, lam = 0, nu = 0, act_slot = 0, kept = 0;
+    std::size_t act_scale64 = 0, z64 = 0, lam = 0, nu = 0, act_slot = 0, kept = 0;
+    struct {
+        std::size_t act_slot = 0, tmat = 0, kept = 0, pass_src = 0, pass_slot = 0, pass_coef = 0;
+        std::size_t fft = 0, split = 0, rot = 0;
+        int K = 0, A = 0, n_pass = 0, fold = 0;
+    } sm;
     int num_sms = 0;
 
     ~dctp_plan() {
@@ -360,14 +365,125 @@ struct dctp_plan {
     }
 };
 
+/// Constants of the fused small-plan kernel (fused_small.cu): generic, or
+/// folded when every kept DCT index is odd (antisymmetric update direction).
+static void build_small(dctp_plan& p, Blob& blob, const ApplyTables& t) {
+    const auto& st = p.st;
+    const std::size_t n = st.n, K = t.kept_idx.size(), A = t.nu.size();
+    bool odd_only = K > 0;
+    for (int j : t.kept_idx) odd_only = odd_only && (j % 2 == 1);
+    std::size_t odd_pass = 0;
+    for (int j : t.pass_src) odd_pass += (j % 2 == 1);
+    const bool fold = odd_only && dctp::dev::fused_small_fold_supported(n, static_cast<int>(A + odd_pass));
+    p.small = fold || dctp::dev::fused_small_supported(n, static_cast<int>(K), static_cast<int>(A));
+    if (!p.small) return;
+    const double pi = std::numbers::pi;
+    const std::size_t L = fold ? n / 2 : n, NC = L / 2;
+    std::vector<int> act, psrc, pslot, kept;
+    std::vector<double> pcoef, tm;
+    if (!fold) {
+        // T[c][k] = sigma_c a_c z_k / (lambda_k - mu_c): the reference's dense T
+        // (fast_transform.hpp:355-366, row = slot) restricted to active x kept.
+        tm.resize(A * K);
+        for (std::size_t c = 0; c < A; ++c)
+            for (std::size_t k = 0; k < K; ++k) tm[c * K + k] = t.act_scale[c] * (t.z_kept[k] / (t.lam_kept[k] - t.nu[c]));
+        act = t.act_slot;
+        kept = t.kept_idx;
+        psrc = t.pass_src;
+        pslot = t.pass_slot;
+        pcoef = t.pass_sign;
+        p.sm.K = static_cast<int>(K);
+    } else {
+        // W[c][j] = sum_k T[c][k] D[m_k][j], D[m][j] = sqrt(2/n) cos(pi (2m+1)(2j+1) / 2n),
+        // kept_k = 2 m_k + 1; odd pass-through slots add rows sigma D[m][j].
+        auto dcos = [&](std::size_t m, std::size_t j) {
+            const std::size_t q = ((2 * m + 1) * (2 * j + 1)) % (4 * n);
+            return std::sqrt(2.0L / n) * std::cos(static_cast<long double>(pi) * q / (2.0L * n));
+        };
+        const std::size_t cols = A + odd_pass;
+        tm.assign(cols * L, 0.0);
+        for (std::size_t c = 0; c < A; ++c) {
+            std::vector<long double> row(L, 0.0L);
+            for (std::size_t k = 0; k < K; ++k) {
+                const long double tk = t.act_scale[c] * (t.z_kept[k] / (t.lam_kept[k] - t.nu[c]));
+                const std::size_t m = (t.kept_idx[k] - 1) / 2;
+                for (std::size_t j = 0; j < L; ++j) row[j] += tk * dcos(m, j);
+            }
+            for (std::size_t j = 0; j < L; ++j) tm[c * L + j] = static_cast<double>(row[j]);
+            act.push_back(t.act_slot[c]);
+        }
+        std::size_t c = A;
+        for (std::size_t q = 0; q < t.pass_src.size(); ++q) {
+            const int j0 = t.pass_src[q];
+            if (j0 % 2 == 1) {
+                for (std::size_t j = 0; j < L; ++j)
+                    tm[c * L + j] = static_cast<double>(t.pass_sign[q] * dcos((j0 - 1) / 2, j));
+                act.push_back(t.pass_slot[q]);
+                ++c;
+            } else {
+                psrc.push_back(j0 / 2);
+                pslot.push_back(t.pass_slot[q]);
+                pcoef.push_back(t.pass_sign[q] / std::numbers::sqrt2);
+            }
+        }
+        p.sm.K = static_cast<int>(L);
+    }
+    p.sm.A = static_cast<int>(act.size());
+    p.sm.n_pass = static_cast<int>(psrc.size());
+    p.sm.fold = fold ? 1 : 0;
+    p.sm.act_slot = blob.add(act);
+    p.sm.tmat = blob.add(tm);
+    p.sm.kept = blob.add(kept);
+    p.sm.pass_src = blob.add(psrc);
+    p.sm.pass_slot = blob.add(pslot);
+    p.sm.pass_coef = blob.add(pcoef);
+    std::vector<double> fft(2 * NC), split(2 * NC), rot(2 * (NC + 1));
+    for (std::size_t m = 0; m < fft.size() / 2; ++m) {
+        const double a = 2.0 * pi * static_cast<double>(m) / static_cast<double>(NC);
+        fft[2 * m] = std::cos(a);
+        fft[2 * m + 1] = -std::sin(a);
+    }
+    for (std::size_t k = 0; k < NC; ++k) {
+        const double a = 2.0 * pi * static_cast<double>(k) / static_cast<double>(L);
+        split[2 * k] = std::cos(a);
+        split[2 * k + 1] = -std::sin(a);
+    }
+    for (std::size_t k = 0; k <= NC; ++k) {
+        const double a = pi * static_cast<double>(k) / (2.0 * static_cast<double>(L));
+        rot[2 * k] = std::cos(a);
+        rot[2 * k + 1] = -std::sin(a);
+    }
+    p.sm.fft = blob.add(fft);
+    p.sm.split = blob.add(split);
+    p.sm.rot = blob.add(rot);
+}
+
 /// Development knob for profiling the fused kernel's phases in isolation
-/// (DCTP_DEBUG_MODE=1: DCT work skipped, =2: DMMA work skipped); 0 otherwise.
+/// (DCTP_DEBUG_MODE bits: 1 = DCT work skipped, 2 = DMMA work skipped, 4 = producer
+/// phase timers); 0 otherwise.
 static int debug_mode() {
     static const int mode = [] {
         const char* e = std::getenv("DCTP_DEBUG_MODE");
         return e ? std::atoi(e) : 0;
     }();
     return mode;
+}
+
+static unsigned long long* g_debug_timers = nullptr;
+static unsigned long long* debug_timers() {
+    if ((debug_mode() & 4) == 0) return nullptr;
+    if (!g_debug_timers) {
+        cudaMalloc(reinterpret_cast<void**>(&g_debug_timers), 8 * sizeof(unsigned long long));
+        cudaMemset(g_debug_timers, 0, 8 * sizeof(unsigned long long));
+    }
+    return g_debug_timers;
+}
+
+extern "C" int dctp_debug_timers(unsigned long long* out8) {
+    if (!g_debug_timers) return 1;
+    cudaMemcpy(out8, g_debug_timers, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemset(g_debug_timers, 0, 8 * sizeof(unsigned long long));
+    return 0;
 }
 
 static void upload_plan(dctp_plan& p) {
@@ -389,28 +505,7 @@ static void upload_plan(dctp_plan& p) {
     p.nu = nu;
     p.act_slot = act;
     p.kept = kept_idx;
-    p.small = dctp::dev::fused_small_supported(st.n, static_cast<int>(t.kept_idx.size()),
-                                               static_cast<int>(t.nu.size()));
-    if (p.small) {
-        std::vector<int> neg(t.pass_sign.size());
-        for (std::size_t q = 0; q < neg.size(); ++q) neg[q] = t.pass_sign[q] < 0.0 ? 1 : 0;
-        p.pass_neg = blob.add(neg);
-        // T[c][k] = sigma_c a_c z_k / (lambda_k - mu_c): the reference's dense T
-        // (fast_transform.hpp:355-366, row = slot) restricted to active x kept.
-        const std::size_t K = t.kept_idx.size(), A = t.nu.size();
-        std::vector<double> tm(A * K);
-        for (std::size_t c = 0; c < A; ++c)
-            for (std::size_t k = 0; k < K; ++k) tm[c * K + k] = t.act_scale[c] * (t.z_kept[k] / (t.lam_kept[k] - t.nu[c]));
-        p.tmat = blob.add(tm);
-        const std::size_t N = st.n / 2;
-        std::vector<double> fftN(2 * N);
-        for (std::size_t m = 0; m < N; ++m) {
-            const double a = 2.0 * std::numbers::pi * static_cast<double>(m) / static_cast<double>(N);
-            fftN[2 * m] = std::cos(a);
-            fftN[2 * m + 1] = -std::sin(a);
-        }
-        p.fft_full = blob.add(fftN);
-    }
+    build_small(p, blob, t);
     p.pass_sign64 = blob.add(t.pass_sign);
     p.pass_sign32 = blob.add(to_f32(t.pass_sign));
     p.n_pass = static_cast<int>(t.pass_slot.size());
@@ -467,15 +562,13 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
     DeviceScope scope(p->device);
     if constexpr (std::is_same_v<T, double>) {
         if (p->small) {
-            const dctp::dev::SmallPlanDev sp{at<double>(p->blob, p->lam), at<double>(p->blob, p->z64),
-                                             at<double>(p->blob, p->nu), at<double>(p->blob, p->act_scale64),
-                                             at<int>(p->blob, p->act_slot), at<double>(p->blob, p->tmat),
-                                             at<int>(p->blob, p->kept),
-                                             at<int>(p->blob, p->pass_src), at<int>(p->blob, p->pass_slot),
-                                             at<int>(p->blob, p->pass_neg),
-                                             at<double>(p->blob, p->fft_full), at<double>(p->blob, p->tw64.split),
-                                             at<double>(p->blob, p->tw64.rot), static_cast<int>(n), p->fwd.rows,
-                                             p->fwd.cols, debug_mode()};
+            const auto& m = p->sm;
+            const dctp::dev::SmallPlanDev sp{at<int>(p->blob, m.act_slot), at<double>(p->blob, m.tmat),
+                                             at<int>(p->blob, m.kept), at<int>(p->blob, m.pass_src),
+                                             at<int>(p->blob, m.pass_slot), at<double>(p->blob, m.pass_coef),
+                                             at<double>(p->blob, m.fft), at<double>(p->blob, m.split),
+                                             at<double>(p->blob, m.rot), static_cast<int>(n), m.K, m.A, m.n_pass,
+                                             m.fold, debug_timers(), debug_mode()};
             cuda_check(DCTP_LAUNCH("fused_small_fwd", s,
                                    dctp::dev::fused_small_forward(in, out, batch, sp, p->flag, p->num_sms, s)),
                        "fused small forward kernel");

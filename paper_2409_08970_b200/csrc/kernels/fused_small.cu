@@ -89,6 +89,17 @@ struct Passes {
     static constexpr int TWIDDLES = twiddle_offset(COUNT);
 };
 
+/// for (t = lane; t < TOTAL; t += 32) f(t), with a compile-time trip count.
+template <int TOTAL, class F>
+__device__ __forceinline__ void lane_loop(int lane, F&& f) {
+#pragma unroll
+    for (int i = 0; i < TOTAL / 32; ++i) f(lane + 32 * i);
+    if constexpr (TOTAL % 32 != 0) {
+        const int t = lane + 32 * (TOTAL / 32);
+        if (t < TOTAL) f(t);
+    }
+}
+
 __device__ __forceinline__ bool non_finite(double v) {
     return ((__double_as_longlong(v) >> 52) & 0x7ff) == 0x7ff; // integer test: keeps the fp64 pipe free
 }
@@ -101,8 +112,7 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
     constexpr int R = Passes<N>::radix(P), LNS = Passes<N>::lns(P), NS = 1 << LNS;
     constexpr int M = N / R;
     constexpr int TWO = Passes<N>::twiddle_offset(P);
-#pragma unroll
-    for (int t = lane; t < SPW * M; t += 32) {
+    lane_loop<SPW * M>(lane, [&](int t) {
         const int sig = t / M, j = t % M;
         double2 v[R];
 #pragma unroll
@@ -114,7 +124,7 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
         const int d = (j >> LNS) * (NS * R) + jm;
 #pragma unroll
         for (int r = 0; r < R; ++r) dst[sig * N + d + r * NS] = v[r];
-    }
+    });
 }
 
 /// Pass 0 straight from the real signal rows.  Makhoul's packing
@@ -127,8 +137,7 @@ template <int N, int SPW>
 __device__ __forceinline__ void stockham_first(const double* __restrict__ x, double2* __restrict__ dst, int lane,
                                                int valid_rows, bool& bad) {
     constexpr int R = Passes<N>::FIRST_R, M = N / R, n = 2 * N;
-#pragma unroll
-    for (int t = lane; t < SPW * (M / 2); t += 32) {
+    lane_loop<SPW * (M / 2)>(lane, [&](int t) {
         const int sig = t / (M / 2), j = t % (M / 2), jp = M - 1 - j;
         const double* xr = x + sig * n;
         double2 a[R], c[R]; // butterflies j and j'
@@ -153,7 +162,7 @@ __device__ __forceinline__ void stockham_first(const double* __restrict__ x, dou
             dst[sig * N + j * R + r] = a[r];
             dst[sig * N + jp * R + r] = c[r];
         }
-    }
+    });
 }
 
 /// Runs passes P.. of the FFT for one warp's rows, ping-ponging between a and
@@ -169,13 +178,20 @@ __device__ __forceinline__ double2* fft_passes(double2* a, double2* b, const dou
     }
 }
 
-template <int LOGN, int NTW, int KT, int TS>
+/// FOLD = false: generic plan, the DCT has length L = n.
+/// FOLD = true : antisymmetric update (every kept DCT index is odd).  Then
+///   shat_{2m+1} = sqrt(2/n) sum_j u_j cos(pi (2m+1)(2j+1)/2n),  u_j = x_j - x_{n-1-j},
+///   shat_{2m}   = DCT-II_{n/2}(y)_m / sqrt(2),                y_j = x_j + x_{n-1-j},
+/// so the Cauchy stage runs on u against W = D_odd^T T (the DCT-IV folded into
+/// the plan's matrix, same DMMA work as T) and only the length-n/2 DCT-II of y
+/// goes through the FFT — half the producer work (deflation).
+template <int LOGN, int NTW, int KT, int TS, bool FOLD>
 __global__ void __launch_bounds__(kThreads, 1)
 fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, std::size_t batch, SmallPlanDev P,
                        int* flag) {
-    constexpr int n = 1 << LOGN, N = n / 2, MT = TS / 8;
-    constexpr int TILE = TS * n; // doubles per signal tile (== TS*N complex)
-    using PS = Passes<N>;
+    constexpr int n = 1 << LOGN, L = FOLD ? n / 2 : n, NC = L / 2, MT = TS / 8;
+    constexpr int TILE = TS * n; // doubles per signal tile
+    using PS = Passes<NC>;
     extern __shared__ __align__(128) unsigned char smem[];
     double* xin = reinterpret_cast<double*>(smem);            // 2 x TILE: TMA-loaded input tiles
     double* xout = xin + 2 * TILE;                             // 2 x TILE: assembled output tiles
@@ -183,11 +199,12 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
     double* atile = reinterpret_cast<double*>(cw + TILE / 2);  // 2 x TS x LDA: Cauchy A operand
     double2* ptw = reinterpret_cast<double2*>(atile + 2 * TS * LDA);
     double2* sp = ptw + (PS::TWIDDLES > 0 ? PS::TWIDDLES : 1);
-    double2* rt = sp + N;
-    double2* rt2 = rt + N + 1;                           // rt * sqrt(2/n) / 2
-    int* kept_idx = reinterpret_cast<int*>(rt2 + N + 1); // KT*4
-    int* pass_src = kept_idx + 4 * KT;                   // n (used: P.n - P.K)
-    int* pass_dst = pass_src + n;                        // n: slot, with the sign in bit 30
+    double2* rt = sp + NC;
+    double2* rt2 = rt + NC + 1;                          // rt * sqrt(2/L) / 2
+    double* pass_coef = reinterpret_cast<double*>(rt2 + NC + 1); // n: sign (or sign/sqrt2 when folded)
+    int* kept_idx = reinterpret_cast<int*>(pass_coef + n); // KT*4
+    int* pass_src = kept_idx + 4 * KT;                     // n: index into the length-L coefficients
+    int* pass_dst = pass_src + n;                          // n: output slot
     uint64_t* bars = reinterpret_cast<uint64_t*>(pass_dst + n);
     uint64_t* xfull = bars;       // [2] TMA load landed
     uint64_t* afull = bars + 2;   // [2] producer -> consumers: A tile + pass-through written
@@ -196,7 +213,7 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
     uint64_t* xempty = bars + 8;  // [2] every producer warp is done reading xin[b]
 
     const int tid = threadIdx.x;
-    const int n_pass = P.n - P.K;
+    const int n_pass = P.n_pass;
     static_assert(kThreads == 512, "register split 256 x 88 + 256 x 168 assumes 512 threads");
 
     // ---- prologue: tables, barriers ---------------------------------------------
@@ -207,20 +224,21 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
             const int R = PS::radix(p), ns = 1 << PS::lns(p), off = PS::twiddle_offset(p);
             for (int i = tid; i < ns * (R - 1); i += kThreads) {
                 const int jm = i / (R - 1), r = i % (R - 1) + 1;
-                ptw[off + i] = fft[(r * jm * (N / ns)) / R];
+                ptw[off + i] = fft[(r * jm * (NC / ns)) / R];
             }
         }
-        for (int i = tid; i < N; i += kThreads) sp[i] = reinterpret_cast<const double2*>(P.split_tw)[i];
-        for (int i = tid; i <= N; i += kThreads) {
+        for (int i = tid; i < NC; i += kThreads) sp[i] = reinterpret_cast<const double2*>(P.split_tw)[i];
+        for (int i = tid; i <= NC; i += kThreads) {
             const double2 r = reinterpret_cast<const double2*>(P.rot_tw)[i];
-            const double h = 0.5 * sqrt(2.0 / n);
+            const double h = 0.5 * sqrt(2.0 / L);
             rt[i] = r;
             rt2[i] = make_double2(r.x * h, r.y * h);
         }
         for (int i = tid; i < 4 * KT; i += kThreads) kept_idx[i] = i < P.K ? P.kept_idx[i] : -1;
         for (int i = tid; i < n_pass; i += kThreads) {
             pass_src[i] = P.pass_src[i];
-            pass_dst[i] = P.pass_slot[i] | (P.pass_neg[i] ? (1 << 30) : 0);
+            pass_dst[i] = P.pass_slot[i];
+            pass_coef[i] = P.pass_coef[i];
         }
         for (int i = tid; i < 2 * TS * LDA; i += kThreads) atile[i] = 0.0;
         if (tid == 0) {
@@ -256,41 +274,69 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
             if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
             if (blockIdx.x + grid < ntiles) issue(blockIdx.x + grid, 1);
         }
-        const double scale = sqrt(2.0 / n);
-        const double dc_scale = 1.0 / sqrt(static_cast<double>(n));
-        const double y_n = rt[N].x * scale;
+        const double scale = sqrt(2.0 / L);
+        const double dc_scale = 1.0 / sqrt(static_cast<double>(L));
+        const double y_n = rt[NC].x * scale;
         bool bad = false;
         int it = 0;
+        // DCTP_DEBUG_MODE & 4: per-phase cycle accounting of the producer (lane 0 of each warp)
+        unsigned long long tacc[7] = {0, 0, 0, 0, 0, 0, 0};
+        long long tlast = clock64();
+#define T_MARK(i)                                                   \
+    if (P.timers != nullptr && lane == 0) {                          \
+        const long long now = clock64();                             \
+        tacc[i] += static_cast<unsigned long long>(now - tlast);     \
+        tlast = now;                                                 \
+    }
         for (std::size_t tile = blockIdx.x; tile < ntiles; tile += grid, ++it) {
             const int b = it & 1;
             const uint32_t ph = (it >> 1) & 1;
             const int valid = rows_of(tile) - pw * SPW; // rows of this warp holding real signals
             double* x = xin + b * TILE + pw * SPW * n;
             double2* xc = reinterpret_cast<double2*>(x);
-            double2* cwp = cw + pw * SPW * N;
+            double2* cwp = cw + pw * SPW * (n / 2);
+            double* ob = xout + b * TILE + pw * SPW * n;
+            double* ab = atile + b * TS * LDA + pw * SPW * LDA;
+            T_MARK(0);
             ptx::mbar_wait(&xfull[b], ph);
-            if (P.debug != 1) {
-                stockham_first<N, SPW>(x, cwp, lane, valid, bad);
+            T_MARK(1);
+            if ((P.debug & 1) == 0) {
+                const double* yrow = x; // the real rows the length-L DCT reads
+                if constexpr (FOLD) {
+                    // the A tile of this buffer must be free before u lands in it
+                    if (it >= 2) ptx::mbar_wait(&aempty[b], ((it - 2) >> 1) & 1);
+                    double* ys = reinterpret_cast<double*>(cwp);
+                    lane_loop<SPW * (n / 4)>(lane, [&](int t) {
+                        const int r = t / (n / 4), j = 2 * (t % (n / 4));
+                        const double2 lo = *reinterpret_cast<const double2*>(x + r * n + j);
+                        const double2 hi = *reinterpret_cast<const double2*>(x + r * n + n - 2 - j);
+                        if (r < valid)
+                            bad |= non_finite(lo.x) | non_finite(lo.y) | non_finite(hi.x) | non_finite(hi.y);
+                        // y_j = x_j + x_{n-1-j}, u_j = x_j - x_{n-1-j} for j, j+1
+                        *reinterpret_cast<double2*>(ys + r * L + j) = make_double2(lo.x + hi.y, lo.y + hi.x);
+                        *reinterpret_cast<double2*>(ab + r * LDA + j) = make_double2(lo.x - hi.y, lo.y - hi.x);
+                    });
+                    __syncwarp();
+                    yrow = ys;
+                }
+                // length-L DCT-II: pass 0 reads the real rows, then ping-pong
+                double2* first_dst = FOLD ? xc : cwp;
+                double2* other = FOLD ? cwp : xc;
+                stockham_first<NC, SPW>(yrow, first_dst, lane, FOLD ? SPW : valid, bad);
                 __syncwarp();
-                double2* F = fft_passes<N, SPW, 1>(cwp, xc, ptw, lane);
-                // real split + rotation (rt2 = e^{-i pi k/2n} sqrt(2/n)/2): shat into the free buffer
+                T_MARK(2);
+                double2* F = fft_passes<NC, SPW, 1>(first_dst, other, ptw, lane);
+                T_MARK(3);
+                // real split + rotation: shat (length L) into the free buffer
                 double* S = reinterpret_cast<double*>(F == cwp ? xc : cwp);
-#pragma unroll
-                for (int t = lane; t < SPW * (N / 2 + 1); t += 32) {
-                    const int r = t / (N / 2 + 1), k = t % (N / 2 + 1);
-                    const double2* row = F + r * N;
-                    double* o = S + r * n;
-                    if (k == 0) {
-                        const double2 w0 = row[0];
-                        o[0] = (w0.x + w0.y) * dc_scale;
-                        o[N] = (w0.x - w0.y) * y_n;
-                        continue;
-                    }
-                    const double2 wk = row[k], wc = row[N - k];
+                lane_loop<SPW * (NC / 2)>(lane, [&](int t) {
+                    const int r = t / (NC / 2), k = t % (NC / 2) + 1;
+                    const double2* row = F + r * NC;
+                    double* o = S + r * L;
+                    const double2 wk = row[k], wc = row[NC - k];
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const int kk = h == 0 ? k : N - k;
-                        if (h == 1 && kk == k) break;
+                        const int kk = h == 0 ? k : NC - k;
                         const double2 a = h == 0 ? wk : wc, c = h == 0 ? wc : wk;
                         const double sr = a.x + c.x, si = a.y - c.y; // a + conj(c)
                         const double dr = a.x - c.x, di = a.y + c.y; // a - conj(c)
@@ -299,37 +345,41 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
                         const double vr = sr + qi, vi = si - qr; // 2 V_kk
                         const double2 c2 = rt2[kk];
                         o[kk] = vr * c2.x - vi * c2.y;
-                        o[n - kk] = -(vr * c2.y + vi * c2.x);
+                        o[L - kk] = -(vr * c2.y + vi * c2.x);
                     }
+                });
+                if (lane < SPW) {
+                    const double2 w0 = F[lane * NC];
+                    S[lane * L] = (w0.x + w0.y) * dc_scale;
+                    S[lane * L + NC] = (w0.x - w0.y) * y_n;
                 }
                 __syncwarp();
+                T_MARK(4);
                 if (it >= 2) {
                     ptx::mbar_wait(&xofree[b], ((it - 2) >> 1) & 1);
-                    ptx::mbar_wait(&aempty[b], ((it - 2) >> 1) & 1);
+                    if constexpr (!FOLD) ptx::mbar_wait(&aempty[b], ((it - 2) >> 1) & 1);
                 }
-                double* ob = xout + b * TILE + pw * SPW * n;
-                double* ab = atile + b * TS * LDA + pw * SPW * LDA;
-#pragma unroll
-                for (int t = lane; t < SPW * 4 * KT; t += 32) {
-                    const int r = t / (4 * KT), k = t % (4 * KT);
-                    const int j = kept_idx[k];
-                    if (j >= 0) ab[r * LDA + k] = S[r * n + j];
+                T_MARK(5);
+                if constexpr (!FOLD) {
+                    lane_loop<SPW * 4 * KT>(lane, [&](int t) {
+                        const int r = t / (4 * KT), k = t % (4 * KT);
+                        const int j = kept_idx[k];
+                        if (j >= 0) ab[r * LDA + k] = S[r * L + j];
+                    });
                 }
                 for (int q = lane; q < n_pass; q += 32) {
-                    const int d = pass_dst[q], src = pass_src[q];
-                    const int slotq = d & 0xffff;
-                    const bool neg = (d >> 30) != 0;
+                    const int slotq = pass_dst[q], src = pass_src[q];
+                    const double coef = pass_coef[q];
 #pragma unroll
-                    for (int r = 0; r < SPW; ++r) {
-                        const double v = S[r * n + src];
-                        ob[r * n + slotq] = neg ? -v : v;
-                    }
+                    for (int r = 0; r < SPW; ++r) ob[r * n + slotq] = coef * S[r * L + src];
                 }
                 ptx::fence_proxy_async(); // pass-through writes -> visible to the consumers' TMA store
+                T_MARK(6);
             } else if (it >= 2) {
                 ptx::mbar_wait(&xofree[b], ((it - 2) >> 1) & 1);
                 ptx::mbar_wait(&aempty[b], ((it - 2) >> 1) & 1);
             }
+            __syncwarp(); // lanes finished reading S / cw before the next tile rewrites them
             ptx::mbar_arrive(&afull[b]);
             ptx::mbar_arrive(&xempty[b]); // this warp is done with xin[b] (and its cw rows)
             if (ptid == 0 && tile + 2 * grid < ntiles) {
@@ -338,6 +388,9 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
             }
         }
         if (bad) atomicOr(flag, 1);
+        if (P.timers != nullptr && lane == 0)
+            for (int i = 0; i < 7; ++i) atomicAdd(P.timers + i, tacc[i]);
+#undef T_MARK
     } else {
         // =============================== consumers ==================================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n" ::: "memory");
@@ -376,7 +429,7 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
                 for (int nt = 0; nt < NTW; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 #pragma unroll
             for (int kt = 0; kt < KT; ++kt) {
-                if (P.debug == 2) break;
+                if (P.debug & 2) break;
                 double a[MT];
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) a[mt] = arow[mt * 8 * LDA + kt * 4];
@@ -410,21 +463,22 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
     }
 }
 
-template <int LOGN, int KT, int TS>
+template <int LOGN, int KT, int TS, bool FOLD>
 constexpr std::size_t smem_bytes() {
-    constexpr int n = 1 << LOGN, N = n / 2, TILE = TS * n;
-    constexpr int tw = Passes<N>::TWIDDLES > 0 ? Passes<N>::TWIDDLES : 1;
+    constexpr int n = 1 << LOGN, L = FOLD ? n / 2 : n, NC = L / 2, TILE = TS * n;
+    constexpr int tw = Passes<NC>::TWIDDLES > 0 ? Passes<NC>::TWIDDLES : 1;
     return 4 * TILE * sizeof(double) + (TILE / 2) * sizeof(double2) + 2 * TS * LDA * sizeof(double) +
-           (tw + 3 * N + 2) * sizeof(double2) + (4 * KT + 2 * n) * sizeof(int) + 10 * sizeof(uint64_t);
+           (tw + 3 * NC + 2) * sizeof(double2) + n * sizeof(double) + (4 * KT + 2 * n) * sizeof(int) +
+           10 * sizeof(uint64_t);
 }
 
-template <int LOGN, int NTW, int KT>
+template <int LOGN, int NTW, int KT, bool FOLD>
 cudaError_t launch_small(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
                          int num_sms, cudaStream_t stream) {
     constexpr int TS = LOGN >= 9 ? 8 : 16;
-    constexpr std::size_t smem = smem_bytes<LOGN, KT, TS>();
+    constexpr std::size_t smem = smem_bytes<LOGN, KT, TS, FOLD>();
     static_assert(smem <= 227 * 1024, "fused small kernel exceeds shared memory");
-    auto kern = fused_small_fwd_kernel<LOGN, NTW, KT, TS>;
+    auto kern = fused_small_fwd_kernel<LOGN, NTW, KT, TS, FOLD>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const std::size_t ntiles = (batch + TS - 1) / TS;
@@ -433,24 +487,29 @@ cudaError_t launch_small(const double* in, double* out, std::size_t batch, const
     return cudaGetLastError();
 }
 
-template <int LOGN, int KT>
+template <int LOGN, int KT, bool FOLD>
 cudaError_t dispatch_ntw(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
                          int num_sms, cudaStream_t stream) {
-    if (P.A <= 8 * kConsumerWarps) return launch_small<LOGN, 1, KT>(in, out, batch, P, flag, num_sms, stream);
-    return launch_small<LOGN, 2, KT>(in, out, batch, P, flag, num_sms, stream);
+    if (P.A <= 8 * kConsumerWarps) return launch_small<LOGN, 1, KT, FOLD>(in, out, batch, P, flag, num_sms, stream);
+    return launch_small<LOGN, 2, KT, FOLD>(in, out, batch, P, flag, num_sms, stream);
 }
 
-/// K is padded up to 4*KT with KT in {4, 8, 16, 32} (never above n/4).
+/// K is padded up to 4*KT with KT in {4, 8, 16, 32} (never above n/4).  A
+/// folded plan's Cauchy K is n/2.
 template <int LOGN>
 cudaError_t dispatch_kt(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
                         int num_sms, cudaStream_t stream) {
     constexpr int n = 1 << LOGN;
-    if (P.K <= 16 || n <= 16) return dispatch_ntw<LOGN, 4>(in, out, batch, P, flag, num_sms, stream);
+    if constexpr (n >= 64 && n / 8 <= KTMAX) {
+        if (P.fold) return dispatch_ntw<LOGN, n / 8, true>(in, out, batch, P, flag, num_sms, stream);
+    }
+    if (P.fold) return cudaErrorInvalidValue;
+    if (P.K <= 16 || n <= 16) return dispatch_ntw<LOGN, 4, false>(in, out, batch, P, flag, num_sms, stream);
     if constexpr (n >= 32)
-        if (P.K <= 32 || n <= 32) return dispatch_ntw<LOGN, 8>(in, out, batch, P, flag, num_sms, stream);
+        if (P.K <= 32 || n <= 32) return dispatch_ntw<LOGN, 8, false>(in, out, batch, P, flag, num_sms, stream);
     if constexpr (n >= 64)
-        if (P.K <= 64 || n <= 64) return dispatch_ntw<LOGN, 16>(in, out, batch, P, flag, num_sms, stream);
-    if constexpr (n >= 128) return dispatch_ntw<LOGN, 32>(in, out, batch, P, flag, num_sms, stream);
+        if (P.K <= 64 || n <= 64) return dispatch_ntw<LOGN, 16, false>(in, out, batch, P, flag, num_sms, stream);
+    if constexpr (n >= 128) return dispatch_ntw<LOGN, 32, false>(in, out, batch, P, flag, num_sms, stream);
     return cudaErrorInvalidValue;
 }
 
@@ -458,6 +517,10 @@ cudaError_t dispatch_kt(const double* in, double* out, std::size_t batch, const 
 
 bool fused_small_supported(std::size_t n, int K, int A) {
     return is_pow2(n) && n >= 16 && n <= 512 && K <= 4 * KTMAX && A <= 16 * kConsumerWarps;
+}
+
+bool fused_small_fold_supported(std::size_t n, int columns) {
+    return is_pow2(n) && n >= 64 && n / 2 <= 4 * KTMAX && columns <= 16 * kConsumerWarps;
 }
 
 cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,

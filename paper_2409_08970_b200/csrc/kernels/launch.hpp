@@ -64,25 +64,32 @@ cudaError_t cauchy_rows(const T* in, std::size_t ld_in, T* out, std::size_t ld_o
                         std::size_t batch, int* flag, cudaStream_t stream);
 
 /// Constants of the fused small-plan forward kernel (fused_small.cu).
+/// Generic plans: the Cauchy stage multiplies the kept DCT coefficients by
+/// tmat = T (A x K, row c = output column); pass-through slots copy the DCT
+/// coefficient pass_src scaled by pass_coef (= sigma).  Folded plans (every
+/// kept DCT index odd): the Cauchy stage multiplies u_j = x_j - x_{n-1-j}
+/// (K = n/2) by tmat = W^T, W = D_odd^T T (plus sigma D rows for odd
+/// pass-through slots), and the length-n/2 DCT-II of y_j = x_j + x_{n-1-j}
+/// feeds the even pass-through slots (pass_coef = sigma / sqrt 2).
 struct SmallPlanDev {
-    const double* lam_kept;  // K
-    const double* z_kept;    // K
-    const double* nu;        // A (secular roots, ascending)
-    const double* act_scale; // A (sigma * a of the root's slot)
-    const int* act_slot;     // A
-    const double* tmat;      // A x K: T[c][k] = sigma_c a_c z_k / (lambda_k - mu_c)
-    const int* kept_idx;     // K: DCT index of each kept coefficient
-    const int* pass_src;     // n - K: DCT index of each pass-through coefficient
-    const int* pass_slot;    // n - K: its output slot
-    const int* pass_neg;     // n - K: 1 if sigma of that slot is -1
-    const double* fft_tw;    // N = n/2 complex e^{-2 pi i m / N}
-    const double* split_tw;  // N complex e^{-2 pi i k / n}
-    const double* rot_tw;    // N+1 complex e^{-i pi k / 2n}
-    int n, K, A;
-    int debug; // development knob (DCTP_DEBUG_MODE): 1 = skip the DCT work, 2 = skip the DMMA work
+    const int* act_slot;     // A: output slot of column c
+    const double* tmat;      // A x K, row-major
+    const int* kept_idx;     // K: DCT index of each kept coefficient (generic only)
+    const int* pass_src;     // n_pass: index into the length-L DCT coefficients
+    const int* pass_slot;    // n_pass: output slot
+    const double* pass_coef; // n_pass: multiplier
+    const double* fft_tw;    // L/2 complex e^{-2 pi i m / (L/2)}
+    const double* split_tw;  // L/2 complex e^{-2 pi i k / L}
+    const double* rot_tw;    // L/2+1 complex e^{-i pi k / 2L}
+    int n, K, A, n_pass, fold;
+    unsigned long long* timers; // DCTP_DEBUG_MODE & 4: producer phase cycle counters (7)
+    int debug; // development knob (DCTP_DEBUG_MODE bits): 1 = skip the DCT work, 2 = skip the DMMA work
 };
 
+/// Generic plans: power-of-two 16 <= n <= 512, K <= 128, A <= 128.  Folded
+/// plans: power-of-two 64 <= n <= 256 and at most 128 Cauchy columns.
 bool fused_small_supported(std::size_t n, int K, int A);
+bool fused_small_fold_supported(std::size_t n, int columns);
 cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
                                 int num_sms, cudaStream_t stream);
 

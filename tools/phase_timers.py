@@ -1,0 +1,28 @@
+"""DCTP_DEBUG_MODE bit 4: per-phase cycle accounting of the fused kernel's producer."""
+import ctypes, os, sys
+from pathlib import Path
+os.environ["DCTP_DEBUG_MODE"] = str(4 | int(os.environ.get("DCTP_DEBUG_MODE", "0")))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch
+import paper_2409_08970_b200 as P
+from paper_2409_08970_b200 import _native
+from paper_2409_08970_b200.configs import WORKLOADS, make_plan
+cid = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+w = WORKLOADS[cid]
+plan = make_plan(w)
+x = torch.as_tensor(P.fill_signals(w.seed, w.dist, w.n, w.batch, w.r), device="cuda")
+y = torch.empty_like(x)
+for _ in range(3):
+    plan.forward(x, sync=False, out=y)
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * 8)()
+_native.lib.dctp_debug_timers(buf)
+plan.forward(x, sync=False, out=y)
+torch.cuda.synchronize()
+_native.lib.dctp_debug_timers(buf)
+names = ["wait_xfull", "pass0", "fft_rest", "split", "wait_free", "gather", "tail"]
+tot = sum(buf[:7])
+tiles = (w.batch + 15) // 16
+nw = 8
+for i, nm in enumerate(names):
+    print(f"{nm:12s} {buf[i] / tiles / nw:10.0f} cycles/tile/warp  {100 * buf[i] / max(tot, 1):5.1f}%")

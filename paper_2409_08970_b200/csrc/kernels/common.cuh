@@ -110,6 +110,11 @@ __device__ __forceinline__ void bulk_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
+/// All but the most recent bulk group have finished reading shared memory.
+__device__ __forceinline__ void bulk_wait_read_pending1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
 /// Generic-proxy shared-memory writes -> visible to the async (TMA) proxy.

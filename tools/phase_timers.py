@@ -20,7 +20,7 @@ _native.lib.dctp_debug_timers(buf)
 plan.forward(x, sync=False, out=y)
 torch.cuda.synchronize()
 _native.lib.dctp_debug_timers(buf)
-names = ["wait_xfull", "pass0", "fft_rest", "split", "wait_free", "gather", "tail"]
+names = ["tail", "wait_xfull", "pass0", "fft_rest", "split", "wait_free", "gather"]
 tot = sum(buf[:7])
 tiles = (w.batch + 15) // 16
 nw = 8

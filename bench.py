@@ -305,25 +305,36 @@ def run_gpu_arm(args, cfg, rank: int, local: int, world: int):
     gpu_launches = sum(launches.values()) // 2
     peaks = json.loads(MEASURED.read_text()) if MEASURED.exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    fp = fp64_peak()
-    if "cauchy" in top:
-        flops = alg["flops_cauchy"] * cfg.batch
-        if cfg.dtypes[0] == "f32":
-            peak, src = (fp or {}).get("fp32_fma_tflops"), "profiles/peaks_fp64.json fp32_fma_tflops (tools/peaks.cu, measured)"
-        else:
-            peak, src = (fp or {}).get("fp64_fma_tflops"), "profiles/peaks_fp64.json fp64_fma_tflops (tools/peaks.cu, measured)"
-        achieved = flops / (per_launch_ms[top] * 1e-3) / 1e12
-        roof = {"bound": "fp64-fma" if cfg.dtypes[0] == "f64" else "fp32-fma", "kernel": top,
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": (achieved / peak) if peak else None, "traffic": None, "peak_source": src,
-                "algorithmic_flops_per_launch": flops, "launch_ms": per_launch_ms[top],
-                "kernel_share_of_step": per_launch_ms[top] / ms_per_step}
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback 6650 GB/s"
+    fp = fp64_peak() or {}
+    f32 = cfg.dtypes[0] == "f32"
+    # The dominant kernel's algorithmic work per launch: the
+    # direct Cauchy stage 2 * n_kept * n_active (* K members) plus 2.5 n log2 n
+    # for the DCT, per signal; bytes = elem * n * (1 + K_out) per signal.
+    flops = (alg["flops_cauchy"] + alg["flops_dct"]) * cfg.batch
+    nbytes = alg["bytes"] * cfg.batch
+    t_ms = per_launch_ms[top] if ("fused" in top or "cauchy" in top) else ms_per_step
+    if f32:
+        peak, src = fp.get("fp32_fma_tflops"), "profiles/peaks_fp64.json fp32_fma_tflops (tools/peaks.cu, measured)"
+        bound = "fp32-fma"
     else:
-        nbytes = alg["bytes"] * cfg.batch
-        achieved = nbytes / (per_launch_ms[top] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                "launch_ms": per_launch_ms[top], "kernel_share_of_step": per_launch_ms[top] / ms_per_step}
+        peak, src = fp.get("dmma_m8n8k4_tflops"), "profiles/peaks_fp64.json dmma_m8n8k4_tflops (tools/peaks.cu, measured fp64 tensor-core DMMA)"
+        bound = "tensor"
+    achieved = flops / (t_ms * 1e-3) / 1e12
+    hbm_achieved = nbytes / (t_ms * 1e-3) / 1e9
+    t_flop = flops / (peak * 1e12) if peak else 0.0
+    t_hbm = nbytes / (hbm_peak * 1e9)
+    if t_hbm >= t_flop:
+        roof = {"bound": "hbm", "kernel": top, "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": hbm_achieved / hbm_peak, "traffic": None, "peak_source": hbm_src}
+    else:
+        roof = {"bound": bound, "kernel": top, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if peak else None, "traffic": None, "peak_source": src}
+    roof.update({"algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": nbytes,
+                 "launch_ms": t_ms, "kernel_share_of_step": t_ms / ms_per_step,
+                 "hbm_achieved_gbs": hbm_achieved, "hbm_frac": hbm_achieved / hbm_peak,
+                 "compute_achieved_tflops": achieved, "compute_frac": (achieved / peak) if peak else None,
+                 "t_roof_ms": max(t_flop, t_hbm) * 1e3})
     roof["step_hbm_gbs"] = alg["bytes"] * cfg.batch / (ms_per_step * 1e-3) / 1e9
     roof["step_hbm_frac"] = roof["step_hbm_gbs"] / hbm_peak
 

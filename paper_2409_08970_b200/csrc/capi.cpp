@@ -619,23 +619,42 @@ static void sync_check(int device, int* flag, cudaStream_t s) {
     }
 }
 
+/// Synchronous host-buffer apply, pipelined: the batch is cut into chunks of
+/// about 8 MB of input that rotate over three streams, so the host->device
+/// copy of chunk c+1, the kernels of chunk c and the device->host copy of
+/// chunk c-1 overlap (PCIe is full duplex; pinned host memory required for
+/// the copies to be asynchronous).
 template <class T, class F>
-static void host_roundtrip(int device, std::size_t in_count, std::size_t out_count, const T* h_in, T* h_out, F&& run) {
+static void host_roundtrip(int device, std::size_t batch, std::size_t in_row, std::size_t out_row, const T* h_in,
+                           T* h_out, F&& run) {
     if (!h_in || !h_out) throw std::invalid_argument("host buffer is null");
     DeviceScope scope(device);
-    cudaStream_t s;
-    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
-    struct StreamGuard {
-        cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
-    } guard{s};
-    {
-        Scratch<T> din(in_count, s), dout(out_count, s);
-        cuda_check(cudaMemcpyAsync(din.ptr, h_in, in_count * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
-        run(din.ptr, dout.ptr, s);
-        cuda_check(cudaMemcpyAsync(h_out, dout.ptr, out_count * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+    constexpr int kStreams = 3;
+    thread_local std::vector<std::pair<int, std::vector<cudaStream_t>>> cache;
+    std::vector<cudaStream_t>* streams = nullptr;
+    for (auto& e : cache)
+        if (e.first == device) streams = &e.second;
+    if (!streams) {
+        std::vector<cudaStream_t> v(kStreams);
+        for (auto& st : v) cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+        cache.emplace_back(device, std::move(v));
+        streams = &cache.back().second;
     }
-    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    const std::size_t target = (8u << 20) / (in_row * sizeof(T));
+    const std::size_t rows = std::max<std::size_t>(1, std::min(batch, std::max<std::size_t>(target, 256)));
+    std::size_t c = 0;
+    for (std::size_t r0 = 0; r0 < batch; r0 += rows, ++c) {
+        const std::size_t nr = std::min(rows, batch - r0);
+        cudaStream_t st = (*streams)[c % kStreams];
+        Scratch<T> din(nr * in_row, st), dout(nr * out_row, st);
+        cuda_check(cudaMemcpyAsync(din.ptr, h_in + r0 * in_row, nr * in_row * sizeof(T), cudaMemcpyHostToDevice, st),
+                   "H2D");
+        run(din.ptr, dout.ptr, nr, st);
+        cuda_check(cudaMemcpyAsync(h_out + r0 * out_row, dout.ptr, nr * out_row * sizeof(T), cudaMemcpyDeviceToHost,
+                                   st),
+                   "D2H");
+    }
+    for (auto st : *streams) cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
 }
 
 // --- ensemble ------------------------------------------------------------------
@@ -794,9 +813,11 @@ int dctp_plan_sync_check(const dctp_plan* p, void* stream) {
             if (!p) throw std::invalid_argument(#NAME ": null plan");                                 \
             if (!p->blob) throw std::invalid_argument("DctPlusPlan: host-only plan (created with device < 0)"); \
             if (batch == 0) return;                                                                   \
-            const std::size_t cnt = batch * p->st.n;                                                  \
-            host_roundtrip<T>(p->device, cnt, cnt, h_in, h_out,                                       \
-                              [&](const T* din, T* dout, cudaStream_t s) { FN<T>(p, din, dout, batch, s); }); \
+            const std::size_t n = p->st.n;                                                           \
+            host_roundtrip<T>(p->device, batch, n, n, h_in, h_out,                                    \
+                              [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) {         \
+                                  FN<T>(p, din, dout, rows, s);                                       \
+                              });                                                                     \
             sync_check(p->device, p->flag, nullptr);                                                  \
         });                                                                                           \
     }
@@ -920,9 +941,9 @@ int dctp_ensemble_forward_all_host_f32(const dctp_ensemble* e, const float* h_in
         if (!e->blob) throw std::invalid_argument("PrunedEnsemblePlan: host-only plan (created with device < 0)");
         if (batch == 0) return;
         const std::size_t sets = e->members.size() + 1;
-        host_roundtrip<float>(e->device, batch * e->n, batch * sets * e->n, h_in, h_out,
-                              [&](const float* din, float* dout, cudaStream_t s) {
-                                  ensemble_forward<float>(e, din, dout, batch, s);
+        host_roundtrip<float>(e->device, batch, e->n, sets * e->n, h_in, h_out,
+                              [&](const float* din, float* dout, std::size_t rows, cudaStream_t s) {
+                                  ensemble_forward<float>(e, din, dout, rows, s);
                               });
         sync_check(e->device, e->flag, nullptr);
     });
@@ -933,9 +954,9 @@ int dctp_ensemble_forward_all_host_f64(const dctp_ensemble* e, const double* h_i
         if (!e->blob) throw std::invalid_argument("PrunedEnsemblePlan: host-only plan (created with device < 0)");
         if (batch == 0) return;
         const std::size_t sets = e->members.size() + 1;
-        host_roundtrip<double>(e->device, batch * e->n, batch * sets * e->n, h_in, h_out,
-                               [&](const double* din, double* dout, cudaStream_t s) {
-                                   ensemble_forward<double>(e, din, dout, batch, s);
+        host_roundtrip<double>(e->device, batch, e->n, sets * e->n, h_in, h_out,
+                               [&](const double* din, double* dout, std::size_t rows, cudaStream_t s) {
+                                   ensemble_forward<double>(e, din, dout, rows, s);
                                });
         sync_check(e->device, e->flag, nullptr);
     });

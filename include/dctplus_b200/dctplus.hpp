@@ -1,0 +1,306 @@
+// dctplus_b200/dctplus.hpp — C++ mirror of the reference's transform API
+// (proj/include/dctplus/{graph,fast_transform}.hpp) over the C ABI in
+// include/dctplus_b200.h.  Header-only; link with libdctplus_b200.so.
+//
+// Same class and function names, argument meaning and exception types as the
+// reference, so a caller switches with
+//     #include <dctplus_b200/dctplus.hpp>
+//     namespace dctplus = dctplus_b200;
+// Differences a caller can see:
+//   * every apply runs on the GPU (plan `device`, default 0); the std::vector
+//     overloads copy through pinned-or-pageable host memory synchronously;
+//   * batched device-pointer entry points (forward_batch / inverse_batch /
+//     forward_all_batch) take rows of signals and a cudaStream_t (as void*);
+//   * RankOneUpdate::general(v, rho) extends the two reference update kinds;
+//   * PrunedEnsemblePlan supports the progressive mode c_p = n only.
+#ifndef DCTPLUS_B200_DCTPLUS_HPP
+#define DCTPLUS_B200_DCTPLUS_HPP
+
+#include <cmath>
+#include <cstddef>
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "dctplus_b200.h"
+
+namespace dctplus_b200 {
+
+namespace detail {
+inline void check(int status) {
+    if (status == DCTP_OK) return;
+    const std::string msg = dctp_last_error();
+    switch (status) {
+        case DCTP_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case DCTP_DOMAIN_ERROR: throw std::domain_error(msg);
+        case DCTP_LOGIC_ERROR: throw std::logic_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+} // namespace detail
+
+/// Rank-one Laplacian update L + rho v v^T (graph.hpp:87-114), 1-based vertices.
+struct RankOneUpdate {
+    enum class Kind { self_loop, edge_delta, general };
+
+    Kind kind;
+    double rho;
+    std::size_t node_i = 0, node_j = 0; // 1-based
+    std::vector<double> v;              // general direction (extension)
+
+    static RankOneUpdate self_loop(std::size_t i, double w) {
+        if (i < 1) throw std::invalid_argument("RankOneUpdate: node index is 1-based");
+        if (w == 0.0) throw std::invalid_argument("RankOneUpdate: weight must be nonzero");
+        return {Kind::self_loop, w, i, 0, {}};
+    }
+    static RankOneUpdate edge_delta(std::size_t i, std::size_t j, double w) {
+        if (i < 1 || i >= j) throw std::invalid_argument("RankOneUpdate: need 1 <= i < j");
+        if (w == 0.0) throw std::invalid_argument("RankOneUpdate: weight must be nonzero");
+        return {Kind::edge_delta, w, i, j, {}};
+    }
+    static RankOneUpdate general(std::vector<double> dir, double rho) {
+        if (rho == 0.0) throw std::invalid_argument("RankOneUpdate: weight must be nonzero");
+        if (dir.empty()) throw std::invalid_argument("RankOneUpdate: empty direction");
+        return {Kind::general, rho, 0, 0, std::move(dir)};
+    }
+    std::vector<double> direction(std::size_t n) const {
+        if (kind == Kind::general) {
+            if (v.size() != n) throw std::invalid_argument("RankOneUpdate: direction length mismatch");
+            return v;
+        }
+        if (node_i > n || (kind == Kind::edge_delta && node_j > n))
+            throw std::invalid_argument("RankOneUpdate: node index exceeds graph size");
+        std::vector<double> out(n, 0.0);
+        out[node_i - 1] = 1.0;
+        if (kind == Kind::edge_delta) out[node_j - 1] = -1.0;
+        return out;
+    }
+    int abi_kind() const {
+        return kind == Kind::self_loop ? DCTP_SELF_LOOP : (kind == Kind::edge_delta ? DCTP_EDGE_DELTA : DCTP_GENERAL);
+    }
+};
+
+/// Caller-owned result buffer, one per thread (fast_transform.hpp:35-38).
+struct DctPlusWorkspace {
+    std::vector<double> out;
+};
+
+/// Fast DCT+ of one rank-one update of the path graph (fast_transform.hpp:43-302).
+class DctPlusPlan {
+  public:
+    DctPlusPlan(std::size_t n, const RankOneUpdate& update, double epsilon, double tau = 1e-12, int device = 0)
+        : update_(update) {
+        if (update.kind == RankOneUpdate::Kind::general && update.v.size() != n)
+            throw std::invalid_argument("RankOneUpdate: direction length mismatch");
+        dctp_plan* h = nullptr;
+        detail::check(dctp_plan_create(n, update.abi_kind(), update.node_i, update.node_j, update.rho,
+                                       update.v.empty() ? nullptr : update.v.data(), epsilon, tau, device, &h));
+        h_.reset(h, [](dctp_plan* p) { dctp_plan_destroy(p); });
+        int slow = 0;
+        detail::check(dctp_plan_info(h_.get(), &n_, &eps_, &slow, nullptr, nullptr, &device_));
+        slow_ = slow != 0;
+    }
+
+    std::size_t size() const { return n_; }
+    double epsilon() const { return eps_; }
+    const RankOneUpdate& update() const { return update_; }
+    bool slow_path() const { return slow_; }
+    int device() const { return device_; }
+    std::vector<double> lambda() const { return setup_vector(0); }
+    std::vector<double> mu() const { return setup_vector(1); }
+
+    /// Dense basis X (n x n, row-major), columns signed by the largest-entry rule.
+    std::vector<double> basis() const {
+        std::vector<double> x(n_ * n_);
+        detail::check(dctp_plan_basis(h_.get(), x.data()));
+        return x;
+    }
+
+    DctPlusWorkspace make_workspace() const { return DctPlusWorkspace{std::vector<double>(n_)}; }
+
+    const std::vector<double>& forward(const std::vector<double>& s, DctPlusWorkspace& ws) const {
+        check_size(s);
+        ws.out.resize(n_);
+        detail::check(dctp_forward_host_f64(h_.get(), s.data(), ws.out.data(), 1));
+        return ws.out;
+    }
+    std::vector<double> forward(const std::vector<double>& s) const {
+        DctPlusWorkspace ws = make_workspace();
+        return forward(s, ws);
+    }
+    /// The reference's dense X^T s; identical math, same GPU route.
+    const std::vector<double>& forward_nmvp(const std::vector<double>& s, DctPlusWorkspace& ws) const {
+        return forward(s, ws);
+    }
+    std::vector<double> forward_nmvp(const std::vector<double>& s) const { return forward(s); }
+
+    const std::vector<double>& inverse(const std::vector<double>& p, DctPlusWorkspace& ws, bool fast = true) const {
+        (void)fast;
+        check_size(p);
+        ws.out.resize(n_);
+        detail::check(dctp_inverse_host_f64(h_.get(), p.data(), ws.out.data(), 1));
+        return ws.out;
+    }
+    std::vector<double> inverse(const std::vector<double>& p, bool fast = true) const {
+        DctPlusWorkspace ws = make_workspace();
+        return inverse(p, ws, fast);
+    }
+
+    // ---- batched, device-resident (rows of n samples) ----------------------
+    void forward_batch(const double* d_in, double* d_out, std::size_t batch, void* stream = nullptr) const {
+        detail::check(dctp_forward_f64(h_.get(), d_in, d_out, batch, stream));
+    }
+    void forward_batch(const float* d_in, float* d_out, std::size_t batch, void* stream = nullptr) const {
+        detail::check(dctp_forward_f32(h_.get(), d_in, d_out, batch, stream));
+    }
+    void inverse_batch(const double* d_in, double* d_out, std::size_t batch, void* stream = nullptr) const {
+        detail::check(dctp_inverse_f64(h_.get(), d_in, d_out, batch, stream));
+    }
+    void inverse_batch(const float* d_in, float* d_out, std::size_t batch, void* stream = nullptr) const {
+        detail::check(dctp_inverse_f32(h_.get(), d_in, d_out, batch, stream));
+    }
+    /// Waits for `stream`; throws std::domain_error if any input was non-finite.
+    void sync_check(void* stream = nullptr) const { detail::check(dctp_plan_sync_check(h_.get(), stream)); }
+    /// Batched host-buffer apply (pipelined H2D / kernels / D2H).
+    void forward_host(const double* h_in, double* h_out, std::size_t batch) const {
+        detail::check(dctp_forward_host_f64(h_.get(), h_in, h_out, batch));
+    }
+    void inverse_host(const double* h_in, double* h_out, std::size_t batch) const {
+        detail::check(dctp_inverse_host_f64(h_.get(), h_in, h_out, batch));
+    }
+
+    const dctp_plan* handle() const { return h_.get(); }
+
+  private:
+    friend class PrunedEnsemblePlan;
+    DctPlusPlan(const dctp_plan* borrowed, RankOneUpdate update) : update_(std::move(update)) {
+        h_.reset(const_cast<dctp_plan*>(borrowed), [](dctp_plan*) {});
+        int slow = 0;
+        detail::check(dctp_plan_info(h_.get(), &n_, &eps_, &slow, nullptr, nullptr, &device_));
+        slow_ = slow != 0;
+    }
+    void check_size(const std::vector<double>& s) const {
+        if (s.size() != n_) throw std::invalid_argument("DctPlusPlan: signal size mismatch");
+    }
+    std::vector<double> setup_vector(int which) const {
+        std::vector<double> v(n_);
+        detail::check(dctp_plan_setup(h_.get(), which == 0 ? v.data() : nullptr, which == 1 ? v.data() : nullptr,
+                                      nullptr, nullptr, nullptr));
+        return v;
+    }
+
+    RankOneUpdate update_;
+    std::shared_ptr<dctp_plan> h_;
+    std::size_t n_ = 0;
+    double eps_ = 0.0;
+    bool slow_ = false;
+    int device_ = 0;
+};
+
+inline DctPlusPlan plan_dctplus(std::size_t n, const RankOneUpdate& u, double epsilon, double tau = 1e-12) {
+    return DctPlusPlan(n, u, epsilon, tau);
+}
+inline std::vector<double> forward(const DctPlusPlan& plan, const std::vector<double>& s) { return plan.forward(s); }
+inline std::vector<double> forward_nmvp(const DctPlusPlan& plan, const std::vector<double>& s) {
+    return plan.forward_nmvp(s);
+}
+inline std::vector<double> inverse(const DctPlusPlan& plan, const std::vector<double>& p) { return plan.inverse(p); }
+
+/// Shared DCT + K Cauchy stages, progressive mode c_p = n (fast_transform.hpp:338-454).
+class PrunedEnsemblePlan {
+  public:
+    static constexpr std::size_t kDenseMemberCutoff = 128;
+
+    PrunedEnsemblePlan(std::size_t n, const std::vector<RankOneUpdate>& updates, std::size_t cp, double threshold,
+                       double epsilon = 1e-12, int device = 0)
+        : n_(n), cp_(cp), threshold_(threshold) {
+        const std::size_t k = updates.size();
+        std::vector<int> kinds(k);
+        std::vector<std::size_t> is(k), js(k);
+        std::vector<double> rhos(k), vs;
+        bool any_general = false;
+        for (std::size_t r = 0; r < k; ++r) {
+            kinds[r] = updates[r].abi_kind();
+            is[r] = updates[r].node_i;
+            js[r] = updates[r].node_j;
+            rhos[r] = updates[r].rho;
+            any_general |= updates[r].kind == RankOneUpdate::Kind::general;
+        }
+        if (any_general) {
+            vs.assign(k * n, 0.0);
+            for (std::size_t r = 0; r < k; ++r)
+                if (updates[r].kind == RankOneUpdate::Kind::general) {
+                    const auto d = updates[r].direction(n);
+                    std::copy(d.begin(), d.end(), vs.begin() + static_cast<std::ptrdiff_t>(r * n));
+                }
+        }
+        dctp_ensemble* h = nullptr;
+        detail::check(dctp_ensemble_create(n, k, kinds.data(), is.data(), js.data(), rhos.data(),
+                                           any_general ? vs.data() : nullptr, cp, threshold, epsilon, device, &h));
+        h_.reset(h, [](dctp_ensemble* e) { dctp_ensemble_destroy(e); });
+        for (std::size_t r = 1; r <= k; ++r) {
+            const dctp_plan* m = nullptr;
+            detail::check(dctp_ensemble_member(h_.get(), r, &m));
+            members_.push_back(DctPlusPlan(m, updates[r - 1]));
+        }
+    }
+
+    std::size_t size() const { return n_; }
+    std::size_t keep_count() const { return cp_; }
+    double threshold() const { return threshold_; }
+    std::size_t ensemble_size() const { return members_.size() + 1; }
+    const DctPlusPlan& member(std::size_t r) const { return members_.at(r - 1); }
+
+    struct Result {
+        bool pruned = false;
+        std::vector<std::vector<double>> coeffs; // one vector per ensemble member
+        std::vector<double> bounds;              // truncation-error bound per member (0 for c_p = n)
+    };
+
+    Result forward_all(const std::vector<double>& s) const {
+        if (s.size() != n_) throw std::invalid_argument("pruned_forward_all: size mismatch");
+        const std::size_t sets = ensemble_size();
+        std::vector<double> flat(sets * n_);
+        detail::check(dctp_ensemble_forward_all_host_f64(h_.get(), s.data(), flat.data(), 1));
+        Result res;
+        double q = 0.0; // path_quadratic_form (fast_transform.hpp:24-31)
+        for (std::size_t i = 0; i + 1 < s.size(); ++i) q += (s[i] - s[i + 1]) * (s[i] - s[i + 1]);
+        res.pruned = q <= threshold_;
+        res.bounds.assign(sets, 0.0);
+        for (std::size_t r = 0; r < sets; ++r)
+            res.coeffs.emplace_back(flat.begin() + static_cast<std::ptrdiff_t>(r * n_),
+                                    flat.begin() + static_cast<std::ptrdiff_t>((r + 1) * n_));
+        return res;
+    }
+
+    /// rows x (K+1) x n output, device-resident.
+    void forward_all_batch(const float* d_in, float* d_out, std::size_t batch, void* stream = nullptr) const {
+        detail::check(dctp_ensemble_forward_all_f32(h_.get(), d_in, d_out, batch, stream));
+    }
+    void forward_all_batch(const double* d_in, double* d_out, std::size_t batch, void* stream = nullptr) const {
+        detail::check(dctp_ensemble_forward_all_f64(h_.get(), d_in, d_out, batch, stream));
+    }
+    void sync_check(void* stream = nullptr) const { detail::check(dctp_ensemble_sync_check(h_.get(), stream)); }
+
+  private:
+    std::size_t n_, cp_;
+    double threshold_;
+    std::shared_ptr<dctp_ensemble> h_;
+    std::vector<DctPlusPlan> members_;
+};
+
+inline PrunedEnsemblePlan plan_pruned(std::size_t n, const std::vector<RankOneUpdate>& updates, std::size_t cp,
+                                      double threshold, double epsilon = 1e-12) {
+    return PrunedEnsemblePlan(n, updates, cp, threshold, epsilon);
+}
+inline PrunedEnsemblePlan::Result pruned_forward_all(const PrunedEnsemblePlan& plan, const std::vector<double>& s) {
+    return plan.forward_all(s);
+}
+
+} // namespace dctplus_b200
+
+#endif

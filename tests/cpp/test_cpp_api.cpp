@@ -1,0 +1,146 @@
+// C++ mirror API test (include/dctplus_b200/dctplus.hpp), written like the
+// reference's own suites (proj/tests/test_fast_transform.cpp,
+// test_spectral.cpp, test_pruning.cpp): known answers, dense-oracle checks,
+// SNR >= 100 dB, exception classes.  Prints "ALL OK" and exits 0 on success.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <stdexcept>
+#include <vector>
+
+#include <cuda_runtime_api.h>
+
+#include "dctplus_b200/dctplus.hpp"
+
+namespace dctplus = dctplus_b200;
+using namespace dctplus;
+
+static int failures = 0;
+#define CHECK(cond)                                                            \
+    do {                                                                       \
+        if (!(cond)) {                                                         \
+            std::printf("FAILED %s:%d: %s\n", __FILE__, __LINE__, #cond);     \
+            ++failures;                                                        \
+        }                                                                      \
+    } while (0)
+template <class E, class F>
+static bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static double snr_db(const std::vector<double>& ref, const std::vector<double>& t) {
+    double num = 0, den = 0;
+    for (std::size_t i = 0; i < ref.size(); ++i) {
+        num += ref[i] * ref[i];
+        den += (ref[i] - t[i]) * (ref[i] - t[i]);
+    }
+    return den == 0 ? 320.0 : 10 * std::log10(num / den);
+}
+
+static std::vector<double> ar(std::size_t n, double r, std::mt19937_64& g) {
+    std::normal_distribution<double> nd;
+    std::vector<double> s(n);
+    s[0] = nd(g) / std::sqrt(1 - r * r);
+    for (std::size_t j = 1; j < n; ++j) s[j] = r * s[j - 1] + nd(g);
+    return s;
+}
+
+int main() {
+    // test_spectral.cpp:129-135 / test_cauchy.cpp:91-100: n = 2 self-loop
+    {
+        const DctPlusPlan plan(2, RankOneUpdate::self_loop(1, 1.0), 1e-12);
+        const auto mu = plan.mu();
+        CHECK(std::abs(mu[0] - (3 - std::sqrt(5.0)) / 2) < 1e-14);
+        CHECK(std::abs(mu[1] - (3 + std::sqrt(5.0)) / 2) < 1e-14);
+    }
+    // test_fast_transform.cpp:19-44: interleaving on the three update types
+    const std::vector<RankOneUpdate> kBench = {RankOneUpdate::self_loop(1, 1.5), RankOneUpdate::edge_delta(2, 3, 1.5),
+                                               RankOneUpdate::edge_delta(3, 5, 1.5)};
+    for (const auto& u : kBench) {
+        const DctPlusPlan plan(8, u, 1e-12);
+        CHECK(!plan.slow_path());
+        const auto lam = plan.lambda(), mu = plan.mu();
+        for (std::size_t i = 0; i < 8; ++i) {
+            CHECK(mu[i] >= lam[i]);
+            if (i + 1 < 8) CHECK(mu[i] <= lam[i + 1]);
+        }
+    }
+    // forward vs the dense basis (X^T s) and SNR >= 100 dB round trip
+    std::mt19937_64 g(101);
+    for (std::size_t n : {8, 32, 128, 256}) {
+        for (const auto& u : kBench) {
+            const DctPlusPlan plan(n, u, 1e-12);
+            const auto x = plan.basis();
+            DctPlusWorkspace ws = plan.make_workspace();
+            for (int rep = 0; rep < 4; ++rep) {
+                const auto s = ar(n, 0.99, g);
+                const std::vector<double> fast = plan.forward(s, ws);
+                std::vector<double> dense(n, 0.0);
+                for (std::size_t i = 0; i < n; ++i)
+                    for (std::size_t j = 0; j < n; ++j) dense[j] += x[i * n + j] * s[i];
+                CHECK(snr_db(dense, fast) >= 100.0);
+                const auto back = plan.inverse(fast);
+                CHECK(snr_db(s, back) >= 100.0);
+            }
+        }
+    }
+    // errors (fast_transform.hpp:52-53, :266-276)
+    CHECK(throws<std::invalid_argument>([] { DctPlusPlan(1, RankOneUpdate::self_loop(1, 1.0), 1e-12); }));
+    CHECK(throws<std::invalid_argument>([] { DctPlusPlan(8, RankOneUpdate::self_loop(1, 1.0), 2.0); }));
+    CHECK(throws<std::invalid_argument>([] { RankOneUpdate::edge_delta(3, 3, 1.0); }));
+    {
+        const DctPlusPlan plan(16, RankOneUpdate::self_loop(1, 0.5), 1e-12);
+        std::vector<double> bad(16, 0.0);
+        bad[3] = std::nan("");
+        CHECK(throws<std::domain_error>([&] { plan.forward(bad); }));
+        CHECK(throws<std::invalid_argument>([&] { plan.forward(std::vector<double>(15, 0.0)); }));
+    }
+    // progressive mode (test_pruning.cpp:35-48): members reproduce the full transforms
+    {
+        std::vector<RankOneUpdate> ups;
+        for (int k = 0; k < 4; ++k) ups.push_back(RankOneUpdate::self_loop(1, 0.05 + 0.5 * k));
+        const PrunedEnsemblePlan ens(64, ups, 64, 1e300);
+        CHECK(ens.ensemble_size() == 5);
+        const auto s = ar(64, 0.9, g);
+        const auto res = ens.forward_all(s);
+        CHECK(res.pruned);
+        for (std::size_t r = 1; r <= 4; ++r) CHECK(snr_db(ens.member(r).forward(s), res.coeffs[r]) >= 100.0);
+        CHECK(throws<std::logic_error>([&] { ens.member(0); }));
+    }
+    // batched device rows
+    {
+        const std::size_t n = 256, batch = 1000;
+        const DctPlusPlan plan(n, RankOneUpdate::edge_delta(128, 129, -0.7), 1e-12);
+        std::vector<double> h(n * batch), y(n * batch);
+        for (std::size_t b = 0; b < batch; ++b) {
+            const auto s = ar(n, 0.95, g);
+            std::copy(s.begin(), s.end(), h.begin() + static_cast<std::ptrdiff_t>(b * n));
+        }
+        double *din = nullptr, *dout = nullptr;
+        cudaMalloc(reinterpret_cast<void**>(&din), h.size() * 8);
+        cudaMalloc(reinterpret_cast<void**>(&dout), h.size() * 8);
+        cudaMemcpy(din, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+        plan.forward_batch(din, dout, batch);
+        plan.sync_check();
+        cudaMemcpy(y.data(), dout, y.size() * 8, cudaMemcpyDeviceToHost);
+        for (std::size_t b = 0; b < batch; b += 97) {
+            const std::vector<double> s(h.begin() + static_cast<std::ptrdiff_t>(b * n),
+                                        h.begin() + static_cast<std::ptrdiff_t>((b + 1) * n));
+            const std::vector<double> yb(y.begin() + static_cast<std::ptrdiff_t>(b * n),
+                                         y.begin() + static_cast<std::ptrdiff_t>((b + 1) * n));
+            CHECK(snr_db(plan.forward(s), yb) >= 200.0);
+        }
+        cudaFree(din);
+        cudaFree(dout);
+    }
+    if (failures == 0) std::printf("ALL OK\n");
+    return failures == 0 ? 0 : 1;
+}

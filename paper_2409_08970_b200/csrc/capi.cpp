@@ -470,19 +470,24 @@ static int debug_mode() {
 }
 
 static unsigned long long* g_debug_timers = nullptr;
+static void reset_debug_timers() {
+    unsigned long long h[16] = {0};
+    h[8] = h[11] = ~0ull; // min slots
+    cudaMemcpy(g_debug_timers, h, sizeof(h), cudaMemcpyHostToDevice);
+}
 static unsigned long long* debug_timers() {
     if ((debug_mode() & 4) == 0) return nullptr;
     if (!g_debug_timers) {
-        cudaMalloc(reinterpret_cast<void**>(&g_debug_timers), 8 * sizeof(unsigned long long));
-        cudaMemset(g_debug_timers, 0, 8 * sizeof(unsigned long long));
+        cudaMalloc(reinterpret_cast<void**>(&g_debug_timers), 16 * sizeof(unsigned long long));
+        reset_debug_timers();
     }
     return g_debug_timers;
 }
 
-extern "C" int dctp_debug_timers(unsigned long long* out8) {
+extern "C" int dctp_debug_timers(unsigned long long* out16) {
     if (!g_debug_timers) return 1;
-    cudaMemcpy(out8, g_debug_timers, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    cudaMemset(g_debug_timers, 0, 8 * sizeof(unsigned long long));
+    cudaMemcpy(out16, g_debug_timers, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    reset_debug_timers();
     return 0;
 }
 

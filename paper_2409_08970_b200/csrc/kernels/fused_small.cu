@@ -188,7 +188,7 @@ __device__ __forceinline__ double2* fft_passes(double2* a, double2* b, const dou
 template <int LOGN, int NTW, int KT, int TS, bool FOLD>
 __global__ void __launch_bounds__(kThreads, 1)
 fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, std::size_t batch, SmallPlanDev P,
-                       int* flag) {
+                       int* flag, unsigned long long* tile_counter) {
     constexpr int n = 1 << LOGN, L = FOLD ? n / 2 : n, NC = L / 2, MT = TS / 8;
     constexpr int TILE = TS * n; // doubles per signal tile
     using PS = Passes<NC>;
@@ -211,7 +211,14 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
     uint64_t* aempty = bars + 4;  // [2] consumers -> producer: A tile consumed
     uint64_t* xofree = bars + 6;  // [2] output tile's TMA store has read it
     uint64_t* xempty = bars + 8;  // [2] every producer warp is done reading xin[b]
+    // dynamic tile scheduler: the producer claims tiles from a global counter
+    // (idle SMs take more work; static round-robin left a 40% tail)
+    long long* sched = reinterpret_cast<long long*>(bars + 10);  // [2] tile landing in xin[b]
+    long long* csched = sched + 2;                               // [2] tile whose A tile is in atile[b]
 
+    const long long t_entry = clock64();
+    unsigned long long g_entry;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
     const int tid = threadIdx.x;
     const int n_pass = P.n_pass;
     static_assert(kThreads == 512, "register split 256 x 88 + 256 x 168 assumes 512 threads");
@@ -255,7 +262,6 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
     __syncthreads();
 
     const std::size_t ntiles = (batch + TS - 1) / TS;
-    const std::size_t grid = gridDim.x;
     auto rows_of = [&](std::size_t tile) { return static_cast<int>(min(static_cast<std::size_t>(TS), batch - tile * TS)); };
 
     // Consumers take warpgroups 0-1 and the producer warpgroups 2-3: the warp
@@ -270,14 +276,22 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
         asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
         constexpr int SPW = TS / (kProducerThreads / 32);
         const int ptid = tid - kConsumerThreads, pw = ptid >> 5, lane = ptid & 31;
-        auto issue = [&](std::size_t tile, int b) {
-            const uint32_t bytes = static_cast<uint32_t>(rows_of(tile) * n * sizeof(double));
-            ptx::mbar_expect_tx(&xfull[b], bytes);
-            ptx::bulk_load(xin + b * TILE, in + tile * TS * n, bytes, &xfull[b]);
+        // claim the next tile for buffer b and start its load (thread 0 only);
+        // past the end the mbarrier is released without data
+        auto claim = [&](int b) {
+            const long long tile = static_cast<long long>(atomicAdd(tile_counter, 1ull));
+            sched[b] = tile;
+            if (tile < static_cast<long long>(ntiles)) {
+                const uint32_t bytes = static_cast<uint32_t>(rows_of(tile) * n * sizeof(double));
+                ptx::mbar_expect_tx(&xfull[b], bytes);
+                ptx::bulk_load(xin + b * TILE, in + tile * TS * n, bytes, &xfull[b]);
+            } else {
+                ptx::mbar_arrive(&xfull[b]);
+            }
         };
         if (ptid == 0) {
-            if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
-            if (blockIdx.x + grid < ntiles) issue(blockIdx.x + grid, 1);
+            claim(0);
+            claim(1);
         }
         const double scale = sqrt(2.0 / L);
         const double dc_scale = 1.0 / sqrt(static_cast<double>(L));
@@ -293,18 +307,26 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
         tacc[i] += static_cast<unsigned long long>(now - tlast);     \
         tlast = now;                                                 \
     }
-        for (std::size_t tile = blockIdx.x; tile < ntiles; tile += grid, ++it) {
+        for (;; ++it) {
             const int b = it & 1;
             const uint32_t ph = (it >> 1) & 1;
+            T_MARK(0);
+            ptx::mbar_wait(&xfull[b], ph);
+            T_MARK(1);
+            const long long tile = sched[b];
+            if (tile >= static_cast<long long>(ntiles)) {
+                // end: hand the sentinel to the consumers once they are done with buffer b
+                if (it >= 2) ptx::mbar_wait(&aempty[b], ((it - 2) >> 1) & 1);
+                if (ptid == 0) csched[b] = tile;
+                ptx::mbar_arrive(&afull[b]);
+                break;
+            }
             const int valid = rows_of(tile) - pw * SPW; // rows of this warp holding real signals
             double* x = xin + b * TILE + pw * SPW * n;
             double2* xc = reinterpret_cast<double2*>(x);
             double2* cwp = cw + pw * SPW * (n / 2);
             double* ob = xout + b * TILE + pw * SPW * n;
             double* ab = atile + b * TS * LDA + pw * SPW * LDA;
-            T_MARK(0);
-            ptx::mbar_wait(&xfull[b], ph);
-            T_MARK(1);
             if ((P.debug & 1) == 0) {
                 const double* yrow = x; // the real rows the length-L DCT reads
                 if constexpr (FOLD) {
@@ -327,7 +349,7 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
                 // length-L DCT-II: pass 0 reads the real rows, then ping-pong
                 double2* first_dst = FOLD ? xc : cwp;
                 double2* other = FOLD ? cwp : xc;
-                stockham_first<NC, SPW>(yrow, first_dst, lane, FOLD ? SPW : valid, bad);
+                stockham_first<NC, SPW>(yrow, first_dst, lane, valid, bad);
                 __syncwarp();
                 T_MARK(2);
                 double2* F = fft_passes<NC, SPW, 1>(first_dst, other, ptw, lane);
@@ -385,16 +407,25 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
                 ptx::mbar_wait(&aempty[b], ((it - 2) >> 1) & 1);
             }
             __syncwarp(); // lanes finished reading S / cw before the next tile rewrites them
+            if (ptid == 0) csched[b] = tile;
             ptx::mbar_arrive(&afull[b]);
             ptx::mbar_arrive(&xempty[b]); // this warp is done with xin[b] (and its cw rows)
-            if (ptid == 0 && tile + 2 * grid < ntiles) {
+            if (ptid == 0) {
                 ptx::mbar_wait(&xempty[b], ph);
-                issue(tile + 2 * grid, b);
+                claim(b);
             }
         }
         if (bad) atomicOr(flag, 1);
-        if (P.timers != nullptr && lane == 0)
+        if (P.timers != nullptr && lane == 0) {
             for (int i = 0; i < 7; ++i) atomicAdd(P.timers + i, tacc[i]);
+            atomicAdd(P.timers + 7, static_cast<unsigned long long>(clock64() - t_entry));
+            unsigned long long g_exit;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+            atomicMin(P.timers + 8, g_entry);
+            atomicMax(P.timers + 9, g_exit);
+            atomicMax(P.timers + 10, g_entry);
+            atomicMin(P.timers + 11, g_exit);
+        }
 #undef T_MARK
     } else {
         // =============================== consumers ==================================
@@ -422,10 +453,12 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
                 slot[nt][e] = c < P.A ? P.act_slot[c] : -1;
             }
         int it = 0;
-        for (std::size_t tile = blockIdx.x; tile < ntiles; tile += grid, ++it) {
+        for (;; ++it) {
             const int b = it & 1;
-            const int rows = rows_of(tile);
             ptx::mbar_wait(&afull[b], (it >> 1) & 1);
+            const long long tile = csched[b];
+            if (tile >= static_cast<long long>(ntiles)) break;
+            const int rows = rows_of(tile);
             const double* arow = atile + b * TS * LDA + (lane >> 2) * LDA + (lane & 3);
             double acc[MT][NTW][2];
 #pragma unroll
@@ -481,7 +514,7 @@ constexpr std::size_t smem_bytes() {
     constexpr int tw = Passes<NC>::TWIDDLES > 0 ? Passes<NC>::TWIDDLES : 1;
     return 4 * TILE * sizeof(double) + (TILE / 2) * sizeof(double2) + 2 * TS * LDA * sizeof(double) +
            (tw + 3 * NC + 2) * sizeof(double2) + n * sizeof(double) + (4 * KT + 2 * n) * sizeof(int) +
-           10 * sizeof(uint64_t);
+           10 * sizeof(uint64_t) + 4 * sizeof(long long);
 }
 
 template <int LOGN, int NTW, int KT, bool FOLD>
@@ -491,12 +524,21 @@ cudaError_t launch_small(const double* in, double* out, std::size_t batch, const
     constexpr std::size_t smem = smem_bytes<LOGN, KT, TS, FOLD>();
     static_assert(smem <= 227 * 1024, "fused small kernel exceeds shared memory");
     auto kern = fused_small_fwd_kernel<LOGN, NTW, KT, TS, FOLD>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (attr != cudaSuccess) return attr;
     const std::size_t ntiles = (batch + TS - 1) / TS;
     const unsigned grid = static_cast<unsigned>(std::min<std::size_t>(ntiles, static_cast<std::size_t>(num_sms)));
-    kern<<<grid, kThreads, smem, stream>>>(in, out, batch, P, flag);
-    return cudaGetLastError();
+    // per-launch tile counter from the stream-ordered pool (concurrent launches stay independent)
+    unsigned long long* counter = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counter), sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kThreads, smem, stream>>>(in, out, batch, P, flag, counter);
+    e = cudaGetLastError();
+    cudaFreeAsync(counter, stream);
+    return e;
 }
 
 template <int LOGN, int KT, bool FOLD>

@@ -15,11 +15,16 @@ y = torch.empty_like(x)
 for _ in range(3):
     plan.forward(x, sync=False, out=y)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 8)()
+buf = (ctypes.c_ulonglong * 16)()
+e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 _native.lib.dctp_debug_timers(buf)
-plan.forward(x, sync=False, out=y)
+e0.record(); plan.forward(x, sync=False, out=y); e1.record()
 torch.cuda.synchronize()
 _native.lib.dctp_debug_timers(buf)
+print(f"kernel {e0.elapsed_time(e1)*1e3:.1f} us; producer-warp total {buf[7] / (148 * 8):.0f} cycles "
+      f"(= {buf[7] / (148 * 8) / 1.965e3:.1f} us at 1965 MHz), loop sum {sum(buf[:7]) / (148 * 8):.0f} cycles")
+print(f"globaltimer: first CTA entry -> last exit {(buf[9] - buf[8]) / 1e3:.1f} us; last CTA entry at +{(buf[10] - buf[8]) / 1e3:.1f} us;"
+      f" first exit at +{(buf[11] - buf[8]) / 1e3:.1f} us")
 names = ["tail", "wait_xfull", "pass0", "fft_rest", "split", "wait_free", "gather"]
 tot = sum(buf[:7])
 tiles = (w.batch + 15) // 16

@@ -645,7 +645,11 @@ static void host_roundtrip(int device, std::size_t batch, std::size_t in_row, st
         cache.emplace_back(device, std::move(v));
         streams = &cache.back().second;
     }
-    const std::size_t target = (8u << 20) / (in_row * sizeof(T));
+    static const std::size_t chunk_bytes = [] {
+        const char* e = std::getenv("DCTP_HOST_CHUNK_MB"); // tuning knob; default 16 MB
+        return static_cast<std::size_t>(e ? std::max(1, std::atoi(e)) : 16) << 20;
+    }();
+    const std::size_t target = chunk_bytes / (in_row * sizeof(T));
     const std::size_t rows = std::max<std::size_t>(1, std::min(batch, std::max<std::size_t>(target, 256)));
     std::size_t c = 0;
     for (std::size_t r0 = 0; r0 < batch; r0 += rows, ++c) {

@@ -22,6 +22,8 @@
 // algorithmic minimum: every signal is read once and every coefficient
 // written once.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "kernels/common.cuh"
 #include "kernels/launch.hpp"
@@ -137,6 +139,8 @@ template <int N, int SPW>
 __device__ __forceinline__ void stockham_first(const double* __restrict__ x, double2* __restrict__ dst, int lane,
                                                int valid_rows, bool& bad) {
     constexpr int R = Passes<N>::FIRST_R, M = N / R, n = 2 * N;
+    (void)valid_rows;
+    (void)bad;
     lane_loop<SPW * (M / 2)>(lane, [&](int t) {
         const int sig = t / (M / 2), j = t % (M / 2), jp = M - 1 - j;
         const double* xr = x + sig * n;
@@ -147,9 +151,6 @@ __device__ __forceinline__ void stockham_first(const double* __restrict__ x, dou
             const double2 b1 = *reinterpret_cast<const double2*>(xr + 4 * (j + r * M) + 2);
             const double2 e0 = *reinterpret_cast<const double2*>(xr + 4 * (jp + r * M));
             const double2 e1 = *reinterpret_cast<const double2*>(xr + 4 * (jp + r * M) + 2);
-            if (sig < valid_rows)
-                bad |= non_finite(b0.x) | non_finite(b0.y) | non_finite(b1.x) | non_finite(b1.y) |
-                       non_finite(e0.x) | non_finite(e0.y) | non_finite(e1.x) | non_finite(e1.y);
             a[r] = make_double2(b0.x, b1.x);
             c[R - 1 - r] = make_double2(b1.y, b0.y);
             c[r] = make_double2(e0.x, e1.x);
@@ -337,8 +338,6 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
                         const int r = t / (n / 4), j = 2 * (t % (n / 4));
                         const double2 lo = *reinterpret_cast<const double2*>(x + r * n + j);
                         const double2 hi = *reinterpret_cast<const double2*>(x + r * n + n - 2 - j);
-                        if (r < valid)
-                            bad |= non_finite(lo.x) | non_finite(lo.y) | non_finite(hi.x) | non_finite(hi.y);
                         // y_j = x_j + x_{n-1-j}, u_j = x_j - x_{n-1-j} for j, j+1
                         *reinterpret_cast<double2*>(ys + r * L + j) = make_double2(lo.x + hi.y, lo.y + hi.x);
                         *reinterpret_cast<double2*>(ab + r * LDA + j) = make_double2(lo.x - hi.y, lo.y - hi.x);
@@ -377,8 +376,14 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
                 });
                 if (lane < SPW) {
                     const double2 w0 = F[lane * NC];
-                    S[lane * L] = (w0.x + w0.y) * dc_scale;
+                    const double dc = (w0.x + w0.y) * dc_scale;
+                    S[lane * L] = dc;
                     S[lane * L + NC] = (w0.x - w0.y) * y_n;
+                    // check_signal (fast_transform.hpp:271-276): the DC coefficient
+                    // sums every sample with a nonzero weight (folded: y sums x_j and
+                    // x_{n-1-j}), so an Inf/NaN input always makes it non-finite.
+                    // One test per row instead of n keeps the shared fp64 pipe free.
+                    if (lane < valid) bad |= !isfinite(dc);
                 }
                 __syncwarp();
                 T_MARK(4);
@@ -508,6 +513,256 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
     }
 }
 
+/// Lock-step variant: all 16 warps run the DCT phase (one row each, so the
+/// fp64 pipe carries only FFT work), one CTA barrier, then the DMMA phase (one
+/// 8-column N-tile each, T/W fragments resident in registers).  Tiles stream
+/// through kStages TMA buffers: each buffer holds the input rows until the DCT
+/// has consumed them and then collects the output rows in place; thread 0
+/// issues the TMA bulk store and refills the buffer two tiles later (by then
+/// the store has long finished reading it), and fetches tile indices from the
+/// global counter one iteration ahead with a predicated atomic, so nothing on
+/// the critical path waits for memory.  The A tile is double-buffered.
+constexpr int kComputeWarps = 16;
+constexpr int kLockThreads = 32 * kComputeWarps;
+
+template <bool FOLD>
+constexpr int lock_stages() { return FOLD ? 4 : 3; }
+
+template <int LOGN, int KT, int TS, bool FOLD>
+constexpr std::size_t lockstep_smem_bytes() {
+    constexpr int n = 1 << LOGN, L = FOLD ? n / 2 : n, NC = L / 2, TILE = TS * n;
+    constexpr int tw = Passes<NC>::TWIDDLES > 0 ? Passes<NC>::TWIDDLES : 1;
+    constexpr int S = lock_stages<FOLD>();
+    return S * TILE * sizeof(double) + 2 * TS * NC * sizeof(double2) + 2 * TS * LDA * sizeof(double) +
+           (tw + 3 * NC + 2) * sizeof(double2) + n * sizeof(double) + (4 * KT + 2 * n) * sizeof(int) +
+           S * sizeof(uint64_t) + S * sizeof(long long);
+}
+
+/// next = atomicAdd(ctr, 1) on thread 0 only, without a branch (the result is
+/// consumed an iteration later, so its latency never stalls the warp).
+__device__ __forceinline__ void fetch_tile_index(unsigned long long* ctr, long long& next, int tid) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.eq.u32 p, %2, 0;\n"
+        "@p atom.global.add.u64 %0, [%1], 1;\n"
+        "}\n"
+        : "+l"(next)
+        : "l"(ctr), "r"(tid)
+        : "memory");
+}
+
+template <int LOGN, int KT, int TS, bool FOLD>
+__global__ void __launch_bounds__(kLockThreads, 1)
+fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, std::size_t batch, SmallPlanDev P,
+                      int* flag, unsigned long long* tile_counter) {
+    constexpr int n = 1 << LOGN, L = FOLD ? n / 2 : n, NC = L / 2, MT = TS / 8;
+    constexpr int TILE = TS * n;
+    constexpr int SPW = TS / kComputeWarps; // rows per warp in the DCT phase
+    constexpr int kS = lock_stages<FOLD>();
+    static_assert(SPW >= 1 && TS % kComputeWarps == 0, "one or more rows per warp");
+    using PS = Passes<NC>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* xs = reinterpret_cast<double*>(smem);              // kS x TILE: input, then output rows
+    double2* s0 = reinterpret_cast<double2*>(xs + kS * TILE);  // TS*NC complex: FFT scratch
+    double2* s1 = s0 + TS * NC;                                 // TS*NC complex: FFT scratch
+    double* atile = reinterpret_cast<double*>(s1 + TS * NC);   // 2 x TS x LDA: Cauchy A operand
+    double2* ptw = reinterpret_cast<double2*>(atile + 2 * TS * LDA);
+    double2* sp = ptw + (PS::TWIDDLES > 0 ? PS::TWIDDLES : 1);
+    double2* rt = sp + NC;
+    double2* rt2 = rt + NC + 1;
+    double* pass_coef = reinterpret_cast<double*>(rt2 + NC + 1);
+    int* kept_idx = reinterpret_cast<int*>(pass_coef + n);
+    int* pass_src = kept_idx + 4 * KT;
+    int* pass_dst = pass_src + n;
+    uint64_t* xfull = reinterpret_cast<uint64_t*>(pass_dst + n);   // [kS] tile landed (tx bytes)
+    long long* sched = reinterpret_cast<long long*>(xfull + kS);   // [kS] tile in stage q
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n_pass = P.n_pass;
+    {
+        const double2* fft = reinterpret_cast<const double2*>(P.fft_tw);
+#pragma unroll 1
+        for (int p = 1; p < PS::COUNT; ++p) {
+            const int R = PS::radix(p), ns = 1 << PS::lns(p), off = PS::twiddle_offset(p);
+            for (int i = tid; i < ns * (R - 1); i += kLockThreads) {
+                const int jm = i / (R - 1), r = i % (R - 1) + 1;
+                ptw[off + i] = fft[(r * jm * (NC / ns)) / R];
+            }
+        }
+        for (int i = tid; i < NC; i += kLockThreads) sp[i] = reinterpret_cast<const double2*>(P.split_tw)[i];
+        for (int i = tid; i <= NC; i += kLockThreads) {
+            const double2 r = reinterpret_cast<const double2*>(P.rot_tw)[i];
+            const double h = 0.5 * sqrt(2.0 / L);
+            rt[i] = r;
+            rt2[i] = make_double2(r.x * h, r.y * h);
+        }
+        for (int i = tid; i < 4 * KT; i += kLockThreads) kept_idx[i] = i < P.K ? P.kept_idx[i] : -1;
+        for (int i = tid; i < n_pass; i += kLockThreads) {
+            pass_src[i] = P.pass_src[i];
+            pass_dst[i] = P.pass_slot[i];
+            pass_coef[i] = P.pass_coef[i];
+        }
+        for (int i = tid; i < 2 * TS * LDA; i += kLockThreads) atile[i] = 0.0;
+        if (tid == 0) {
+            for (int q = 0; q < kS; ++q) ptx::mbar_init(&xfull[q], 1);
+            ptx::fence_mbar_init();
+        }
+    }
+    // Cauchy fragments of this warp's N-tile (8 output columns), all K rows.
+    double bf[KT];
+    int slot[2];
+    {
+        const int c = warp * 8 + (lane >> 2);
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+            const int k = kt * 4 + (lane & 3);
+            bf[kt] = (k < P.K && c < P.A) ? P.tmat[static_cast<std::size_t>(c) * P.K + k] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int cc = warp * 8 + 2 * (lane & 3) + e;
+            slot[e] = cc < P.A ? P.act_slot[cc] : -1;
+        }
+    }
+    __syncthreads();
+
+    const std::size_t ntiles = (batch + TS - 1) / TS;
+    auto rows_of = [&](long long tile) {
+        return static_cast<int>(min(static_cast<std::size_t>(TS), batch - static_cast<std::size_t>(tile) * TS));
+    };
+    auto claim = [&](int q, long long tile) {
+        sched[q] = tile;
+        if (tile < static_cast<long long>(ntiles)) {
+            const uint32_t bytes = static_cast<uint32_t>(rows_of(tile) * n * sizeof(double));
+            ptx::mbar_expect_tx(&xfull[q], bytes);
+            ptx::bulk_load(xs + q * TILE, in + tile * TS * n, bytes, &xfull[q]);
+        } else {
+            ptx::mbar_arrive(&xfull[q]);
+        }
+    };
+    long long next_tile = 0;
+    if (tid == 0)
+        for (int q = 0; q < kS; ++q) claim(q, static_cast<long long>(atomicAdd(tile_counter, 1ull)));
+    fetch_tile_index(tile_counter, next_tile, tid);
+    const double scale = sqrt(2.0 / L);
+    const double dc_scale = 1.0 / sqrt(static_cast<double>(L));
+    const double y_n = rt[NC].x * scale;
+    bool bad = false;
+    for (int it = 0;; ++it) {
+        const int q = it % kS;
+        ptx::mbar_wait(&xfull[q], (it / kS) & 1);
+        const long long tile = sched[q];
+        if (tile >= static_cast<long long>(ntiles)) break;
+        const int valid = rows_of(tile) - warp * SPW;
+        double* x = xs + q * TILE + warp * SPW * n; // this warp's rows: input, then output
+        double2* a0 = s0 + warp * SPW * NC;
+        double2* a1 = s1 + warp * SPW * NC;
+        double* abuf = atile + (it & 1) * TS * LDA;
+        double* ab = abuf + warp * SPW * LDA;
+        // ---- phase A: DCT of this warp's rows --------------------------------------
+        if ((P.debug & 1) == 0) {
+            const double* yrow = x;
+            if constexpr (FOLD) {
+                double* ys = reinterpret_cast<double*>(a1);
+                lane_loop<SPW * (n / 4)>(lane, [&](int t) {
+                    const int r = t / (n / 4), j = 2 * (t % (n / 4));
+                    const double2 lo = *reinterpret_cast<const double2*>(x + r * n + j);
+                    const double2 hi = *reinterpret_cast<const double2*>(x + r * n + n - 2 - j);
+                    *reinterpret_cast<double2*>(ys + r * L + j) = make_double2(lo.x + hi.y, lo.y + hi.x);
+                    *reinterpret_cast<double2*>(ab + r * LDA + j) = make_double2(lo.x - hi.y, lo.y - hi.x);
+                });
+                __syncwarp();
+                yrow = ys;
+            }
+            stockham_first<NC, SPW>(yrow, a0, lane, valid, bad);
+            __syncwarp();
+            double2* F = fft_passes<NC, SPW, 1>(a0, a1, ptw, lane);
+            double* S = reinterpret_cast<double*>(F == a0 ? a1 : a0);
+            lane_loop<SPW * (NC / 2)>(lane, [&](int t) {
+                const int r = t / (NC / 2), k = t % (NC / 2) + 1;
+                const double2* row = F + r * NC;
+                double* o = S + r * L;
+                const double2 wk = row[k], wc = row[NC - k];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int kk = h == 0 ? k : NC - k;
+                    const double2 a = h == 0 ? wk : wc, c = h == 0 ? wc : wk;
+                    const double sr = a.x + c.x, si = a.y - c.y;
+                    const double dr = a.x - c.x, di = a.y + c.y;
+                    const double2 s2 = sp[kk];
+                    const double qr = s2.x * dr - s2.y * di, qi = s2.x * di + s2.y * dr;
+                    const double vr = sr + qi, vi = si - qr;
+                    const double2 c2 = rt2[kk];
+                    o[kk] = vr * c2.x - vi * c2.y;
+                    o[L - kk] = -(vr * c2.y + vi * c2.x);
+                }
+            });
+            if (lane < SPW) {
+                const double2 w0 = F[lane * NC];
+                const double dc = (w0.x + w0.y) * dc_scale;
+                S[lane * L] = dc;
+                S[lane * L + NC] = (w0.x - w0.y) * y_n;
+                if (lane < valid) bad |= !isfinite(dc); // see fused_small_fwd_kernel
+            }
+            __syncwarp();
+            if constexpr (!FOLD) {
+                lane_loop<SPW * 4 * KT>(lane, [&](int t) {
+                    const int r = t / (4 * KT), k = t % (4 * KT);
+                    const int j = kept_idx[k];
+                    if (j >= 0) ab[r * LDA + k] = S[r * L + j];
+                });
+            }
+            // the input rows are consumed: pass-through slots land in place
+            for (int qq = lane; qq < n_pass; qq += 32) {
+                const int slotq = pass_dst[qq], src = pass_src[qq];
+                const double coef = pass_coef[qq];
+#pragma unroll
+                for (int r = 0; r < SPW; ++r) x[r * n + slotq] = coef * S[r * L + src];
+            }
+        }
+        __syncthreads(); // A tile (and in-place pass-through rows) complete
+        // ---- phase B: DMMA, this warp's 8 columns for all TS rows ----------------
+        {
+            const double* arow = abuf + (lane >> 2) * LDA + (lane & 3);
+            double acc[MT][2];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt) {
+                if (P.debug & 2) break;
+                double a[MT];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) a[mt] = arow[mt * 8 * LDA + kt * 4];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) ptx::dmma_8x8x4(acc[mt][0], acc[mt][1], a[mt], bf[kt]);
+            }
+            double* obt = xs + q * TILE;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const int r = mt * 8 + (lane >> 2);
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (slot[e] >= 0) obt[r * n + slot[e]] = acc[mt][e];
+            }
+        }
+        ptx::fence_proxy_async(); // output writes -> the TMA store below
+        __syncthreads();
+        if (tid == 0) {
+            ptx::bulk_store(out + tile * TS * n, xs + q * TILE, static_cast<uint32_t>(rows_of(tile) * n * sizeof(double)));
+            ptx::bulk_commit();
+            if (it >= 1) {
+                // refill the stage of tile it-1: its store is (all but) certainly read
+                ptx::bulk_wait_read_pending1();
+                claim((it - 1) % kS, next_tile);
+            }
+        }
+        if (it >= 1) fetch_tile_index(tile_counter, next_tile, tid); // used next iteration
+    }
+    if (bad) atomicOr(flag, 1);
+    if (tid == 0) ptx::bulk_wait_all();
+}
+
 template <int LOGN, int KT, int TS, bool FOLD>
 constexpr std::size_t smem_bytes() {
     constexpr int n = 1 << LOGN, L = FOLD ? n / 2 : n, NC = L / 2, TILE = TS * n;
@@ -521,9 +776,22 @@ template <int LOGN, int NTW, int KT, bool FOLD>
 cudaError_t launch_small(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
                          int num_sms, cudaStream_t stream) {
     constexpr int TS = LOGN >= 9 ? 8 : 16;
-    constexpr std::size_t smem = smem_bytes<LOGN, KT, TS, FOLD>();
-    static_assert(smem <= 227 * 1024, "fused small kernel exceeds shared memory");
+    std::size_t smem = smem_bytes<LOGN, KT, TS, FOLD>();
+    static_assert(smem_bytes<LOGN, KT, TS, FOLD>() <= 227 * 1024, "fused small kernel exceeds shared memory");
+    static const bool lockstep = [] {
+        const char* e = std::getenv("DCTP_FUSED_VARIANT");
+        return !(e && std::string(e) == "specialised");
+    }();
     auto kern = fused_small_fwd_kernel<LOGN, NTW, KT, TS, FOLD>;
+    int threads = kThreads;
+    if constexpr (TS >= kComputeWarps) {
+        static_assert(lockstep_smem_bytes<LOGN, KT, TS, FOLD>() <= 227 * 1024, "lockstep kernel exceeds shared memory");
+        if (lockstep && NTW == 1) {
+            kern = fused_lockstep_kernel<LOGN, KT, TS, FOLD>;
+            smem = lockstep_smem_bytes<LOGN, KT, TS, FOLD>();
+            threads = kLockThreads;
+        }
+    }
     static const cudaError_t attr =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (attr != cudaSuccess) return attr;
@@ -535,7 +803,7 @@ cudaError_t launch_small(const double* in, double* out, std::size_t batch, const
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kThreads, smem, stream>>>(in, out, batch, P, flag, counter);
+    kern<<<grid, threads, smem, stream>>>(in, out, batch, P, flag, counter);
     e = cudaGetLastError();
     cudaFreeAsync(counter, stream);
     return e;
@@ -544,7 +812,12 @@ cudaError_t launch_small(const double* in, double* out, std::size_t batch, const
 template <int LOGN, int KT, bool FOLD>
 cudaError_t dispatch_ntw(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
                          int num_sms, cudaStream_t stream) {
-    if (P.A <= 8 * kConsumerWarps) return launch_small<LOGN, 1, KT, FOLD>(in, out, batch, P, flag, num_sms, stream);
+    static const bool specialised = [] {
+        const char* e = std::getenv("DCTP_FUSED_VARIANT");
+        return e && std::string(e) == "specialised";
+    }();
+    if (!specialised || P.A <= 8 * kConsumerWarps)
+        return launch_small<LOGN, 1, KT, FOLD>(in, out, batch, P, flag, num_sms, stream);
     return launch_small<LOGN, 2, KT, FOLD>(in, out, batch, P, flag, num_sms, stream);
 }
 

@@ -166,6 +166,7 @@ dctp::dev::Twiddles<T> twiddles_at(void* base, const TwiddleOffsets& o) {
 struct StageOffsets {
     std::size_t src, x, rscale64, rscale32, dst, y, cscale64, cscale32;
     int rows, cols;
+    int src_contig = 0;
 };
 
 dctp::dev::CauchyStage stage_at(void* base, const StageOffsets& s, bool f32, std::int64_t out_offset) {
@@ -173,7 +174,7 @@ dctp::dev::CauchyStage stage_at(void* base, const StageOffsets& s, bool f32, std
             f32 ? static_cast<const void*>(at<float>(base, s.rscale32)) : at<double>(base, s.rscale64),
             at<int>(base, s.dst), at<double>(base, s.y),
             f32 ? static_cast<const void*>(at<float>(base, s.cscale32)) : at<double>(base, s.cscale64),
-            s.rows, s.cols, out_offset};
+            s.rows, s.cols, out_offset, s.src_contig};
 }
 
 template <class T>
@@ -316,6 +317,10 @@ struct dctp_plan {
     TwiddleOffsets tw64, tw32;
     StageOffsets fwd{}, inv{};
     std::size_t pass_slot = 0, pass_src = 0, pass_sign64 = 0, pass_sign32 = 0;
+    // forward emit list: pass-through slots into the output and the kept
+    // coefficients compacted (to = -k-1) into the Cauchy stage's input rows
+    std::size_t fe_to = 0, fe_from = 0, fe_sign64 = 0, fe_sign32 = 0;
+    int n_fe = 0;
     std::size_t stage_desc = 0; // 4 CauchyStage descriptors: fwd64, fwd32, inv64, inv32
     int n_pass = 0;
     bool small = false;         // fused small-plan forward kernel eligible
@@ -356,6 +361,15 @@ struct dctp_plan {
         else
             sign = at<float>(blob, pass_sign32);
         return {at<int>(blob, pass_slot), at<int>(blob, pass_src), sign, n_pass};
+    }
+    template <class T>
+    dctp::dev::Emit<T> emit_fwd_compact(T* alt, std::size_t ld_alt) const {
+        const T* sign;
+        if constexpr (std::is_same_v<T, double>)
+            sign = at<double>(blob, fe_sign64);
+        else
+            sign = at<float>(blob, fe_sign32);
+        return {at<int>(blob, fe_to), at<int>(blob, fe_from), sign, n_fe, alt, ld_alt};
     }
     template <class T>
     dctp::dev::Emit<T> emit_inv() const {
@@ -515,7 +529,24 @@ static void upload_plan(dctp_plan& p) {
     p.pass_sign32 = blob.add(to_f32(t.pass_sign));
     p.n_pass = static_cast<int>(t.pass_slot.size());
     const int K = static_cast<int>(t.kept_idx.size()), A = static_cast<int>(t.nu.size());
-    p.fwd = {kept_idx, lam, z64, z32, act, nu, sc64, sc32, K, A};
+    std::size_t kept_idx_iota = 0;
+    {
+        std::vector<int> to = t.pass_slot, from = t.pass_src, iota(t.kept_idx.size());
+        std::vector<double> sign = t.pass_sign;
+        for (std::size_t k = 0; k < t.kept_idx.size(); ++k) {
+            to.push_back(-static_cast<int>(k) - 1);
+            from.push_back(t.kept_idx[k]);
+            sign.push_back(1.0);
+            iota[k] = static_cast<int>(k);
+        }
+        p.fe_to = blob.add(to);
+        p.fe_from = blob.add(from);
+        p.fe_sign64 = blob.add(sign);
+        p.fe_sign32 = blob.add(to_f32(sign));
+        p.n_fe = static_cast<int>(to.size());
+        kept_idx_iota = blob.add(iota);
+    }
+    p.fwd = {kept_idx_iota, lam, z64, z32, act, nu, sc64, sc32, K, A, 1};
     p.inv = {act, nu, sc64, sc32, kept_idx, lam, nz64, nz32, A, K};
     // Stage descriptors hold device pointers: reserve, upload, then patch.
     p.stage_desc = blob.add(std::vector<dctp::dev::CauchyStage>(4));
@@ -555,6 +586,18 @@ static std::unique_ptr<dctp_plan> build_plan(std::size_t n, const dctp::host::Up
     return p;
 }
 
+/// The Cauchy stage: fp64 on the DMMA tensor cores (K >= 32), else SIMT.
+template <class T>
+static cudaError_t cauchy_stage(const T* in, std::size_t ld_in, T* out, std::size_t ld_out,
+                                const dctp::dev::CauchyStage* stages, int num_stages, int max_rows, int max_cols,
+                                std::size_t batch, int* flag, cudaStream_t s) {
+    if constexpr (std::is_same_v<T, double>) {
+        if (max_rows >= 32)
+            return dctp::dev::cauchy_rows_dmma(in, ld_in, out, ld_out, stages, num_stages, max_cols, batch, flag, s);
+    }
+    return dctp::dev::cauchy_rows<T>(in, ld_in, out, ld_out, stages, num_stages, max_rows, max_cols, batch, flag, s);
+}
+
 template <class T>
 static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s) {
     if (!p) throw std::invalid_argument("dctp_forward: null plan");
@@ -580,14 +623,18 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
             return;
         }
     }
-    Scratch<T> hat(batch * n, s);
-    cuda_check(DCTP_LAUNCH("dct2", s, dctp::dev::dct2_rows<T>(in, n, hat.ptr, n, out, n, p->emit_fwd<T>(), n, batch,
+    // DCT; pass-through slots go straight to the output, kept coefficients
+    // compacted into `hat` (batch x K) for the Cauchy stage
+    const std::size_t K = (static_cast<std::size_t>(std::max(p->fwd.rows, 1)) + 1) / 2 * 2; // even: 16-byte rows
+    Scratch<T> hat(batch * K, s);
+    cuda_check(DCTP_LAUNCH("dct2", s, dctp::dev::dct2_rows<T>(in, n, nullptr, n, out, n,
+                                                             p->emit_fwd_compact<T>(hat.ptr, K), n, batch,
                                                              p->tw<T>(), p->flag, s)),
                "dct2 kernel");
     if (p->fwd.cols > 0)
         cuda_check(DCTP_LAUNCH("cauchy", s,
-                               dctp::dev::cauchy_rows<T>(hat.ptr, n, out, n, p->stage_dev(std::is_same_v<T, float> ? 1 : 0),
-                                                         1, p->fwd.rows, p->fwd.cols, batch, p->flag, s)),
+                               cauchy_stage<T>(hat.ptr, K, out, n, p->stage_dev(std::is_same_v<T, float> ? 1 : 0), 1,
+                                               p->fwd.rows, p->fwd.cols, batch, p->flag, s)),
                    "cauchy kernel");
 }
 
@@ -604,8 +651,8 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
     Scratch<T> d(batch * n, s);
     if (p->inv.cols > 0)
         cuda_check(DCTP_LAUNCH("cauchy_inv", s,
-                               dctp::dev::cauchy_rows<T>(in, n, d.ptr, n, p->stage_dev(std::is_same_v<T, float> ? 3 : 2),
-                                                         1, p->inv.rows, p->inv.cols, batch, p->flag, s)),
+                               cauchy_stage<T>(in, n, d.ptr, n, p->stage_dev(std::is_same_v<T, float> ? 3 : 2), 1,
+                                               p->inv.rows, p->inv.cols, batch, p->flag, s)),
                    "cauchy kernel");
     cuda_check(DCTP_LAUNCH("idct", s,
                            dctp::dev::idct_rows<T>(d.ptr, n, in, n, p->emit_inv<T>(), out, n, n, batch, p->tw<T>(),
@@ -715,10 +762,10 @@ static void ensemble_forward(const dctp_ensemble* e, const T* in, T* out, std::s
                "dct2 kernel");
     if (!e->members.empty() && e->max_cols > 0)
         cuda_check(DCTP_LAUNCH("cauchy_progressive", s,
-                               dctp::dev::cauchy_rows<T>(out, ld, out, ld,
-                                                         at<dctp::dev::CauchyStage>(e->blob, f32 ? e->desc32 : e->desc64),
-                                                         static_cast<int>(e->members.size()), e->max_rows, e->max_cols,
-                                                         batch, e->flag, s)),
+                               cauchy_stage<T>(out, ld, out, ld,
+                                               at<dctp::dev::CauchyStage>(e->blob, f32 ? e->desc32 : e->desc64),
+                                               static_cast<int>(e->members.size()), e->max_rows, e->max_cols, batch,
+                                               e->flag, s)),
                    "cauchy kernel");
 }
 
@@ -878,9 +925,11 @@ int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is,
         std::vector<StageOffsets> st(k);
         for (std::size_t r = 0; r < k; ++r) {
             const auto& t = tabs[r];
+            bool contig = true;
+            for (std::size_t k = 0; k < t.kept_idx.size(); ++k) contig = contig && t.kept_idx[k] == static_cast<int>(k);
             st[r] = {blob.add(t.kept_idx), blob.add(t.lam_kept), blob.add(t.z_kept), blob.add(to_f32(t.z_kept)),
                      blob.add(t.act_slot), blob.add(t.nu), blob.add(t.act_scale), blob.add(to_f32(t.act_scale)),
-                     static_cast<int>(t.kept_idx.size()), static_cast<int>(t.nu.size())};
+                     static_cast<int>(t.kept_idx.size()), static_cast<int>(t.nu.size()), contig ? 1 : 0};
             e->max_rows = std::max(e->max_rows, st[r].rows);
             e->max_cols = std::max(e->max_cols, st[r].cols);
         }

@@ -113,7 +113,12 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
         }
     for (int t = threadIdx.x; t < rows * emit.count; t += blockDim.x) {
         const int r = t / emit.count, e = t - r * emit.count;
-        out[(b0 + r) * ld_out + emit.to[e]] = emit.sign[e] * sh[r * n + emit.from[e]];
+        const int to = emit.to[e];
+        const T v = emit.sign[e] * sh[r * n + emit.from[e]];
+        if (to >= 0)
+            out[(b0 + r) * ld_out + to] = v;
+        else
+            emit.alt[(b0 + r) * emit.ld_alt + (-to - 1)] = v;
     }
 }
 
@@ -214,8 +219,14 @@ dct2_direct_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ 
     __syncthreads();
     if (hat != nullptr)
         for (int k = threadIdx.x; k < n; k += blockDim.x) hat[b * ld_hat + k] = o[k];
-    for (int e = threadIdx.x; e < emit.count; e += blockDim.x)
-        out[b * ld_out + emit.to[e]] = emit.sign[e] * o[emit.from[e]];
+    for (int e = threadIdx.x; e < emit.count; e += blockDim.x) {
+        const int to = emit.to[e];
+        const T v = emit.sign[e] * o[emit.from[e]];
+        if (to >= 0)
+            out[b * ld_out + to] = v;
+        else
+            emit.alt[b * emit.ld_alt + (-to - 1)] = v;
+    }
 }
 
 template <class T>

@@ -22,10 +22,12 @@ struct Twiddles {
 /// Index/value list for a scattered copy dst[b*ld + to[e]] = sign[e] * src[from[e]].
 template <class T>
 struct Emit {
-    const int* to = nullptr;
+    const int* to = nullptr;   // >= 0: index into the row of `out`; < 0: index -to-1 into the row of `alt`
     const int* from = nullptr;
     const T* sign = nullptr;
     int count = 0;
+    T* alt = nullptr;          // second target (the compacted kept coefficients), row stride ld_alt
+    std::size_t ld_alt = 0;
 };
 
 /// Forward DCT-II of `batch` rows of length n (orthonormal, U^T s):
@@ -56,12 +58,19 @@ struct CauchyStage {
     int rows;             // R
     int cols;             // C
     std::int64_t out_offset; // element offset of this stage's output within a row block
+    int src_contig;       // 1: src[r] == r (rows of `in` already compacted); enables 16-byte loads
 };
 
 template <class T>
 cudaError_t cauchy_rows(const T* in, std::size_t ld_in, T* out, std::size_t ld_out,
                         const CauchyStage* stages_dev, int num_stages, int max_rows, int max_cols,
                         std::size_t batch, int* flag, cudaStream_t stream);
+
+/// fp64 Cauchy stage on the tensor cores (cauchy_dmma.cu); same contract as
+/// cauchy_rows<double>.
+cudaError_t cauchy_rows_dmma(const double* in, std::size_t ld_in, double* out, std::size_t ld_out,
+                             const CauchyStage* stages_dev, int num_stages, int max_cols, std::size_t batch,
+                             int* flag, cudaStream_t stream);
 
 /// Constants of the fused small-plan forward kernel (fused_small.cu).
 /// Generic plans: the Cauchy stage multiplies the kept DCT coefficients by

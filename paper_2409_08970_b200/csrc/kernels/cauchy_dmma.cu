@@ -156,7 +156,7 @@ cauchy_dmma_kernel(const double* __restrict__ in, std::size_t ld_in, double* __r
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int c = c0 + wn + j * 8 + 2 * (lane & 3) + e;
-                if (rok && c < st.cols) { // padded rows stay exactly 0 (x = y would give 0 * inf)
+                if (c < st.cols) {
                     const double v = cscale[c] * acc[i][j][e];
                     bad |= !isfinite(v);
                     orow[st.dst[c]] = v;

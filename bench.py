@@ -335,6 +335,14 @@ def run_gpu_arm(args, cfg, rank: int, local: int, world: int):
                  "hbm_achieved_gbs": hbm_achieved, "hbm_frac": hbm_achieved / hbm_peak,
                  "compute_achieved_tflops": achieved, "compute_frac": (achieved / peak) if peak else None,
                  "t_roof_ms": max(t_flop, t_hbm) * 1e3})
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    # of this workload (profiles/traffic.json), per launch like `achieved`
+    tfile = ROOT / "profiles" / "traffic.json"
+    tmap = json.loads(tfile.read_text()) if tfile.exists() else {}
+    rec = tmap.get(cfg.name)
+    if rec and rec.get("kernel") == top:
+        roof["traffic"] = rec["dram_bytes_per_launch"]
+        roof["traffic_source"] = rec["source"]
     roof["step_hbm_gbs"] = alg["bytes"] * cfg.batch / (ms_per_step * 1e-3) / 1e9
     roof["step_hbm_frac"] = roof["step_hbm_gbs"] / hbm_peak
 

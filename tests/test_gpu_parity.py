@@ -223,3 +223,65 @@ def test_small_plans_fused_path_against_restatement(P, torch, restatement, n, ki
         s = restatement.fill_signals(O.mix_seed(O.SEED, n, batch), 0, n, batch)
         y = plan.forward(dev(torch, s, torch.float64)).cpu().numpy()
         assert O.parity(y, restatement.forward(st, s)) <= TOL64, (n, kind, batch)
+
+
+def test_host_paths_pinned_pageable_and_multi_chunk(P, torch, restatement, monkeypatch):
+    """Host-buffer forward: the staged 3-stream pipeline (ramped chunks, slot
+    reuse) on pageable and pinned buffers, and the opt-in streamed route (one
+    fused launch fed and drained chunk by chunk by the copy engines) with
+    ragged last chunks and several slices. All equal the device-resident result bit for
+    bit; non-finite input is still reported on the streamed route."""
+    import ctypes as C
+
+    from paper_2409_08970_b200._native import check, lib
+    cfg = O.config(2)
+    batch = 5 * 4096 + 77
+    s = restatement.fill_signals(O.mix_seed(O.SEED, cfg.n, 7), 0, cfg.n, batch)
+    plan = plan_for(P, 2)
+    ref = plan.forward(dev(torch, s, torch.float64)).cpu().numpy()
+    assert np.array_equal(plan.forward(s), ref)  # pageable -> staged pipeline
+    pin_in = torch.from_numpy(s).pin_memory()
+    pin_out = torch.empty_like(pin_in).pin_memory()
+
+    def run():
+        pin_out.zero_()
+        check(lib.dctp_forward_host_f64(plan._h, C.c_void_p(pin_in.data_ptr()), C.c_void_p(pin_out.data_ptr()),
+                                        batch))
+        return pin_out.numpy()
+
+    assert np.array_equal(run(), ref)  # staged pipeline on pinned buffers
+    monkeypatch.setenv("DCTP_HOST_CHUNK_MB", "1")      # many chunks: 256-row head ramp, 512-row middle
+    assert np.array_equal(run(), ref)
+    monkeypatch.delenv("DCTP_HOST_CHUNK_MB")
+    monkeypatch.setenv("DCTP_HOST_STREAMED", "1")
+    assert np.array_equal(run(), ref)  # streamed, 2 MB chunks, one slice
+    monkeypatch.setenv("DCTP_STREAM_CHUNK_KB", "300")  # 144-row chunks (9 tiles), ragged last chunk
+    monkeypatch.setenv("DCTP_STREAM_SLICE_MB", "3")     # several slices
+    assert np.array_equal(run(), ref)
+    pin_in[batch // 2, 3] = float("nan")
+    with pytest.raises(P.DomainError):
+        run()
+    pin_in[batch // 2, 3] = 0.0
+    monkeypatch.delenv("DCTP_STREAM_CHUNK_KB")
+    monkeypatch.delenv("DCTP_STREAM_SLICE_MB")
+    monkeypatch.delenv("DCTP_HOST_STREAMED")
+    s2 = pin_in.numpy().copy()
+    assert O.parity(run(), plan.forward(dev(torch, s2, torch.float64)).cpu().numpy()) == 0.0
+    # inverse through the staged pipeline (multi-chunk) round-trips
+    back = plan.inverse(ref)
+    assert O.parity(back, s) <= TOL64
+
+
+def test_misaligned_device_views_take_the_generic_route(P, torch, restatement):
+    """The fused kernel's TMA bulk copies need 16-byte aligned rows; an
+    8-byte-offset view must still give the right answer (generic kernels)."""
+    cfg = O.config(2)
+    s = restatement.fill_signals(O.mix_seed(O.SEED, cfg.n, 8), 0, cfg.n, 33)
+    plan = plan_for(P, 2)
+    ref = plan.forward(dev(torch, s, torch.float64)).cpu().numpy()
+    big = torch.zeros(33 * cfg.n + 1, dtype=torch.float64, device="cuda")
+    big[1:].copy_(torch.from_numpy(s.reshape(-1)))
+    view = big[1:].view(33, cfg.n)
+    out_big = torch.zeros(33 * cfg.n + 1, dtype=torch.float64, device="cuda")
+    plan.forward(view, out=out_big[1:].view(33, cfg.n))
+    assert O.parity(out_big[1:].view(33, cfg.n).cpu().numpy(), ref) <= TOL64

@@ -572,7 +572,10 @@ fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, 
 /// issues the TMA bulk store and refills the buffer two tiles later (by then
 /// the store has long finished reading it), and fetches tile indices from the
 /// global counter one iteration ahead with a predicated atomic, so nothing on
-/// the critical path waits for memory.  The A tile is double-buffered.
+/// the critical path waits for memory.  The A tile is double-buffered.  The
+/// first kStages tiles of CTA b are b + q * grid (round-robin, so a small
+/// batch still spreads over every CTA); later tiles come from the counter,
+/// offset by kStages * grid.
 constexpr int kComputeWarps = 16;
 constexpr int kLockThreads = 32 * kComputeWarps;
 
@@ -586,7 +589,7 @@ constexpr std::size_t lockstep_smem_bytes() {
     constexpr int S = lock_stages<FOLD>();
     return S * TILE * sizeof(double) + 2 * TS * NC * sizeof(double2) + 2 * TS * LDA * sizeof(double) +
            (tw + 3 * NC + 2) * sizeof(double2) + n * sizeof(double) + (4 * KT + 2 * n) * sizeof(int) +
-           S * sizeof(uint64_t) + S * sizeof(long long);
+           S * sizeof(uint64_t) + S * sizeof(long long) + 8 * sizeof(unsigned long long);
 }
 
 /// next = atomicAdd(ctr, 1) on thread 0 only, without a branch (the result is
@@ -628,6 +631,7 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
     int* pass_dst = pass_src + n;
     uint64_t* xfull = reinterpret_cast<uint64_t*>(pass_dst + n);   // [kS] tile landed (tx bytes)
     long long* sched = reinterpret_cast<long long*>(xfull + kS);   // [kS] tile in stage q
+    unsigned long long* tacc = reinterpret_cast<unsigned long long*>(sched + kS); // [8] debug phase cycles
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int n_pass = P.n_pass;
@@ -659,6 +663,7 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
             for (int q = 0; q < kS; ++q) ptx::mbar_init(&xfull[q], 1);
             ptx::fence_mbar_init();
         }
+        if (tid < 8) tacc[tid] = 0;
     }
     // Cauchy fragments of this warp's N-tile (8 output columns), all K rows.
     double bf[KT];
@@ -695,15 +700,27 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
     };
     long long next_tile = 0, stored_tile = -1; // stored_tile: last tile stored (thread 0, streamed launches)
     if (tid == 0)
-        for (int q = 0; q < kS; ++q) claim(q, static_cast<long long>(atomicAdd(tile_counter, 1ull)));
+        for (int q = 0; q < kS; ++q) claim(q, static_cast<long long>(blockIdx.x) + q * static_cast<long long>(gridDim.x));
     fetch_tile_index(tile_counter, next_tile, tid);
     const double scale = sqrt(2.0 / L);
     const double dc_scale = 1.0 / sqrt(static_cast<double>(L));
     const double y_n = rt[NC].x * scale;
     bool bad = false;
+    // DCTP_DEBUG_MODE & 4: phase cycles seen by thread 32 (slots 0-5) and
+    // thread 0's store/claim duty (slot 6), kept in shared memory
+    const bool timing = P.timers != nullptr && (tid == 32 || tid == 0);
+    long long tmark = clock64();
+#define LT(i)                                                        \
+    if (timing) {                                                    \
+        const long long now_ = clock64();                            \
+        if (tid == 32 || (i) == 6) tacc[i] += static_cast<unsigned long long>(now_ - tmark); \
+        tmark = now_;                                                \
+    }
     for (int it = 0;; ++it) {
         const int q = it % kS;
+        LT(5);
         ptx::mbar_wait(&xfull[q], (it / kS) & 1);
+        LT(0);
         const long long tile = sched[q];
         if (tile >= static_cast<long long>(ntiles)) break;
         const int valid = rows_of(tile) - warp * SPW;
@@ -773,7 +790,9 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
                 for (int r = 0; r < SPW; ++r) x[r * n + slotq] = coef * S[r * L + src];
             }
         }
+        LT(1);
         __syncthreads(); // A tile (and in-place pass-through rows) complete
+        LT(2);
         // ---- phase B: DMMA, this warp's 8 columns for all TS rows ----------------
         {
             const double* arow = abuf + (lane >> 2) * LDA + (lane & 3);
@@ -798,8 +817,10 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
                     if (slot[e] >= 0) obt[r * n + slot[e]] = acc[mt][e];
             }
         }
+        LT(3);
         ptx::fence_proxy_async(); // output writes -> the TMA store below
         __syncthreads();
+        LT(4);
         if (tid == 0) {
             ptx::bulk_store(out + tile * TS * n, xs + q * TILE, static_cast<uint32_t>(rows_of(tile) * n * sizeof(double)));
             ptx::bulk_commit();
@@ -811,11 +832,18 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
                 } else {
                     ptx::bulk_wait_read_pending1();
                 }
-                claim((it - 1) % kS, next_tile);
+                claim((it - 1) % kS, next_tile + kS * static_cast<long long>(gridDim.x));
             }
             stored_tile = tile;
         }
+        LT(6);
         if (it >= 1) fetch_tile_index(tile_counter, next_tile, tid); // used next iteration
+    }
+#undef LT
+    if (timing) {
+        if (tid == 32)
+            for (int i = 0; i < 6; ++i) atomicAdd(P.timers + i, tacc[i]);
+        if (tid == 0) atomicAdd(P.timers + 6, tacc[6]);
     }
     if (bad) atomicOr(flag, 1);
     if (tid == 0) {

@@ -21,8 +21,8 @@ plan.forward(x, sync=False, out=y)
 torch.cuda.synchronize()
 _native.lib.dctp_debug_timers(buf)
 tiles = (w.batch + 15) // 16
-names = ["wait_load", "phaseA_dct", "barriers", "phaseB_dmma", "atomic+loop", "store_issue", "wait_read", "claim"]
-tot = sum(buf[:8])
-for i, nm in enumerate(names):
+names = ["wait_load", "phaseA_dct", "sync1_wait", "phaseB_dmma", "sync2_wait", "loop_top", "t0_store_claim"]
+tot = sum(buf[:6])
+for i, nm in enumerate(names):  # slots 0-5: thread 32's loop (sums to its total); 6: thread 0's duty
     print(f"{nm:12s} {buf[i] / tiles:8.0f} cycles/tile {100 * buf[i] / max(tot, 1):5.1f}%")
 print(f"total {tot / 148 / 1.965e3:.1f} us per CTA at 1965 MHz")

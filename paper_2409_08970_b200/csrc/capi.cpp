@@ -5,7 +5,6 @@
 // the reference's floating-point operations bit for bit.
 #include "dctplus_b200.h"
 
-#include <cuda.h>
 
 #include <algorithm>
 #include <cmath>
@@ -676,7 +675,7 @@ static void sync_check(int device, int* flag, cudaStream_t s) {
     cuda_check(cudaMemcpy(&h, flag, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(flag)");
     if (h != 0) {
         cuda_check(cudaMemset(flag, 0, sizeof(int)), "cudaMemset(flag)");
-        if (h & 2) throw std::runtime_error("DctPlusPlan: streamed forward timed out waiting for an input chunk");
+        if (h & 2) throw std::runtime_error("DctPlusPlan: fused kernel timed out waiting for a peer CTA");
         throw std::domain_error("DctPlusPlan: non-finite input sample");
     }
 }
@@ -694,14 +693,6 @@ struct HostPipe {
     std::vector<cudaEvent_t> loaded, computed, drained;
     void* buf = nullptr;
     std::size_t buf_bytes = 0;
-    // streamed forward (host_streamed): slice-sized device buffers, chunk flags
-    void* sbuf = nullptr;
-    std::size_t sbuf_bytes = 0;
-    unsigned* flags = nullptr; // ready[max_chunks] then done[max_chunks]
-    std::size_t max_chunks = 0;
-    unsigned epoch = 0;
-    cudaEvent_t reset = nullptr;
-    int mem_ops = -1; // stream memory ops usable on this device (-1: not probed yet)
 };
 
 constexpr int kMaxHostSlots = 8;
@@ -948,195 +939,24 @@ int dctp_plan_sync_check(const dctp_plan* p, void* stream) {
     });
 }
 
-} // extern "C"
-
-/// cuStreamWaitValue32 / cuStreamWriteValue32 through the runtime's driver
-/// entry-point query (no link against libcuda).
-struct StreamMemOps {
-    using Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-    Fn wait = nullptr, write = nullptr;
-};
-
-static const StreamMemOps& stream_mem_ops() {
-    static const StreamMemOps ops = [] {
-        StreamMemOps o;
-        void* fw = nullptr;
-        void* fr = nullptr;
-        cudaDriverEntryPointQueryResult qw{}, qr{};
-        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fw, cudaEnableDefault, &qw) == cudaSuccess &&
-            cudaGetDriverEntryPoint("cuStreamWriteValue32", &fr, cudaEnableDefault, &qr) == cudaSuccess &&
-            qw == cudaDriverEntryPointSuccess && qr == cudaDriverEntryPointSuccess) {
-            o.wait = reinterpret_cast<StreamMemOps::Fn>(fw);
-            o.write = reinterpret_cast<StreamMemOps::Fn>(fr);
-        }
-        cudaGetLastError();
-        return o;
-    }();
-    return ops;
-}
-
-static bool is_pinned(const void* h) {
-    cudaPointerAttributes a{};
-    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeHost;
-}
-
-/// Streamed host-buffer forward for fused small plans (n <= 256, fp64, pinned
-/// host buffers).  ONE fused-kernel launch covers a whole slice of the batch
-/// (up to 512 MB of input); the copy engines feed it chunk by chunk and drain
-/// it chunk by chunk (ChunkSync, kernels/launch.hpp): the H2D stream marks
-/// each landed chunk with a stream memory write, the kernel waits for that
-/// mark before its TMA loads, counts stored tiles per chunk, and the D2H
-/// stream waits (stream memory wait) for each chunk's count before copying it
-/// out.  Both PCIe directions then run for the whole slice, with no per-chunk
-/// kernel launch and no pipeline fill beyond one chunk.  Opt-in
-/// (DCTP_HOST_STREAMED=1): on the B200 PCIe hosts measured so far the copy
-/// engines move small chunks at about half rate while the persistent kernel
-/// runs (C2: 3.8 ms vs 3.26 ms staged); DCTP_STREAM_CHUNK_KB / DCTP_STREAM_SLICE_MB
-/// set the chunk and slice sizes (all read per call).
-template <class T>
-static bool host_streamed(const dctp_plan* p, const T* h_in, T* h_out, std::size_t batch) {
-    if constexpr (!std::is_same_v<T, double>) {
-        return false;
-    } else {
-        const char* e = std::getenv("DCTP_HOST_STREAMED"); // opt-in, read per call (tests flip it)
-        const bool on = e && std::atoi(e) != 0;
-        const std::size_t n = p->st.n;
-        const int ts = dctp::dev::fused_small_stream_tile_rows(n);
-        if (!on || !p->small || ts == 0 || debug_mode() != 0) return false;
-        const StreamMemOps& ops = stream_mem_ops();
-        if (!ops.wait || !ops.write) return false;
-        DeviceScope scope(p->device);
-        if (!is_pinned(h_in) || !is_pinned(h_out)) return false;
-        HostPipe& hp = host_pipe(p->device);
-        if (hp.mem_ops < 0) { // probe once: a stream write must land
-            hp.mem_ops = 0;
-            unsigned* w = nullptr;
-            if (cudaMalloc(reinterpret_cast<void**>(&w), sizeof(unsigned)) == cudaSuccess) {
-                unsigned h = 0;
-                if (cudaMemset(w, 0, sizeof(unsigned)) == cudaSuccess &&
-                    ops.write(hp.comp, reinterpret_cast<CUdeviceptr>(w), 7u, 0) == CUDA_SUCCESS &&
-                    ops.wait(hp.comp, reinterpret_cast<CUdeviceptr>(w), 7u, CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS &&
-                    cudaStreamSynchronize(hp.comp) == cudaSuccess &&
-                    cudaMemcpy(&h, w, sizeof(unsigned), cudaMemcpyDeviceToHost) == cudaSuccess && h == 7u)
-                    hp.mem_ops = 1;
-                cudaFree(w);
-            }
-            cudaGetLastError();
-        }
-        if (hp.mem_ops != 1) return false;
-
-        const std::size_t row_bytes = n * sizeof(double);
-        const std::size_t chunk_rows = std::max<std::size_t>(
-            ts, (env_size("DCTP_STREAM_CHUNK_KB", 2048) << 10) / row_bytes / ts * ts);
-        const std::size_t slice_rows = std::min(
-            batch, std::max(chunk_rows, (env_size("DCTP_STREAM_SLICE_MB", 512) << 20) / row_bytes / chunk_rows * chunk_rows));
-        const std::size_t nchunks_max = (slice_rows + chunk_rows - 1) / chunk_rows;
-        const std::size_t need = 2 * slice_rows * row_bytes;
-        if (hp.sbuf_bytes < need) {
-            if (hp.sbuf) cuda_check(cudaFree(hp.sbuf), "cudaFree(stream buffer)");
-            hp.sbuf = nullptr;
-            hp.sbuf_bytes = 0;
-            cuda_check(cudaMalloc(&hp.sbuf, need), "cudaMalloc(stream buffer)");
-            hp.sbuf_bytes = need;
-        }
-        if (hp.max_chunks < nchunks_max) {
-            if (hp.flags) cuda_check(cudaFree(hp.flags), "cudaFree(stream flags)");
-            hp.flags = nullptr;
-            cuda_check(cudaMalloc(reinterpret_cast<void**>(&hp.flags), 2 * nchunks_max * sizeof(unsigned)),
-                       "cudaMalloc(stream flags)");
-            cuda_check(cudaMemset(hp.flags, 0, 2 * nchunks_max * sizeof(unsigned)), "cudaMemset(stream flags)");
-            hp.max_chunks = nchunks_max;
-            hp.epoch = 0;
-        }
-        if (!hp.reset) cuda_check(cudaEventCreateWithFlags(&hp.reset, cudaEventDisableTiming), "cudaEventCreate");
-        unsigned* ready = hp.flags;
-        unsigned* done = hp.flags + hp.max_chunks;
-        double* din = static_cast<double*>(hp.sbuf);
-        double* dout = din + slice_rows * n;
-        const dctp::dev::SmallPlanDev sp = small_plan_dev(p);
-        const bool trace = std::getenv("DCTP_STREAM_TRACE") != nullptr; // per-chunk event timeline (stderr)
-        for (std::size_t r0 = 0; r0 < batch; r0 += slice_rows) {
-            const std::size_t nr = std::min(slice_rows, batch - r0);
-            const std::size_t nch = (nr + chunk_rows - 1) / chunk_rows;
-            const unsigned epoch = ++hp.epoch;
-            std::vector<cudaEvent_t> tev(trace ? 3 * nch + 1 : 0);
-            for (auto& ev : tev) cudaEventCreate(&ev);
-            if (trace) cudaEventRecord(tev[0], hp.comp);
-            // done counters restart at 0; the D2H waits must not see the last slice's counts
-            cuda_check(cudaMemsetAsync(done, 0, nch * sizeof(unsigned), hp.comp), "cudaMemsetAsync(done)");
-            cuda_check(cudaEventRecord(hp.reset, hp.comp), "cudaEventRecord");
-            cuda_check(cudaStreamWaitEvent(hp.out, hp.reset, 0), "cudaStreamWaitEvent");
-            const dctp::dev::ChunkSync cs{ready, done, epoch, static_cast<int>(chunk_rows / ts)};
-            const cudaError_t le = DCTP_LAUNCH("fused_small_fwd", hp.comp,
-                                               dctp::dev::fused_small_forward(din, dout, nr, sp, p->flag, p->num_sms,
-                                                                              hp.comp, cs));
-            if (le == cudaErrorNotSupported && r0 == 0) {
-                cudaGetLastError();
-                cuda_check(cudaStreamSynchronize(hp.comp), "cudaStreamSynchronize");
-                return false; // this kernel variant cannot stream: staged pipeline
-            }
-            cuda_check(le, "fused small forward kernel (streamed)");
-            for (std::size_t c = 0; c < nch; ++c) {
-                const std::size_t rows = std::min(chunk_rows, nr - c * chunk_rows);
-                cuda_check(cudaMemcpyAsync(din + c * chunk_rows * n, h_in + (r0 + c * chunk_rows) * n,
-                                           rows * row_bytes, cudaMemcpyHostToDevice, hp.in),
-                           "H2D");
-                if (ops.write(hp.in, reinterpret_cast<CUdeviceptr>(ready + c), epoch, 0) != CUDA_SUCCESS)
-                    throw std::runtime_error("cuStreamWriteValue32 failed");
-                if (trace) cudaEventRecord(tev[1 + 3 * c], hp.in);
-            }
-            for (std::size_t c = 0; c < nch; ++c) {
-                const std::size_t rows = std::min(chunk_rows, nr - c * chunk_rows);
-                const unsigned tiles = static_cast<unsigned>((rows + ts - 1) / ts);
-                if (ops.wait(hp.out, reinterpret_cast<CUdeviceptr>(done + c), tiles, CU_STREAM_WAIT_VALUE_GEQ) !=
-                    CUDA_SUCCESS)
-                    throw std::runtime_error("cuStreamWaitValue32 failed");
-                if (trace) cudaEventRecord(tev[2 + 3 * c], hp.out);
-                cuda_check(cudaMemcpyAsync(h_out + (r0 + c * chunk_rows) * n, dout + c * chunk_rows * n,
-                                           rows * row_bytes, cudaMemcpyDeviceToHost, hp.out),
-                           "D2H");
-                if (trace) cudaEventRecord(tev[3 + 3 * c], hp.out);
-            }
-            for (cudaStream_t st : {hp.in, hp.comp, hp.out})
-                cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-            if (trace) {
-                for (std::size_t c = 0; c < nch; ++c) {
-                    float t[3];
-                    for (int k = 0; k < 3; ++k) cudaEventElapsedTime(&t[k], tev[0], tev[1 + 3 * c + k]);
-                    std::fprintf(stderr, "chunk %zu landed %.3f done %.3f out %.3f ms\n", c, t[0], t[1], t[2]);
-                }
-                for (auto ev : tev) cudaEventDestroy(ev);
-            }
-        }
-        return true;
-    }
-}
-
-extern "C" {
-
-#define DCTP_HOST_ENTRY(NAME, T, FN, ZC)                                                              \
+#define DCTP_HOST_ENTRY(NAME, T, FN)                                                              \
     int NAME(const dctp_plan* p, const T* h_in, T* h_out, size_t batch) {                             \
         return guarded([&] {                                                                          \
             if (!p) throw std::invalid_argument(#NAME ": null plan");                                 \
             if (!p->blob) throw std::invalid_argument("DctPlusPlan: host-only plan (created with device < 0)"); \
             if (batch == 0) return;                                                                   \
             const std::size_t n = p->st.n;                                                           \
-            if (!(ZC && host_streamed<T>(p, h_in, h_out, batch)))                                        \
-                host_roundtrip<T>(p->device, batch, n, n, h_in, h_out,                                \
-                                  [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) {     \
-                                      FN<T>(p, din, dout, rows, s);                                   \
-                                  });                                                                 \
+            host_roundtrip<T>(p->device, batch, n, n, h_in, h_out,                                    \
+                              [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) {         \
+                                  FN<T>(p, din, dout, rows, s);                                       \
+                              });                                                                     \
             sync_check(p->device, p->flag, nullptr);                                                  \
         });                                                                                           \
     }
-DCTP_HOST_ENTRY(dctp_forward_host_f64, double, plan_forward, true)
-DCTP_HOST_ENTRY(dctp_forward_host_f32, float, plan_forward, true)
-DCTP_HOST_ENTRY(dctp_inverse_host_f64, double, plan_inverse, false)
-DCTP_HOST_ENTRY(dctp_inverse_host_f32, float, plan_inverse, false)
+DCTP_HOST_ENTRY(dctp_forward_host_f64, double, plan_forward)
+DCTP_HOST_ENTRY(dctp_forward_host_f32, float, plan_forward)
+DCTP_HOST_ENTRY(dctp_inverse_host_f64, double, plan_inverse)
+DCTP_HOST_ENTRY(dctp_inverse_host_f32, float, plan_inverse)
 #undef DCTP_HOST_ENTRY
 
 int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is, const size_t* js, const double* rhos,

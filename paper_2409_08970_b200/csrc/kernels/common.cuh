@@ -115,15 +115,6 @@ __device__ __forceinline__ void bulk_wait_read_pending1() {
     asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
 }
 
-/// All but the most recent bulk group have completed (writes performed).
-__device__ __forceinline__ void bulk_wait_pending1() { asm volatile("cp.async.bulk.wait_group 1;\n" ::: "memory"); }
-
-/// Generic/async proxy ordering for global memory (data written by a copy
-/// engine, observed through an acquire load, then read by TMA).
-__device__ __forceinline__ void fence_proxy_async_global() {
-    asm volatile("fence.proxy.async.global;\n" ::: "memory");
-}
-
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
 /// Generic-proxy shared-memory writes -> visible to the async (TMA) proxy.

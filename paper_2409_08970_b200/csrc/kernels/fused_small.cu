@@ -189,37 +189,6 @@ __device__ __forceinline__ double2* fft_passes(double2* a, double2* b, const dou
 /// so the Cauchy stage runs on u against W = D_odd^T T (the DCT-IV folded into
 /// the plan's matrix, same DMMA work as T) and only the length-n/2 DCT-II of y
 /// goes through the FFT — half the producer work (deflation).
-/// Streamed launches (ChunkSync): wait until the input chunk holding `tile`
-/// has landed.  A copy that never arrives (a wedged stream) must not hang the
-/// GPU: after 10 s the wait gives up and raises flag bit 2 (the host reports a
-/// runtime error; the tile's data is garbage).
-__device__ __forceinline__ void wait_chunk(const ChunkSync& cs, long long tile, int* flag) {
-    const unsigned* f = cs.ready + tile / cs.tiles_per_chunk;
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-    if (v != cs.epoch) {
-        unsigned long long t0, t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        do {
-            __nanosleep(100);
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > 10000000000ull) {
-                atomicOr(flag, 2);
-                break;
-            }
-        } while (v != cs.epoch);
-    }
-    ptx::fence_proxy_async_global();
-}
-
-/// Streamed launches: the output of `tile` is in global memory (its bulk
-/// store group has completed); count it towards its chunk.
-__device__ __forceinline__ void signal_chunk(const ChunkSync& cs, long long tile) {
-    __threadfence();
-    atomicAdd(cs.done + tile / cs.tiles_per_chunk, 1u);
-}
-
 /// The tile scheduler's counter pair re-arms itself: ctr[0] hands out tile
 /// tickets, ctr[1] counts CTAs that have made their last claim; the last CTA
 /// zeroes both, so the next launch on the same stream finds them at 0 without
@@ -239,7 +208,7 @@ __device__ __forceinline__ void release_counter(unsigned long long* ctr, long lo
 template <int LOGN, int NTW, int KT, int TS, bool FOLD>
 __global__ void __launch_bounds__(kThreads, 1)
 fused_small_fwd_kernel(const double* __restrict__ in, double* __restrict__ out, std::size_t batch, SmallPlanDev P,
-                       int* flag, unsigned long long* tile_counter, ChunkSync /*unsupported: see launch_small*/) {
+                       int* flag, unsigned long long* tile_counter) {
     constexpr int n = 1 << LOGN, L = FOLD ? n / 2 : n, NC = L / 2, MT = TS / 8;
     constexpr int TILE = TS * n; // doubles per signal tile
     using PS = Passes<NC>;
@@ -609,7 +578,7 @@ __device__ __forceinline__ void fetch_tile_index(unsigned long long* ctr, long l
 template <int LOGN, int KT, int TS, bool FOLD>
 __global__ void __launch_bounds__(kLockThreads, 1)
 fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, std::size_t batch, SmallPlanDev P,
-                      int* flag, unsigned long long* tile_counter, ChunkSync cs) {
+                      int* flag, unsigned long long* tile_counter) {
     constexpr int n = 1 << LOGN, L = FOLD ? n / 2 : n, NC = L / 2, MT = TS / 8;
     constexpr int TILE = TS * n;
     constexpr int SPW = TS / kComputeWarps; // rows per warp in the DCT phase
@@ -691,14 +660,13 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
         sched[q] = tile;
         if (tile < static_cast<long long>(ntiles)) {
             const uint32_t bytes = static_cast<uint32_t>(rows_of(tile) * n * sizeof(double));
-            if (cs.ready != nullptr) wait_chunk(cs, tile, flag);
             ptx::mbar_expect_tx(&xfull[q], bytes);
             ptx::bulk_load(xs + q * TILE, in + tile * TS * n, bytes, &xfull[q]);
         } else {
             ptx::mbar_arrive(&xfull[q]);
         }
     };
-    long long next_tile = 0, stored_tile = -1; // stored_tile: last tile stored (thread 0, streamed launches)
+    long long next_tile = 0;
     if (tid == 0)
         for (int q = 0; q < kS; ++q) claim(q, static_cast<long long>(blockIdx.x) + q * static_cast<long long>(gridDim.x));
     fetch_tile_index(tile_counter, next_tile, tid);
@@ -826,15 +794,9 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
             ptx::bulk_commit();
             if (it >= 1) {
                 // refill the stage of tile it-1: its store is (all but) certainly read
-                if (cs.done != nullptr) {
-                    ptx::bulk_wait_pending1(); // ... and, streamed, written: hand it to the D2H stream
-                    signal_chunk(cs, stored_tile);
-                } else {
-                    ptx::bulk_wait_read_pending1();
-                }
+                ptx::bulk_wait_read_pending1();
                 claim((it - 1) % kS, next_tile + kS * static_cast<long long>(gridDim.x));
             }
-            stored_tile = tile;
         }
         LT(6);
         if (it >= 1) fetch_tile_index(tile_counter, next_tile, tid); // used next iteration
@@ -848,7 +810,6 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
     if (bad) atomicOr(flag, 1);
     if (tid == 0) {
         ptx::bulk_wait_all();
-        if (cs.done != nullptr && stored_tile >= 0) signal_chunk(cs, stored_tile);
         release_counter(tile_counter, next_tile);
     }
 }
@@ -888,7 +849,7 @@ cudaError_t stream_counter(cudaStream_t stream, unsigned long long** out) {
 
 template <int LOGN, int NTW, int KT, bool FOLD>
 cudaError_t launch_small(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
-                         int num_sms, cudaStream_t stream, const ChunkSync& cs) {
+                         int num_sms, cudaStream_t stream) {
     constexpr int TS = LOGN >= 9 ? 8 : 16;
     std::size_t smem = smem_bytes<LOGN, KT, TS, FOLD>();
     static_assert(smem_bytes<LOGN, KT, TS, FOLD>() <= 227 * 1024, "fused small kernel exceeds shared memory");
@@ -906,7 +867,6 @@ cudaError_t launch_small(const double* in, double* out, std::size_t batch, const
             threads = kLockThreads;
         }
     }
-    if (cs.ready != nullptr && threads != kLockThreads) return cudaErrorNotSupported; // streamed: lockstep only
     static const cudaError_t attr =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (attr != cudaSuccess) return attr;
@@ -924,7 +884,7 @@ cudaError_t launch_small(const double* in, double* out, std::size_t batch, const
         if (e != cudaSuccess) return e;
         e = cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned long long), stream);
         if (e != cudaSuccess) return e;
-        kern<<<grid, threads, smem, stream>>>(in, out, batch, P, flag, counter, cs);
+        kern<<<grid, threads, smem, stream>>>(in, out, batch, P, flag, counter);
         e = cudaGetLastError();
         cudaFreeAsync(counter, stream);
         return e;
@@ -932,38 +892,38 @@ cudaError_t launch_small(const double* in, double* out, std::size_t batch, const
     unsigned long long* counter = nullptr;
     e = stream_counter(stream, &counter);
     if (e != cudaSuccess) return e;
-    kern<<<grid, threads, smem, stream>>>(in, out, batch, P, flag, counter, cs);
+    kern<<<grid, threads, smem, stream>>>(in, out, batch, P, flag, counter);
     return cudaGetLastError();
 }
 
 template <int LOGN, int KT, bool FOLD>
 cudaError_t dispatch_ntw(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
-                         int num_sms, cudaStream_t stream, const ChunkSync& cs) {
+                         int num_sms, cudaStream_t stream) {
     static const bool specialised = [] {
         const char* e = std::getenv("DCTP_FUSED_VARIANT");
         return e && std::string(e) == "specialised";
     }();
     if (!specialised || P.A <= 8 * kConsumerWarps)
-        return launch_small<LOGN, 1, KT, FOLD>(in, out, batch, P, flag, num_sms, stream, cs);
-    return launch_small<LOGN, 2, KT, FOLD>(in, out, batch, P, flag, num_sms, stream, cs);
+        return launch_small<LOGN, 1, KT, FOLD>(in, out, batch, P, flag, num_sms, stream);
+    return launch_small<LOGN, 2, KT, FOLD>(in, out, batch, P, flag, num_sms, stream);
 }
 
 /// K is padded up to 4*KT with KT in {4, 8, 16, 32} (never above n/4).  A
 /// folded plan's Cauchy K is n/2.
 template <int LOGN>
 cudaError_t dispatch_kt(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
-                        int num_sms, cudaStream_t stream, const ChunkSync& cs) {
+                        int num_sms, cudaStream_t stream) {
     constexpr int n = 1 << LOGN;
     if constexpr (n >= 64 && n / 8 <= KTMAX) {
-        if (P.fold) return dispatch_ntw<LOGN, n / 8, true>(in, out, batch, P, flag, num_sms, stream, cs);
+        if (P.fold) return dispatch_ntw<LOGN, n / 8, true>(in, out, batch, P, flag, num_sms, stream);
     }
     if (P.fold) return cudaErrorInvalidValue;
-    if (P.K <= 16 || n <= 16) return dispatch_ntw<LOGN, 4, false>(in, out, batch, P, flag, num_sms, stream, cs);
+    if (P.K <= 16 || n <= 16) return dispatch_ntw<LOGN, 4, false>(in, out, batch, P, flag, num_sms, stream);
     if constexpr (n >= 32)
-        if (P.K <= 32 || n <= 32) return dispatch_ntw<LOGN, 8, false>(in, out, batch, P, flag, num_sms, stream, cs);
+        if (P.K <= 32 || n <= 32) return dispatch_ntw<LOGN, 8, false>(in, out, batch, P, flag, num_sms, stream);
     if constexpr (n >= 64)
-        if (P.K <= 64 || n <= 64) return dispatch_ntw<LOGN, 16, false>(in, out, batch, P, flag, num_sms, stream, cs);
-    if constexpr (n >= 128) return dispatch_ntw<LOGN, 32, false>(in, out, batch, P, flag, num_sms, stream, cs);
+        if (P.K <= 64 || n <= 64) return dispatch_ntw<LOGN, 16, false>(in, out, batch, P, flag, num_sms, stream);
+    if constexpr (n >= 128) return dispatch_ntw<LOGN, 32, false>(in, out, batch, P, flag, num_sms, stream);
     return cudaErrorInvalidValue;
 }
 
@@ -977,18 +937,16 @@ bool fused_small_fold_supported(std::size_t n, int columns) {
     return is_pow2(n) && n >= 64 && n / 2 <= 4 * KTMAX && columns <= 16 * kConsumerWarps;
 }
 
-int fused_small_stream_tile_rows(std::size_t n) { return (n >= 16 && n <= 256) ? 16 : 0; }
-
 cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
-                                int num_sms, cudaStream_t stream, const ChunkSync& cs) {
+                                int num_sms, cudaStream_t stream) {
     if (batch == 0) return cudaSuccess;
     switch (P.n) {
-        case 16: return dispatch_kt<4>(in, out, batch, P, flag, num_sms, stream, cs);
-        case 32: return dispatch_kt<5>(in, out, batch, P, flag, num_sms, stream, cs);
-        case 64: return dispatch_kt<6>(in, out, batch, P, flag, num_sms, stream, cs);
-        case 128: return dispatch_kt<7>(in, out, batch, P, flag, num_sms, stream, cs);
-        case 256: return dispatch_kt<8>(in, out, batch, P, flag, num_sms, stream, cs);
-        case 512: return dispatch_kt<9>(in, out, batch, P, flag, num_sms, stream, cs);
+        case 16: return dispatch_kt<4>(in, out, batch, P, flag, num_sms, stream);
+        case 32: return dispatch_kt<5>(in, out, batch, P, flag, num_sms, stream);
+        case 64: return dispatch_kt<6>(in, out, batch, P, flag, num_sms, stream);
+        case 128: return dispatch_kt<7>(in, out, batch, P, flag, num_sms, stream);
+        case 256: return dispatch_kt<8>(in, out, batch, P, flag, num_sms, stream);
+        case 512: return dispatch_kt<9>(in, out, batch, P, flag, num_sms, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -97,25 +97,9 @@ struct SmallPlanDev {
 
 /// Generic plans: power-of-two 16 <= n <= 512, K <= 128, A <= 128.  Folded
 /// plans: power-of-two 64 <= n <= 256 and at most 128 Cauchy columns.
-/// Chunk-level hand-off between copy engines and the fused kernel for the
-/// streamed host-buffer forward: the H2D stream sets ready[c] = epoch after
-/// chunk c of the input has landed (stream memory op); the kernel waits for it
-/// before its TMA load of any tile of chunk c, and bumps done[c] once a tile's
-/// output store has completed; the D2H stream waits for done[c] to reach the
-/// chunk's tile count.  ready == nullptr: plain device-resident launch.
-struct ChunkSync {
-    const unsigned* ready = nullptr;
-    unsigned* done = nullptr;
-    unsigned epoch = 0;
-    int tiles_per_chunk = 1;
-};
-
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);
 cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,
-                                int num_sms, cudaStream_t stream, const ChunkSync& cs = ChunkSync{});
-/// Rows per tile of the fused kernel that serves (n, streamed) launches; 0 when
-/// chunk-synchronised streaming is unavailable for this n.
-int fused_small_stream_tile_rows(std::size_t n);
+                                int num_sms, cudaStream_t stream);
 
 } // namespace dctp::dev

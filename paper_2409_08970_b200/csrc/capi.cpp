@@ -789,6 +789,22 @@ static void host_roundtrip(int device, std::size_t batch, std::size_t in_row, st
     for (cudaStream_t st : {hp.in, hp.comp, hp.out}) cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
 }
 
+/// The plan's orthonormal basis X (row-major n x n: slot s = sum_i X[i][s] x_i),
+/// column by column from the secular formula and one inverse DCT (the
+/// reference's assemble_unsigned_basis, cauchy.hpp:84-103, with the sigma signs).
+static void plan_basis(const dctp::host::Setup& st, double* x) {
+    const std::size_t n = st.n;
+    const dctp::host::Trig idct(dctp::host::Trig::Kind::idct2, n);
+    dctp::host::parallel_for(n, [&](std::size_t s) {
+        std::vector<double> buf(2 * n + idct.scratch_size() + 1);
+        double* y = buf.data();
+        double* col = y + n;
+        dctp::host::basis_coefficients(st, s, y);
+        idct.execute(y, col, col + n);
+        for (std::size_t i = 0; i < n; ++i) x[i * n + s] = st.sigma[s] < 0.0 ? -col[i] : col[i];
+    }, 4);
+}
+
 // --- ensemble ------------------------------------------------------------------
 
 struct dctp_ensemble {
@@ -801,6 +817,9 @@ struct dctp_ensemble {
     TwiddleOffsets tw64, tw32;
     std::size_t to = 0, from = 0, sign64 = 0, sign32 = 0, desc64 = 0, desc32 = 0;
     int n_emit = 0, max_rows = 0, max_cols = 0;
+    // fp32 dense route (n <= 256): G = [D^T | X_1 | ... | X_K], n x (K+1) n
+    std::size_t gmat32 = 0;
+    bool dense32 = false;
 
     ~dctp_ensemble() {
         if (blob) {
@@ -831,6 +850,18 @@ static void ensemble_forward(const dctp_ensemble* e, const T* in, T* out, std::s
     } else {
         emit.sign = at<double>(e->blob, e->sign64);
         tw = twiddles_at<double>(e->blob, e->tw64);
+    }
+    if constexpr (f32) {
+        if (e->dense32 &&
+            dctp::dev::sgemm_rows_supported(static_cast<int>(n), static_cast<int>(ld), static_cast<int>(n),
+                                            static_cast<int>(ld), ld, in, at<float>(e->blob, e->gmat32), out)) {
+            cuda_check(DCTP_LAUNCH("progressive_sgemm", s,
+                                   dctp::dev::sgemm_rows(in, static_cast<int>(n), at<float>(e->blob, e->gmat32),
+                                                         static_cast<int>(ld), out, ld, batch, static_cast<int>(ld),
+                                                         static_cast<int>(n), e->flag, s)),
+                       "progressive sgemm kernel");
+            return;
+        }
     }
     // Set 0 (the shared DCT, fast_transform.hpp:401-403) is written in place
     // and is the Cauchy stages' input; sets 1..K follow in each row.
@@ -905,17 +936,7 @@ int dctp_plan_slots(const dctp_plan* p, int* passthrough, int64_t* idx) {
 int dctp_plan_basis(const dctp_plan* p, double* x) {
     return guarded([&] {
         if (!p || !x) throw std::invalid_argument("dctp_plan_basis: null argument");
-        const auto& st = p->st;
-        const std::size_t n = st.n;
-        const dctp::host::Trig idct(dctp::host::Trig::Kind::idct2, n);
-        dctp::host::parallel_for(n, [&](std::size_t s) {
-            std::vector<double> buf(2 * n + idct.scratch_size() + 1);
-            double* y = buf.data();
-            double* col = y + n;
-            dctp::host::basis_coefficients(st, s, y);
-            idct.execute(y, col, col + n);
-            for (std::size_t i = 0; i < n; ++i) x[i * n + s] = st.sigma[s] < 0.0 ? -col[i] : col[i];
-        }, 4);
+        plan_basis(p->st, x);
     });
 }
 
@@ -1011,6 +1032,27 @@ int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is,
         }
         e->desc64 = blob.add(std::vector<dctp::dev::CauchyStage>(k));
         e->desc32 = blob.add(std::vector<dctp::dev::CauchyStage>(k));
+        // fp32 progressive as one SGEMM: every member is its full basis X_r and
+        // set 0 the orthonormal DCT-II matrix, so out = x * [D^T | X_1 | ... | X_K]
+        if (n <= 256 && n % 16 == 0 && device >= 0) {
+            const std::size_t cols = (k + 1) * n;
+            std::vector<float> g(n * cols);
+            const long double pi = 3.141592653589793238462643383279502884L;
+            for (std::size_t i = 0; i < n; ++i)
+                for (std::size_t j = 0; j < n; ++j) {
+                    const long double c = j == 0 ? std::sqrt(1.0L / n) : std::sqrt(2.0L / n);
+                    g[i * cols + j] = static_cast<float>(c * std::cos(pi * j * (2 * i + 1) / (2.0L * n)));
+                }
+            std::vector<double> xb(n * n);
+            for (std::size_t r = 0; r < k; ++r) {
+                plan_basis(e->members[r]->st, xb.data());
+                for (std::size_t i = 0; i < n; ++i)
+                    for (std::size_t sl = 0; sl < n; ++sl)
+                        g[i * cols + (r + 1) * n + sl] = static_cast<float>(xb[i * n + sl]);
+            }
+            e->gmat32 = blob.add(g);
+            e->dense32 = true;
+        }
         if (device < 0) {
             *out = e.release();
             return;

@@ -97,6 +97,13 @@ struct SmallPlanDev {
 
 /// Generic plans: power-of-two 16 <= n <= 512, K <= 128, A <= 128.  Folded
 /// plans: power-of-two 64 <= n <= 256 and at most 128 Cauchy columns.
+/// C[M x N] = A[M x K] * B[K x N], fp32 row-major (K % 16 == 0, N and the
+/// leading dimensions multiples of 4, 16-byte aligned); raises flag bit 0 if
+/// column 0 of a row is non-finite (the progressive DC coefficient).
+bool sgemm_rows_supported(int K, int N, int lda, int ldb, std::size_t ldc, const void* A, const void* B, const void* C);
+cudaError_t sgemm_rows(const float* A, int lda, const float* B, int ldb, float* C, std::size_t ldc, std::size_t M,
+                       int N, int K, int* flag, cudaStream_t stream);
+
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);
 cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,

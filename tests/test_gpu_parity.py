@@ -133,10 +133,13 @@ def test_progressive_full_batch_properties(P, torch, restatement):
     for r in (0, 1, 8, 16):
         nr = torch.linalg.vector_norm(y[:, r, :].double(), dim=1)
         assert float(((nr - ns).abs() / ns).max()) <= 1e-5
-    # set 0 is the plain orthonormal DCT-II
+    # set 0 is the plain orthonormal DCT-II (fp32: the dense route's rounding
+    # differs from the FFT kernel's, so compare norm-wise per signal)
     import paper_2409_08970_b200 as P_
 
-    assert float((y[:, 0, :] - P_.dct2(s)).abs().max()) == 0.0
+    d = P_.dct2(s)
+    err = (y[:, 0, :] - d).abs().amax(dim=1) / d.abs().amax(dim=1)
+    assert float(err.max()) <= 1e-5
 
 
 def test_reference_edge_cases(P, torch):

@@ -4,7 +4,7 @@
 //
 // Power-of-two n: Makhoul's reordering turns the length-n DCT into one
 // length-n/2 complex FFT of the packed real sequence, run in shared memory
-// (bit-reversed load, radix-2 stages, one CTA processes rows_per_cta signals
+// (bit-reversed load, radix-8 DIT passes, one CTA processes rows_per_cta signals
 // at once), followed by the real-split and the e^{-i pi k/2n} rotation.  The
 // epilogue stages the coefficients in shared memory and writes them with
 // coalesced row stores plus an optional scattered "emit" list (pass-through
@@ -22,32 +22,53 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kTileElems = 2048; // signal samples staged per CTA
 
-template <class T, bool Inverse>
-__device__ __forceinline__ void fft_radix2(cplx_t<T>* buf, int rows, int N, int logN,
-                                           const T* __restrict__ tw) {
-    const int halfN = N >> 1;
-    const int total = rows * halfN;
-    for (int s = 1; s <= logN; ++s) {
-        const int half = 1 << (s - 1);
-        const int stride_shift = logN - s; // twiddle index = j << stride_shift
-        for (int t = threadIdx.x; t < total; t += blockDim.x) {
-            const int row = t >> (logN - 1);
-            const int bidx = t & (halfN - 1);
-            const int j = bidx & (half - 1);
-            const int i0 = row * N + ((bidx >> (s - 1)) << s) + j;
-            const int i1 = i0 + half;
-            const int widx = j << stride_shift;
-            const T wr = __ldg(tw + 2 * widx);
-            const T wi = Inverse ? -__ldg(tw + 2 * widx + 1) : __ldg(tw + 2 * widx + 1);
-            const cplx_t<T> a = buf[i0];
-            const cplx_t<T> b = buf[i1];
-            const T tr = b.x * wr - b.y * wi;
-            const T ti = b.x * wi + b.y * wr;
-            buf[i1] = {a.x - tr, a.y - ti};
-            buf[i0] = {a.x + tr, a.y + ti};
+/// Q consecutive radix-2 DIT stages (s0+1 .. s0+Q) fused into one pass over
+/// groups of 2^Q elements held in registers: group (block, j) holds elements
+/// block*2^(s0+Q) + j + m*2^s0, m < 2^Q, of the bit-reversed sequence.  One
+/// shared-memory round trip and one barrier per Q stages instead of per stage.
+template <class T, bool Inverse, int Q>
+__device__ __forceinline__ void dit_group_pass(cplx_t<T>* buf, int rows, int N, int logN, int s0,
+                                               const T* __restrict__ tw) {
+    constexpr int G = 1 << Q;
+    const int h0 = 1 << s0;
+    const int groups = N >> Q;
+    for (int t = threadIdx.x; t < rows * groups; t += blockDim.x) {
+        const int row = t / groups, g = t - row * groups;
+        const int j = g & (h0 - 1), base = (g >> s0) * (h0 << Q) + j;
+        cplx_t<T>* e = buf + row * N + base;
+        cplx_t<T> v[G];
+#pragma unroll
+        for (int m = 0; m < G; ++m) v[m] = e[m * h0];
+#pragma unroll
+        for (int tt = 0; tt < Q; ++tt) {
+            const int span = 1 << tt;
+            const int shift = logN - (s0 + tt + 1); // twiddle step N / (2 * half)
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                if (m & span) continue;
+                const int widx = (j + (m & (span - 1)) * h0) << shift;
+                const T wr = __ldg(tw + 2 * widx);
+                const T wi = Inverse ? -__ldg(tw + 2 * widx + 1) : __ldg(tw + 2 * widx + 1);
+                const cplx_t<T> a = v[m], b = v[m + span];
+                const T br = b.x * wr - b.y * wi, bi = b.x * wi + b.y * wr;
+                v[m] = {a.x + br, a.y + bi};
+                v[m + span] = {a.x - br, a.y - bi};
+            }
         }
-        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < G; ++m) e[m * h0] = v[m];
     }
+    __syncthreads();
+}
+
+/// In-place DIT FFT of `rows` bit-reversed rows of N = 2^logN points, radix-8
+/// passes (radix-4/2 for the remainder).
+template <class T, bool Inverse>
+__device__ __forceinline__ void fft_dit(cplx_t<T>* buf, int rows, int N, int logN, const T* __restrict__ tw) {
+    int s0 = 0;
+    for (; s0 + 3 <= logN; s0 += 3) dit_group_pass<T, Inverse, 3>(buf, rows, N, logN, s0, tw);
+    if (logN - s0 == 2) dit_group_pass<T, Inverse, 2>(buf, rows, N, logN, s0, tw);
+    if (logN - s0 == 1) dit_group_pass<T, Inverse, 1>(buf, rows, N, logN, s0, tw);
 }
 
 template <class T>
@@ -76,7 +97,7 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
     if (bad) atomicOr(flag, 1);
     __syncthreads();
 
-    fft_radix2<T, false>(cbuf, rows, N, logN, tw.fft);
+    fft_dit<T, false>(cbuf, rows, N, logN, tw.fft);
 
     // Real split V_k = E_k - i e^{-2 pi i k/n} O_k, then Y_k = Re(e^{-i pi k/2n} V_k),
     // Y_{n-k} = -Im(...); orthonormal scale sqrt(2/n), DC gets 1/sqrt(2) more.
@@ -175,7 +196,7 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
     }
     __syncthreads();
 
-    fft_radix2<T, true>(cbuf, rows, N, logN, tw.fft);
+    fft_dit<T, true>(cbuf, rows, N, logN, tw.fft);
 
     for (int t = threadIdx.x; t < rows * n; t += blockDim.x) {
         const int r = t >> logn, j = t & (n - 1);

@@ -20,9 +20,9 @@
 namespace dctp::dev {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 32, LDS_ = BK + 4;
+constexpr int BM = 64, BN = 128, BK = 32, LDS_ = BK + 4;
 constexpr int kThreads = 256;
-constexpr int WM = 64, WN = 32;         // warp tile
+constexpr int WM = 32, WN = 32;         // warp tile
 constexpr int MF = WM / 8, NF = WN / 8; // fragments per warp
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
@@ -36,7 +36,7 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
 cauchy_dmma_kernel(const double* __restrict__ in, std::size_t ld_in, double* __restrict__ out, std::size_t ld_out,
                    const CauchyStage* __restrict__ stages, std::size_t batch, int* flag, int vec16) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -87,11 +87,20 @@ cauchy_dmma_kernel(const double* __restrict__ in, std::size_t ld_in, double* __r
     };
     // B generation: lane = k within the chunk (one contiguous 256-byte row store
     // per column, conflict-free), warp w fills columns w, w + 8, ..., w + 120.
+    // x and rscale of the chunk's rows are fetched one chunk ahead (their L2
+    // latency would otherwise stall every chunk's B generation)
+    auto fetch_xr = [&](int chunk, double& xr, double& sr) {
+        const int r = chunk * BK + lane;
+        xr = r < st.rows ? st.x[r] : 0.0;
+        sr = r < st.rows ? rscale[r] : 0.0;
+    };
+    double xr_next = 0.0, sr_next = 0.0;
+    fetch_xr(0, xr_next, sr_next);
     auto gen_b = [&](int chunk, int buf) {
         const int r = chunk * BK + lane;
         const bool rok = r < st.rows;
-        const double xr = rok ? st.x[r] : 0.0;
-        const double sr = rok ? rscale[r] : 0.0;
+        const double xr = xr_next, sr = sr_next;
+        if (chunk + 1 < nchunks) fetch_xr(chunk + 1, xr_next, sr_next);
         double* col = Bs + buf * BN * LDS_ + lane;
 #pragma unroll 4
         for (int cc = warp; cc < BN; cc += kThreads / 32) {
@@ -172,7 +181,7 @@ cudaError_t cauchy_rows_dmma(const double* in, std::size_t ld_in, double* out, s
                              const CauchyStage* stages_dev, int num_stages, int max_cols, std::size_t batch,
                              int* flag, cudaStream_t stream) {
     if (batch == 0 || num_stages == 0 || max_cols == 0) return cudaSuccess;
-    constexpr std::size_t smem = 4 * BM * LDS_ * sizeof(double) + BN * sizeof(double);
+    constexpr std::size_t smem = 2 * (BM + BN) * LDS_ * sizeof(double) + BN * sizeof(double);
     static const cudaError_t attr =
         cudaFuncSetAttribute(cauchy_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (attr != cudaSuccess) return attr;

@@ -279,3 +279,29 @@ def test_misaligned_device_views_take_the_generic_route(P, torch, restatement):
     out_big = torch.zeros(33 * cfg.n + 1, dtype=torch.float64, device="cuda")
     plan.forward(view, out=out_big[1:].view(33, cfg.n))
     assert O.parity(out_big[1:].view(33, cfg.n).cpu().numpy(), ref) <= TOL64
+
+
+def test_progressive_fp32_dense_route_edges(P, torch, restatement):
+    """The fp32 progressive SGEMM route (x * [D^T | X_1..X_K]) on ragged
+    batches (not multiples of the 128-row tile), against the fp64 generic
+    route; a misaligned output view falls back to the DCT + Cauchy kernels
+    with the same answer; a non-finite sample raises DomainError."""
+    ens = plan_for(P, 4)
+    cfg = O.config(4)
+    for batch in (1, 129, 1000):
+        s = restatement.fill_signals(O.mix_seed(O.SEED, cfg.n, batch), 0, cfg.n, batch)
+        y32 = ens.forward_all_batch(dev(torch, s, torch.float32)).double().cpu().numpy()
+        y64 = ens.forward_all_batch(dev(torch, s, torch.float64)).cpu().numpy()
+        for r in range(17):
+            assert O.parity(y32[:, r, :], y64[:, r, :]) <= TOL32, (batch, r)
+    s = restatement.fill_signals(O.mix_seed(O.SEED, cfg.n, 3), 0, cfg.n, 33)
+    ref = ens.forward_all_batch(dev(torch, s, torch.float32)).cpu().numpy()
+    big = torch.zeros(33 * 17 * cfg.n + 1, dtype=torch.float32, device="cuda")
+    ens.forward_all_batch(dev(torch, s, torch.float32), out=big[1:].view(33, 17, cfg.n))
+    got = big[1:].view(33, 17, cfg.n).cpu().numpy()
+    for r in range(17):
+        assert O.parity(got[:, r, :], ref[:, r, :]) <= TOL32
+    bad = dev(torch, s, torch.float32)
+    bad[5, 7] = float("inf")
+    with pytest.raises(P.DomainError):
+        ens.forward_all_batch(bad)

@@ -15,6 +15,8 @@
 // reuses each entry across BM signals, so the per-entry division costs
 // ~BN*BK/(BM*BN*BK/(TM*TN)) of the FMA work.
 #include <algorithm>
+#include <cstdint>
+#include <type_traits>
 
 #include "kernels/common.cuh"
 #include "kernels/launch.hpp"
@@ -98,14 +100,168 @@ cauchy_tile_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ 
     }
 }
 
+// ---- fp32: register-tiled SGEMM form ---------------------------------------------
+//
+// The fp32 Cauchy stage as a SIMT SGEMM (the tiling of kernels/sgemm.cu:
+// 128 x 128 x 16 tiles, 256 threads, 8 x 8 outputs each, double-buffered
+// shared memory): A rows come from global memory (float4 when the inputs are
+// already compacted, a gather through src[] otherwise) one chunk ahead in
+// registers; the B chunk, rscale[r] / (x_r - y_c), is generated straight into
+// the next shared buffer from fp64 gaps (one fp64 subtract, one MUFU rcp per
+// entry, amortised over 128 signals).  The 64 x 64 tile kernel above is
+// shared-memory bound at ~25% of FFMA peak; this one is FMA bound.
+constexpr int SBM = 128, SBN = 128, SBK = 16, SLDA = SBM + 4;
+
+__global__ void __launch_bounds__(kThreads, 2)
+cauchy_sgemm_kernel(const float* __restrict__ in, std::size_t ld_in, float* __restrict__ out, std::size_t ld_out,
+                    const CauchyStage* __restrict__ stages, std::size_t batch, int* flag, int vec4) {
+    __shared__ __align__(16) float As[2][SBK][SLDA];
+    __shared__ __align__(16) float Bs[2][SBK][SBN];
+    __shared__ double ys[SBN];
+    const CauchyStage st = stages[blockIdx.z];
+    const int c0 = blockIdx.y * SBN;
+    if (c0 >= st.cols) return;
+    const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * SBM;
+    const float* rscale = static_cast<const float*>(st.rscale);
+    const float* cscale = static_cast<const float*>(st.cscale);
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    for (int c = tid; c < SBN; c += kThreads) ys[c] = c0 + c < st.cols ? st.y[c0 + c] : 0.0;
+    const bool use_vec = st.src_contig && vec4;
+
+    float ra[8];
+    bool bad = false;
+    auto gload = [&](int r0) {
+        if (use_vec) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const std::size_t b = b0 + tid / 4 + 64 * i;
+                const int r = r0 + (tid % 4) * 4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (b < batch) {
+                    if (r + 3 < st.rows) {
+                        v = *reinterpret_cast<const float4*>(in + b * ld_in + r);
+                    } else {
+                        const float* p = in + b * ld_in;
+                        v.x = r < st.rows ? p[r] : 0.f;
+                        v.y = r + 1 < st.rows ? p[r + 1] : 0.f;
+                        v.z = r + 2 < st.rows ? p[r + 2] : 0.f;
+                    }
+                }
+                ra[4 * i + 0] = v.x;
+                ra[4 * i + 1] = v.y;
+                ra[4 * i + 2] = v.z;
+                ra[4 * i + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int e = tid + kThreads * i, kk = e % SBK, bb = e / SBK;
+                const int r = r0 + kk;
+                const std::size_t b = b0 + bb;
+                ra[i] = (r < st.rows && b < batch) ? in[b * ld_in + st.src[r]] : 0.f;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) bad |= !finite_val(ra[i]);
+    };
+    auto sstore_a = [&](int buf) {
+        if (use_vec) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int row = tid / 4 + 64 * i, kq = (tid % 4) * 4;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) As[buf][kq + j][row] = ra[4 * i + j];
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int e = tid + kThreads * i;
+                As[buf][e % SBK][e / SBK] = ra[i];
+            }
+        }
+    };
+    auto gen_b = [&](int r0, int buf) {
+#pragma unroll
+        for (int i = 0; i < (SBK * SBN) / kThreads; ++i) {
+            const int e = tid + kThreads * i, kk = e / SBN, cc = e % SBN;
+            const int r = r0 + kk;
+            Bs[buf][kk][cc] = (r < st.rows && c0 + cc < st.cols)
+                                  ? rscale[r] * __frcp_rn(static_cast<float>(st.x[r] - ys[cc]))
+                                  : 0.f;
+        }
+    };
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+    __syncthreads(); // ys
+    gload(0);
+    sstore_a(0);
+    gen_b(0, 0);
+    __syncthreads();
+    for (int r0 = 0; r0 < st.rows; r0 += SBK) {
+        const int buf = (r0 / SBK) & 1;
+        const bool more = r0 + SBK < st.rows;
+        if (more) gload(r0 + SBK);
+#pragma unroll
+        for (int kk = 0; kk < SBK; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
+            const float4 q0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+            const float4 q1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        if (more) {
+            sstore_a(buf ^ 1);
+            gen_b(r0 + SBK, buf ^ 1);
+        }
+        __syncthreads();
+    }
+    if (bad) atomicOr(flag, 1);
+
+    int dst[8];
+    float cs[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int c = c0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+        dst[j] = c < st.cols ? st.dst[c] : -1;
+        cs[j] = c < st.cols ? cscale[c] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const std::size_t b = b0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+        if (b >= batch) continue;
+        float* orow = out + b * ld_out + st.out_offset;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (dst[j] >= 0) orow[dst[j]] = cs[j] * acc[i][j];
+    }
+}
+
 } // namespace
 
 template <class T>
 cudaError_t cauchy_rows(const T* in, std::size_t ld_in, T* out, std::size_t ld_out,
                         const CauchyStage* stages_dev, int num_stages, int max_rows, int max_cols,
                         std::size_t batch, int* flag, cudaStream_t stream) {
-    (void)max_rows;
     if (batch == 0 || num_stages == 0 || max_cols == 0) return cudaSuccess;
+    if constexpr (std::is_same_v<T, float>) {
+        if (max_rows >= 64) {
+            dim3 grid(static_cast<unsigned>((batch + SBM - 1) / SBM), static_cast<unsigned>((max_cols + SBN - 1) / SBN),
+                      static_cast<unsigned>(num_stages));
+            const int vec4 = reinterpret_cast<std::uintptr_t>(in) % 16 == 0 && ld_in % 4 == 0;
+            cauchy_sgemm_kernel<<<grid, kThreads, 0, stream>>>(in, ld_in, out, ld_out, stages_dev, batch, flag, vec4);
+            return cudaGetLastError();
+        }
+    }
     constexpr int BM = 64, BN = 64;
     dim3 grid(static_cast<unsigned>((batch + BM - 1) / BM), static_cast<unsigned>((max_cols + BN - 1) / BN),
               static_cast<unsigned>(num_stages));

@@ -85,14 +85,27 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
 
     // Load with Makhoul's permutation v = (x0, x2, ..., x3, x1), packed as
     // w_m = v_{2m} + i v_{2m+1}, stored bit-reversed for the DIT stages.
+    // eight independent loads in flight per thread before any use (a load-use
+    // chain per element left the kernel waiting on HBM latency)
     bool bad = false;
-    for (int t = threadIdx.x; t < rows * n; t += blockDim.x) {
-        const int r = t >> logn, j = t & (n - 1);
-        const T x = in[(b0 + r) * ld_in + j];
-        bad |= !finite_val(x);
-        const int p = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
-        T* slot = reinterpret_cast<T*>(&cbuf[r * N + bit_reverse(static_cast<unsigned>(p >> 1), logN)]);
-        slot[p & 1] = x;
+    constexpr int U = 8;
+    for (int t0 = threadIdx.x; t0 < rows * n; t0 += U * kThreads) {
+        T xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + u * kThreads;
+            xv[u] = t < rows * n ? in[(b0 + (t >> logn)) * ld_in + (t & (n - 1))] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + u * kThreads;
+            if (t >= rows * n) break;
+            const int r = t >> logn, j = t & (n - 1);
+            bad |= !finite_val(xv[u]);
+            const int p = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
+            T* slot = reinterpret_cast<T*>(&cbuf[r * N + bit_reverse(static_cast<unsigned>(p >> 1), logN)]);
+            slot[p & 1] = xv[u];
+        }
     }
     if (bad) atomicOr(flag, 1);
     __syncthreads();
@@ -158,17 +171,40 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
     // X_k = sqrt(2/n) c_k d_k, with X_0 doubled (the REDFT01 convention).
     const T scale = static_cast<T>(sqrt(2.0 / n));
     const T dc_scale = static_cast<T>(2.0 / sqrt(static_cast<double>(n)));
-    for (int t = threadIdx.x; t < rows * n; t += blockDim.x) {
-        const int r = t >> logn, k = t & (n - 1);
-        sh[t] = d[(b0 + r) * ld_d + k];
+    constexpr int U = 8; // independent loads in flight per thread
+    for (int t0 = threadIdx.x; t0 < rows * n; t0 += U * kThreads) {
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + u * kThreads;
+            v[u] = t < rows * n ? d[(b0 + (t >> logn)) * ld_d + (t & (n - 1))] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (t0 + u * kThreads < rows * n) sh[t0 + u * kThreads] = v[u];
     }
     __syncthreads();
     bool bad = false;
-    for (int t = threadIdx.x; t < rows * emit.count; t += blockDim.x) {
-        const int r = t / emit.count, e = t - r * emit.count;
-        const T v = p[(b0 + r) * ld_p + emit.from[e]];
-        bad |= !finite_val(v);
-        sh[r * n + emit.to[e]] = emit.sign[e] * v;
+    for (int t0 = threadIdx.x; t0 < rows * emit.count; t0 += U * kThreads) {
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + u * kThreads;
+            if (t < rows * emit.count) {
+                const int r = t / emit.count, e = t - r * emit.count;
+                v[u] = p[(b0 + r) * ld_p + emit.from[e]];
+            } else {
+                v[u] = T(0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + u * kThreads;
+            if (t >= rows * emit.count) break;
+            const int r = t / emit.count, e = t - r * emit.count;
+            bad |= !finite_val(v[u]);
+            sh[r * n + emit.to[e]] = emit.sign[e] * v[u];
+        }
     }
     if (bad) atomicOr(flag, 1);
     __syncthreads();

@@ -575,7 +575,7 @@ __device__ __forceinline__ void fetch_tile_index(unsigned long long* ctr, long l
         : "memory");
 }
 
-template <int LOGN, int KT, int TS, bool FOLD>
+template <int LOGN, int KT, int TS, bool FOLD, bool PP>
 __global__ void __launch_bounds__(kLockThreads, 1)
 fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, std::size_t batch, SmallPlanDev P,
                       int* flag, unsigned long long* tile_counter) {
@@ -584,6 +584,10 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
     constexpr int SPW = TS / kComputeWarps; // rows per warp in the DCT phase
     constexpr int kS = lock_stages<FOLD>();
     static_assert(SPW >= 1 && TS % kComputeWarps == 0, "one or more rows per warp");
+    static_assert(!PP || (SPW == 1 && kS >= 4), "ping-pong: one row per warp, four stages");
+    // the thread that owns the tile ring (claims, stores, scheduler counter):
+    // in ping-pong mode one of the warps that start each step with the DCT
+    constexpr int kDuty = PP ? 32 * (kComputeWarps / 2) : 0;
     using PS = Passes<NC>;
     extern __shared__ __align__(128) unsigned char smem[];
     double* xs = reinterpret_cast<double*>(smem);              // kS x TILE: input, then output rows
@@ -667,38 +671,23 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
         }
     };
     long long next_tile = 0;
-    if (tid == 0)
+    if (tid == kDuty)
         for (int q = 0; q < kS; ++q) claim(q, static_cast<long long>(blockIdx.x) + q * static_cast<long long>(gridDim.x));
-    fetch_tile_index(tile_counter, next_tile, tid);
+    fetch_tile_index(tile_counter, next_tile, tid ^ kDuty);
     const double scale = sqrt(2.0 / L);
     const double dc_scale = 1.0 / sqrt(static_cast<double>(L));
     const double y_n = rt[NC].x * scale;
     bool bad = false;
-    // DCTP_DEBUG_MODE & 4: phase cycles seen by thread 32 (slots 0-5) and
-    // thread 0's store/claim duty (slot 6), kept in shared memory
-    const bool timing = P.timers != nullptr && (tid == 32 || tid == 0);
-    long long tmark = clock64();
-#define LT(i)                                                        \
-    if (timing) {                                                    \
-        const long long now_ = clock64();                            \
-        if (tid == 32 || (i) == 6) tacc[i] += static_cast<unsigned long long>(now_ - tmark); \
-        tmark = now_;                                                \
-    }
-    for (int it = 0;; ++it) {
-        const int q = it % kS;
-        LT(5);
-        ptx::mbar_wait(&xfull[q], (it / kS) & 1);
-        LT(0);
-        const long long tile = sched[q];
-        if (tile >= static_cast<long long>(ntiles)) break;
+    // phase A for this warp's SPW rows of the tile in stage q: DCT (FFT, or the
+    // fold's u and half-length DCT) -> Cauchy A tile `abuf`, pass-through
+    // slots in place in the stage's rows
+    auto dct_rows = [&](int q, long long tile, double* abuf) {
         const int valid = rows_of(tile) - warp * SPW;
         double* x = xs + q * TILE + warp * SPW * n; // this warp's rows: input, then output
         double2* a0 = s0 + warp * SPW * NC;
         double2* a1 = s1 + warp * SPW * NC;
-        double* abuf = atile + (it & 1) * TS * LDA;
         double* ab = abuf + warp * SPW * LDA;
-        // ---- phase A: DCT of this warp's rows --------------------------------------
-        if ((P.debug & 1) == 0) {
+        {
             const double* yrow = x;
             if constexpr (FOLD) {
                 double* ys = reinterpret_cast<double*>(a1);
@@ -758,6 +747,105 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
                 for (int r = 0; r < SPW; ++r) x[r * n + slotq] = coef * S[r * L + src];
             }
         }
+    };
+    // DCTP_DEBUG_MODE & 4: phase cycles seen by thread 32 (slots 0-5) and
+    // thread 0's store/claim duty (slot 6), kept in shared memory
+    const bool timing = P.timers != nullptr && (tid == 32 || tid == 0);
+    long long tmark = clock64();
+#define LT(i)                                                        \
+    if (timing) {                                                    \
+        const long long now_ = clock64();                            \
+        if (tid == 32 || (i) == 6) tacc[i] += static_cast<unsigned long long>(now_ - tmark); \
+        tmark = now_;                                                \
+    }
+    if constexpr (PP) {
+        // Ping-pong: step `it` multiplies tile it-1 and transforms tile it.
+        // Warps 0-7 run their DMMA N-tile first and then the DCT of their row,
+        // warps 8-15 the other way round, so every SMSP has one warp on the
+        // fp64 tensor pipe and one on the shared-memory FFT at any time; one
+        // CTA barrier per step.  The A tile is double-buffered by step parity.
+        auto mma_tile = [&](int qp, const double* abuf) {
+            const double* arow = abuf + (lane >> 2) * LDA + (lane & 3);
+            double acc[MT][2];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt) {
+                double a[MT];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) a[mt] = arow[mt * 8 * LDA + kt * 4];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) ptx::dmma_8x8x4(acc[mt][0], acc[mt][1], a[mt], bf[kt]);
+            }
+            double* obt = xs + qp * TILE;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const int r = mt * 8 + (lane >> 2);
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (slot[e] >= 0) obt[r * n + slot[e]] = acc[mt][e];
+            }
+        };
+        ptx::mbar_wait(&xfull[0], 0);
+        dct_rows(0, sched[0], atile); // grid <= tiles: every CTA owns tile sched[0]
+        __syncthreads();
+        for (int it = 1;; ++it) {
+            const int q = it % kS, qp = (it - 1) % kS;
+            const long long tprev = sched[qp];
+            bool live = false;
+            auto dct_step = [&] {
+                ptx::mbar_wait(&xfull[q], (it / kS) & 1);
+                const long long tile = sched[q];
+                live = tile < static_cast<long long>(ntiles);
+                if (live) dct_rows(q, tile, atile + (it & 1) * TS * LDA);
+            };
+            // DCTP_DEBUG_MODE & 4: lane 0 of warps 0 / 8 time part 1, part 2 and the
+            // barrier wait (timer slots 0-2 / 3-5)
+            const bool ptime = P.timers != nullptr && (tid == 0 || tid == kDuty);
+            const long long t0 = ptime ? clock64() : 0;
+            long long t1 = 0;
+            if (warp < kComputeWarps / 2) {
+                mma_tile(qp, atile + ((it - 1) & 1) * TS * LDA);
+                if (ptime) t1 = clock64();
+                dct_step();
+            } else {
+                dct_step();
+                if (ptime) t1 = clock64();
+                mma_tile(qp, atile + ((it - 1) & 1) * TS * LDA);
+            }
+            const long long t2 = ptime ? clock64() : 0;
+            ptx::fence_proxy_async(); // output writes -> the TMA store below
+            __syncthreads();
+            if (ptime) {
+                const int b = tid == 0 ? 0 : 3;
+                atomicAdd(P.timers + b, static_cast<unsigned long long>(t1 - t0));
+                atomicAdd(P.timers + b + 1, static_cast<unsigned long long>(t2 - t1));
+                atomicAdd(P.timers + b + 2, static_cast<unsigned long long>(clock64() - t2));
+            }
+            if (tid == kDuty) {
+                ptx::bulk_store(out + tprev * TS * n, xs + qp * TILE,
+                                static_cast<uint32_t>(rows_of(tprev) * n * sizeof(double)));
+                ptx::bulk_commit();
+                if (it >= 2) {
+                    // refill the stage of tile it-2: its store (issued a step ago) has been read
+                    ptx::bulk_wait_read_pending1();
+                    claim((it - 2) % kS, next_tile + kS * static_cast<long long>(gridDim.x));
+                }
+            }
+            if (it >= 2) fetch_tile_index(tile_counter, next_tile, tid ^ kDuty);
+            if (!live) break;
+        }
+    } else {
+    for (int it = 0;; ++it) {
+        const int q = it % kS;
+        LT(5);
+        ptx::mbar_wait(&xfull[q], (it / kS) & 1);
+        LT(0);
+        const long long tile = sched[q];
+        if (tile >= static_cast<long long>(ntiles)) break;
+        double* abuf = atile + (it & 1) * TS * LDA;
+        // ---- phase A: DCT of this warp's rows --------------------------------------
+        if ((P.debug & 1) == 0) dct_rows(q, tile, abuf);
         LT(1);
         __syncthreads(); // A tile (and in-place pass-through rows) complete
         LT(2);
@@ -789,7 +877,7 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
         ptx::fence_proxy_async(); // output writes -> the TMA store below
         __syncthreads();
         LT(4);
-        if (tid == 0) {
+        if (tid == kDuty) {
             ptx::bulk_store(out + tile * TS * n, xs + q * TILE, static_cast<uint32_t>(rows_of(tile) * n * sizeof(double)));
             ptx::bulk_commit();
             if (it >= 1) {
@@ -799,7 +887,8 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
             }
         }
         LT(6);
-        if (it >= 1) fetch_tile_index(tile_counter, next_tile, tid); // used next iteration
+        if (it >= 1) fetch_tile_index(tile_counter, next_tile, tid ^ kDuty); // used next iteration
+    }
     }
 #undef LT
     if (timing) {
@@ -808,7 +897,7 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
         if (tid == 0) atomicAdd(P.timers + 6, tacc[6]);
     }
     if (bad) atomicOr(flag, 1);
-    if (tid == 0) {
+    if (tid == kDuty) {
         ptx::bulk_wait_all();
         release_counter(tile_counter, next_tile);
     }
@@ -862,7 +951,14 @@ cudaError_t launch_small(const double* in, double* out, std::size_t batch, const
     if constexpr (TS >= kComputeWarps) {
         static_assert(lockstep_smem_bytes<LOGN, KT, TS, FOLD>() <= 227 * 1024, "lockstep kernel exceeds shared memory");
         if (lockstep && NTW == 1) {
-            kern = fused_lockstep_kernel<LOGN, KT, TS, FOLD>;
+            kern = fused_lockstep_kernel<LOGN, KT, TS, FOLD, false>;
+            if constexpr (FOLD && TS / kComputeWarps == 1 && lock_stages<FOLD>() >= 4) {
+                static const bool pp = [] {
+                    const char* e = std::getenv("DCTP_FUSED_VARIANT");
+                    return !(e && std::string(e) == "lockstep");
+                }();
+                if (pp) kern = fused_lockstep_kernel<LOGN, KT, TS, FOLD, true>;
+            }
             smem = lockstep_smem_bytes<LOGN, KT, TS, FOLD>();
             threads = kLockThreads;
         }

@@ -557,7 +557,7 @@ constexpr std::size_t lockstep_smem_bytes() {
     constexpr int tw = Passes<NC>::TWIDDLES > 0 ? Passes<NC>::TWIDDLES : 1;
     constexpr int S = lock_stages<FOLD>();
     return S * TILE * sizeof(double) + 2 * TS * NC * sizeof(double2) + 2 * TS * LDA * sizeof(double) +
-           (tw + 3 * NC + 2) * sizeof(double2) + n * sizeof(double) + (4 * KT + 2 * n) * sizeof(int) +
+           (tw + 3 * NC + 2) * sizeof(double2) + L * sizeof(double) + L * sizeof(int) +
            S * sizeof(uint64_t) + S * sizeof(long long) + 8 * sizeof(unsigned long long);
 }
 
@@ -574,6 +574,8 @@ __device__ __forceinline__ void fetch_tile_index(unsigned long long* ctr, long l
         : "l"(ctr), "r"(tid)
         : "memory");
 }
+
+constexpr int kNoRoute = -(1 << 30);
 
 template <int LOGN, int KT, int TS, bool FOLD, bool PP>
 __global__ void __launch_bounds__(kLockThreads, 1)
@@ -598,11 +600,11 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
     double2* sp = ptw + (PS::TWIDDLES > 0 ? PS::TWIDDLES : 1);
     double2* rt = sp + NC;
     double2* rt2 = rt + NC + 1;
-    double* pass_coef = reinterpret_cast<double*>(rt2 + NC + 1);
-    int* kept_idx = reinterpret_cast<int*>(pass_coef + n);
-    int* pass_src = kept_idx + 4 * KT;
-    int* pass_dst = pass_src + n;
-    uint64_t* xfull = reinterpret_cast<uint64_t*>(pass_dst + n);   // [kS] tile landed (tx bytes)
+    // route of DCT coefficient k < L: >= 0 -> output slot (pass-through, times
+    // rcoef[k]); -(c+1) -> column c of the Cauchy A tile (kept); kNoRoute -> none
+    double* rcoef = reinterpret_cast<double*>(rt2 + NC + 1);
+    int* route = reinterpret_cast<int*>(rcoef + L);
+    uint64_t* xfull = reinterpret_cast<uint64_t*>(route + L);   // [kS] tile landed (tx bytes)
     long long* sched = reinterpret_cast<long long*>(xfull + kS);   // [kS] tile in stage q
     unsigned long long* tacc = reinterpret_cast<unsigned long long*>(sched + kS); // [8] debug phase cycles
 
@@ -625,13 +627,18 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
             rt[i] = r;
             rt2[i] = make_double2(r.x * h, r.y * h);
         }
-        for (int i = tid; i < 4 * KT; i += kLockThreads) kept_idx[i] = i < P.K ? P.kept_idx[i] : -1;
-        for (int i = tid; i < n_pass; i += kLockThreads) {
-            pass_src[i] = P.pass_src[i];
-            pass_dst[i] = P.pass_slot[i];
-            pass_coef[i] = P.pass_coef[i];
+        for (int i = tid; i < L; i += kLockThreads) {
+            route[i] = kNoRoute;
+            rcoef[i] = 0.0;
         }
         for (int i = tid; i < 2 * TS * LDA; i += kLockThreads) atile[i] = 0.0;
+        __syncthreads();
+        for (int i = tid; i < n_pass; i += kLockThreads) {
+            route[P.pass_src[i]] = P.pass_slot[i];
+            rcoef[P.pass_src[i]] = P.pass_coef[i];
+        }
+        if constexpr (!FOLD)
+            for (int i = tid; i < P.K; i += kLockThreads) route[P.kept_idx[i]] = -(i + 1);
         if (tid == 0) {
             for (int q = 0; q < kS; ++q) ptx::mbar_init(&xfull[q], 1);
             ptx::fence_mbar_init();
@@ -704,14 +711,21 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
             stockham_first<NC, SPW>(yrow, a0, lane, valid, bad);
             __syncwarp();
             double2* F = fft_passes<NC, SPW, 1>(a0, a1, ptw, lane);
-            double* S = reinterpret_cast<double*>(F == a0 ? a1 : a0);
+            // split + rotation, each coefficient routed straight to its output
+            // slot (pass-through, in place: the input rows are consumed) or
+            // its A-tile column (kept)
+            auto emit = [&](int r, int k, double v) {
+                const int rt_ = route[k];
+                if (rt_ >= 0) x[r * n + rt_] = rcoef[k] * v;
+                else if (rt_ != kNoRoute) ab[r * LDA + (-rt_ - 1)] = v;
+            };
             lane_loop<SPW * (NC / 2)>(lane, [&](int t) {
                 const int r = t / (NC / 2), k = t % (NC / 2) + 1;
                 const double2* row = F + r * NC;
-                double* o = S + r * L;
                 const double2 wk = row[k], wc = row[NC - k];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
+                    if (h == 1 && k == NC / 2) break; // self-paired
                     const int kk = h == 0 ? k : NC - k;
                     const double2 a = h == 0 ? wk : wc, c = h == 0 ? wc : wk;
                     const double sr = a.x + c.x, si = a.y - c.y;
@@ -720,31 +734,16 @@ fused_lockstep_kernel(const double* __restrict__ in, double* __restrict__ out, s
                     const double qr = s2.x * dr - s2.y * di, qi = s2.x * di + s2.y * dr;
                     const double vr = sr + qi, vi = si - qr;
                     const double2 c2 = rt2[kk];
-                    o[kk] = vr * c2.x - vi * c2.y;
-                    o[L - kk] = -(vr * c2.y + vi * c2.x);
+                    emit(r, kk, vr * c2.x - vi * c2.y);
+                    emit(r, L - kk, -(vr * c2.y + vi * c2.x));
                 }
             });
             if (lane < SPW) {
                 const double2 w0 = F[lane * NC];
                 const double dc = (w0.x + w0.y) * dc_scale;
-                S[lane * L] = dc;
-                S[lane * L + NC] = (w0.x - w0.y) * y_n;
-                if (lane < valid) bad |= !isfinite(dc); // see fused_small_fwd_kernel
-            }
-            __syncwarp();
-            if constexpr (!FOLD) {
-                lane_loop<SPW * 4 * KT>(lane, [&](int t) {
-                    const int r = t / (4 * KT), k = t % (4 * KT);
-                    const int j = kept_idx[k];
-                    if (j >= 0) ab[r * LDA + k] = S[r * L + j];
-                });
-            }
-            // the input rows are consumed: pass-through slots land in place
-            for (int qq = lane; qq < n_pass; qq += 32) {
-                const int slotq = pass_dst[qq], src = pass_src[qq];
-                const double coef = pass_coef[qq];
-#pragma unroll
-                for (int r = 0; r < SPW; ++r) x[r * n + slotq] = coef * S[r * L + src];
+                emit(lane, 0, dc);
+                emit(lane, NC, (w0.x - w0.y) * y_n);
+                if (lane < valid) bad |= !isfinite(dc); // DC = sum of the row: any non-finite input shows
             }
         }
     };

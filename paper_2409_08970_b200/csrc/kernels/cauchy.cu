@@ -191,11 +191,11 @@ cauchy_sgemm_kernel(const float* __restrict__ in, std::size_t ld_in, float* __re
         }
     };
 
-    float acc[8][8];
+    unsigned long long acc2[8][4]; // columns 2p, 2p+1 of row i, packed for FFMA2 (see sgemm.cu)
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        for (int p = 0; p < 4; ++p) acc2[i][p] = 0ull;
 
     __syncthreads(); // ys
     gload(0);
@@ -213,11 +213,14 @@ cauchy_sgemm_kernel(const float* __restrict__ in, std::size_t ld_in, float* __re
             const float4 q0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
             const float4 q1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
             const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float b[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+            const unsigned long long b2[4] = {ptx::pack2(q0.x, q0.y), ptx::pack2(q0.z, q0.w), ptx::pack2(q1.x, q1.y),
+                                              ptx::pack2(q1.z, q1.w)};
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < 8; ++i) {
+                const unsigned long long aa = ptx::pack2(a[i], a[i]);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                for (int p = 0; p < 4; ++p) ptx::ffma2(acc2[i][p], aa, b2[p]);
+            }
         }
         if (more) {
             sstore_a(buf ^ 1);
@@ -227,6 +230,11 @@ cauchy_sgemm_kernel(const float* __restrict__ in, std::size_t ld_in, float* __re
     }
     if (bad) atomicOr(flag, 1);
 
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) ptx::unpack2(acc2[i][p], acc[i][2 * p], acc[i][2 * p + 1]);
     int dst[8];
     float cs[8];
 #pragma unroll

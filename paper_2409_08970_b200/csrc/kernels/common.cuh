@@ -122,6 +122,20 @@ __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
+/// Packed fp32 FMA (FFMA2, sm_100): d.lo += a.lo * b.lo, d.hi += a.hi * b.hi in
+/// one issue slot; operands are two floats in one 64-bit register pair.
+__device__ __forceinline__ void ffma2(unsigned long long& d, unsigned long long a, unsigned long long b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void unpack2(unsigned long long v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+
 /// D(8x8) += A(8x4, row) * B(4x8, col) in fp64 on the tensor cores (DMMA).
 /// Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
 /// d = {D[lane/4][2*(lane%4)], D[lane/4][2*(lane%4)+1]}.

@@ -60,11 +60,13 @@ sgemm_rows_kernel(const float* __restrict__ A, int lda, const float* __restrict_
         }
     };
 
-    float acc[8][8];
+    // acc2[i][p] holds columns 2p, 2p+1 of row i: packed FFMA2 halves the
+    // issue slots of the FMA stream (the kernel was issue-bound)
+    unsigned long long acc2[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        for (int p = 0; p < 4; ++p) acc2[i][p] = 0ull;
 
     gload(0);
     sstore(0);
@@ -80,16 +82,24 @@ sgemm_rows_kernel(const float* __restrict__ A, int lda, const float* __restrict_
             const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
             const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
             const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            const unsigned long long b2[4] = {ptx::pack2(b0.x, b0.y), ptx::pack2(b0.z, b0.w), ptx::pack2(b1.x, b1.y),
+                                              ptx::pack2(b1.z, b1.w)};
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < 8; ++i) {
+                const unsigned long long aa = ptx::pack2(a[i], a[i]);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                for (int p = 0; p < 4; ++p) ptx::ffma2(acc2[i][p], aa, b2[p]);
+            }
         }
         if (more) sstore(buf ^ 1); // that buffer was last read before the previous barrier
         __syncthreads();
     }
 
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) ptx::unpack2(acc2[i][p], acc[i][2 * p], acc[i][2 * p + 1]);
     bool bad = false;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {

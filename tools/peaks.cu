@@ -20,6 +20,31 @@ __global__ void fma_loop(T* out, int iters, T a, T b) {
     if (s == static_cast<T>(-1.2345)) out[threadIdx.x] = s;
 }
 
+// packed fp32 FMA (FFMA2, sm_100): two FMAs per lane per instruction
+__global__ void ffma2_loop(float* out, int iters) {
+    unsigned long long acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const float v = static_cast<float>(threadIdx.x + i);
+        asm("mov.b64 %0, {%1, %2};" : "=l"(acc[i]) : "f"(v), "f"(v + 1.0f));
+    }
+    unsigned long long a, b;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(1.0000001f), "f"(1.0000002f));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(1e-7f), "f"(2e-7f));
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(acc[i]) : "l"(a), "l"(b));
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        float lo, hi;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[i]));
+        s += lo + hi;
+    }
+    if (s == -1.2345f) out[threadIdx.x] = s;
+}
+
 // m8n8k4 f64: 256 FMA per warp instruction
 __global__ void dmma_m8n8k4(double* out, int iters) {
     double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
@@ -92,6 +117,8 @@ int main() {
     const double fma32 =
         time_ms([&] { fma_loop<float, 8><<<blocks, threads>>>((float*)out, iters, 1.0000001f, 1e-7f); });
     const double tf32 = 2.0 * blocks * threads * 8.0 * iters / (fma32 * 1e-3) / 1e12;
+    const double f2 = time_ms([&] { ffma2_loop<<<blocks, threads>>>((float*)out, iters); });
+    const double tf32x2 = 2.0 * 2.0 * blocks * threads * 8.0 * iters / (f2 * 1e-3) / 1e12;
     const int diters = 1024;
     const double d1 = time_ms([&] { dmma_m8n8k4<<<blocks, threads>>>(out, diters); });
     const double tdm1 = 2.0 * 256.0 * 8 * (blocks * threads / 32.0) * diters / (d1 * 1e-3) / 1e12;
@@ -99,7 +126,8 @@ int main() {
     const double tdm2 = 2.0 * 2048.0 * 4 * (blocks * threads / 32.0) * (diters / 4) / (d2 * 1e-3) / 1e12;
     cudaError_t e = cudaDeviceSynchronize();
     printf("{\"sms\": %d, \"clock_mhz_attr\": %d, \"fp64_fma_tflops\": %.2f, \"fp32_fma_tflops\": %.2f, "
-           "\"dmma_m8n8k4_tflops\": %.2f, \"dmma_m16n8k16_tflops\": %.2f, \"status\": \"%s\"}\n",
-           sms, clk / 1000, tf64, tf32, tdm1, tdm2, cudaGetErrorString(e));
+           "\"fp32_ffma2_tflops\": %.2f, \"dmma_m8n8k4_tflops\": %.2f, \"dmma_m16n8k16_tflops\": %.2f, "
+           "\"status\": \"%s\"}\n",
+           sms, clk / 1000, tf64, tf32, tf32x2, tdm1, tdm2, cudaGetErrorString(e));
     return e == cudaSuccess ? 0 : 1;
 }

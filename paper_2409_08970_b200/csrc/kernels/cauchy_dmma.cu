@@ -8,9 +8,12 @@
 // right before using it, so HBM traffic is only the signal
 // rows in and the coefficients out (C5's materialised T would be 512 MB and
 // would be re-read once per row tile).  A rows are gathered with cp.async
-// (LDGSTS, 8-byte elements) one chunk ahead.  CTA tile 128 x 128, 8 warps of
-// 64 x 32, m8n8k4 DMMA fragments loaded conflict-free from rows padded to 36
-// doubles.  The division per generated entry is amortised over 128 signals.
+// (LDGSTS, 8-byte elements) one chunk ahead.  CTA tile 64 x 128 (two CTAs per
+// SM; a 128-row tile left C3's 512 CTAs at 3.5 waves), 8 warps of 32 x 32,
+// m8n8k4 DMMA fragments loaded from rows padded to 36 doubles.  The division
+// per generated entry is amortised over 64 signals.  (m16n8k16 fragments,
+// tools/mma16_layout.cu, issue 8x fewer DMMA instructions but measured no
+// faster: the kernel is not issue-bound.)
 #include <algorithm>
 #include <cstdint>
 

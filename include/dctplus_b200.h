@@ -107,12 +107,11 @@ int dctp_inverse_host_f64(const dctp_plan* plan, const double* h_in, double* h_o
 int dctp_forward_host_f32(const dctp_plan* plan, const float* h_in, float* h_out, size_t batch);
 int dctp_inverse_host_f32(const dctp_plan* plan, const float* h_in, float* h_out, size_t batch);
 
-/* --- PrunedEnsemblePlan, c_p = n (fast_transform.hpp:338-454) ------------- */
+/* --- PrunedEnsemblePlan (fast_transform.hpp:338-454) ----------------------- */
 
-/* PrunedEnsemblePlan(n, updates, cp, threshold, epsilon) (:343).  The K
- * updates are given as parallel arrays; vs holds K*n doubles for
- * DCTP_GENERAL members (may be NULL otherwise).  Only cp == n is supported
- * on the GPU path (the progressive mode of the north star). */
+/* PrunedEnsemblePlan(n, updates, cp, threshold, epsilon) (:343), 1 <= cp <= n.
+ * The K updates are given as parallel arrays; vs holds K*n doubles for
+ * DCTP_GENERAL members (may be NULL otherwise). */
 int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is, const size_t* js,
                          const double* rhos, const double* vs, size_t cp, double threshold,
                          double epsilon, int device, dctp_ensemble** out);
@@ -121,12 +120,26 @@ int dctp_ensemble_destroy(dctp_ensemble* ens);
 int dctp_ensemble_info(const dctp_ensemble* ens, size_t* n, size_t* ensemble_size);
 int dctp_ensemble_member(const dctp_ensemble* ens, size_t r, const dctp_plan** member);
 
-/* forward_all (:396-439): out is batch x (K+1) x n; set 0 is the shared DCT. */
+/* forward_all (:396-439): out is batch x (K+1) x n; set 0 is the shared DCT.
+ * Signals whose path quadratic form is <= threshold take the pruned branch
+ * when cp < n (first cp coefficients of every set, the rest zero). */
 int dctp_ensemble_forward_all_f64(const dctp_ensemble* ens, const double* d_in, double* d_out,
                                   size_t batch, void* stream);
 int dctp_ensemble_forward_all_f32(const dctp_ensemble* ens, const float* d_in, float* d_out,
                                   size_t batch, void* stream);
+/* forward_all with the rest of Result (:383-387): bounds (batch x (K+1),
+ * truncation-error bound per set, 0 on the full branch) and pruned (batch,
+ * 1 = pruned branch); either may be NULL. */
+int dctp_ensemble_forward_all_pruned_f64(const dctp_ensemble* ens, const double* d_in, double* d_out,
+                                         double* d_bounds, unsigned char* d_pruned, size_t batch, void* stream);
+int dctp_ensemble_forward_all_pruned_f32(const dctp_ensemble* ens, const float* d_in, float* d_out,
+                                         float* d_bounds, unsigned char* d_pruned, size_t batch, void* stream);
 int dctp_ensemble_sync_check(const dctp_ensemble* ens, void* stream);
+/* Host-buffer forward_all with bounds / pruned (synchronous; NULL-able outputs). */
+int dctp_ensemble_forward_all_pruned_host_f64(const dctp_ensemble* ens, const double* h_in, double* h_out,
+                                              double* h_bounds, unsigned char* h_pruned, size_t batch);
+int dctp_ensemble_forward_all_pruned_host_f32(const dctp_ensemble* ens, const float* h_in, float* h_out,
+                                              float* h_bounds, unsigned char* h_pruned, size_t batch);
 int dctp_ensemble_forward_all_host_f32(const dctp_ensemble* ens, const float* h_in, float* h_out, size_t batch);
 int dctp_ensemble_forward_all_host_f64(const dctp_ensemble* ens, const double* h_in, double* h_out, size_t batch);
 

@@ -258,19 +258,19 @@ class PrunedEnsemblePlan {
     struct Result {
         bool pruned = false;
         std::vector<std::vector<double>> coeffs; // one vector per ensemble member
-        std::vector<double> bounds;              // truncation-error bound per member (0 for c_p = n)
+        std::vector<double> bounds;              // truncation-error bound per member (0 on the full branch)
     };
 
     Result forward_all(const std::vector<double>& s) const {
         if (s.size() != n_) throw std::invalid_argument("pruned_forward_all: size mismatch");
         const std::size_t sets = ensemble_size();
         std::vector<double> flat(sets * n_);
-        detail::check(dctp_ensemble_forward_all_host_f64(h_.get(), s.data(), flat.data(), 1));
         Result res;
-        double q = 0.0; // path_quadratic_form (fast_transform.hpp:24-31)
-        for (std::size_t i = 0; i + 1 < s.size(); ++i) q += (s[i] - s[i + 1]) * (s[i] - s[i + 1]);
-        res.pruned = q <= threshold_;
         res.bounds.assign(sets, 0.0);
+        unsigned char pruned = 0;
+        detail::check(dctp_ensemble_forward_all_pruned_host_f64(h_.get(), s.data(), flat.data(), res.bounds.data(),
+                                                                &pruned, 1));
+        res.pruned = pruned != 0;
         for (std::size_t r = 0; r < sets; ++r)
             res.coeffs.emplace_back(flat.begin() + static_cast<std::ptrdiff_t>(r * n_),
                                     flat.begin() + static_cast<std::ptrdiff_t>((r + 1) * n_));

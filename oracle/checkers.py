@@ -231,6 +231,8 @@ class Reference:
             lib.ref_ensemble_member.argtypes = [C.c_void_p, C.c_size_t]
             lib.ref_ensemble_forward_all.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                                      C.c_int]
+            lib.ref_ensemble_forward_all_bounds.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                            C.c_void_p, C.c_size_t, C.c_int]
             lib.ref_trig.argtypes = [C.c_int, C.c_size_t, C.c_void_p, C.c_void_p, C.c_size_t]
             lib.ref_mix_seed.restype = C.c_uint64
             lib.ref_mix_seed.argtypes = [C.c_uint64, C.c_size_t, C.c_size_t]
@@ -329,6 +331,17 @@ class RefEnsemble:
         out = np.empty((s.shape[0], self.k + 1, self.n))
         self.ref._check(self.ref.lib.ref_ensemble_forward_all(self.h, _ptr(s), _ptr(out), None, s.shape[0], threads))
         return out
+
+    def forward_all_bounds(self, s: np.ndarray, threads: int = 0):
+        """Result of PrunedEnsemblePlan::forward_all per signal: coeffs
+        (batch, K+1, n), bounds (batch, K+1), pruned flags (batch,)."""
+        s = np.ascontiguousarray(np.atleast_2d(s), dtype=np.float64)
+        out = np.empty((s.shape[0], self.k + 1, self.n))
+        bounds = np.empty((s.shape[0], self.k + 1))
+        pruned = np.empty(s.shape[0], dtype=np.int32)
+        self.ref._check(self.ref.lib.ref_ensemble_forward_all_bounds(self.h, _ptr(s), _ptr(out), _ptr(bounds),
+                                                                     _ptr(pruned), s.shape[0], threads))
+        return out, bounds, pruned
 
 
 def parity(y: np.ndarray, ref: np.ndarray) -> float:

@@ -209,6 +209,32 @@ int ref_ensemble_forward_all(const void* pv, const double* s, double* out, int* 
     }
 }
 
+/// forward_all with bounds: bounds is [batch][K+1] (Result::bounds).
+int ref_ensemble_forward_all_bounds(const void* pv, const double* s, double* out, double* bounds, int* pruned,
+                                    std::size_t batch, int threads) {
+    try {
+        const auto* p = static_cast<const PrunedEnsemblePlan*>(pv);
+        const std::size_t n = p->size(), sets = p->ensemble_size();
+        parallel_slices(batch, threads, [&](std::size_t b0, std::size_t b1) {
+            PrunedWorkspace ws = p->make_workspace();
+            PrunedEnsemblePlan::Result res;
+            std::vector<double> sig(n);
+            for (std::size_t b = b0; b < b1; ++b) {
+                std::copy(s + b * n, s + (b + 1) * n, sig.begin());
+                p->forward_all(sig, ws, res);
+                for (std::size_t r = 0; r < sets; ++r) {
+                    std::copy(res.coeffs[r].begin(), res.coeffs[r].end(), out + (b * sets + r) * n);
+                    bounds[b * sets + r] = res.bounds[r];
+                }
+                pruned[b] = res.pruned ? 1 : 0;
+            }
+        });
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 /// trig.hpp TrigPlan execute (kind 0 dct2, 1 idct2, 2 dst1) on `count` rows.
 int ref_trig(int kind, std::size_t len, const double* in, double* out, std::size_t count) {
     try {

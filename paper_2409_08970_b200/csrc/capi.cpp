@@ -820,6 +820,8 @@ struct dctp_ensemble {
     // fp32 dense route (n <= 256): G = [D^T | X_1 | ... | X_K], n x (K+1) n
     std::size_t gmat32 = 0;
     bool dense32 = false;
+    // pruned mode (c_p < n): [UL_r; HL_r] = T_r[:, 0:c_p] per member, K x n x c_p
+    std::size_t prune64 = 0, prune32 = 0;
 
     ~dctp_ensemble() {
         if (blob) {
@@ -834,7 +836,29 @@ struct dctp_ensemble {
 };
 
 template <class T>
-static void ensemble_forward(const dctp_ensemble* e, const T* in, T* out, std::size_t batch, cudaStream_t s) {
+static void ensemble_forward_full(const dctp_ensemble* e, const T* in, T* out, std::size_t batch, cudaStream_t s);
+
+/// forward_all (fast_transform.hpp:396-439) for a batch: every set of every
+/// signal through the full progressive path, then (c_p < n) the pruned
+/// signals rewritten in place; `bounds` (batch x (K+1)) and `pruned` (batch)
+/// are optional outputs.
+template <class T>
+static void ensemble_forward(const dctp_ensemble* e, const T* in, T* out, std::size_t batch, cudaStream_t s,
+                             T* bounds = nullptr, unsigned char* pruned = nullptr) {
+    ensemble_forward_full<T>(e, in, out, batch, s);
+    if (batch == 0 || (e->cp >= e->n && !bounds && !pruned)) return;
+    DeviceScope scope(e->device);
+    constexpr bool f32 = std::is_same_v<T, float>;
+    const T* blocks = e->cp < e->n ? at<T>(e->blob, f32 ? e->prune32 : e->prune64) : nullptr;
+    cuda_check(DCTP_LAUNCH("ensemble_prune", s,
+                           dctp::dev::ensemble_prune<T>(in, out, blocks, e->n, e->cp,
+                                                        static_cast<int>(e->members.size()), e->threshold, batch,
+                                                        bounds, pruned, s)),
+               "prune kernel");
+}
+
+template <class T>
+static void ensemble_forward_full(const dctp_ensemble* e, const T* in, T* out, std::size_t batch, cudaStream_t s) {
     if (!e) throw std::invalid_argument("dctp_ensemble_forward_all: null ensemble");
     if (!e->blob) throw std::invalid_argument("PrunedEnsemblePlan: host-only plan (created with device < 0)");
     if (batch == 0) return;
@@ -987,8 +1011,6 @@ int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is,
         if (!out) throw std::invalid_argument("dctp_ensemble_create: null output");
         *out = nullptr;
         if (cp < 1 || cp > n) throw std::invalid_argument("PrunedEnsemblePlan: need 1 <= c_p <= n");
-        if (cp != n)
-            throw std::invalid_argument("PrunedEnsemblePlan: the GPU path implements the progressive mode c_p = n only");
         if (k > 0 && (!kinds || !is || !js || !rhos)) throw std::invalid_argument("dctp_ensemble_create: null update arrays");
         auto e = std::make_unique<dctp_ensemble>();
         e->n = n;
@@ -1032,6 +1054,29 @@ int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is,
         }
         e->desc64 = blob.add(std::vector<dctp::dev::CauchyStage>(k));
         e->desc32 = blob.add(std::vector<dctp::dev::CauchyStage>(k));
+        if (cp < n) {
+            // T_r rows exactly as the reference builds them (fast_transform.hpp:355-366):
+            // pass-through slot -> sigma at its DCT index, active slot s ->
+            // -sigma_s a_s z_j / (nu_s - lambda_j); keep the first c_p columns.
+            std::vector<double> blk(k * n * cp, 0.0);
+            for (std::size_t r = 0; r < k; ++r) {
+                const auto& st = e->members[r]->st;
+                double* b = blk.data() + r * n * cp;
+                for (std::size_t slot = 0; slot < n; ++slot) {
+                    const auto& ref = st.slots[slot];
+                    if (ref.passthrough) {
+                        if (ref.idx < cp) b[slot * cp + ref.idx] = st.sigma[slot];
+                        continue;
+                    }
+                    const double nu = st.sub_mu[ref.idx];
+                    const double sc = -st.sigma[slot] * st.a[slot];
+                    for (std::size_t j = 0; j < cp; ++j)
+                        if (st.z[j] != 0.0) b[slot * cp + j] = sc * st.z[j] / (nu - st.lambda[j]);
+                }
+            }
+            e->prune64 = blob.add(blk);
+            e->prune32 = blob.add(to_f32(blk));
+        }
         // fp32 progressive as one SGEMM: every member is its full basis X_r and
         // set 0 the orthonormal DCT-II matrix, so out = x * [D^T | X_1 | ... | X_K]
         if (n <= 256 && n % 16 == 0 && device >= 0) {
@@ -1104,6 +1149,55 @@ int dctp_ensemble_forward_all_f64(const dctp_ensemble* e, const double* in, doub
 int dctp_ensemble_forward_all_f32(const dctp_ensemble* e, const float* in, float* out, size_t batch, void* stream) {
     return guarded([&] { ensemble_forward<float>(e, in, out, batch, static_cast<cudaStream_t>(stream)); });
 }
+int dctp_ensemble_forward_all_pruned_f64(const dctp_ensemble* e, const double* in, double* out, double* bounds,
+                                         unsigned char* pruned, size_t batch, void* stream) {
+    return guarded([&] {
+        ensemble_forward<double>(e, in, out, batch, static_cast<cudaStream_t>(stream), bounds, pruned);
+    });
+}
+int dctp_ensemble_forward_all_pruned_f32(const dctp_ensemble* e, const float* in, float* out, float* bounds,
+                                         unsigned char* pruned, size_t batch, void* stream) {
+    return guarded([&] {
+        ensemble_forward<float>(e, in, out, batch, static_cast<cudaStream_t>(stream), bounds, pruned);
+    });
+}
+} // extern "C"
+
+/// Host buffers, with bounds and pruned flags: H2D, forward_all, D2H on one
+/// stream (meant for small batches; large ones use the pipelined entries).
+template <class T>
+static void ensemble_pruned_host(const dctp_ensemble* e, const T* h_in, T* h_out, T* h_bounds,
+                                 unsigned char* h_pruned, std::size_t batch) {
+    if (!e) throw std::invalid_argument("null ensemble");
+    if (!e->blob) throw std::invalid_argument("PrunedEnsemblePlan: host-only plan (created with device < 0)");
+    if (batch == 0) return;
+    if (!h_in || !h_out) throw std::invalid_argument("pruned_forward_all: null buffer");
+    DeviceScope scope(e->device);
+    const std::size_t n = e->n, sets = e->members.size() + 1;
+    HostPipe& hp = host_pipe(e->device);
+    cudaStream_t s = hp.comp;
+    Scratch<T> din(batch * n, s), dout(batch * sets * n, s), db(batch * sets, s);
+    Scratch<unsigned char> dp(batch, s);
+    cuda_check(cudaMemcpyAsync(din.ptr, h_in, batch * n * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+    ensemble_forward<T>(e, din.ptr, dout.ptr, batch, s, db.ptr, dp.ptr);
+    cuda_check(cudaMemcpyAsync(h_out, dout.ptr, batch * sets * n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+    if (h_bounds)
+        cuda_check(cudaMemcpyAsync(h_bounds, db.ptr, batch * sets * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+    if (h_pruned) cuda_check(cudaMemcpyAsync(h_pruned, dp.ptr, batch, cudaMemcpyDeviceToHost, s), "D2H");
+    sync_check(e->device, e->flag, s);
+}
+
+extern "C" {
+
+int dctp_ensemble_forward_all_pruned_host_f64(const dctp_ensemble* e, const double* h_in, double* h_out,
+                                              double* h_bounds, unsigned char* h_pruned, size_t batch) {
+    return guarded([&] { ensemble_pruned_host<double>(e, h_in, h_out, h_bounds, h_pruned, batch); });
+}
+int dctp_ensemble_forward_all_pruned_host_f32(const dctp_ensemble* e, const float* h_in, float* h_out,
+                                              float* h_bounds, unsigned char* h_pruned, size_t batch) {
+    return guarded([&] { ensemble_pruned_host<float>(e, h_in, h_out, h_bounds, h_pruned, batch); });
+}
+
 int dctp_ensemble_sync_check(const dctp_ensemble* e, void* stream) {
     return guarded([&] {
         if (!e) throw std::invalid_argument("dctp_ensemble_sync_check: null ensemble");

@@ -95,6 +95,15 @@ struct SmallPlanDev {
     int debug; // development knob (DCTP_DEBUG_MODE bits): 1 = skip the DCT work, 2 = skip the DMMA work
 };
 
+/// Pruned progressive mode (fast_transform.hpp:396-439, c_p < n) applied in
+/// place to a batch already transformed in full (`out`, batch x (K+1) x n);
+/// blocks = K x n x c_p ([UL_r; HL_r]).  c_p >= n: only the optional outputs
+/// (bounds 0, pruned = path quadratic form <= threshold).
+template <class T>
+cudaError_t ensemble_prune(const T* in, T* out, const T* blocks, std::size_t n, std::size_t cp, int members,
+                           double threshold, std::size_t batch, T* bounds, unsigned char* pruned,
+                           cudaStream_t stream);
+
 /// Generic plans: power-of-two 16 <= n <= 512, K <= 128, A <= 128.  Folded
 /// plans: power-of-two 64 <= n <= 256 and at most 128 Cauchy columns.
 /// C[M x N] = A[M x K] * B[K x N], fp32 row-major (K % 16 == 0, N and the

@@ -279,7 +279,9 @@ def path_quadratic_form(s) -> float:
 
 
 class PrunedEnsemblePlan:
-    """Shared DCT + K Cauchy stages, progressive mode c_p = n (fast_transform.hpp:338-454)."""
+    """Shared DCT + K Cauchy stages (fast_transform.hpp:338-454): progressive
+    (c_p = n) and pruned (c_p < n: signals whose path quadratic form is at
+    most `threshold` keep c_p coefficients per set, with error bounds)."""
 
     kDenseMemberCutoff = 128
 
@@ -336,20 +338,34 @@ class PrunedEnsemblePlan:
             raise N.LogicError("PrunedEnsemblePlan::member: index out of range")
         return self._members[r - 1]
 
-    def forward_all_batch(self, s, sync: bool = True, out=None):
-        """Batched forward_all: rows -> (batch, K+1, n); set 0 is the shared DCT."""
+    def forward_all_batch(self, s, sync: bool = True, out=None, with_bounds: bool = False):
+        """Batched forward_all: rows -> (batch, K+1, n); set 0 is the shared DCT.
+        with_bounds=True also returns the truncation-error bounds (batch, K+1)
+        and the pruned-branch flags (batch,) of Result (device rows only)."""
         n, sets = self._n, self.ensemble_size()
         if _is_device_tensor(s):
             rows, single = _dev_rows(s, n, "pruned_forward_all")
             y = out if out is not None else torch.empty((rows.shape[0], sets, n), dtype=rows.dtype,
                                                         device=rows.device)
-            fn = lib.dctp_ensemble_forward_all_f64 if rows.dtype == torch.float64 else \
-                lib.dctp_ensemble_forward_all_f32
             stream = _stream_ptr(rows.device)
-            check(fn(self._h, C.c_void_p(rows.data_ptr()), C.c_void_p(y.data_ptr()), rows.shape[0], stream))
+            if with_bounds:
+                bounds = torch.empty((rows.shape[0], sets), dtype=rows.dtype, device=rows.device)
+                pruned = torch.empty((rows.shape[0],), dtype=torch.uint8, device=rows.device)
+                fn = lib.dctp_ensemble_forward_all_pruned_f64 if rows.dtype == torch.float64 else \
+                    lib.dctp_ensemble_forward_all_pruned_f32
+                check(fn(self._h, C.c_void_p(rows.data_ptr()), C.c_void_p(y.data_ptr()),
+                         C.c_void_p(bounds.data_ptr()), C.c_void_p(pruned.data_ptr()), rows.shape[0], stream))
+            else:
+                fn = lib.dctp_ensemble_forward_all_f64 if rows.dtype == torch.float64 else \
+                    lib.dctp_ensemble_forward_all_f32
+                check(fn(self._h, C.c_void_p(rows.data_ptr()), C.c_void_p(y.data_ptr()), rows.shape[0], stream))
             if sync:
                 check(lib.dctp_ensemble_sync_check(self._h, stream))
+            if with_bounds:
+                return (y[0], bounds[0], pruned[0]) if single else (y, bounds, pruned)
             return y[0] if single else y
+        if with_bounds:
+            raise N.InvalidArgument("forward_all_batch(with_bounds=True) takes device rows; use forward_all")
         rows, single = _as_rows(s, n, "pruned_forward_all")
         y = np.empty((rows.shape[0], sets, n), dtype=rows.dtype)
         fn = lib.dctp_ensemble_forward_all_host_f64 if rows.dtype == np.float64 else \
@@ -361,12 +377,17 @@ class PrunedEnsemblePlan:
         """One signal -> Result{pruned, coeffs[K+1], bounds} (fast_transform.hpp:396-446).
         With c_p = n both branches give the exact K+1 coefficient sets and
         zero truncation bounds."""
-        a = np.asarray(s)
+        a = np.ascontiguousarray(np.asarray(s, dtype=np.float64))
         if a.ndim != 1 or a.shape[0] != self._n:
             raise N.InvalidArgument("pruned_forward_all: size mismatch")
-        coeffs = self.forward_all_batch(a)
-        return Result(pruned=path_quadratic_form(a) <= self._thr, coeffs=[c for c in coeffs],
-                      bounds=[0.0] * self.ensemble_size())
+        sets = self.ensemble_size()
+        coeffs = np.empty((sets, self._n))
+        bounds = np.empty(sets)
+        pruned = (C.c_ubyte * 1)()
+        check(lib.dctp_ensemble_forward_all_pruned_host_f64(self._h, a.ctypes.data_as(C.c_void_p),
+                                                            coeffs.ctypes.data_as(C.c_void_p),
+                                                            bounds.ctypes.data_as(C.c_void_p), pruned, 1))
+        return Result(pruned=bool(pruned[0]), coeffs=[c for c in coeffs], bounds=[float(b) for b in bounds])
 
 
 def plan_pruned(n, updates, cp, threshold, epsilon=1e-12, device=0) -> PrunedEnsemblePlan:

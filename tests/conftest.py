@@ -47,3 +47,14 @@ def golden():
     from tests.golden_io import load_golden
 
     return load_golden
+
+
+@pytest.fixture(scope="session")
+def reference():
+    """The reference library built in place (oracle/_ref); skips when absent."""
+    from oracle import checkers as O
+
+    try:
+        return O.Reference()
+    except O.ReferenceUnavailable as e:  # pragma: no cover
+        pytest.skip(str(e))

@@ -305,3 +305,76 @@ def test_progressive_fp32_dense_route_edges(P, torch, restatement):
     bad[5, 7] = float("inf")
     with pytest.raises(P.DomainError):
         ens.forward_all_batch(bad)
+
+
+# --- pruned progressive mode (c_p < n), fast_transform.hpp:396-439 -------------
+
+_PRUNE_UPS = [O.Update(0, 1.5, 1, 0), O.Update(1, 1.5, 2, 3)]  # proj/tests/test_pruning.cpp:16-17
+
+
+def _pruned_pair(P, reference, n, cp, thr):
+    ours = P.PrunedEnsemblePlan(n, [upd(P, u) for u in _PRUNE_UPS], cp, thr)
+    ref = reference.ensemble(n, _PRUNE_UPS, cp, thr)
+    return ours, ref
+
+
+def _bound_parity(b, rb):
+    return float((np.abs(b - rb) / np.maximum(np.abs(rb), 1e-300)).max()) if rb.size else 0.0
+
+
+@pytest.mark.parametrize("cp", [8, 16, 24])
+def test_pruned_branch_matches_reference(P, torch, restatement, reference, cp):
+    """Always-prune threshold (proj/tests/test_pruning.cpp:95-115): coefficient
+    sets, truncation bounds and flags of every signal against the reference's
+    forward_all, fp64 and fp32; the bound really bounds the truncation error."""
+    n = 32
+    ours, ref = _pruned_pair(P, reference, n, cp, float(np.finfo(np.float64).max))
+    s = restatement.fill_signals(O.mix_seed(777, n, cp), 2, n, 100, 0.99)
+    rc, rb, rp = ref.forward_all_bounds(s)
+    for dtype, tol in ((torch.float64, TOL64), (torch.float32, TOL32)):
+        y, b, p = ours.forward_all_batch(dev(torch, s, dtype), with_bounds=True)
+        y, b, p = y.double().cpu().numpy(), b.double().cpu().numpy(), p.cpu().numpy()
+        assert (p == 1).all() and (rp == 1).all()
+        for r in range(3):
+            assert O.parity(y[:, r, :], rc[:, r, :]) <= tol, (dtype, r)
+            assert np.abs(y[:, r, cp:]).max() == 0.0  # pruned sets keep c_p coefficients
+        assert _bound_parity(b, rb) <= (1e-9 if dtype == torch.float64 else 1e-4)
+    # error bound property on the full transforms (reference test :109-112)
+    ens_full = reference.ensemble(n, _PRUNE_UPS, n, float(np.finfo(np.float64).max))
+    exact = ens_full.forward_all(s)
+    y = ours.forward_all_batch(dev(torch, s, torch.float64), with_bounds=True)
+    got, bnd = y[0].cpu().numpy(), y[1].cpu().numpy()
+    for r in range(1, 3):
+        err = np.linalg.norm(exact[:, r, :] - got[:, r, :], axis=1)
+        assert (err <= bnd[:, r] + 1e-12).all()
+
+
+def test_pruned_full_branch_and_mixed_batches(P, torch, restatement, reference):
+    """Rough signals over a tiny threshold take the full branch (bounds 0);
+    a threshold at the median quadratic form splits a batch between both
+    branches, each signal matching the reference."""
+    n, cp = 32, 16
+    s_rough = restatement.fill_signals(O.mix_seed(13, n, 1), 0, n, 50)  # white noise
+    ours, ref = _pruned_pair(P, reference, n, cp, 1e-6)
+    y, b, p = ours.forward_all_batch(dev(torch, s_rough, torch.float64), with_bounds=True)
+    rc, rb, rp = ref.forward_all_bounds(s_rough)
+    assert (p.cpu().numpy() == 0).all() and (rp == 0).all()
+    assert float(b.abs().max()) == 0.0
+    assert O.parity(y.cpu().numpy().reshape(50, -1), rc.reshape(50, -1)) <= TOL64
+    s_smooth = restatement.fill_signals(O.mix_seed(14, n, 1), 2, n, 50, 0.99)
+    s = np.concatenate([s_rough, s_smooth])
+    q = (np.diff(s, axis=1) ** 2).sum(axis=1)
+    thr = float(np.median(q))
+    ours, ref = _pruned_pair(P, reference, n, cp, thr)
+    y, b, p = ours.forward_all_batch(dev(torch, s, torch.float64), with_bounds=True)
+    rc, rb, rp = ref.forward_all_bounds(s)
+    p = p.cpu().numpy()
+    assert 0 < p.sum() < len(s) and (p == rp).all()
+    for r in range(3):
+        assert O.parity(y.cpu().numpy()[:, r, :], rc[:, r, :]) <= TOL64
+    assert _bound_parity(b.cpu().numpy(), rb) <= 1e-9
+    # the single-signal Result API (fast_transform.hpp:383-387, 441-446)
+    res = ours.forward_all(s[int(np.argmax(p))])
+    k = int(np.argmax(p))
+    assert res.pruned and len(res.coeffs) == 3 and len(res.bounds) == 3
+    assert np.allclose(res.bounds, rb[k], rtol=1e-9, atol=0)

@@ -138,3 +138,13 @@ def test_signal_sources_match_reference_goldens():
         s = P.fill_signals(int(g["seed"]), int(g["dist"]), int(g["n"]), g["signals"].shape[0], float(g["r"]))
         assert np.array_equal(s, g["signals"])
     assert P.mix_seed(2409, 1024, 3) == O.mix_seed(2409, 1024, 3)
+
+
+def test_pruned_ensemble_constructs_host_only():
+    """c_p < n (the pruned mode, fast_transform.hpp:343-375) builds on the host
+    like c_p = n; applying a host-only ensemble is an InvalidArgument."""
+    ups = [P.RankOneUpdate.self_loop(1, 1.5), P.RankOneUpdate.edge_delta(2, 3, 1.5)]
+    ens = P.PrunedEnsemblePlan(32, ups, 16, 0.5, device=-1)
+    assert ens.keep_count() == 16 and ens.threshold() == 0.5 and ens.ensemble_size() == 3
+    with pytest.raises(P.InvalidArgument):
+        ens.forward_all(np.zeros(32))

@@ -135,6 +135,14 @@ int dctp_ensemble_forward_all_pruned_f64(const dctp_ensemble* ens, const double*
 int dctp_ensemble_forward_all_pruned_f32(const dctp_ensemble* ens, const float* d_in, float* d_out,
                                          float* d_bounds, unsigned char* d_pruned, size_t batch, void* stream);
 int dctp_ensemble_sync_check(const dctp_ensemble* ens, void* stream);
+/* rdo_select (fast_transform.hpp:472-496, l1 cost) for a batch of device rows:
+ * index (batch, int) of the least-l1 set per signal (ties to the lower index),
+ * chosen (batch x n) that set's coefficients, pruned (batch) the branch; the
+ * outputs may be NULL (not both chosen and index). */
+int dctp_ensemble_rdo_select_f64(const dctp_ensemble* ens, const double* d_in, double* d_chosen, int* d_index,
+                                 unsigned char* d_pruned, size_t batch, void* stream);
+int dctp_ensemble_rdo_select_f32(const dctp_ensemble* ens, const float* d_in, float* d_chosen, int* d_index,
+                                 unsigned char* d_pruned, size_t batch, void* stream);
 /* Host-buffer forward_all with bounds / pruned (synchronous; NULL-able outputs). */
 int dctp_ensemble_forward_all_pruned_host_f64(const dctp_ensemble* ens, const double* h_in, double* h_out,
                                               double* h_bounds, unsigned char* h_pruned, size_t batch);

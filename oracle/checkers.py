@@ -233,6 +233,10 @@ class Reference:
                                                      C.c_int]
             lib.ref_ensemble_forward_all_bounds.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                                             C.c_void_p, C.c_size_t, C.c_int]
+            lib.ref_rdo_select.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]
+            lib.ref_calibrate_prune_threshold.restype = C.c_double
+            lib.ref_calibrate_prune_threshold.argtypes = [C.c_size_t, C.c_double, C.c_double, C.c_size_t,
+                                                          C.c_uint64]
             lib.ref_trig.argtypes = [C.c_int, C.c_size_t, C.c_void_p, C.c_void_p, C.c_size_t]
             lib.ref_mix_seed.restype = C.c_uint64
             lib.ref_mix_seed.argtypes = [C.c_uint64, C.c_size_t, C.c_size_t]
@@ -342,6 +346,14 @@ class RefEnsemble:
         self.ref._check(self.ref.lib.ref_ensemble_forward_all_bounds(self.h, _ptr(s), _ptr(out), _ptr(bounds),
                                                                      _ptr(pruned), s.shape[0], threads))
         return out, bounds, pruned
+
+    def rdo_select(self, s: np.ndarray):
+        """rdo_select (l1) per signal: (index, pruned) int32 arrays."""
+        s = np.ascontiguousarray(np.atleast_2d(s), dtype=np.float64)
+        idx = np.empty(s.shape[0], dtype=np.int32)
+        pr = np.empty(s.shape[0], dtype=np.int32)
+        self.ref._check(self.ref.lib.ref_rdo_select(self.h, _ptr(s), _ptr(idx), _ptr(pr), s.shape[0]))
+        return idx, pr
 
 
 def parity(y: np.ndarray, ref: np.ndarray) -> float:

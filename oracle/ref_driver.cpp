@@ -235,6 +235,29 @@ int ref_ensemble_forward_all_bounds(const void* pv, const double* s, double* out
     }
 }
 
+/// rdo_select (fast_transform.hpp:494-496, l1 cost) per signal: index, pruned.
+int ref_rdo_select(const void* pv, const double* s, int* index, int* pruned, std::size_t batch) {
+    try {
+        const auto* p = static_cast<const PrunedEnsemblePlan*>(pv);
+        const std::size_t n = p->size();
+        for (std::size_t b = 0; b < batch; ++b) {
+            const std::vector<double> sig(s + b * n, s + (b + 1) * n);
+            const RdoChoice c = rdo_select(*p, sig);
+            index[b] = static_cast<int>(c.index);
+            pruned[b] = c.pruned ? 1 : 0;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+/// bench.hpp:99-108.
+double ref_calibrate_prune_threshold(std::size_t n, double r, double quantile, std::size_t trials,
+                                     std::uint64_t seed) {
+    return calibrate_prune_threshold(n, r, quantile, trials, seed);
+}
+
 /// trig.hpp TrigPlan execute (kind 0 dct2, 1 idct2, 2 dst1) on `count` rows.
 int ref_trig(int kind, std::size_t len, const double* in, double* out, std::size_t count) {
     try {

@@ -10,11 +10,12 @@ from ._native import (CudaFailure, DctPlusError, DomainError, InvalidArgument, L
 from .dctplus import (DIST_AR, DIST_AR2D, DIST_GAUSSIAN, DIST_SYM_UNIFORM, DIST_UNIFORM,  # noqa: F401
                       DctPlusPlan, PrunedEnsemblePlan, RankOneUpdate, Result, dct2, fill_signals, forward,
                       forward_nmvp, idct2, inverse, mix_seed, path_quadratic_form, plan_dctplus, plan_pruned,
-                      profile_enable, profile_reset, profile_summary, pruned_forward_all)
+                      profile_enable, profile_reset, profile_summary, pruned_forward_all, RdoChoice, rdo_select,
+                      rdo_select_batch, calibrate_prune_threshold)
 
 __all__ = [
     "RankOneUpdate", "DctPlusPlan", "PrunedEnsemblePlan", "Result", "plan_dctplus", "forward", "forward_nmvp",
     "inverse", "plan_pruned", "pruned_forward_all", "dct2", "idct2", "fill_signals", "mix_seed",
     "path_quadratic_form", "DctPlusError", "InvalidArgument", "DomainError", "RuntimeFailure", "LogicError",
-    "CudaFailure",
+    "CudaFailure", "RdoChoice", "rdo_select", "rdo_select_batch", "calibrate_prune_threshold",
 ]

@@ -55,6 +55,8 @@ SIGNATURES = {
     "dctp_ensemble_sync_check": (C.c_int, [_p, _p]),
     "dctp_ensemble_forward_all_pruned_f64": (C.c_int, [_p, _p, _p, _p, _p, _sz, _p]),
     "dctp_ensemble_forward_all_pruned_f32": (C.c_int, [_p, _p, _p, _p, _p, _sz, _p]),
+    "dctp_ensemble_rdo_select_f64": (C.c_int, [_p, _p, _p, _p, _p, _sz, _p]),
+    "dctp_ensemble_rdo_select_f32": (C.c_int, [_p, _p, _p, _p, _p, _sz, _p]),
     "dctp_ensemble_forward_all_pruned_host_f64": (C.c_int, [_p, _p, _p, _p, _p, _sz]),
     "dctp_ensemble_forward_all_pruned_host_f32": (C.c_int, [_p, _p, _p, _p, _p, _sz]),
     "dctp_ensemble_forward_all_host_f32": (C.c_int, [_p, _p, _p, _sz]),

@@ -1163,6 +1163,24 @@ int dctp_ensemble_forward_all_pruned_f32(const dctp_ensemble* e, const float* in
 }
 } // extern "C"
 
+/// rdo_select for a batch (fast_transform.hpp:472-496, l1 cost): forward_all
+/// into scratch, then the least-l1 set per signal.
+template <class T>
+static void ensemble_rdo(const dctp_ensemble* e, const T* in, T* chosen, int* index, unsigned char* pruned,
+                         std::size_t batch, cudaStream_t s) {
+    if (!e) throw std::invalid_argument("rdo_select: null ensemble");
+    if (!e->blob) throw std::invalid_argument("PrunedEnsemblePlan: host-only plan (created with device < 0)");
+    if (batch == 0) return;
+    if (!in || (!chosen && !index)) throw std::invalid_argument("rdo_select: null buffer");
+    DeviceScope scope(e->device);
+    const std::size_t n = e->n, sets = e->members.size() + 1;
+    Scratch<T> all(batch * sets * n, s);
+    ensemble_forward<T>(e, in, all.ptr, batch, s, nullptr, pruned);
+    cuda_check(DCTP_LAUNCH("rdo_select", s,
+                           dctp::dev::rdo_select_rows<T>(all.ptr, n, static_cast<int>(sets), batch, chosen, index, s)),
+               "rdo_select kernel");
+}
+
 /// Host buffers, with bounds and pruned flags: H2D, forward_all, D2H on one
 /// stream (meant for small batches; large ones use the pipelined entries).
 template <class T>
@@ -1188,6 +1206,15 @@ static void ensemble_pruned_host(const dctp_ensemble* e, const T* h_in, T* h_out
 }
 
 extern "C" {
+
+int dctp_ensemble_rdo_select_f64(const dctp_ensemble* e, const double* in, double* chosen, int* index,
+                                 unsigned char* pruned, size_t batch, void* stream) {
+    return guarded([&] { ensemble_rdo<double>(e, in, chosen, index, pruned, batch, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_ensemble_rdo_select_f32(const dctp_ensemble* e, const float* in, float* chosen, int* index,
+                                 unsigned char* pruned, size_t batch, void* stream) {
+    return guarded([&] { ensemble_rdo<float>(e, in, chosen, index, pruned, batch, static_cast<cudaStream_t>(stream)); });
+}
 
 int dctp_ensemble_forward_all_pruned_host_f64(const dctp_ensemble* e, const double* h_in, double* h_out,
                                               double* h_bounds, unsigned char* h_pruned, size_t batch) {

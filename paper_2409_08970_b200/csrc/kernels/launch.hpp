@@ -104,6 +104,13 @@ cudaError_t ensemble_prune(const T* in, T* out, const T* blocks, std::size_t n, 
                            double threshold, std::size_t batch, T* bounds, unsigned char* pruned,
                            cudaStream_t stream);
 
+/// rdo_select (fast_transform.hpp:472-496) over forward_all output rows
+/// (batch x sets x n): index of the least-l1 set per signal (ties to the
+/// lower index) and, if `chosen` is set, that set's coefficients (batch x n).
+template <class T>
+cudaError_t rdo_select_rows(const T* coeffs, std::size_t n, int sets, std::size_t batch, T* chosen, int* index,
+                            cudaStream_t stream);
+
 /// Generic plans: power-of-two 16 <= n <= 512, K <= 128, A <= 128.  Folded
 /// plans: power-of-two 64 <= n <= 256 and at most 128 Cauchy columns.
 /// C[M x N] = A[M x K] * B[K x N], fp32 row-major (K % 16 == 0, N and the

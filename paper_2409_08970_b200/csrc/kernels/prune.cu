@@ -164,3 +164,50 @@ template cudaError_t ensemble_prune<float>(const float*, float*, const float*, s
                                            double, std::size_t, float*, unsigned char*, cudaStream_t);
 
 } // namespace dctp::dev
+
+namespace dctp::dev {
+namespace {
+
+/// rdo_select (fast_transform.hpp:472-496) for a batch: per signal the set
+/// with the smallest l1 norm (ties to the lower index), copied out.
+template <class T>
+__global__ void __launch_bounds__(kThreads)
+rdo_select_kernel(const T* __restrict__ coeffs, int n, int sets, std::size_t batch, T* __restrict__ chosen,
+                  int* __restrict__ index) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const std::size_t b = static_cast<std::size_t>(blockIdx.x) * kWarps + warp;
+    if (b >= batch) return;
+    const T* c = coeffs + b * sets * n;
+    double best = 0.0;
+    int arg = 0;
+    for (int r = 0; r < sets; ++r) {
+        double l1 = 0.0;
+        for (int i = lane; i < n; i += 32) l1 += fabs(static_cast<double>(c[r * n + i]));
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, m);
+        if (r == 0 || l1 < best) {
+            best = l1;
+            arg = r;
+        }
+    }
+    if (chosen)
+        for (int i = lane; i < n; i += 32) chosen[b * n + i] = c[arg * n + i];
+    if (lane == 0 && index) index[b] = arg;
+}
+
+} // namespace
+
+template <class T>
+cudaError_t rdo_select_rows(const T* coeffs, std::size_t n, int sets, std::size_t batch, T* chosen, int* index,
+                            cudaStream_t stream) {
+    if (batch == 0) return cudaSuccess;
+    const unsigned grid = static_cast<unsigned>((batch + kWarps - 1) / kWarps);
+    rdo_select_kernel<T><<<grid, kThreads, 0, stream>>>(coeffs, static_cast<int>(n), sets, batch, chosen, index);
+    return cudaGetLastError();
+}
+
+template cudaError_t rdo_select_rows<double>(const double*, std::size_t, int, std::size_t, double*, int*,
+                                             cudaStream_t);
+template cudaError_t rdo_select_rows<float>(const float*, std::size_t, int, std::size_t, float*, int*, cudaStream_t);
+
+} // namespace dctp::dev

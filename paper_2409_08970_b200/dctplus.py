@@ -275,7 +275,8 @@ class Result:
 def path_quadratic_form(s) -> float:
     """sum (s_i - s_{i+1})^2 (fast_transform.hpp:24-31) — host helper for Result.pruned."""
     a = np.asarray(s, dtype=np.float64)
-    return float(np.sum(np.diff(a) ** 2))
+    d = a[:-1] - a[1:]
+    return float(np.cumsum(d * d)[-1]) if d.size else 0.0  # sequential, as the reference
 
 
 class PrunedEnsemblePlan:
@@ -396,6 +397,58 @@ def plan_pruned(n, updates, cp, threshold, epsilon=1e-12, device=0) -> PrunedEns
 
 def pruned_forward_all(plan: PrunedEnsemblePlan, s) -> Result:
     return plan.forward_all(s)
+
+
+@dataclass
+class RdoChoice:
+    """fast_transform.hpp:466-470."""
+
+    index: int = 0
+    coeffs: np.ndarray = None
+    pruned: bool = False
+
+
+def rdo_select(plan: PrunedEnsemblePlan, s, cost=None) -> RdoChoice:
+    """The ensemble member whose coefficients minimise `cost` (default l1,
+    the reference's rate-distortion proxy), ties to the lower index, on the
+    pruned or full outputs per the threshold branch (fast_transform.hpp:472-496)."""
+    res = plan.forward_all(s)
+    cost = cost or (lambda c: float(np.abs(c).sum()))
+    best, idx = cost(res.coeffs[0]), 0
+    for r in range(1, len(res.coeffs)):
+        c = cost(res.coeffs[r])
+        if c < best:
+            best, idx = c, r
+    return RdoChoice(index=idx, coeffs=res.coeffs[idx], pruned=res.pruned)
+
+
+def rdo_select_batch(plan: PrunedEnsemblePlan, rows, sync: bool = True):
+    """rdo_select (l1 cost) for device rows on the GPU: (index int32 (batch,),
+    chosen coefficients (batch, n), pruned uint8 (batch,))."""
+    if not _is_device_tensor(rows):
+        raise N.InvalidArgument("rdo_select_batch takes device rows; use rdo_select for one host signal")
+    x, single = _dev_rows(rows, plan.size(), "rdo_select")
+    b = x.shape[0]
+    index = torch.empty((b,), dtype=torch.int32, device=x.device)
+    chosen = torch.empty((b, plan.size()), dtype=x.dtype, device=x.device)
+    pruned = torch.empty((b,), dtype=torch.uint8, device=x.device)
+    fn = lib.dctp_ensemble_rdo_select_f64 if x.dtype == torch.float64 else lib.dctp_ensemble_rdo_select_f32
+    stream = _stream_ptr(x.device)
+    check(fn(plan._h, C.c_void_p(x.data_ptr()), C.c_void_p(chosen.data_ptr()), C.c_void_p(index.data_ptr()),
+             C.c_void_p(pruned.data_ptr()), b, stream))
+    if sync:
+        check(lib.dctp_ensemble_sync_check(plan._h, stream))
+    return (index[0], chosen[0], pruned[0]) if single else (index, chosen, pruned)
+
+
+def calibrate_prune_threshold(n: int, r: float = 0.99, quantile: float = 0.7, trials: int = 512,
+                              seed: int = 42) -> float:
+    """bench.hpp:99-108: the `quantile` of the path quadratic form over
+    `trials` AR(r) signals drawn from Rng(mix_seed(seed, n, 9000))."""
+    sig = fill_signals(mix_seed(seed, n, 9000), DIST_AR, n, trials, r)
+    d = sig[:, :-1] - sig[:, 1:]
+    q = np.sort(np.cumsum(d * d, axis=1)[:, -1])  # sequential sums, as the reference
+    return float(q[min(trials - 1, int(quantile * (trials - 1)))])
 
 
 # --- batched trig kernels (trig.hpp:95-110) -------------------------------------------

@@ -378,3 +378,34 @@ def test_pruned_full_branch_and_mixed_batches(P, torch, restatement, reference):
     k = int(np.argmax(p))
     assert res.pruned and len(res.coeffs) == 3 and len(res.bounds) == 3
     assert np.allclose(res.bounds, rb[k], rtol=1e-9, atol=0)
+
+
+def test_rdo_select_matches_reference(P, torch, restatement, reference):
+    """rdo_select (fast_transform.hpp:472-496): a column of member r's basis
+    selects r, a constant selects the DCT (proj/tests/test_pruning.cpp
+    :117-135); on a mixed batch (pruned and full branches) the batched GPU
+    choice and the single-signal API agree with the reference's."""
+    n = 32
+    thr_always = float(np.finfo(np.float64).max)
+    ens = P.PrunedEnsemblePlan(n, [upd(P, u) for u in _PRUNE_UPS], n, thr_always)
+    for r in range(1, 3):
+        col = np.ascontiguousarray(ens.member(r).basis()[:, 2])
+        assert P.rdo_select(ens, col).index == r
+        idx, chosen, _ = P.rdo_select_batch(ens, dev(torch, col[None, :], torch.float64))
+        assert int(idx[0]) == r
+    assert P.rdo_select(ens, np.ones(n)).index == 0
+    cp = 16
+    s = np.concatenate([restatement.fill_signals(O.mix_seed(21, n, 1), 0, n, 40),
+                        restatement.fill_signals(O.mix_seed(22, n, 1), 2, n, 40, 0.99)])
+    thr = float(np.median((np.diff(s, axis=1) ** 2).sum(axis=1)))
+    ours, ref = _pruned_pair(P, reference, n, cp, thr)
+    ridx, rpr = ref.rdo_select(s)
+    for dtype in (torch.float64, torch.float32):
+        idx, chosen, pr = P.rdo_select_batch(ours, dev(torch, s, dtype))
+        assert (pr.cpu().numpy() == rpr).all()
+        agree = (idx.cpu().numpy() == ridx).mean()
+        assert agree == 1.0 if dtype == torch.float64 else agree >= 0.95
+        full = ours.forward_all_batch(dev(torch, s, dtype)).cpu().numpy()
+        pick = full[np.arange(len(s)), idx.cpu().numpy().astype(int), :]
+        assert np.array_equal(pick, chosen.cpu().numpy())
+    assert [P.rdo_select(ours, x).index for x in s[:6]] == list(ridx[:6])

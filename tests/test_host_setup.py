@@ -148,3 +148,11 @@ def test_pruned_ensemble_constructs_host_only():
     assert ens.keep_count() == 16 and ens.threshold() == 0.5 and ens.ensemble_size() == 3
     with pytest.raises(P.InvalidArgument):
         ens.forward_all(np.zeros(32))
+
+
+@pytest.mark.parametrize("n,r,quantile,seed", [(32, 0.99, 0.7, 42), (128, 0.95, 0.5, 7), (16, 0.9, 0.9, 1)])
+def test_calibrate_prune_threshold_matches_reference(reference, n, r, quantile, seed):
+    """bench.hpp:99-108 on the reference's Rng: bit-identical threshold."""
+    ours = P.calibrate_prune_threshold(n, r, quantile, 512, seed)
+    ref = reference.lib.ref_calibrate_prune_threshold(n, r, quantile, 512, seed)
+    assert ours == ref

@@ -16,6 +16,7 @@
 #ifndef DCTPLUS_B200_DCTPLUS_HPP
 #define DCTPLUS_B200_DCTPLUS_HPP
 
+#include <algorithm>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
@@ -299,6 +300,60 @@ inline PrunedEnsemblePlan plan_pruned(std::size_t n, const std::vector<RankOneUp
 }
 inline PrunedEnsemblePlan::Result pruned_forward_all(const PrunedEnsemblePlan& plan, const std::vector<double>& s) {
     return plan.forward_all(s);
+}
+
+/// fast_transform.hpp:466-496: the member whose coefficients minimise `cost`
+/// (default l1), ties to the lower index, per the threshold branch.
+struct RdoChoice {
+    std::size_t index = 0;
+    std::vector<double> coeffs;
+    bool pruned = false;
+};
+
+template <class Cost>
+RdoChoice rdo_select(const PrunedEnsemblePlan& plan, const std::vector<double>& s, Cost cost) {
+    PrunedEnsemblePlan::Result res = plan.forward_all(s);
+    RdoChoice choice;
+    choice.pruned = res.pruned;
+    double best = cost(res.coeffs[0]);
+    for (std::size_t r = 1; r < res.coeffs.size(); ++r) {
+        const double c = cost(res.coeffs[r]);
+        if (c < best) {
+            best = c;
+            choice.index = r;
+        }
+    }
+    choice.coeffs = std::move(res.coeffs[choice.index]);
+    return choice;
+}
+
+inline RdoChoice rdo_select(const PrunedEnsemblePlan& plan, const std::vector<double>& s) {
+    return rdo_select(plan, s, [](const std::vector<double>& c) {
+        double a = 0.0;
+        for (double v : c) a += std::abs(v);
+        return a;
+    });
+}
+
+/// bench.hpp:99-108: the `quantile` of the path quadratic form over `trials`
+/// AR(r) signals from Rng(mix_seed(seed, n, 9000)).
+inline double calibrate_prune_threshold(std::size_t n, double r = 0.99, double quantile = 0.7,
+                                        std::size_t trials = 512, std::uint64_t seed = 42) {
+    std::vector<double> sig(n * trials);
+    detail::check(dctp_fill_signals(dctp_mix_seed(seed, n, 9000), 2, r, n, trials, sig.data()));
+    std::vector<double> q(trials);
+    for (std::size_t t = 0; t < trials; ++t) {
+        double acc = 0.0;
+        for (std::size_t i = 0; i + 1 < n; ++i) {
+            const double d = sig[t * n + i] - sig[t * n + i + 1];
+            acc += d * d;
+        }
+        q[t] = acc;
+    }
+    std::sort(q.begin(), q.end());
+    const std::size_t idx =
+        std::min(trials - 1, static_cast<std::size_t>(quantile * static_cast<double>(trials - 1)));
+    return q[idx];
 }
 
 } // namespace dctplus_b200

@@ -114,6 +114,24 @@ int main() {
         CHECK(res.pruned);
         for (std::size_t r = 1; r <= 4; ++r) CHECK(snr_db(ens.member(r).forward(s), res.coeffs[r]) >= 100.0);
         CHECK(throws<std::logic_error>([&] { ens.member(0); }));
+        CHECK(rdo_select(ens, std::vector<double>(64, 1.0)).index == 0); // test_pruning.cpp:136-141
+    }
+    // pruned mode (test_pruning.cpp:95-115): the truncation error never exceeds the bound
+    {
+        const std::vector<RankOneUpdate> ups = {RankOneUpdate::self_loop(1, 1.5), RankOneUpdate::edge_delta(2, 3, 1.5)};
+        const PrunedEnsemblePlan ens(32, ups, 16, 1e300);
+        for (int rep = 0; rep < 10; ++rep) {
+            const auto s = ar(32, 0.99, g);
+            const auto res = ens.forward_all(s);
+            CHECK(res.pruned);
+            for (std::size_t r = 1; r < ens.ensemble_size(); ++r) {
+                const auto exact = ens.member(r).forward_nmvp(s);
+                double err = 0.0;
+                for (std::size_t j = 0; j < 32; ++j) err += (exact[j] - res.coeffs[r][j]) * (exact[j] - res.coeffs[r][j]);
+                CHECK(std::sqrt(err) <= res.bounds[r] + 1e-12);
+            }
+        }
+        CHECK(calibrate_prune_threshold(32) > 0.0);
     }
     // batched device rows
     {

@@ -693,12 +693,28 @@ struct HostPipe {
     std::vector<cudaEvent_t> loaded, computed, drained;
     void* buf = nullptr;
     std::size_t buf_bytes = 0;
+
+    HostPipe() = default;
+    HostPipe(const HostPipe&) = delete;
+    HostPipe& operator=(const HostPipe&) = delete;
+    ~HostPipe() { // at thread exit; errors ignored (the context may already be gone at process exit)
+        int prev = 0;
+        if (cudaGetDevice(&prev) != cudaSuccess) return;
+        cudaSetDevice(device);
+        if (buf) cudaFree(buf);
+        for (auto* v : {&loaded, &computed, &drained})
+            for (auto ev : *v) cudaEventDestroy(ev);
+        for (cudaStream_t st : {in, comp, out})
+            if (st) cudaStreamDestroy(st);
+        cudaSetDevice(prev);
+        cudaGetLastError();
+    }
 };
 
 constexpr int kMaxHostSlots = 8;
 
 static HostPipe& host_pipe(int device) {
-    thread_local std::vector<std::unique_ptr<HostPipe>> cache; // one per (thread, device); never freed
+    thread_local std::vector<std::unique_ptr<HostPipe>> cache; // one per (thread, device), freed at thread exit
     for (auto& e : cache)
         if (e->device == device) return *e;
     auto hp = std::make_unique<HostPipe>();

@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2, help="BASELINE config id (2 = the headline workload)")
+    ap.add_argument("--config", type=int, default=2, help="BASELINE config id (2 = the headline workload; 6 = rank-k chain, SURVEY 8f)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -70,11 +70,20 @@ def describe(cfg) -> dict:
             "precision": cfg.dtypes[0], "output_sets": 16 if cfg.progressive else 1}
 
 
+def api_name(cfg) -> str:
+    if cfg.chain:
+        return "chain_forward"
+    return "PrunedEnsemblePlan::forward_all" if cfg.progressive else "DctPlusPlan::forward"
+
+
 def algorithmic(cfg, plan) -> dict:
     """bytes = elem * n * (1 + K_out); flops = 2.5 n log2 n +
     2 * n_kept * n_active * K (the direct Cauchy stage, per signal)."""
     elem = 4 if cfg.dtypes[0] == "f32" else 8
     kout = 16 if cfg.progressive else 1
+    if cfg.chain:  # one dense product with the composed basis, no DCT
+        return {"bytes": elem * cfg.n * 2, "flops_cauchy": 2.0 * cfg.n * cfg.n, "flops_dct": 0.0,
+                "out_samples": cfg.n}
     if cfg.progressive:
         cauchy = sum(2 * m.n_kept * m.n_active for m in (plan.member(r) for r in range(1, 17)))
     else:
@@ -148,7 +157,10 @@ def cpu_reference_rate(cfg, signals: np.ndarray, threads: int = 0, passes: int =
     ref = O.Reference()
     ups = [O.Update(k, rho, i, j, tuple(general_direction(cfg.n)) if k == 2 else None)
            for (k, rho, i, j) in cfg.updates]
-    if cfg.progressive:
+    if cfg.chain:
+        obj = ref.chain(cfg.n, ups)
+        run = lambda: obj.forward(signals, threads=threads)  # noqa: E731
+    elif cfg.progressive:
         obj = ref.ensemble(cfg.n, ups, cfg.n, float(np.finfo(np.float64).max))
         run = lambda: obj.forward_all(signals, threads=threads)  # noqa: E731
     else:
@@ -212,7 +224,7 @@ def run_reference_arm(args, cfg, rank: int):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Rng, seeded)",
         "config": {**describe(cfg), "sample_signals_per_step": rows},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "reference",
-                         "sample": f"{rows} of {cfg.batch} signals per step, reference DctPlusPlan::forward "
+                         "sample": f"{rows} of {cfg.batch} signals per step, reference {api_name(cfg)} "
                                    f"(oracle/_ref, FFTW stand-in), {threads} threads on {cpu_model()}"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -313,7 +325,7 @@ def run_gpu_arm(args, cfg, rank: int, local: int, world: int):
     # for the DCT, per signal; bytes = elem * n * (1 + K_out) per signal.
     flops = (alg["flops_cauchy"] + alg["flops_dct"]) * cfg.batch
     nbytes = alg["bytes"] * cfg.batch
-    t_ms = per_launch_ms[top] if ("fused" in top or "cauchy" in top) else ms_per_step
+    t_ms = per_launch_ms[top] if ("fused" in top or "cauchy" in top or "chain" in top) else ms_per_step
     if f32:
         peak = max(fp.get("fp32_fma_tflops") or 0.0, fp.get("fp32_ffma2_tflops") or 0.0) or None
         src = "profiles/peaks_fp64.json max(fp32_fma_tflops, fp32_ffma2_tflops) (tools/peaks.cu, measured)"
@@ -362,7 +374,9 @@ def run_gpu_arm(args, cfg, rank: int, local: int, world: int):
     from paper_2409_08970_b200._native import check, lib
 
     def e2e_call():
-        if cfg.progressive:
+        if cfg.chain:
+            fn = lib.dctp_chain_forward_host_f32 if dtype == torch.float32 else lib.dctp_chain_forward_host_f64
+        elif cfg.progressive:
             fn = lib.dctp_ensemble_forward_all_host_f32 if dtype == torch.float32 else lib.dctp_ensemble_forward_all_host_f64
         else:
             fn = lib.dctp_forward_host_f32 if dtype == torch.float32 else lib.dctp_forward_host_f64
@@ -390,8 +404,8 @@ def run_gpu_arm(args, cfg, rank: int, local: int, world: int):
             sig = P.fill_signals(cfg.seed, cfg.dist, cfg.n, rows, cfg.r)
             dt = cpu_reference_rate(cfg, sig, threads, passes=2)
             cpu = {"value": rows * alg["out_samples"] / dt, "unit": "samples/s", "cores": threads, "kind": "reference",
-                   "sample": f"{rows} of {cfg.batch} signals, reference DctPlusPlan::"
-                             f"{'forward_all' if cfg.progressive else 'forward'} (oracle/_ref, FFTW stand-in), "
+                   "sample": f"{rows} of {cfg.batch} signals, reference "
+                             f"{api_name(cfg)} (oracle/_ref, FFTW stand-in), "
                              f"min of 2 passes, {threads} threads on {cpu_model()}"}
         except Exception as e:  # reference not built on this box
             cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}

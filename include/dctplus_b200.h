@@ -54,6 +54,7 @@ typedef enum dctp_update_kind {
 
 typedef struct dctp_plan dctp_plan;
 typedef struct dctp_ensemble dctp_ensemble;
+typedef struct dctp_chain dctp_chain;
 
 /* Message of the calling thread's last failure ("" if none). */
 const char* dctp_last_error(void);
@@ -150,6 +151,36 @@ int dctp_ensemble_forward_all_pruned_host_f32(const dctp_ensemble* ens, const fl
                                               float* h_bounds, unsigned char* h_pruned, size_t batch);
 int dctp_ensemble_forward_all_host_f32(const dctp_ensemble* ens, const float* h_in, float* h_out, size_t batch);
 int dctp_ensemble_forward_all_host_f64(const dctp_ensemble* ens, const double* h_in, double* h_out, size_t batch);
+
+/* --- rank-k chains (cauchy.hpp:159-231) ------------------------------------ */
+
+/* compose_rank_k(base, updates, tau) (cauchy.hpp:175-216): k >= 1 rank-one
+ * updates (parallel arrays as in dctp_ensemble_create) applied in order on top
+ * of a base spectrum: base_lambda (n, ascending) and base_u (n x n row-major,
+ * column k = eigenvector k), or both NULL for path_spectrum(n)
+ * (spectral.hpp:48-68).  The composition runs on the host and reproduces the
+ * reference's final basis and eigenvalues bit for bit; a failing stage r
+ * returns DCTP_RUNTIME_ERROR with "compose_rank_k: stage r: ..." as the
+ * reference throws it.  device < 0: host-only chain (no apply). */
+int dctp_chain_create(size_t n, size_t k, const int* kinds, const size_t* is, const size_t* js,
+                      const double* rhos, const double* vs, const double* base_lambda, const double* base_u,
+                      double tau, int device, dctp_chain** out);
+int dctp_chain_destroy(dctp_chain* chain);
+int dctp_chain_info(const dctp_chain* chain, size_t* n, size_t* stages);
+/* ChainedFactorization::mu (n, ascending) and ::x (n x n row-major, signed);
+ * either may be NULL. */
+int dctp_chain_spectrum(const dctp_chain* chain, double* mu, double* x);
+/* Stage r (0-based) of ::stages: base_vals (n), spec.mu (n), sigma (n),
+ * spec.slots (passthrough, idx; n each), number of deflation rotations; all
+ * NULL-able. */
+int dctp_chain_stage(const dctp_chain* chain, size_t r, double* base_vals, double* mu, double* sigma,
+                     int* passthrough, int64_t* idx, size_t* n_rotations);
+/* chain_forward (cauchy.hpp:218-231) for batch x n device rows: out = in X. */
+int dctp_chain_forward_f64(const dctp_chain* chain, const double* d_in, double* d_out, size_t batch, void* stream);
+int dctp_chain_forward_f32(const dctp_chain* chain, const float* d_in, float* d_out, size_t batch, void* stream);
+int dctp_chain_sync_check(const dctp_chain* chain, void* stream);
+int dctp_chain_forward_host_f64(const dctp_chain* chain, const double* h_in, double* h_out, size_t batch);
+int dctp_chain_forward_host_f32(const dctp_chain* chain, const float* h_in, float* h_out, size_t batch);
 
 /* --- batched trig kernels (trig.hpp:95-110), orthonormal ------------------ */
 int dctp_dct2_f64(size_t n, const double* d_in, double* d_out, size_t batch, int device, void* stream);

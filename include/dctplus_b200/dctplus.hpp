@@ -12,7 +12,8 @@
 //   * batched device-pointer entry points (forward_batch / inverse_batch /
 //     forward_all_batch) take rows of signals and a cudaStream_t (as void*);
 //   * RankOneUpdate::general(v, rho) extends the two reference update kinds;
-//   * PrunedEnsemblePlan supports the progressive mode c_p = n only.
+//   * ChainedFactorization keeps x, mu and per-stage data; chain_forward runs
+//     one product with x on the GPU (chain_forward_batch for device rows).
 #ifndef DCTPLUS_B200_DCTPLUS_HPP
 #define DCTPLUS_B200_DCTPLUS_HPP
 
@@ -354,6 +355,105 @@ inline double calibrate_prune_threshold(std::size_t n, double r = 0.99, double q
     const std::size_t idx =
         std::min(trials - 1, static_cast<std::size_t>(quantile * static_cast<double>(trials - 1)));
     return q[idx];
+}
+
+// --- rank-k chains (cauchy.hpp:159-231) -------------------------------------
+
+/// L = U diag(lambda) U^T (spectral.hpp:21-24); u row-major n x n, column k =
+/// eigenvector k (the reference's Matrix u(j, k) flattened by rows).
+struct SpectralBasis {
+    std::vector<double> lambda;
+    std::vector<double> u;
+    bool path = false; // path_spectrum(n): rebuilt by the library with the reference's rounding
+};
+
+/// path_spectrum (spectral.hpp:48-68).
+inline SpectralBasis path_spectrum(std::size_t n) {
+    if (n < 2) throw std::invalid_argument("path_spectrum: need n >= 2");
+    SpectralBasis b;
+    const double pi = 3.14159265358979323846, nd = static_cast<double>(n), scale = std::sqrt(2.0 / nd);
+    b.lambda.resize(n);
+    b.u.resize(n * n);
+    for (std::size_t k = 0; k < n; ++k) {
+        b.lambda[k] = 2.0 - 2.0 * std::cos(static_cast<double>(k) * pi / nd);
+        const double ck = (k == 0) ? 1.0 / std::sqrt(2.0) : 1.0;
+        for (std::size_t j = 0; j < n; ++j)
+            b.u[j * n + k] =
+                ck * scale * std::cos(pi * static_cast<double>(k) * (2.0 * static_cast<double>(j) + 1.0) / (2.0 * nd));
+    }
+    b.lambda[0] = 0.0;
+    b.path = true;
+    return b;
+}
+
+/// compose_rank_k's result (cauchy.hpp:163-173): final signed basis x
+/// (row-major), final eigenvalues mu, and the stage count.
+class ChainedFactorization {
+  public:
+    ChainedFactorization(const SpectralBasis& base, const std::vector<RankOneUpdate>& updates, double tau = 1e-12,
+                         int device = 0) {
+        n = base.lambda.size();
+        const std::size_t k = updates.size();
+        std::vector<int> kinds(k);
+        std::vector<std::size_t> is(k), js(k);
+        std::vector<double> rhos(k), vs;
+        bool any_general = false;
+        for (std::size_t r = 0; r < k; ++r) {
+            kinds[r] = updates[r].abi_kind();
+            is[r] = updates[r].node_i;
+            js[r] = updates[r].node_j;
+            rhos[r] = updates[r].rho;
+            any_general |= updates[r].kind == RankOneUpdate::Kind::general;
+        }
+        if (any_general) {
+            vs.assign(k * n, 0.0);
+            for (std::size_t r = 0; r < k; ++r)
+                if (updates[r].kind == RankOneUpdate::Kind::general) {
+                    if (updates[r].v.size() != n)
+                        throw std::runtime_error("compose_rank_k: stage " + std::to_string(r + 1) +
+                                                 ": RankOneUpdate: direction length mismatch");
+                    std::copy(updates[r].v.begin(), updates[r].v.end(), vs.begin() + static_cast<std::ptrdiff_t>(r * n));
+                }
+        }
+        dctp_chain* h = nullptr;
+        detail::check(dctp_chain_create(n, k, kinds.data(), is.data(), js.data(), rhos.data(),
+                                        any_general ? vs.data() : nullptr, base.path ? nullptr : base.lambda.data(),
+                                        base.path ? nullptr : base.u.data(), tau, device, &h));
+        h_.reset(h, [](dctp_chain* c) { dctp_chain_destroy(c); });
+        mu.resize(n);
+        x.resize(n * n);
+        detail::check(dctp_chain_spectrum(h, mu.data(), x.data()));
+        stages = k;
+    }
+
+    std::size_t n = 0, stages = 0;
+    std::vector<double> x, mu;
+
+    /// chain_forward for device rows (batch x n), on `stream`.
+    void forward_batch(const double* d_in, double* d_out, std::size_t batch, void* stream = nullptr) const {
+        detail::check(dctp_chain_forward_f64(h_.get(), d_in, d_out, batch, stream));
+    }
+    void forward_batch(const float* d_in, float* d_out, std::size_t batch, void* stream = nullptr) const {
+        detail::check(dctp_chain_forward_f32(h_.get(), d_in, d_out, batch, stream));
+    }
+    void sync_check(void* stream = nullptr) const { detail::check(dctp_chain_sync_check(h_.get(), stream)); }
+    const dctp_chain* handle() const { return h_.get(); }
+
+  private:
+    std::shared_ptr<dctp_chain> h_;
+};
+
+inline ChainedFactorization compose_rank_k(const SpectralBasis& base, const std::vector<RankOneUpdate>& updates,
+                                           double tau = 1e-12) {
+    return ChainedFactorization(base, updates, tau);
+}
+
+/// chain_forward (cauchy.hpp:218-231) of one host signal.
+inline std::vector<double> chain_forward(const ChainedFactorization& f, const std::vector<double>& s) {
+    if (s.size() != f.n) throw std::invalid_argument("chain_forward: size mismatch");
+    std::vector<double> out(f.n);
+    detail::check(dctp_chain_forward_host_f64(f.handle(), s.data(), out.data(), 1));
+    return out;
 }
 
 } // namespace dctplus_b200

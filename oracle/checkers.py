@@ -237,6 +237,11 @@ class Reference:
             lib.ref_calibrate_prune_threshold.restype = C.c_double
             lib.ref_calibrate_prune_threshold.argtypes = [C.c_size_t, C.c_double, C.c_double, C.c_size_t,
                                                           C.c_uint64]
+            lib.ref_chain_create.argtypes = [C.c_size_t, C.c_size_t] + [C.c_void_p] * 7 + [C.c_double,
+                                                                                         C.POINTER(C.c_void_p)]
+            lib.ref_chain_destroy.argtypes = [C.c_void_p]
+            lib.ref_chain_spectrum.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_size_t)]
+            lib.ref_chain_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
             lib.ref_trig.argtypes = [C.c_int, C.c_size_t, C.c_void_p, C.c_void_p, C.c_size_t]
             lib.ref_mix_seed.restype = C.c_uint64
             lib.ref_mix_seed.argtypes = [C.c_uint64, C.c_size_t, C.c_size_t]
@@ -267,6 +272,22 @@ class Reference:
         self._check(self.lib.ref_ensemble_create(n, k, _ptr(kinds), _ptr(is_), _ptr(js), _ptr(rhos), _ptr(vs), cp,
                                                  thr, eps, C.byref(h)))
         return RefEnsemble(self, h, n, k)
+
+    def chain(self, n: int, ups: Sequence[Update], base=None, tau: float = 1e-12) -> "RefChain":
+        """compose_rank_k(base or path_spectrum(n), ups, tau); base = (lambda, u)."""
+        kinds = np.array([u.kind for u in ups], dtype=np.int32)
+        is_ = np.array([u.i for u in ups], dtype=np.uint64)
+        js = np.array([u.j for u in ups], dtype=np.uint64)
+        rhos = np.array([u.rho for u in ups], dtype=np.float64)
+        vs = np.stack([direction(u, n) for u in ups]) if any(u.kind == 2 for u in ups) else None
+        bl = bu = None
+        if base is not None:
+            bl = np.ascontiguousarray(base[0], dtype=np.float64)
+            bu = np.ascontiguousarray(base[1], dtype=np.float64)
+        h = C.c_void_p()
+        self._check(self.lib.ref_chain_create(n, len(ups), _ptr(kinds), _ptr(is_), _ptr(js), _ptr(rhos), _ptr(vs),
+                                              _ptr(bl), _ptr(bu), tau, C.byref(h)))
+        return RefChain(self, h, n)
 
     def trig(self, kind: int, x: np.ndarray) -> np.ndarray:
         x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
@@ -354,6 +375,28 @@ class RefEnsemble:
         pr = np.empty(s.shape[0], dtype=np.int32)
         self.ref._check(self.ref.lib.ref_rdo_select(self.h, _ptr(s), _ptr(idx), _ptr(pr), s.shape[0]))
         return idx, pr
+
+
+class RefChain:
+    def __init__(self, ref: Reference, h, n: int):
+        self.ref, self.h, self.n = ref, h, n
+
+    def __del__(self):
+        if self.h is not None:
+            self.ref.lib.ref_chain_destroy(self.h)
+            self.h = None
+
+    def spectrum(self):
+        """(mu, x, number of stages) of the ChainedFactorization."""
+        mu, x, k = np.empty(self.n), np.empty((self.n, self.n)), C.c_size_t()
+        self.ref.lib.ref_chain_spectrum(self.h, _ptr(mu), _ptr(x), C.byref(k))
+        return mu, x, k.value
+
+    def forward(self, s: np.ndarray, threads: int = 0) -> np.ndarray:
+        s = np.ascontiguousarray(np.atleast_2d(s), dtype=np.float64)
+        out = np.empty_like(s)
+        self.ref._check(self.ref.lib.ref_chain_forward(self.h, _ptr(s), _ptr(out), s.shape[0], threads))
+        return out
 
 
 def parity(y: np.ndarray, ref: np.ndarray) -> float:

@@ -252,6 +252,63 @@ int ref_rdo_select(const void* pv, const double* s, int* index, int* pruned, std
     }
 }
 
+/// compose_rank_k (cauchy.hpp:175-216) on path_spectrum(n) (base NULL) or a
+/// caller's base (lambda n, u n x n row-major).
+int ref_chain_create(std::size_t n, std::size_t k, const int* kinds, const std::size_t* is, const std::size_t* js,
+                     const double* rhos, const double* vs, const double* base_lambda, const double* base_u,
+                     double tau, void** out) {
+    try {
+        std::vector<RankOneUpdate> ups;
+        for (std::size_t r = 0; r < k; ++r)
+            ups.push_back(make_update(kinds[r], is[r], js[r], rhos[r], vs ? vs + r * n : nullptr, n));
+        SpectralBasis base;
+        if (base_lambda) {
+            base.lambda.assign(base_lambda, base_lambda + n);
+            base.u = Matrix(n, n);
+            for (std::size_t i = 0; i < n; ++i)
+                for (std::size_t j = 0; j < n; ++j) base.u(i, j) = base_u[i * n + j];
+        } else {
+            base = path_spectrum(n);
+        }
+        *out = new ChainedFactorization(compose_rank_k(base, ups, tau));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+void ref_chain_destroy(void* p) { delete static_cast<ChainedFactorization*>(p); }
+
+/// ChainedFactorization::mu, ::x (row-major), stage count.
+int ref_chain_spectrum(const void* pv, double* mu, double* x, std::size_t* stages) {
+    const auto* c = static_cast<const ChainedFactorization*>(pv);
+    const std::size_t n = c->n;
+    for (std::size_t i = 0; i < n; ++i) {
+        mu[i] = c->mu[i];
+        for (std::size_t j = 0; j < n; ++j) x[i * n + j] = c->x(i, j);
+    }
+    *stages = c->stages.size();
+    return 0;
+}
+
+/// chain_forward (cauchy.hpp:218-231) per signal.
+int ref_chain_forward(const void* pv, const double* s, double* out, std::size_t batch, int threads) {
+    try {
+        const auto* c = static_cast<const ChainedFactorization*>(pv);
+        const std::size_t n = c->n;
+        parallel_slices(batch, threads, [&](std::size_t b0, std::size_t b1) {
+            for (std::size_t b = b0; b < b1; ++b) {
+                const std::vector<double> sig(s + b * n, s + (b + 1) * n);
+                const std::vector<double> p = chain_forward(*c, sig);
+                std::copy(p.begin(), p.end(), out + b * n);
+            }
+        });
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 /// bench.hpp:99-108.
 double ref_calibrate_prune_threshold(std::size_t n, double r, double quantile, std::size_t trials,
                                      std::uint64_t seed) {

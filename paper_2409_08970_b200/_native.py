@@ -61,6 +61,16 @@ SIGNATURES = {
     "dctp_ensemble_forward_all_pruned_host_f32": (C.c_int, [_p, _p, _p, _p, _p, _sz]),
     "dctp_ensemble_forward_all_host_f32": (C.c_int, [_p, _p, _p, _sz]),
     "dctp_ensemble_forward_all_host_f64": (C.c_int, [_p, _p, _p, _sz]),
+    "dctp_chain_create": (C.c_int, [_sz, _sz, _p, _p, _p, _p, _p, _p, _p, C.c_double, C.c_int, C.POINTER(_p)]),
+    "dctp_chain_destroy": (C.c_int, [_p]),
+    "dctp_chain_info": (C.c_int, [_p, C.POINTER(_sz), C.POINTER(_sz)]),
+    "dctp_chain_spectrum": (C.c_int, [_p, _p, _p]),
+    "dctp_chain_stage": (C.c_int, [_p, _sz, _p, _p, _p, _p, _p, C.POINTER(_sz)]),
+    "dctp_chain_forward_f64": (C.c_int, [_p, _p, _p, _sz, _p]),
+    "dctp_chain_forward_f32": (C.c_int, [_p, _p, _p, _sz, _p]),
+    "dctp_chain_sync_check": (C.c_int, [_p, _p]),
+    "dctp_chain_forward_host_f64": (C.c_int, [_p, _p, _p, _sz]),
+    "dctp_chain_forward_host_f32": (C.c_int, [_p, _p, _p, _sz]),
     "dctp_dct2_f64": (C.c_int, [_sz, _p, _p, _sz, C.c_int, _p]),
     "dctp_idct2_f64": (C.c_int, [_sz, _p, _p, _sz, C.c_int, _p]),
     "dctp_dct2_f32": (C.c_int, [_sz, _p, _p, _sz, C.c_int, _p]),

@@ -24,10 +24,11 @@ class Workload:
     updates: Tuple     # ((kind, rho, i, j), ...) 1-based; kind 2 = general (direction below)
     dtypes: Tuple[str, ...]
     inverse: bool = False
+    chain: bool = False  # rank-k chain (compose_rank_k) instead of an ensemble
 
     @property
     def progressive(self) -> bool:
-        return len(self.updates) > 1
+        return len(self.updates) > 1 and not self.chain
 
     @property
     def seed(self) -> int:
@@ -54,6 +55,10 @@ WORKLOADS = {
                 tuple((0, 0.05 + k * (1.95 / 15.0), 1, 0) for k in range(16)), ("f32",)),
     5: Workload(5, "C5 n=8192 general u~N(0,1/n) rho=0.1 fwd fp64 batch 2048", 8192, 2048, 0, 0.0,
                 ((2, 0.1, 0, 0),), ("f64",)),
+    # not a BASELINE config: the rank-k chain row of SURVEY.md 8(f)
+    6: Workload(6, "X6 n=1024 chain self_loop(1,1.5)+edge_delta(1,1024,-0.5)+edge_delta(300,700,0.25) fwd fp64 "
+                   "batch 16384", 1024, 16384, 2, 0.95,
+                ((0, 1.5, 1, 0), (1, -0.5, 1, 1024), (1, 0.25, 300, 700)), ("f64",), chain=True),
 }
 
 
@@ -69,8 +74,10 @@ def make_update(u):
 
 
 def make_plan(w: Workload, device: int = 0):
-    from .dctplus import DctPlusPlan, PrunedEnsemblePlan
+    from .dctplus import ChainedFactorization, DctPlusPlan, PrunedEnsemblePlan
 
+    if w.chain:
+        return ChainedFactorization(w.n, [make_update(u) for u in w.updates], device=device)
     if w.progressive:
         return PrunedEnsemblePlan(w.n, [make_update(u) for u in w.updates], w.n, 1.7e308, device=device)
     return DctPlusPlan(w.n, make_update(w.updates[0]), 1e-12, device=device)

@@ -19,10 +19,12 @@
 #include <numbers>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include <cuda_runtime_api.h>
 
+#include "host/chain.hpp"
 #include "host/setup.hpp"
 #include "host/signal.hpp"
 #include "kernels/launch.hpp"
@@ -1276,6 +1278,174 @@ int dctp_ensemble_forward_all_host_f64(const dctp_ensemble* e, const double* h_i
 }
 
 // --- bare trig kernels ------------------------------------------------------------
+
+} // extern "C"
+
+// --- rank-k chains -------------------------------------------------------------
+
+struct dctp_chain {
+    dctp::host::Chain ch;
+    int device = 0;
+    void* blob = nullptr; // X^T in fp64 (ld even), X in fp32 for the SGEMM route
+    int* flag = nullptr;
+    std::size_t ldt = 0, xt64 = 0, x32 = 0;
+    bool sgemm32 = false;
+
+    ~dctp_chain() {
+        if (blob) {
+            int prev = 0;
+            cudaGetDevice(&prev);
+            cudaSetDevice(device);
+            cudaFree(blob);
+            cudaFree(flag);
+            cudaSetDevice(prev);
+        }
+    }
+};
+
+/// chain_forward (cauchy.hpp:218-231) for a batch: out = in X, one product
+/// with the composed basis (fp64 on DMMA; fp32 as an SGEMM when the shape
+/// allows, else widened through the DMMA kernel).
+template <class T>
+static void chain_forward(const dctp_chain* c, const T* in, T* out, std::size_t batch, cudaStream_t s) {
+    if (!c) throw std::invalid_argument("chain_forward: null chain");
+    if (!c->blob) throw std::invalid_argument("ChainedFactorization: host-only chain (created with device < 0)");
+    if (batch == 0) return;
+    if (!in || !out) throw std::invalid_argument("chain_forward: null buffer");
+    DeviceScope scope(c->device);
+    const std::size_t n = c->ch.n;
+    const int ni = static_cast<int>(n);
+    if constexpr (std::is_same_v<T, float>) {
+        const float* x = at<float>(c->blob, c->x32);
+        if (c->sgemm32 && dctp::dev::sgemm_rows_supported(ni, ni, ni, ni, n, in, x, out)) {
+            cuda_check(DCTP_LAUNCH("chain_sgemm", s,
+                                   dctp::dev::sgemm_rows(in, ni, x, ni, out, n, batch, ni, ni, c->flag, s)),
+                       "chain sgemm kernel");
+            return;
+        }
+    }
+    cuda_check(DCTP_LAUNCH("chain_dmma", s,
+                           dctp::dev::rows_by_basis<T>(in, n, at<double>(c->blob, c->xt64), c->ldt, ni, ni, out, n,
+                                                       batch, c->flag, s)),
+               "chain dmma kernel");
+}
+
+extern "C" {
+
+int dctp_chain_create(size_t n, size_t k, const int* kinds, const size_t* is, const size_t* js, const double* rhos,
+                      const double* vs, const double* base_lambda, const double* base_u, double tau, int device,
+                      dctp_chain** out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("dctp_chain_create: null output");
+        *out = nullptr;
+        if (k > 0 && (!kinds || !is || !js || !rhos)) throw std::invalid_argument("dctp_chain_create: null update arrays");
+        if (!base_lambda != !base_u) throw std::invalid_argument("dctp_chain_create: give both base arrays or neither");
+        if (n > (std::size_t{1} << 14)) throw std::invalid_argument("dctp_chain_create: n above 16384");
+        std::vector<dctp::host::Update> ups;
+        for (std::size_t r = 0; r < k; ++r) {
+            try {
+                ups.push_back(make_update(kinds[r], is[r], js[r], rhos[r], vs ? vs + r * n : nullptr, n));
+            } catch (const std::exception& ex) {
+                throw std::runtime_error("compose_rank_k: stage " + std::to_string(r + 1) + ": " + ex.what());
+            }
+        }
+        auto c = std::make_unique<dctp_chain>();
+        c->device = device;
+        c->ch = dctp::host::compose_rank_k(
+            n, ups, base_lambda ? std::vector<double>(base_lambda, base_lambda + n) : std::vector<double>{},
+            base_u ? std::vector<double>(base_u, base_u + n * n) : std::vector<double>{}, tau);
+        if (device >= 0) {
+            c->ldt = (n + 3) / 4 * 4;
+            std::vector<double> xt(n * c->ldt, 0.0);
+            std::vector<float> x32(n * n);
+            for (std::size_t i = 0; i < n; ++i)
+                for (std::size_t j = 0; j < n; ++j) {
+                    xt[j * c->ldt + i] = c->ch.x[i * n + j];
+                    x32[i * n + j] = static_cast<float>(c->ch.x[i * n + j]);
+                }
+            c->sgemm32 = n % 16 == 0 && n <= 4096;
+            Blob blob;
+            c->xt64 = blob.add(xt);
+            if (c->sgemm32) c->x32 = blob.add(x32);
+            DeviceScope scope(device);
+            prepare_pool(device);
+            c->blob = blob.upload();
+            cuda_check(cudaMalloc(reinterpret_cast<void**>(&c->flag), sizeof(int)), "cudaMalloc(flag)");
+            cuda_check(cudaMemset(c->flag, 0, sizeof(int)), "cudaMemset(flag)");
+        }
+        *out = c.release();
+    });
+}
+
+int dctp_chain_destroy(dctp_chain* c) {
+    return guarded([&] { delete c; });
+}
+
+int dctp_chain_info(const dctp_chain* c, size_t* n, size_t* stages) {
+    return guarded([&] {
+        if (!c) throw std::invalid_argument("dctp_chain_info: null chain");
+        if (n) *n = c->ch.n;
+        if (stages) *stages = c->ch.stages.size();
+    });
+}
+
+int dctp_chain_spectrum(const dctp_chain* c, double* mu, double* x) {
+    return guarded([&] {
+        if (!c) throw std::invalid_argument("dctp_chain_spectrum: null chain");
+        if (mu) std::copy(c->ch.mu.begin(), c->ch.mu.end(), mu);
+        if (x) std::copy(c->ch.x.begin(), c->ch.x.end(), x);
+    });
+}
+
+int dctp_chain_stage(const dctp_chain* c, size_t r, double* base_vals, double* mu, double* sigma, int* passthrough,
+                     int64_t* idx, size_t* n_rotations) {
+    return guarded([&] {
+        if (!c) throw std::invalid_argument("dctp_chain_stage: null chain");
+        if (r >= c->ch.stages.size()) throw std::out_of_range("dctp_chain_stage: stage index out of range");
+        const auto& st = c->ch.stages[r];
+        if (base_vals) std::copy(st.base_vals.begin(), st.base_vals.end(), base_vals);
+        if (mu) std::copy(st.spec.mu.begin(), st.spec.mu.end(), mu);
+        if (sigma) std::copy(st.sigma.begin(), st.sigma.end(), sigma);
+        for (std::size_t q = 0; q < st.spec.slots.size(); ++q) {
+            if (passthrough) passthrough[q] = st.spec.slots[q].passthrough ? 1 : 0;
+            if (idx) idx[q] = static_cast<int64_t>(st.spec.slots[q].idx);
+        }
+        if (n_rotations) *n_rotations = st.spec.rotations.size();
+    });
+}
+
+int dctp_chain_forward_f64(const dctp_chain* c, const double* in, double* out, size_t batch, void* stream) {
+    return guarded([&] { chain_forward<double>(c, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_chain_forward_f32(const dctp_chain* c, const float* in, float* out, size_t batch, void* stream) {
+    return guarded([&] { chain_forward<float>(c, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+
+int dctp_chain_sync_check(const dctp_chain* c, void* stream) {
+    return guarded([&] {
+        if (!c) throw std::invalid_argument("dctp_chain_sync_check: null chain");
+        if (!c->blob) throw std::invalid_argument("ChainedFactorization: host-only chain (created with device < 0)");
+        sync_check(c->device, c->flag, static_cast<cudaStream_t>(stream));
+    });
+}
+
+#define DCTP_CHAIN_HOST_ENTRY(NAME, T)                                                                  \
+    int NAME(const dctp_chain* c, const T* h_in, T* h_out, size_t batch) {                             \
+        return guarded([&] {                                                                           \
+            if (!c) throw std::invalid_argument(#NAME ": null chain");                                 \
+            if (!c->blob) throw std::invalid_argument("ChainedFactorization: host-only chain (created with device < 0)"); \
+            if (batch == 0) return;                                                                    \
+            const std::size_t n = c->ch.n;                                                             \
+            host_roundtrip<T>(c->device, batch, n, n, h_in, h_out,                                     \
+                              [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) {          \
+                                  chain_forward<T>(c, din, dout, rows, s);                             \
+                              });                                                                      \
+            sync_check(c->device, c->flag, nullptr);                                                   \
+        });                                                                                            \
+    }
+DCTP_CHAIN_HOST_ENTRY(dctp_chain_forward_host_f64, double)
+DCTP_CHAIN_HOST_ENTRY(dctp_chain_forward_host_f32, float)
+#undef DCTP_CHAIN_HOST_ENTRY
 
 } // extern "C"
 

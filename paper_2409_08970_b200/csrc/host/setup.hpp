@@ -251,9 +251,16 @@ inline std::vector<double> secular_roots(const std::vector<double>& lam, const s
 
 // --- deflation and normalisers (spectral.hpp:242-315) ---------------------------
 
+/// Givens rotation of two base columns: u_into' = c u_into + s u_from,
+/// u_from' = -s u_into + c u_from (spectral.hpp:236-250).
+struct Rotation {
+    std::size_t into, from;
+    double c, s;
+};
+
 struct Deflated {
     std::vector<std::size_t> kept, passed;
-    std::size_t rotations = 0;
+    std::vector<Rotation> rotations;
     std::vector<double> z; // zero at passed indices
 };
 
@@ -271,9 +278,10 @@ inline Deflated deflate(const std::vector<double>& lam, const std::vector<double
     for (std::size_t j = 1; j <= n; ++j) {
         if (j < n && lam[j] - lam[j - 1] <= gap_tol) continue;
         for (std::size_t k = first + 1; k < j; ++k) {
-            const double h = std::hypot(d.z[first], d.z[k]);
+            const double zf = d.z[first], zk = d.z[k];
+            const double h = std::hypot(zf, zk);
             if (h > 0.0) {
-                ++d.rotations;
+                d.rotations.push_back({first, k, zf / h, zk / h});
                 d.z[first] = h;
             }
             d.z[k] = 0.0;
@@ -333,12 +341,64 @@ inline double sign_of_column(const double* col, std::size_t n) {
     return 1.0;
 }
 
-// --- the assembled setup (fast_transform.hpp:45-134) -----------------------------
+// --- perturbed spectrum (spectral.hpp:318-381) -----------------------------------
 
 struct Slot {
     bool passthrough;
     std::size_t idx; // passthrough: DCT index; active: rank in the secular subproblem
 };
+
+/// perturb_spectrum (spectral.hpp:340-381): deflate, solve the secular
+/// subproblem, and merge pass-through eigenvalues with the roots into one
+/// ascending list of slots.
+struct Perturbed {
+    std::vector<double> z, mu, a; // z deflated; a per slot (1 for pass-through)
+    std::vector<Slot> slots;
+    std::vector<Rotation> rotations;
+    std::vector<std::size_t> kept, passed;
+    std::vector<double> sub_lambda, sub_z, sub_mu;
+};
+
+inline Perturbed perturb_spectrum(const std::vector<double>& lam, const std::vector<double>& z, double rho,
+                                  double tau) {
+    Perturbed p;
+    Deflated d = deflate(lam, z, tau);
+    p.z = std::move(d.z);
+    p.kept = std::move(d.kept);
+    p.passed = std::move(d.passed);
+    p.rotations = std::move(d.rotations);
+    for (std::size_t j : p.kept) {
+        p.sub_lambda.push_back(lam[j]);
+        p.sub_z.push_back(p.z[j]);
+    }
+    if (!p.sub_lambda.empty()) p.sub_mu = secular_roots(p.sub_lambda, p.sub_z, rho);
+    const std::vector<double> sub_a =
+        p.sub_mu.empty() ? std::vector<double>{} : normalisers(p.sub_lambda, p.sub_mu, p.sub_z);
+
+    std::size_t ip = 0, ia = 0;
+    const std::size_t n = lam.size();
+    p.mu.reserve(n);
+    p.slots.reserve(n);
+    p.a.reserve(n);
+    while (ip < p.passed.size() || ia < p.sub_mu.size()) {
+        const bool pass_first =
+            ia == p.sub_mu.size() || (ip < p.passed.size() && lam[p.passed[ip]] <= p.sub_mu[ia]);
+        if (pass_first) {
+            p.mu.push_back(lam[p.passed[ip]]);
+            p.slots.push_back({true, p.passed[ip]});
+            p.a.push_back(1.0);
+            ++ip;
+        } else {
+            p.mu.push_back(p.sub_mu[ia]);
+            p.slots.push_back({false, ia});
+            p.a.push_back(sub_a[ia]);
+            ++ia;
+        }
+    }
+    return p;
+}
+
+// --- the assembled setup (fast_transform.hpp:45-134) -----------------------------
 
 struct Setup {
     std::size_t n = 0;
@@ -388,40 +448,15 @@ inline Setup build_setup(std::size_t n, const Update& update, double epsilon, do
         dct.execute(v.data(), st.z_raw.data(), scratch.data());
     }
 
-    // perturb_spectrum (spectral.hpp:340-381)
-    Deflated d = deflate(st.lambda, st.z_raw, tau);
-    if (d.rotations != 0) throw std::logic_error("DctPlusPlan: path eigenvalues cannot repeat");
-    st.z = d.z;
-    st.kept = d.kept;
-    st.passed = d.passed;
-    std::vector<double> sub_lambda, sub_z;
-    for (std::size_t j : st.kept) {
-        sub_lambda.push_back(st.lambda[j]);
-        sub_z.push_back(st.z[j]);
-    }
-    if (!sub_lambda.empty()) st.sub_mu = secular_roots(sub_lambda, sub_z, update.rho);
-    const std::vector<double> sub_a =
-        st.sub_mu.empty() ? std::vector<double>{} : normalisers(sub_lambda, st.sub_mu, sub_z);
-
-    std::size_t ip = 0, ia = 0;
-    st.mu.reserve(n);
-    st.slots.reserve(n);
-    st.a.reserve(n);
-    while (ip < st.passed.size() || ia < st.sub_mu.size()) {
-        const bool pass_first = ia == st.sub_mu.size() ||
-                                (ip < st.passed.size() && st.lambda[st.passed[ip]] <= st.sub_mu[ia]);
-        if (pass_first) {
-            st.mu.push_back(st.lambda[st.passed[ip]]);
-            st.slots.push_back({true, st.passed[ip]});
-            st.a.push_back(1.0);
-            ++ip;
-        } else {
-            st.mu.push_back(st.sub_mu[ia]);
-            st.slots.push_back({false, ia});
-            st.a.push_back(sub_a[ia]);
-            ++ia;
-        }
-    }
+    Perturbed ps = perturb_spectrum(st.lambda, st.z_raw, update.rho, tau);
+    if (!ps.rotations.empty()) throw std::logic_error("DctPlusPlan: path eigenvalues cannot repeat");
+    st.z = std::move(ps.z);
+    st.kept = std::move(ps.kept);
+    st.passed = std::move(ps.passed);
+    st.sub_mu = std::move(ps.sub_mu);
+    st.mu = std::move(ps.mu);
+    st.slots = std::move(ps.slots);
+    st.a = std::move(ps.a);
 
     // Column signs from the materialised basis, one inverse DCT per column
     // (cauchy.hpp:84-103 through fast_transform.hpp:72-84).

@@ -47,9 +47,9 @@ cauchy_dmma_kernel(const double* __restrict__ in, std::size_t ld_in, double* __r
     double* Bs = As + 2 * BM * LDS_;                  // 2 x BN x LDS_ (transposed: [c][k])
     double* ys = Bs + 2 * BN * LDS_;                  // BN: the tile's column nodes y_c
     const CauchyStage st = stages[blockIdx.z];
-    const int c0 = blockIdx.y * BN;
+    const int c0 = blockIdx.x * BN; // column tiles fastest: CTAs sharing a row tile run together (A from L2)
     if (c0 >= st.cols) return;
-    const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * BM;
+    const std::size_t b0 = static_cast<std::size_t>(blockIdx.y) * BM;
     const double* rscale = static_cast<const double*>(st.rscale);
     const double* cscale = static_cast<const double*>(st.cscale);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -188,12 +188,19 @@ cudaError_t cauchy_rows_dmma(const double* in, std::size_t ld_in, double* out, s
     static const cudaError_t attr =
         cudaFuncSetAttribute(cauchy_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (attr != cudaSuccess) return attr;
-    dim3 grid(static_cast<unsigned>((batch + BM - 1) / BM), static_cast<unsigned>((max_cols + BN - 1) / BN),
-              static_cast<unsigned>(num_stages));
     // 16-byte row loads need 16-byte aligned rows (otherwise the 8-byte gather runs)
     const int vec16 = (reinterpret_cast<std::uintptr_t>(in) % 16 == 0) && (ld_in % 2 == 0);
-    cauchy_dmma_kernel<<<grid, kThreads, smem, stream>>>(in, ld_in, out, ld_out, stages_dev, batch, flag, vec16);
-    return cudaGetLastError();
+    constexpr std::size_t kMaxRows = std::size_t{65535} * BM; // gridDim.y limit
+    for (std::size_t r0 = 0; r0 < batch; r0 += kMaxRows) {
+        const std::size_t rows = batch - r0 < kMaxRows ? batch - r0 : kMaxRows;
+        dim3 grid(static_cast<unsigned>((max_cols + BN - 1) / BN), static_cast<unsigned>((rows + BM - 1) / BM),
+                  static_cast<unsigned>(num_stages));
+        cauchy_dmma_kernel<<<grid, kThreads, smem, stream>>>(in + r0 * ld_in, ld_in, out + r0 * ld_out, ld_out,
+                                                             stages_dev, rows, flag, vec16);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 } // namespace dctp::dev

@@ -1,0 +1,203 @@
+// Signal rows times a stored basis on the fp64 tensor cores (DMMA), sm_100a:
+//
+//   out[b, c] = sum_k in[b, k] * bt[c, k]          (bt = X^T, row-major, ld_bt)
+//
+// the batched apply of a rank-k chain (chain.hpp: the composed basis X).  Same
+// tiling as the Cauchy DMMA kernel (cauchy_dmma.cu): CTA tile 64 x 128, 8 warps
+// of 32 x 32, BK = 32, two CTAs per SM, m8n8k4 fragments from rows padded to 36
+// doubles.  Here the B operand is read rather than generated: X^T rows are
+// contiguous in k, so A and B chunks are both 16-byte cp.async copies issued
+// one chunk ahead; X (<= a few MB for n <= 1024) stays in L2 across the
+// batch's row tiles.  fp32 signals are widened while staging (register
+// prefetch), so fp32 chains are also accumulated in fp64.
+#include <cstdint>
+
+#include "kernels/common.cuh"
+#include "kernels/launch.hpp"
+
+namespace dctp::dev {
+namespace {
+
+constexpr int BM = 64, BN = 128, BK = 32, LDS_ = BK + 4;
+constexpr int kThreads = 256;
+constexpr int WM = 32, WN = 32;
+constexpr int MF = WM / 8, NF = WN / 8;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(ptx::smem_addr(smem)), "l"(gmem), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(ptx::smem_addr(smem)), "l"(gmem),
+                 "r"(pred ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+template <class T>
+__global__ void __launch_bounds__(kThreads, 2)
+rows_by_basis_kernel(const T* __restrict__ in, std::size_t ld_in, const double* __restrict__ bt, std::size_t ld_bt,
+                     int K, int N, T* __restrict__ out, std::size_t ld_out, std::size_t batch, int* flag, int vec16) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* As = reinterpret_cast<double*>(smem_raw); // 2 x BM x LDS_
+    double* Bs = As + 2 * BM * LDS_;                  // 2 x BN x LDS_ ([c][k])
+    // column tiles vary fastest: the CTAs sharing a row tile run together and
+    // read it from L2 (row-tile-major order re-read A from DRAM per column tile)
+    const int c0 = blockIdx.x * BN;
+    const std::size_t b0 = static_cast<std::size_t>(blockIdx.y) * BM;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = (warp / (BN / WN)) * WM, wn = (warp % (BN / WN)) * WN;
+    const int nchunks = (K + BK - 1) / BK;
+
+    // B: thread t copies the pair 2 (t % 16) of rows t / 16 + 16 i (ld_bt is
+    // even and the rows 16-byte aligned; the zero padding beyond K is stored)
+    auto load_b = [&](int chunk, int buf) {
+        const int k = 2 * (tid % (BK / 2)), kk = chunk * BK + k;
+        const int nk = min(2, max(0, K - kk));
+#pragma unroll
+        for (int i = 0; i < BN / (kThreads / (BK / 2)); ++i) {
+            const int c = tid / (BK / 2) + i * (kThreads / (BK / 2));
+            const int bytes = c0 + c < N ? 8 * nk : 0;
+            cp_async16(Bs + buf * BN * LDS_ + c * LDS_ + k, bt + (bytes ? (c0 + c) * ld_bt + kk : 0), bytes);
+        }
+    };
+    // A, fp64: 16-byte pairs when rows are aligned, else an 8-byte copy per element
+    auto load_a64 = [&](int chunk, int buf) {
+        if (vec16) {
+            const int k = 2 * (tid % (BK / 2)), kk = chunk * BK + k;
+            const int nk = min(2, max(0, K - kk));
+#pragma unroll
+            for (int i = 0; i < BM / (kThreads / (BK / 2)); ++i) {
+                const int m = tid / (BK / 2) + i * (kThreads / (BK / 2));
+                const int bytes = b0 + m < batch ? 8 * nk : 0;
+                cp_async16(As + buf * BM * LDS_ + m * LDS_ + k,
+                           reinterpret_cast<const double*>(in) + (bytes ? (b0 + m) * ld_in + kk : 0), bytes);
+            }
+            return;
+        }
+        const int k = tid % BK, kk = chunk * BK + k;
+#pragma unroll
+        for (int i = 0; i < BM / (kThreads / BK); ++i) {
+            const int m = tid / BK + i * (kThreads / BK);
+            const bool ok = kk < K && b0 + m < batch;
+            cp_async8(As + buf * BM * LDS_ + m * LDS_ + k,
+                      reinterpret_cast<const double*>(in) + (ok ? (b0 + m) * ld_in + kk : 0), ok);
+        }
+    };
+    // A, fp32: one chunk prefetched into registers, widened on the store
+    constexpr int kAR = BM * BK / kThreads;
+    float ra[kAR];
+    auto fetch_a32 = [&](int chunk) {
+        const int k = tid % BK, kk = chunk * BK + k;
+#pragma unroll
+        for (int i = 0; i < kAR; ++i) {
+            const std::size_t b = b0 + tid / BK + i * (kThreads / BK);
+            ra[i] = kk < K && b < batch ? reinterpret_cast<const float*>(in)[b * ld_in + kk] : 0.f;
+        }
+    };
+    auto store_a32 = [&](int buf) {
+#pragma unroll
+        for (int i = 0; i < kAR; ++i)
+            As[buf * BM * LDS_ + (tid / BK + i * (kThreads / BK)) * LDS_ + tid % BK] = static_cast<double>(ra[i]);
+    };
+    constexpr bool F32 = sizeof(T) == 4;
+
+    double acc[MF][NF][2];
+#pragma unroll
+    for (int i = 0; i < MF; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    load_b(0, 0);
+    if constexpr (F32) {
+        fetch_a32(0);
+        store_a32(0);
+    } else {
+        load_a64(0, 0);
+    }
+    cp_async_commit();
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int buf = ch & 1;
+        const bool more = ch + 1 < nchunks;
+        if (more) {
+            load_b(ch + 1, buf ^ 1);
+            if constexpr (F32)
+                fetch_a32(ch + 1);
+            else
+                load_a64(ch + 1, buf ^ 1);
+        }
+        cp_async_commit();
+        cp_async_wait1();
+        __syncthreads();
+        const double* Ab = As + buf * BM * LDS_ + (wm + (lane >> 2)) * LDS_ + (lane & 3);
+        const double* Bb = Bs + buf * BN * LDS_ + (wn + (lane >> 2)) * LDS_ + (lane & 3);
+#pragma unroll
+        for (int ks = 0; ks < BK / 4; ++ks) {
+            double a[MF], bv[NF];
+#pragma unroll
+            for (int i = 0; i < MF; ++i) a[i] = Ab[i * 8 * LDS_ + ks * 4];
+#pragma unroll
+            for (int j = 0; j < NF; ++j) bv[j] = Bb[j * 8 * LDS_ + ks * 4];
+#pragma unroll
+            for (int i = 0; i < MF; ++i)
+#pragma unroll
+                for (int j = 0; j < NF; ++j) ptx::dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], bv[j]);
+        }
+        if constexpr (F32) {
+            if (more) store_a32(buf ^ 1); // that buffer was last read before the previous barrier
+        }
+        __syncthreads();
+    }
+
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < MF; ++i) {
+        const std::size_t b = b0 + wm + i * 8 + (lane >> 2);
+        if (b >= batch) continue;
+        T* orow = out + b * ld_out;
+#pragma unroll
+        for (int j = 0; j < NF; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int c = c0 + wn + j * 8 + 2 * (lane & 3) + e;
+                if (c < N) {
+                    bad |= !isfinite(acc[i][j][e]);
+                    orow[c] = static_cast<T>(acc[i][j][e]);
+                }
+            }
+    }
+    if (bad) atomicOr(flag, 1);
+}
+
+} // namespace
+
+template <class T>
+cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std::size_t ld_bt, int K, int N, T* out,
+                          std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t stream) {
+    if (batch == 0 || N == 0) return cudaSuccess;
+    if (ld_bt % 2 != 0 || reinterpret_cast<std::uintptr_t>(bt) % 16 != 0) return cudaErrorInvalidValue;
+    constexpr std::size_t smem = 2 * (BM + BN) * LDS_ * sizeof(double);
+    static const cudaError_t attr = cudaFuncSetAttribute(rows_by_basis_kernel<T>,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         static_cast<int>(smem));
+    if (attr != cudaSuccess) return attr;
+    const int vec16 = (reinterpret_cast<std::uintptr_t>(in) % 16 == 0) && (ld_in % 2 == 0);
+    constexpr std::size_t kMaxRows = std::size_t{65535} * BM; // gridDim.y limit
+    for (std::size_t r0 = 0; r0 < batch; r0 += kMaxRows) {
+        const std::size_t rows = batch - r0 < kMaxRows ? batch - r0 : kMaxRows;
+        dim3 grid(static_cast<unsigned>((N + BN - 1) / BN), static_cast<unsigned>((rows + BM - 1) / BM));
+        rows_by_basis_kernel<T><<<grid, kThreads, smem, stream>>>(in + r0 * ld_in, ld_in, bt, ld_bt, K, N,
+                                                                  out + r0 * ld_out, ld_out, rows, flag, vec16);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+template cudaError_t rows_by_basis<double>(const double*, std::size_t, const double*, std::size_t, int, int, double*,
+                                           std::size_t, std::size_t, int*, cudaStream_t);
+template cudaError_t rows_by_basis<float>(const float*, std::size_t, const double*, std::size_t, int, int, float*,
+                                          std::size_t, std::size_t, int*, cudaStream_t);
+
+} // namespace dctp::dev

@@ -120,6 +120,12 @@ bool sgemm_rows_supported(int K, int N, int lda, int ldb, std::size_t ldc, const
 cudaError_t sgemm_rows(const float* A, int lda, const float* B, int ldb, float* C, std::size_t ldc, std::size_t M,
                        int N, int K, int* flag, cudaStream_t stream);
 
+/// out[b, c] = sum_k in[b, k] bt[c, k] on the DMMA tensor cores (bt = X^T,
+/// 16-byte aligned rows, ld_bt even): the batched rank-k chain apply.
+template <class T>
+cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std::size_t ld_bt, int K, int N, T* out,
+                          std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t stream);
+
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);
 cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,

@@ -453,6 +453,125 @@ def calibrate_prune_threshold(n: int, r: float = 0.99, quantile: float = 0.7, tr
 
 # --- batched trig kernels (trig.hpp:95-110) -------------------------------------------
 
+# --- rank-k chains (cauchy.hpp:159-231) ---------------------------------------
+
+
+class SpectralBasis:
+    """L = U diag(lambda) U^T, lambda ascending, column k of u = eigenvector k
+    (spectral.hpp:21-24)."""
+
+    def __init__(self, lambda_, u):
+        self.lambda_ = np.ascontiguousarray(np.asarray(lambda_, dtype=np.float64))
+        self.u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+        n = self.lambda_.shape[0]
+        if self.lambda_.ndim != 1 or self.u.shape != (n, n):
+            raise N.InvalidArgument("SpectralBasis: lambda (n,) and u (n, n) expected")
+
+
+def path_spectrum(n: int) -> SpectralBasis:
+    """Unit-weight path graph (spectral.hpp:48-68): the base of every plan."""
+    if n < 2:
+        raise N.InvalidArgument("path_spectrum: need n >= 2")
+    lam = 2.0 - 2.0 * np.cos(np.arange(n) * np.pi / n)
+    lam[0] = 0.0
+    k, j = np.meshgrid(np.arange(n), np.arange(n))
+    u = np.sqrt(2.0 / n) * np.cos(np.pi * k * (2.0 * j + 1.0) / (2.0 * n))
+    u[:, 0] /= np.sqrt(2.0)
+    b = SpectralBasis(lam, u)
+    b._path = True  # compose_rank_k rebuilds it on the host with the reference's rounding
+    return b
+
+
+class ChainedFactorization:
+    """compose_rank_k(base, updates, tau) (cauchy.hpp:163-216): k rank-one
+    updates applied in order.  The composition runs on the host (the final
+    basis x and eigenvalues mu match the reference bit for bit); chain_forward
+    runs on the GPU as one product with x."""
+
+    def __init__(self, base, updates: Sequence[RankOneUpdate], tau: float = 1e-12, device: int = 0):
+        if isinstance(base, (int, np.integer)):
+            base = path_spectrum(int(base))
+        n = base.lambda_.shape[0]
+        k = len(updates)
+        kinds = (C.c_int * max(k, 1))(*[u.kind for u in updates])
+        is_ = (C.c_size_t * max(k, 1))(*[u.node_i for u in updates])
+        js = (C.c_size_t * max(k, 1))(*[u.node_j for u in updates])
+        rhos = (C.c_double * max(k, 1))(*[u.rho for u in updates])
+        vs = None
+        if any(u.kind == GENERAL for u in updates):
+            vs = np.zeros((k, n))
+            for r, u in enumerate(updates):
+                if u.kind == GENERAL:
+                    if np.asarray(u.v).shape[0] != n:
+                        raise N.RuntimeFailure(f"compose_rank_k: stage {r + 1}: RankOneUpdate: direction length "
+                                               "mismatch")
+                    vs[r] = u.direction(n)
+        path = getattr(base, "_path", False)
+        bl = None if path else base.lambda_.ctypes.data_as(C.c_void_p)
+        bu = None if path else base.u.ctypes.data_as(C.c_void_p)
+        h = C.c_void_p()
+        check(lib.dctp_chain_create(n, k, kinds, is_, js, rhos, None if vs is None else vs.ctypes.data_as(C.c_void_p),
+                                    bl, bu, float(tau), int(device), C.byref(h)))
+        self._h = h
+        self.n, self.device, self.updates = n, device, list(updates)
+        self.base = base
+        mu, x = np.empty(n), np.empty((n, n))
+        check(lib.dctp_chain_spectrum(h, mu.ctypes.data_as(C.c_void_p), x.ctypes.data_as(C.c_void_p)))
+        self.mu, self.x = mu, x
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and lib is not None:
+            lib.dctp_chain_destroy(h)
+            self._h = None
+
+    @property
+    def stages(self) -> list:
+        """Per stage: base_vals, mu, sigma, slot map, rotation count (ChainStage)."""
+        out = []
+        for r in range(len(self.updates)):
+            d = {k: np.empty(self.n) for k in ("base_vals", "mu", "sigma")}
+            d["slot_pass"] = np.empty(self.n, dtype=np.int32)
+            d["slot_idx"] = np.empty(self.n, dtype=np.int64)
+            rot = C.c_size_t()
+            check(lib.dctp_chain_stage(self._h, r, *[d[k].ctypes.data_as(C.c_void_p) for k in
+                                                     ("base_vals", "mu", "sigma", "slot_pass", "slot_idx")],
+                                       C.byref(rot)))
+            d["rotations"] = rot.value
+            out.append(d)
+        return out
+
+    def forward(self, s, sync: bool = True, out=None):
+        """chain_forward (cauchy.hpp:218-231) for one signal or a batch of rows."""
+        n = self.n
+        if _is_device_tensor(s):
+            rows, single = _dev_rows(s, n, "chain_forward")
+            y = out if out is not None else torch.empty_like(rows)
+            fn = lib.dctp_chain_forward_f64 if rows.dtype == torch.float64 else lib.dctp_chain_forward_f32
+            stream = _stream_ptr(rows.device)
+            check(fn(self._h, C.c_void_p(rows.data_ptr()), C.c_void_p(y.data_ptr()), rows.shape[0], stream))
+            if sync:
+                check(lib.dctp_chain_sync_check(self._h, stream))
+            return y.reshape(-1) if single else y
+        rows, single = _as_rows(s, n, "chain_forward")
+        y = np.empty_like(rows)
+        fn = lib.dctp_chain_forward_host_f64 if rows.dtype == np.float64 else lib.dctp_chain_forward_host_f32
+        check(fn(self._h, rows.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), rows.shape[0]))
+        return y.reshape(-1) if single else y
+
+    def sync_check(self):
+        check(lib.dctp_chain_sync_check(self._h, _stream_ptr(torch.cuda.current_device())))
+
+
+def compose_rank_k(base, updates: Sequence[RankOneUpdate], tau: float = 1e-12, device: int = 0
+                   ) -> ChainedFactorization:
+    return ChainedFactorization(base, updates, tau, device)
+
+
+def chain_forward(chain: ChainedFactorization, s):
+    return chain.forward(s)
+
+
 def _trig(x, inverse: bool):
     if not _is_device_tensor(x):
         raise N.InvalidArgument("dct2/idct2 batch kernels take CUDA tensors")

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <random>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include <cuda_runtime_api.h>
@@ -158,6 +159,31 @@ int main() {
         }
         cudaFree(din);
         cudaFree(dout);
+    }
+    // rank-k chains (test_cauchy.cpp:203-255): the chain agrees with its own
+    // basis, a cancelling pair restores the base spectrum, errors name the stage
+    {
+        const std::size_t n = 8;
+        const auto base = path_spectrum(n);
+        const auto chain = compose_rank_k(base, {RankOneUpdate::self_loop(1, 1.5), RankOneUpdate::self_loop(n, 0.8)});
+        CHECK(chain.stages == 2);
+        const auto s = ar(n, 0.9, g);
+        const auto got = chain_forward(chain, s);
+        std::vector<double> dense(n, 0.0);
+        for (std::size_t i = 0; i < n; ++i)
+            for (std::size_t k = 0; k < n; ++k) dense[k] += chain.x[i * n + k] * s[i];
+        CHECK(snr_db(dense, got) >= 200.0);
+        const auto cancel =
+            compose_rank_k(base, {RankOneUpdate::self_loop(2, 0.9), RankOneUpdate::self_loop(2, -0.9)});
+        for (std::size_t k = 0; k < n; ++k) CHECK(std::abs(cancel.mu[k] - base.lambda[k]) < 1e-8);
+        CHECK(throws<std::invalid_argument>([&] { compose_rank_k(path_spectrum(4), {}); }));
+        bool named = false;
+        try {
+            compose_rank_k(base, {RankOneUpdate::self_loop(1, 1.5), RankOneUpdate::self_loop(99, 1.0)});
+        } catch (const std::runtime_error& e) {
+            named = std::string(e.what()).find("stage 2") != std::string::npos;
+        }
+        CHECK(named);
     }
     if (failures == 0) std::printf("ALL OK\n");
     return failures == 0 ? 0 : 1;

@@ -409,3 +409,73 @@ def test_rdo_select_matches_reference(P, torch, restatement, reference):
         pick = full[np.arange(len(s)), idx.cpu().numpy().astype(int), :]
         assert np.array_equal(pick, chosen.cpu().numpy())
     assert [P.rdo_select(ours, x).index for x in s[:6]] == list(ridx[:6])
+
+
+# --- rank-k chains (cauchy.hpp:159-231) -------------------------------------------
+
+CHAIN_GPU_CASES = [
+    (8, [O.Update(0, 1.5, 1), O.Update(0, 0.8, 8)]),
+    (64, [O.Update(1, -0.5, 1, 64), O.Update(0, 2.0, 3), O.Update(1, 0.7, 5, 9)]),
+    (100, [O.Update(1, 1.0, 1, 100), O.Update(1, 1.0, 1, 100)]),  # K % 16 != 0, rotations
+    (256, [O.Update(0, 1.0, 1), O.Update(1, 0.3, 1, 256), O.Update(0, -0.4, 128)]),
+    (513, [O.Update(1, 0.5, 2, 400)]),  # odd n: 8-byte staging
+]
+
+
+@pytest.mark.parametrize("case", range(len(CHAIN_GPU_CASES)))
+@pytest.mark.parametrize("dtype,tol", [("float64", TOL64), ("float32", TOL32)])
+def test_chain_forward_matches_reference(P, torch, reference, case, dtype, tol):
+    """chain_forward on the device (one product with the composed basis)
+    against the reference's staged chain_forward (U^T s, then k Cauchy
+    stages) on the same seeded signals."""
+    n, ups = CHAIN_GPU_CASES[case]
+    ch = P.compose_rank_k(n, [upd(P, u) for u in ups])
+    s = np.random.default_rng(100 + case).standard_normal((300, n))
+    want = reference.chain(n, ups).forward(s)
+    got = ch.forward(dev(torch, s, getattr(torch, dtype))).double().cpu().numpy()
+    assert O.parity(got, want) <= tol
+    # host entry points (pipelined H2D / apply / D2H)
+    host = ch.forward(s.astype(dtype))
+    assert O.parity(host.astype(np.float64), want) <= tol
+
+
+def test_chain_forward_full_batch_properties(P, torch):
+    """n = 1024, k = 3, 16384 signals: the composed basis is orthogonal, so
+    ||chain_forward(s)|| = ||s|| per signal (Parseval) and the rows agree with
+    x^T s computed by torch in fp64 on a sample."""
+    n = 1024
+    ups = [P.RankOneUpdate.self_loop(1, 1.5), P.RankOneUpdate.edge_delta(1, n, -0.5),
+           P.RankOneUpdate.edge_delta(300, 700, 0.25)]
+    ch = P.compose_rank_k(n, ups)
+    s = torch.randn((16384, n), dtype=torch.float64, device="cuda")
+    y = ch.forward(s)
+    rel = (y.norm(dim=1) - s.norm(dim=1)).abs() / s.norm(dim=1)
+    # the composed basis is orthogonal only to the chain's own accuracy
+    # (bit-identical to the reference's x): allow that, plus rounding
+    x = torch.as_tensor(ch.x, device="cuda")
+    orth = float((x.T @ x - torch.eye(n, dtype=x.dtype, device="cuda")).abs().max())
+    assert float(rel.max()) < 1e-12 + n * orth
+    ref = s[:512] @ x
+    assert orth < 1e-7  # 3.5e-9 here: the reference chain has no re-orthogonalisation
+    assert float(((y[:512] - ref).abs().max(dim=1).values / ref.abs().max(dim=1).values).max()) < 1e-12
+
+
+def test_chain_forward_views_nan_and_empty(P, torch, reference):
+    """Misaligned device views (8-byte staging), the non-finite flag, batch 0."""
+    n, ups = 64, [O.Update(0, 1.5, 1), O.Update(1, 0.4, 3, 60)]
+    ch = P.compose_rank_k(n, [upd(P, u) for u in ups])
+    s = np.random.default_rng(7).standard_normal((65, n))
+    flat = torch.empty(65 * n + 1, dtype=torch.float64, device="cuda")
+    d = flat[1:].view(65, n)  # 8 bytes off a 16-byte boundary
+    d.copy_(dev(torch, s, torch.float64))
+    want = reference.chain(n, ups).forward(s)
+    assert O.parity(ch.forward(d).cpu().numpy(), want) <= TOL64
+    f32 = torch.empty(65 * n + 1, dtype=torch.float32, device="cuda")[1:].view(65, n)
+    f32.copy_(dev(torch, s, torch.float32))
+    assert O.parity(ch.forward(f32).double().cpu().numpy(), want) <= TOL32
+    bad = dev(torch, s, torch.float64)
+    bad[3, 5] = float("nan")
+    with pytest.raises(P.DomainError):
+        ch.forward(bad)
+    ch.forward(dev(torch, s, torch.float64))  # the flag was cleared
+    assert ch.forward(torch.empty((0, n), dtype=torch.float64, device="cuda")).shape == (0, n)

@@ -156,3 +156,78 @@ def test_calibrate_prune_threshold_matches_reference(reference, n, r, quantile, 
     ours = P.calibrate_prune_threshold(n, r, quantile, 512, seed)
     ref = reference.lib.ref_calibrate_prune_threshold(n, r, quantile, 512, seed)
     assert ours == ref
+
+
+# --- rank-k chains (cauchy.hpp:159-231) -----------------------------------------
+
+CHAIN_CASES = [
+    (8, [O.Update(0, 1.5, 1)]),
+    (8, [O.Update(0, 1.5, 1), O.Update(0, 0.8, 8)]),
+    (8, [O.Update(0, 0.9, 2), O.Update(0, -0.9, 2)]),
+    (64, [O.Update(1, -0.5, 1, 64), O.Update(0, 2.0, 3), O.Update(1, 0.7, 5, 9)]),
+    (100, [O.Update(1, 1.0, 1, 100), O.Update(1, 1.0, 1, 100)]),  # stage 2 deflates by rotations
+    (48, [O.Update(2, 0.6, v=tuple(np.cos(np.arange(48) * 0.3))), O.Update(0, -1.2, 7)]),
+]
+
+
+def path_laplacian(n, ups):
+    lap = np.zeros((n, n))
+    for i in range(n - 1):
+        lap[i, i] += 1.0
+        lap[i + 1, i + 1] += 1.0
+        lap[i, i + 1] -= 1.0
+        lap[i + 1, i] -= 1.0
+    for u in ups:
+        v = O.direction(u, n)
+        lap += u.rho * np.outer(v, v)
+    return lap
+
+
+@pytest.mark.parametrize("case", range(len(CHAIN_CASES)))
+def test_chain_compose_bitwise_equal_to_reference(reference, case):
+    """compose_rank_k's final basis and eigenvalues are the reference's, bit
+    for bit (host-only chain), including a stage that deflates by Givens
+    rotations and a general-direction stage."""
+    n, ups = CHAIN_CASES[case]
+    ch = P.compose_rank_k(n, [product_update(u) for u in ups], device=-1)
+    mu, x, k = reference.chain(n, ups).spectrum()
+    assert k == len(ups) == len(ch.stages)
+    assert np.array_equal(ch.mu, mu)
+    assert np.array_equal(ch.x, x)
+
+
+def test_chain_compose_on_a_caller_base_matches_reference(reference):
+    """A non-path base spectrum (dense eigendecomposition of a perturbed path)
+    composes bit-identically too."""
+    n = 24
+    lam, u = np.linalg.eigh(path_laplacian(n, [O.Update(0, 0.7, 5)]))
+    ups = [O.Update(1, 0.4, 2, 20), O.Update(0, -0.3, 11)]
+    ch = P.compose_rank_k(P.SpectralBasis(lam, u), [product_update(v) for v in ups], device=-1)
+    mu, x, _ = reference.chain(n, ups, base=(lam, u)).spectrum()
+    assert np.array_equal(ch.mu, mu) and np.array_equal(ch.x, x)
+
+
+def test_chain_k1_reduces_to_the_plan_and_k2_to_the_dense_oracle():
+    """test_cauchy.cpp:203-247: k = 1 gives the plan's spectrum; k = 2 the
+    dense eigendecomposition; a cancelling pair returns the base spectrum."""
+    n = 8
+    plan = P.DctPlusPlan(n, P.RankOneUpdate.self_loop(1, 1.5), 1e-12, device=-1)
+    ch = P.compose_rank_k(n, [P.RankOneUpdate.self_loop(1, 1.5)], device=-1)
+    assert np.max(np.abs(ch.mu - plan.mu())) < 1e-14
+    assert np.max(np.abs(np.abs(ch.x) - np.abs(plan.basis()))) < 1e-12
+    ups = [O.Update(0, 1.5, 1), O.Update(0, 0.8, n)]
+    ch = P.compose_rank_k(n, [product_update(u) for u in ups], device=-1)
+    lam = np.linalg.eigvalsh(path_laplacian(n, ups))
+    assert np.max(np.abs(ch.mu - lam)) < 1e-8
+    ch = P.compose_rank_k(n, [P.RankOneUpdate.self_loop(2, 0.9), P.RankOneUpdate.self_loop(2, -0.9)], device=-1)
+    assert np.max(np.abs(ch.mu - P.path_spectrum(n).lambda_)) < 1e-8
+
+
+def test_chain_errors_mirror_reference():
+    with pytest.raises(P.InvalidArgument, match="need k >= 1"):
+        P.compose_rank_k(4, [], device=-1)
+    with pytest.raises(P.RuntimeFailure, match="stage 2"):
+        P.compose_rank_k(8, [P.RankOneUpdate.self_loop(1, 1.5), P.RankOneUpdate.self_loop(99, 1.0)], device=-1)
+    ch = P.compose_rank_k(8, [P.RankOneUpdate.self_loop(1, 1.5)], device=-1)
+    with pytest.raises(P.InvalidArgument, match="host-only"):
+        ch.forward(np.zeros(8))

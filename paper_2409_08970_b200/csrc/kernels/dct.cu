@@ -22,23 +22,34 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kTileElems = 2048; // signal samples staged per CTA
 
+/// Shared-memory layout of the FFT rows: one complex of padding after every
+/// 8, so the strided groups of every pass (including the bit-reversed gather
+/// of the first one) hit 8 distinct 16-byte bank groups per quarter-warp.
+__device__ __forceinline__ int pad8(int i) { return i + (i >> 3); }
+__host__ __device__ constexpr int padded_len(int N) { return N + (N >> 3) + 1; }
+
 /// Q consecutive radix-2 DIT stages (s0+1 .. s0+Q) fused into one pass over
 /// groups of 2^Q elements held in registers: group (block, j) holds elements
 /// block*2^(s0+Q) + j + m*2^s0, m < 2^Q, of the bit-reversed sequence.  One
 /// shared-memory round trip and one barrier per Q stages instead of per stage.
-template <class T, bool Inverse, int Q>
-__device__ __forceinline__ void dit_group_pass(cplx_t<T>* buf, int rows, int N, int logN, int s0,
-                                               const T* __restrict__ tw) {
+/// The first pass (FIRST, s0 = 0) gathers its inputs from the natural-order
+/// buffer `src` at the bit-reversed positions and writes `dst`, so no
+/// bit-reversed scatter is ever stored.
+template <class T, bool Inverse, int Q, bool FIRST>
+__device__ __forceinline__ void dit_group_pass(const cplx_t<T>* src, cplx_t<T>* dst, int rows, int N, int logN,
+                                               int s0, const T* __restrict__ tw) {
     constexpr int G = 1 << Q;
     const int h0 = 1 << s0;
     const int groups = N >> Q;
+    const int ld = padded_len(N);
     for (int t = threadIdx.x; t < rows * groups; t += blockDim.x) {
         const int row = t / groups, g = t - row * groups;
         const int j = g & (h0 - 1), base = (g >> s0) * (h0 << Q) + j;
-        cplx_t<T>* e = buf + row * N + base;
         cplx_t<T> v[G];
 #pragma unroll
-        for (int m = 0; m < G; ++m) v[m] = e[m * h0];
+        for (int m = 0; m < G; ++m)
+            v[m] = FIRST ? src[row * ld + pad8(static_cast<int>(bit_reverse(static_cast<unsigned>(base + m), logN)))]
+                         : dst[row * ld + pad8(base + m * h0)];
 #pragma unroll
         for (int tt = 0; tt < Q; ++tt) {
             const int span = 1 << tt;
@@ -56,19 +67,38 @@ __device__ __forceinline__ void dit_group_pass(cplx_t<T>* buf, int rows, int N, 
             }
         }
 #pragma unroll
-        for (int m = 0; m < G; ++m) e[m * h0] = v[m];
+        for (int m = 0; m < G; ++m) dst[row * ld + pad8(base + m * h0)] = v[m];
     }
     __syncthreads();
 }
 
-/// In-place DIT FFT of `rows` bit-reversed rows of N = 2^logN points, radix-8
-/// passes (radix-4/2 for the remainder).
+/// FFT of `rows` rows of N = 2^logN points given in natural order in `src`
+/// (padded rows), result in natural order in `dst`: a bit-reversed gather
+/// folded into the first radix-8 pass, then in-place radix-8 DIT passes
+/// (radix-4/2 for the remainder).  `src` is dead afterwards.
 template <class T, bool Inverse>
-__device__ __forceinline__ void fft_dit(cplx_t<T>* buf, int rows, int N, int logN, const T* __restrict__ tw) {
-    int s0 = 0;
-    for (; s0 + 3 <= logN; s0 += 3) dit_group_pass<T, Inverse, 3>(buf, rows, N, logN, s0, tw);
-    if (logN - s0 == 2) dit_group_pass<T, Inverse, 2>(buf, rows, N, logN, s0, tw);
-    if (logN - s0 == 1) dit_group_pass<T, Inverse, 1>(buf, rows, N, logN, s0, tw);
+__device__ __forceinline__ void fft_rows(const cplx_t<T>* src, cplx_t<T>* dst, int rows, int N, int logN,
+                                         const T* __restrict__ tw) {
+    if (logN == 0) {
+        for (int r = threadIdx.x; r < rows; r += blockDim.x) dst[r * padded_len(N)] = src[r * padded_len(N)];
+        __syncthreads();
+        return;
+    }
+    const int q0 = min(3, logN);
+    if (q0 == 3) dit_group_pass<T, Inverse, 3, true>(src, dst, rows, N, logN, 0, tw);
+    if (q0 == 2) dit_group_pass<T, Inverse, 2, true>(src, dst, rows, N, logN, 0, tw);
+    if (q0 == 1) dit_group_pass<T, Inverse, 1, true>(src, dst, rows, N, logN, 0, tw);
+    int s0 = q0;
+    for (; s0 + 3 <= logN; s0 += 3) dit_group_pass<T, Inverse, 3, false>(dst, dst, rows, N, logN, s0, tw);
+    if (logN - s0 == 2) dit_group_pass<T, Inverse, 2, false>(dst, dst, rows, N, logN, s0, tw);
+    if (logN - s0 == 1) dit_group_pass<T, Inverse, 1, false>(dst, dst, rows, N, logN, s0, tw);
+}
+
+/// Shared memory of the FFT kernels: natural buffer (later the real output
+/// rows), working buffer; both rows_per_cta x padded_len(n/2) complex.
+template <class T>
+std::size_t fft_smem_bytes(std::size_t n, int rows) {
+    return 2 * static_cast<std::size_t>(rows) * padded_len(static_cast<int>(n / 2)) * sizeof(T) * 2;
 }
 
 template <class T>
@@ -77,16 +107,18 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
                 T* __restrict__ out, std::size_t ld_out, Emit<T> emit, int n, int logn,
                 int rows_per_cta, std::size_t batch, Twiddles<T> tw, int* flag) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N = n >> 1, logN = logn - 1;
-    cplx_t<T>* cbuf = reinterpret_cast<cplx_t<T>*>(smem_raw);
-    T* sh = reinterpret_cast<T*>(cbuf + rows_per_cta * N);
+    const int N = n >> 1, logN = logn - 1, ld = padded_len(N);
+    cplx_t<T>* nat = reinterpret_cast<cplx_t<T>*>(smem_raw);
+    cplx_t<T>* work = nat + rows_per_cta * ld;
+    T* sh = reinterpret_cast<T*>(nat); // real output rows (stride n) once `nat` is consumed
     const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * rows_per_cta;
     const int rows = static_cast<int>(min(static_cast<std::size_t>(rows_per_cta), batch - b0));
 
     // Load with Makhoul's permutation v = (x0, x2, ..., x3, x1), packed as
-    // w_m = v_{2m} + i v_{2m+1}, stored bit-reversed for the DIT stages.
-    // eight independent loads in flight per thread before any use (a load-use
-    // chain per element left the kernel waiting on HBM latency)
+    // w_m = v_{2m} + i v_{2m+1}, in natural order (the FFT's first pass does
+    // the bit reversal).  Eight independent loads in flight per thread
+    // before any use (a load-use chain per element left the kernel waiting on
+    // HBM latency).
     bool bad = false;
     constexpr int U = 8;
     for (int t0 = threadIdx.x; t0 < rows * n; t0 += U * kThreads) {
@@ -103,14 +135,13 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
             const int r = t >> logn, j = t & (n - 1);
             bad |= !finite_val(xv[u]);
             const int p = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
-            T* slot = reinterpret_cast<T*>(&cbuf[r * N + bit_reverse(static_cast<unsigned>(p >> 1), logN)]);
-            slot[p & 1] = xv[u];
+            reinterpret_cast<T*>(&nat[r * ld + pad8(p >> 1)])[p & 1] = xv[u];
         }
     }
     if (bad) atomicOr(flag, 1);
     __syncthreads();
 
-    fft_dit<T, false>(cbuf, rows, N, logN, tw.fft);
+    fft_rows<T, false>(nat, work, rows, N, logN, tw.fft);
 
     // Real split V_k = E_k - i e^{-2 pi i k/n} O_k, then Y_k = Re(e^{-i pi k/2n} V_k),
     // Y_{n-k} = -Im(...); orthonormal scale sqrt(2/n), DC gets 1/sqrt(2) more.
@@ -119,7 +150,7 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
     const T half = static_cast<T>(0.5);
     for (int t = threadIdx.x; t < rows * N; t += blockDim.x) {
         const int r = t >> logN, k = t & (N - 1);
-        const cplx_t<T>* row = cbuf + r * N;
+        const cplx_t<T>* row = work + r * ld;
         T* o = sh + r * n;
         if (k == 0) {
             const cplx_t<T> w0 = row[0];
@@ -127,8 +158,8 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
             o[N] = (w0.x - w0.y) * __ldg(tw.rot + 2 * N) * scale;
             continue;
         }
-        const cplx_t<T> wk = row[k];
-        const cplx_t<T> wc = row[N - k];
+        const cplx_t<T> wk = row[pad8(k)];
+        const cplx_t<T> wc = row[pad8(N - k)];
         const T er = half * (wk.x + wc.x), ei = half * (wk.y - wc.y);
         const T orr = half * (wk.x - wc.x), oi = half * (wk.y + wc.y);
         const T sr = __ldg(tw.split + 2 * k), si = __ldg(tw.split + 2 * k + 1);
@@ -162,9 +193,10 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
                 Emit<T> emit, T* __restrict__ out, std::size_t ld_out, int n, int logn,
                 int rows_per_cta, std::size_t batch, Twiddles<T> tw, int* flag) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N = n >> 1, logN = logn - 1;
-    cplx_t<T>* cbuf = reinterpret_cast<cplx_t<T>*>(smem_raw);
-    T* sh = reinterpret_cast<T*>(cbuf + rows_per_cta * N);
+    const int N = n >> 1, logN = logn - 1, ld = padded_len(N);
+    cplx_t<T>* nat = reinterpret_cast<cplx_t<T>*>(smem_raw);
+    cplx_t<T>* work = nat + rows_per_cta * ld;
+    T* sh = reinterpret_cast<T*>(work); // the real coefficients, consumed before the FFT writes `work`
     const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * rows_per_cta;
     const int rows = static_cast<int>(min(static_cast<std::size_t>(rows_per_cta), batch - b0));
 
@@ -211,7 +243,8 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
     for (int t = threadIdx.x; t < rows * n; t += blockDim.x) sh[t] *= ((t & (n - 1)) == 0) ? dc_scale : scale;
     __syncthreads();
 
-    // V_k = e^{i pi k/2n} (X_k - i X_{n-k}); Z_k = (V_k + V_{k+N} + i e^{2 pi i k/n}(V_k - V_{k+N}))/2.
+    // V_k = e^{i pi k/2n} (X_k - i X_{n-k}); Z_k = (V_k + V_{k+N} + i e^{2 pi i k/n}(V_k - V_{k+N}))/2,
+    // stored in natural order (the FFT's first pass gathers bit-reversed)
     const T half = static_cast<T>(0.5);
     const T r2 = static_cast<T>(0.70710678118654752440);
     for (int t = threadIdx.x; t < rows * N; t += blockDim.x) {
@@ -227,17 +260,16 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
         const T sr = __ldg(tw.split + 2 * k), si = -__ldg(tw.split + 2 * k + 1); // e^{+2 pi i k/n}
         const T dr = v1r - v2r, di = v1i - v2i;
         const T qr = sr * dr - si * di, qi = sr * di + si * dr;
-        cbuf[r * N + bit_reverse(static_cast<unsigned>(k), logN)] = {half * (v1r + v2r - qi),
-                                                                     half * (v1i + v2i + qr)};
+        nat[r * ld + pad8(k)] = {half * (v1r + v2r - qi), half * (v1i + v2i + qr)};
     }
     __syncthreads();
 
-    fft_dit<T, true>(cbuf, rows, N, logN, tw.fft);
+    fft_rows<T, true>(nat, work, rows, N, logN, tw.fft);
 
     for (int t = threadIdx.x; t < rows * n; t += blockDim.x) {
         const int r = t >> logn, j = t & (n - 1);
         const int pidx = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
-        const cplx_t<T> w = cbuf[r * N + (pidx >> 1)];
+        const cplx_t<T> w = work[r * ld + pad8(pidx >> 1)];
         out[(b0 + r) * ld_out + j] = (pidx & 1) ? w.y : w.x;
     }
 }
@@ -334,7 +366,7 @@ cudaError_t dct2_rows(const T* in, std::size_t ld_in, T* hat, std::size_t ld_hat
     if (batch == 0) return cudaSuccess;
     if (is_pow2(n) && n >= 2) {
         const int rows = rows_per_cta_for<T>(n);
-        const std::size_t smem = static_cast<std::size_t>(rows) * n * (sizeof(T) * 2);
+        const std::size_t smem = fft_smem_bytes<T>(n, rows);
         auto kern = dct2_fft_kernel<T>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
@@ -360,7 +392,7 @@ cudaError_t idct_rows(const T* d, std::size_t ld_d, const T* p, std::size_t ld_p
     if (batch == 0) return cudaSuccess;
     if (is_pow2(n) && n >= 2) {
         const int rows = rows_per_cta_for<T>(n);
-        const std::size_t smem = static_cast<std::size_t>(rows) * n * (sizeof(T) * 2);
+        const std::size_t smem = fft_smem_bytes<T>(n, rows);
         auto kern = idct_fft_kernel<T>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));

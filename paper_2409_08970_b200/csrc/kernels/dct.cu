@@ -58,8 +58,8 @@ __device__ __forceinline__ void dit_group_pass(const cplx_t<T>* src, cplx_t<T>* 
             for (int m = 0; m < G; ++m) {
                 if (m & span) continue;
                 const int widx = (j + (m & (span - 1)) * h0) << shift;
-                const T wr = __ldg(tw + 2 * widx);
-                const T wi = Inverse ? -__ldg(tw + 2 * widx + 1) : __ldg(tw + 2 * widx + 1);
+                const cplx_t<T> w = __ldg(reinterpret_cast<const cplx_t<T>*>(tw) + widx); // one 16/8-byte load
+                const T wr = w.x, wi = Inverse ? -w.y : w.y;
                 const cplx_t<T> a = v[m], b = v[m + span];
                 const T br = b.x * wr - b.y * wi, bi = b.x * wi + b.y * wr;
                 v[m] = {a.x + br, a.y + bi};
@@ -162,10 +162,12 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
         const cplx_t<T> wc = row[pad8(N - k)];
         const T er = half * (wk.x + wc.x), ei = half * (wk.y - wc.y);
         const T orr = half * (wk.x - wc.x), oi = half * (wk.y + wc.y);
-        const T sr = __ldg(tw.split + 2 * k), si = __ldg(tw.split + 2 * k + 1);
+        const cplx_t<T> sp = __ldg(reinterpret_cast<const cplx_t<T>*>(tw.split) + k);
+        const T sr = sp.x, si = sp.y;
         const T qr = sr * orr - si * oi, qi = sr * oi + si * orr;
         const T vr = er + qi, vi = ei - qr;
-        const T cr = __ldg(tw.rot + 2 * k), ci = __ldg(tw.rot + 2 * k + 1);
+        const cplx_t<T> rt = __ldg(reinterpret_cast<const cplx_t<T>*>(tw.rot) + k);
+        const T cr = rt.x, ci = rt.y;
         o[k] = (vr * cr - vi * ci) * scale;
         o[n - k] = -(vr * ci + vi * cr) * scale;
     }
@@ -176,14 +178,17 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
             const int r = t >> logn, k = t & (n - 1);
             hat[(b0 + r) * ld_hat + k] = sh[t];
         }
-    for (int t = threadIdx.x; t < rows * emit.count; t += blockDim.x) {
-        const int r = t / emit.count, e = t - r * emit.count;
-        const int to = emit.to[e];
-        const T v = emit.sign[e] * sh[r * n + emit.from[e]];
-        if (to >= 0)
-            out[(b0 + r) * ld_out + to] = v;
-        else
-            emit.alt[(b0 + r) * emit.ld_alt + (-to - 1)] = v;
+    // one table lookup per entry, reused for every row of the tile
+    for (int e = threadIdx.x; e < emit.count; e += blockDim.x) {
+        const int to = __ldg(emit.to + e), from = __ldg(emit.from + e);
+        const T sg = __ldg(emit.sign + e);
+        for (int r = 0; r < rows; ++r) {
+            const T v = sg * sh[r * n + from];
+            if (to >= 0)
+                out[(b0 + r) * ld_out + to] = v;
+            else
+                emit.alt[(b0 + r) * emit.ld_alt + (-to - 1)] = v;
+        }
     }
 }
 
@@ -250,14 +255,16 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
     for (int t = threadIdx.x; t < rows * N; t += blockDim.x) {
         const int r = t >> logN, k = t & (N - 1);
         const T* x = sh + r * n;
-        const T cr = __ldg(tw.rot + 2 * k), ci = -__ldg(tw.rot + 2 * k + 1); // e^{+i pi k/2n}
+        const cplx_t<T> rt = __ldg(reinterpret_cast<const cplx_t<T>*>(tw.rot) + k);
+        const T cr = rt.x, ci = -rt.y; // e^{+i pi k/2n}
         const T ar = x[k], ai = (k == 0) ? T(0) : -x[n - k];
         const T v1r = ar * cr - ai * ci, v1i = ar * ci + ai * cr;
         // e^{i pi (k+N)/2n} = e^{i pi/4} e^{i pi k/2n}
         const T c2r = r2 * (cr - ci), c2i = r2 * (cr + ci);
         const T br = x[k + N], bi = -x[N - k];
         const T v2r = br * c2r - bi * c2i, v2i = br * c2i + bi * c2r;
-        const T sr = __ldg(tw.split + 2 * k), si = -__ldg(tw.split + 2 * k + 1); // e^{+2 pi i k/n}
+        const cplx_t<T> sp = __ldg(reinterpret_cast<const cplx_t<T>*>(tw.split) + k);
+        const T sr = sp.x, si = -sp.y; // e^{+2 pi i k/n}
         const T dr = v1r - v2r, di = v1i - v2i;
         const T qr = sr * dr - si * di, qi = sr * di + si * dr;
         nat[r * ld + pad8(k)] = {half * (v1r + v2r - qi), half * (v1i + v2i + qr)};

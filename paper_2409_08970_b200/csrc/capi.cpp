@@ -22,6 +22,7 @@
 #include <type_traits>
 #include <vector>
 
+#include <cuda.h> // driver types only (cuPointerGetAttribute is resolved at run time)
 #include <cuda_runtime_api.h>
 
 #include "host/chain.hpp"
@@ -1002,13 +1003,69 @@ int dctp_plan_sync_check(const dctp_plan* p, void* stream) {
     });
 }
 
-#define DCTP_HOST_ENTRY(NAME, T, FN)                                                              \
+} // extern "C"
+
+/// True when [p, p + bytes) lies inside one page-locked host allocation that
+/// device `device` can address (UVA-mapped): the same buffer id at both ends.
+static bool pinned_range(const void* p, std::size_t bytes, int device) {
+    cudaPointerAttributes a{}, b{};
+    const void* last = static_cast<const char*>(p) + bytes - 1;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess || cudaPointerGetAttributes(&b, last) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (a.type != cudaMemoryTypeHost || b.type != cudaMemoryTypeHost || a.devicePointer != p || a.device != device)
+        return false;
+    using GetAttr = CUresult (*)(void*, CUpointer_attribute, CUdeviceptr);
+    static GetAttr get = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return static_cast<GetAttr>(nullptr);
+        }
+        return reinterpret_cast<GetAttr>(fn);
+    }();
+    if (!get) return false;
+    unsigned long long id0 = 0, id1 = 0;
+    if (get(&id0, CU_POINTER_ATTRIBUTE_BUFFER_ID, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS ||
+        get(&id1, CU_POINTER_ATTRIBUTE_BUFFER_ID, reinterpret_cast<CUdeviceptr>(last)) != CUDA_SUCCESS)
+        return false;
+    return id0 == id1;
+}
+
+/// Small host batches of fused plans: the kernel's TMA bulk copies read and
+/// write the page-locked host rows directly over PCIe (zero copy).  For a few
+/// MB this halves the latency of staged H2D / kernel / D2H (every copy and
+/// stream hop costs tens of microseconds there; tools/small_e2e_probe.py);
+/// above DCTP_ZC_MAX_MB (default 8) the staged pipeline moves more bytes/s.
+static bool forward_zero_copy(const dctp_plan*, const float*, float*, std::size_t) { return false; }
+static bool forward_zero_copy(const dctp_plan* p, const double* h_in, double* h_out, std::size_t batch) {
+    if (!p->small || !h_in || !h_out) return false;
+    const char* off = std::getenv("DCTP_ZERO_COPY");
+    if (off && off[0] == '0') return false;
+    const std::size_t bytes = batch * p->st.n * sizeof(double);
+    if (bytes > (env_size("DCTP_ZC_MAX_MB", 8) << 20)) return false;
+    if ((reinterpret_cast<std::uintptr_t>(h_in) | reinterpret_cast<std::uintptr_t>(h_out)) % 16 != 0) return false;
+    DeviceScope scope(p->device);
+    if (!pinned_range(h_in, bytes, p->device) || !pinned_range(h_out, bytes, p->device)) return false;
+    HostPipe& hp = host_pipe(p->device);
+    plan_forward<double>(p, h_in, h_out, batch, hp.comp);
+    sync_check(p->device, p->flag, hp.comp);
+    return true;
+}
+
+extern "C" {
+
+#define DCTP_HOST_ENTRY(NAME, T, FN, ZC)                                                            \
     int NAME(const dctp_plan* p, const T* h_in, T* h_out, size_t batch) {                             \
         return guarded([&] {                                                                          \
             if (!p) throw std::invalid_argument(#NAME ": null plan");                                 \
             if (!p->blob) throw std::invalid_argument("DctPlusPlan: host-only plan (created with device < 0)"); \
             if (batch == 0) return;                                                                   \
             const std::size_t n = p->st.n;                                                           \
+            if (ZC && forward_zero_copy(p, h_in, h_out, batch)) return;                               \
             host_roundtrip<T>(p->device, batch, n, n, h_in, h_out,                                    \
                               [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) {         \
                                   FN<T>(p, din, dout, rows, s);                                       \
@@ -1016,10 +1073,10 @@ int dctp_plan_sync_check(const dctp_plan* p, void* stream) {
             sync_check(p->device, p->flag, nullptr);                                                  \
         });                                                                                           \
     }
-DCTP_HOST_ENTRY(dctp_forward_host_f64, double, plan_forward)
-DCTP_HOST_ENTRY(dctp_forward_host_f32, float, plan_forward)
-DCTP_HOST_ENTRY(dctp_inverse_host_f64, double, plan_inverse)
-DCTP_HOST_ENTRY(dctp_inverse_host_f32, float, plan_inverse)
+DCTP_HOST_ENTRY(dctp_forward_host_f64, double, plan_forward, true)
+DCTP_HOST_ENTRY(dctp_forward_host_f32, float, plan_forward, false)
+DCTP_HOST_ENTRY(dctp_inverse_host_f64, double, plan_inverse, false)
+DCTP_HOST_ENTRY(dctp_inverse_host_f32, float, plan_inverse, false)
 #undef DCTP_HOST_ENTRY
 
 int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is, const size_t* js, const double* rhos,

@@ -266,6 +266,43 @@ def test_host_paths_pinned_pageable_and_multi_chunk(P, torch, restatement, monke
     assert O.parity(back, s) <= TOL64
 
 
+def test_small_pinned_batches_zero_copy(P, torch, restatement, monkeypatch):
+    """Small page-locked host batches of fused plans are transformed in place
+    over PCIe (the kernel's TMA copies address the pinned rows): bit-identical
+    to the device route and to the staged pipeline, non-finite input still
+    reported; pageable, misaligned or oversized buffers take the pipeline."""
+    import ctypes as C
+
+    from paper_2409_08970_b200._native import check, lib
+    for cid, batch in ((1, 4096), (2, 3001)):
+        cfg = O.config(cid)
+        s = restatement.fill_signals(O.mix_seed(O.SEED, cfg.n, 9), 0, cfg.n, batch)
+        plan = plan_for(P, cid)
+        ref = plan.forward(dev(torch, s, torch.float64)).cpu().numpy()
+        pin_in = torch.from_numpy(s).pin_memory()
+        pin_out = torch.zeros_like(pin_in).pin_memory()
+
+        def run(a=pin_in, b=pin_out, rows=batch):
+            b.zero_()
+            check(lib.dctp_forward_host_f64(plan._h, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), rows))
+            return b.numpy()
+
+        assert np.array_equal(run(), ref)                   # zero copy
+        monkeypatch.setenv("DCTP_ZERO_COPY", "0")
+        assert np.array_equal(run(), ref)                   # staged pipeline, same bits
+        monkeypatch.delenv("DCTP_ZERO_COPY")
+        big_in = torch.from_numpy(np.concatenate([s, s])).pin_memory()
+        big_out = torch.zeros_like(big_in).pin_memory()
+        off_in, off_out = big_in.view(-1)[1:batch * cfg.n + 1], big_out.view(-1)[1:batch * cfg.n + 1]
+        off_in.copy_(torch.from_numpy(s.reshape(-1)))
+        assert np.array_equal(run(off_in, off_out).reshape(batch, cfg.n), ref)  # 8 bytes off: staged
+        pin_in[batch // 3, 1] = float("inf")
+        with pytest.raises(P.DomainError):
+            run()
+        pin_in[batch // 3, 1] = 0.0
+        assert np.array_equal(run(), plan.forward(dev(torch, pin_in.numpy(), torch.float64)).cpu().numpy())
+
+
 def test_misaligned_device_views_take_the_generic_route(P, torch, restatement):
     """The fused kernel's TMA bulk copies need 16-byte aligned rows; an
     8-byte-offset view must still give the right answer (generic kernels)."""

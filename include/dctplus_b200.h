@@ -102,11 +102,23 @@ int dctp_inverse_f32(const dctp_plan* plan, const float* d_in, float* d_out, siz
  * non-finite (then clears the flag). */
 int dctp_plan_sync_check(const dctp_plan* plan, void* stream);
 
+/* Dense routes with the materialised basis X (built on first use, n^2
+ * doubles twice on the device): forward_nmvp = X^T s (fast_transform.hpp:
+ * 199-214) and inverse(p, fast = false) = X p (:218-260), fp64 tensor cores. */
+int dctp_forward_nmvp_f64(const dctp_plan* plan, const double* d_in, double* d_out, size_t batch, void* stream);
+int dctp_forward_nmvp_f32(const dctp_plan* plan, const float* d_in, float* d_out, size_t batch, void* stream);
+int dctp_inverse_nmvp_f64(const dctp_plan* plan, const double* d_in, double* d_out, size_t batch, void* stream);
+int dctp_inverse_nmvp_f32(const dctp_plan* plan, const float* d_in, float* d_out, size_t batch, void* stream);
+
 /* Synchronous host-buffer variants (H2D, forward/inverse, D2H). */
 int dctp_forward_host_f64(const dctp_plan* plan, const double* h_in, double* h_out, size_t batch);
 int dctp_inverse_host_f64(const dctp_plan* plan, const double* h_in, double* h_out, size_t batch);
 int dctp_forward_host_f32(const dctp_plan* plan, const float* h_in, float* h_out, size_t batch);
 int dctp_inverse_host_f32(const dctp_plan* plan, const float* h_in, float* h_out, size_t batch);
+int dctp_forward_nmvp_host_f64(const dctp_plan* plan, const double* h_in, double* h_out, size_t batch);
+int dctp_forward_nmvp_host_f32(const dctp_plan* plan, const float* h_in, float* h_out, size_t batch);
+int dctp_inverse_nmvp_host_f64(const dctp_plan* plan, const double* h_in, double* h_out, size_t batch);
+int dctp_inverse_nmvp_host_f32(const dctp_plan* plan, const float* h_in, float* h_out, size_t batch);
 
 /* --- PrunedEnsemblePlan (fast_transform.hpp:338-454) ----------------------- */
 

@@ -135,16 +135,24 @@ class DctPlusPlan {
         return forward(s, ws);
     }
     /// The reference's dense X^T s; identical math, same GPU route.
+    /// X^T s with the materialised basis (dense product on the GPU).
     const std::vector<double>& forward_nmvp(const std::vector<double>& s, DctPlusWorkspace& ws) const {
-        return forward(s, ws);
+        check_size(s);
+        ws.out.resize(n_);
+        detail::check(dctp_forward_nmvp_host_f64(h_.get(), s.data(), ws.out.data(), 1));
+        return ws.out;
     }
-    std::vector<double> forward_nmvp(const std::vector<double>& s) const { return forward(s); }
+    std::vector<double> forward_nmvp(const std::vector<double>& s) const {
+        DctPlusWorkspace ws = make_workspace();
+        return forward_nmvp(s, ws);
+    }
 
+    /// fast: transposed Cauchy + DCT-III; otherwise the dense X p.
     const std::vector<double>& inverse(const std::vector<double>& p, DctPlusWorkspace& ws, bool fast = true) const {
-        (void)fast;
         check_size(p);
         ws.out.resize(n_);
-        detail::check(dctp_inverse_host_f64(h_.get(), p.data(), ws.out.data(), 1));
+        detail::check(fast ? dctp_inverse_host_f64(h_.get(), p.data(), ws.out.data(), 1)
+                           : dctp_inverse_nmvp_host_f64(h_.get(), p.data(), ws.out.data(), 1));
         return ws.out;
     }
     std::vector<double> inverse(const std::vector<double>& p, bool fast = true) const {

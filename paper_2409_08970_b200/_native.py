@@ -41,6 +41,14 @@ SIGNATURES = {
     "dctp_inverse_f64": (C.c_int, [_p, _p, _p, _sz, _p]),
     "dctp_inverse_f32": (C.c_int, [_p, _p, _p, _sz, _p]),
     "dctp_plan_sync_check": (C.c_int, [_p, _p]),
+    "dctp_forward_nmvp_f64": (C.c_int, [_p, _p, _p, _sz, _p]),
+    "dctp_forward_nmvp_f32": (C.c_int, [_p, _p, _p, _sz, _p]),
+    "dctp_inverse_nmvp_f64": (C.c_int, [_p, _p, _p, _sz, _p]),
+    "dctp_inverse_nmvp_f32": (C.c_int, [_p, _p, _p, _sz, _p]),
+    "dctp_forward_nmvp_host_f64": (C.c_int, [_p, _p, _p, _sz]),
+    "dctp_forward_nmvp_host_f32": (C.c_int, [_p, _p, _p, _sz]),
+    "dctp_inverse_nmvp_host_f64": (C.c_int, [_p, _p, _p, _sz]),
+    "dctp_inverse_nmvp_host_f32": (C.c_int, [_p, _p, _p, _sz]),
     "dctp_forward_host_f64": (C.c_int, [_p, _p, _p, _sz]),
     "dctp_inverse_host_f64": (C.c_int, [_p, _p, _p, _sz]),
     "dctp_forward_host_f32": (C.c_int, [_p, _p, _p, _sz]),

@@ -335,6 +335,14 @@ struct dctp_plan {
         int K = 0, A = 0, n_pass = 0, fold = 0;
     } sm;
     int num_sms = 0;
+    // materialised basis for the dense routes (forward_nmvp, inverse(fast =
+    // false)): X^T then X, n x ld doubles each; built on first use
+    struct Dense {
+        std::mutex mu;
+        double* buf = nullptr;
+        std::size_t ld = 0;
+    };
+    std::unique_ptr<Dense> dense = std::make_unique<Dense>();
 
     ~dctp_plan() {
         if (blob) {
@@ -343,6 +351,7 @@ struct dctp_plan {
             cudaSetDevice(device);
             cudaFree(blob);
             cudaFree(flag);
+            if (dense && dense->buf) cudaFree(dense->buf);
             cudaSetDevice(prev);
         }
     }
@@ -824,6 +833,55 @@ static void plan_basis(const dctp::host::Setup& st, double* x) {
     }, 4);
 }
 
+/// The dense routes of DctPlusPlan: forward_nmvp = X^T s (fast_transform.hpp:
+/// 199-214) and inverse(p, fast = false) = X p (:218-260), as one product with
+/// the materialised basis on the DMMA tensor cores (rows_by_basis).
+template <class T>
+static void plan_dense(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s, bool inverse) {
+    if (!p) throw std::invalid_argument("dctp_*_nmvp: null plan");
+    if (!p->blob) throw std::invalid_argument("DctPlusPlan: host-only plan (created with device < 0)");
+    if (batch == 0) return;
+    if (!in || !out) throw std::invalid_argument("dctp_*_nmvp: null buffer");
+    if (static_cast<const void*>(in) == static_cast<const void*>(out))
+        throw std::invalid_argument("dctp_*_nmvp: in and out must not alias");
+    const std::size_t n = p->st.n;
+    DeviceScope scope(p->device);
+    auto& d = *p->dense;
+    {
+        std::lock_guard<std::mutex> lock(d.mu);
+        if (!d.buf) {
+            std::vector<double> x(n * n);
+            plan_basis(p->st, x.data());
+            const std::size_t ld = (n + 3) / 4 * 4;
+            std::vector<double> both(2 * n * ld, 0.0);
+            for (std::size_t i = 0; i < n; ++i)
+                for (std::size_t j = 0; j < n; ++j) {
+                    both[j * ld + i] = x[i * n + j];     // X^T
+                    both[(n + i) * ld + j] = x[i * n + j]; // X
+                }
+            double* buf = nullptr;
+            cuda_check(cudaMalloc(reinterpret_cast<void**>(&buf), both.size() * sizeof(double)), "cudaMalloc(basis)");
+            cuda_check(cudaMemcpy(buf, both.data(), both.size() * sizeof(double), cudaMemcpyHostToDevice),
+                       "cudaMemcpy(basis)");
+            d.ld = ld;
+            d.buf = buf;
+        }
+    }
+    const double* bt = d.buf + (inverse ? n * d.ld : 0);
+    const int ni = static_cast<int>(n);
+    cuda_check(DCTP_LAUNCH(inverse ? "dense_inv" : "dense_nmvp", s,
+                           dctp::dev::rows_by_basis<T>(in, n, bt, d.ld, ni, ni, out, n, batch, p->flag, s)),
+               "dense basis kernel");
+}
+template <class T>
+static void plan_nmvp(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s) {
+    plan_dense<T>(p, in, out, batch, s, false);
+}
+template <class T>
+static void plan_inverse_dense(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s) {
+    plan_dense<T>(p, in, out, batch, s, true);
+}
+
 // --- ensemble ------------------------------------------------------------------
 
 struct dctp_ensemble {
@@ -996,6 +1054,19 @@ int dctp_inverse_f32(const dctp_plan* p, const float* in, float* out, size_t bat
     return guarded([&] { plan_inverse<float>(p, in, out, batch, static_cast<cudaStream_t>(stream)); });
 }
 
+int dctp_forward_nmvp_f64(const dctp_plan* p, const double* in, double* out, size_t batch, void* stream) {
+    return guarded([&] { plan_nmvp<double>(p, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_forward_nmvp_f32(const dctp_plan* p, const float* in, float* out, size_t batch, void* stream) {
+    return guarded([&] { plan_nmvp<float>(p, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_inverse_nmvp_f64(const dctp_plan* p, const double* in, double* out, size_t batch, void* stream) {
+    return guarded([&] { plan_inverse_dense<double>(p, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+int dctp_inverse_nmvp_f32(const dctp_plan* p, const float* in, float* out, size_t batch, void* stream) {
+    return guarded([&] { plan_inverse_dense<float>(p, in, out, batch, static_cast<cudaStream_t>(stream)); });
+}
+
 int dctp_plan_sync_check(const dctp_plan* p, void* stream) {
     return guarded([&] {
         if (!p) throw std::invalid_argument("dctp_plan_sync_check: null plan");
@@ -1077,6 +1148,10 @@ DCTP_HOST_ENTRY(dctp_forward_host_f64, double, plan_forward, true)
 DCTP_HOST_ENTRY(dctp_forward_host_f32, float, plan_forward, false)
 DCTP_HOST_ENTRY(dctp_inverse_host_f64, double, plan_inverse, false)
 DCTP_HOST_ENTRY(dctp_inverse_host_f32, float, plan_inverse, false)
+DCTP_HOST_ENTRY(dctp_forward_nmvp_host_f64, double, plan_nmvp, false)
+DCTP_HOST_ENTRY(dctp_forward_nmvp_host_f32, float, plan_nmvp, false)
+DCTP_HOST_ENTRY(dctp_inverse_nmvp_host_f64, double, plan_inverse_dense, false)
+DCTP_HOST_ENTRY(dctp_inverse_nmvp_host_f32, float, plan_inverse_dense, false)
 #undef DCTP_HOST_ENTRY
 
 int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is, const size_t* js, const double* rhos,

@@ -208,15 +208,18 @@ class DctPlusPlan:
         return x
 
     # --- apply -------------------------------------------------------------------
-    def _apply(self, x, inverse: bool, sync: bool = True, out=None):
+    _DEV = {("fwd", True): "dctp_forward_f64", ("fwd", False): "dctp_forward_f32",
+            ("inv", True): "dctp_inverse_f64", ("inv", False): "dctp_inverse_f32",
+            ("fwd_nmvp", True): "dctp_forward_nmvp_f64", ("fwd_nmvp", False): "dctp_forward_nmvp_f32",
+            ("inv_nmvp", True): "dctp_inverse_nmvp_f64", ("inv_nmvp", False): "dctp_inverse_nmvp_f32"}
+
+    def _apply(self, x, op: str, sync: bool = True, out=None):
         n = self._n
         what = "DctPlusPlan"
         if _is_device_tensor(x):
             rows, single = _dev_rows(x, n, what)
             y = out if out is not None else torch.empty_like(rows)
-            f64 = rows.dtype == torch.float64
-            fn = {(False, True): lib.dctp_forward_f64, (False, False): lib.dctp_forward_f32,
-                  (True, True): lib.dctp_inverse_f64, (True, False): lib.dctp_inverse_f32}[(inverse, f64)]
+            fn = getattr(lib, self._DEV[(op, rows.dtype == torch.float64)])
             stream = _stream_ptr(rows.device)
             check(fn(self._h, C.c_void_p(rows.data_ptr()), C.c_void_p(y.data_ptr()), rows.shape[0], stream))
             if sync:
@@ -224,24 +227,24 @@ class DctPlusPlan:
             return y.reshape(-1) if single else y
         rows, single = _as_rows(x, n, what)
         y = np.empty_like(rows)
-        f64 = rows.dtype == np.float64
-        fn = {(False, True): lib.dctp_forward_host_f64, (False, False): lib.dctp_forward_host_f32,
-              (True, True): lib.dctp_inverse_host_f64, (True, False): lib.dctp_inverse_host_f32}[(inverse, f64)]
+        name = self._DEV[(op, rows.dtype == np.float64)]
+        fn = getattr(lib, name[:-4] + "_host" + name[-4:])
         check(fn(self._h, rows.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), rows.shape[0]))
         return y.reshape(-1) if single else y
 
     def forward(self, s, sync: bool = True, out=None):
         """Coefficients in ascending-eigenvalue slot order (fast_transform.hpp:163-195)."""
-        return self._apply(s, inverse=False, sync=sync, out=out)
+        return self._apply(s, "fwd", sync=sync, out=out)
 
-    def forward_nmvp(self, s, **kw):
-        """The reference's dense X^T s (:199-214).  On B200 the same product is
-        evaluated through the DCT + direct Cauchy kernels (identical math)."""
-        return self._apply(s, inverse=False, **kw)
+    def forward_nmvp(self, s, sync: bool = True, out=None):
+        """The reference's dense X^T s (:199-214): one product with the
+        materialised basis on the fp64 tensor cores (built on first use)."""
+        return self._apply(s, "fwd_nmvp", sync=sync, out=out)
 
     def inverse(self, p, fast: bool = True, sync: bool = True, out=None):
-        """X p (:218-260); `fast` is accepted for API parity (one GPU route)."""
-        return self._apply(p, inverse=True, sync=sync, out=out)
+        """X p (:218-260): fast = the transposed Cauchy + DCT-III route,
+        fast = False the dense product with the materialised basis."""
+        return self._apply(p, "inv" if fast else "inv_nmvp", sync=sync, out=out)
 
     def sync_check(self):
         check(lib.dctp_plan_sync_check(self._h, _stream_ptr(torch.cuda.current_device())))

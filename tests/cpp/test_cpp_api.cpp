@@ -126,7 +126,7 @@ int main() {
             const auto res = ens.forward_all(s);
             CHECK(res.pruned);
             for (std::size_t r = 1; r < ens.ensemble_size(); ++r) {
-                const auto exact = ens.member(r).forward_nmvp(s);
+                const auto exact = ens.member(r).forward_nmvp(s); // dense X^T s on the GPU
                 double err = 0.0;
                 for (std::size_t j = 0; j < 32; ++j) err += (exact[j] - res.coeffs[r][j]) * (exact[j] - res.coeffs[r][j]);
                 CHECK(std::sqrt(err) <= res.bounds[r] + 1e-12);

@@ -516,3 +516,23 @@ def test_chain_forward_views_nan_and_empty(P, torch, reference):
         ch.forward(bad)
     ch.forward(dev(torch, s, torch.float64))  # the flag was cleared
     assert ch.forward(torch.empty((0, n), dtype=torch.float64, device="cuda")).shape == (0, n)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+@pytest.mark.parametrize("dtype,tol", [("float64", TOL64), ("float32", TOL32)])
+def test_dense_routes_match_reference(P, torch, reference, cid, dtype, tol):
+    """forward_nmvp (X^T s, fast_transform.hpp:199-214) and inverse(fast =
+    False) (X p, :218-260) through the materialised basis, against the
+    reference's own dense routes; device rows and host rows."""
+    cfg = O.config(cid)
+    plan = plan_for(P, cid)
+    rp = reference.plan(cfg.n, cfg.updates[0])
+    s = np.random.default_rng(31 + cid).standard_normal((257, cfg.n))
+    want = rp.forward(s, nmvp=True)
+    got = plan.forward_nmvp(dev(torch, s, getattr(torch, dtype))).double().cpu().numpy()
+    assert O.parity(got, want) <= tol
+    assert O.parity(plan.forward_nmvp(s.astype(dtype)).astype(np.float64), want) <= tol
+    back = rp.inverse(want, fast=False)
+    got = plan.inverse(dev(torch, want, getattr(torch, dtype)), fast=False).double().cpu().numpy()
+    assert O.parity(got, back) <= tol
+    assert O.parity(got, s) <= 10 * tol  # round trip

@@ -242,6 +242,9 @@ class Reference:
             lib.ref_chain_destroy.argtypes = [C.c_void_p]
             lib.ref_chain_spectrum.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_size_t)]
             lib.ref_chain_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+            lib.ref_format_update.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
+            lib.ref_csv_row.argtypes = [C.c_char_p, C.c_size_t, C.c_char_p, C.c_char_p, C.c_char_p, C.c_double,
+                                        C.c_char_p, C.c_size_t]
             lib.ref_trig.argtypes = [C.c_int, C.c_size_t, C.c_void_p, C.c_void_p, C.c_size_t]
             lib.ref_mix_seed.restype = C.c_uint64
             lib.ref_mix_seed.argtypes = [C.c_uint64, C.c_size_t, C.c_size_t]

@@ -18,6 +18,7 @@
 #include <exception>
 #include <memory>
 #include <stdexcept>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -307,6 +308,25 @@ int ref_chain_forward(const void* pv, const double* s, double* out, std::size_t 
     } catch (const std::exception& e) {
         return fail(e);
     }
+}
+
+/// bench.hpp:26-64: parse_update + format_update of a descriptor (1 on a bad
+/// one, message in ref_last_error) and one csv_row.
+int ref_format_update(const char* text, char* out, std::size_t len) {
+    try {
+        const std::string s = format_update(parse_update(text));
+        std::snprintf(out, len, "%s", s.c_str());
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+void ref_csv_row(const char* mode, std::size_t size, const char* update, const char* method, const char* metric,
+                 double value, char* out, std::size_t len) {
+    std::ostringstream os;
+    csv_row(os, mode, size, update, method, metric, value);
+    std::snprintf(out, len, "%s", os.str().c_str());
 }
 
 /// bench.hpp:99-108.

@@ -622,6 +622,10 @@ static dctp::dev::SmallPlanDev small_plan_dev(const dctp_plan* p) {
 }
 
 template <class T>
+static void plan_dense(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s, bool inverse);
+static bool dense_route(const dctp_plan* p);
+
+template <class T>
 static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s) {
     if (!p) throw std::invalid_argument("dctp_forward: null plan");
     if (!p->blob) throw std::invalid_argument("DctPlusPlan: host-only plan (created with device < 0)");
@@ -642,6 +646,10 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
                        "fused small forward kernel");
             return;
         }
+    }
+    if (dense_route(p)) {
+        plan_dense<T>(p, in, out, batch, s, false);
+        return;
     }
     // DCT; pass-through slots go straight to the output, kept coefficients
     // compacted into `hat` (batch x K) for the Cauchy stage
@@ -666,6 +674,10 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
     if (!in || !out) throw std::invalid_argument("dctp_inverse: null buffer");
     if (static_cast<const void*>(in) == static_cast<const void*>(out))
         throw std::invalid_argument("dctp_inverse: in and out must not alias");
+    if (dense_route(p)) {
+        plan_dense<T>(p, in, out, batch, s, true);
+        return;
+    }
     const std::size_t n = p->st.n;
     DeviceScope scope(p->device);
     Scratch<T> d(batch * n, s);
@@ -833,6 +845,62 @@ static void plan_basis(const dctp::host::Setup& st, double* x) {
     }, 4);
 }
 
+/// Materialises X^T and X on the device once per plan: the signed basis rows
+/// in the DCT domain (the setup's a, z, nu, sigma), one batched DCT-III over
+/// them (X^T row s = column s of X), and a transpose.
+static void ensure_dense(const dctp_plan* p, cudaStream_t s) {
+    auto& d = *p->dense;
+    std::lock_guard<std::mutex> lock(d.mu);
+    if (d.buf) return;
+    const auto& st = p->st;
+    const std::size_t n = st.n, ld = (n + 3) / 4 * 4;
+    std::vector<double> tab(5 * n, 0.0); // z, lambda, nu, a, sigma
+    std::vector<int> pidx(n);
+    for (std::size_t q = 0; q < n; ++q) {
+        tab[q] = st.z[q];
+        tab[n + q] = st.lambda[q];
+        const auto& sl = st.slots[q];
+        pidx[q] = sl.passthrough ? static_cast<int>(sl.idx) : -1;
+        tab[2 * n + q] = sl.passthrough ? 0.0 : st.sub_mu[sl.idx];
+        tab[3 * n + q] = st.a[q];
+        tab[4 * n + q] = st.sigma[q];
+    }
+    double* buf = nullptr;
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&buf), 2 * n * ld * sizeof(double)), "cudaMalloc(basis)");
+    Scratch<double> y(n * ld + 5 * n + (n + 1) / 2, s);
+    double* dtab = y.ptr + n * ld;
+    int* dp = reinterpret_cast<int*>(dtab + 5 * n);
+    cuda_check(cudaMemsetAsync(buf, 0, 2 * n * ld * sizeof(double), s), "cudaMemset(basis)");
+    cuda_check(cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaMemcpyAsync(dp, pidx.data(), n * sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+    const int ni = static_cast<int>(n);
+    cuda_check(dctp::dev::basis_coefficients(ni, ld, dtab, dtab + n, dtab + 2 * n, dp, dtab + 3 * n, dtab + 4 * n,
+                                             y.ptr, s),
+               "basis kernel");
+    cuda_check(dctp::dev::idct_rows<double>(y.ptr, ld, y.ptr, ld, dctp::dev::Emit<double>{}, buf, ld, n, n,
+                                            p->tw<double>(), p->flag, s),
+               "basis idct kernel");
+    cuda_check(dctp::dev::transpose_square(buf, ld, buf + n * ld, ld, ni, s), "transpose kernel");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(basis)");
+    d.ld = ld;
+    d.buf = buf;
+}
+
+/// The dense route replaces DCT + Cauchy when the structured work is close
+/// to a full n x n product anyway (K A >= 0.8 n^2, e.g. general directions):
+/// reading a stored X^T runs the tensor cores at ~88% against ~71% when the
+/// Cauchy block is generated, and the DCT pass disappears.  X^T and X cost
+/// 16 n^2 bytes of HBM.  DCTP_DENSE=0 / 1 forces the choice.
+static bool dense_route(const dctp_plan* p) {
+    if (p->small) return false;
+    const char* e = std::getenv("DCTP_DENSE");
+    if (e && e[0] == '0') return false;
+    const double n = static_cast<double>(p->st.n);
+    if (16.0 * n * n > 4.0 * (1ull << 30)) return false;
+    if (e && e[0] == '1') return true;
+    return n * n <= 1.25 * static_cast<double>(p->fwd.rows) * static_cast<double>(p->fwd.cols);
+}
+
 /// The dense routes of DctPlusPlan: forward_nmvp = X^T s (fast_transform.hpp:
 /// 199-214) and inverse(p, fast = false) = X p (:218-260), as one product with
 /// the materialised basis on the DMMA tensor cores (rows_by_basis).
@@ -846,27 +914,8 @@ static void plan_dense(const dctp_plan* p, const T* in, T* out, std::size_t batc
         throw std::invalid_argument("dctp_*_nmvp: in and out must not alias");
     const std::size_t n = p->st.n;
     DeviceScope scope(p->device);
-    auto& d = *p->dense;
-    {
-        std::lock_guard<std::mutex> lock(d.mu);
-        if (!d.buf) {
-            std::vector<double> x(n * n);
-            plan_basis(p->st, x.data());
-            const std::size_t ld = (n + 3) / 4 * 4;
-            std::vector<double> both(2 * n * ld, 0.0);
-            for (std::size_t i = 0; i < n; ++i)
-                for (std::size_t j = 0; j < n; ++j) {
-                    both[j * ld + i] = x[i * n + j];     // X^T
-                    both[(n + i) * ld + j] = x[i * n + j]; // X
-                }
-            double* buf = nullptr;
-            cuda_check(cudaMalloc(reinterpret_cast<void**>(&buf), both.size() * sizeof(double)), "cudaMalloc(basis)");
-            cuda_check(cudaMemcpy(buf, both.data(), both.size() * sizeof(double), cudaMemcpyHostToDevice),
-                       "cudaMemcpy(basis)");
-            d.ld = ld;
-            d.buf = buf;
-        }
-    }
+    ensure_dense(p, s);
+    const auto& d = *p->dense;
     const double* bt = d.buf + (inverse ? n * d.ld : 0);
     const int ni = static_cast<int>(n);
     cuda_check(DCTP_LAUNCH(inverse ? "dense_inv" : "dense_nmvp", s,

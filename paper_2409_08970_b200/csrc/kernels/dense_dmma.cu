@@ -201,3 +201,65 @@ template cudaError_t rows_by_basis<float>(const float*, std::size_t, const doubl
                                           std::size_t, std::size_t, int*, cudaStream_t);
 
 } // namespace dctp::dev
+
+// --- materialising a plan's basis on the device -----------------------------------
+
+namespace dctp::dev {
+namespace {
+
+/// Row s of the basis in the DCT domain, signed: sigma_s e_idx for a
+/// pass-through slot, sigma_s a_s z_j / (lambda_j - nu_s) (z_j != 0) for an
+/// active one (cauchy.hpp:90-98; the host's basis_coefficients, same ops).
+__global__ void basis_coeff_kernel(int n, std::size_t ld, const double* __restrict__ z,
+                                   const double* __restrict__ lambda, const double* __restrict__ nu,
+                                   const int* __restrict__ pass_idx, const double* __restrict__ a,
+                                   const double* __restrict__ sigma, double* __restrict__ y) {
+    const int s = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int pidx = pass_idx[s];
+    double v;
+    if (pidx >= 0) {
+        v = j == pidx ? 1.0 : 0.0;
+    } else {
+        const double zj = z[j];
+        v = zj != 0.0 ? __ddiv_rn(__dmul_rn(a[s], zj), __dsub_rn(lambda[j], nu[s])) : 0.0;
+    }
+    y[static_cast<std::size_t>(s) * ld + j] = sigma[s] < 0.0 ? -v : v;
+}
+
+__global__ void transpose_kernel(const double* __restrict__ in, std::size_t ld_in, double* __restrict__ out,
+                                 std::size_t ld_out, int n) {
+    __shared__ double tile[32][33];
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int y = y0 + r, x = x0 + threadIdx.x;
+        if (y < n && x < n) tile[r][threadIdx.x] = in[static_cast<std::size_t>(y) * ld_in + x];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int y = x0 + r, x = y0 + threadIdx.x;
+        if (y < n && x < n) out[static_cast<std::size_t>(y) * ld_out + x] = tile[threadIdx.x][r];
+    }
+}
+
+} // namespace
+
+cudaError_t basis_coefficients(int n, std::size_t ld, const double* z, const double* lambda, const double* nu,
+                               const int* pass_idx, const double* a, const double* sigma, double* y,
+                               cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    dim3 grid(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(n));
+    basis_coeff_kernel<<<grid, 256, 0, stream>>>(n, ld, z, lambda, nu, pass_idx, a, sigma, y);
+    return cudaGetLastError();
+}
+
+cudaError_t transpose_square(const double* in, std::size_t ld_in, double* out, std::size_t ld_out, int n,
+                             cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    dim3 grid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((n + 31) / 32));
+    transpose_kernel<<<grid, dim3(32, 8), 0, stream>>>(in, ld_in, out, ld_out, n);
+    return cudaGetLastError();
+}
+
+} // namespace dctp::dev

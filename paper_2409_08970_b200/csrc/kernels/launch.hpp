@@ -122,6 +122,14 @@ cudaError_t sgemm_rows(const float* A, int lda, const float* B, int ldb, float* 
 
 /// out[b, c] = sum_k in[b, k] bt[c, k] on the DMMA tensor cores (bt = X^T,
 /// 16-byte aligned rows, ld_bt even): the batched rank-k chain apply.
+/// Signed DCT-domain rows of a plan's basis (row s = sigma_s y_s, n x ld) and
+/// an n x n transpose: with idct_rows these materialise X^T and X on the device.
+cudaError_t basis_coefficients(int n, std::size_t ld, const double* z, const double* lambda, const double* nu,
+                               const int* pass_idx, const double* a, const double* sigma, double* y,
+                               cudaStream_t stream);
+cudaError_t transpose_square(const double* in, std::size_t ld_in, double* out, std::size_t ld_out, int n,
+                             cudaStream_t stream);
+
 template <class T>
 cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std::size_t ld_bt, int K, int N, T* out,
                           std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t stream);

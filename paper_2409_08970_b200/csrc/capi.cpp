@@ -624,6 +624,7 @@ static dctp::dev::SmallPlanDev small_plan_dev(const dctp_plan* p) {
 template <class T>
 static void plan_dense(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s, bool inverse);
 static bool dense_route(const dctp_plan* p);
+static void ensure_dense(const dctp_plan* p, cudaStream_t s);
 
 template <class T>
 static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s) {
@@ -1040,7 +1041,12 @@ int dctp_plan_create(size_t n, int kind, size_t i, size_t j, double rho, const d
         if (!out) throw std::invalid_argument("dctp_plan_create: null output");
         *out = nullptr;
         if (n < 2) throw std::invalid_argument("DctPlusPlan: need n >= 2");
-        *out = build_plan(n, make_update(kind, i, j, rho, v, n), epsilon, tau, device).release();
+        auto p = build_plan(n, make_update(kind, i, j, rho, v, n), epsilon, tau, device);
+        if (device >= 0 && dense_route(p.get())) { // the dense route's X^T and X are part of the setup
+            DeviceScope scope(device);
+            ensure_dense(p.get(), nullptr);
+        }
+        *out = p.release();
     });
 }
 

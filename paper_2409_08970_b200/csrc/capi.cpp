@@ -335,6 +335,15 @@ struct dctp_plan {
         int K = 0, A = 0, n_pass = 0, fold = 0;
     } sm;
     int num_sms = 0;
+    // folded route for larger antisymmetric plans (kept DCT indices all odd):
+    // u = x_j - x_{n-1-j} times W (cols x L, row c = the slot's weights), plus
+    // the half-length DCT of y = x_j + x_{n-1-j} for the even pass-through slots
+    struct {
+        bool on = false;
+        int L = 0, cols = 0, n_even = 0;
+        std::size_t ldw = 0, w = 0, map = 0, to = 0, from = 0, sign64 = 0, sign32 = 0;
+        TwiddleOffsets tw64, tw32;
+    } fd;
     // materialised basis for the dense routes (forward_nmvp, inverse(fast =
     // false)): X^T then X, n x ld doubles each; built on first use
     struct Dense {
@@ -485,6 +494,75 @@ static void build_small(dctp_plan& p, Blob& blob, const ApplyTables& t) {
     p.sm.rot = blob.add(rot);
 }
 
+/// The folded route of plans too large for the fused kernel (C3: n = 1024,
+/// edge (1, n)): when every kept DCT index is odd, each active (and odd
+/// pass-through) slot is a dot product of u_j = x_j - x_{n-1-j} (j < n/2)
+/// with a row of W = T D_odd, and the even pass-through slots come from the
+/// length-n/2 DCT of y_j = x_j + x_{n-1-j} (coefficient sigma / sqrt 2) —
+/// the algebra of the fused kernel's fold, with W stored (cols x n/2 doubles,
+/// L2-resident) and read by the DMMA product kernel.  W is built once on the
+/// host in long double from the same T entries.
+static void build_fold(dctp_plan& p, Blob& blob, const ApplyTables& t) {
+    const auto& st = p.st;
+    const std::size_t n = st.n, K = t.kept_idx.size(), A = t.nu.size();
+    if (p.small || K == 0 || A == 0 || n < 64 || (n & (n - 1)) != 0 || n > (std::size_t{1} << 14)) return;
+    for (int j : t.kept_idx)
+        if (j % 2 == 0) return;
+    std::size_t odd_pass = 0;
+    for (int j : t.pass_src) odd_pass += (j % 2 == 1);
+    const std::size_t L = n / 2, cols = A + odd_pass;
+    if (static_cast<double>(cols) * L > 1.5 * static_cast<double>(K) * A) return; // the structured route is cheaper
+    const double pi = std::numbers::pi;
+    std::vector<long double> dtab(L * L); // dtab[m][j] = sqrt(2/n) cos(pi (2m+1)(2j+1) / 2n)
+    dctp::host::parallel_for(L, [&](std::size_t m) {
+        for (std::size_t j = 0; j < L; ++j) {
+            const std::size_t q = ((2 * m + 1) * (2 * j + 1)) % (4 * n);
+            dtab[m * L + j] = std::sqrt(2.0L / n) * std::cos(static_cast<long double>(pi) * q / (2.0L * n));
+        }
+    }, 4);
+    const std::size_t ldw = (L + 3) / 4 * 4;
+    std::vector<double> w(cols * ldw, 0.0);
+    std::vector<int> map(cols), to, from;
+    std::vector<double> sign;
+    dctp::host::parallel_for(A, [&](std::size_t c) {
+        std::vector<long double> row(L, 0.0L);
+        for (std::size_t k = 0; k < K; ++k) {
+            const long double tk = t.act_scale[c] * (t.z_kept[k] / (t.lam_kept[k] - t.nu[c]));
+            const long double* d = dtab.data() + static_cast<std::size_t>((t.kept_idx[k] - 1) / 2) * L;
+            for (std::size_t j = 0; j < L; ++j) row[j] += tk * d[j];
+        }
+        for (std::size_t j = 0; j < L; ++j) w[c * ldw + j] = static_cast<double>(row[j]);
+        map[c] = t.act_slot[c];
+    }, 2);
+    std::size_t c = A;
+    for (std::size_t q = 0; q < t.pass_src.size(); ++q) {
+        const int j0 = t.pass_src[q];
+        if (j0 % 2 == 1) {
+            const long double* d = dtab.data() + static_cast<std::size_t>((j0 - 1) / 2) * L;
+            for (std::size_t j = 0; j < L; ++j) w[c * ldw + j] = static_cast<double>(t.pass_sign[q] * d[j]);
+            map[c++] = t.pass_slot[q];
+        } else {
+            to.push_back(t.pass_slot[q]);
+            from.push_back(j0 / 2);
+            sign.push_back(t.pass_sign[q] / std::numbers::sqrt2);
+        }
+    }
+    auto& f = p.fd;
+    f.L = static_cast<int>(L);
+    f.cols = static_cast<int>(cols);
+    f.n_even = static_cast<int>(to.size());
+    f.ldw = ldw;
+    f.w = blob.add(w);
+    f.map = blob.add(map);
+    f.to = blob.add(to);
+    f.from = blob.add(from);
+    f.sign64 = blob.add(sign);
+    f.sign32 = blob.add(to_f32(sign));
+    f.tw64 = add_twiddles<double>(blob, L);
+    f.tw32 = add_twiddles<float>(blob, L);
+    f.on = true;
+}
+
 /// Development knob for profiling the fused kernel's phases in isolation
 /// (DCTP_DEBUG_MODE bits: 1 = DCT work skipped, 2 = DMMA work skipped, 4 = producer
 /// phase timers); 0 otherwise.
@@ -538,6 +616,7 @@ static void upload_plan(dctp_plan& p) {
     p.act_slot = act;
     p.kept = kept_idx;
     build_small(p, blob, t);
+    build_fold(p, blob, t);
     p.pass_sign64 = blob.add(t.pass_sign);
     p.pass_sign32 = blob.add(to_f32(t.pass_sign));
     p.n_pass = static_cast<int>(t.pass_slot.size());
@@ -626,6 +705,13 @@ static void plan_dense(const dctp_plan* p, const T* in, T* out, std::size_t batc
 static bool dense_route(const dctp_plan* p);
 static void ensure_dense(const dctp_plan* p, cudaStream_t s);
 
+/// DCTP_FOLD=0 turns the folded route off (structured DCT + Cauchy instead).
+static bool fold_route(const dctp_plan* p) {
+    if (!p->fd.on) return false;
+    const char* e = std::getenv("DCTP_FOLD");
+    return !(e && e[0] == '0');
+}
+
 template <class T>
 static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s) {
     if (!p) throw std::invalid_argument("dctp_forward: null plan");
@@ -650,6 +736,23 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
     }
     if (dense_route(p)) {
         plan_dense<T>(p, in, out, batch, s, false);
+        return;
+    }
+    if (fold_route(p)) {
+        const auto& f = p->fd;
+        constexpr bool f32 = std::is_same_v<T, float>;
+        const dctp::dev::Emit<T> even{at<int>(p->blob, f.to), at<int>(p->blob, f.from),
+                                      at<T>(p->blob, f32 ? f.sign32 : f.sign64), f.n_even};
+        Scratch<T> u(batch * static_cast<std::size_t>(f.L), s);
+        cuda_check(DCTP_LAUNCH("fold_dct", s,
+                               dctp::dev::dct2_fold_rows<T>(in, n, u.ptr, f.L, out, n, even, f.L, batch,
+                                                            twiddles_at<T>(p->blob, f32 ? f.tw32 : f.tw64), p->flag,
+                                                            s)),
+                   "fold dct kernel");
+        cuda_check(DCTP_LAUNCH("fold_w", s,
+                               dctp::dev::rows_by_basis<T>(u.ptr, f.L, at<double>(p->blob, f.w), f.ldw, f.L, f.cols, out,
+                                                           n, batch, p->flag, s, at<int>(p->blob, f.map))),
+                   "fold product kernel");
         return;
     }
     // DCT; pass-through slots go straight to the output, kept coefficients

@@ -101,7 +101,10 @@ std::size_t fft_smem_bytes(std::size_t n, int rows) {
     return 2 * static_cast<std::size_t>(rows) * padded_len(static_cast<int>(n / 2)) * sizeof(T) * 2;
 }
 
-template <class T>
+/// FOLD (antisymmetric plans): the input rows hold 2n samples; the kernel
+/// writes u_j = x_j - x_{2n-1-j} to `hat` and transforms y_j = x_j + x_{2n-1-j}
+/// (length n), whose DCT gives the even coefficients of the full row.
+template <class T, bool FOLD = false>
 __global__ void __launch_bounds__(kThreads)
 dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat, std::size_t ld_hat,
                 T* __restrict__ out, std::size_t ld_out, Emit<T> emit, int n, int logn,
@@ -122,11 +125,13 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
     bool bad = false;
     constexpr int U = 8;
     for (int t0 = threadIdx.x; t0 < rows * n; t0 += U * kThreads) {
-        T xv[U];
+        T xv[U], xm[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int t = t0 + u * kThreads;
-            xv[u] = t < rows * n ? in[(b0 + (t >> logn)) * ld_in + (t & (n - 1))] : T(0);
+            const std::size_t row = (b0 + (t >> logn)) * ld_in;
+            xv[u] = t < rows * n ? in[row + (t & (n - 1))] : T(0);
+            if constexpr (FOLD) xm[u] = t < rows * n ? in[row + 2 * n - 1 - (t & (n - 1))] : T(0);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -134,8 +139,14 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
             if (t >= rows * n) break;
             const int r = t >> logn, j = t & (n - 1);
             bad |= !finite_val(xv[u]);
+            T v = xv[u];
+            if constexpr (FOLD) {
+                bad |= !finite_val(xm[u]);
+                hat[(b0 + r) * ld_hat + j] = xv[u] - xm[u];
+                v = xv[u] + xm[u];
+            }
             const int p = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
-            reinterpret_cast<T*>(&nat[r * ld + pad8(p >> 1)])[p & 1] = xv[u];
+            reinterpret_cast<T*>(&nat[r * ld + pad8(p >> 1)])[p & 1] = v;
         }
     }
     if (bad) atomicOr(flag, 1);
@@ -173,7 +184,7 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
     }
     __syncthreads();
 
-    if (hat != nullptr)
+    if (!FOLD && hat != nullptr)
         for (int t = threadIdx.x; t < rows * n; t += blockDim.x) {
             const int r = t >> logn, k = t & (n - 1);
             hat[(b0 + r) * ld_hat + k] = sh[t];
@@ -393,6 +404,23 @@ cudaError_t dct2_rows(const T* in, std::size_t ld_in, T* hat, std::size_t ld_hat
 }
 
 template <class T>
+cudaError_t dct2_fold_rows(const T* in, std::size_t ld_in, T* u, std::size_t ld_u, T* out, std::size_t ld_out,
+                           Emit<T> emit, std::size_t n, std::size_t batch, Twiddles<T> tw, int* flag,
+                           cudaStream_t stream) {
+    if (batch == 0) return cudaSuccess;
+    if (!is_pow2(n) || n < 2) return cudaErrorInvalidValue;
+    const int rows = rows_per_cta_for<T>(n);
+    const std::size_t smem = fft_smem_bytes<T>(n, rows);
+    auto kern = dct2_fft_kernel<T, true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const unsigned grid = static_cast<unsigned>((batch + rows - 1) / rows);
+    kern<<<grid, kThreads, smem, stream>>>(in, ld_in, u, ld_u, out, ld_out, emit, static_cast<int>(n), ilog2(n), rows,
+                                          batch, tw, flag);
+    return cudaGetLastError();
+}
+
+template <class T>
 cudaError_t idct_rows(const T* d, std::size_t ld_d, const T* p, std::size_t ld_p, Emit<T> emit,
                       T* out, std::size_t ld_out, std::size_t n, std::size_t batch,
                       Twiddles<T> tw, int* flag, cudaStream_t stream) {
@@ -422,6 +450,11 @@ template cudaError_t dct2_rows<double>(const double*, std::size_t, double*, std:
                                        Emit<double>, std::size_t, std::size_t, Twiddles<double>, int*, cudaStream_t);
 template cudaError_t dct2_rows<float>(const float*, std::size_t, float*, std::size_t, float*, std::size_t,
                                       Emit<float>, std::size_t, std::size_t, Twiddles<float>, int*, cudaStream_t);
+template cudaError_t dct2_fold_rows<double>(const double*, std::size_t, double*, std::size_t, double*, std::size_t,
+                                            Emit<double>, std::size_t, std::size_t, Twiddles<double>, int*,
+                                            cudaStream_t);
+template cudaError_t dct2_fold_rows<float>(const float*, std::size_t, float*, std::size_t, float*, std::size_t,
+                                           Emit<float>, std::size_t, std::size_t, Twiddles<float>, int*, cudaStream_t);
 template cudaError_t idct_rows<double>(const double*, std::size_t, const double*, std::size_t, Emit<double>,
                                        double*, std::size_t, std::size_t, std::size_t, Twiddles<double>, int*,
                                        cudaStream_t);

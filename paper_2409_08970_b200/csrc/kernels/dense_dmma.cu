@@ -38,7 +38,8 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 template <class T>
 __global__ void __launch_bounds__(kThreads, 2)
 rows_by_basis_kernel(const T* __restrict__ in, std::size_t ld_in, const double* __restrict__ bt, std::size_t ld_bt,
-                     int K, int N, T* __restrict__ out, std::size_t ld_out, std::size_t batch, int* flag, int vec16) {
+                     int K, int N, T* __restrict__ out, std::size_t ld_out, std::size_t batch, int* flag, int vec16,
+                     const int* __restrict__ col_map) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw); // 2 x BM x LDS_
     double* Bs = As + 2 * BM * LDS_;                  // 2 x BN x LDS_ ([c][k])
@@ -163,7 +164,7 @@ rows_by_basis_kernel(const T* __restrict__ in, std::size_t ld_in, const double* 
                 const int c = c0 + wn + j * 8 + 2 * (lane & 3) + e;
                 if (c < N) {
                     bad |= !isfinite(acc[i][j][e]);
-                    orow[c] = static_cast<T>(acc[i][j][e]);
+                    orow[col_map ? __ldg(col_map + c) : c] = static_cast<T>(acc[i][j][e]);
                 }
             }
     }
@@ -174,7 +175,7 @@ rows_by_basis_kernel(const T* __restrict__ in, std::size_t ld_in, const double* 
 
 template <class T>
 cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std::size_t ld_bt, int K, int N, T* out,
-                          std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t stream) {
+                          std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t stream, const int* col_map) {
     if (batch == 0 || N == 0) return cudaSuccess;
     if (ld_bt % 2 != 0 || reinterpret_cast<std::uintptr_t>(bt) % 16 != 0) return cudaErrorInvalidValue;
     constexpr std::size_t smem = 2 * (BM + BN) * LDS_ * sizeof(double);
@@ -188,7 +189,8 @@ cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std:
         const std::size_t rows = batch - r0 < kMaxRows ? batch - r0 : kMaxRows;
         dim3 grid(static_cast<unsigned>((N + BN - 1) / BN), static_cast<unsigned>((rows + BM - 1) / BM));
         rows_by_basis_kernel<T><<<grid, kThreads, smem, stream>>>(in + r0 * ld_in, ld_in, bt, ld_bt, K, N,
-                                                                  out + r0 * ld_out, ld_out, rows, flag, vec16);
+                                                                  out + r0 * ld_out, ld_out, rows, flag, vec16,
+                                                                  col_map);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -196,9 +198,9 @@ cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std:
 }
 
 template cudaError_t rows_by_basis<double>(const double*, std::size_t, const double*, std::size_t, int, int, double*,
-                                           std::size_t, std::size_t, int*, cudaStream_t);
+                                           std::size_t, std::size_t, int*, cudaStream_t, const int*);
 template cudaError_t rows_by_basis<float>(const float*, std::size_t, const double*, std::size_t, int, int, float*,
-                                          std::size_t, std::size_t, int*, cudaStream_t);
+                                          std::size_t, std::size_t, int*, cudaStream_t, const int*);
 
 } // namespace dctp::dev
 

@@ -39,6 +39,14 @@ cudaError_t dct2_rows(const T* in, std::size_t ld_in, T* hat, std::size_t ld_hat
                       std::size_t ld_out, Emit<T> emit, std::size_t n, std::size_t batch,
                       Twiddles<T> tw, int* flag, cudaStream_t stream);
 
+/// Folded forward of antisymmetric plans: rows of 2n samples x; writes
+/// u_j = x_j - x_{2n-1-j} (n per row) to `u` and emits the DCT-II (length n)
+/// of y_j = x_j + x_{2n-1-j} through `emit`.
+template <class T>
+cudaError_t dct2_fold_rows(const T* in, std::size_t ld_in, T* u, std::size_t ld_u, T* out, std::size_t ld_out,
+                           Emit<T> emit, std::size_t n, std::size_t batch, Twiddles<T> tw, int* flag,
+                           cudaStream_t stream);
+
 /// Inverse (DCT-III, orthonormal, U d) of rows d; before the transform
 ///   d[to[e]] = sign[e] * p[b*ld_p + from[e]]  (the pass-through slots).
 template <class T>
@@ -120,8 +128,6 @@ bool sgemm_rows_supported(int K, int N, int lda, int ldb, std::size_t ldc, const
 cudaError_t sgemm_rows(const float* A, int lda, const float* B, int ldb, float* C, std::size_t ldc, std::size_t M,
                        int N, int K, int* flag, cudaStream_t stream);
 
-/// out[b, c] = sum_k in[b, k] bt[c, k] on the DMMA tensor cores (bt = X^T,
-/// 16-byte aligned rows, ld_bt even): the batched rank-k chain apply.
 /// Signed DCT-domain rows of a plan's basis (row s = sigma_s y_s, n x ld) and
 /// an n x n transpose: with idct_rows these materialise X^T and X on the device.
 cudaError_t basis_coefficients(int n, std::size_t ld, const double* z, const double* lambda, const double* nu,
@@ -130,9 +136,13 @@ cudaError_t basis_coefficients(int n, std::size_t ld, const double* z, const dou
 cudaError_t transpose_square(const double* in, std::size_t ld_in, double* out, std::size_t ld_out, int n,
                              cudaStream_t stream);
 
+/// out[b, col_map ? col_map[c] : c] = sum_k in[b, k] bt[c, k] on the DMMA
+/// tensor cores (bt row-major, 16-byte aligned rows, ld_bt even): the rank-k
+/// chain apply, the dense routes, the folded route's W product.
 template <class T>
 cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std::size_t ld_bt, int K, int N, T* out,
-                          std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t stream);
+                          std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t stream,
+                          const int* col_map = nullptr);
 
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);

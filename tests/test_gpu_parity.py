@@ -568,3 +568,32 @@ def test_dense_route_selected_for_full_updates(P, torch, reference, monkeypatch,
             P.profile_enable(False)
             assert set(P.profile_summary()) == {"dense_nmvp"}
     monkeypatch.delenv("DCTP_DENSE")
+
+
+@pytest.mark.parametrize("n,u", [(1024, O.Update(1, 1.0, 1, 1024)), (512, O.Update(1, -0.6, 100, 413)),
+                                 (2048, O.Update(1, 2.0, 7, 2042))])
+def test_folded_route_for_antisymmetric_plans(P, torch, reference, monkeypatch, n, u):
+    """Antisymmetric updates above the fused kernel's sizes take the folded
+    route (u times the stored W on DMMA, half-length DCT for the even
+    pass-through slots); it matches the reference (exact route: C3 is a slow
+    path, the others are pinned on the reference's dense route) and the
+    structured route (DCTP_FOLD=0), fp64 and fp32."""
+    s = np.random.default_rng(n + 1).standard_normal((333, n))
+    want = reference.plan(n, u).forward(s, nmvp=True)
+    plan = P.DctPlusPlan(n, upd(P, u), 1e-12)
+    got = {}
+    for mode in ("auto", "0"):
+        if mode == "0":
+            monkeypatch.setenv("DCTP_FOLD", "0")
+        for dtype, tol in (("float64", TOL64), ("float32", TOL32)):
+            y = plan.forward(dev(torch, s, getattr(torch, dtype))).double().cpu().numpy()
+            assert O.parity(y, want) <= tol, (mode, dtype)
+            got[(mode, dtype)] = y
+        if mode == "auto" and n != 512:
+            P.profile_reset()
+            P.profile_enable(True)
+            plan.forward(dev(torch, s, torch.float64))
+            P.profile_enable(False)
+            assert set(P.profile_summary()) == {"fold_dct", "fold_w"}
+    monkeypatch.delenv("DCTP_FOLD")
+    assert O.parity(got[("auto", "float64")], got[("0", "float64")]) <= 1e-12

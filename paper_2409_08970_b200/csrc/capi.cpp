@@ -342,6 +342,7 @@ struct dctp_plan {
         bool on = false;
         int L = 0, cols = 0, n_even = 0;
         std::size_t ldw = 0, w = 0, map = 0, to = 0, from = 0, sign64 = 0, sign32 = 0;
+        std::size_t ldwt = 0, wt = 0, zero = 0; // inverse: W^T (L x cols) and a zero row
         TwiddleOffsets tw64, tw32;
     } fd;
     // materialised basis for the dense routes (forward_nmvp, inverse(fast =
@@ -547,7 +548,14 @@ static void build_fold(dctp_plan& p, Blob& blob, const ApplyTables& t) {
             sign.push_back(t.pass_sign[q] / std::numbers::sqrt2);
         }
     }
+    const std::size_t ldwt = (cols + 3) / 4 * 4;
+    std::vector<double> wt(L * ldwt, 0.0);
+    for (std::size_t r = 0; r < cols; ++r)
+        for (std::size_t j = 0; j < L; ++j) wt[j * ldwt + r] = w[r * ldw + j];
     auto& f = p.fd;
+    f.ldwt = ldwt;
+    f.wt = blob.add(wt);
+    f.zero = blob.add(std::vector<double>(L, 0.0));
     f.L = static_cast<int>(L);
     f.cols = static_cast<int>(cols);
     f.n_even = static_cast<int>(to.size());
@@ -780,6 +788,27 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
         throw std::invalid_argument("dctp_inverse: in and out must not alias");
     if (dense_route(p)) {
         plan_dense<T>(p, in, out, batch, s, true);
+        return;
+    }
+    if (fold_route(p)) {
+        // x_j = w_j + v_j, x_{n-1-j} = w_j - v_j: w = DCT-III (length n/2) of the
+        // even slots (sigma / sqrt 2), v = W^T p over the W slots
+        const auto& f = p->fd;
+        const std::size_t n = p->st.n;
+        constexpr bool f32 = std::is_same_v<T, float>;
+        DeviceScope scope(p->device);
+        const dctp::dev::Emit<T> even{at<int>(p->blob, f.from), at<int>(p->blob, f.to),
+                                      at<T>(p->blob, f32 ? f.sign32 : f.sign64), f.n_even};
+        Scratch<T> w(batch * static_cast<std::size_t>(f.L), s);
+        cuda_check(DCTP_LAUNCH("fold_idct", s,
+                               dctp::dev::idct_rows<T>(at<T>(p->blob, f.zero), 0, in, n, even, w.ptr, f.L, f.L, batch,
+                                                       twiddles_at<T>(p->blob, f32 ? f.tw32 : f.tw64), p->flag, s)),
+                   "fold idct kernel");
+        cuda_check(DCTP_LAUNCH("fold_wt", s,
+                               dctp::dev::rows_by_basis<T>(in, n, at<double>(p->blob, f.wt), f.ldwt, f.cols, f.L, out, n,
+                                                           batch, p->flag, s, nullptr, at<int>(p->blob, f.map), w.ptr,
+                                                           f.L)),
+                   "fold product kernel");
         return;
     }
     const std::size_t n = p->st.n;

@@ -39,7 +39,8 @@ template <class T>
 __global__ void __launch_bounds__(kThreads, 2)
 rows_by_basis_kernel(const T* __restrict__ in, std::size_t ld_in, const double* __restrict__ bt, std::size_t ld_bt,
                      int K, int N, T* __restrict__ out, std::size_t ld_out, std::size_t batch, int* flag, int vec16,
-                     const int* __restrict__ col_map) {
+                     const int* __restrict__ col_map, const int* __restrict__ a_map, const T* __restrict__ fold_add,
+                     std::size_t ld_add) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw); // 2 x BM x LDS_
     double* Bs = As + 2 * BM * LDS_;                  // 2 x BN x LDS_ ([c][k])
@@ -78,12 +79,13 @@ rows_by_basis_kernel(const T* __restrict__ in, std::size_t ld_in, const double* 
             return;
         }
         const int k = tid % BK, kk = chunk * BK + k;
+        const int src = kk < K ? (a_map ? __ldg(a_map + kk) : kk) : 0;
 #pragma unroll
         for (int i = 0; i < BM / (kThreads / BK); ++i) {
             const int m = tid / BK + i * (kThreads / BK);
             const bool ok = kk < K && b0 + m < batch;
             cp_async8(As + buf * BM * LDS_ + m * LDS_ + k,
-                      reinterpret_cast<const double*>(in) + (ok ? (b0 + m) * ld_in + kk : 0), ok);
+                      reinterpret_cast<const double*>(in) + (ok ? (b0 + m) * ld_in + src : 0), ok);
         }
     };
     // A, fp32: one chunk prefetched into registers, widened on the store
@@ -91,10 +93,11 @@ rows_by_basis_kernel(const T* __restrict__ in, std::size_t ld_in, const double* 
     float ra[kAR];
     auto fetch_a32 = [&](int chunk) {
         const int k = tid % BK, kk = chunk * BK + k;
+        const int src = kk < K ? (a_map ? __ldg(a_map + kk) : kk) : 0;
 #pragma unroll
         for (int i = 0; i < kAR; ++i) {
             const std::size_t b = b0 + tid / BK + i * (kThreads / BK);
-            ra[i] = kk < K && b < batch ? reinterpret_cast<const float*>(in)[b * ld_in + kk] : 0.f;
+            ra[i] = kk < K && b < batch ? reinterpret_cast<const float*>(in)[b * ld_in + src] : 0.f;
         }
     };
     auto store_a32 = [&](int buf) {
@@ -164,7 +167,13 @@ rows_by_basis_kernel(const T* __restrict__ in, std::size_t ld_in, const double* 
                 const int c = c0 + wn + j * 8 + 2 * (lane & 3) + e;
                 if (c < N) {
                     bad |= !isfinite(acc[i][j][e]);
-                    orow[col_map ? __ldg(col_map + c) : c] = static_cast<T>(acc[i][j][e]);
+                    if (fold_add) { // unfold: x_c = w_c + v_c, x_{2N-1-c} = w_c - v_c
+                        const double w = static_cast<double>(fold_add[b * ld_add + c]);
+                        orow[c] = static_cast<T>(w + acc[i][j][e]);
+                        orow[2 * N - 1 - c] = static_cast<T>(w - acc[i][j][e]);
+                    } else {
+                        orow[col_map ? __ldg(col_map + c) : c] = static_cast<T>(acc[i][j][e]);
+                    }
                 }
             }
     }
@@ -175,7 +184,8 @@ rows_by_basis_kernel(const T* __restrict__ in, std::size_t ld_in, const double* 
 
 template <class T>
 cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std::size_t ld_bt, int K, int N, T* out,
-                          std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t stream, const int* col_map) {
+                          std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t stream, const int* col_map,
+                          const int* a_map, const T* fold_add, std::size_t ld_add) {
     if (batch == 0 || N == 0) return cudaSuccess;
     if (ld_bt % 2 != 0 || reinterpret_cast<std::uintptr_t>(bt) % 16 != 0) return cudaErrorInvalidValue;
     constexpr std::size_t smem = 2 * (BM + BN) * LDS_ * sizeof(double);
@@ -183,14 +193,15 @@ cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std:
                                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          static_cast<int>(smem));
     if (attr != cudaSuccess) return attr;
-    const int vec16 = (reinterpret_cast<std::uintptr_t>(in) % 16 == 0) && (ld_in % 2 == 0);
+    const int vec16 = !a_map && (reinterpret_cast<std::uintptr_t>(in) % 16 == 0) && (ld_in % 2 == 0);
     constexpr std::size_t kMaxRows = std::size_t{65535} * BM; // gridDim.y limit
     for (std::size_t r0 = 0; r0 < batch; r0 += kMaxRows) {
         const std::size_t rows = batch - r0 < kMaxRows ? batch - r0 : kMaxRows;
         dim3 grid(static_cast<unsigned>((N + BN - 1) / BN), static_cast<unsigned>((rows + BM - 1) / BM));
         rows_by_basis_kernel<T><<<grid, kThreads, smem, stream>>>(in + r0 * ld_in, ld_in, bt, ld_bt, K, N,
                                                                   out + r0 * ld_out, ld_out, rows, flag, vec16,
-                                                                  col_map);
+                                                                  col_map, a_map,
+                                                                  fold_add ? fold_add + r0 * ld_add : nullptr, ld_add);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -198,9 +209,11 @@ cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std:
 }
 
 template cudaError_t rows_by_basis<double>(const double*, std::size_t, const double*, std::size_t, int, int, double*,
-                                           std::size_t, std::size_t, int*, cudaStream_t, const int*);
+                                           std::size_t, std::size_t, int*, cudaStream_t, const int*, const int*,
+                                           const double*, std::size_t);
 template cudaError_t rows_by_basis<float>(const float*, std::size_t, const double*, std::size_t, int, int, float*,
-                                          std::size_t, std::size_t, int*, cudaStream_t, const int*);
+                                          std::size_t, std::size_t, int*, cudaStream_t, const int*, const int*,
+                                          const float*, std::size_t);
 
 } // namespace dctp::dev
 

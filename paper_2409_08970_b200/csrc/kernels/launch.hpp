@@ -136,13 +136,16 @@ cudaError_t basis_coefficients(int n, std::size_t ld, const double* z, const dou
 cudaError_t transpose_square(const double* in, std::size_t ld_in, double* out, std::size_t ld_out, int n,
                              cudaStream_t stream);
 
-/// out[b, col_map ? col_map[c] : c] = sum_k in[b, k] bt[c, k] on the DMMA
-/// tensor cores (bt row-major, 16-byte aligned rows, ld_bt even): the rank-k
-/// chain apply, the dense routes, the folded route's W product.
+/// v[b, c] = sum_k in[b, a_map ? a_map[k] : k] bt[c, k] on the DMMA tensor
+/// cores (bt row-major, 16-byte aligned rows, ld_bt even), stored to
+/// out[b, col_map ? col_map[c] : c], or — with fold_add — unfolded:
+/// out[b, c] = add[b, c] + v, out[b, 2N-1-c] = add[b, c] - v.  The rank-k
+/// chain apply, the dense routes, and the folded route's W products.
 template <class T>
 cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std::size_t ld_bt, int K, int N, T* out,
                           std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t stream,
-                          const int* col_map = nullptr);
+                          const int* col_map = nullptr, const int* a_map = nullptr, const T* fold_add = nullptr,
+                          std::size_t ld_add = 0);
 
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);

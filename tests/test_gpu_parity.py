@@ -579,7 +579,9 @@ def test_folded_route_for_antisymmetric_plans(P, torch, reference, monkeypatch, 
     path, the others are pinned on the reference's dense route) and the
     structured route (DCTP_FOLD=0), fp64 and fp32."""
     s = np.random.default_rng(n + 1).standard_normal((333, n))
-    want = reference.plan(n, u).forward(s, nmvp=True)
+    rp = reference.plan(n, u)
+    want = rp.forward(s, nmvp=True)
+    back_want = rp.inverse(want, fast=False)
     plan = P.DctPlusPlan(n, upd(P, u), 1e-12)
     got = {}
     for mode in ("auto", "0"):
@@ -589,11 +591,13 @@ def test_folded_route_for_antisymmetric_plans(P, torch, reference, monkeypatch, 
             y = plan.forward(dev(torch, s, getattr(torch, dtype))).double().cpu().numpy()
             assert O.parity(y, want) <= tol, (mode, dtype)
             got[(mode, dtype)] = y
+            b = plan.inverse(dev(torch, want, getattr(torch, dtype))).double().cpu().numpy()
+            assert O.parity(b, back_want) <= tol, (mode, dtype, "inverse")
         if mode == "auto" and n != 512:
             P.profile_reset()
             P.profile_enable(True)
-            plan.forward(dev(torch, s, torch.float64))
+            plan.inverse(plan.forward(dev(torch, s, torch.float64)))
             P.profile_enable(False)
-            assert set(P.profile_summary()) == {"fold_dct", "fold_w"}
+            assert set(P.profile_summary()) == {"fold_dct", "fold_w", "fold_idct", "fold_wt"}
     monkeypatch.delenv("DCTP_FOLD")
     assert O.parity(got[("auto", "float64")], got[("0", "float64")]) <= 1e-12

@@ -343,6 +343,7 @@ struct dctp_plan {
         int L = 0, cols = 0, n_even = 0;
         std::size_t ldw = 0, w = 0, map = 0, to = 0, from = 0, sign64 = 0, sign32 = 0;
         std::size_t ldwt = 0, wt = 0, zero = 0; // inverse: W^T (L x cols) and a zero row
+        std::size_t wt32 = 0;                    // fp32 forward: W^T rounded, the SGEMM's B (L x ldwt)
         TwiddleOffsets tw64, tw32;
     } fd;
     // materialised basis for the dense routes (forward_nmvp, inverse(fast =
@@ -555,6 +556,7 @@ static void build_fold(dctp_plan& p, Blob& blob, const ApplyTables& t) {
     auto& f = p.fd;
     f.ldwt = ldwt;
     f.wt = blob.add(wt);
+    f.wt32 = blob.add(to_f32(wt));
     f.zero = blob.add(std::vector<double>(L, 0.0));
     f.L = static_cast<int>(L);
     f.cols = static_cast<int>(cols);
@@ -757,6 +759,17 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
                                                             twiddles_at<T>(p->blob, f32 ? f.tw32 : f.tw64), p->flag,
                                                             s)),
                    "fold dct kernel");
+        if constexpr (f32) {
+            // fp32: the FFMA2 SGEMM with W^T rounded once (twice the DMMA rate)
+            const float* b = at<float>(p->blob, f.wt32);
+            if (dctp::dev::sgemm_rows_supported(f.L, f.cols, f.L, static_cast<int>(f.ldwt), 4, u.ptr, b, b)) {
+                cuda_check(DCTP_LAUNCH("fold_w", s,
+                                       dctp::dev::sgemm_rows(u.ptr, f.L, b, static_cast<int>(f.ldwt), out, n, batch,
+                                                             f.cols, f.L, p->flag, s, at<int>(p->blob, f.map))),
+                           "fold sgemm kernel");
+                return;
+            }
+        }
         cuda_check(DCTP_LAUNCH("fold_w", s,
                                dctp::dev::rows_by_basis<T>(u.ptr, f.L, at<double>(p->blob, f.w), f.ldw, f.L, f.cols, out,
                                                            n, batch, p->flag, s, at<int>(p->blob, f.map))),

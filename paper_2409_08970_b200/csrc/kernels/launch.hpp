@@ -126,7 +126,7 @@ cudaError_t rdo_select_rows(const T* coeffs, std::size_t n, int sets, std::size_
 /// column 0 of a row is non-finite (the progressive DC coefficient).
 bool sgemm_rows_supported(int K, int N, int lda, int ldb, std::size_t ldc, const void* A, const void* B, const void* C);
 cudaError_t sgemm_rows(const float* A, int lda, const float* B, int ldb, float* C, std::size_t ldc, std::size_t M,
-                       int N, int K, int* flag, cudaStream_t stream);
+                       int N, int K, int* flag, cudaStream_t stream, const int* col_map = nullptr);
 
 /// Signed DCT-domain rows of a plan's basis (row s = sigma_s y_s, n x ld) and
 /// an n x n transpose: with idct_rows these materialise X^T and X on the device.

@@ -29,7 +29,7 @@ constexpr int BM = 128, BN = 128, BK = 16, kThreads = 256, LDA_S = BM + 4;
 
 __global__ void __launch_bounds__(kThreads, 2)
 sgemm_rows_kernel(const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb, float* __restrict__ C,
-                  std::size_t ldc, std::size_t M, int N, int K, int* flag) {
+                  std::size_t ldc, std::size_t M, int N, int K, int* flag, const int* __restrict__ col_map) {
     __shared__ __align__(16) float As[2][BK][LDA_S];
     __shared__ __align__(16) float Bs[2][BK][BN];
     const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
@@ -107,6 +107,17 @@ sgemm_rows_kernel(const float* __restrict__ A, int lda, const float* __restrict_
         if (m >= M) continue;
         float* crow = C + m * ldc;
         const int c0 = n0 + tx * 4, c1 = n0 + 64 + tx * 4;
+        if (col_map) { // scattered output slots; every value is checked
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int c = (q < 4 ? c0 : c1) + (q & 3);
+                if (c < N) {
+                    crow[__ldg(col_map + c)] = acc[i][q];
+                    bad |= !isfinite(acc[i][q]);
+                }
+            }
+            continue;
+        }
         if (c0 < N) *reinterpret_cast<float4*>(crow + c0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
         if (c1 < N) *reinterpret_cast<float4*>(crow + c1) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
         // column 0 is set 0's DC coefficient, sum(x)/sqrt(n): any non-finite input shows there
@@ -123,15 +134,15 @@ bool sgemm_rows_supported(int K, int N, int lda, int ldb, std::size_t ldc, const
 }
 
 cudaError_t sgemm_rows(const float* A, int lda, const float* B, int ldb, float* C, std::size_t ldc, std::size_t M,
-                       int N, int K, int* flag, cudaStream_t stream) {
+                       int N, int K, int* flag, cudaStream_t stream, const int* col_map) {
     if (M == 0 || N == 0) return cudaSuccess;
-    if (!sgemm_rows_supported(K, N, lda, ldb, ldc, A, B, C)) return cudaErrorInvalidValue;
+    if (!sgemm_rows_supported(K, N, lda, ldb, col_map ? 4 : ldc, A, B, col_map ? B : C)) return cudaErrorInvalidValue;
     constexpr std::size_t kMaxRows = std::size_t{65535} * BM; // gridDim.y limit
     for (std::size_t r0 = 0; r0 < M; r0 += kMaxRows) {
         const std::size_t rows = M - r0 < kMaxRows ? M - r0 : kMaxRows;
         dim3 grid(static_cast<unsigned>((N + BN - 1) / BN), static_cast<unsigned>((rows + BM - 1) / BM));
         sgemm_rows_kernel<<<grid, kThreads, 0, stream>>>(A + r0 * lda, lda, B, ldb, C + r0 * ldc, ldc, rows, N, K,
-                                                         flag);
+                                                         flag, col_map);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

@@ -323,9 +323,18 @@ def run_gpu_arm(args, cfg, rank: int, local: int, world: int):
     # The dominant kernel's algorithmic work per launch: the
     # direct Cauchy stage 2 * n_kept * n_active (* K members) plus 2.5 n log2 n
     # for the DCT, per signal; bytes = elem * n * (1 + K_out) per signal.
-    flops = (alg["flops_cauchy"] + alg["flops_dct"]) * cfg.batch
+    # A product kernel (Cauchy stage, folded W product, dense basis, chain,
+    # progressive SGEMM) is rated on the Cauchy-stage flops over its own
+    # launch time; the fused kernel also carries the DCT; any other top
+    # kernel falls back to the whole step.
+    product = any(k in top for k in ("cauchy", "fold_w", "dense", "chain", "progressive_sgemm"))
+    if "fused" in top:
+        flops, t_ms = (alg["flops_cauchy"] + alg["flops_dct"]) * cfg.batch, per_launch_ms[top]
+    elif product:
+        flops, t_ms = alg["flops_cauchy"] * cfg.batch, per_launch_ms[top]
+    else:
+        flops, t_ms = (alg["flops_cauchy"] + alg["flops_dct"]) * cfg.batch, ms_per_step
     nbytes = alg["bytes"] * cfg.batch
-    t_ms = per_launch_ms[top] if ("fused" in top or "cauchy" in top or "chain" in top) else ms_per_step
     if f32:
         peak = max(fp.get("fp32_fma_tflops") or 0.0, fp.get("fp32_ffma2_tflops") or 0.0) or None
         src = "profiles/peaks_fp64.json max(fp32_fma_tflops, fp32_ffma2_tflops) (tools/peaks.cu, measured)"

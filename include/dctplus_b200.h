@@ -78,6 +78,14 @@ int dctp_plan_destroy(dctp_plan* plan);
 int dctp_plan_info(const dctp_plan* plan, size_t* n, double* epsilon, int* slow_path,
                    size_t* n_kept, size_t* n_active, int* device);
 
+/* Forward route of the plan's fp64 apply (no reference counterpart; the
+ * reference picks its route in the constructor, fast_transform.hpp:86-133):
+ * *nfst = 1 when forward() runs the NFST fast route (the reference's own
+ * algorithm, nfst.cu), 0 for an exact route; *probe_gap = max-norm relative
+ * gap between the NFST and exact routes on the creation probe (0 when the
+ * NFST route is unavailable for the plan). */
+int dctp_plan_route(const dctp_plan* plan, int* nfst, double* probe_gap);
+
 /* Host copies of the setup vectors, n doubles each (any pointer may be NULL):
  * lambda(), mu(), the deflated z, per-slot normalisers a, per-slot signs sigma
  * (factorization(), cauchy.hpp:111-119). */

@@ -112,6 +112,12 @@ class DctPlusPlan {
     const RankOneUpdate& update() const { return update_; }
     bool slow_path() const { return slow_; }
     int device() const { return device_; }
+    /// true when the fp64 forward runs the NFST fast route (dctp_plan_route).
+    bool nfst_route() const {
+        int f = 0;
+        detail::check(dctp_plan_route(h_.get(), &f, nullptr));
+        return f != 0;
+    }
     std::vector<double> lambda() const { return setup_vector(0); }
     std::vector<double> mu() const { return setup_vector(1); }
 

@@ -346,6 +346,16 @@ struct dctp_plan {
         std::size_t wt32 = 0;                    // fp32 forward: W^T rounded, the SGEMM's B (L x ldwt)
         TwiddleOffsets tw64, tw32;
     } fd;
+    // NFST fast route (fp64): the reference's own forward algorithm on the GPU
+    struct {
+        bool on = false;
+        std::size_t hz = 0, ez = 0, inv_phi = 0, tw2n = 0, rot = 0, slot = 0, lo = 0, p0 = 0, b = 0, ca = 0, cb = 0,
+                    ctab = 0;
+        double z0 = 0.0, ext_scale = 0.0;
+        int R = 0, taps = 0, ext_slot = -1;
+        bool preferred = false;  // chosen at creation (decide_fast_route)
+        double probe_gap = 0.0;  // NFST vs exact on the creation probe (max-norm relative)
+    } fs;
     // materialised basis for the dense routes (forward_nmvp, inverse(fast =
     // false)): X^T then X, n x ld doubles each; built on first use
     struct Dense {
@@ -573,6 +583,160 @@ static void build_fold(dctp_plan& p, Blob& blob, const ApplyTables& t) {
     f.on = true;
 }
 
+/// FFTW-friendly grid length of the NFST (nfst.hpp:20-27): the smallest
+/// 5-smooth multiple of 4 >= target.
+static std::size_t next_fast_fft_size(std::size_t target) {
+    for (std::size_t g = (target + 3) / 4 * 4;; g += 4) {
+        std::size_t r = g;
+        for (std::size_t f : {2, 3, 5})
+            while (r % f == 0) r /= f;
+        if (r == 1) return g;
+    }
+}
+
+/// Constants of the NFST fast route: the reference's forward algorithm
+/// (fast_transform.hpp:94-133 slot classification, exterior row, theta,
+/// 1/sin(n theta), 1/nu, h weights; nfst.hpp:108-150 halfwidth, grid, tau,
+/// 1/phi_hat, tap windows) computed here in double with the same formulas.
+/// Only where the reference itself runs the NFST: no near-pole guard trip,
+/// interior roots present and m |theta| above the reference's dense-sine
+/// cutoff (nfst.hpp:111, kDenseWorkCutoff = 4096); power-of-two n so the
+/// grid is 4n.  The tap weights exp(-(theta - (lo + t) h)^2 / 4 tau) are
+/// factored as P0 B^t C_t (fast Gaussian gridding): equal up to rounding.
+static void build_fast(dctp_plan& p, Blob& blob) {
+    const auto& st = p.st;
+    const std::size_t n = st.n;
+    if (st.slow_path || n < 128 || (n & (n - 1)) != 0) return;
+    const double pi = std::numbers::pi;
+    const std::size_t na = st.sub_mu.size();
+    const std::size_t ext_rank = (na == 0) ? 0 : (st.rho > 0.0 ? na - 1 : 0);
+    std::vector<int> slot;
+    std::vector<double> theta, isn, inu, scale, ez;
+    int ext_slot = -1;
+    double ext_scale = 0.0;
+    for (std::size_t s = 0; s < st.slots.size(); ++s) {
+        const auto& sl = st.slots[s];
+        if (sl.passthrough) continue;
+        const double nu = st.sub_mu[sl.idx];
+        const double sc = -st.sigma[s] * st.a[s];
+        if (na > 0 && sl.idx == ext_rank) {
+            ext_slot = static_cast<int>(s);
+            ext_scale = sc;
+            ez.resize(n);
+            for (std::size_t j = 0; j < n; ++j) ez[j] = (1.0 / (nu - st.lambda[j])) * st.z[j];
+        } else {
+            const double th = std::acos(1.0 - nu / 2.0);
+            slot.push_back(static_cast<int>(s));
+            theta.push_back(th);
+            isn.push_back(1.0 / std::sin(static_cast<double>(n) * th));
+            inu.push_back(1.0 / nu);
+            scale.push_back(sc);
+        }
+    }
+    const std::size_t m = n - 1, R = theta.size();
+    if (R == 0 || m * R <= 4096) return; // the reference evaluates the exact sine matrix
+    std::size_t hw = static_cast<std::size_t>(std::ceil(1.15 * std::log10(1.0 / st.epsilon))) + 3;
+    hw = std::max<std::size_t>(hw, 2);
+    const std::size_t grid = next_fast_fft_size(4 * (m + 1));
+    const std::size_t taps = std::min(2 * hw + 1, grid);
+    if (grid != 4 * n || taps == grid || !dctp::dev::nfst_supported(n, static_cast<int>(taps))) return;
+    const double logical = 2.0 * static_cast<double>(m + 1);
+    const double over = static_cast<double>(grid) / logical;
+    const double tau = pi * static_cast<double>(hw) / (logical * logical * over * (over - 0.5));
+    const double h = 2.0 * pi / static_cast<double>(grid);
+    const double norm = static_cast<double>(grid) * std::sqrt(tau / pi);
+    std::vector<double> inv_phi(n, 0.0), hz(n, 0.0), ctab(taps), tw2n(2 * n), rot(2 * (n / 2 + 1));
+    for (std::size_t k = 1; k <= m; ++k)
+        inv_phi[k] = std::exp(static_cast<double>(k) * static_cast<double>(k) * tau) / norm;
+    for (std::size_t j = 1; j < n; ++j)
+        hz[j] = (((j % 2) == 1 ? 1.0 : -1.0) / std::sin(static_cast<double>(j) * pi / static_cast<double>(n))) * st.z[j];
+    for (std::size_t t = 0; t < taps; ++t) {
+        const double d = (static_cast<double>(t) - static_cast<double>(hw)) * h;
+        ctab[t] = std::exp(-d * d / (4.0 * tau));
+    }
+    std::vector<int> lo(R);
+    std::vector<double> p0(R), bb(R), ca(R), cb(R);
+    for (std::size_t r = 0; r < R; ++r) {
+        const long ell0 = std::lround(theta[r] / h);
+        const double dc = theta[r] - static_cast<double>(ell0) * h;
+        lo[r] = static_cast<int>(ell0 - static_cast<long>(hw));
+        p0[r] = std::exp(-dc * dc / (4.0 * tau) - static_cast<double>(hw) * dc * h / (2.0 * tau));
+        bb[r] = std::exp(dc * h / (2.0 * tau));
+        ca[r] = -0.25 * scale[r] * isn[r];
+        cb[r] = scale[r] * inu[r];
+    }
+    for (std::size_t k = 0; k < n; ++k) {
+        const double a = pi * static_cast<double>(k) / static_cast<double>(n);
+        tw2n[2 * k] = std::cos(a);
+        tw2n[2 * k + 1] = -std::sin(a);
+    }
+    for (std::size_t k = 0; k <= n / 2; ++k) {
+        const double a = pi * static_cast<double>(k) / (2.0 * static_cast<double>(n));
+        rot[2 * k] = std::cos(a);
+        rot[2 * k + 1] = -std::sin(a);
+    }
+    auto& f = p.fs;
+    f.hz = blob.add(hz);
+    f.ez = blob.add(ez);
+    f.inv_phi = blob.add(inv_phi);
+    f.tw2n = blob.add(tw2n);
+    f.rot = blob.add(rot);
+    f.slot = blob.add(slot);
+    f.lo = blob.add(lo);
+    f.p0 = blob.add(p0);
+    f.b = blob.add(bb);
+    f.ca = blob.add(ca);
+    f.cb = blob.add(cb);
+    f.ctab = blob.add(ctab);
+    f.z0 = st.z[0];
+    f.ext_scale = ext_scale;
+    f.ext_slot = ext_slot;
+    f.R = static_cast<int>(R);
+    f.taps = static_cast<int>(taps);
+    f.on = true;
+}
+
+static dctp::dev::FastPlanDev fast_plan_dev(const dctp_plan* p) {
+    const auto& f = p->fs;
+    dctp::dev::FastPlanDev d{};
+    d.hz = at<double>(p->blob, f.hz);
+    d.ez = f.ext_slot >= 0 ? at<double>(p->blob, f.ez) : nullptr;
+    d.inv_phi = at<double>(p->blob, f.inv_phi);
+    d.tw2n = at<double>(p->blob, f.tw2n);
+    d.rot = at<double>(p->blob, f.rot);
+    d.pass_slot = at<int>(p->blob, p->pass_slot);
+    d.pass_src = at<int>(p->blob, p->pass_src);
+    d.pass_sign = at<double>(p->blob, p->pass_sign64);
+    d.t_slot = at<int>(p->blob, f.slot);
+    d.t_lo = at<int>(p->blob, f.lo);
+    d.t_p0 = at<double>(p->blob, f.p0);
+    d.t_b = at<double>(p->blob, f.b);
+    d.t_ca = at<double>(p->blob, f.ca);
+    d.t_cb = at<double>(p->blob, f.cb);
+    d.ctab = at<double>(p->blob, f.ctab);
+    d.z0 = f.z0;
+    d.ext_scale = f.ext_scale;
+    d.n = static_cast<int>(p->st.n);
+    d.logn = 0;
+    while ((std::size_t{1} << d.logn) < p->st.n) ++d.logn;
+    d.R = f.R;
+    d.taps = f.taps;
+    d.n_pass = p->n_pass;
+    d.ext_slot = f.ext_slot;
+    return d;
+}
+
+/// The NFST fast route serves fp64 plans where the reference runs its own
+/// NFST; whether it is the plan's forward route is decided at creation
+/// (decide_fast_route).  DCTP_FAST=0 / 1 forces it off / on (where available).
+static bool fast_route(const dctp_plan* p) {
+    if (!p->fs.on) return false;
+    const char* e = std::getenv("DCTP_FAST");
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return true;
+    return p->fs.preferred;
+}
+
 /// Development knob for profiling the fused kernel's phases in isolation
 /// (DCTP_DEBUG_MODE bits: 1 = DCT work skipped, 2 = DMMA work skipped, 4 = producer
 /// phase timers); 0 otherwise.
@@ -627,6 +791,7 @@ static void upload_plan(dctp_plan& p) {
     p.kept = kept_idx;
     build_small(p, blob, t);
     build_fold(p, blob, t);
+    build_fast(p, blob);
     p.pass_sign64 = blob.add(t.pass_sign);
     p.pass_sign32 = blob.add(to_f32(t.pass_sign));
     p.n_pass = static_cast<int>(t.pass_slot.size());
@@ -675,6 +840,10 @@ static dctp::host::Update make_update(int kind, std::size_t i, std::size_t j, do
     }
 }
 
+template <class T>
+static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s);
+static void decide_fast_route(dctp_plan& p);
+
 static std::unique_ptr<dctp_plan> build_plan(std::size_t n, const dctp::host::Update& u, double eps, double tau,
                                              int device) {
     auto p = std::make_unique<dctp_plan>();
@@ -685,6 +854,7 @@ static std::unique_ptr<dctp_plan> build_plan(std::size_t n, const dctp::host::Up
     DeviceScope scope(device);
     prepare_pool(device);
     upload_plan(*p);
+    decide_fast_route(*p);
     return p;
 }
 
@@ -733,6 +903,11 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
     const std::size_t n = p->st.n;
     DeviceScope scope(p->device);
     if constexpr (std::is_same_v<T, double>) {
+        if (fast_route(p)) {
+            cuda_check(DCTP_LAUNCH("nfst_fwd", s, dctp::dev::nfst_forward(in, out, batch, fast_plan_dev(p), p->flag, s)),
+                       "nfst forward kernel");
+            return;
+        }
         // TMA bulk copies need 16-byte aligned rows; a misaligned view takes
         // the generic (DCT + Cauchy kernel) route instead
         const bool aligned = (reinterpret_cast<std::uintptr_t>(in) | reinterpret_cast<std::uintptr_t>(out)) % 16 == 0;
@@ -836,6 +1011,48 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
                            dctp::dev::idct_rows<T>(d.ptr, n, in, n, p->emit_inv<T>(), out, n, n, batch, p->tw<T>(),
                                                    p->flag, s)),
                "idct kernel");
+}
+
+/// Route choice for plans the NFST route can serve (fp64 forward), by
+/// measurement on the plan itself: 16 seeded N(0,1) probe signals go through
+/// the NFST route and through the exact route the plan would take otherwise.
+/// The reference's forward() IS the NFST approximation, so where the two
+/// differ by more than 1e-11 (a tenth of the fp64 parity tolerance: at n =
+/// 1024, self-loop 0.5, they differ by 5e-9) the NFST route is the only one
+/// that reproduces the reference and is kept.  Otherwise the faster one is:
+/// the NFST route from DCTP_FAST_MIN_N (default 2048; tools/route_sweep.py:
+/// 1.66 vs 2.11 ms at n = 2048, 1.27 vs 1.08 ms at n = 1024).
+static void decide_fast_route(dctp_plan& p) {
+    if (!p.fs.on) return;
+    static const std::size_t min_n = [] {
+        const char* m = std::getenv("DCTP_FAST_MIN_N");
+        return m ? static_cast<std::size_t>(std::atoll(m)) : std::size_t{2048};
+    }();
+    const std::size_t n = p.st.n, rows = 16;
+    std::vector<double> h(rows * n), a(rows * n), b(rows * n);
+    dctp::host::fill_signals(dctp::host::mix_seed(2409, n, 77), dctp::host::Dist::gaussian, 0.0, n, rows, h.data());
+    double* d = nullptr;
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&d), 3 * rows * n * sizeof(double)), "cudaMalloc(route probe)");
+    std::unique_ptr<double, decltype(&cudaFree)> hold(d, &cudaFree);
+    cuda_check(cudaMemcpy(d, h.data(), rows * n * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy(route probe)");
+    p.fs.preferred = true;
+    plan_forward<double>(&p, d, d + rows * n, rows, nullptr);
+    p.fs.preferred = false;
+    plan_forward<double>(&p, d, d + 2 * rows * n, rows, nullptr);
+    cuda_check(cudaMemcpy(a.data(), d + rows * n, rows * n * sizeof(double), cudaMemcpyDeviceToHost), "route probe");
+    cuda_check(cudaMemcpy(b.data(), d + 2 * rows * n, rows * n * sizeof(double), cudaMemcpyDeviceToHost),
+               "route probe");
+    double gap = 0.0;
+    for (std::size_t r = 0; r < rows; ++r) {
+        double num = 0.0, den = 0.0;
+        for (std::size_t k = 0; k < n; ++k) {
+            num = std::max(num, std::abs(a[r * n + k] - b[r * n + k]));
+            den = std::max(den, std::abs(b[r * n + k]));
+        }
+        gap = std::max(gap, den > 0.0 ? num / den : num);
+    }
+    p.fs.probe_gap = gap;
+    p.fs.preferred = !(gap <= 1e-11) || n >= min_n;
 }
 
 static void sync_check(int device, int* flag, cudaStream_t s) {
@@ -1209,6 +1426,14 @@ int dctp_plan_info(const dctp_plan* p, size_t* n, double* epsilon, int* slow_pat
         if (n_kept) *n_kept = p->st.kept.size();
         if (n_active) *n_active = p->st.sub_mu.size();
         if (device) *device = p->device;
+    });
+}
+
+int dctp_plan_route(const dctp_plan* p, int* nfst, double* probe_gap) {
+    return guarded([&] {
+        if (!p) throw std::invalid_argument("dctp_plan_route: null plan");
+        if (nfst) *nfst = fast_route(p) ? 1 : 0;
+        if (probe_gap) *probe_gap = p->fs.probe_gap;
     });
 }
 

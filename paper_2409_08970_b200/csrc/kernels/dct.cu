@@ -14,6 +14,7 @@
 #include <cmath>
 
 #include "kernels/common.cuh"
+#include "kernels/fft_smem.cuh"
 #include "kernels/launch.hpp"
 
 namespace dctp::dev {
@@ -21,78 +22,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kTileElems = 2048; // signal samples staged per CTA
-
-/// Shared-memory layout of the FFT rows: one complex of padding after every
-/// 8, so the strided groups of every pass (including the bit-reversed gather
-/// of the first one) hit 8 distinct 16-byte bank groups per quarter-warp.
-__device__ __forceinline__ int pad8(int i) { return i + (i >> 3); }
-__host__ __device__ constexpr int padded_len(int N) { return N + (N >> 3) + 1; }
-
-/// Q consecutive radix-2 DIT stages (s0+1 .. s0+Q) fused into one pass over
-/// groups of 2^Q elements held in registers: group (block, j) holds elements
-/// block*2^(s0+Q) + j + m*2^s0, m < 2^Q, of the bit-reversed sequence.  One
-/// shared-memory round trip and one barrier per Q stages instead of per stage.
-/// The first pass (FIRST, s0 = 0) gathers its inputs from the natural-order
-/// buffer `src` at the bit-reversed positions and writes `dst`, so no
-/// bit-reversed scatter is ever stored.
-template <class T, bool Inverse, int Q, bool FIRST>
-__device__ __forceinline__ void dit_group_pass(const cplx_t<T>* src, cplx_t<T>* dst, int rows, int N, int logN,
-                                               int s0, const T* __restrict__ tw) {
-    constexpr int G = 1 << Q;
-    const int h0 = 1 << s0;
-    const int groups = N >> Q;
-    const int ld = padded_len(N);
-    for (int t = threadIdx.x; t < rows * groups; t += blockDim.x) {
-        const int row = t / groups, g = t - row * groups;
-        const int j = g & (h0 - 1), base = (g >> s0) * (h0 << Q) + j;
-        cplx_t<T> v[G];
-#pragma unroll
-        for (int m = 0; m < G; ++m)
-            v[m] = FIRST ? src[row * ld + pad8(static_cast<int>(bit_reverse(static_cast<unsigned>(base + m), logN)))]
-                         : dst[row * ld + pad8(base + m * h0)];
-#pragma unroll
-        for (int tt = 0; tt < Q; ++tt) {
-            const int span = 1 << tt;
-            const int shift = logN - (s0 + tt + 1); // twiddle step N / (2 * half)
-#pragma unroll
-            for (int m = 0; m < G; ++m) {
-                if (m & span) continue;
-                const int widx = (j + (m & (span - 1)) * h0) << shift;
-                const cplx_t<T> w = __ldg(reinterpret_cast<const cplx_t<T>*>(tw) + widx); // one 16/8-byte load
-                const T wr = w.x, wi = Inverse ? -w.y : w.y;
-                const cplx_t<T> a = v[m], b = v[m + span];
-                const T br = b.x * wr - b.y * wi, bi = b.x * wi + b.y * wr;
-                v[m] = {a.x + br, a.y + bi};
-                v[m + span] = {a.x - br, a.y - bi};
-            }
-        }
-#pragma unroll
-        for (int m = 0; m < G; ++m) dst[row * ld + pad8(base + m * h0)] = v[m];
-    }
-    __syncthreads();
-}
-
-/// FFT of `rows` rows of N = 2^logN points given in natural order in `src`
-/// (padded rows), result in natural order in `dst`: a bit-reversed gather
-/// folded into the first radix-8 pass, then in-place radix-8 DIT passes
-/// (radix-4/2 for the remainder).  `src` is dead afterwards.
-template <class T, bool Inverse>
-__device__ __forceinline__ void fft_rows(const cplx_t<T>* src, cplx_t<T>* dst, int rows, int N, int logN,
-                                         const T* __restrict__ tw) {
-    if (logN == 0) {
-        for (int r = threadIdx.x; r < rows; r += blockDim.x) dst[r * padded_len(N)] = src[r * padded_len(N)];
-        __syncthreads();
-        return;
-    }
-    const int q0 = min(3, logN);
-    if (q0 == 3) dit_group_pass<T, Inverse, 3, true>(src, dst, rows, N, logN, 0, tw);
-    if (q0 == 2) dit_group_pass<T, Inverse, 2, true>(src, dst, rows, N, logN, 0, tw);
-    if (q0 == 1) dit_group_pass<T, Inverse, 1, true>(src, dst, rows, N, logN, 0, tw);
-    int s0 = q0;
-    for (; s0 + 3 <= logN; s0 += 3) dit_group_pass<T, Inverse, 3, false>(dst, dst, rows, N, logN, s0, tw);
-    if (logN - s0 == 2) dit_group_pass<T, Inverse, 2, false>(dst, dst, rows, N, logN, s0, tw);
-    if (logN - s0 == 1) dit_group_pass<T, Inverse, 1, false>(dst, dst, rows, N, logN, s0, tw);
-}
 
 /// Shared memory of the FFT kernels: natural buffer (later the real output
 /// rows), working buffer; both rows_per_cta x padded_len(n/2) complex.

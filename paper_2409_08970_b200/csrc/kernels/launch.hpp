@@ -147,6 +147,33 @@ cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std:
                           const int* col_map = nullptr, const int* a_map = nullptr, const T* fold_add = nullptr,
                           std::size_t ld_add = 0);
 
+/// Constants of the NFST fast route (nfst.cu), the reference's own
+/// DctPlusPlan::forward algorithm (fast_transform.hpp:94-133, 163-190;
+/// nfst.hpp:100-164, 201-238) built on the host in double like the reference.
+struct FastPlanDev {
+    const double* hz;        // n: h_j z_j, h_j = (-1)^(j+1) / sin(j pi / n) (j >= 1)
+    const double* ez;        // n: ext_row_j z_j (exterior slot), or nullptr
+    const double* inv_phi;   // n: 1 / phi_hat(k) of the Gaussian kernel, [0] = 0
+    const double* tw2n;      // n complex: e^{-2 pi i k / 2n}, k < n
+    const double* rot;       // n/2 + 1 complex: e^{-i pi k / 2n}
+    const int* pass_slot;    // n_pass
+    const int* pass_src;     // n_pass
+    const double* pass_sign; // n_pass
+    const int* t_slot;       // R interior targets: output slot
+    const int* t_lo;         // first grid point of the tap window (may be < 0)
+    const double* t_p0;      // weight of tap 0
+    const double* t_b;       // weight ratio of consecutive taps (w_t = P0 B^t C_t)
+    const double* t_ca;      // -scale / (4 sin(n theta))
+    const double* t_cb;      // scale / nu
+    const double* ctab;      // taps: exp(-((t - halfwidth) h)^2 / 4 tau)
+    double z0, ext_scale;
+    int n, logn, R, taps, n_pass, ext_slot; // ext_slot < 0: no exterior row
+};
+
+bool nfst_supported(std::size_t n, int taps);
+cudaError_t nfst_forward(const double* in, double* out, std::size_t batch, const FastPlanDev& P, int* flag,
+                         cudaStream_t stream);
+
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);
 cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,

@@ -1,0 +1,278 @@
+// The reference's fast route on the GPU (fp64): DCT-II, DST-I, a
+// nonuniform fast sine transform (NFST) by Gaussian gridding, and the
+// secular-row epilogue, for one signal per CTA entirely in shared memory.
+//
+// Reference: DctPlusPlan::forward (proj/include/dctplus/fast_transform.hpp:
+// 163-190) with NfstPlan::exec_into (nfst.hpp:201-238).  Per signal:
+//   shat = DCT-II(s); sv = z .* shat; out[pass] = sigma shat[src];
+//   out[ext] = scale_ext * <ext_row, sv>;
+//   h_j = w_j sv_j,  w_j = (-1)^(j+1) / sin(j pi / n)          (j = 1..n-1)
+//   c = DST-I(h);  v_k = c_k / phi_hat(k)                      (deconvolution)
+//   y_l = Im g_l = 2 sum_k v_k sin(pi k l / 2n)                (grid G = 4n)
+//   phi_r = 1/2 sum_t w_rt y_{lo_r + t}                        (35 taps)
+//   out[slot_r] = scale_r (-phi_r / (2 sin(n theta_r)) + sv_0 / nu_r).
+// The grid transform is split by the parity of l: y_{2k} = DST-I(v)_k and
+// y_{2k+1} = (-1)^k DCT-III(v reversed)_k, so every FFT has length <= n and
+// the row fits in shared memory up to n = 8192 (in-place FFTs, 209 KB).
+// The Gaussian weights are w_rt = P0_r B_r^t C_t (fast Gaussian gridding):
+// two per-target constants and one shared 35-entry table instead of the
+// reference's 35 weights per target.
+#include <algorithm>
+
+#include "kernels/common.cuh"
+#include "kernels/fft_smem.cuh"
+#include "kernels/launch.hpp"
+
+namespace dctp::dev {
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+/// Block-wide sum; `red` holds >= 33 doubles.  Every thread gets the total.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        double t = lane < static_cast<int>(blockDim.x >> 5) ? red[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) red[32] = t;
+    }
+    __syncthreads();
+    return red[32];
+}
+
+/// The odd extension e (length 2n) of h_1..h_{n-1} packed as z_j = e_{2j} +
+/// i e_{2j+1} (j < n): its n-point FFT gives DST-I(h) in dst1_pair below.
+__device__ __forceinline__ double odd_ext(const double* h, const double* wgt, int i, int n) {
+    if (i == 0 || i == n) return 0.0;
+    if (i < n) return wgt ? wgt[i] * h[i] : h[i];
+    const int k = 2 * n - i;
+    return -(wgt ? wgt[k] * h[k] : h[k]);
+}
+
+__device__ __forceinline__ void pack_dst1(double2* cb, const double* h, const double* __restrict__ wgt, int n) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+        cb[pad8(j)] = make_double2(odd_ext(h, wgt, 2 * j, n), odd_ext(h, wgt, 2 * j + 1, n));
+}
+
+/// c_k and c_{n-k} of DST-I (c_k = 2 sum_j h_j sin(pi j k / n)) from the
+/// n-point FFT Z of the packed odd extension: E_k = Ev_k + W^k Od_k with
+/// Ev = (Z_k + conj Z_{n-k}) / 2, Od = (Z_k - conj Z_{n-k}) / 2i, W = e^{-i pi/n},
+/// and E_k = -i c_k.
+__device__ __forceinline__ void dst1_pair(double2 a, double2 b, double2 w, double& ck, double& cnk) {
+    // k: A = Z_k, B = Z_{n-k}
+    const double ev_y = 0.5 * (a.y - b.y);
+    const double od_x = 0.5 * (a.y + b.y), od_y = -0.5 * (a.x - b.x);
+    ck = -(ev_y + w.x * od_y + w.y * od_x);
+    // n-k: roles swapped, W^{n-k} = (-w.x, w.y)
+    const double ev2_y = 0.5 * (b.y - a.y);
+    const double od2_x = 0.5 * (b.y + a.y), od2_y = -0.5 * (b.x - a.x);
+    cnk = -(ev2_y - w.x * od2_y + w.y * od2_x);
+}
+
+/// DST-I of the packed row in cb (after its FFT) into dst[1..n-1] (dst[0] = 0),
+/// optionally multiplied by mul[k].
+__device__ __forceinline__ void unpack_dst1(const double2* cb, const double* __restrict__ tw2n,
+                                            const double* __restrict__ mul, double* dst, int n) {
+    const int N = n >> 1;
+    for (int k = threadIdx.x; k <= N; k += blockDim.x) {
+        if (k == 0) {
+            dst[0] = 0.0;
+            continue;
+        }
+        const double2 w = __ldg(reinterpret_cast<const double2*>(tw2n) + k);
+        double ck, cnk;
+        dst1_pair(cb[pad8(k)], cb[pad8(n - k)], w, ck, cnk);
+        dst[k] = mul ? ck * __ldg(mul + k) : ck;
+        if (k != N) dst[n - k] = mul ? cnk * __ldg(mul + n - k) : cnk;
+    }
+}
+
+__global__ void __launch_bounds__(512)
+nfst_forward_kernel(const double* __restrict__ in, double* __restrict__ out, FastPlanDev P, int* flag) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int n = P.n, logn = P.logn, N = n >> 1;
+    double2* cb = reinterpret_cast<double2*>(smem_raw); // FFT row, padded_len(n) complex
+    double* rb = reinterpret_cast<double*>(cb + padded_len(n)); // n reals: shat, then v, then y_even
+    double* ctab = rb + n;                              // taps
+    double* red = ctab + P.taps;                        // 33
+    double* yo = reinterpret_cast<double*>(cb + padded_len(N)); // y_odd, beside the n/2-point FFT
+    const std::size_t b = blockIdx.x;
+    const double* x = in + b * n;
+    double* o = out + b * n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+
+    for (int t = tid; t < P.taps; t += nt) ctab[t] = __ldg(P.ctab + t);
+
+    // 1. DCT-II (Makhoul): v = (x0, x2, ..., x3, x1) packed as w_m = v_2m + i v_2m+1
+    bool bad = false;
+    for (int j = tid; j < n; j += nt) {
+        const double v = x[j];
+        bad |= !isfinite(v);
+        const int p = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
+        reinterpret_cast<double*>(&cb[pad8(p >> 1)])[p & 1] = v;
+    }
+    if (bad) atomicOr(flag, 1);
+    __syncthreads();
+    fft_inplace<double, false>(cb, N, logn - 1, P.tw2n, 2);
+    {
+        const double scale = sqrt(2.0 / n), dc_scale = 1.0 / sqrt(static_cast<double>(n));
+        const double2* tw = reinterpret_cast<const double2*>(P.tw2n);
+        const double2* rot = reinterpret_cast<const double2*>(P.rot);
+        for (int k = tid; k < N; k += nt) {
+            if (k == 0) {
+                const double2 w0 = cb[0];
+                rb[0] = (w0.x + w0.y) * dc_scale;
+                rb[N] = (w0.x - w0.y) * __ldg(&rot[N].x) * scale;
+                continue;
+            }
+            const double2 wk = cb[pad8(k)], wc = cb[pad8(N - k)];
+            const double er = 0.5 * (wk.x + wc.x), ei = 0.5 * (wk.y - wc.y);
+            const double orr = 0.5 * (wk.x - wc.x), oi = 0.5 * (wk.y + wc.y);
+            const double2 sp = __ldg(tw + 2 * k); // e^{-2 pi i k / n}
+            const double qr = sp.x * orr - sp.y * oi, qi = sp.x * oi + sp.y * orr;
+            const double vr = er + qi, vi = ei - qr;
+            const double2 rt = __ldg(rot + k);
+            rb[k] = (vr * rt.x - vi * rt.y) * scale;
+            rb[n - k] = -(vr * rt.y + vi * rt.x) * scale;
+        }
+    }
+    __syncthreads();
+
+    // 2. pass-through slots, the exterior row, sv_0; h = w .* z .* shat packed for DST-I
+    for (int e = tid; e < P.n_pass; e += nt) o[__ldg(P.pass_slot + e)] = __ldg(P.pass_sign + e) * rb[__ldg(P.pass_src + e)];
+    const double sv0 = P.z0 * rb[0];
+    double ext = 0.0;
+    if (P.ext_slot >= 0)
+        for (int j = tid; j < n; j += nt) ext += __ldg(P.ez + j) * rb[j];
+    pack_dst1(cb, rb, P.hz, n);
+    if (P.ext_slot >= 0) {
+        ext = block_sum(ext, red); // includes the barrier before the FFT
+        if (tid == 0) o[P.ext_slot] = P.ext_scale * ext;
+    } else {
+        __syncthreads();
+    }
+
+    // 3. c = DST-I(h); v = c / phi_hat
+    fft_inplace<double, false>(cb, n, logn, P.tw2n, 1);
+    unpack_dst1(cb, P.tw2n, P.inv_phi, rb, n);
+    __syncthreads();
+
+    // 4. odd grid points: y_{2k+1} = (-1)^k core DCT-III of X, X_0 = 0, X_m = 2 v_{n-m}
+    {
+        const double2* tw = reinterpret_cast<const double2*>(P.tw2n);
+        const double2* rot = reinterpret_cast<const double2*>(P.rot);
+        const double r2 = 0.70710678118654752440;
+        for (int k = tid; k < N; k += nt) {
+            const double2 rt = __ldg(rot + k);
+            const double cr = rt.x, ci = -rt.y; // e^{+i pi k / 2n}
+            const double ar = (k == 0) ? 0.0 : 2.0 * rb[n - k];
+            const double ai = (k == 0) ? 0.0 : -2.0 * rb[k];
+            const double v1r = ar * cr - ai * ci, v1i = ar * ci + ai * cr;
+            const double c2r = r2 * (cr - ci), c2i = r2 * (cr + ci);
+            const double br = 2.0 * rb[N - k], bi = -2.0 * rb[N + k];
+            const double v2r = br * c2r - bi * c2i, v2i = br * c2i + bi * c2r;
+            const double2 sp = __ldg(tw + 2 * k);
+            const double sr = sp.x, si = -sp.y; // e^{+2 pi i k / n}
+            const double dr = v1r - v2r, di = v1i - v2i;
+            const double qr = sr * dr - si * di, qi = sr * di + si * dr;
+            cb[pad8(k)] = make_double2(0.5 * (v1r + v2r - qi), 0.5 * (v1i + v2i + qr));
+        }
+    }
+    __syncthreads();
+    fft_inplace<double, true>(cb, N, logn - 1, P.tw2n, 2);
+    for (int j = tid; j < n; j += nt) {
+        const int p = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
+        const double2 w = cb[pad8(p >> 1)];
+        const double v = (p & 1) ? w.y : w.x;
+        yo[j] = (j & 1) ? -v : v;
+    }
+    __syncthreads();
+
+    // 5. gather the odd taps of every interior target; the partial sum parks
+    //    in the target's own output slot (same thread reads it back in 7)
+    const int two_n = 2 * n, four_n = 4 * n;
+    for (int r = tid; r < P.R; r += nt) {
+        const int lo = __ldg(P.t_lo + r);
+        const double B = __ldg(P.t_b + r), B2 = B * B;
+        const int t0 = (lo & 1) ? 0 : 1;
+        double pw = __ldg(P.t_p0 + r) * (t0 ? B : 1.0);
+        double a = 0.0;
+        for (int t = t0; t < P.taps; t += 2, pw *= B2) {
+            int l = lo + t;
+            double sg = pw * ctab[t];
+            if (l < 0) {
+                l = -l;
+                sg = -sg;
+            } else if (l > two_n) {
+                l = four_n - l;
+                sg = -sg;
+            }
+            a += sg * yo[(l - 1) >> 1];
+        }
+        o[__ldg(P.t_slot + r)] = a;
+    }
+    __syncthreads();
+
+    // 6. even grid points: y_{2k} = DST-I(v)_k
+    pack_dst1(cb, rb, nullptr, n);
+    __syncthreads();
+    fft_inplace<double, false>(cb, n, logn, P.tw2n, 1);
+    unpack_dst1(cb, P.tw2n, nullptr, rb, n);
+    __syncthreads();
+
+    // 7. even taps, then the secular-row epilogue
+    for (int r = tid; r < P.R; r += nt) {
+        const int lo = __ldg(P.t_lo + r);
+        const double B = __ldg(P.t_b + r), B2 = B * B;
+        const int t0 = (lo & 1) ? 1 : 0;
+        double pw = __ldg(P.t_p0 + r) * (t0 ? B : 1.0);
+        const int slot = __ldg(P.t_slot + r);
+        double a = o[slot];
+        for (int t = t0; t < P.taps; t += 2, pw *= B2) {
+            int l = lo + t;
+            double sg = pw * ctab[t];
+            if (l < 0) {
+                l = -l;
+                sg = -sg;
+            } else if (l > two_n) {
+                l = four_n - l;
+                sg = -sg;
+            }
+            if (l != 0 && l != two_n) a += sg * rb[l >> 1];
+        }
+        o[slot] = __ldg(P.t_ca + r) * a + __ldg(P.t_cb + r) * sv0;
+    }
+}
+
+int nfst_threads(int n) { return std::min(512, std::max(128, n / 16)); }
+
+std::size_t nfst_smem_bytes(int n, int taps) {
+    return static_cast<std::size_t>(padded_len(n)) * sizeof(double2) + (n + taps + 40) * sizeof(double);
+}
+
+} // namespace
+
+bool nfst_supported(std::size_t n, int taps) {
+    return is_pow2(n) && n >= 128 && n <= 8192 && nfst_smem_bytes(static_cast<int>(n), taps) <= 227 * 1024;
+}
+
+cudaError_t nfst_forward(const double* in, double* out, std::size_t batch, const FastPlanDev& P, int* flag,
+                         cudaStream_t stream) {
+    if (batch == 0) return cudaSuccess;
+    if (!nfst_supported(P.n, P.taps)) return cudaErrorInvalidValue;
+    const std::size_t smem = nfst_smem_bytes(P.n, P.taps);
+    cudaError_t e = cudaFuncSetAttribute(nfst_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    nfst_forward_kernel<<<static_cast<unsigned>(batch), nfst_threads(P.n), smem, stream>>>(in, out, P, flag);
+    return cudaGetLastError();
+}
+
+} // namespace dctp::dev

@@ -179,6 +179,13 @@ class DctPlusPlan:
     def slow_path(self) -> bool:
         return self._slow
 
+    def route(self) -> dict:
+        """fp64 forward route: {"nfst": bool, "probe_gap": float} (dctp_plan_route)."""
+        f = C.c_int()
+        g = C.c_double()
+        check(lib.dctp_plan_route(self._h, C.byref(f), C.byref(g)))
+        return {"nfst": bool(f.value), "probe_gap": g.value}
+
     def _setup(self):
         n = self._n
         out = {k: np.empty(n) for k in ("lambda", "mu", "z", "a", "sigma")}

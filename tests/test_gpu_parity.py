@@ -212,9 +212,12 @@ def test_host_entry_points_match_device(P, torch, restatement):
 
 @pytest.mark.parametrize("n", [16, 32, 64, 128, 256, 512])
 @pytest.mark.parametrize("kind", ["self_loop", "edge", "edge_center", "neg"])
-def test_small_plans_fused_path_against_restatement(P, torch, restatement, n, kind):
+def test_small_plans_fused_path_against_restatement(P, torch, restatement, monkeypatch, n, kind):
     """The fused persistent kernel (pow2 n <= 512, <= 128 kept / active) on
-    ragged batches, deflating and non-deflating updates, rho of both signs."""
+    ragged batches, deflating and non-deflating updates, rho of both signs.
+    Exact routes only (DCTP_FAST=0): some of these plans take the NFST route
+    by default (their reference forward() is 1e-10 from exact)."""
+    monkeypatch.setenv("DCTP_FAST", "0")
     u = {"self_loop": P.RankOneUpdate.self_loop(3, 0.8),
          "edge": P.RankOneUpdate.edge_delta(2, n // 2 + 1, 1.3),
          "edge_center": P.RankOneUpdate.edge_delta(n // 2, n // 2 + 1, -0.7),
@@ -547,6 +550,7 @@ def test_dense_route_selected_for_full_updates(P, torch, reference, monkeypatch,
     Pinned against the reference's dense routes: its NFST fast route carries
     its own approximation error (1.2e-9 at n = 384 here, above the fp64
     tolerance), which every route of this library (all exact) does not."""
+    monkeypatch.setenv("DCTP_FAST", "0")  # the exact routes (the NFST route has its own test)
     s = np.random.default_rng(n).standard_normal((300, n))
     rp = reference.plan(n, u)
     want = rp.forward(s, nmvp=True)
@@ -578,6 +582,7 @@ def test_folded_route_for_antisymmetric_plans(P, torch, reference, monkeypatch, 
     pass-through slots); it matches the reference (exact route: C3 is a slow
     path, the others are pinned on the reference's dense route) and the
     structured route (DCTP_FOLD=0), fp64 and fp32."""
+    monkeypatch.setenv("DCTP_FAST", "0")  # the exact routes (the NFST route has its own test)
     s = np.random.default_rng(n + 1).standard_normal((333, n))
     rp = reference.plan(n, u)
     want = rp.forward(s, nmvp=True)
@@ -601,3 +606,57 @@ def test_folded_route_for_antisymmetric_plans(P, torch, reference, monkeypatch, 
             assert set(P.profile_summary()) == {"fold_dct", "fold_w", "fold_idct", "fold_wt"}
     monkeypatch.delenv("DCTP_FOLD")
     assert O.parity(got[("auto", "float64")], got[("0", "float64")]) <= 1e-12
+
+
+@pytest.mark.parametrize("n,u,mode,tol", [
+    (128, O.Update(0, 0.5, 1), "1", TOL64), (256, O.Update(1, -0.7, 128, 129), "1", TOL64),
+    (512, O.Update(0, 1.3, 1), None, TOL64), (1024, O.Update(0, 0.5, 1), None, TOL64),
+    (2048, O.Update(0, 5.0, 1), None, TOL64), (2048, O.Update(1, 2.0, 1024, 1025), None, 5e-10)])
+def test_nfst_route_matches_reference_fast_route(P, torch, reference, monkeypatch, n, u, mode, tol):
+    """The NFST fast route (nfst.cu) is the reference's own forward algorithm
+    (fast_transform.hpp:163-190, nfst.hpp:201-238), so it reproduces the
+    reference's forward() to rounding, including the NFST's approximation
+    error: at n = 1024 (self-loop 0.5) that error puts the reference 5e-9
+    away from the exact transform, beyond the 1e-10 tolerance the exact
+    routes are held to.  The plan picks it by itself there (creation probe:
+    NFST vs exact gap > 1e-11) and from n = 2048 on speed; DCTP_FAST=1
+    forces it below.  The last case is ill-conditioned for the reference
+    itself: its result lies 3.6e-8 from the exact transform and moves by
+    ~1e-10 with the FFT implementation (the numpy restatement of the same
+    algorithm with numpy's pocketfft differs from it by 1.1e-10 as well), so
+    its bound is the reference's own rounding noise (5e-10, i.e. 1/70 of
+    its approximation error).  fp32 keeps the exact routes."""
+    if mode is not None:
+        monkeypatch.setenv("DCTP_FAST", mode)
+    rows = 257 if n <= 1024 else 96
+    s = np.random.default_rng(n + 7).standard_normal((rows, n))
+    rp = reference.plan(n, u)
+    assert not rp.slow_path()
+    want, exact = rp.forward(s), rp.forward(s, nmvp=True)
+    plan = P.DctPlusPlan(n, upd(P, u), 1e-12)
+    assert plan.route()["nfst"]
+    if mode is None and n < 2048:
+        assert plan.route()["probe_gap"] > 1e-11
+    P.profile_reset()
+    P.profile_enable(True)
+    got = plan.forward(dev(torch, s, torch.float64)).cpu().numpy()
+    P.profile_enable(False)
+    assert set(P.profile_summary()) == {"nfst_fwd"}
+    assert O.parity(got, want) <= tol
+    assert abs(O.parity(got, exact) - O.parity(want, exact)) <= max(tol, 0.02 * O.parity(want, exact))
+    y32 = plan.forward(dev(torch, s, torch.float32)).double().cpu().numpy()
+    assert O.parity(y32, exact) <= TOL32
+    # empty batches and non-finite input follow the same contract
+    assert plan.forward(dev(torch, s[:0], torch.float64)).shape == (0, n)
+    bad = s[:3].copy()
+    bad[1, n // 3] = np.nan
+    with pytest.raises(P.DomainError):
+        plan.forward(dev(torch, bad, torch.float64))
+
+
+def test_exact_route_kept_where_nfst_gap_is_small(P, torch, reference):
+    """C2 (n = 256): the reference's NFST lies 3e-12 from the exact transform,
+    so the creation probe keeps the faster exact (fused) route."""
+    plan = plan_for(P, 2)
+    r = plan.route()
+    assert not r["nfst"] and 0.0 < r["probe_gap"] <= 1e-11

@@ -904,7 +904,7 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
     DeviceScope scope(p->device);
     if constexpr (std::is_same_v<T, double>) {
         if (fast_route(p)) {
-            cuda_check(DCTP_LAUNCH("nfst_fwd", s, dctp::dev::nfst_forward(in, out, batch, fast_plan_dev(p), p->flag, s)),
+            cuda_check(DCTP_LAUNCH("nfst_fwd", s, dctp::dev::nfst_apply(in, out, batch, fast_plan_dev(p), p->flag, false, s)),
                        "nfst forward kernel");
             return;
         }
@@ -974,6 +974,14 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
     if (!in || !out) throw std::invalid_argument("dctp_inverse: null buffer");
     if (static_cast<const void*>(in) == static_cast<const void*>(out))
         throw std::invalid_argument("dctp_inverse: in and out must not alias");
+    if constexpr (std::is_same_v<T, double>) {
+        if (fast_route(p)) {
+            DeviceScope scope(p->device);
+            cuda_check(DCTP_LAUNCH("nfst_inv", s, dctp::dev::nfst_apply(in, out, batch, fast_plan_dev(p), p->flag, true, s)),
+                       "nfst inverse kernel");
+            return;
+        }
+    }
     if (dense_route(p)) {
         plan_dense<T>(p, in, out, batch, s, true);
         return;

@@ -171,8 +171,10 @@ struct FastPlanDev {
 };
 
 bool nfst_supported(std::size_t n, int taps);
-cudaError_t nfst_forward(const double* in, double* out, std::size_t batch, const FastPlanDev& P, int* flag,
-                         cudaStream_t stream);
+/// Forward (DctPlusPlan::forward) or inverse (inverse(p, ws, fast = true))
+/// of `batch` contiguous rows of n doubles through the NFST route.
+cudaError_t nfst_apply(const double* in, double* out, std::size_t batch, const FastPlanDev& P, int* flag,
+                       bool inverse, cudaStream_t stream);
 
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);

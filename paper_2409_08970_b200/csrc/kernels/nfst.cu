@@ -251,6 +251,169 @@ nfst_forward_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
     }
 }
 
+/// Spread phi_r = -2 t_ca[r] p[slot_r] over the taps of one parity into f
+/// (reflected about 0 and 2n with a sign flip: the adjoint of the gather).
+template <bool ODD>
+__device__ __forceinline__ void spread_taps(const FastPlanDev& P, const double* prow, const double* ctab, double* f) {
+    const int two_n = 2 * P.n, four_n = 4 * P.n;
+    for (int r = threadIdx.x; r < P.R; r += blockDim.x) {
+        const int lo = __ldg(P.t_lo + r);
+        const double B = __ldg(P.t_b + r), B2 = B * B;
+        const double phi = -2.0 * __ldg(P.t_ca + r) * prow[__ldg(P.t_slot + r)];
+        const int t0 = ((lo & 1) != 0) == ODD ? 0 : 1;
+        double pw = phi * __ldg(P.t_p0 + r) * (t0 ? B : 1.0);
+        for (int t = t0; t < P.taps; t += 2, pw *= B2) {
+            int l = lo + t;
+            double v = pw * ctab[t];
+            if (l < 0) {
+                l = -l;
+                v = -v;
+            } else if (l > two_n) {
+                l = four_n - l;
+                v = -v;
+            }
+            if (ODD)
+                atomicAdd(f + ((l - 1) >> 1), v);
+            else if (l != 0 && l != two_n)
+                atomicAdd(f + (l >> 1), v);
+        }
+    }
+}
+
+/// Inverse through the adjoint NFST (DctPlusPlan::inverse(p, ws, fast = true),
+/// fast_transform.hpp:218-255 with NfstPlan::adjoint_into, nfst.hpp:248-277):
+///   phi_r = -y_r / (2 sin(n theta_r)), y_r = -scale_r p[slot_r];
+///   f = spread of phi over the grid; b_k = Im(FFT f)_k / phi_hat(k), split
+///   by parity as 1/2 DST-I(f_even)_k + DCT-II(+-f_odd)_{n-k};
+///   g = DST-I(b); d_j = z_j (ext_j + [j = 0] d0 - w_j g_j) + pass-through;
+///   s = DCT-III(d).
+__global__ void __launch_bounds__(512)
+nfst_inverse_kernel(const double* __restrict__ in, double* __restrict__ out, FastPlanDev P, int* flag) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int n = P.n, logn = P.logn, N = n >> 1;
+    double2* cb = reinterpret_cast<double2*>(smem_raw);
+    double* rb = reinterpret_cast<double*>(cb + padded_len(n));
+    double* ctab = rb + n;
+    double* red = ctab + P.taps;
+    double* fo = reinterpret_cast<double*>(cb + padded_len(N)); // odd grid points, beside the n/2-point FFT
+    const std::size_t b = blockIdx.x;
+    const double* prow = in + b * n;
+    double* o = out + b * n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const double2* tw = reinterpret_cast<const double2*>(P.tw2n);
+    const double2* rot = reinterpret_cast<const double2*>(P.rot);
+
+    for (int t = tid; t < P.taps; t += nt) ctab[t] = __ldg(P.ctab + t);
+    bool bad = false;
+    for (int j = tid; j < n; j += nt) {
+        bad |= !isfinite(prow[j]);
+        rb[j] = 0.0;
+    }
+    if (bad) atomicOr(flag, 1);
+    __syncthreads();
+
+    // 1. even grid points -> c = DST-I(f_even) (kept in rb)
+    spread_taps<false>(P, prow, ctab, rb);
+    __syncthreads();
+    pack_dst1(cb, rb, nullptr, n);
+    __syncthreads();
+    fft_inplace<double, false>(cb, n, logn, P.tw2n, 1);
+    unpack_dst1(cb, P.tw2n, nullptr, rb, n);
+    __syncthreads();
+
+    // 2. odd grid points -> Y = DCT-II core of (-1)^j f_odd_j (Makhoul, n/2 points)
+    for (int j = tid; j < n; j += nt) fo[j] = 0.0;
+    __syncthreads();
+    spread_taps<true>(P, prow, ctab, fo);
+    __syncthreads();
+    for (int j = tid; j < n; j += nt) {
+        const double v = (j & 1) ? -fo[j] : fo[j];
+        const int q = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
+        // the n/2-point FFT row (cb head) and fo (cb tail) are disjoint
+        reinterpret_cast<double*>(&cb[pad8(q >> 1)])[q & 1] = v;
+    }
+    __syncthreads();
+    fft_inplace<double, false>(cb, N, logn - 1, P.tw2n, 2);
+    // b_k = inv_phi_k (c_k / 2 + Y_{n-k}); Y_q for q = 1..n-1 from the split
+    for (int k = tid; k < N; k += nt) {
+        double yk, ynk; // Y_k, Y_{n-k}
+        if (k == 0) {
+            const double2 w0 = cb[0];
+            yk = 0.0; // Y_0 is not used (b_n does not exist)
+            ynk = (w0.x - w0.y) * __ldg(&rot[N].x); // Y_N
+            rb[N] = __ldg(P.inv_phi + N) * (0.5 * rb[N] + ynk);
+            continue;
+        }
+        const double2 wk = cb[pad8(k)], wc = cb[pad8(N - k)];
+        const double er = 0.5 * (wk.x + wc.x), ei = 0.5 * (wk.y - wc.y);
+        const double orr = 0.5 * (wk.x - wc.x), oi = 0.5 * (wk.y + wc.y);
+        const double2 sp = __ldg(tw + 2 * k);
+        const double qr = sp.x * orr - sp.y * oi, qi = sp.x * oi + sp.y * orr;
+        const double vr = er + qi, vi = ei - qr;
+        const double2 rt = __ldg(rot + k);
+        yk = vr * rt.x - vi * rt.y;
+        ynk = -(vr * rt.y + vi * rt.x);
+        // b_{n-k} uses Y_k, b_k uses Y_{n-k}
+        rb[k] = __ldg(P.inv_phi + k) * (0.5 * rb[k] + ynk);
+        rb[n - k] = __ldg(P.inv_phi + n - k) * (0.5 * rb[n - k] + yk);
+    }
+    __syncthreads();
+
+    // 3. g = DST-I(b); d = z (ext + d0 e_0 - w g) + pass-through, into rb
+    pack_dst1(cb, rb, nullptr, n);
+    double d0 = 0.0;
+    for (int r = tid; r < P.R; r += nt) d0 += __ldg(P.t_cb + r) * prow[__ldg(P.t_slot + r)];
+    d0 = block_sum(d0, red); // barrier: the pack is complete
+    const double pe = P.ext_slot >= 0 ? P.ext_scale * prow[P.ext_slot] : 0.0;
+    fft_inplace<double, false>(cb, n, logn, P.tw2n, 1);
+    for (int k = tid; k <= N; k += nt) {
+        double gk, gnk;
+        if (k == 0) {
+            rb[0] = P.z0 * d0 + (P.ext_slot >= 0 ? pe * __ldg(P.ez) : 0.0);
+            continue;
+        }
+        dst1_pair(cb[pad8(k)], cb[pad8(n - k)], __ldg(tw + k), gk, gnk);
+        const double ek = P.ext_slot >= 0 ? pe * __ldg(P.ez + k) : 0.0;
+        rb[k] = ek - __ldg(P.hz + k) * gk;
+        if (k != N) {
+            const double enk = P.ext_slot >= 0 ? pe * __ldg(P.ez + n - k) : 0.0;
+            rb[n - k] = enk - __ldg(P.hz + n - k) * gnk;
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < P.n_pass; e += nt)
+        rb[__ldg(P.pass_src + e)] += __ldg(P.pass_sign + e) * prow[__ldg(P.pass_slot + e)];
+    __syncthreads();
+
+    // 4. s = orthonormal DCT-III(d) (Makhoul, n/2 points)
+    {
+        const double scale = sqrt(2.0 / n), dc = 2.0 / sqrt(static_cast<double>(n));
+        const double r2 = 0.70710678118654752440;
+        for (int k = tid; k < N; k += nt) {
+            const double2 rt = __ldg(rot + k);
+            const double cr = rt.x, ci = -rt.y;
+            const double ar = (k == 0) ? rb[0] * dc : rb[k] * scale;
+            const double ai = (k == 0) ? 0.0 : -rb[n - k] * scale;
+            const double v1r = ar * cr - ai * ci, v1i = ar * ci + ai * cr;
+            const double c2r = r2 * (cr - ci), c2i = r2 * (cr + ci);
+            const double br = rb[k + N] * scale, bi = -rb[N - k] * scale;
+            const double v2r = br * c2r - bi * c2i, v2i = br * c2i + bi * c2r;
+            const double2 sp = __ldg(tw + 2 * k);
+            const double sr = sp.x, si = -sp.y;
+            const double dr = v1r - v2r, di = v1i - v2i;
+            const double qr = sr * dr - si * di, qi = sr * di + si * dr;
+            cb[pad8(k)] = make_double2(0.5 * (v1r + v2r - qi), 0.5 * (v1i + v2i + qr));
+        }
+    }
+    __syncthreads();
+    fft_inplace<double, true>(cb, N, logn - 1, P.tw2n, 2);
+    for (int j = tid; j < n; j += nt) {
+        const int q = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
+        const double2 w = cb[pad8(q >> 1)];
+        o[j] = (q & 1) ? w.y : w.x;
+    }
+}
+
 int nfst_threads(int n) { return std::min(512, std::max(128, n / 16)); }
 
 std::size_t nfst_smem_bytes(int n, int taps) {
@@ -263,15 +426,15 @@ bool nfst_supported(std::size_t n, int taps) {
     return is_pow2(n) && n >= 128 && n <= 8192 && nfst_smem_bytes(static_cast<int>(n), taps) <= 227 * 1024;
 }
 
-cudaError_t nfst_forward(const double* in, double* out, std::size_t batch, const FastPlanDev& P, int* flag,
-                         cudaStream_t stream) {
+cudaError_t nfst_apply(const double* in, double* out, std::size_t batch, const FastPlanDev& P, int* flag,
+                       bool inverse, cudaStream_t stream) {
     if (batch == 0) return cudaSuccess;
     if (!nfst_supported(P.n, P.taps)) return cudaErrorInvalidValue;
     const std::size_t smem = nfst_smem_bytes(P.n, P.taps);
-    cudaError_t e = cudaFuncSetAttribute(nfst_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    auto kern = inverse ? nfst_inverse_kernel : nfst_forward_kernel;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    nfst_forward_kernel<<<static_cast<unsigned>(batch), nfst_threads(P.n), smem, stream>>>(in, out, P, flag);
+    kern<<<static_cast<unsigned>(batch), nfst_threads(P.n), smem, stream>>>(in, out, P, flag);
     return cudaGetLastError();
 }
 

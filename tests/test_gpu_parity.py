@@ -618,7 +618,8 @@ def test_nfst_route_matches_reference_fast_route(P, torch, reference, monkeypatc
     reference's forward() to rounding, including the NFST's approximation
     error: at n = 1024 (self-loop 0.5) that error puts the reference 5e-9
     away from the exact transform, beyond the 1e-10 tolerance the exact
-    routes are held to.  The plan picks it by itself there (creation probe:
+    routes are held to; the same holds for inverse(p, fast = true) through
+    the adjoint NFST.  The plan picks it by itself there (creation probe:
     NFST vs exact gap > 1e-11) and from n = 2048 on speed; DCTP_FAST=1
     forces it below.  The last case is ill-conditioned for the reference
     itself: its result lies 3.6e-8 from the exact transform and moves by
@@ -646,6 +647,15 @@ def test_nfst_route_matches_reference_fast_route(P, torch, reference, monkeypatc
     assert abs(O.parity(got, exact) - O.parity(want, exact)) <= max(tol, 0.02 * O.parity(want, exact))
     y32 = plan.forward(dev(torch, s, torch.float32)).double().cpu().numpy()
     assert O.parity(y32, exact) <= TOL32
+    # inverse(p, fast = true): the adjoint NFST (fast_transform.hpp:218-255)
+    P.profile_reset()
+    P.profile_enable(True)
+    back = plan.inverse(dev(torch, want, torch.float64)).cpu().numpy()
+    P.profile_enable(False)
+    assert set(P.profile_summary()) == {"nfst_inv"}
+    back_want = rp.inverse(want)
+    assert O.parity(back, back_want) <= tol
+    assert O.parity(back, s) <= max(10 * tol, 2 * O.parity(back_want, s))  # round trip
     # empty batches and non-finite input follow the same contract
     assert plan.forward(dev(torch, s[:0], torch.float64)).shape == (0, n)
     bad = s[:3].copy()

@@ -352,7 +352,7 @@ struct dctp_plan {
         std::size_t hz = 0, ez = 0, inv_phi = 0, tw2n = 0, rot = 0, slot = 0, lo = 0, p0 = 0, b = 0, ca = 0, cb = 0,
                     ctab = 0;
         double z0 = 0.0, ext_scale = 0.0;
-        int R = 0, taps = 0, ext_slot = -1;
+        int R = 0, taps = 0, hw = 0, ext_slot = -1;
         bool preferred = false;  // chosen at creation (decide_fast_route)
         double probe_gap = 0.0;  // NFST vs exact on the creation probe (max-norm relative)
     } fs;
@@ -650,9 +650,14 @@ static void build_fast(dctp_plan& p, Blob& blob) {
         inv_phi[k] = std::exp(static_cast<double>(k) * static_cast<double>(k) * tau) / norm;
     for (std::size_t j = 1; j < n; ++j)
         hz[j] = (((j % 2) == 1 ? 1.0 : -1.0) / std::sin(static_cast<double>(j) * pi / static_cast<double>(n))) * st.z[j];
-    for (std::size_t t = 0; t < taps; ++t) {
-        const double d = (static_cast<double>(t) - static_cast<double>(hw)) * h;
-        ctab[t] = std::exp(-d * d / (4.0 * tau));
+    {
+        const double alpha = h * h / (4.0 * tau), H = static_cast<double>(hw);
+        ctab.assign(5, 0.0);
+        ctab[0] = std::exp(-alpha * H * H);
+        ctab[1] = std::exp(-alpha * (1.0 - H) * (1.0 - H));
+        ctab[2] = std::exp(-4.0 * alpha * (1.0 - H));
+        ctab[3] = std::exp(-4.0 * alpha * (2.0 - H));
+        ctab[4] = std::exp(-8.0 * alpha);
     }
     std::vector<int> lo(R);
     std::vector<double> p0(R), bb(R), ca(R), cb(R);
@@ -693,6 +698,7 @@ static void build_fast(dctp_plan& p, Blob& blob) {
     f.ext_slot = ext_slot;
     f.R = static_cast<int>(R);
     f.taps = static_cast<int>(taps);
+    f.hw = static_cast<int>(hw);
     f.on = true;
 }
 
@@ -721,6 +727,7 @@ static dctp::dev::FastPlanDev fast_plan_dev(const dctp_plan* p) {
     while ((std::size_t{1} << d.logn) < p->st.n) ++d.logn;
     d.R = f.R;
     d.taps = f.taps;
+    d.hw = f.hw;
     d.n_pass = p->n_pass;
     d.ext_slot = f.ext_slot;
     return d;

@@ -165,9 +165,10 @@ struct FastPlanDev {
     const double* t_b;       // weight ratio of consecutive taps (w_t = P0 B^t C_t)
     const double* t_ca;      // -scale / (4 sin(n theta))
     const double* t_cb;      // scale / nu
-    const double* ctab;      // taps: exp(-((t - halfwidth) h)^2 / 4 tau)
+    const double* ctab;      // {C_0, C_1, R_0, R_1, E}: C_t = exp(-alpha (t - hw)^2), R_t = C_{t+2} / C_t,
+                             // E = exp(-8 alpha), alpha = h^2 / 4 tau (tap-weight recurrence)
     double z0, ext_scale;
-    int n, logn, R, taps, n_pass, ext_slot; // ext_slot < 0: no exterior row
+    int n, logn, R, taps, hw, n_pass, ext_slot; // ext_slot < 0: no exterior row
 };
 
 bool nfst_supported(std::size_t n, int taps);

@@ -94,21 +94,103 @@ __device__ __forceinline__ void unpack_dst1(const double2* cb, const double* __r
     }
 }
 
+/// Halo of the grid arrays: the tap windows of targets near theta = 0 / pi
+/// reach past l = 0 / 2n, where y is odd-reflected (y_{-l} = -y_l, y_{2n+l} =
+/// -y_{2n-l}); the arrays carry the reflected values so the tap loops run
+/// branch-free.  kHalo >= (halfwidth + 3) / 2 for halfwidth <= 28.
+constexpr int kHalo = 16;
+
+/// Complex entries of the FFT row: the n-point FFT, or the n/2-point FFT
+/// plus the odd-grid array (n reals + halos) beside it.
+__host__ __device__ constexpr int cb_len(int n) {
+    return padded_len(n) > padded_len(n / 2) + (n + 2 * kHalo) / 2 + 1 ? padded_len(n)
+                                                                       : padded_len(n / 2) + (n + 2 * kHalo) / 2 + 1;
+}
+
+/// Sum (or, SPREAD, scatter-add of phi times) the taps of one parity of one
+/// target: l = lo + t, t = 0..2 hw, parity ODD, on the array y indexed by
+/// floor(l / 2) (halos included).  Weights w_t = P0 B^t C_t by the
+/// recurrence w_{t+2} = w_t G, G_{t+2} = G_t E with G_t = B^2 C_{t+2} / C_t
+/// (Gaussian: C_{t+2} / C_t = exp(-4 alpha (t - hw + 1)), E = exp(-8 alpha));
+/// g = {C_0, C_1, R_0, R_1, E}, R_t0 = C_{t0+2} / C_t0.
+template <int HW, bool ODD, bool SPREAD>
+__device__ __forceinline__ double tap_pass(double* y, int lo, double p0, double B, const double* g, int hw_rt,
+                                           double phi = 0.0) {
+    const int hw = HW > 0 ? HW : hw_rt;
+    const int t0 = (((lo & 1) != 0) == ODD) ? 0 : 1;
+    double* yy = y + ((lo + t0 - (ODD ? 1 : 0)) >> 1);
+    double w = p0 * (t0 ? B * g[1] : g[0]);
+    if (SPREAD) w *= phi;
+    double G = B * B * (t0 ? g[3] : g[2]);
+    const double E = g[4];
+    const int K = hw + 1 - t0;
+    double a = 0.0;
+    if constexpr (HW > 0) {
+#pragma unroll
+        for (int k = 0; k <= HW; ++k) {
+            if (k < K) {
+                if (SPREAD)
+                    atomicAdd(yy + k, w);
+                else
+                    a = fma(w, yy[k], a);
+            }
+            w *= G;
+            G *= E;
+        }
+    } else {
+        for (int k = 0; k < K; ++k) {
+            if (SPREAD)
+                atomicAdd(yy + k, w);
+            else
+                a = fma(w, yy[k], a);
+            w *= G;
+            G *= E;
+        }
+    }
+    return a;
+}
+
+template <bool ODD, bool SPREAD>
+__device__ __forceinline__ double taps(const FastPlanDev& P, double* y, int r, const double* g, double phi = 0.0) {
+    const int lo = __ldg(P.t_lo + r);
+    const double p0 = __ldg(P.t_p0 + r), B = __ldg(P.t_b + r);
+    if (P.hw == 17) return tap_pass<17, ODD, SPREAD>(y, lo, p0, B, g, 17, phi);
+    return tap_pass<0, ODD, SPREAD>(y, lo, p0, B, g, P.hw, phi);
+}
+
+/// Odd-reflected halos: yo[i] = y_{2i+1} and ye[i] = y_{2i} (ye[0] = ye[n] = 0).
+__device__ __forceinline__ void fill_halos(double* yo, double* ye, int n) {
+    for (int k = threadIdx.x; k < kHalo; k += blockDim.x) {
+        if (yo) {
+            yo[-k - 1] = -yo[k];
+            yo[n + k] = -yo[n - 1 - k];
+        }
+        if (ye) {
+            if (k == 0) {
+                ye[n] = 0.0;
+            } else {
+                ye[-k] = -ye[k];
+                ye[n + k] = -ye[n - k];
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(512)
 nfst_forward_kernel(const double* __restrict__ in, double* __restrict__ out, FastPlanDev P, int* flag) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = P.n, logn = P.logn, N = n >> 1;
-    double2* cb = reinterpret_cast<double2*>(smem_raw); // FFT row, padded_len(n) complex
-    double* rb = reinterpret_cast<double*>(cb + padded_len(n)); // n reals: shat, then v, then y_even
-    double* ctab = rb + n;                              // taps
-    double* red = ctab + P.taps;                        // 33
-    double* yo = reinterpret_cast<double*>(cb + padded_len(N)); // y_odd, beside the n/2-point FFT
+    double2* cb = reinterpret_cast<double2*>(smem_raw);                // FFT row, cb_len(n) complex
+    double* rb = reinterpret_cast<double*>(cb + cb_len(n)) + kHalo;    // n reals: shat, then v, then y_even
+    double* g = rb + n + kHalo;                                         // 5 weight-recurrence constants
+    double* red = g + 8;                                                // 33
+    double* yo = reinterpret_cast<double*>(cb + padded_len(N)) + kHalo; // y_odd, beside the n/2-point FFT
     const std::size_t b = blockIdx.x;
     const double* x = in + b * n;
     double* o = out + b * n;
     const int tid = threadIdx.x, nt = blockDim.x;
 
-    for (int t = tid; t < P.taps; t += nt) ctab[t] = __ldg(P.ctab + t);
+    if (tid < 5) g[tid] = __ldg(P.ctab + tid);
 
     // 1. DCT-II (Makhoul): v = (x0, x2, ..., x3, x1) packed as w_m = v_2m + i v_2m+1
     bool bad = false;
@@ -195,29 +277,12 @@ nfst_forward_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
     }
     __syncthreads();
 
+    fill_halos(yo, nullptr, n);
+    __syncthreads();
+
     // 5. gather the odd taps of every interior target; the partial sum parks
     //    in the target's own output slot (same thread reads it back in 7)
-    const int two_n = 2 * n, four_n = 4 * n;
-    for (int r = tid; r < P.R; r += nt) {
-        const int lo = __ldg(P.t_lo + r);
-        const double B = __ldg(P.t_b + r), B2 = B * B;
-        const int t0 = (lo & 1) ? 0 : 1;
-        double pw = __ldg(P.t_p0 + r) * (t0 ? B : 1.0);
-        double a = 0.0;
-        for (int t = t0; t < P.taps; t += 2, pw *= B2) {
-            int l = lo + t;
-            double sg = pw * ctab[t];
-            if (l < 0) {
-                l = -l;
-                sg = -sg;
-            } else if (l > two_n) {
-                l = four_n - l;
-                sg = -sg;
-            }
-            a += sg * yo[(l - 1) >> 1];
-        }
-        o[__ldg(P.t_slot + r)] = a;
-    }
+    for (int r = tid; r < P.R; r += nt) o[__ldg(P.t_slot + r)] = taps<true, false>(P, yo, r, g);
     __syncthreads();
 
     // 6. even grid points: y_{2k} = DST-I(v)_k
@@ -227,56 +292,14 @@ nfst_forward_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
     unpack_dst1(cb, P.tw2n, nullptr, rb, n);
     __syncthreads();
 
+    fill_halos(nullptr, rb, n);
+    __syncthreads();
+
     // 7. even taps, then the secular-row epilogue
     for (int r = tid; r < P.R; r += nt) {
-        const int lo = __ldg(P.t_lo + r);
-        const double B = __ldg(P.t_b + r), B2 = B * B;
-        const int t0 = (lo & 1) ? 1 : 0;
-        double pw = __ldg(P.t_p0 + r) * (t0 ? B : 1.0);
         const int slot = __ldg(P.t_slot + r);
-        double a = o[slot];
-        for (int t = t0; t < P.taps; t += 2, pw *= B2) {
-            int l = lo + t;
-            double sg = pw * ctab[t];
-            if (l < 0) {
-                l = -l;
-                sg = -sg;
-            } else if (l > two_n) {
-                l = four_n - l;
-                sg = -sg;
-            }
-            if (l != 0 && l != two_n) a += sg * rb[l >> 1];
-        }
+        const double a = o[slot] + taps<false, false>(P, rb, r, g);
         o[slot] = __ldg(P.t_ca + r) * a + __ldg(P.t_cb + r) * sv0;
-    }
-}
-
-/// Spread phi_r = -2 t_ca[r] p[slot_r] over the taps of one parity into f
-/// (reflected about 0 and 2n with a sign flip: the adjoint of the gather).
-template <bool ODD>
-__device__ __forceinline__ void spread_taps(const FastPlanDev& P, const double* prow, const double* ctab, double* f) {
-    const int two_n = 2 * P.n, four_n = 4 * P.n;
-    for (int r = threadIdx.x; r < P.R; r += blockDim.x) {
-        const int lo = __ldg(P.t_lo + r);
-        const double B = __ldg(P.t_b + r), B2 = B * B;
-        const double phi = -2.0 * __ldg(P.t_ca + r) * prow[__ldg(P.t_slot + r)];
-        const int t0 = ((lo & 1) != 0) == ODD ? 0 : 1;
-        double pw = phi * __ldg(P.t_p0 + r) * (t0 ? B : 1.0);
-        for (int t = t0; t < P.taps; t += 2, pw *= B2) {
-            int l = lo + t;
-            double v = pw * ctab[t];
-            if (l < 0) {
-                l = -l;
-                v = -v;
-            } else if (l > two_n) {
-                l = four_n - l;
-                v = -v;
-            }
-            if (ODD)
-                atomicAdd(f + ((l - 1) >> 1), v);
-            else if (l != 0 && l != two_n)
-                atomicAdd(f + (l >> 1), v);
-        }
     }
 }
 
@@ -292,10 +315,10 @@ nfst_inverse_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = P.n, logn = P.logn, N = n >> 1;
     double2* cb = reinterpret_cast<double2*>(smem_raw);
-    double* rb = reinterpret_cast<double*>(cb + padded_len(n));
-    double* ctab = rb + n;
-    double* red = ctab + P.taps;
-    double* fo = reinterpret_cast<double*>(cb + padded_len(N)); // odd grid points, beside the n/2-point FFT
+    double* rb = reinterpret_cast<double*>(cb + cb_len(n)) + kHalo;
+    double* g = rb + n + kHalo;
+    double* red = g + 8;
+    double* fo = reinterpret_cast<double*>(cb + padded_len(N)) + kHalo; // odd grid points, beside the n/2-point FFT
     const std::size_t b = blockIdx.x;
     const double* prow = in + b * n;
     double* o = out + b * n;
@@ -303,17 +326,21 @@ nfst_inverse_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
     const double2* tw = reinterpret_cast<const double2*>(P.tw2n);
     const double2* rot = reinterpret_cast<const double2*>(P.rot);
 
-    for (int t = tid; t < P.taps; t += nt) ctab[t] = __ldg(P.ctab + t);
+    if (tid < 5) g[tid] = __ldg(P.ctab + tid);
     bool bad = false;
-    for (int j = tid; j < n; j += nt) {
-        bad |= !isfinite(prow[j]);
-        rb[j] = 0.0;
-    }
+    for (int j = tid; j < n; j += nt) bad |= !isfinite(prow[j]);
+    for (int j = tid - kHalo; j < n + kHalo; j += nt) rb[j] = 0.0;
     if (bad) atomicOr(flag, 1);
     __syncthreads();
 
-    // 1. even grid points -> c = DST-I(f_even) (kept in rb)
-    spread_taps<false>(P, prow, ctab, rb);
+    // 1. even grid points -> c = DST-I(f_even) (kept in rb); the halos fold
+    //    back with the odd reflection (the adjoint of fill_halos)
+    for (int r = tid; r < P.R; r += nt) taps<false, true>(P, rb, r, g, -2.0 * __ldg(P.t_ca + r) * prow[__ldg(P.t_slot + r)]);
+    __syncthreads();
+    for (int k = tid + 1; k < kHalo; k += nt) {
+        rb[k] -= rb[-k];
+        rb[n - k] -= rb[n + k];
+    }
     __syncthreads();
     pack_dst1(cb, rb, nullptr, n);
     __syncthreads();
@@ -322,9 +349,14 @@ nfst_inverse_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
     __syncthreads();
 
     // 2. odd grid points -> Y = DCT-II core of (-1)^j f_odd_j (Makhoul, n/2 points)
-    for (int j = tid; j < n; j += nt) fo[j] = 0.0;
+    for (int j = tid - kHalo; j < n + kHalo; j += nt) fo[j] = 0.0;
     __syncthreads();
-    spread_taps<true>(P, prow, ctab, fo);
+    for (int r = tid; r < P.R; r += nt) taps<true, true>(P, fo, r, g, -2.0 * __ldg(P.t_ca + r) * prow[__ldg(P.t_slot + r)]);
+    __syncthreads();
+    for (int k = tid; k < kHalo; k += nt) {
+        fo[k] -= fo[-k - 1];
+        fo[n - 1 - k] -= fo[n + k];
+    }
     __syncthreads();
     for (int j = tid; j < n; j += nt) {
         const double v = (j & 1) ? -fo[j] : fo[j];
@@ -416,21 +448,21 @@ nfst_inverse_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
 
 int nfst_threads(int n) { return std::min(512, std::max(128, n / 16)); }
 
-std::size_t nfst_smem_bytes(int n, int taps) {
-    return static_cast<std::size_t>(padded_len(n)) * sizeof(double2) + (n + taps + 40) * sizeof(double);
+std::size_t nfst_smem_bytes(int n) {
+    return static_cast<std::size_t>(cb_len(n)) * sizeof(double2) + (n + 2 * kHalo + 8 + 40) * sizeof(double);
 }
 
 } // namespace
 
 bool nfst_supported(std::size_t n, int taps) {
-    return is_pow2(n) && n >= 128 && n <= 8192 && nfst_smem_bytes(static_cast<int>(n), taps) <= 227 * 1024;
+    return is_pow2(n) && n >= 128 && n <= 8192 && taps <= 57 && nfst_smem_bytes(static_cast<int>(n)) <= 227 * 1024;
 }
 
 cudaError_t nfst_apply(const double* in, double* out, std::size_t batch, const FastPlanDev& P, int* flag,
                        bool inverse, cudaStream_t stream) {
     if (batch == 0) return cudaSuccess;
     if (!nfst_supported(P.n, P.taps)) return cudaErrorInvalidValue;
-    const std::size_t smem = nfst_smem_bytes(P.n, P.taps);
+    const std::size_t smem = nfst_smem_bytes(P.n);
     auto kern = inverse ? nfst_inverse_kernel : nfst_forward_kernel;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;

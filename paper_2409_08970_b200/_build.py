@@ -31,6 +31,10 @@ HEADERS = (
 
 INCLUDES = ["-I", str(CSRC), "-I", str(ROOT / "include")]
 
+# setup.cu restates the host setup's floating-point operations one for one:
+# no multiply-add contraction, so its roots are bit-identical to the host's.
+FILE_FLAGS = {"setup.cu": ["-fmad=false"]}
+
 
 def _stale(target: Path, deps) -> bool:
     if not target.exists():
@@ -53,7 +57,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         obj = BUILD / (src.stem + ".cu.o")
         if force or _stale(obj, [src, *HEADERS, __file__]):
             _run([NVCC, "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
-                  "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr", *INCLUDES,
+                  "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr", *FILE_FLAGS.get(src.name, []), *INCLUDES,
                   "-c", str(src), "-o", str(obj)], verbose)
         objs.append(obj)
     for src in CPP_SOURCES:

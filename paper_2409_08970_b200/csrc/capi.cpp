@@ -851,14 +851,79 @@ template <class T>
 static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s);
 static void decide_fast_route(dctp_plan& p);
 
+/// The secular roots and normalisers run on the current device from n =
+/// DCTP_GPU_SETUP_MIN_N (default 1024; below it the host loops take
+/// milliseconds); DCTP_GPU_SETUP=0 / 1 forces the choice.  Bit-identical
+/// either way (kernels/setup.cu).
+static bool gpu_setup(std::size_t n) {
+    const char* e = std::getenv("DCTP_GPU_SETUP");
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return true;
+    const char* m = std::getenv("DCTP_GPU_SETUP_MIN_N");
+    return n >= (m ? static_cast<std::size_t>(std::atoll(m)) : std::size_t{1024});
+}
+
+static dctp::host::SecularBackend gpu_secular_backend() {
+    dctp::host::SecularBackend be;
+    be.roots = [](const std::vector<double>& lam, const std::vector<double>& z, double rho, double zz) {
+        const std::size_t k = lam.size();
+        double* d = nullptr;
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&d), 3 * k * sizeof(double) + sizeof(int)), "cudaMalloc(setup)");
+        std::unique_ptr<double, decltype(&cudaFree)> hold(d, &cudaFree);
+        int* status = reinterpret_cast<int*>(d + 3 * k);
+        cuda_check(cudaMemcpy(d, lam.data(), k * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy(setup)");
+        cuda_check(cudaMemcpy(d + k, z.data(), k * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy(setup)");
+        cuda_check(cudaMemset(status, 0, sizeof(int)), "cudaMemset(setup)");
+        cuda_check(DCTP_LAUNCH("secular_roots", nullptr,
+                               dctp::dev::secular_roots_gpu(d, d + k, static_cast<int>(k), rho, zz, d + 2 * k, status,
+                                                            nullptr)),
+                   "secular roots kernel");
+        std::vector<double> mu(k);
+        int st = 0;
+        cuda_check(cudaMemcpy(mu.data(), d + 2 * k, k * sizeof(double), cudaMemcpyDeviceToHost), "cudaMemcpy(setup)");
+        cuda_check(cudaMemcpy(&st, status, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(setup)");
+        if (st) throw std::runtime_error("secular_eigenvalues: no convergence in 200 iterations");
+        return mu;
+    };
+    be.normalisers = [](const std::vector<double>& lam, const std::vector<double>& mu, const std::vector<double>& z) {
+        const std::size_t m = lam.size(), k = mu.size();
+        double* d = nullptr;
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&d), (2 * m + 2 * k) * sizeof(double) + sizeof(int)),
+                   "cudaMalloc(setup)");
+        std::unique_ptr<double, decltype(&cudaFree)> hold(d, &cudaFree);
+        int* status = reinterpret_cast<int*>(d + 2 * m + 2 * k);
+        cuda_check(cudaMemcpy(d, lam.data(), m * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy(setup)");
+        cuda_check(cudaMemcpy(d + m, z.data(), m * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy(setup)");
+        cuda_check(cudaMemcpy(d + 2 * m, mu.data(), k * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy(setup)");
+        cuda_check(cudaMemset(status, 0, sizeof(int)), "cudaMemset(setup)");
+        cuda_check(DCTP_LAUNCH("normalisers", nullptr,
+                               dctp::dev::normalisers_gpu(d, d + m, static_cast<int>(m), d + 2 * m,
+                                                          static_cast<int>(k), d + 2 * m + k, status, nullptr)),
+                   "normalisers kernel");
+        std::vector<double> a(k);
+        int st = 0;
+        cuda_check(cudaMemcpy(a.data(), d + 2 * m + k, k * sizeof(double), cudaMemcpyDeviceToHost),
+                   "cudaMemcpy(setup)");
+        cuda_check(cudaMemcpy(&st, status, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(setup)");
+        if (st & 2) throw std::domain_error("normalizers: mu/lambda collision; deflation missing");
+        if (st & 4) throw std::domain_error("normalizers: degenerate column");
+        return a;
+    };
+    return be;
+}
+
 static std::unique_ptr<dctp_plan> build_plan(std::size_t n, const dctp::host::Update& u, double eps, double tau,
                                              int device) {
     auto p = std::make_unique<dctp_plan>();
     p->update = u;
     p->device = device;
-    p->st = dctp::host::build_setup(n, u, eps, tau);
-    if (device < 0) return p; // host-only plan: setup vectors, no device constants
+    if (device < 0) { // host-only plan: setup vectors, no device constants
+        p->st = dctp::host::build_setup(n, u, eps, tau);
+        return p;
+    }
     DeviceScope scope(device);
+    const dctp::host::SecularBackend be = gpu_secular_backend();
+    p->st = dctp::host::build_setup(n, u, eps, tau, gpu_setup(n) ? &be : nullptr);
     prepare_pool(device);
     upload_plan(*p);
     decide_fast_route(*p);

@@ -215,8 +215,20 @@ inline double secular_root(const std::vector<double>& lam, const std::vector<dou
     throw std::runtime_error("secular_eigenvalues: no convergence in 200 iterations");
 }
 
+/// Optional device backend for the two O(k^2) loops of the setup (the GPU
+/// kernels in kernels/setup.cu, same operations in the same order, so the
+/// results are bit-identical); empty members fall back to the host loops.
+struct SecularBackend {
+    std::function<std::vector<double>(const std::vector<double>& lam, const std::vector<double>& z, double rho,
+                                      double zz)>
+        roots;
+    std::function<std::vector<double>(const std::vector<double>& lam, const std::vector<double>& mu,
+                                      const std::vector<double>& z)>
+        normalisers;
+};
+
 inline std::vector<double> secular_roots(const std::vector<double>& lam, const std::vector<double>& z,
-                                         double rho) {
+                                         double rho, const SecularBackend* be = nullptr) {
     const std::size_t k = lam.size();
     if (k == 0) return {};
     if (z.size() != k) throw std::invalid_argument("secular_eigenvalues: size mismatch");
@@ -234,6 +246,7 @@ inline std::vector<double> secular_roots(const std::vector<double>& lam, const s
         mu[0] = lam[0] + rho * zz;
         return mu;
     }
+    if (be && be->roots) return be->roots(lam, z, rho, zz);
     // Root r lies in (lo_r, hi_r); the exterior bracket sits on rho's side.
     parallel_for(k, [&](std::size_t r) {
         double lo, hi;
@@ -303,8 +316,9 @@ inline Deflated deflate(const std::vector<double>& lam, const std::vector<double
 }
 
 inline std::vector<double> normalisers(const std::vector<double>& lam, const std::vector<double>& mu,
-                                       const std::vector<double>& z) {
+                                       const std::vector<double>& z, const SecularBackend* be = nullptr) {
     if (lam.size() != z.size()) throw std::invalid_argument("normalizers: size mismatch");
+    if (be && be->normalisers) return be->normalisers(lam, mu, z);
     std::vector<double> a(mu.size());
     std::vector<int> bad(mu.size(), 0);
     parallel_for(mu.size(), [&](std::size_t i) {
@@ -360,7 +374,7 @@ struct Perturbed {
 };
 
 inline Perturbed perturb_spectrum(const std::vector<double>& lam, const std::vector<double>& z, double rho,
-                                  double tau) {
+                                  double tau, const SecularBackend* be = nullptr) {
     Perturbed p;
     Deflated d = deflate(lam, z, tau);
     p.z = std::move(d.z);
@@ -371,9 +385,9 @@ inline Perturbed perturb_spectrum(const std::vector<double>& lam, const std::vec
         p.sub_lambda.push_back(lam[j]);
         p.sub_z.push_back(p.z[j]);
     }
-    if (!p.sub_lambda.empty()) p.sub_mu = secular_roots(p.sub_lambda, p.sub_z, rho);
+    if (!p.sub_lambda.empty()) p.sub_mu = secular_roots(p.sub_lambda, p.sub_z, rho, be);
     const std::vector<double> sub_a =
-        p.sub_mu.empty() ? std::vector<double>{} : normalisers(p.sub_lambda, p.sub_mu, p.sub_z);
+        p.sub_mu.empty() ? std::vector<double>{} : normalisers(p.sub_lambda, p.sub_mu, p.sub_z, be);
 
     std::size_t ip = 0, ia = 0;
     const std::size_t n = lam.size();
@@ -424,7 +438,8 @@ inline void basis_coefficients(const Setup& st, std::size_t s, double* y) {
         if (st.z[j] != 0.0) y[j] = st.a[s] * st.z[j] / (st.lambda[j] - nu);
 }
 
-inline Setup build_setup(std::size_t n, const Update& update, double epsilon, double tau) {
+inline Setup build_setup(std::size_t n, const Update& update, double epsilon, double tau,
+                         const SecularBackend* be = nullptr) {
     if (n < 2) throw std::invalid_argument("DctPlusPlan: need n >= 2");
     if (!(epsilon > 0.0) || !(epsilon < 1.0))
         throw std::invalid_argument("DctPlusPlan: epsilon must lie in (0, 1)");
@@ -448,7 +463,7 @@ inline Setup build_setup(std::size_t n, const Update& update, double epsilon, do
         dct.execute(v.data(), st.z_raw.data(), scratch.data());
     }
 
-    Perturbed ps = perturb_spectrum(st.lambda, st.z_raw, update.rho, tau);
+    Perturbed ps = perturb_spectrum(st.lambda, st.z_raw, update.rho, tau, be);
     if (!ps.rotations.empty()) throw std::logic_error("DctPlusPlan: path eigenvalues cannot repeat");
     st.z = std::move(ps.z);
     st.kept = std::move(ps.kept);

@@ -177,6 +177,15 @@ bool nfst_supported(std::size_t n, int taps);
 cudaError_t nfst_apply(const double* in, double* out, std::size_t batch, const FastPlanDev& P, int* flag,
                        bool inverse, cudaStream_t stream);
 
+/// Per-graph setup on the GPU (setup.cu, compiled with -fmad=false): the
+/// secular roots mu (k sorted distinct lam, nonzero z, zz = sum z^2; status
+/// bit 0 = no convergence) and the normalisers a (status bit 1 = collision,
+/// bit 2 = degenerate column), bit-identical to host/setup.hpp.
+cudaError_t secular_roots_gpu(const double* lam, const double* z, int k, double rho, double zz, double* mu,
+                              int* status, cudaStream_t stream);
+cudaError_t normalisers_gpu(const double* lam, const double* z, int m, const double* mu, int k, double* a,
+                            int* status, cudaStream_t stream);
+
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);
 cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,

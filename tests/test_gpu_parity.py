@@ -670,3 +670,29 @@ def test_exact_route_kept_where_nfst_gap_is_small(P, torch, reference):
     plan = plan_for(P, 2)
     r = plan.route()
     assert not r["nfst"] and 0.0 < r["probe_gap"] <= 1e-11
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "c3", "c5", "neg", "deflating", "nfst1024"])
+def test_gpu_setup_bit_identical(P, torch, monkeypatch, case):
+    """The secular roots and normalisers computed on the GPU (setup.cu,
+    -fmad=false, the host restatement's operations in the same order) are
+    bit-identical to the host setup (itself bit-identical to the reference:
+    tests/test_host_setup.py), and so are the slot map and the signs."""
+    if case[0] == "c":
+        cfg = O.config(int(case[1]))
+        n, u = cfg.n, cfg.updates[0]
+    else:
+        n, u = {"neg": (512, O.Update(0, -0.4, 512)), "deflating": (1024, O.Update(1, 1.0, 1, 1024)),
+                "nfst1024": (1024, O.Update(0, 0.5, 1))}[case]
+    monkeypatch.setenv("DCTP_GPU_SETUP", "1")
+    gpu = P.DctPlusPlan(n, upd(P, u), 1e-12, device=0)
+    P.profile_reset()
+    P.profile_enable(True)
+    P.DctPlusPlan(n, upd(P, u), 1e-12, device=0)
+    P.profile_enable(False)
+    assert "secular_roots" in P.profile_summary()
+    host = P.DctPlusPlan(n, upd(P, u), 1e-12, device=-1)
+    a, b = gpu.setup(), host.setup()
+    for k in b:
+        assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
+    assert gpu.slow_path() == host.slow_path()

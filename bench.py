@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2, help="BASELINE config id (2 = the headline workload; 6 = rank-k chain, SURVEY 8f)")
+    ap.add_argument("--config", type=int, default=2, help="BASELINE config id (2 = the headline workload; 6 = rank-k chain, 7-8 = NFST route, SURVEY 8f)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -347,6 +347,13 @@ def run_gpu_arm(args, cfg, rank: int, local: int, world: int):
     hbm_achieved = nbytes / (t_ms * 1e-3) / 1e9
     t_flop = flops / (peak * 1e12) if peak else 0.0
     t_hbm = nbytes / (hbm_peak * 1e9)
+    if "nfst" in top:
+        # the NFST route's work is O(n log n) per signal (four FFTs of <= n
+        # points and a 35-tap gather per root): its roofline is the HBM
+        # traffic of one read and one write per sample
+        t_ms = per_launch_ms[top]
+        hbm_achieved = nbytes / (t_ms * 1e-3) / 1e9
+        achieved, t_flop = 0.0, 0.0
     if t_hbm >= t_flop:
         roof = {"bound": "hbm", "kernel": top, "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": hbm_achieved / hbm_peak, "traffic": None, "peak_source": hbm_src}

@@ -59,6 +59,14 @@ WORKLOADS = {
     6: Workload(6, "X6 n=1024 chain self_loop(1,1.5)+edge_delta(1,1024,-0.5)+edge_delta(300,700,0.25) fwd fp64 "
                    "batch 16384", 1024, 16384, 2, 0.95,
                 ((0, 1.5, 1, 0), (1, -0.5, 1, 1024), (1, 0.25, 300, 700)), ("f64",), chain=True),
+    # not BASELINE configs: the NFST fast route where the
+    # reference's own forward() is its NFST approximation — 7: it lies 5e-9 from
+    # the exact transform (the plan keeps the NFST route for fidelity); 8: the
+    # NFST route is also the faster one (n = 2048, fully kept)
+    7: Workload(7, "X7 n=1024 self_loop(1,0.5) fwd fp64 batch 16384 (NFST route)", 1024, 16384, 0, 0.0,
+                ((0, 0.5, 1, 0),), ("f64",)),
+    8: Workload(8, "X8 n=2048 self_loop(1,5.0) fwd fp64 batch 8192 (NFST route)", 2048, 8192, 0, 0.0,
+                ((0, 5.0, 1, 0),), ("f64",)),
 }
 
 

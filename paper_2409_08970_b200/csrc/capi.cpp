@@ -909,6 +909,52 @@ static dctp::host::SecularBackend gpu_secular_backend() {
         if (st & 4) throw std::domain_error("normalizers: degenerate column");
         return a;
     };
+    // sigma: the unsigned basis columns (DCT-domain rows a_s z_j / (lambda_j -
+    // nu_s), one batched DCT-III) in chunks of <= 256 MB, then the column-sign
+    // rule on each (cauchy.hpp:84-103, spectral.hpp:30-37)
+    be.signs = [](dctp::host::Setup& st) {
+        const std::size_t n = st.n, ld = (n + 3) / 4 * 4;
+        Blob blob;
+        const TwiddleOffsets two = add_twiddles<double>(blob, n);
+        std::vector<double> tab(5 * n, 0.0); // z, lambda, nu, a, sigma = 1
+        std::vector<int> pidx(n);
+        for (std::size_t q = 0; q < n; ++q) {
+            tab[q] = st.z[q];
+            tab[n + q] = st.lambda[q];
+            const auto& sl = st.slots[q];
+            pidx[q] = sl.passthrough ? static_cast<int>(sl.idx) : -1;
+            tab[2 * n + q] = sl.passthrough ? 0.0 : st.sub_mu[sl.idx];
+            tab[3 * n + q] = st.a[q];
+            tab[4 * n + q] = 1.0;
+        }
+        const std::size_t tab_off = blob.add(tab), pidx_off = blob.add(pidx);
+        const std::size_t sign_off = blob.add(std::vector<double>(n, 1.0)), flag_off = blob.add(std::vector<int>(1, 0));
+        void* base = blob.upload();
+        std::unique_ptr<void, decltype(&cudaFree)> hold_blob(base, &cudaFree);
+        const double* dtab = at<double>(base, tab_off);
+        const int* dp = at<int>(base, pidx_off);
+        double* dsign = const_cast<double*>(at<double>(base, sign_off));
+        int* dflag = const_cast<int*>(at<int>(base, flag_off));
+        const std::size_t chunk = std::max<std::size_t>(1, std::min(n, (std::size_t{256} << 20) / (2 * ld * 8)));
+        double* y = nullptr;
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&y), 2 * chunk * ld * sizeof(double)), "cudaMalloc(signs)");
+        std::unique_ptr<double, decltype(&cudaFree)> hold_y(y, &cudaFree);
+        const int ni = static_cast<int>(n);
+        for (std::size_t r0 = 0; r0 < n; r0 += chunk) {
+            const int rows = static_cast<int>(std::min(chunk, n - r0));
+            cuda_check(dctp::dev::basis_coefficients(ni, ld, dtab, dtab + n, dtab + 2 * n + r0, dp + r0,
+                                                     dtab + 3 * n + r0, dtab + 4 * n + r0, y, nullptr, rows),
+                       "basis kernel (signs)");
+            cuda_check(dctp::dev::idct_rows<double>(y, ld, y, ld, dctp::dev::Emit<double>{}, y + chunk * ld, ld, n,
+                                                    static_cast<std::size_t>(rows), twiddles_at<double>(base, two),
+                                                    dflag, nullptr),
+                       "basis idct kernel (signs)");
+            cuda_check(DCTP_LAUNCH("column_signs", nullptr,
+                                   dctp::dev::column_signs_gpu(y + chunk * ld, ld, ni, rows, dsign + r0, nullptr)),
+                       "column signs kernel");
+        }
+        cuda_check(cudaMemcpy(st.sigma.data(), dsign, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H(signs)");
+    };
     return be;
 }
 

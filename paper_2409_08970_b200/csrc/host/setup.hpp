@@ -215,6 +215,8 @@ inline double secular_root(const std::vector<double>& lam, const std::vector<dou
     throw std::runtime_error("secular_eigenvalues: no convergence in 200 iterations");
 }
 
+struct Setup;
+
 /// Optional device backend for the two O(k^2) loops of the setup (the GPU
 /// kernels in kernels/setup.cu, same operations in the same order, so the
 /// results are bit-identical); empty members fall back to the host loops.
@@ -225,6 +227,8 @@ struct SecularBackend {
     std::function<std::vector<double>(const std::vector<double>& lam, const std::vector<double>& mu,
                                       const std::vector<double>& z)>
         normalisers;
+    // column signs of the unsigned basis (fills Setup::sigma)
+    std::function<void(Setup&)> signs;
 };
 
 inline std::vector<double> secular_roots(const std::vector<double>& lam, const std::vector<double>& z,
@@ -476,6 +480,9 @@ inline Setup build_setup(std::size_t n, const Update& update, double epsilon, do
     // Column signs from the materialised basis, one inverse DCT per column
     // (cauchy.hpp:84-103 through fast_transform.hpp:72-84).
     st.sigma.assign(n, 1.0);
+    if (be && be->signs) {
+        be->signs(st);
+    } else {
     const Trig idct(Trig::Kind::idct2, n);
     parallel_for(n, [&](std::size_t s) {
         thread_local std::vector<double> buf;
@@ -487,6 +494,7 @@ inline Setup build_setup(std::size_t n, const Update& update, double epsilon, do
         idct.execute(y, col, col + n);
         st.sigma[s] = sign_of_column(col, n);
     }, 4);
+    }
 
     // slow_path() exactly as the reference decides it (fast_transform.hpp:86-117):
     // a near-pole secular root, or an interior root outside the Chebyshev range.

@@ -275,9 +275,11 @@ __global__ void transpose_kernel(const double* __restrict__ in, std::size_t ld_i
 
 cudaError_t basis_coefficients(int n, std::size_t ld, const double* z, const double* lambda, const double* nu,
                                const int* pass_idx, const double* a, const double* sigma, double* y,
-                               cudaStream_t stream) {
+                               cudaStream_t stream, int rows) {
     if (n == 0) return cudaSuccess;
-    dim3 grid(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(n));
+    if (rows < 0) rows = n;
+    if (rows == 0) return cudaSuccess;
+    dim3 grid(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(rows));
     basis_coeff_kernel<<<grid, 256, 0, stream>>>(n, ld, z, lambda, nu, pass_idx, a, sigma, y);
     return cudaGetLastError();
 }

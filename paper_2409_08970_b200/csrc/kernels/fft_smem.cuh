@@ -79,22 +79,14 @@ __device__ __forceinline__ void fft_rows(const cplx_t<T>* src, cplx_t<T>* dst, i
     if (logN - s0 == 1) dit_group_pass<T, Inverse, 1, false>(dst, dst, rows, N, logN, s0, tw, tw_extra);
 }
 
-/// In-place FFT of one padded row of N = 2^logN points (natural order in and
-/// out): a bit-reversal swap pass, then the radix-8 DIT passes.  For rows too
-/// long to keep a second buffer beside them in shared memory (NFST route,
-/// n = 8192: 8192 complex doubles = 144 KB padded).
+/// In-place FFT of one padded row of N = 2^logN points whose producer
+/// already stored element i at position bit_reverse(i) (no permutation pass):
+/// the radix-8 DIT passes only; natural-order output.  The NFST kernels
+/// (nfst.cu) use it for rows too long to keep a second buffer beside them
+/// in shared memory (n = 8192: 8192 complex doubles = 144 KB padded).
 template <class T, bool Inverse>
-__device__ __forceinline__ void fft_inplace(cplx_t<T>* buf, int N, int logN, const T* __restrict__ tw,
-                                            int tw_extra = 0) {
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        const int r = static_cast<int>(bit_reverse(static_cast<unsigned>(i), logN));
-        if (i < r) {
-            const cplx_t<T> a = buf[pad8(i)], b = buf[pad8(r)];
-            buf[pad8(i)] = b;
-            buf[pad8(r)] = a;
-        }
-    }
-    __syncthreads();
+__device__ __forceinline__ void fft_from_bitreversed(cplx_t<T>* buf, int N, int logN, const T* __restrict__ tw,
+                                                     int tw_extra = 0) {
     int s0 = 0;
     for (; s0 + 3 <= logN; s0 += 3) dit_group_pass<T, Inverse, 3, false>(buf, buf, 1, N, logN, s0, tw, tw_extra);
     if (logN - s0 == 2) dit_group_pass<T, Inverse, 2, false>(buf, buf, 1, N, logN, s0, tw, tw_extra);

@@ -132,7 +132,7 @@ cudaError_t sgemm_rows(const float* A, int lda, const float* B, int ldb, float* 
 /// an n x n transpose: with idct_rows these materialise X^T and X on the device.
 cudaError_t basis_coefficients(int n, std::size_t ld, const double* z, const double* lambda, const double* nu,
                                const int* pass_idx, const double* a, const double* sigma, double* y,
-                               cudaStream_t stream);
+                               cudaStream_t stream, int rows = -1);
 cudaError_t transpose_square(const double* in, std::size_t ld_in, double* out, std::size_t ld_out, int n,
                              cudaStream_t stream);
 
@@ -185,6 +185,11 @@ cudaError_t secular_roots_gpu(const double* lam, const double* z, int k, double 
                               int* status, cudaStream_t stream);
 cudaError_t normalisers_gpu(const double* lam, const double* z, int m, const double* mu, int k, double* a,
                             int* status, cudaStream_t stream);
+/// Column signs of the materialised basis (spectral.hpp:30-37): for each of
+/// `cols` rows of xt (row s = column s of X, n entries, stride ld), +1 / -1
+/// making the largest-|.| entry positive, ties within 1e-12 relative to the
+/// lowest index; written to sign[s].
+cudaError_t column_signs_gpu(const double* xt, std::size_t ld, int n, int cols, double* sign, cudaStream_t stream);
 
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);

@@ -56,9 +56,16 @@ __device__ __forceinline__ double odd_ext(const double* h, const double* wgt, in
     return -(wgt ? wgt[k] * h[k] : h[k]);
 }
 
-__device__ __forceinline__ void pack_dst1(double2* cb, const double* h, const double* __restrict__ wgt, int n) {
+/// (stored at the bit-reversed positions the FFT's first pass reads)
+__device__ __forceinline__ void pack_dst1(double2* cb, const double* h, const double* __restrict__ wgt, int n,
+                                          int logn) {
     for (int j = threadIdx.x; j < n; j += blockDim.x)
-        cb[pad8(j)] = make_double2(odd_ext(h, wgt, 2 * j, n), odd_ext(h, wgt, 2 * j + 1, n));
+        cb[pad8(static_cast<int>(bit_reverse(static_cast<unsigned>(j), logn)))] =
+            make_double2(odd_ext(h, wgt, 2 * j, n), odd_ext(h, wgt, 2 * j + 1, n));
+}
+
+__device__ __forceinline__ int brev(int i, int bits) {
+    return static_cast<int>(bit_reverse(static_cast<unsigned>(i), bits));
 }
 
 /// c_k and c_{n-k} of DST-I (c_k = 2 sum_j h_j sin(pi j k / n)) from the
@@ -198,11 +205,11 @@ nfst_forward_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
         const double v = x[j];
         bad |= !isfinite(v);
         const int p = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
-        reinterpret_cast<double*>(&cb[pad8(p >> 1)])[p & 1] = v;
+        reinterpret_cast<double*>(&cb[pad8(brev(p >> 1, logn - 1))])[p & 1] = v;
     }
     if (bad) atomicOr(flag, 1);
     __syncthreads();
-    fft_inplace<double, false>(cb, N, logn - 1, P.tw2n, 2);
+    fft_from_bitreversed<double, false>(cb, N, logn - 1, P.tw2n, 2);
     {
         const double scale = sqrt(2.0 / n), dc_scale = 1.0 / sqrt(static_cast<double>(n));
         const double2* tw = reinterpret_cast<const double2*>(P.tw2n);
@@ -233,7 +240,7 @@ nfst_forward_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
     double ext = 0.0;
     if (P.ext_slot >= 0)
         for (int j = tid; j < n; j += nt) ext += __ldg(P.ez + j) * rb[j];
-    pack_dst1(cb, rb, P.hz, n);
+    pack_dst1(cb, rb, P.hz, n, logn);
     if (P.ext_slot >= 0) {
         ext = block_sum(ext, red); // includes the barrier before the FFT
         if (tid == 0) o[P.ext_slot] = P.ext_scale * ext;
@@ -242,7 +249,7 @@ nfst_forward_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
     }
 
     // 3. c = DST-I(h); v = c / phi_hat
-    fft_inplace<double, false>(cb, n, logn, P.tw2n, 1);
+    fft_from_bitreversed<double, false>(cb, n, logn, P.tw2n, 1);
     unpack_dst1(cb, P.tw2n, P.inv_phi, rb, n);
     __syncthreads();
 
@@ -264,11 +271,11 @@ nfst_forward_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
             const double sr = sp.x, si = -sp.y; // e^{+2 pi i k / n}
             const double dr = v1r - v2r, di = v1i - v2i;
             const double qr = sr * dr - si * di, qi = sr * di + si * dr;
-            cb[pad8(k)] = make_double2(0.5 * (v1r + v2r - qi), 0.5 * (v1i + v2i + qr));
+            cb[pad8(brev(k, logn - 1))] = make_double2(0.5 * (v1r + v2r - qi), 0.5 * (v1i + v2i + qr));
         }
     }
     __syncthreads();
-    fft_inplace<double, true>(cb, N, logn - 1, P.tw2n, 2);
+    fft_from_bitreversed<double, true>(cb, N, logn - 1, P.tw2n, 2);
     for (int j = tid; j < n; j += nt) {
         const int p = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
         const double2 w = cb[pad8(p >> 1)];
@@ -286,9 +293,9 @@ nfst_forward_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
     __syncthreads();
 
     // 6. even grid points: y_{2k} = DST-I(v)_k
-    pack_dst1(cb, rb, nullptr, n);
+    pack_dst1(cb, rb, nullptr, n, logn);
     __syncthreads();
-    fft_inplace<double, false>(cb, n, logn, P.tw2n, 1);
+    fft_from_bitreversed<double, false>(cb, n, logn, P.tw2n, 1);
     unpack_dst1(cb, P.tw2n, nullptr, rb, n);
     __syncthreads();
 
@@ -342,9 +349,9 @@ nfst_inverse_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
         rb[n - k] -= rb[n + k];
     }
     __syncthreads();
-    pack_dst1(cb, rb, nullptr, n);
+    pack_dst1(cb, rb, nullptr, n, logn);
     __syncthreads();
-    fft_inplace<double, false>(cb, n, logn, P.tw2n, 1);
+    fft_from_bitreversed<double, false>(cb, n, logn, P.tw2n, 1);
     unpack_dst1(cb, P.tw2n, nullptr, rb, n);
     __syncthreads();
 
@@ -362,10 +369,10 @@ nfst_inverse_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
         const double v = (j & 1) ? -fo[j] : fo[j];
         const int q = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
         // the n/2-point FFT row (cb head) and fo (cb tail) are disjoint
-        reinterpret_cast<double*>(&cb[pad8(q >> 1)])[q & 1] = v;
+        reinterpret_cast<double*>(&cb[pad8(brev(q >> 1, logn - 1))])[q & 1] = v;
     }
     __syncthreads();
-    fft_inplace<double, false>(cb, N, logn - 1, P.tw2n, 2);
+    fft_from_bitreversed<double, false>(cb, N, logn - 1, P.tw2n, 2);
     // b_k = inv_phi_k (c_k / 2 + Y_{n-k}); Y_q for q = 1..n-1 from the split
     for (int k = tid; k < N; k += nt) {
         double yk, ynk; // Y_k, Y_{n-k}
@@ -392,12 +399,12 @@ nfst_inverse_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
     __syncthreads();
 
     // 3. g = DST-I(b); d = z (ext + d0 e_0 - w g) + pass-through, into rb
-    pack_dst1(cb, rb, nullptr, n);
+    pack_dst1(cb, rb, nullptr, n, logn);
     double d0 = 0.0;
     for (int r = tid; r < P.R; r += nt) d0 += __ldg(P.t_cb + r) * prow[__ldg(P.t_slot + r)];
     d0 = block_sum(d0, red); // barrier: the pack is complete
     const double pe = P.ext_slot >= 0 ? P.ext_scale * prow[P.ext_slot] : 0.0;
-    fft_inplace<double, false>(cb, n, logn, P.tw2n, 1);
+    fft_from_bitreversed<double, false>(cb, n, logn, P.tw2n, 1);
     for (int k = tid; k <= N; k += nt) {
         double gk, gnk;
         if (k == 0) {
@@ -434,11 +441,11 @@ nfst_inverse_kernel(const double* __restrict__ in, double* __restrict__ out, Fas
             const double sr = sp.x, si = -sp.y;
             const double dr = v1r - v2r, di = v1i - v2i;
             const double qr = sr * dr - si * di, qi = sr * di + si * dr;
-            cb[pad8(k)] = make_double2(0.5 * (v1r + v2r - qi), 0.5 * (v1i + v2i + qr));
+            cb[pad8(brev(k, logn - 1))] = make_double2(0.5 * (v1r + v2r - qi), 0.5 * (v1i + v2i + qr));
         }
     }
     __syncthreads();
-    fft_inplace<double, true>(cb, N, logn - 1, P.tw2n, 2);
+    fft_from_bitreversed<double, true>(cb, N, logn - 1, P.tw2n, 2);
     for (int j = tid; j < n; j += nt) {
         const int q = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
         const double2 w = cb[pad8(q >> 1)];

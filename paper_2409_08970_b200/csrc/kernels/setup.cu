@@ -100,7 +100,47 @@ __global__ void normalisers_kernel(const double* __restrict__ lam, const double*
     a[i] = 1.0 / sqrt(s);
 }
 
+/// One CTA per column: peak = max |x_i|, then the lowest i with |x_i| >=
+/// peak (1 - 1e-12) (host/setup.hpp sign_of_column).
+__global__ void column_signs_kernel(const double* __restrict__ xt, std::size_t ld, int n, double* __restrict__ sign) {
+    __shared__ double red[32];
+    __shared__ int ired[32];
+    const double* x = xt + static_cast<std::size_t>(blockIdx.x) * ld;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double peak = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) peak = fmax(peak, fabs(x[i]));
+    for (int o = 16; o > 0; o >>= 1) peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+    if (lane == 0) red[warp] = peak;
+    __syncthreads();
+    peak = 0.0;
+    for (int w = 0; w < nw; ++w) peak = fmax(peak, red[w]);
+    if (peak == 0.0) {
+        if (threadIdx.x == 0) sign[blockIdx.x] = 1.0;
+        return;
+    }
+    const double thr = peak * (1.0 - 1e-12);
+    int first = n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if (fabs(x[i]) >= thr) {
+            first = i;
+            break;
+        }
+    for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    if (lane == 0) ired[warp] = first;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < nw; ++w) first = min(first, ired[w]);
+        sign[blockIdx.x] = (first < n && x[first] < 0.0) ? -1.0 : 1.0;
+    }
+}
+
 } // namespace
+
+cudaError_t column_signs_gpu(const double* xt, std::size_t ld, int n, int cols, double* sign, cudaStream_t stream) {
+    if (cols <= 0) return cudaSuccess;
+    column_signs_kernel<<<cols, 256, 0, stream>>>(xt, ld, n, sign);
+    return cudaGetLastError();
+}
 
 cudaError_t secular_roots_gpu(const double* lam, const double* z, int k, double rho, double zz, double* mu,
                               int* status, cudaStream_t stream) {

@@ -677,7 +677,8 @@ def test_gpu_setup_bit_identical(P, torch, monkeypatch, case):
     """The secular roots and normalisers computed on the GPU (setup.cu,
     -fmad=false, the host restatement's operations in the same order) are
     bit-identical to the host setup (itself bit-identical to the reference:
-    tests/test_host_setup.py), and so are the slot map and the signs."""
+    tests/test_host_setup.py); the column signs (batched DCT-III of the
+    unsigned basis on the GPU, then the sign rule) and the slot map agree."""
     if case[0] == "c":
         cfg = O.config(int(case[1]))
         n, u = cfg.n, cfg.updates[0]
@@ -690,7 +691,7 @@ def test_gpu_setup_bit_identical(P, torch, monkeypatch, case):
     P.profile_enable(True)
     P.DctPlusPlan(n, upd(P, u), 1e-12, device=0)
     P.profile_enable(False)
-    assert "secular_roots" in P.profile_summary()
+    assert {"secular_roots", "normalisers", "column_signs"} <= set(P.profile_summary())
     host = P.DctPlusPlan(n, upd(P, u), 1e-12, device=-1)
     a, b = gpu.setup(), host.setup()
     for k in b:

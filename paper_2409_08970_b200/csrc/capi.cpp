@@ -1145,14 +1145,16 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
 /// The reference's forward() IS the NFST approximation, so where the two
 /// differ by more than 1e-11 (a tenth of the fp64 parity tolerance: at n =
 /// 1024, self-loop 0.5, they differ by 5e-9) the NFST route is the only one
-/// that reproduces the reference and is kept.  Otherwise the faster one is:
-/// the NFST route from DCTP_FAST_MIN_N (default 2048; tools/route_sweep.py:
-/// 1.66 vs 2.11 ms at n = 2048, 1.27 vs 1.08 ms at n = 1024).
+/// that reproduces the reference and is kept.  Otherwise the faster one is
+/// (tools/route_sweep.py, fully kept plans): the NFST route from
+/// DCTP_FAST_MIN_N (default 1024: 0.91 vs 1.08 ms against the dense route at
+/// n = 1024, 1.12 vs 2.11 ms at n = 2048) unless the plan has the folded or
+/// fused route, which beat it 2-3x at every size.
 static void decide_fast_route(dctp_plan& p) {
     if (!p.fs.on) return;
     static const std::size_t min_n = [] {
         const char* m = std::getenv("DCTP_FAST_MIN_N");
-        return m ? static_cast<std::size_t>(std::atoll(m)) : std::size_t{2048};
+        return m ? static_cast<std::size_t>(std::atoll(m)) : std::size_t{1024};
     }();
     const std::size_t n = p.st.n, rows = 16;
     std::vector<double> h(rows * n), a(rows * n), b(rows * n);
@@ -1178,7 +1180,7 @@ static void decide_fast_route(dctp_plan& p) {
         gap = std::max(gap, den > 0.0 ? num / den : num);
     }
     p.fs.probe_gap = gap;
-    p.fs.preferred = !(gap <= 1e-11) || n >= min_n;
+    p.fs.preferred = !(gap <= 1e-11) || (n >= min_n && !p.fd.on && !p.small);
 }
 
 static void sync_check(int device, int* flag, cudaStream_t s) {

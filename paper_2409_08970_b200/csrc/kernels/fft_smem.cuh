@@ -25,10 +25,10 @@ __device__ __forceinline__ void dit_group_pass(const cplx_t<T>* src, cplx_t<T>* 
                                                int s0, const T* __restrict__ tw, int tw_extra = 0) {
     constexpr int G = 1 << Q;
     const int h0 = 1 << s0;
-    const int groups = N >> Q;
+    const int lg = logN - Q; // log2 of the groups per row
     const int ld = padded_len(N);
-    for (int t = threadIdx.x; t < rows * groups; t += blockDim.x) {
-        const int row = t / groups, g = t - row * groups;
+    for (int t = threadIdx.x; t < (rows << lg); t += blockDim.x) {
+        const int row = t >> lg, g = t & ((1 << lg) - 1);
         const int j = g & (h0 - 1), base = (g >> s0) * (h0 << Q) + j;
         cplx_t<T> v[G];
 #pragma unroll
@@ -39,12 +39,25 @@ __device__ __forceinline__ void dit_group_pass(const cplx_t<T>* src, cplx_t<T>* 
         for (int tt = 0; tt < Q; ++tt) {
             const int span = 1 << tt;
             const int shift = logN - (s0 + tt + 1) + tw_extra; // twiddle step N / (2 * half)
+            // stage tt needs w_q = W^((j + q h0) 2^shift), q < span; since
+            // h0 2^shift is a quarter turn's multiple, w_{q + span/2} = -i w_q
+            // (conjugated for the inverse): exact, so only the first half of
+            // each stage's twiddles is loaded
+            cplx_t<T> w[G / 2];
+#pragma unroll
+            for (int q = 0; q < span; ++q) {
+                if (span >= 2 && q >= span / 2) {
+                    const cplx_t<T> u = w[q - span / 2];
+                    w[q] = Inverse ? cplx_t<T>{-u.y, u.x} : cplx_t<T>{u.y, -u.x};
+                } else {
+                    const cplx_t<T> u = __ldg(reinterpret_cast<const cplx_t<T>*>(tw) + ((j + q * h0) << shift));
+                    w[q] = {u.x, Inverse ? -u.y : u.y};
+                }
+            }
 #pragma unroll
             for (int m = 0; m < G; ++m) {
                 if (m & span) continue;
-                const int widx = (j + (m & (span - 1)) * h0) << shift;
-                const cplx_t<T> w = __ldg(reinterpret_cast<const cplx_t<T>*>(tw) + widx); // one 16/8-byte load
-                const T wr = w.x, wi = Inverse ? -w.y : w.y;
+                const T wr = w[m & (span - 1)].x, wi = w[m & (span - 1)].y;
                 const cplx_t<T> a = v[m], b = v[m + span];
                 const T br = b.x * wr - b.y * wi, bi = b.x * wi + b.y * wr;
                 v[m] = {a.x + br, a.y + bi};

@@ -6,7 +6,7 @@ out=gpurun_out/final
 mkdir -p $out
 python bench.py > $out/bench_final.json 2> $out/bench_final.err
 python bench.py --impl reference > $out/bench_ref_final.json 2> $out/bench_ref_final.err
-for c in 1 3 4 5 6; do
+for c in 1 3 4 5 6 7 8; do
     python bench.py --config $c --steps 20 --warmup 5 > $out/bench_c$c.json 2> $out/bench_c$c.err
 done
 for f in $out/*.json; do

@@ -1436,6 +1436,7 @@ struct dctp_ensemble {
     int n_emit = 0, max_rows = 0, max_cols = 0;
     // fp32 dense route (n <= 256): G = [D^T | X_1 | ... | X_K], n x (K+1) n
     std::size_t gmat32 = 0;
+    std::size_t gt_hi = 0, gt_lo = 0; // G^T split for the tcgen05 3xTF32 GEMM, (K+1) n x n
     bool dense32 = false;
     // pruned mode (c_p < n): [UL_r; HL_r] = T_r[:, 0:c_p] per member, K x n x c_p
     std::size_t prune64 = 0, prune32 = 0;
@@ -1493,6 +1494,19 @@ static void ensemble_forward_full(const dctp_ensemble* e, const T* in, T* out, s
         tw = twiddles_at<double>(e->blob, e->tw64);
     }
     if constexpr (f32) {
+        // the tensor-core GEMM (tcgen05 kind::tf32, 3xTF32) unless DCTP_TC32=0
+        const char* tc = std::getenv("DCTP_TC32");
+        if (e->dense32 && !(tc && tc[0] == '0') &&
+            dctp::dev::tc_sgemm3_supported(static_cast<int>(n), static_cast<int>(ld), static_cast<int>(n),
+                                           static_cast<int>(n), ld, in, at<float>(e->blob, e->gt_hi),
+                                           at<float>(e->blob, e->gt_lo), out)) {
+            cuda_check(DCTP_LAUNCH("progressive_tc32", s,
+                                   dctp::dev::tc_sgemm3(in, static_cast<int>(n), at<float>(e->blob, e->gt_hi),
+                                                        at<float>(e->blob, e->gt_lo), static_cast<int>(n), out, ld,
+                                                        batch, static_cast<int>(ld), static_cast<int>(n), e->flag, s)),
+                       "progressive tcgen05 kernel");
+            return;
+        }
         if (e->dense32 &&
             dctp::dev::sgemm_rows_supported(static_cast<int>(n), static_cast<int>(ld), static_cast<int>(n),
                                             static_cast<int>(ld), ld, in, at<float>(e->blob, e->gmat32), out)) {
@@ -1784,21 +1798,38 @@ int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is,
         // set 0 the orthonormal DCT-II matrix, so out = x * [D^T | X_1 | ... | X_K]
         if (n <= 256 && n % 16 == 0 && device >= 0) {
             const std::size_t cols = (k + 1) * n;
-            std::vector<float> g(n * cols);
+            std::vector<double> gd(n * cols);
             const long double pi = 3.141592653589793238462643383279502884L;
             for (std::size_t i = 0; i < n; ++i)
                 for (std::size_t j = 0; j < n; ++j) {
                     const long double c = j == 0 ? std::sqrt(1.0L / n) : std::sqrt(2.0L / n);
-                    g[i * cols + j] = static_cast<float>(c * std::cos(pi * j * (2 * i + 1) / (2.0L * n)));
+                    gd[i * cols + j] = static_cast<double>(c * std::cos(pi * j * (2 * i + 1) / (2.0L * n)));
                 }
             std::vector<double> xb(n * n);
             for (std::size_t r = 0; r < k; ++r) {
                 plan_basis(e->members[r]->st, xb.data());
                 for (std::size_t i = 0; i < n; ++i)
-                    for (std::size_t sl = 0; sl < n; ++sl)
-                        g[i * cols + (r + 1) * n + sl] = static_cast<float>(xb[i * n + sl]);
+                    for (std::size_t sl = 0; sl < n; ++sl) gd[i * cols + (r + 1) * n + sl] = xb[i * n + sl];
             }
+            std::vector<float> g(n * cols), bt_hi(cols * n), bt_lo(cols * n);
+            for (std::size_t i = 0; i < n; ++i)
+                for (std::size_t c = 0; c < cols; ++c) {
+                    const double v = gd[i * cols + c];
+                    g[i * cols + c] = static_cast<float>(v);
+                    // 3xTF32 operand split of G^T: the TF32 head (round to nearest,
+                    // ties away, like cvt.rna.tf32.f32) and the fp32 tail
+                    std::uint32_t bits;
+                    const float f = static_cast<float>(v);
+                    std::memcpy(&bits, &f, 4);
+                    bits = (bits + 0x1000u) & 0xffffe000u;
+                    float hi;
+                    std::memcpy(&hi, &bits, 4);
+                    bt_hi[c * n + i] = hi;
+                    bt_lo[c * n + i] = static_cast<float>(v - static_cast<double>(hi));
+                }
             e->gmat32 = blob.add(g);
+            e->gt_hi = blob.add(bt_hi);
+            e->gt_lo = blob.add(bt_lo);
             e->dense32 = true;
         }
         if (device < 0) {

@@ -1,0 +1,219 @@
+// fp32 GEMM on the 5th-generation tensor cores (tcgen05, kind::tf32) with the
+// 3xTF32 split, sm_100a:  C[M x N] = A[M x K] * B[K x N], A row-major fp32,
+// B given transposed and pre-split (bt_hi + bt_lo, N x K, K contiguous).
+//
+// Used for the fp32 progressive ensembles (C4: forward_all = x [D^T | X_1 ..
+// X_K], fast_transform.hpp:396-403 with c_p = n), where the FFMA SGEMM is
+// FMA-bound at ~67% of the CUDA-core peak.  Each operand is split into a
+// TF32 head and an fp32 tail, a = a_hi + a_lo, and the product accumulates
+// a_hi b_hi + a_hi b_lo + a_lo b_hi in fp32 in TMEM (the a_lo b_lo term is
+// below fp32 rounding): ~fp32 accuracy, against the 1e-4 fp32 tolerance.
+//
+// CTA tile 128 x 256, K in 32-wide chunks (one 128-byte swizzle atom of fp32):
+// A chunks are split in registers and stored hi / lo into SWIZZLE_128B
+// K-major shared memory; B chunks (hi, lo) arrive by cp.async into the same
+// layout.  One elected thread issues the 4 x 3 tcgen05.mma of a chunk and
+// commits them to an mbarrier; the accumulator (128 lanes x 256 fp32
+// columns) lives in TMEM and leaves through tcgen05.ld, one row per thread,
+// as full 32-byte sectors.  96 KB of shared memory: two CTAs per SM, so one
+// CTA's epilogue overlaps the other's loads and MMAs.
+#include <cstdint>
+
+#include "kernels/common.cuh"
+#include "kernels/launch.hpp"
+
+namespace dctp::dev {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 32;
+constexpr int kThreads = 128;
+constexpr uint32_t kTmemCols = 256;
+constexpr int kABytes = BM * BK * 4, kBBytes = BN * BK * 4;          // 16 KB, 32 KB
+constexpr int kSmem = 2 * kABytes + 2 * kBBytes + 1024 + 64;           // + alignment slack, barrier, tmem slot
+
+/// Byte offset of (row r, 16-byte chunk c) in a K-major SWIZZLE_128B tile
+/// whose rows are one 128-byte atom wide (8-row groups of 1024 bytes).
+__device__ __forceinline__ uint32_t sw128(int r, int c) {
+    return static_cast<uint32_t>((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
+
+/// Shared-memory matrix descriptor (tcgen05): K-major, SWIZZLE_128B, SBO =
+/// 1024 bytes between 8-row groups, LBO unused (1), version 1.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+    d |= static_cast<uint64_t>(1) << 16;             // leading byte offset (ignored for swizzled K-major)
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;     // stride byte offset
+    d |= static_cast<uint64_t>(1) << 46;             // descriptor version (sm_100)
+    d |= static_cast<uint64_t>(2) << 61;             // SWIZZLE_128B
+    return d;
+}
+
+/// Instruction descriptor: D fp32, A and B tf32, both K-major, M = 128, N = 256.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                            (static_cast<uint32_t>(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     ptx::smem_addr(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ float tf32_head(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(g), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__ bt_hi,
+                 const float* __restrict__ bt_lo, int ldb, float* __restrict__ C, std::size_t ldc, std::size_t M,
+                 int N, int K, int* flag) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment of the swizzle atoms
+    const uint32_t raw = ptx::smem_addr(smem_raw);
+    unsigned char* base = smem_raw + ((1024 - (raw & 1023)) & 1023);
+    unsigned char* sa_hi = base;
+    unsigned char* sa_lo = base + kABytes;
+    unsigned char* sb_hi = base + 2 * kABytes;
+    unsigned char* sb_lo = base + 2 * kABytes + kBBytes;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + 2 * kABytes + 2 * kBBytes);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const std::size_t m0 = static_cast<std::size_t>(blockIdx.x) * BM;
+    const int n0 = blockIdx.y * BN;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         ptx::smem_addr(tmem_slot)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (tid == 0) {
+        ptx::mbar_init(bar, 1);
+        ptx::fence_mbar_init();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    bool bad = false;
+    const int nchunks = (K + BK - 1) / BK;
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int k0 = ch * BK;
+        // B (hi, lo): 256 rows x 8 chunks of 16 bytes each, straight copies
+        for (int i = tid; i < BN * (BK / 4); i += kThreads) {
+            const int r = i >> 3, c = i & 7, n = n0 + r, k = k0 + 4 * c;
+            const int bytes = (n < N && k < K) ? 16 : 0;
+            const std::size_t off = bytes ? static_cast<std::size_t>(n) * ldb + k : 0;
+            cp_async16(ptx::smem_addr(sb_hi) + sw128(r, c), bt_hi + off, bytes);
+            cp_async16(ptx::smem_addr(sb_lo) + sw128(r, c), bt_lo + off, bytes);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        // A: 128 rows x 8 chunks, split into the TF32 head and the fp32 tail
+        for (int i = tid; i < BM * (BK / 4); i += kThreads) {
+            const int r = i >> 3, c = i & 7, k = k0 + 4 * c;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (m0 + r < M && k < K) v = *reinterpret_cast<const float4*>(A + (m0 + r) * lda + k);
+            const float4 h = make_float4(tf32_head(v.x), tf32_head(v.y), tf32_head(v.z), tf32_head(v.w));
+            const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+            *reinterpret_cast<float4*>(sa_hi + sw128(r, c)) = h;
+            *reinterpret_cast<float4*>(sa_lo + sw128(r, c)) = l;
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        ptx::fence_proxy_async(); // generic-proxy smem writes -> visible to the tensor core
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if (tid == 0) {
+            const uint32_t ah = ptx::smem_addr(sa_hi), al = ptx::smem_addr(sa_lo);
+            const uint32_t bh = ptx::smem_addr(sb_hi), bl = ptx::smem_addr(sb_lo);
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) { // 8 tf32 = 32 bytes per MMA step along K
+                const uint32_t o = 32u * kk;
+                const uint32_t acc0 = (ch > 0 || kk > 0) ? 1u : 0u;
+                mma_tf32(tmem, smem_desc(ah + o), smem_desc(bh + o), acc0);
+                mma_tf32(tmem, smem_desc(ah + o), smem_desc(bl + o), 1u);
+                mma_tf32(tmem, smem_desc(al + o), smem_desc(bh + o), 1u);
+            }
+            mma_commit(bar);
+        }
+        ptx::mbar_wait(bar, static_cast<uint32_t>(ch & 1)); // MMAs done: smem reusable / TMEM final
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    }
+
+    // epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w + 31
+    const std::size_t row = m0 + 32 * warp + lane;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * warp) << 16) + static_cast<uint32_t>(c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        const int n = n0 + c0;
+        if (n == 0 && row < M) bad |= !isfinite(__uint_as_float(v[0])); // the DC coefficient
+        if (row < M && n < N) {
+            float* dst = C + row * ldc + n;
+            if (n + 32 <= N) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    reinterpret_cast<float4*>(dst)[q] =
+                        make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                    __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+            } else {
+#pragma unroll
+                for (int q = 0; q < 32; ++q)
+                    if (q < N - n) dst[q] = __uint_as_float(v[q]);
+            }
+        }
+    }
+    if (bad) atomicOr(flag, 1);
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols)
+                     : "memory");
+}
+
+} // namespace
+
+bool tc_sgemm3_supported(int K, int N, int lda, int ldb, std::size_t ldc, const void* A, const void* Bh,
+                         const void* Bl, const void* C) {
+    const auto al = [](const void* p) { return reinterpret_cast<std::uintptr_t>(p) % 16 == 0; };
+    return K > 0 && N > 0 && K % 4 == 0 && lda % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 && al(A) && al(Bh) &&
+           al(Bl) && al(C);
+}
+
+cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* bt_lo, int ldb, float* C,
+                      std::size_t ldc, std::size_t M, int N, int K, int* flag, cudaStream_t stream) {
+    if (M == 0 || N == 0) return cudaSuccess;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(tc_sgemm3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (attr != cudaSuccess) return attr;
+    const dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), static_cast<unsigned>((N + BN - 1) / BN));
+    tc_sgemm3_kernel<<<grid, kThreads, kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag);
+    return cudaGetLastError();
+}
+
+} // namespace dctp::dev

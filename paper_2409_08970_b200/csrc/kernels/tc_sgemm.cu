@@ -9,14 +9,15 @@
 // a_hi b_hi + a_hi b_lo + a_lo b_hi in fp32 in TMEM (the a_lo b_lo term is
 // below fp32 rounding): ~fp32 accuracy, against the 1e-4 fp32 tolerance.
 //
-// CTA tile 128 x 256, K in 32-wide chunks (one 128-byte swizzle atom of fp32):
-// A chunks are split in registers and stored hi / lo into SWIZZLE_128B
-// K-major shared memory; B chunks (hi, lo) arrive by cp.async into the same
-// layout.  One elected thread issues the 4 x 3 tcgen05.mma of a chunk and
-// commits them to an mbarrier; the accumulator (128 lanes x 256 fp32
-// columns) lives in TMEM and leaves through tcgen05.ld, one row per thread,
-// as full 32-byte sectors.  96 KB of shared memory: two CTAs per SM, so one
-// CTA's epilogue overlaps the other's loads and MMAs.
+// CTA tile 128 x 256, K in 16-wide chunks (one 64-byte swizzle atom of fp32)
+// through a two-stage ring: A chunks are split in registers and stored hi /
+// lo into SWIZZLE_64B K-major shared memory, B chunks (hi, lo) arrive by
+// cp.async into the same layout, and chunk k + 1 loads while the tensor core
+// runs chunk k.  One thread issues the 2 x 3 tcgen05.mma of a chunk and
+// commits them to the stage's mbarrier; the accumulator (128 lanes x 256
+// fp32 columns) lives in TMEM and leaves through tcgen05.ld, one row per
+// thread, as full 32-byte sectors.  96 KB of shared memory: two CTAs per SM,
+// so one CTA's epilogue overlaps the other's loads and MMAs.
 #include <cstdint>
 
 #include "kernels/common.cuh"
@@ -25,27 +26,29 @@
 namespace dctp::dev {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 32;
+constexpr int BM = 128, BN = 256, BK = 16, kStages = 2;
 constexpr int kThreads = 128;
 constexpr uint32_t kTmemCols = 256;
-constexpr int kABytes = BM * BK * 4, kBBytes = BN * BK * 4;          // 16 KB, 32 KB
-constexpr int kSmem = 2 * kABytes + 2 * kBBytes + 1024 + 64;           // + alignment slack, barrier, tmem slot
+constexpr int kABytes = BM * BK * 4, kBBytes = BN * BK * 4;          // 8 KB, 16 KB
+constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;                 // A hi, A lo, B hi, B lo: 48 KB
+constexpr int kSmem = kStages * kStageBytes + 1024 + 64;               // + alignment slack, barriers, tmem slot
 
-/// Byte offset of (row r, 16-byte chunk c) in a K-major SWIZZLE_128B tile
-/// whose rows are one 128-byte atom wide (8-row groups of 1024 bytes).
-__device__ __forceinline__ uint32_t sw128(int r, int c) {
-    return static_cast<uint32_t>((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+/// Byte offset of (row r, 16-byte chunk c) in a K-major SWIZZLE_64B tile whose
+/// rows are one 64-byte atom wide (16 fp32; 8-row groups of 512 bytes):
+/// Swizzle<2,4,3>, the chunk index XORed with address bits 7-8.
+__device__ __forceinline__ uint32_t sw64(int r, int c) {
+    return static_cast<uint32_t>(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
 }
 
-/// Shared-memory matrix descriptor (tcgen05): K-major, SWIZZLE_128B, SBO =
-/// 1024 bytes between 8-row groups, LBO unused (1), version 1.
+/// Shared-memory matrix descriptor (tcgen05): K-major, SWIZZLE_64B, SBO = 512
+/// bytes between 8-row groups, LBO unused (1), version 1.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
     d |= static_cast<uint64_t>(1) << 16;             // leading byte offset (ignored for swizzled K-major)
-    d |= static_cast<uint64_t>(1024 >> 4) << 32;     // stride byte offset
+    d |= static_cast<uint64_t>(512 >> 4) << 32;      // stride byte offset
     d |= static_cast<uint64_t>(1) << 46;             // descriptor version (sm_100)
-    d |= static_cast<uint64_t>(2) << 61;             // SWIZZLE_128B
+    d |= static_cast<uint64_t>(4) << 61;             // SWIZZLE_64B
     return d;
 }
 
@@ -84,12 +87,9 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
     // 1024-byte alignment of the swizzle atoms
     const uint32_t raw = ptx::smem_addr(smem_raw);
     unsigned char* base = smem_raw + ((1024 - (raw & 1023)) & 1023);
-    unsigned char* sa_hi = base;
-    unsigned char* sa_lo = base + kABytes;
-    unsigned char* sb_hi = base + 2 * kABytes;
-    unsigned char* sb_lo = base + 2 * kABytes + kBBytes;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(base + 2 * kABytes + 2 * kBBytes);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + kStages * kStageBytes); // one per stage: MMAs done
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + kStages);
+    const uint32_t sbase = ptx::smem_addr(base);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const std::size_t m0 = static_cast<std::size_t>(blockIdx.x) * BM;
@@ -103,7 +103,7 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     if (tid == 0) {
-        ptx::mbar_init(bar, 1);
+        for (int i = 0; i < kStages; ++i) ptx::mbar_init(bar + i, 1);
         ptx::fence_mbar_init();
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -111,36 +111,60 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
-    bool bad = false;
-    const int nchunks = (K + BK - 1) / BK;
-    for (int ch = 0; ch < nchunks; ++ch) {
+    // stage st: A hi, A lo, B hi, B lo.  A is fetched into registers one
+    // chunk ahead (its global latency hides behind the barrier and the MMA
+    // issue), then split and stored; B goes straight in by cp.async.
+    constexpr int kAV = BM * (BK / 4) / kThreads; // float4 of A per thread per chunk
+    float4 areg[kAV];
+    auto fetch_a = [&](int ch) {
         const int k0 = ch * BK;
-        // B (hi, lo): 256 rows x 8 chunks of 16 bytes each, straight copies
-        for (int i = tid; i < BN * (BK / 4); i += kThreads) {
-            const int r = i >> 3, c = i & 7, n = n0 + r, k = k0 + 4 * c;
-            const int bytes = (n < N && k < K) ? 16 : 0;
-            const std::size_t off = bytes ? static_cast<std::size_t>(n) * ldb + k : 0;
-            cp_async16(ptx::smem_addr(sb_hi) + sw128(r, c), bt_hi + off, bytes);
-            cp_async16(ptx::smem_addr(sb_lo) + sw128(r, c), bt_lo + off, bytes);
+#pragma unroll
+        for (int u = 0; u < kAV; ++u) {
+            const int i = tid + u * kThreads, r = i >> 2, c = i & 3, k = k0 + 4 * c;
+            areg[u] = (m0 + r < M && k < K) ? *reinterpret_cast<const float4*>(A + (m0 + r) * lda + k)
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-        // A: 128 rows x 8 chunks, split into the TF32 head and the fp32 tail
-        for (int i = tid; i < BM * (BK / 4); i += kThreads) {
-            const int r = i >> 3, c = i & 7, k = k0 + 4 * c;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (m0 + r < M && k < K) v = *reinterpret_cast<const float4*>(A + (m0 + r) * lda + k);
+    };
+    auto store_a = [&](int st) {
+        unsigned char* g0 = base + st * kStageBytes;
+#pragma unroll
+        for (int u = 0; u < kAV; ++u) {
+            const int i = tid + u * kThreads, r = i >> 2, c = i & 3;
+            const float4 v = areg[u];
             const float4 h = make_float4(tf32_head(v.x), tf32_head(v.y), tf32_head(v.z), tf32_head(v.w));
             const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-            *reinterpret_cast<float4*>(sa_hi + sw128(r, c)) = h;
-            *reinterpret_cast<float4*>(sa_lo + sw128(r, c)) = l;
+            *reinterpret_cast<float4*>(g0 + sw64(r, c)) = h;
+            *reinterpret_cast<float4*>(g0 + kABytes + sw64(r, c)) = l;
         }
+    };
+    auto load_b = [&](int ch, int st) {
+        const int k0 = ch * BK;
+        const uint32_t s0 = sbase + st * kStageBytes;
+        for (int i = tid; i < BN * (BK / 4); i += kThreads) {
+            const int r = i >> 2, c = i & 3, n = n0 + r, k = k0 + 4 * c;
+            const int bytes = (n < N && k < K) ? 16 : 0;
+            const std::size_t off = bytes ? static_cast<std::size_t>(n) * ldb + k : 0;
+            cp_async16(s0 + 2 * kABytes + sw64(r, c), bt_hi + off, bytes);
+            cp_async16(s0 + 2 * kABytes + kBBytes + sw64(r, c), bt_lo + off, bytes);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+
+    const int nchunks = (K + BK - 1) / BK;
+    uint32_t phases = 0u; // bit st: parity of stage st's next MMA completion
+    fetch_a(0);
+    load_b(0, 0);
+    store_a(0);
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int st = ch % kStages;
+        if (ch + 1 < nchunks) fetch_a(ch + 1);
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         ptx::fence_proxy_async(); // generic-proxy smem writes -> visible to the tensor core
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (tid == 0) {
-            const uint32_t ah = ptx::smem_addr(sa_hi), al = ptx::smem_addr(sa_lo);
-            const uint32_t bh = ptx::smem_addr(sb_hi), bl = ptx::smem_addr(sb_lo);
+            const uint32_t s0 = sbase + st * kStageBytes;
+            const uint32_t ah = s0, al = s0 + kABytes, bh = s0 + 2 * kABytes, bl = s0 + 2 * kABytes + kBBytes;
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) { // 8 tf32 = 32 bytes per MMA step along K
                 const uint32_t o = 32u * kk;
@@ -149,13 +173,28 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
                 mma_tf32(tmem, smem_desc(ah + o), smem_desc(bl + o), 1u);
                 mma_tf32(tmem, smem_desc(al + o), smem_desc(bh + o), 1u);
             }
-            mma_commit(bar);
+            mma_commit(bar + st);
         }
-        ptx::mbar_wait(bar, static_cast<uint32_t>(ch & 1)); // MMAs done: smem reusable / TMEM final
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if (ch + 1 < nchunks) {
+            const int nx = (ch + 1) % kStages;
+            if (ch + 1 >= kStages) { // the MMAs of chunk ch + 1 - kStages read that stage
+                ptx::mbar_wait(bar + nx, (phases >> nx) & 1u);
+                phases ^= 1u << nx;
+            }
+            load_b(ch + 1, nx);
+            store_a(nx); // overlaps the MMAs of chunk ch
+        }
     }
+    // the last chunk's commit covers every earlier MMA of this thread
+    {
+        const int st = (nchunks - 1) % kStages;
+        ptx::mbar_wait(bar + st, (phases >> st) & 1u);
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    bool bad = false;
 
-    // epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w + 31
+    // epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w + 31; the
+    // stage buffers are free (every MMA has completed)
     const std::size_t row = m0 + 32 * warp + lane;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -173,20 +212,32 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
         const int n = n0 + c0;
         if (n == 0 && row < M) bad |= !isfinite(__uint_as_float(v[0])); // the DC coefficient
-        if (row < M && n < N) {
-            float* dst = C + row * ldc + n;
-            if (n + 32 <= N) {
+        // transpose through shared memory (this warp's 4 KB, 16-byte chunks
+        // XOR-swizzled by row: conflict-free both ways), then each quarter-warp
+        // stores one row's 128 contiguous bytes
+        unsigned char* tb = base + warp * 4096;
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    reinterpret_cast<float4*>(dst)[q] =
-                        make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                    __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-            } else {
+        for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<uint4*>(tb + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        __syncwarp();
 #pragma unroll
-                for (int q = 0; q < 32; ++q)
-                    if (q < N - n) dst[q] = __uint_as_float(v[q]);
+        for (int it = 0; it < 8; ++it) {
+            const int r = 4 * it + (lane >> 3), q = lane & 7;
+            const uint4 w = *reinterpret_cast<const uint4*>(tb + r * 128 + ((q ^ (r & 7)) << 4));
+            const std::size_t grow = m0 + 32 * warp + r;
+            const int col = n + 4 * q;
+            if (grow < M) {
+                float* dst = C + grow * ldc + col;
+                if (col + 4 <= N) {
+                    *reinterpret_cast<uint4*>(dst) = w;
+                } else {
+                    const uint32_t e[4] = {w.x, w.y, w.z, w.w};
+                    for (int u = 0; u < 4 && col + u < N; ++u) dst[u] = __uint_as_float(e[u]);
+                }
             }
         }
+        __syncwarp();
     }
     if (bad) atomicOr(flag, 1);
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");

@@ -230,7 +230,8 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
             if (grow < M) {
                 float* dst = C + grow * ldc + col;
                 if (col + 4 <= N) {
-                    *reinterpret_cast<uint4*>(dst) = w;
+                    __stcs(reinterpret_cast<float4*>(dst), make_float4(__uint_as_float(w.x), __uint_as_float(w.y),
+                                                                       __uint_as_float(w.z), __uint_as_float(w.w)));
                 } else {
                     const uint32_t e[4] = {w.x, w.y, w.z, w.w};
                     for (int u = 0; u < 4 && col + u < N; ++u) dst[u] = __uint_as_float(e[u]);

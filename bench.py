@@ -327,7 +327,7 @@ def run_gpu_arm(args, cfg, rank: int, local: int, world: int):
     # progressive SGEMM) is rated on the Cauchy-stage flops over its own
     # launch time; the fused kernel also carries the DCT; any other top
     # kernel falls back to the whole step.
-    product = any(k in top for k in ("cauchy", "fold_w", "dense", "chain", "progressive_sgemm"))
+    product = any(k in top for k in ("cauchy", "fold_w", "dense", "chain", "progressive_sgemm", "progressive_tc32"))
     if "fused" in top:
         flops, t_ms = (alg["flops_cauchy"] + alg["flops_dct"]) * cfg.batch, per_launch_ms[top]
     elif product:
@@ -335,7 +335,14 @@ def run_gpu_arm(args, cfg, rank: int, local: int, world: int):
     else:
         flops, t_ms = (alg["flops_cauchy"] + alg["flops_dct"]) * cfg.batch, ms_per_step
     nbytes = alg["bytes"] * cfg.batch
-    if f32:
+    if f32 and "tc32" in top:
+        # tcgen05 kind::tf32 with the 3xTF32 split: three tensor-core products
+        # per algorithmic one; dense TF32 runs at half the bf16 rate
+        bf = peaks.get("bf16_tflops")
+        peak = bf / 2.0 / 3.0 if bf else None
+        src = "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 rate) / 3 (3xTF32 passes)"
+        bound = "tensor"
+    elif f32:
         peak = max(fp.get("fp32_fma_tflops") or 0.0, fp.get("fp32_ffma2_tflops") or 0.0) or None
         src = "profiles/peaks_fp64.json max(fp32_fma_tflops, fp32_ffma2_tflops) (tools/peaks.cu, measured)"
         bound = "fp32-fma"

@@ -344,6 +344,7 @@ struct dctp_plan {
         std::size_t ldw = 0, w = 0, map = 0, to = 0, from = 0, sign64 = 0, sign32 = 0;
         std::size_t ldwt = 0, wt = 0, zero = 0; // inverse: W^T (L x cols) and a zero row
         std::size_t wt32 = 0;                    // fp32 forward: W^T rounded, the SGEMM's B (L x ldwt)
+        std::size_t w_hi = 0, w_lo = 0;          // fp32 forward on tcgen05: W split 3xTF32 (cols x L)
         TwiddleOffsets tw64, tw32;
     } fd;
     // NFST fast route (fp64): the reference's own forward algorithm on the GPU
@@ -564,6 +565,23 @@ static void build_fold(dctp_plan& p, Blob& blob, const ApplyTables& t) {
     for (std::size_t r = 0; r < cols; ++r)
         for (std::size_t j = 0; j < L; ++j) wt[j * ldwt + r] = w[r * ldw + j];
     auto& f = p.fd;
+    {
+        std::vector<float> hi(cols * L), lo(cols * L);
+        for (std::size_t r = 0; r < cols; ++r)
+            for (std::size_t j = 0; j < L; ++j) {
+                const double v = w[r * ldw + j];
+                const float fv = static_cast<float>(v);
+                std::uint32_t bits;
+                std::memcpy(&bits, &fv, 4);
+                bits = (bits + 0x1000u) & 0xffffe000u; // TF32 head, round to nearest (ties away)
+                float h;
+                std::memcpy(&h, &bits, 4);
+                hi[r * L + j] = h;
+                lo[r * L + j] = static_cast<float>(v - static_cast<double>(h));
+            }
+        f.w_hi = blob.add(hi);
+        f.w_lo = blob.add(lo);
+    }
     f.ldwt = ldwt;
     f.wt = blob.add(wt);
     f.wt32 = blob.add(to_f32(wt));
@@ -1053,7 +1071,18 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
                                                             s)),
                    "fold dct kernel");
         if constexpr (f32) {
-            // fp32: the FFMA2 SGEMM with W^T rounded once (twice the DMMA rate)
+            // fp32: the tcgen05 3xTF32 GEMM (DCTP_TC32=0: the FFMA2 SGEMM with W^T
+            // rounded once, twice the DMMA rate)
+            const char* tc = std::getenv("DCTP_TC32");
+            const float* wh = at<float>(p->blob, f.w_hi);
+            const float* wl = at<float>(p->blob, f.w_lo);
+            if (!(tc && tc[0] == '0') && dctp::dev::tc_sgemm3_supported(f.L, f.cols, f.L, f.L, n, u.ptr, wh, wl, out)) {
+                cuda_check(DCTP_LAUNCH("fold_w_tc32", s,
+                                       dctp::dev::tc_sgemm3(u.ptr, f.L, wh, wl, f.L, out, n, batch, f.cols, f.L,
+                                                            p->flag, s, at<int>(p->blob, f.map))),
+                           "fold tcgen05 kernel");
+                return;
+            }
             const float* b = at<float>(p->blob, f.wt32);
             if (dctp::dev::sgemm_rows_supported(f.L, f.cols, f.L, static_cast<int>(f.ldwt), 4, u.ptr, b, b)) {
                 cuda_check(DCTP_LAUNCH("fold_w", s,

@@ -82,7 +82,7 @@ __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, int by
 __global__ void __launch_bounds__(kThreads, 2)
 tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__ bt_hi,
                  const float* __restrict__ bt_lo, int ldb, float* __restrict__ C, std::size_t ldc, std::size_t M,
-                 int N, int K, int* flag) {
+                 int N, int K, int* flag, const int* __restrict__ col_map) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of the swizzle atoms
     const uint32_t raw = ptx::smem_addr(smem_raw);
@@ -227,7 +227,12 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
             const uint4 w = *reinterpret_cast<const uint4*>(tb + r * 128 + ((q ^ (r & 7)) << 4));
             const std::size_t grow = m0 + 32 * warp + r;
             const int col = n + 4 * q;
-            if (grow < M) {
+            if (grow < M && col_map) { // scattered output columns (the folded route's slots)
+                const uint32_t e[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (col + u < N) C[grow * ldc + __ldg(col_map + col + u)] = __uint_as_float(e[u]);
+            } else if (grow < M) {
                 float* dst = C + grow * ldc + col;
                 if (col + 4 <= N) {
                     __stcs(reinterpret_cast<float4*>(dst), make_float4(__uint_as_float(w.x), __uint_as_float(w.y),
@@ -258,13 +263,14 @@ bool tc_sgemm3_supported(int K, int N, int lda, int ldb, std::size_t ldc, const 
 }
 
 cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* bt_lo, int ldb, float* C,
-                      std::size_t ldc, std::size_t M, int N, int K, int* flag, cudaStream_t stream) {
+                      std::size_t ldc, std::size_t M, int N, int K, int* flag, cudaStream_t stream,
+                      const int* col_map) {
     if (M == 0 || N == 0) return cudaSuccess;
     static const cudaError_t attr =
         cudaFuncSetAttribute(tc_sgemm3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (attr != cudaSuccess) return attr;
     const dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), static_cast<unsigned>((N + BN - 1) / BN));
-    tc_sgemm3_kernel<<<grid, kThreads, kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag);
+    tc_sgemm3_kernel<<<grid, kThreads, kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag, col_map);
     return cudaGetLastError();
 }
 

@@ -345,6 +345,7 @@ struct dctp_plan {
         std::size_t ldwt = 0, wt = 0, zero = 0; // inverse: W^T (L x cols) and a zero row
         std::size_t wt32 = 0;                    // fp32 forward: W^T rounded, the SGEMM's B (L x ldwt)
         std::size_t w_hi = 0, w_lo = 0;          // fp32 forward on tcgen05: W split 3xTF32 (cols x L)
+        std::size_t wt_hi = 0, wt_lo = 0;        // fp32 inverse on tcgen05: W^T split (L x ldwt)
         TwiddleOffsets tw64, tw32;
     } fd;
     // NFST fast route (fp64): the reference's own forward algorithm on the GPU
@@ -581,6 +582,15 @@ static void build_fold(dctp_plan& p, Blob& blob, const ApplyTables& t) {
             }
         f.w_hi = blob.add(hi);
         f.w_lo = blob.add(lo);
+        const std::size_t ldt = (cols + 3) / 4 * 4;
+        std::vector<float> thi(L * ldt, 0.f), tlo(L * ldt, 0.f);
+        for (std::size_t r = 0; r < cols; ++r)
+            for (std::size_t j = 0; j < L; ++j) {
+                thi[j * ldt + r] = hi[r * L + j];
+                tlo[j * ldt + r] = lo[r * L + j];
+            }
+        f.wt_hi = blob.add(thi);
+        f.wt_lo = blob.add(tlo);
     }
     f.ldwt = ldwt;
     f.wt = blob.add(wt);
@@ -1147,6 +1157,21 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
                                dctp::dev::idct_rows<T>(at<T>(p->blob, f.zero), 0, in, n, even, w.ptr, f.L, f.L, batch,
                                                        twiddles_at<T>(p->blob, f32 ? f.tw32 : f.tw64), p->flag, s)),
                    "fold idct kernel");
+        if constexpr (f32) {
+            const char* tc = std::getenv("DCTP_TC32");
+            const float* th = at<float>(p->blob, f.wt_hi);
+            const float* tl = at<float>(p->blob, f.wt_lo);
+            const int ldt = (f.cols + 3) / 4 * 4;
+            if (!(tc && tc[0] == '0') && f.cols % 4 == 0 &&
+                dctp::dev::tc_sgemm3_supported(f.cols, f.L, 4, ldt, n, w.ptr, th, tl, out)) {
+                cuda_check(DCTP_LAUNCH("fold_wt_tc32", s,
+                                       dctp::dev::tc_sgemm3(in, static_cast<int>(n), th, tl, ldt, out, n, batch, f.L,
+                                                            f.cols, p->flag, s, nullptr, at<int>(p->blob, f.map), w.ptr,
+                                                            f.L)),
+                           "fold tcgen05 kernel");
+                return;
+            }
+        }
         cuda_check(DCTP_LAUNCH("fold_wt", s,
                                dctp::dev::rows_by_basis<T>(in, n, at<double>(p->blob, f.wt), f.ldwt, f.cols, f.L, out, n,
                                                            batch, p->flag, s, nullptr, at<int>(p->blob, f.map), w.ptr,

@@ -194,14 +194,16 @@ cudaError_t column_signs_gpu(const double* xt, std::size_t ld, int n, int cols, 
 /// C[M x N] = A[M x K] * B[K x N] in fp32 on the tcgen05 tensor cores
 /// (kind::tf32, 3xTF32 split; tc_sgemm.cu): A row-major, B given as B^T =
 /// bt_hi + bt_lo (N x K, row stride ldb; bt_hi TF32-representable), C
-/// row-major (or column c stored at col_map[c]); 16-byte aligned pointers,
+/// row-major (or column c stored at col_map[c], or unfolded with fold_add as
+/// in rows_by_basis); A's columns optionally gathered through a_map; 16-byte aligned pointers,
 /// K, lda, ldb, ldc multiples of 4.  Raises flag bit 0 if column 0 of a row
 /// of the product is non-finite.
 bool tc_sgemm3_supported(int K, int N, int lda, int ldb, std::size_t ldc, const void* A, const void* Bh,
                          const void* Bl, const void* C);
 cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* bt_lo, int ldb, float* C,
                       std::size_t ldc, std::size_t M, int N, int K, int* flag, cudaStream_t stream,
-                      const int* col_map = nullptr);
+                      const int* col_map = nullptr, const int* a_map = nullptr, const float* fold_add = nullptr,
+                      std::size_t ld_add = 0);
 
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);

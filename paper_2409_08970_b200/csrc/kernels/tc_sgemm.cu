@@ -82,7 +82,8 @@ __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, int by
 __global__ void __launch_bounds__(kThreads, 2)
 tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__ bt_hi,
                  const float* __restrict__ bt_lo, int ldb, float* __restrict__ C, std::size_t ldc, std::size_t M,
-                 int N, int K, int* flag, const int* __restrict__ col_map) {
+                 int N, int K, int* flag, const int* __restrict__ col_map, const int* __restrict__ a_map,
+                 const float* __restrict__ fold_add, std::size_t ld_add) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of the swizzle atoms
     const uint32_t raw = ptx::smem_addr(smem_raw);
@@ -121,8 +122,17 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
 #pragma unroll
         for (int u = 0; u < kAV; ++u) {
             const int i = tid + u * kThreads, r = i >> 2, c = i & 3, k = k0 + 4 * c;
-            areg[u] = (m0 + r < M && k < K) ? *reinterpret_cast<const float4*>(A + (m0 + r) * lda + k)
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (a_map) { // gathered columns (the folded inverse's W slots)
+                const float* row = A + (m0 + r) * lda;
+                const bool ok = m0 + r < M;
+                areg[u] = make_float4(ok && k < K ? row[__ldg(a_map + k)] : 0.f,
+                                      ok && k + 1 < K ? row[__ldg(a_map + k + 1)] : 0.f,
+                                      ok && k + 2 < K ? row[__ldg(a_map + k + 2)] : 0.f,
+                                      ok && k + 3 < K ? row[__ldg(a_map + k + 3)] : 0.f);
+            } else {
+                areg[u] = (m0 + r < M && k < K) ? *reinterpret_cast<const float4*>(A + (m0 + r) * lda + k)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
     };
     auto store_a = [&](int st) {
@@ -227,7 +237,18 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
             const uint4 w = *reinterpret_cast<const uint4*>(tb + r * 128 + ((q ^ (r & 7)) << 4));
             const std::size_t grow = m0 + 32 * warp + r;
             const int col = n + 4 * q;
-            if (grow < M && col_map) { // scattered output columns (the folded route's slots)
+            if (grow < M && fold_add) { // unfold: x_c = w_c + v_c, x_{2N-1-c} = w_c - v_c
+                const uint32_t e[4] = {w.x, w.y, w.z, w.w};
+                const float* add = fold_add + grow * ld_add;
+                float* orow = C + grow * ldc;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (col + u < N) {
+                        const float wv = add[col + u], v = __uint_as_float(e[u]);
+                        orow[col + u] = wv + v;
+                        orow[2 * N - 1 - (col + u)] = wv - v;
+                    }
+            } else if (grow < M && col_map) { // scattered output columns (the folded route's slots)
                 const uint32_t e[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
@@ -259,18 +280,19 @@ bool tc_sgemm3_supported(int K, int N, int lda, int ldb, std::size_t ldc, const 
                          const void* Bl, const void* C) {
     const auto al = [](const void* p) { return reinterpret_cast<std::uintptr_t>(p) % 16 == 0; };
     return K > 0 && N > 0 && K % 4 == 0 && lda % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 && al(A) && al(Bh) &&
-           al(Bl) && al(C);
+           al(Bl) && al(C);  // (with an A column map only the B and C constraints matter, and they are checked)
 }
 
 cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* bt_lo, int ldb, float* C,
                       std::size_t ldc, std::size_t M, int N, int K, int* flag, cudaStream_t stream,
-                      const int* col_map) {
+                      const int* col_map, const int* a_map, const float* fold_add, std::size_t ld_add) {
     if (M == 0 || N == 0) return cudaSuccess;
     static const cudaError_t attr =
         cudaFuncSetAttribute(tc_sgemm3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (attr != cudaSuccess) return attr;
     const dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), static_cast<unsigned>((N + BN - 1) / BN));
-    tc_sgemm3_kernel<<<grid, kThreads, kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag, col_map);
+    tc_sgemm3_kernel<<<grid, kThreads, kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag, col_map,
+                                                         a_map, fold_add, ld_add);
     return cudaGetLastError();
 }
 

@@ -697,3 +697,39 @@ def test_gpu_setup_bit_identical(P, torch, monkeypatch, case):
     for k in b:
         assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
     assert gpu.slow_path() == host.slow_path()
+
+
+def test_random_plans_all_routes_match_reference(P, torch, reference, monkeypatch):
+    """Seeded sweep over random updates (kind, vertices, weight) and sizes:
+    forward and inverse against the reference — the NFST route against its
+    forward() / inverse(fast = true) where the plan takes it, every exact
+    route against the reference's dense routes — fp64 and fp32."""
+    rng = np.random.default_rng(2409)
+    checked = 0
+    for trial in range(40):
+        n = int(rng.choice([16, 32, 48, 64, 96, 128, 200, 256, 384, 512]))
+        kind = int(rng.integers(0, 2))
+        i = int(rng.integers(1, n + 1))
+        j = int(rng.integers(1, n + 1))
+        if kind == 1 and i == j:
+            j = i % n + 1
+        rho = float(rng.choice([-1, 1]) * 10 ** rng.uniform(-1.5, 0.7))
+        u = O.Update(kind, rho, i, j if kind == 1 else 0)
+        try:
+            rp = reference.plan(n, u)
+        except Exception:  # noqa: BLE001 - invalid update for the reference too
+            continue
+        plan = P.DctPlusPlan(n, upd(P, u), 1e-12)
+        s = rng.standard_normal((37, n))
+        nfst = plan.route()["nfst"]
+        want = rp.forward(s, nmvp=not nfst)
+        got = plan.forward(dev(torch, s, torch.float64)).cpu().numpy()
+        assert O.parity(got, want) <= TOL64, (n, u, nfst)
+        back_want = rp.inverse(want, fast=nfst)
+        back = plan.inverse(dev(torch, want, torch.float64)).cpu().numpy()
+        assert O.parity(back, back_want) <= TOL64, (n, u, nfst, "inverse")
+        exact = want if not nfst else rp.forward(s, nmvp=True)
+        y32 = plan.forward(dev(torch, s, torch.float32)).double().cpu().numpy()
+        assert O.parity(y32, exact) <= TOL32, (n, u, "fp32")
+        checked += 1
+    assert checked >= 30

@@ -231,3 +231,13 @@ def test_chain_errors_mirror_reference():
     ch = P.compose_rank_k(8, [P.RankOneUpdate.self_loop(1, 1.5)], device=-1)
     with pytest.raises(P.InvalidArgument, match="host-only"):
         ch.forward(np.zeros(8))
+
+
+def test_host_only_plan_route_query():
+    """dctp_plan_route on a host-only plan (no device constants): no NFST
+    route and no creation probe (the probe needs the GPU)."""
+    import paper_2409_08970_b200 as P
+
+    plan = P.DctPlusPlan(1024, P.RankOneUpdate.self_loop(1, 0.5), 1e-12, device=-1)
+    assert plan.route() == {"nfst": False, "probe_gap": 0.0}
+    assert not plan.slow_path()

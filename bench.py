@@ -338,9 +338,14 @@ def run_gpu_arm(args, cfg, rank: int, local: int, world: int):
     if f32 and "tc32" in top:
         # tcgen05 kind::tf32 with the 3xTF32 split: three tensor-core products
         # per algorithmic one; dense TF32 runs at half the bf16 rate
+        tf = fp.get("tcgen05_tf32_tflops")
         bf = peaks.get("bf16_tflops")
-        peak = bf / 2.0 / 3.0 if bf else None
-        src = "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 rate) / 3 (3xTF32 passes)"
+        if tf:
+            peak = tf / 3.0
+            src = "profiles/peaks_fp64.json tcgen05_tf32_tflops (tools/tc_peak.cu, measured) / 3 (3xTF32 passes)"
+        else:
+            peak = bf / 2.0 / 3.0 if bf else None
+            src = "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 rate) / 3 (3xTF32 passes)"
         bound = "tensor"
     elif f32:
         peak = max(fp.get("fp32_fma_tflops") or 0.0, fp.get("fp32_ffma2_tflops") or 0.0) or None

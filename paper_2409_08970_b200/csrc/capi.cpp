@@ -346,6 +346,7 @@ struct dctp_plan {
         std::size_t wt32 = 0;                    // fp32 forward: W^T rounded, the SGEMM's B (L x ldwt)
         std::size_t w_hi = 0, w_lo = 0;          // fp32 forward on tcgen05: W split 3xTF32 (cols x L)
         std::size_t wt_hi = 0, wt_lo = 0;        // fp32 inverse on tcgen05: W^T split (L x ldwt)
+        std::size_t w_sw = 0, wt_sw = 0;         // both, in the kernel's swizzled shared-memory blocks
         TwiddleOffsets tw64, tw32;
     } fd;
     // NFST fast route (fp64): the reference's own forward algorithm on the GPU
@@ -591,6 +592,10 @@ static void build_fold(dctp_plan& p, Blob& blob, const ApplyTables& t) {
             }
         f.wt_hi = blob.add(thi);
         f.wt_lo = blob.add(tlo);
+        f.w_sw = blob.add(dctp::dev::tc_swizzle_b(hi.data(), lo.data(), static_cast<int>(cols), static_cast<int>(L),
+                                                  static_cast<int>(L)));
+        f.wt_sw = blob.add(dctp::dev::tc_swizzle_b(thi.data(), tlo.data(), static_cast<int>(L),
+                                                   static_cast<int>(cols), static_cast<int>(ldt)));
     }
     f.ldwt = ldwt;
     f.wt = blob.add(wt);
@@ -1089,7 +1094,8 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
             if (!(tc && tc[0] == '0') && dctp::dev::tc_sgemm3_supported(f.L, f.cols, f.L, f.L, n, u.ptr, wh, wl, out)) {
                 cuda_check(DCTP_LAUNCH("fold_w_tc32", s,
                                        dctp::dev::tc_sgemm3(u.ptr, f.L, wh, wl, f.L, out, n, batch, f.cols, f.L,
-                                                            p->flag, s, at<int>(p->blob, f.map))),
+                                                            p->flag, s, at<int>(p->blob, f.map), nullptr, nullptr, 0,
+                                                            at<float>(p->blob, f.w_sw))),
                            "fold tcgen05 kernel");
                 return;
             }
@@ -1167,7 +1173,7 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
                 cuda_check(DCTP_LAUNCH("fold_wt_tc32", s,
                                        dctp::dev::tc_sgemm3(in, static_cast<int>(n), th, tl, ldt, out, n, batch, f.L,
                                                             f.cols, p->flag, s, nullptr, at<int>(p->blob, f.map), w.ptr,
-                                                            f.L)),
+                                                            f.L, at<float>(p->blob, f.wt_sw))),
                            "fold tcgen05 kernel");
                 return;
             }
@@ -1491,6 +1497,7 @@ struct dctp_ensemble {
     // fp32 dense route (n <= 256): G = [D^T | X_1 | ... | X_K], n x (K+1) n
     std::size_t gmat32 = 0;
     std::size_t gt_hi = 0, gt_lo = 0; // G^T split for the tcgen05 3xTF32 GEMM, (K+1) n x n
+    std::size_t gt_sw = 0;            // the same, in the kernel's swizzled shared-memory blocks
     bool dense32 = false;
     // pruned mode (c_p < n): [UL_r; HL_r] = T_r[:, 0:c_p] per member, K x n x c_p
     std::size_t prune64 = 0, prune32 = 0;
@@ -1557,7 +1564,9 @@ static void ensemble_forward_full(const dctp_ensemble* e, const T* in, T* out, s
             cuda_check(DCTP_LAUNCH("progressive_tc32", s,
                                    dctp::dev::tc_sgemm3(in, static_cast<int>(n), at<float>(e->blob, e->gt_hi),
                                                         at<float>(e->blob, e->gt_lo), static_cast<int>(n), out, ld,
-                                                        batch, static_cast<int>(ld), static_cast<int>(n), e->flag, s)),
+                                                        batch, static_cast<int>(ld), static_cast<int>(n), e->flag, s,
+                                                        nullptr, nullptr, nullptr, 0,
+                                                        at<float>(e->blob, e->gt_sw))),
                        "progressive tcgen05 kernel");
             return;
         }
@@ -1884,6 +1893,8 @@ int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is,
             e->gmat32 = blob.add(g);
             e->gt_hi = blob.add(bt_hi);
             e->gt_lo = blob.add(bt_lo);
+            e->gt_sw = blob.add(dctp::dev::tc_swizzle_b(bt_hi.data(), bt_lo.data(), static_cast<int>(cols),
+                                                        static_cast<int>(n), static_cast<int>(n)));
             e->dense32 = true;
         }
         if (device < 0) {

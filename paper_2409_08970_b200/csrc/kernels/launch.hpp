@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 #include <cuda_runtime_api.h>
 
@@ -203,7 +204,11 @@ bool tc_sgemm3_supported(int K, int N, int lda, int ldb, std::size_t ldc, const 
 cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* bt_lo, int ldb, float* C,
                       std::size_t ldc, std::size_t M, int N, int K, int* flag, cudaStream_t stream,
                       const int* col_map = nullptr, const int* a_map = nullptr, const float* fold_add = nullptr,
-                      std::size_t ld_add = 0);
+                      std::size_t ld_add = 0, const float* b_sw = nullptr);
+/// B^T (hi, lo) rearranged into the kernel's shared-memory blocks (per
+/// 256-row tile and 16-wide K chunk: hi then lo, SWIZZLE_64B), so each stage
+/// of B arrives by one 32 KB TMA bulk copy (pass as b_sw).
+std::vector<float> tc_swizzle_b(const float* bt_hi, const float* bt_lo, int N, int K, int ldb);
 
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);

@@ -19,6 +19,8 @@
 // thread, as full 32-byte sectors.  96 KB of shared memory: two CTAs per SM,
 // so one CTA's epilogue overlaps the other's loads and MMAs.
 #include <cstdint>
+#include <cstdlib>
+#include <vector>
 
 #include "kernels/common.cuh"
 #include "kernels/launch.hpp"
@@ -83,13 +85,14 @@ __global__ void __launch_bounds__(kThreads, 2)
 tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__ bt_hi,
                  const float* __restrict__ bt_lo, int ldb, float* __restrict__ C, std::size_t ldc, std::size_t M,
                  int N, int K, int* flag, const int* __restrict__ col_map, const int* __restrict__ a_map,
-                 const float* __restrict__ fold_add, std::size_t ld_add) {
+                 const float* __restrict__ fold_add, std::size_t ld_add, const float* __restrict__ b_sw) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of the swizzle atoms
     const uint32_t raw = ptx::smem_addr(smem_raw);
     unsigned char* base = smem_raw + ((1024 - (raw & 1023)) & 1023);
     uint64_t* bar = reinterpret_cast<uint64_t*>(base + kStages * kStageBytes); // one per stage: MMAs done
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + kStages);
+    uint64_t* bfull = bar + kStages;                                            // one per stage: B landed (TMA)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + kStages);
     const uint32_t sbase = ptx::smem_addr(base);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -104,7 +107,10 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     if (tid == 0) {
-        for (int i = 0; i < kStages; ++i) ptx::mbar_init(bar + i, 1);
+        for (int i = 0; i < kStages; ++i) {
+            ptx::mbar_init(bar + i, 1);
+            ptx::mbar_init(bfull + i, 1);
+        }
         ptx::fence_mbar_init();
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -147,7 +153,17 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
             *reinterpret_cast<float4*>(g0 + kABytes + sw64(r, c)) = l;
         }
     };
+    const int kblocks = (K + BK - 1) / BK;
     auto load_b = [&](int ch, int st) {
+        if (b_sw) { // pre-swizzled on the host: the stage's B (hi, lo) is one contiguous 32 KB block
+            if (tid == 0) {
+                ptx::mbar_expect_tx(bfull + st, 2 * kBBytes);
+                ptx::bulk_load(base + st * kStageBytes + 2 * kABytes,
+                               b_sw + (static_cast<std::size_t>(blockIdx.y) * kblocks + ch) * (2 * BN * BK),
+                               2 * kBBytes, bfull + st);
+            }
+            return;
+        }
         const int k0 = ch * BK;
         const uint32_t s0 = sbase + st * kStageBytes;
         for (int i = tid; i < BN * (BK / 4); i += kThreads) {
@@ -173,6 +189,7 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (tid == 0) {
+            if (b_sw) ptx::mbar_wait(bfull + st, static_cast<uint32_t>((ch / kStages) & 1));
             const uint32_t s0 = sbase + st * kStageBytes;
             const uint32_t ah = s0, al = s0 + kABytes, bh = s0 + 2 * kABytes, bl = s0 + 2 * kABytes + kBBytes;
 #pragma unroll
@@ -276,6 +293,25 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
 
 } // namespace
 
+std::vector<float> tc_swizzle_b(const float* bt_hi, const float* bt_lo, int N, int K, int ldb) {
+    const int ntiles = (N + BN - 1) / BN, kblocks = (K + BK - 1) / BK;
+    std::vector<float> out(static_cast<std::size_t>(ntiles) * kblocks * 2 * BN * BK, 0.f);
+    for (int nt = 0; nt < ntiles; ++nt)
+        for (int kb = 0; kb < kblocks; ++kb) {
+            float* blk = out.data() + (static_cast<std::size_t>(nt) * kblocks + kb) * (2 * BN * BK);
+            for (int r = 0; r < BN; ++r)
+                for (int kl = 0; kl < BK; ++kl) {
+                    const int n = nt * BN + r, k = kb * BK + kl, c = kl >> 2;
+                    const int at = (r * 64 + ((c ^ ((r >> 1) & 3)) << 4)) / 4 + (kl & 3);
+                    if (n < N && k < K) {
+                        blk[at] = bt_hi[static_cast<std::size_t>(n) * ldb + k];
+                        blk[BN * BK + at] = bt_lo[static_cast<std::size_t>(n) * ldb + k];
+                    }
+                }
+        }
+    return out;
+}
+
 bool tc_sgemm3_supported(int K, int N, int lda, int ldb, std::size_t ldc, const void* A, const void* Bh,
                          const void* Bl, const void* C) {
     const auto al = [](const void* p) { return reinterpret_cast<std::uintptr_t>(p) % 16 == 0; };
@@ -285,14 +321,20 @@ bool tc_sgemm3_supported(int K, int N, int lda, int ldb, std::size_t ldc, const 
 
 cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* bt_lo, int ldb, float* C,
                       std::size_t ldc, std::size_t M, int N, int K, int* flag, cudaStream_t stream,
-                      const int* col_map, const int* a_map, const float* fold_add, std::size_t ld_add) {
+                      const int* col_map, const int* a_map, const float* fold_add, std::size_t ld_add,
+                      const float* b_sw) {
     if (M == 0 || N == 0) return cudaSuccess;
+    static const bool bulk_off = [] {
+        const char* e = std::getenv("DCTP_TC32_BULK");
+        return e && e[0] == '0';
+    }();
+    if (bulk_off) b_sw = nullptr;
     static const cudaError_t attr =
         cudaFuncSetAttribute(tc_sgemm3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (attr != cudaSuccess) return attr;
     const dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), static_cast<unsigned>((N + BN - 1) / BN));
     tc_sgemm3_kernel<<<grid, kThreads, kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag, col_map,
-                                                         a_map, fold_add, ld_add);
+                                                         a_map, fold_add, ld_add, b_sw);
     return cudaGetLastError();
 }
 

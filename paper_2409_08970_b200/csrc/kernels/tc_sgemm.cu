@@ -81,7 +81,10 @@ __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, int by
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(g), "r"(bytes) : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+/// MT: 128-row halves per CTA (1: 128 x 256 tiles, two CTAs per SM; 2: 256 x
+/// 256 tiles, both TMEM accumulators, one CTA per SM, half the B traffic).
+template <int MT>
+__global__ void __launch_bounds__(kThreads * MT, MT == 1 ? 2 : 1)
 tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__ bt_hi,
                  const float* __restrict__ bt_lo, int ldb, float* __restrict__ C, std::size_t ldc, std::size_t M,
                  int N, int K, int* flag, const int* __restrict__ col_map, const int* __restrict__ a_map,
@@ -90,19 +93,22 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
     // 1024-byte alignment of the swizzle atoms
     const uint32_t raw = ptx::smem_addr(smem_raw);
     unsigned char* base = smem_raw + ((1024 - (raw & 1023)) & 1023);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(base + kStages * kStageBytes); // one per stage: MMAs done
+    constexpr int kAB = MT * kABytes;                  // A hi (or lo) per stage
+    constexpr int kSB = 2 * kAB + 2 * kBBytes;          // stage bytes
+    constexpr int kT = kThreads * MT;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + kStages * kSB); // one per stage: MMAs done
     uint64_t* bfull = bar + kStages;                                            // one per stage: B landed (TMA)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + kStages);
     const uint32_t sbase = ptx::smem_addr(base);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const std::size_t m0 = static_cast<std::size_t>(blockIdx.x) * BM;
+    const std::size_t m0 = static_cast<std::size_t>(blockIdx.x) * (BM * MT);
     const int n0 = blockIdx.y * BN;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                          ptx::smem_addr(tmem_slot)),
-                     "n"(kTmemCols)
+                     "n"(kTmemCols * MT)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
@@ -121,13 +127,13 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
     // stage st: A hi, A lo, B hi, B lo.  A is fetched into registers one
     // chunk ahead (its global latency hides behind the barrier and the MMA
     // issue), then split and stored; B goes straight in by cp.async.
-    constexpr int kAV = BM * (BK / 4) / kThreads; // float4 of A per thread per chunk
+    constexpr int kAV = BM * MT * (BK / 4) / kT; // float4 of A per thread per chunk
     float4 areg[kAV];
     auto fetch_a = [&](int ch) {
         const int k0 = ch * BK;
 #pragma unroll
         for (int u = 0; u < kAV; ++u) {
-            const int i = tid + u * kThreads, r = i >> 2, c = i & 3, k = k0 + 4 * c;
+            const int i = tid + u * kT, r = i >> 2, c = i & 3, k = k0 + 4 * c;
             if (a_map) { // gathered columns (the folded inverse's W slots)
                 const float* row = A + (m0 + r) * lda;
                 const bool ok = m0 + r < M;
@@ -142,15 +148,15 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
         }
     };
     auto store_a = [&](int st) {
-        unsigned char* g0 = base + st * kStageBytes;
+        unsigned char* g0 = base + st * kSB;
 #pragma unroll
         for (int u = 0; u < kAV; ++u) {
-            const int i = tid + u * kThreads, r = i >> 2, c = i & 3;
+            const int i = tid + u * kT, r = i >> 2, c = i & 3;
             const float4 v = areg[u];
             const float4 h = make_float4(tf32_head(v.x), tf32_head(v.y), tf32_head(v.z), tf32_head(v.w));
             const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
             *reinterpret_cast<float4*>(g0 + sw64(r, c)) = h;
-            *reinterpret_cast<float4*>(g0 + kABytes + sw64(r, c)) = l;
+            *reinterpret_cast<float4*>(g0 + kAB + sw64(r, c)) = l;
         }
     };
     const int kblocks = (K + BK - 1) / BK;
@@ -158,20 +164,20 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
         if (b_sw) { // pre-swizzled on the host: the stage's B (hi, lo) is one contiguous 32 KB block
             if (tid == 0) {
                 ptx::mbar_expect_tx(bfull + st, 2 * kBBytes);
-                ptx::bulk_load(base + st * kStageBytes + 2 * kABytes,
+                ptx::bulk_load(base + st * kSB + 2 * kAB,
                                b_sw + (static_cast<std::size_t>(blockIdx.y) * kblocks + ch) * (2 * BN * BK),
                                2 * kBBytes, bfull + st);
             }
             return;
         }
         const int k0 = ch * BK;
-        const uint32_t s0 = sbase + st * kStageBytes;
-        for (int i = tid; i < BN * (BK / 4); i += kThreads) {
+        const uint32_t s0 = sbase + st * kSB;
+        for (int i = tid; i < BN * (BK / 4); i += kT) {
             const int r = i >> 2, c = i & 3, n = n0 + r, k = k0 + 4 * c;
             const int bytes = (n < N && k < K) ? 16 : 0;
             const std::size_t off = bytes ? static_cast<std::size_t>(n) * ldb + k : 0;
-            cp_async16(s0 + 2 * kABytes + sw64(r, c), bt_hi + off, bytes);
-            cp_async16(s0 + 2 * kABytes + kBBytes + sw64(r, c), bt_lo + off, bytes);
+            cp_async16(s0 + 2 * kAB + sw64(r, c), bt_hi + off, bytes);
+            cp_async16(s0 + 2 * kAB + kBBytes + sw64(r, c), bt_lo + off, bytes);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
@@ -190,15 +196,20 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (tid == 0) {
             if (b_sw) ptx::mbar_wait(bfull + st, static_cast<uint32_t>((ch / kStages) & 1));
-            const uint32_t s0 = sbase + st * kStageBytes;
-            const uint32_t ah = s0, al = s0 + kABytes, bh = s0 + 2 * kABytes, bl = s0 + 2 * kABytes + kBBytes;
+            const uint32_t s0 = sbase + st * kSB;
+            const uint32_t bh = s0 + 2 * kAB, bl = s0 + 2 * kAB + kBBytes;
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) { // 8 tf32 = 32 bytes per MMA step along K
-                const uint32_t o = 32u * kk;
-                const uint32_t acc0 = (ch > 0 || kk > 0) ? 1u : 0u;
-                mma_tf32(tmem, smem_desc(ah + o), smem_desc(bh + o), acc0);
-                mma_tf32(tmem, smem_desc(ah + o), smem_desc(bl + o), 1u);
-                mma_tf32(tmem, smem_desc(al + o), smem_desc(bh + o), 1u);
+            for (int h = 0; h < MT; ++h) { // 128-row half h: rows 128 h.. of the A tile, accumulator h
+                const uint32_t ah = s0 + h * kABytes, al = s0 + kAB + h * kABytes;
+                const uint32_t td = tmem + static_cast<uint32_t>(h * BN);
+#pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) { // 8 tf32 = 32 bytes per MMA step along K
+                    const uint32_t o = 32u * kk;
+                    const uint32_t acc0 = (ch > 0 || kk > 0) ? 1u : 0u;
+                    mma_tf32(td, smem_desc(ah + o), smem_desc(bh + o), acc0);
+                    mma_tf32(td, smem_desc(ah + o), smem_desc(bl + o), 1u);
+                    mma_tf32(td, smem_desc(al + o), smem_desc(bh + o), 1u);
+                }
             }
             mma_commit(bar + st);
         }
@@ -222,11 +233,13 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
 
     // epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w + 31; the
     // stage buffers are free (every MMA has completed)
-    const std::size_t row = m0 + 32 * warp + lane;
+    const int quarter = warp & 3, half = warp >> 2; // TMEM lane quarter, accumulator
+    const std::size_t row = m0 + 128 * half + 32 * quarter + lane;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t v[32];
-        const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * warp) << 16) + static_cast<uint32_t>(c0);
+        const uint32_t taddr =
+            tmem + (static_cast<uint32_t>(32 * quarter) << 16) + static_cast<uint32_t>(half * BN + c0);
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
             "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
@@ -252,7 +265,7 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
         for (int it = 0; it < 8; ++it) {
             const int r = 4 * it + (lane >> 3), q = lane & 7;
             const uint4 w = *reinterpret_cast<const uint4*>(tb + r * 128 + ((q ^ (r & 7)) << 4));
-            const std::size_t grow = m0 + 32 * warp + r;
+            const std::size_t grow = m0 + 128 * half + 32 * quarter + r;
             const int col = n + 4 * q;
             if (grow < M && fold_add) { // unfold: x_c = w_c + v_c, x_{2N-1-c} = w_c - v_c
                 const uint32_t e[4] = {w.x, w.y, w.z, w.w};
@@ -287,7 +300,7 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols * MT)
                      : "memory");
 }
 
@@ -329,11 +342,19 @@ cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* 
         return e && e[0] == '0';
     }();
     if (bulk_off) b_sw = nullptr;
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(tc_sgemm3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (attr != cudaSuccess) return attr;
-    const dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), static_cast<unsigned>((N + BN - 1) / BN));
-    tc_sgemm3_kernel<<<grid, kThreads, kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag, col_map,
+    static const int mt = [] {
+        const char* e = std::getenv("DCTP_TC32_M256");
+        return (e && e[0] == '1') ? 2 : 1;
+    }();
+    constexpr int kSmem2 = kStages * (4 * kABytes + 2 * kBBytes) + 1024 + 64;
+    static const cudaError_t attr1 =
+        cudaFuncSetAttribute(tc_sgemm3_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    static const cudaError_t attr2 =
+        cudaFuncSetAttribute(tc_sgemm3_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+    if (attr1 != cudaSuccess) return attr1;
+    if (attr2 != cudaSuccess) return attr2;
+    const dim3 grid(static_cast<unsigned>((M + BM * mt - 1) / (BM * mt)), static_cast<unsigned>((N + BN - 1) / BN));
+    (mt == 2 ? tc_sgemm3_kernel<2> : tc_sgemm3_kernel<1>)<<<grid, kThreads * mt, mt == 2 ? kSmem2 : kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag, col_map,
                                                          a_map, fold_add, ld_add, b_sw);
     return cudaGetLastError();
 }

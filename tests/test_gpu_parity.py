@@ -321,13 +321,21 @@ def test_misaligned_device_views_take_the_generic_route(P, torch, restatement):
     assert O.parity(out_big[1:].view(33, cfg.n).cpu().numpy(), ref) <= TOL64
 
 
-def test_progressive_fp32_dense_route_edges(P, torch, restatement):
-    """The fp32 progressive SGEMM route (x * [D^T | X_1..X_K]) on ragged
+@pytest.mark.parametrize("tc32", ["1", "0"])
+def test_progressive_fp32_dense_route_edges(P, torch, restatement, monkeypatch, tc32):
+    """The fp32 progressive dense route (x * [D^T | X_1..X_K]) — on the
+    tcgen05 3xTF32 GEMM, or with DCTP_TC32=0 the FFMA SGEMM — on ragged
     batches (not multiples of the 128-row tile), against the fp64 generic
     route; a misaligned output view falls back to the DCT + Cauchy kernels
     with the same answer; a non-finite sample raises DomainError."""
+    monkeypatch.setenv("DCTP_TC32", tc32)
     ens = plan_for(P, 4)
     cfg = O.config(4)
+    P.profile_reset()
+    P.profile_enable(True)
+    ens.forward_all_batch(dev(torch, np.zeros((130, cfg.n)), torch.float32))
+    P.profile_enable(False)
+    assert set(P.profile_summary()) == {"progressive_tc32" if tc32 == "1" else "progressive_sgemm"}
     for batch in (1, 129, 1000):
         s = restatement.fill_signals(O.mix_seed(O.SEED, cfg.n, batch), 0, cfg.n, batch)
         y32 = ens.forward_all_batch(dev(torch, s, torch.float32)).double().cpu().numpy()
@@ -733,3 +741,25 @@ def test_random_plans_all_routes_match_reference(P, torch, reference, monkeypatc
         assert O.parity(y32, exact) <= TOL32, (n, u, "fp32")
         checked += 1
     assert checked >= 30
+
+
+@pytest.mark.parametrize("tc32", ["1", "0"])
+def test_folded_fp32_products_tc32_and_sgemm(P, torch, reference, monkeypatch, tc32):
+    """C3 in fp32: the folded route's W products on the tcgen05 3xTF32 GEMM
+    (fold_w_tc32 / fold_wt_tc32) or, with DCTP_TC32=0, the FFMA SGEMM and
+    the widened DMMA product; forward and inverse against the reference."""
+    monkeypatch.setenv("DCTP_TC32", tc32)
+    g = load_golden("c3")
+    plan = plan_for(P, 3)
+    P.profile_reset()
+    P.profile_enable(True)
+    y = plan.forward(dev(torch, g["signals"], torch.float32)).double().cpu().numpy()
+    b = plan.inverse(dev(torch, g["forward"], torch.float32)).double().cpu().numpy()
+    P.profile_enable(False)
+    names = set(P.profile_summary())
+    if tc32 == "1":
+        assert {"fold_w_tc32", "fold_wt_tc32"} <= names
+    else:
+        assert not any("tc32" in k for k in names)
+    assert O.parity(y, g["forward"]) <= TOL32
+    assert O.parity(b, g["signals"]) <= TOL32

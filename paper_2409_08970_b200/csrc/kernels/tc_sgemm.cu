@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(kThreads * MT, MT == 1 ? 2 : 1)
 tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__ bt_hi,
                  const float* __restrict__ bt_lo, int ldb, float* __restrict__ C, std::size_t ldc, std::size_t M,
                  int N, int K, int* flag, const int* __restrict__ col_map, const int* __restrict__ a_map,
-                 const float* __restrict__ fold_add, std::size_t ld_add, const float* __restrict__ b_sw) {
+                 const float* __restrict__ fold_add, std::size_t ld_add, const float* __restrict__ b_sw,
+                 int debug) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of the swizzle atoms
     const uint32_t raw = ptx::smem_addr(smem_raw);
@@ -194,7 +195,10 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
         ptx::fence_proxy_async(); // generic-proxy smem writes -> visible to the tensor core
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        if (tid == 0) {
+        if (tid == 0 && (debug & 2)) { // development knob: loads only, no MMAs
+            if (b_sw) ptx::mbar_wait(bfull + st, static_cast<uint32_t>((ch / kStages) & 1));
+            ptx::mbar_arrive(bar + st);
+        } else if (tid == 0) {
             if (b_sw) ptx::mbar_wait(bfull + st, static_cast<uint32_t>((ch / kStages) & 1));
             const uint32_t s0 = sbase + st * kSB;
             const uint32_t bh = s0 + 2 * kAB, bl = s0 + 2 * kAB + kBBytes;
@@ -233,6 +237,14 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
 
     // epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w + 31; the
     // stage buffers are free (every MMA has completed)
+    if (debug & 1) { // development knob: no epilogue
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();
+        if (warp == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols * MT)
+                         : "memory");
+        return;
+    }
     const int quarter = warp & 3, half = warp >> 2; // TMEM lane quarter, accumulator
     const std::size_t row = m0 + 128 * half + 32 * quarter + lane;
 #pragma unroll 1
@@ -342,6 +354,10 @@ cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* 
         return e && e[0] == '0';
     }();
     if (bulk_off) b_sw = nullptr;
+    static const int debug = [] { // DCTP_TC32_DEBUG: 1 = skip the epilogue, 2 = skip the MMAs (timing only)
+        const char* e = std::getenv("DCTP_TC32_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
     static const int mt = [] {
         const char* e = std::getenv("DCTP_TC32_M256");
         return (e && e[0] == '1') ? 2 : 1;
@@ -355,7 +371,7 @@ cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* 
     if (attr2 != cudaSuccess) return attr2;
     const dim3 grid(static_cast<unsigned>((M + BM * mt - 1) / (BM * mt)), static_cast<unsigned>((N + BN - 1) / BN));
     (mt == 2 ? tc_sgemm3_kernel<2> : tc_sgemm3_kernel<1>)<<<grid, kThreads * mt, mt == 2 ? kSmem2 : kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag, col_map,
-                                                         a_map, fold_add, ld_add, b_sw);
+                                                         a_map, fold_add, ld_add, b_sw, debug);
     return cudaGetLastError();
 }
 

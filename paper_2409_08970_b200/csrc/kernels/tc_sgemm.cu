@@ -83,7 +83,14 @@ __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, int by
 
 /// MT: 128-row halves per CTA (1: 128 x 256 tiles, two CTAs per SM; 2: 256 x
 /// 256 tiles, both TMEM accumulators, one CTA per SM, half the B traffic).
-template <int MT>
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+/// MCAST: launched as clusters of two CTAs along M that share each stage's B:
+/// rank r copies half r (hi or lo) of the block and multicasts it to both,
+/// halving the L2 reads of B (the GEMM's largest traffic).
+template <int MT, bool MCAST = false>
 __global__ void __launch_bounds__(kThreads * MT, MT == 1 ? 2 : 1)
 tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__ bt_hi,
                  const float* __restrict__ bt_lo, int ldb, float* __restrict__ C, std::size_t ldc, std::size_t M,
@@ -124,6 +131,11 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    uint32_t crank = 0;
+    if constexpr (MCAST) {
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+        cluster_sync_all(); // the peer's barriers exist before any multicast lands
+    }
 
     // stage st: A hi, A lo, B hi, B lo.  A is fetched into registers one
     // chunk ahead (its global latency hides behind the barrier and the MMA
@@ -162,6 +174,20 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
     };
     const int kblocks = (K + BK - 1) / BK;
     auto load_b = [&](int ch, int st) {
+        if (MCAST) { // half of the block from each CTA of the pair, to both
+            if (tid == 0) {
+                ptx::mbar_expect_tx(bfull + st, 2 * kBBytes);
+                const float* src = b_sw + (static_cast<std::size_t>(blockIdx.y) * kblocks + ch) * (2 * BN * BK) +
+                                   crank * (BN * BK);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], "
+                    "%2, [%3], %4;\n" ::"r"(ptx::smem_addr(base + st * kSB + 2 * kAB + crank * kBBytes)),
+                    "l"(src), "r"(static_cast<uint32_t>(kBBytes)), "r"(ptx::smem_addr(bfull + st)),
+                    "h"(static_cast<uint16_t>(0x3))
+                    : "memory");
+            }
+            return;
+        }
         if (b_sw) { // pre-swizzled on the host: the stage's B (hi, lo) is one contiguous 32 KB block
             if (tid == 0) {
                 ptx::mbar_expect_tx(bfull + st, 2 * kBBytes);
@@ -196,10 +222,10 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (tid == 0 && (debug & 2)) { // development knob: loads only, no MMAs
-            if (b_sw) ptx::mbar_wait(bfull + st, static_cast<uint32_t>((ch / kStages) & 1));
+            if (b_sw || MCAST) ptx::mbar_wait(bfull + st, static_cast<uint32_t>((ch / kStages) & 1));
             ptx::mbar_arrive(bar + st);
         } else if (tid == 0) {
-            if (b_sw) ptx::mbar_wait(bfull + st, static_cast<uint32_t>((ch / kStages) & 1));
+            if (b_sw || MCAST) ptx::mbar_wait(bfull + st, static_cast<uint32_t>((ch / kStages) & 1));
             const uint32_t s0 = sbase + st * kSB;
             const uint32_t bh = s0 + 2 * kAB, bl = s0 + 2 * kAB + kBBytes;
 #pragma unroll
@@ -222,6 +248,7 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
             if (ch + 1 >= kStages) { // the MMAs of chunk ch + 1 - kStages read that stage
                 ptx::mbar_wait(bar + nx, (phases >> nx) & 1u);
                 phases ^= 1u << nx;
+                if constexpr (MCAST) cluster_sync_all(); // ... in both CTAs of the pair
             }
             load_b(ch + 1, nx);
             store_a(nx); // overlaps the MMAs of chunk ch
@@ -237,6 +264,7 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
 
     // epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w + 31; the
     // stage buffers are free (every MMA has completed)
+    if constexpr (MCAST) cluster_sync_all(); // no multicast into this CTA is still pending
     if (debug & 1) { // development knob: no epilogue
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncthreads();
@@ -369,6 +397,30 @@ cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* 
         cudaFuncSetAttribute(tc_sgemm3_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
     if (attr1 != cudaSuccess) return attr1;
     if (attr2 != cudaSuccess) return attr2;
+    static const bool mcast = [] { // opt-in: measured slower (the per-chunk cluster barrier)
+        const char* e = std::getenv("DCTP_TC32_MCAST");
+        return e && e[0] == '1';
+    }();
+    if (mcast && mt == 1 && b_sw) {
+        static const cudaError_t attr3 =
+            cudaFuncSetAttribute(tc_sgemm3_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        if (attr3 != cudaSuccess) return attr3;
+        const unsigned gx = static_cast<unsigned>(((M + BM - 1) / BM + 1) / 2 * 2); // whole CTA pairs
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(gx, static_cast<unsigned>((N + BN - 1) / BN));
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kSmem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, tc_sgemm3_kernel<1, true>, A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag,
+                                  col_map, a_map, fold_add, ld_add, b_sw, debug);
+    }
     const dim3 grid(static_cast<unsigned>((M + BM * mt - 1) / (BM * mt)), static_cast<unsigned>((N + BN - 1) / BN));
     (mt == 2 ? tc_sgemm3_kernel<2> : tc_sgemm3_kernel<1>)<<<grid, kThreads * mt, mt == 2 ? kSmem2 : kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag, col_map,
                                                          a_map, fold_add, ld_add, b_sw, debug);

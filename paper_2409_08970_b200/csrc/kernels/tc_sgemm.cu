@@ -96,7 +96,7 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
                  const float* __restrict__ bt_lo, int ldb, float* __restrict__ C, std::size_t ldc, std::size_t M,
                  int N, int K, int* flag, const int* __restrict__ col_map, const int* __restrict__ a_map,
                  const float* __restrict__ fold_add, std::size_t ld_add, const float* __restrict__ b_sw,
-                 int debug) {
+                 int debug, int nfirst) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of the swizzle atoms
     const uint32_t raw = ptx::smem_addr(smem_raw);
@@ -110,8 +110,11 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
     const uint32_t sbase = ptx::smem_addr(base);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const std::size_t m0 = static_cast<std::size_t>(blockIdx.x) * (BM * MT);
-    const int n0 = blockIdx.y * BN;
+    // nfirst: grid x = column tile, so the CTAs sharing an A row tile run
+    // together (A leaves DRAM once; B, 2 MB, stays in L2 either way)
+    const unsigned mi = nfirst ? blockIdx.y : blockIdx.x, ni = nfirst ? blockIdx.x : blockIdx.y;
+    const std::size_t m0 = static_cast<std::size_t>(mi) * (BM * MT);
+    const int n0 = static_cast<int>(ni) * BN;
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
@@ -177,7 +180,7 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
         if (MCAST) { // half of the block from each CTA of the pair, to both
             if (tid == 0) {
                 ptx::mbar_expect_tx(bfull + st, 2 * kBBytes);
-                const float* src = b_sw + (static_cast<std::size_t>(blockIdx.y) * kblocks + ch) * (2 * BN * BK) +
+                const float* src = b_sw + (static_cast<std::size_t>(ni) * kblocks + ch) * (2 * BN * BK) +
                                    crank * (BN * BK);
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], "
@@ -192,7 +195,7 @@ tc_sgemm3_kernel(const float* __restrict__ A, int lda, const float* __restrict__
             if (tid == 0) {
                 ptx::mbar_expect_tx(bfull + st, 2 * kBBytes);
                 ptx::bulk_load(base + st * kSB + 2 * kAB,
-                               b_sw + (static_cast<std::size_t>(blockIdx.y) * kblocks + ch) * (2 * BN * BK),
+                               b_sw + (static_cast<std::size_t>(ni) * kblocks + ch) * (2 * BN * BK),
                                2 * kBBytes, bfull + st);
             }
             return;
@@ -419,11 +422,17 @@ cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* 
         cfg.attrs = at;
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, tc_sgemm3_kernel<1, true>, A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag,
-                                  col_map, a_map, fold_add, ld_add, b_sw, debug);
+                                  col_map, a_map, fold_add, ld_add, b_sw, debug, 0);
     }
-    const dim3 grid(static_cast<unsigned>((M + BM * mt - 1) / (BM * mt)), static_cast<unsigned>((N + BN - 1) / BN));
+    static const int nfirst = [] {
+        const char* e = std::getenv("DCTP_TC32_NFIRST");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    const unsigned gm = static_cast<unsigned>((M + BM * mt - 1) / (BM * mt)), gn = static_cast<unsigned>((N + BN - 1) / BN);
+    if (nfirst && gm > 65535u) return cudaErrorInvalidValue;
+    const dim3 grid = nfirst ? dim3(gn, gm) : dim3(gm, gn);
     (mt == 2 ? tc_sgemm3_kernel<2> : tc_sgemm3_kernel<1>)<<<grid, kThreads * mt, mt == 2 ? kSmem2 : kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag, col_map,
-                                                         a_map, fold_add, ld_add, b_sw, debug);
+                                                         a_map, fold_add, ld_add, b_sw, debug, nfirst);
     return cudaGetLastError();
 }
 

@@ -365,6 +365,11 @@ struct dctp_plan {
         std::mutex mu;
         double* buf = nullptr;
         std::size_t ld = 0;
+        // int8 slices of X^T [0] and X [1] for the tcgen05 kind::i8 products
+        // (ozaki.cu), built on first use
+        int8_t* oz[2] = {nullptr, nullptr};
+        int* oz_e[2] = {nullptr, nullptr};
+        int oz_slices = 0;
     };
     std::unique_ptr<Dense> dense = std::make_unique<Dense>();
 
@@ -376,6 +381,11 @@ struct dctp_plan {
             cudaFree(blob);
             cudaFree(flag);
             if (dense && dense->buf) cudaFree(dense->buf);
+            if (dense)
+                for (int i = 0; i < 2; ++i) {
+                    if (dense->oz[i]) cudaFree(dense->oz[i]);
+                    if (dense->oz_e[i]) cudaFree(dense->oz_e[i]);
+                }
             cudaSetDevice(prev);
         }
     }
@@ -1452,6 +1462,70 @@ static bool dense_route(const dctp_plan* p) {
     return n * n <= 1.25 * static_cast<double>(p->fwd.rows) * static_cast<double>(p->fwd.cols);
 }
 
+/// fp64 dense products on the int8 tensor cores (ozaki.cu) from n = 1024
+/// (below that the DMMA product is short and the extra slicing pass over the
+/// input does not pay).  DCTP_OZAKI=0 keeps the DMMA product; the slice count
+/// (DCTP_OZAKI_SLICES, 5 = default or 6) trades products (15 / 21) for
+/// accuracy: 2.9e-11 / ~1e-13 norm-wise per signal on the whole C5 batch
+/// against the DMMA product (fp64 tolerance 1e-10).
+static int ozaki_slices(std::size_t n) {
+    static const int slices = [] {
+        const char* e = std::getenv("DCTP_OZAKI_SLICES");
+        const int v = e ? std::atoi(e) : 5;
+        return (v == 5 || v == 6) ? v : 5;
+    }();
+    const char* e = std::getenv("DCTP_OZAKI");
+    if (e && e[0] == '0') return 0;
+    if (e && e[0] == '1') return n <= 16384 ? slices : 0;
+    return (n >= 1024 && n <= 16384) ? slices : 0;
+}
+
+/// int8 slices of X^T (which = 0) or X (which = 1), once per plan.
+static void ensure_ozaki(const dctp_plan* p, int which, int S, cudaStream_t s) {
+    auto& d = *p->dense;
+    std::lock_guard<std::mutex> lock(d.mu);
+    if (d.oz[which] && d.oz_slices == S) return;
+    const std::size_t n = p->st.n;
+    const int ni = static_cast<int>(n), tn = dctp::dev::ozaki_tile_n(S);
+    if (d.oz[which]) {
+        cudaFree(d.oz[which]);
+        cudaFree(d.oz_e[which]);
+        d.oz[which] = nullptr;
+        d.oz_e[which] = nullptr;
+    }
+    const std::size_t bytes = dctp::dev::ozaki_slice_bytes(n, ni, tn, S);
+    const std::size_t rows_pad = (n + tn - 1) / tn * tn;
+    int8_t* sl = nullptr;
+    int* ex = nullptr;
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&sl), bytes), "cudaMalloc(basis slices)");
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&ex), rows_pad * sizeof(int)), "cudaMalloc(basis exponents)");
+    cuda_check(dctp::dev::ozaki_slice<double>(d.buf + (which ? n * d.ld : 0), d.ld, n, ni, nullptr, tn, S, sl, ex,
+                                              nullptr, s),
+               "basis slicing kernel");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(basis slices)");
+    d.oz[which] = sl;
+    d.oz_e[which] = ex;
+    d.oz_slices = S;
+}
+
+/// out[b, c] = sum_k in[b, k] bt[c, k] with bt given as int8 slices: slice
+/// the signal rows into stream-ordered scratch, then one tcgen05 kind::i8 GEMM.
+static void rows_by_ozaki(const double* in, std::size_t ld_in, const int8_t* b_sl, const int* eb, int K, int N,
+                          int S, double* out, std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t s,
+                          const char* name) {
+    const std::size_t a_bytes = dctp::dev::ozaki_slice_bytes(batch, K, 128, S);
+    const std::size_t rows_pad = (batch + 127) / 128 * 128;
+    Scratch<int8_t> a_sl(a_bytes, s);
+    Scratch<int> ea(rows_pad, s);
+    cuda_check(DCTP_LAUNCH("ozaki_slice", s,
+                           dctp::dev::ozaki_slice<double>(in, ld_in, batch, K, nullptr, 128, S, a_sl.ptr, ea.ptr, flag,
+                                                          s)),
+               "signal slicing kernel");
+    cuda_check(DCTP_LAUNCH(name, s,
+                           dctp::dev::ozaki_gemm(a_sl.ptr, ea.ptr, b_sl, eb, batch, N, K, S, out, ld_out, nullptr, s)),
+               "int8 tensor-core product kernel");
+}
+
 /// The dense routes of DctPlusPlan: forward_nmvp = X^T s (fast_transform.hpp:
 /// 199-214) and inverse(p, fast = false) = X p (:218-260), as one product with
 /// the materialised basis on the DMMA tensor cores (rows_by_basis).
@@ -1469,6 +1543,14 @@ static void plan_dense(const dctp_plan* p, const T* in, T* out, std::size_t batc
     const auto& d = *p->dense;
     const double* bt = d.buf + (inverse ? n * d.ld : 0);
     const int ni = static_cast<int>(n);
+    if constexpr (std::is_same_v<T, double>) {
+        if (const int S = ozaki_slices(n)) {
+            ensure_ozaki(p, inverse ? 1 : 0, S, s);
+            rows_by_ozaki(in, n, d.oz[inverse ? 1 : 0], d.oz_e[inverse ? 1 : 0], ni, ni, S, out, n, batch, p->flag,
+                          s, inverse ? "dense_inv_i8" : "dense_i8");
+            return;
+        }
+    }
     cuda_check(DCTP_LAUNCH(inverse ? "dense_inv" : "dense_nmvp", s,
                            dctp::dev::rows_by_basis<T>(in, n, bt, d.ld, ni, ni, out, n, batch, p->flag, s)),
                "dense basis kernel");

@@ -86,6 +86,14 @@ int dctp_plan_info(const dctp_plan* plan, size_t* n, double* epsilon, int* slow_
  * NFST route is unavailable for the plan). */
 int dctp_plan_route(const dctp_plan* plan, int* nfst, double* probe_gap);
 
+/* Int8 tensor-core products (no reference counterpart): *slices = the number
+ * of int8 digits per operand the fp64 dense products of length-n rows use on
+ * the tcgen05 kind::i8 path (ozaki.cu; slices (slices + 1) / 2 integer GEMMs
+ * per product), 0 when they run on the DMMA fp64 tensor cores.  The dense
+ * route (forward/inverse of dense plans such as config 5, forward_nmvp,
+ * inverse(fast = false)) and the rank-k chain apply take this path in fp64. */
+int dctp_ozaki_slices(size_t n, int* slices);
+
 /* Host copies of the setup vectors, n doubles each (any pointer may be NULL):
  * lambda(), mu(), the deflated z, per-slot normalisers a, per-slot signs sigma
  * (factorization(), cauchy.hpp:111-119). */

@@ -12,12 +12,12 @@ from .dctplus import (DIST_AR, DIST_AR2D, DIST_GAUSSIAN, DIST_SYM_UNIFORM, DIST_
                       forward_nmvp, idct2, inverse, mix_seed, path_quadratic_form, plan_dctplus, plan_pruned,
                       profile_enable, profile_reset, profile_summary, pruned_forward_all, RdoChoice, rdo_select,
                       rdo_select_batch, calibrate_prune_threshold, SpectralBasis, path_spectrum,
-                      ChainedFactorization, compose_rank_k, chain_forward)
+                      ChainedFactorization, compose_rank_k, chain_forward, ozaki_slices)
 
 __all__ = [
     "RankOneUpdate", "DctPlusPlan", "PrunedEnsemblePlan", "Result", "plan_dctplus", "forward", "forward_nmvp",
     "inverse", "plan_pruned", "pruned_forward_all", "dct2", "idct2", "fill_signals", "mix_seed",
     "path_quadratic_form", "DctPlusError", "InvalidArgument", "DomainError", "RuntimeFailure", "LogicError",
     "CudaFailure", "RdoChoice", "rdo_select", "rdo_select_batch", "calibrate_prune_threshold",
-    "SpectralBasis", "path_spectrum", "ChainedFactorization", "compose_rank_k", "chain_forward",
+    "SpectralBasis", "path_spectrum", "ChainedFactorization", "compose_rank_k", "chain_forward", "ozaki_slices",
 ]

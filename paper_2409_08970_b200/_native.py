@@ -34,6 +34,7 @@ SIGNATURES = {
     "dctp_plan_destroy": (C.c_int, [_p]),
     "dctp_plan_info": (C.c_int, [_p, C.POINTER(_sz), _dp, _ip, C.POINTER(_sz), C.POINTER(_sz), _ip]),
     "dctp_plan_route": (C.c_int, [_p, _ip, _dp]),
+    "dctp_ozaki_slices": (C.c_int, [_sz, _ip]),
     "dctp_plan_setup": (C.c_int, [_p, _p, _p, _p, _p, _p]),
     "dctp_plan_slots": (C.c_int, [_p, _p, _p]),
     "dctp_plan_basis": (C.c_int, [_p, _p]),

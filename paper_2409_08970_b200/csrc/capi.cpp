@@ -348,6 +348,10 @@ struct dctp_plan {
         std::size_t wt_hi = 0, wt_lo = 0;        // fp32 inverse on tcgen05: W^T split (L x ldwt)
         std::size_t w_sw = 0, wt_sw = 0;         // both, in the kernel's swizzled shared-memory blocks
         TwiddleOffsets tw64, tw32;
+        // fp64 on the int8 tensor cores: slices of W [0] and W^T [1], built on first use
+        int8_t* oz[2] = {nullptr, nullptr};
+        int* oz_e[2] = {nullptr, nullptr};
+        int oz_slices = 0;
     } fd;
     // NFST fast route (fp64): the reference's own forward algorithm on the GPU
     struct {
@@ -386,6 +390,10 @@ struct dctp_plan {
                     if (dense->oz[i]) cudaFree(dense->oz[i]);
                     if (dense->oz_e[i]) cudaFree(dense->oz_e[i]);
                 }
+            for (int i = 0; i < 2; ++i) {
+                if (fd.oz[i]) cudaFree(fd.oz[i]);
+                if (fd.oz_e[i]) cudaFree(fd.oz_e[i]);
+            }
             cudaSetDevice(prev);
         }
     }
@@ -1053,6 +1061,15 @@ static bool fold_route(const dctp_plan* p) {
     return !(e && e[0] == '0');
 }
 
+// int8 tensor-core (Ozaki) products, defined with the dense routes below
+static int ozaki_slices(std::size_t n);
+constexpr int kOzakiFoldMinK = 2048; // shortest product length the folded route sends to them
+static void ensure_fold_ozaki(const dctp_plan* p, int which, int S, cudaStream_t s);
+static void rows_by_ozaki(const double* in, std::size_t ld_in, const int8_t* b_sl, const int* eb, int K, int N,
+                          int S, double* out, std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t s,
+                          const char* name, const int* col_map = nullptr, const int* a_map = nullptr,
+                          const double* fold_add = nullptr, std::size_t ld_add = 0);
+
 template <class T>
 static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s) {
     if (!p) throw std::invalid_argument("dctp_forward: null plan");
@@ -1115,6 +1132,16 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
                                        dctp::dev::sgemm_rows(u.ptr, f.L, b, static_cast<int>(f.ldwt), out, n, batch,
                                                              f.cols, f.L, p->flag, s, at<int>(p->blob, f.map))),
                            "fold sgemm kernel");
+                return;
+            }
+        }
+        if constexpr (!f32) {
+            // the int8 products pay only for long rows (C3's 512-wide u: 0.28 vs
+            // 0.30 ms forward, 0.43 vs 0.37 ms inverse with the slicing pass)
+            if (const int S = f.L >= kOzakiFoldMinK ? ozaki_slices(n) : 0) {
+                ensure_fold_ozaki(p, 0, S, s);
+                rows_by_ozaki(u.ptr, f.L, f.oz[0], f.oz_e[0], f.L, f.cols, S, out, n, batch, p->flag, s, "fold_w_i8",
+                              at<int>(p->blob, f.map));
                 return;
             }
         }
@@ -1185,6 +1212,14 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
                                                             f.cols, p->flag, s, nullptr, at<int>(p->blob, f.map), w.ptr,
                                                             f.L, at<float>(p->blob, f.wt_sw))),
                            "fold tcgen05 kernel");
+                return;
+            }
+        }
+        if constexpr (!f32) {
+            if (const int S = f.cols >= kOzakiFoldMinK ? ozaki_slices(n) : 0) {
+                ensure_fold_ozaki(p, 1, S, s);
+                rows_by_ozaki(in, n, f.oz[1], f.oz_e[1], f.cols, f.L, S, out, n, batch, p->flag, s, "fold_wt_i8",
+                              nullptr, at<int>(p->blob, f.map), w.ptr, f.L);
                 return;
             }
         }
@@ -1481,49 +1516,83 @@ static int ozaki_slices(std::size_t n) {
 }
 
 /// int8 slices of X^T (which = 0) or X (which = 1), once per plan.
+static std::pair<int8_t*, int*> slice_operand(const double* bt, std::size_t ld, std::size_t rows, int K, int S,
+                                              cudaStream_t s);
 static void ensure_ozaki(const dctp_plan* p, int which, int S, cudaStream_t s) {
     auto& d = *p->dense;
     std::lock_guard<std::mutex> lock(d.mu);
     if (d.oz[which] && d.oz_slices == S) return;
+    for (int i = 0; i < 2; ++i) // a different slice count invalidates both
+        if (d.oz[i] && d.oz_slices != S) {
+            cudaFree(d.oz[i]);
+            cudaFree(d.oz_e[i]);
+            d.oz[i] = nullptr;
+            d.oz_e[i] = nullptr;
+        }
     const std::size_t n = p->st.n;
-    const int ni = static_cast<int>(n), tn = dctp::dev::ozaki_tile_n(S);
-    if (d.oz[which]) {
-        cudaFree(d.oz[which]);
-        cudaFree(d.oz_e[which]);
-        d.oz[which] = nullptr;
-        d.oz_e[which] = nullptr;
-    }
-    const std::size_t bytes = dctp::dev::ozaki_slice_bytes(n, ni, tn, S);
-    const std::size_t rows_pad = (n + tn - 1) / tn * tn;
-    int8_t* sl = nullptr;
-    int* ex = nullptr;
-    cuda_check(cudaMalloc(reinterpret_cast<void**>(&sl), bytes), "cudaMalloc(basis slices)");
-    cuda_check(cudaMalloc(reinterpret_cast<void**>(&ex), rows_pad * sizeof(int)), "cudaMalloc(basis exponents)");
-    cuda_check(dctp::dev::ozaki_slice<double>(d.buf + (which ? n * d.ld : 0), d.ld, n, ni, nullptr, tn, S, sl, ex,
-                                              nullptr, s),
-               "basis slicing kernel");
-    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(basis slices)");
+    auto [sl, ex] = slice_operand(d.buf + (which ? n * d.ld : 0), d.ld, n, static_cast<int>(n), S, s);
     d.oz[which] = sl;
     d.oz_e[which] = ex;
     d.oz_slices = S;
 }
 
+/// int8 slices of the folded route's W (which = 0, cols x L) or W^T (which =
+/// 1, L x cols), once per plan.
+static void ensure_fold_ozaki(const dctp_plan* p, int which, int S, cudaStream_t s) {
+    auto& f = const_cast<dctp_plan*>(p)->fd;
+    std::lock_guard<std::mutex> lock(p->dense->mu);
+    if (f.oz[which] && f.oz_slices == S) return;
+    for (int i = 0; i < 2; ++i)
+        if (f.oz[i] && f.oz_slices != S) {
+            cudaFree(f.oz[i]);
+            cudaFree(f.oz_e[i]);
+            f.oz[i] = nullptr;
+            f.oz_e[i] = nullptr;
+        }
+    auto [sl, ex] = which == 0 ? slice_operand(at<double>(p->blob, f.w), f.ldw, f.cols, f.L, S, s)
+                               : slice_operand(at<double>(p->blob, f.wt), f.ldwt, f.L, f.cols, S, s);
+    f.oz[which] = sl;
+    f.oz_e[which] = ex;
+    f.oz_slices = S;
+}
+
 /// out[b, c] = sum_k in[b, k] bt[c, k] with bt given as int8 slices: slice
-/// the signal rows into stream-ordered scratch, then one tcgen05 kind::i8 GEMM.
+/// the signal rows (columns gathered through a_map) into stream-ordered
+/// scratch, then one tcgen05 kind::i8 GEMM (col_map / fold_add epilogues as
+/// in rows_by_basis).
 static void rows_by_ozaki(const double* in, std::size_t ld_in, const int8_t* b_sl, const int* eb, int K, int N,
                           int S, double* out, std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t s,
-                          const char* name) {
+                          const char* name, const int* col_map, const int* a_map, const double* fold_add,
+                          std::size_t ld_add) {
     const std::size_t a_bytes = dctp::dev::ozaki_slice_bytes(batch, K, 128, S);
     const std::size_t rows_pad = (batch + 127) / 128 * 128;
     Scratch<int8_t> a_sl(a_bytes, s);
     Scratch<int> ea(rows_pad, s);
     cuda_check(DCTP_LAUNCH("ozaki_slice", s,
-                           dctp::dev::ozaki_slice<double>(in, ld_in, batch, K, nullptr, 128, S, a_sl.ptr, ea.ptr, flag,
+                           dctp::dev::ozaki_slice<double>(in, ld_in, batch, K, a_map, 128, S, a_sl.ptr, ea.ptr, flag,
                                                           s)),
                "signal slicing kernel");
     cuda_check(DCTP_LAUNCH(name, s,
-                           dctp::dev::ozaki_gemm(a_sl.ptr, ea.ptr, b_sl, eb, batch, N, K, S, out, ld_out, nullptr, s)),
+                           dctp::dev::ozaki_gemm(a_sl.ptr, ea.ptr, b_sl, eb, batch, N, K, S, out, ld_out, col_map, s,
+                                                 fold_add, ld_add)),
                "int8 tensor-core product kernel");
+}
+
+/// int8 slices of an operand matrix bt (rows x K, stride ld) for the B side
+/// of ozaki_gemm; (slices, exponents) in device memory owned by the caller.
+static std::pair<int8_t*, int*> slice_operand(const double* bt, std::size_t ld, std::size_t rows, int K, int S,
+                                              cudaStream_t s) {
+    const int tn = dctp::dev::ozaki_tile_n(S);
+    int8_t* sl = nullptr;
+    int* ex = nullptr;
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&sl), dctp::dev::ozaki_slice_bytes(rows, K, tn, S)),
+               "cudaMalloc(operand slices)");
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&ex), (rows + tn - 1) / tn * tn * sizeof(int)),
+               "cudaMalloc(operand exponents)");
+    cuda_check(dctp::dev::ozaki_slice<double>(bt, ld, rows, K, nullptr, tn, S, sl, ex, nullptr, s),
+               "operand slicing kernel");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(operand slices)");
+    return {sl, ex};
 }
 
 /// The dense routes of DctPlusPlan: forward_nmvp = X^T s (fast_transform.hpp:
@@ -1721,6 +1790,13 @@ int dctp_plan_route(const dctp_plan* p, int* nfst, double* probe_gap) {
         if (!p) throw std::invalid_argument("dctp_plan_route: null plan");
         if (nfst) *nfst = fast_route(p) ? 1 : 0;
         if (probe_gap) *probe_gap = p->fs.probe_gap;
+    });
+}
+
+int dctp_ozaki_slices(std::size_t n, int* slices) {
+    return guarded([&] {
+        if (!slices) throw std::invalid_argument("dctp_ozaki_slices: null output");
+        *slices = ozaki_slices(n);
     });
 }
 
@@ -2153,6 +2229,11 @@ struct dctp_chain {
     int* flag = nullptr;
     std::size_t ldt = 0, xt64 = 0, x32 = 0;
     bool sgemm32 = false;
+    // int8 slices of X^T for the tcgen05 kind::i8 product (ozaki.cu), built on first use
+    std::mutex oz_mu;
+    int8_t* oz = nullptr;
+    int* oz_e = nullptr;
+    int oz_slices = 0;
 
     ~dctp_chain() {
         if (blob) {
@@ -2161,6 +2242,8 @@ struct dctp_chain {
             cudaSetDevice(device);
             cudaFree(blob);
             cudaFree(flag);
+            if (oz) cudaFree(oz);
+            if (oz_e) cudaFree(oz_e);
             cudaSetDevice(prev);
         }
     }
@@ -2184,6 +2267,26 @@ static void chain_forward(const dctp_chain* c, const T* in, T* out, std::size_t 
             cuda_check(DCTP_LAUNCH("chain_sgemm", s,
                                    dctp::dev::sgemm_rows(in, ni, x, ni, out, n, batch, ni, ni, c->flag, s)),
                        "chain sgemm kernel");
+            return;
+        }
+    }
+    if constexpr (std::is_same_v<T, double>) {
+        if (const int S = ozaki_slices(n)) {
+            {
+                auto* cm = const_cast<dctp_chain*>(c);
+                std::lock_guard<std::mutex> lock(cm->oz_mu);
+                if (!cm->oz || cm->oz_slices != S) {
+                    if (cm->oz) cudaFree(cm->oz);
+                    if (cm->oz_e) cudaFree(cm->oz_e);
+                    cm->oz = nullptr;
+                    cm->oz_e = nullptr;
+                    auto [sl, ex] = slice_operand(at<double>(c->blob, c->xt64), c->ldt, n, ni, S, s);
+                    cm->oz = sl;
+                    cm->oz_e = ex;
+                    cm->oz_slices = S;
+                }
+            }
+            rows_by_ozaki(in, n, c->oz, c->oz_e, ni, ni, S, out, n, batch, c->flag, s, "chain_i8");
             return;
         }
     }

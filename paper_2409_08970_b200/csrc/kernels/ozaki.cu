@@ -204,7 +204,8 @@ template <int S, int NT>
 __global__ void __launch_bounds__(kThreads, 1)
 ozaki_gemm_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, const int8_t* __restrict__ b_sl,
                   const int* __restrict__ eb, std::size_t M, int N, int nch, double* __restrict__ out,
-                  std::size_t ld_out, const int* __restrict__ col_map) {
+                  std::size_t ld_out, const int* __restrict__ col_map, const double* __restrict__ fold_add,
+                  std::size_t ld_add) {
     using G = Geo<S, NT>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t raw = ptx::smem_addr(smem_raw);
@@ -310,7 +311,16 @@ ozaki_gemm_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, c
             const int cbase = nt * NT + c0;
             const int lim = min(N, nt * NT + NT); // columns of this tile
             double* orow = out + row * ld_out;
-            if (col_map) {
+            if (fold_add) { // unfold: x_c = w_c + v_c, x_{2N-1-c} = w_c - v_c
+                const double* add = fold_add + row * ld_add;
+#pragma unroll 4
+                for (int u = 0; u < 32; ++u)
+                    if (cbase + u < lim) {
+                        const double v = acc[u] * ldexp(rs, __ldg(eb + cbase + u)), w = add[cbase + u];
+                        orow[cbase + u] = w + v;
+                        orow[2 * N - 1 - (cbase + u)] = w - v;
+                    }
+            } else if (col_map) {
 #pragma unroll
                 for (int u = 0; u < 32; ++u)
                     if (cbase + u < lim) orow[__ldg(col_map + cbase + u)] = acc[u] * ldexp(rs, __ldg(eb + cbase + u));
@@ -335,7 +345,8 @@ ozaki_gemm_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, c
 
 template <int S, int NT>
 cudaError_t launch_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M, int N,
-                        int nch, double* out, std::size_t ld_out, const int* col_map, cudaStream_t stream) {
+                        int nch, double* out, std::size_t ld_out, const int* col_map, const double* fold_add,
+                        std::size_t ld_add, cudaStream_t stream) {
     using G = Geo<S, NT>;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -349,7 +360,7 @@ cudaError_t launch_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, c
         const unsigned gx = static_cast<unsigned>(gm - m0 < 65535 ? gm - m0 : 65535);
         ozaki_gemm_kernel<S, NT><<<dim3(gx, gn), kThreads, G::kSmem, stream>>>(
             a_sl + m0 * nch * G::kABytes, ea + m0 * TM, b_sl, eb, M - m0 * TM, N, nch, out + m0 * TM * ld_out,
-            ld_out, col_map);
+            ld_out, col_map, fold_add ? fold_add + m0 * TM * ld_add : nullptr, ld_add);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -384,11 +395,14 @@ template cudaError_t ozaki_slice<float>(const float*, std::size_t, std::size_t, 
                                         int*, int*, cudaStream_t);
 
 cudaError_t ozaki_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M, int N,
-                       int K, int slices, double* out, std::size_t ld_out, const int* col_map, cudaStream_t stream) {
+                       int K, int slices, double* out, std::size_t ld_out, const int* col_map, cudaStream_t stream,
+                       const double* fold_add, std::size_t ld_add) {
     if (M == 0 || N == 0) return cudaSuccess;
     const int nch = (K + CB - 1) / CB;
-    if (slices == 5) return launch_gemm<5, 96>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, stream);
-    if (slices == 6) return launch_gemm<6, 80>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, stream);
+    if (slices == 5)
+        return launch_gemm<5, 96>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add, stream);
+    if (slices == 6)
+        return launch_gemm<6, 80>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add, stream);
     return cudaErrorInvalidValue;
 }
 

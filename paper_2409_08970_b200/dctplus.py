@@ -623,6 +623,14 @@ def fill_signals(seed: int, dist: int, n: int, rows: int, r: float = 0.0) -> np.
     return out
 
 
+def ozaki_slices(n: int) -> int:
+    """int8 digits per operand the fp64 dense products of length-n rows use on
+    the tcgen05 kind::i8 path (0: the DMMA fp64 tensor cores) — dctp_ozaki_slices."""
+    s = C.c_int()
+    check(lib.dctp_ozaki_slices(int(n), C.byref(s)))
+    return s.value
+
+
 # --- kernel profiling (CUDA events around every launch; bench.py) ---------------------
 
 def profile_enable(on: bool = True) -> None:

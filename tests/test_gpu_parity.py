@@ -490,7 +490,8 @@ def test_chain_forward_matches_reference(P, torch, reference, case, dtype, tol):
 def test_chain_forward_full_batch_properties(P, torch):
     """n = 1024, k = 3, 16384 signals: the composed basis is orthogonal, so
     ||chain_forward(s)|| = ||s|| per signal (Parseval) and the rows agree with
-    x^T s computed by torch in fp64 on a sample."""
+    x^T s computed by torch in fp64 on a sample (fp64 tolerance: the product
+    runs on the int8 tensor cores, ~3e-11 of the row maxima)."""
     n = 1024
     ups = [P.RankOneUpdate.self_loop(1, 1.5), P.RankOneUpdate.edge_delta(1, n, -0.5),
            P.RankOneUpdate.edge_delta(300, 700, 0.25)]
@@ -505,7 +506,7 @@ def test_chain_forward_full_batch_properties(P, torch):
     assert float(rel.max()) < 1e-12 + n * orth
     ref = s[:512] @ x
     assert orth < 1e-7  # 3.5e-9 here: the reference chain has no re-orthogonalisation
-    assert float(((y[:512] - ref).abs().max(dim=1).values / ref.abs().max(dim=1).values).max()) < 1e-12
+    assert float(((y[:512] - ref).abs().max(dim=1).values / ref.abs().max(dim=1).values).max()) < TOL64
 
 
 def test_chain_forward_views_nan_and_empty(P, torch, reference):
@@ -578,7 +579,9 @@ def test_dense_route_selected_for_full_updates(P, torch, reference, monkeypatch,
             P.profile_enable(True)
             plan.forward(dev(torch, s, torch.float64))
             P.profile_enable(False)
-            assert set(P.profile_summary()) == {"dense_nmvp"}
+            # fp64 dense products run on the int8 tensor cores from n = 1024
+            want_k = {"dense_i8", "ozaki_slice"} if P.ozaki_slices(n) else {"dense_nmvp"}
+            assert set(P.profile_summary()) == want_k
     monkeypatch.delenv("DCTP_DENSE")
 
 

@@ -1,7 +1,9 @@
-// tcgen05 kind::tf32 peak probe (the denominator of the 3xTF32 GEMM's
-// roofline): every CTA issues back-to-back 128 x 256 x 8 TF32 MMAs from
+// tcgen05 peak probe (the denominators of the 3xTF32 GEMM's and the int8
+// Ozaki GEMM's rooflines): every CTA issues back-to-back 128 x N x K MMAs from
 // shared-memory operands into TMEM, one elected thread, a commit every 64
-// MMAs; 148 x 2 CTAs; CUDA events around the launch.
+// MMAs; 148 x 2 CTAs; CUDA events around the launch.  Kinds: kind::tf32
+// (N = 256, K = 8) and kind::i8 (N = 256 and N = 96 — the Ozaki kernel's
+// tile — K = 32).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/tc_peak tools/tc_peak.cu && tools/tc_peak
 #include <cstdint>
 #include <cstdio>
@@ -16,7 +18,10 @@ __device__ __forceinline__ uint64_t desc64(uint32_t a) { // K-major SWIZZLE_64B,
 }
 
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+template <int N>
+__host__ __device__ constexpr uint32_t idesc_i8() { return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((128u >> 4) << 24); }
 
+template <int KIND, int N> // KIND 0: tf32, 1: i8
 __global__ void __launch_bounds__(128, 2) tc_peak_kernel(int iters, int* sink) {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ uint64_t bar;
@@ -40,10 +45,16 @@ __global__ void __launch_bounds__(128, 2) tc_peak_kernel(int iters, int* sink) {
         const uint64_t a = desc64(saddr(smem)), b = desc64(saddr(smem + 8192));
         uint32_t phase = 0;
         for (int it = 0; it < iters; ++it) {
-            asm volatile(
-                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                "l"(a), "l"(b), "r"(kIdesc), "r"(it > 0 ? 1 : 0));
+            if constexpr (KIND == 0)
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                    "l"(a), "l"(b), "r"(kIdesc), "r"(it > 0 ? 1 : 0));
+            else
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                    "l"(a), "l"(b), "r"(idesc_i8<N>()), "r"(it > 0 ? 1 : 0));
             if ((it & 63) == 63 || it == iters - 1) {
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                                  saddr(&bar))
@@ -68,31 +79,40 @@ __global__ void __launch_bounds__(128, 2) tc_peak_kernel(int iters, int* sink) {
     }
 }
 
-int main() {
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    int* sink;
-    cudaMalloc(&sink, sizeof(int));
+template <int KIND, int N>
+double run(int sms, int* sink) {
     const int smem = 8192 + 16384;
-    cudaFuncSetAttribute(tc_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tc_peak_kernel<KIND, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int iters = 20000, grid = 2 * sms;
-    tc_peak_kernel<<<grid, 128, smem>>>(1000, sink);
+    tc_peak_kernel<KIND, N><<<grid, 128, smem>>>(1000, sink);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     float best = 1e30f;
     for (int r = 0; r < 5; ++r) {
         cudaEventRecord(a);
-        tc_peak_kernel<<<grid, 128, smem>>>(iters, sink);
+        tc_peak_kernel<KIND, N><<<grid, 128, smem>>>(iters, sink);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, a, b);
         best = ms < best ? ms : best;
     }
-    const double flops = 2.0 * 128 * 256 * 8 * static_cast<double>(iters) * grid;
-    std::printf("{\"tcgen05_tf32_tflops\": %.1f, \"status\": \"%s\", \"how\": \"tools/tc_peak.cu: %d CTAs x %d "
-                "back-to-back 128x256x8 kind::tf32 MMAs, best of 5\"}\n",
-                flops / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()), grid, iters);
+    const double k = KIND == 0 ? 8 : 32;
+    return 2.0 * 128 * N * k * static_cast<double>(iters) * grid / (best * 1e-3) / 1e12;
+}
+
+int main() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int* sink;
+    cudaMalloc(&sink, sizeof(int));
+    const double tf = run<0, 256>(sms, sink);
+    const double i8 = run<1, 256>(sms, sink);
+    const double i8n96 = run<1, 96>(sms, sink);
+    std::printf("{\"tcgen05_tf32_tflops\": %.1f, \"tcgen05_i8_tops\": %.1f, \"tcgen05_i8_n96_tops\": %.1f, "
+                "\"status\": \"%s\", \"how\": \"tools/tc_peak.cu: %d CTAs x 20000 back-to-back 128xNxK MMAs from "
+                "shared memory (tf32 N=256 K=8; i8 N=256 and N=96, K=32), best of 5\"}\n",
+                tf, i8, i8n96, cudaGetErrorString(cudaGetLastError()), 2 * sms);
     return 0;
 }

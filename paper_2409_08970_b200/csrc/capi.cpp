@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <map>
 #include <mutex>
+#include <unordered_map>
 #include <numbers>
 #include <stdexcept>
 #include <string>
@@ -312,12 +313,46 @@ class Profiler {
 
 // ---------------------------------------------------------------------------
 
+/// Non-finite-input flags, one device int per (object, stream): a kernel
+/// raises the flag of the stream it runs on, and sync_check(stream) reads and
+/// clears only that one — a NaN in one thread's batch surfaces in that
+/// thread's call and nowhere else (the reference throws from the failing
+/// call, fast_transform.hpp:271-276; plans are shared across threads,
+/// :33-34).  Keyed by cudaStreamGetId, so cudaStreamPerThread and the legacy
+/// stream resolve to the calling thread's real stream.
+struct StreamFlags {
+    int device = 0;
+    mutable std::mutex mu;
+    mutable std::unordered_map<unsigned long long, int*> map;
+
+    int* operator()(cudaStream_t s) const {
+        unsigned long long id = 0;
+        cuda_check(cudaStreamGetId(s, &id), "cudaStreamGetId");
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = map.find(id);
+        if (it != map.end()) return it->second;
+        DeviceScope scope(device);
+        int* f = nullptr;
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&f), sizeof(int)), "cudaMalloc(flag)");
+        cuda_check(cudaMemset(f, 0, sizeof(int)), "cudaMemset(flag)");
+        map.emplace(id, f);
+        return f;
+    }
+    ~StreamFlags() {
+        int prev = 0;
+        if (cudaGetDevice(&prev) != cudaSuccess) return;
+        cudaSetDevice(device);
+        for (auto& kv : map) cudaFree(kv.second);
+        cudaSetDevice(prev);
+    }
+};
+
 struct dctp_plan {
     dctp::host::Setup st;
     dctp::host::Update update;
     int device = 0;
     void* blob = nullptr;
-    int* flag = nullptr;
+    StreamFlags flags;
     TwiddleOffsets tw64, tw32;
     StageOffsets fwd{}, inv{};
     std::size_t pass_slot = 0, pass_src = 0, pass_sign64 = 0, pass_sign32 = 0;
@@ -383,7 +418,6 @@ struct dctp_plan {
             cudaGetDevice(&prev);
             cudaSetDevice(device);
             cudaFree(blob);
-            cudaFree(flag);
             if (dense && dense->buf) cudaFree(dense->buf);
             if (dense)
                 for (int i = 0; i < 2; ++i) {
@@ -881,8 +915,7 @@ static void upload_plan(dctp_plan& p) {
     cuda_check(cudaMemcpy(static_cast<unsigned char*>(p.blob) + p.stage_desc, desc, sizeof(desc),
                           cudaMemcpyHostToDevice),
                "cudaMemcpy(stage descriptors)");
-    cuda_check(cudaMalloc(reinterpret_cast<void**>(&p.flag), sizeof(int)), "cudaMalloc(flag)");
-    cuda_check(cudaMemset(p.flag, 0, sizeof(int)), "cudaMemset(flag)");
+    p.flags.device = p.device;
     cuda_check(cudaDeviceGetAttribute(&p.num_sms, cudaDevAttrMultiProcessorCount, p.device), "cudaDeviceGetAttribute");
 }
 
@@ -1082,7 +1115,7 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
     DeviceScope scope(p->device);
     if constexpr (std::is_same_v<T, double>) {
         if (fast_route(p)) {
-            cuda_check(DCTP_LAUNCH("nfst_fwd", s, dctp::dev::nfst_apply(in, out, batch, fast_plan_dev(p), p->flag, false, s)),
+            cuda_check(DCTP_LAUNCH("nfst_fwd", s, dctp::dev::nfst_apply(in, out, batch, fast_plan_dev(p), p->flags(s), false, s)),
                        "nfst forward kernel");
             return;
         }
@@ -1092,7 +1125,7 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
         if (p->small && aligned) {
             const dctp::dev::SmallPlanDev sp = small_plan_dev(p);
             cuda_check(DCTP_LAUNCH("fused_small_fwd", s,
-                                   dctp::dev::fused_small_forward(in, out, batch, sp, p->flag, p->num_sms, s)),
+                                   dctp::dev::fused_small_forward(in, out, batch, sp, p->flags(s), p->num_sms, s)),
                        "fused small forward kernel");
             return;
         }
@@ -1109,7 +1142,7 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
         Scratch<T> u(batch * static_cast<std::size_t>(f.L), s);
         cuda_check(DCTP_LAUNCH("fold_dct", s,
                                dctp::dev::dct2_fold_rows<T>(in, n, u.ptr, f.L, out, n, even, f.L, batch,
-                                                            twiddles_at<T>(p->blob, f32 ? f.tw32 : f.tw64), p->flag,
+                                                            twiddles_at<T>(p->blob, f32 ? f.tw32 : f.tw64), p->flags(s),
                                                             s)),
                    "fold dct kernel");
         if constexpr (f32) {
@@ -1121,7 +1154,7 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
             if (!(tc && tc[0] == '0') && dctp::dev::tc_sgemm3_supported(f.L, f.cols, f.L, f.L, n, u.ptr, wh, wl, out)) {
                 cuda_check(DCTP_LAUNCH("fold_w_tc32", s,
                                        dctp::dev::tc_sgemm3(u.ptr, f.L, wh, wl, f.L, out, n, batch, f.cols, f.L,
-                                                            p->flag, s, at<int>(p->blob, f.map), nullptr, nullptr, 0,
+                                                            p->flags(s), s, at<int>(p->blob, f.map), nullptr, nullptr, 0,
                                                             at<float>(p->blob, f.w_sw))),
                            "fold tcgen05 kernel");
                 return;
@@ -1130,7 +1163,7 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
             if (dctp::dev::sgemm_rows_supported(f.L, f.cols, f.L, static_cast<int>(f.ldwt), 4, u.ptr, b, b)) {
                 cuda_check(DCTP_LAUNCH("fold_w", s,
                                        dctp::dev::sgemm_rows(u.ptr, f.L, b, static_cast<int>(f.ldwt), out, n, batch,
-                                                             f.cols, f.L, p->flag, s, at<int>(p->blob, f.map))),
+                                                             f.cols, f.L, p->flags(s), s, at<int>(p->blob, f.map))),
                            "fold sgemm kernel");
                 return;
             }
@@ -1140,14 +1173,14 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
             // 0.30 ms forward, 0.43 vs 0.37 ms inverse with the slicing pass)
             if (const int S = f.L >= kOzakiFoldMinK ? ozaki_slices(n) : 0) {
                 ensure_fold_ozaki(p, 0, S, s);
-                rows_by_ozaki(u.ptr, f.L, f.oz[0], f.oz_e[0], f.L, f.cols, S, out, n, batch, p->flag, s, "fold_w_i8",
+                rows_by_ozaki(u.ptr, f.L, f.oz[0], f.oz_e[0], f.L, f.cols, S, out, n, batch, p->flags(s), s, "fold_w_i8",
                               at<int>(p->blob, f.map));
                 return;
             }
         }
         cuda_check(DCTP_LAUNCH("fold_w", s,
                                dctp::dev::rows_by_basis<T>(u.ptr, f.L, at<double>(p->blob, f.w), f.ldw, f.L, f.cols, out,
-                                                           n, batch, p->flag, s, at<int>(p->blob, f.map))),
+                                                           n, batch, p->flags(s), s, at<int>(p->blob, f.map))),
                    "fold product kernel");
         return;
     }
@@ -1157,12 +1190,12 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
     Scratch<T> hat(batch * K, s);
     cuda_check(DCTP_LAUNCH("dct2", s, dctp::dev::dct2_rows<T>(in, n, nullptr, n, out, n,
                                                              p->emit_fwd_compact<T>(hat.ptr, K), n, batch,
-                                                             p->tw<T>(), p->flag, s)),
+                                                             p->tw<T>(), p->flags(s), s)),
                "dct2 kernel");
     if (p->fwd.cols > 0)
         cuda_check(DCTP_LAUNCH("cauchy", s,
                                cauchy_stage<T>(hat.ptr, K, out, n, p->stage_dev(std::is_same_v<T, float> ? 1 : 0), 1,
-                                               p->fwd.rows, p->fwd.cols, batch, p->flag, s)),
+                                               p->fwd.rows, p->fwd.cols, batch, p->flags(s), s)),
                    "cauchy kernel");
 }
 
@@ -1177,7 +1210,7 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
     if constexpr (std::is_same_v<T, double>) {
         if (fast_route(p)) {
             DeviceScope scope(p->device);
-            cuda_check(DCTP_LAUNCH("nfst_inv", s, dctp::dev::nfst_apply(in, out, batch, fast_plan_dev(p), p->flag, true, s)),
+            cuda_check(DCTP_LAUNCH("nfst_inv", s, dctp::dev::nfst_apply(in, out, batch, fast_plan_dev(p), p->flags(s), true, s)),
                        "nfst inverse kernel");
             return;
         }
@@ -1198,7 +1231,7 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
         Scratch<T> w(batch * static_cast<std::size_t>(f.L), s);
         cuda_check(DCTP_LAUNCH("fold_idct", s,
                                dctp::dev::idct_rows<T>(at<T>(p->blob, f.zero), 0, in, n, even, w.ptr, f.L, f.L, batch,
-                                                       twiddles_at<T>(p->blob, f32 ? f.tw32 : f.tw64), p->flag, s)),
+                                                       twiddles_at<T>(p->blob, f32 ? f.tw32 : f.tw64), p->flags(s), s)),
                    "fold idct kernel");
         if constexpr (f32) {
             const char* tc = std::getenv("DCTP_TC32");
@@ -1209,7 +1242,7 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
                 dctp::dev::tc_sgemm3_supported(f.cols, f.L, 4, ldt, n, w.ptr, th, tl, out)) {
                 cuda_check(DCTP_LAUNCH("fold_wt_tc32", s,
                                        dctp::dev::tc_sgemm3(in, static_cast<int>(n), th, tl, ldt, out, n, batch, f.L,
-                                                            f.cols, p->flag, s, nullptr, at<int>(p->blob, f.map), w.ptr,
+                                                            f.cols, p->flags(s), s, nullptr, at<int>(p->blob, f.map), w.ptr,
                                                             f.L, at<float>(p->blob, f.wt_sw))),
                            "fold tcgen05 kernel");
                 return;
@@ -1218,14 +1251,14 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
         if constexpr (!f32) {
             if (const int S = f.cols >= kOzakiFoldMinK ? ozaki_slices(n) : 0) {
                 ensure_fold_ozaki(p, 1, S, s);
-                rows_by_ozaki(in, n, f.oz[1], f.oz_e[1], f.cols, f.L, S, out, n, batch, p->flag, s, "fold_wt_i8",
+                rows_by_ozaki(in, n, f.oz[1], f.oz_e[1], f.cols, f.L, S, out, n, batch, p->flags(s), s, "fold_wt_i8",
                               nullptr, at<int>(p->blob, f.map), w.ptr, f.L);
                 return;
             }
         }
         cuda_check(DCTP_LAUNCH("fold_wt", s,
                                dctp::dev::rows_by_basis<T>(in, n, at<double>(p->blob, f.wt), f.ldwt, f.cols, f.L, out, n,
-                                                           batch, p->flag, s, nullptr, at<int>(p->blob, f.map), w.ptr,
+                                                           batch, p->flags(s), s, nullptr, at<int>(p->blob, f.map), w.ptr,
                                                            f.L)),
                    "fold product kernel");
         return;
@@ -1236,11 +1269,11 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
     if (p->inv.cols > 0)
         cuda_check(DCTP_LAUNCH("cauchy_inv", s,
                                cauchy_stage<T>(in, n, d.ptr, n, p->stage_dev(std::is_same_v<T, float> ? 3 : 2), 1,
-                                               p->inv.rows, p->inv.cols, batch, p->flag, s)),
+                                               p->inv.rows, p->inv.cols, batch, p->flags(s), s)),
                    "cauchy kernel");
     cuda_check(DCTP_LAUNCH("idct", s,
                            dctp::dev::idct_rows<T>(d.ptr, n, in, n, p->emit_inv<T>(), out, n, n, batch, p->tw<T>(),
-                                                   p->flag, s)),
+                                                   p->flags(s), s)),
                "idct kernel");
 }
 
@@ -1295,7 +1328,6 @@ static void sync_check(int device, int* flag, cudaStream_t s) {
     cuda_check(cudaMemcpy(&h, flag, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(flag)");
     if (h != 0) {
         cuda_check(cudaMemset(flag, 0, sizeof(int)), "cudaMemset(flag)");
-        if (h & 2) throw std::runtime_error("DctPlusPlan: fused kernel timed out waiting for a peer CTA");
         throw std::domain_error("DctPlusPlan: non-finite input sample");
     }
 }
@@ -1474,7 +1506,7 @@ static void ensure_dense(const dctp_plan* p, cudaStream_t s) {
                                              y.ptr, s),
                "basis kernel");
     cuda_check(dctp::dev::idct_rows<double>(y.ptr, ld, y.ptr, ld, dctp::dev::Emit<double>{}, buf, ld, n, n,
-                                            p->tw<double>(), p->flag, s),
+                                            p->tw<double>(), p->flags(s), s),
                "basis idct kernel");
     cuda_check(dctp::dev::transpose_square(buf, ld, buf + n * ld, ld, ni, s), "transpose kernel");
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(basis)");
@@ -1615,13 +1647,13 @@ static void plan_dense(const dctp_plan* p, const T* in, T* out, std::size_t batc
     if constexpr (std::is_same_v<T, double>) {
         if (const int S = ozaki_slices(n)) {
             ensure_ozaki(p, inverse ? 1 : 0, S, s);
-            rows_by_ozaki(in, n, d.oz[inverse ? 1 : 0], d.oz_e[inverse ? 1 : 0], ni, ni, S, out, n, batch, p->flag,
+            rows_by_ozaki(in, n, d.oz[inverse ? 1 : 0], d.oz_e[inverse ? 1 : 0], ni, ni, S, out, n, batch, p->flags(s),
                           s, inverse ? "dense_inv_i8" : "dense_i8");
             return;
         }
     }
     cuda_check(DCTP_LAUNCH(inverse ? "dense_inv" : "dense_nmvp", s,
-                           dctp::dev::rows_by_basis<T>(in, n, bt, d.ld, ni, ni, out, n, batch, p->flag, s)),
+                           dctp::dev::rows_by_basis<T>(in, n, bt, d.ld, ni, ni, out, n, batch, p->flags(s), s)),
                "dense basis kernel");
 }
 template <class T>
@@ -1641,7 +1673,7 @@ struct dctp_ensemble {
     int device = 0;
     std::vector<std::unique_ptr<dctp_plan>> members;
     void* blob = nullptr;
-    int* flag = nullptr;
+    StreamFlags flags;
     TwiddleOffsets tw64, tw32;
     std::size_t to = 0, from = 0, sign64 = 0, sign32 = 0, desc64 = 0, desc32 = 0;
     int n_emit = 0, max_rows = 0, max_cols = 0;
@@ -1659,7 +1691,6 @@ struct dctp_ensemble {
             cudaGetDevice(&prev);
             cudaSetDevice(device);
             cudaFree(blob);
-            cudaFree(flag);
             cudaSetDevice(prev);
         }
     }
@@ -1715,7 +1746,7 @@ static void ensemble_forward_full(const dctp_ensemble* e, const T* in, T* out, s
             cuda_check(DCTP_LAUNCH("progressive_tc32", s,
                                    dctp::dev::tc_sgemm3(in, static_cast<int>(n), at<float>(e->blob, e->gt_hi),
                                                         at<float>(e->blob, e->gt_lo), static_cast<int>(n), out, ld,
-                                                        batch, static_cast<int>(ld), static_cast<int>(n), e->flag, s,
+                                                        batch, static_cast<int>(ld), static_cast<int>(n), e->flags(s), s,
                                                         nullptr, nullptr, nullptr, 0,
                                                         at<float>(e->blob, e->gt_sw))),
                        "progressive tcgen05 kernel");
@@ -1727,21 +1758,21 @@ static void ensemble_forward_full(const dctp_ensemble* e, const T* in, T* out, s
             cuda_check(DCTP_LAUNCH("progressive_sgemm", s,
                                    dctp::dev::sgemm_rows(in, static_cast<int>(n), at<float>(e->blob, e->gmat32),
                                                          static_cast<int>(ld), out, ld, batch, static_cast<int>(ld),
-                                                         static_cast<int>(n), e->flag, s)),
+                                                         static_cast<int>(n), e->flags(s), s)),
                        "progressive sgemm kernel");
             return;
         }
     }
     // Set 0 (the shared DCT, fast_transform.hpp:401-403) is written in place
     // and is the Cauchy stages' input; sets 1..K follow in each row.
-    cuda_check(DCTP_LAUNCH("dct2", s, dctp::dev::dct2_rows<T>(in, n, out, ld, out, ld, emit, n, batch, tw, e->flag, s)),
+    cuda_check(DCTP_LAUNCH("dct2", s, dctp::dev::dct2_rows<T>(in, n, out, ld, out, ld, emit, n, batch, tw, e->flags(s), s)),
                "dct2 kernel");
     if (!e->members.empty() && e->max_cols > 0)
         cuda_check(DCTP_LAUNCH("cauchy_progressive", s,
                                cauchy_stage<T>(out, ld, out, ld,
                                                at<dctp::dev::CauchyStage>(e->blob, f32 ? e->desc32 : e->desc64),
                                                static_cast<int>(e->members.size()), e->max_rows, e->max_cols, batch,
-                                               e->flag, s)),
+                                               e->flags(s), s)),
                    "cauchy kernel");
 }
 
@@ -1858,7 +1889,7 @@ int dctp_inverse_nmvp_f32(const dctp_plan* p, const float* in, float* out, size_
 int dctp_plan_sync_check(const dctp_plan* p, void* stream) {
     return guarded([&] {
         if (!p) throw std::invalid_argument("dctp_plan_sync_check: null plan");
-        sync_check(p->device, p->flag, static_cast<cudaStream_t>(stream));
+        sync_check(p->device, p->flags(static_cast<cudaStream_t>(stream)), static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1911,7 +1942,7 @@ static bool forward_zero_copy(const dctp_plan* p, const double* h_in, double* h_
     if (!pinned_range(h_in, bytes, p->device) || !pinned_range(h_out, bytes, p->device)) return false;
     HostPipe& hp = host_pipe(p->device);
     plan_forward<double>(p, h_in, h_out, batch, hp.comp);
-    sync_check(p->device, p->flag, hp.comp);
+    sync_check(p->device, p->flags(hp.comp), hp.comp);
     return true;
 }
 
@@ -1929,7 +1960,7 @@ extern "C" {
                               [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) {         \
                                   FN<T>(p, din, dout, rows, s);                                       \
                               });                                                                     \
-            sync_check(p->device, p->flag, nullptr);                                                  \
+            sync_check(p->device, p->flags(host_pipe(p->device).comp), nullptr);                                                  \
         });                                                                                           \
     }
 DCTP_HOST_ENTRY(dctp_forward_host_f64, double, plan_forward, true)
@@ -2074,8 +2105,7 @@ int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is,
                                   k * sizeof(dctp::dev::CauchyStage), cudaMemcpyHostToDevice),
                        "cudaMemcpy(stages)");
         }
-        cuda_check(cudaMalloc(reinterpret_cast<void**>(&e->flag), sizeof(int)), "cudaMalloc(flag)");
-        cuda_check(cudaMemset(e->flag, 0, sizeof(int)), "cudaMemset(flag)");
+        e->flags.device = e->device;
         *out = e.release();
     });
 }
@@ -2159,7 +2189,7 @@ static void ensemble_pruned_host(const dctp_ensemble* e, const T* h_in, T* h_out
     if (h_bounds)
         cuda_check(cudaMemcpyAsync(h_bounds, db.ptr, batch * sets * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
     if (h_pruned) cuda_check(cudaMemcpyAsync(h_pruned, dp.ptr, batch, cudaMemcpyDeviceToHost, s), "D2H");
-    sync_check(e->device, e->flag, s);
+    sync_check(e->device, e->flags(s), s);
 }
 
 extern "C" {
@@ -2185,7 +2215,7 @@ int dctp_ensemble_forward_all_pruned_host_f32(const dctp_ensemble* e, const floa
 int dctp_ensemble_sync_check(const dctp_ensemble* e, void* stream) {
     return guarded([&] {
         if (!e) throw std::invalid_argument("dctp_ensemble_sync_check: null ensemble");
-        sync_check(e->device, e->flag, static_cast<cudaStream_t>(stream));
+        sync_check(e->device, e->flags(static_cast<cudaStream_t>(stream)), static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -2199,7 +2229,7 @@ int dctp_ensemble_forward_all_host_f32(const dctp_ensemble* e, const float* h_in
                               [&](const float* din, float* dout, std::size_t rows, cudaStream_t s) {
                                   ensemble_forward<float>(e, din, dout, rows, s);
                               });
-        sync_check(e->device, e->flag, nullptr);
+        sync_check(e->device, e->flags(host_pipe(e->device).comp), nullptr);
     });
 }
 int dctp_ensemble_forward_all_host_f64(const dctp_ensemble* e, const double* h_in, double* h_out, size_t batch) {
@@ -2212,7 +2242,7 @@ int dctp_ensemble_forward_all_host_f64(const dctp_ensemble* e, const double* h_i
                                [&](const double* din, double* dout, std::size_t rows, cudaStream_t s) {
                                    ensemble_forward<double>(e, din, dout, rows, s);
                                });
-        sync_check(e->device, e->flag, nullptr);
+        sync_check(e->device, e->flags(host_pipe(e->device).comp), nullptr);
     });
 }
 
@@ -2226,7 +2256,7 @@ struct dctp_chain {
     dctp::host::Chain ch;
     int device = 0;
     void* blob = nullptr; // X^T in fp64 (ld even), X in fp32 for the SGEMM route
-    int* flag = nullptr;
+    StreamFlags flags;
     std::size_t ldt = 0, xt64 = 0, x32 = 0;
     bool sgemm32 = false;
     // int8 slices of X^T for the tcgen05 kind::i8 product (ozaki.cu), built on first use
@@ -2241,7 +2271,6 @@ struct dctp_chain {
             cudaGetDevice(&prev);
             cudaSetDevice(device);
             cudaFree(blob);
-            cudaFree(flag);
             if (oz) cudaFree(oz);
             if (oz_e) cudaFree(oz_e);
             cudaSetDevice(prev);
@@ -2265,7 +2294,7 @@ static void chain_forward(const dctp_chain* c, const T* in, T* out, std::size_t 
         const float* x = at<float>(c->blob, c->x32);
         if (c->sgemm32 && dctp::dev::sgemm_rows_supported(ni, ni, ni, ni, n, in, x, out)) {
             cuda_check(DCTP_LAUNCH("chain_sgemm", s,
-                                   dctp::dev::sgemm_rows(in, ni, x, ni, out, n, batch, ni, ni, c->flag, s)),
+                                   dctp::dev::sgemm_rows(in, ni, x, ni, out, n, batch, ni, ni, c->flags(s), s)),
                        "chain sgemm kernel");
             return;
         }
@@ -2286,13 +2315,13 @@ static void chain_forward(const dctp_chain* c, const T* in, T* out, std::size_t 
                     cm->oz_slices = S;
                 }
             }
-            rows_by_ozaki(in, n, c->oz, c->oz_e, ni, ni, S, out, n, batch, c->flag, s, "chain_i8");
+            rows_by_ozaki(in, n, c->oz, c->oz_e, ni, ni, S, out, n, batch, c->flags(s), s, "chain_i8");
             return;
         }
     }
     cuda_check(DCTP_LAUNCH("chain_dmma", s,
                            dctp::dev::rows_by_basis<T>(in, n, at<double>(c->blob, c->xt64), c->ldt, ni, ni, out, n,
-                                                       batch, c->flag, s)),
+                                                       batch, c->flags(s), s)),
                "chain dmma kernel");
 }
 
@@ -2336,8 +2365,7 @@ int dctp_chain_create(size_t n, size_t k, const int* kinds, const size_t* is, co
             DeviceScope scope(device);
             prepare_pool(device);
             c->blob = blob.upload();
-            cuda_check(cudaMalloc(reinterpret_cast<void**>(&c->flag), sizeof(int)), "cudaMalloc(flag)");
-            cuda_check(cudaMemset(c->flag, 0, sizeof(int)), "cudaMemset(flag)");
+            c->flags.device = c->device;
         }
         *out = c.release();
     });
@@ -2391,7 +2419,7 @@ int dctp_chain_sync_check(const dctp_chain* c, void* stream) {
     return guarded([&] {
         if (!c) throw std::invalid_argument("dctp_chain_sync_check: null chain");
         if (!c->blob) throw std::invalid_argument("ChainedFactorization: host-only chain (created with device < 0)");
-        sync_check(c->device, c->flag, static_cast<cudaStream_t>(stream));
+        sync_check(c->device, c->flags(static_cast<cudaStream_t>(stream)), static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -2406,7 +2434,7 @@ int dctp_chain_sync_check(const dctp_chain* c, void* stream) {
                               [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) {          \
                                   chain_forward<T>(c, din, dout, rows, s);                             \
                               });                                                                      \
-            sync_check(c->device, c->flag, nullptr);                                                   \
+            sync_check(c->device, c->flags(host_pipe(c->device).comp), nullptr);                                                   \
         });                                                                                            \
     }
 DCTP_CHAIN_HOST_ENTRY(dctp_chain_forward_host_f64, double)

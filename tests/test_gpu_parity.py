@@ -106,17 +106,19 @@ def test_full_batch_against_restatement(P, torch, restatement, cid):
     assert O.parity(y, restatement.forward(setup_of(g), s)) <= TOL64
 
 
-@pytest.mark.parametrize("cid,dtype", [(1, "float64"), (2, "float64"), (3, "float64"), (3, "float32"),
-                                       (5, "float64")])
+@pytest.mark.parametrize("cid,dtype", [(1, "float64"), (2, "float64"), (3, "float64"), (3, "float32")])
 def test_full_size_orthogonality(P, torch, restatement, cid, dtype):
     """Size-independent properties at the BASELINE batch: Parseval and
-    inverse(forward(s)) == s (X is orthogonal)."""
+    inverse(forward(s)) == s (X is orthogonal).  C5 is not here: its basis
+    is orthogonal only to ~1e-9 in the reference itself (near-pole columns,
+    SURVEY.md Appendix A.3), so its whole batch is pinned directly against the
+    reference instead (tests/test_full_batch_parity.py)."""
     cfg = O.config(cid)
     t = getattr(torch, dtype)
     s = dev(torch, restatement.signals(cfg, cfg.batch), t)
     plan = plan_for(P, cid)
     y = plan.forward(s)
-    tol = TOL32 if dtype == "float32" else (1e-8 if cid == 5 else TOL64)
+    tol = TOL32 if dtype == "float32" else TOL64
     ns, ny = torch.linalg.vector_norm(s.double(), dim=1), torch.linalg.vector_norm(y.double(), dim=1)
     assert float(((ny - ns).abs() / ns).max()) <= tol
     back = plan.inverse(y)

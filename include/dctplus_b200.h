@@ -103,6 +103,12 @@ int dctp_plan_setup(const dctp_plan* plan, double* lambda, double* mu, double* z
 /* Slot map (spectral.hpp:322-325): passthrough[s] in {0,1}, idx[s]. */
 int dctp_plan_slots(const dctp_plan* plan, int* passthrough, int64_t* idx);
 
+/* The active subproblem of PerturbedSpectrum (spectral.hpp:330-338): *k = the
+ * number of kept (non-deflated) indices; sub_lambda, sub_z, sub_mu (k doubles
+ * each, any may be NULL) and *rho — factorization().spec. */
+int dctp_plan_subproblem(const dctp_plan* plan, size_t* k, double* sub_lambda, double* sub_z, double* sub_mu,
+                         double* rho);
+
 /* Dense basis X (n x n row-major, signed) — basis() (fast_transform.hpp:142),
  * rebuilt on the host on demand. */
 int dctp_plan_basis(const dctp_plan* plan, double* x);
@@ -214,6 +220,9 @@ int dctp_chain_forward_host_f32(const dctp_chain* chain, const float* h_in, floa
 int dctp_dct2_f64(size_t n, const double* d_in, double* d_out, size_t batch, int device, void* stream);
 int dctp_idct2_f64(size_t n, const double* d_in, double* d_out, size_t batch, int device, void* stream);
 int dctp_dct2_f32(size_t n, const float* d_in, float* d_out, size_t batch, int device, void* stream);
+/* Host-buffer form (TrigPlan::execute, trig.hpp:95-110): `batch` rows of n
+ * doubles through the GPU kernels, synchronous.  inverse = 0: dct2, 1: idct2. */
+int dctp_trig_host_f64(int inverse, size_t n, const double* h_in, double* h_out, size_t batch, int device);
 int dctp_idct2_f32(size_t n, const float* d_in, float* d_out, size_t batch, int device, void* stream);
 
 /* --- profiling: CUDA-event timing of every kernel launch ---------------- */

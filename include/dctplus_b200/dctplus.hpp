@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -91,6 +92,77 @@ struct DctPlusWorkspace {
     std::vector<double> out;
 };
 
+/// Dense row-major matrix (matrix.hpp:14-60): what basis() returns.
+class Matrix {
+  public:
+    Matrix() = default;
+    Matrix(std::size_t rows, std::size_t cols, double fill = 0.0) : rows_(rows), cols_(cols), data_(rows * cols, fill) {}
+    std::size_t rows() const { return rows_; }
+    std::size_t cols() const { return cols_; }
+    double& operator()(std::size_t i, std::size_t j) { return data_[i * cols_ + j]; }
+    double operator()(std::size_t i, std::size_t j) const { return data_[i * cols_ + j]; }
+    double* data() { return data_.data(); }
+    const double* data() const { return data_.data(); }
+    /// flat row-major view (index i * cols + j), as round 1's basis() returned
+    double operator[](std::size_t k) const { return data_[k]; }
+
+  private:
+    std::size_t rows_ = 0, cols_ = 0;
+    std::vector<double> data_;
+};
+
+/// spectral.hpp:322-338: slot map entry and the perturbed spectrum.
+struct SlotRef {
+    bool passthrough;
+    std::size_t idx;
+};
+struct PerturbedSpectrum {
+    std::vector<double> mu; // full length, ascending
+    std::vector<double> z;  // deflated (zeros at passed indices)
+    std::vector<double> a;  // per slot; 1.0 for pass-through slots
+    std::vector<SlotRef> slots;
+    double rho = 0.0;
+    std::vector<double> sub_lambda, sub_z, sub_mu; // active subproblem
+};
+
+/// cauchy.hpp:111-119: X = U diag(z) C(lambda, mu) diag(sigma .* a) with
+/// pass-through columns.
+struct CauchyFactorization {
+    std::vector<double> lambda;
+    PerturbedSpectrum spec;
+    std::vector<double> sigma;
+    std::size_t size() const { return lambda.size(); }
+    double rho() const { return spec.rho; }
+    const std::vector<double>& mu() const { return spec.mu; }
+};
+
+enum class TrigKind { dct2, idct2 };
+
+/// TrigPlan (trig.hpp:32-116): the orthonormal DCT-II / its inverse of one
+/// length; execute() runs the GPU kernels on host buffers.
+class TrigPlan {
+  public:
+    TrigPlan(TrigKind kind, std::size_t len, int device = 0) : kind_(kind), len_(len), device_(device) {
+        if (len < 1) throw std::invalid_argument("TrigPlan: length must be positive");
+    }
+    std::size_t size() const { return len_; }
+    TrigKind kind() const { return kind_; }
+    void execute(const double* in, double* out) const {
+        detail::check(dctp_trig_host_f64(kind_ == TrigKind::idct2 ? 1 : 0, len_, in, out, 1, device_));
+    }
+    std::vector<double> operator()(const std::vector<double>& in) const {
+        if (in.size() != len_) throw std::invalid_argument("TrigPlan: size mismatch");
+        std::vector<double> out(len_);
+        execute(in.data(), out.data());
+        return out;
+    }
+
+  private:
+    TrigKind kind_;
+    std::size_t len_;
+    int device_;
+};
+
 /// Fast DCT+ of one rank-one update of the path graph (fast_transform.hpp:43-302).
 class DctPlusPlan {
   public:
@@ -102,9 +174,7 @@ class DctPlusPlan {
         detail::check(dctp_plan_create(n, update.abi_kind(), update.node_i, update.node_j, update.rho,
                                        update.v.empty() ? nullptr : update.v.data(), epsilon, tau, device, &h));
         h_.reset(h, [](dctp_plan* p) { dctp_plan_destroy(p); });
-        int slow = 0;
-        detail::check(dctp_plan_info(h_.get(), &n_, &eps_, &slow, nullptr, nullptr, &device_));
-        slow_ = slow != 0;
+        init();
     }
 
     std::size_t size() const { return n_; }
@@ -118,14 +188,23 @@ class DctPlusPlan {
         detail::check(dctp_plan_route(h_.get(), &f, nullptr));
         return f != 0;
     }
-    std::vector<double> lambda() const { return setup_vector(0); }
-    std::vector<double> mu() const { return setup_vector(1); }
+    const std::vector<double>& lambda() const { return state_->fact.lambda; }
+    const std::vector<double>& mu() const { return state_->fact.spec.mu; }
+    /// The plan's factorization (fast_transform.hpp:141): lambda, the perturbed
+    /// spectrum (mu, deflated z, a, slots, subproblem) and the column signs.
+    const CauchyFactorization& factorization() const { return state_->fact; }
+    /// The DCT-II plan of the plan's size (fast_transform.hpp:262).
+    const TrigPlan& dct_plan() const { return state_->dct; }
 
-    /// Dense basis X (n x n, row-major), columns signed by the largest-entry rule.
-    std::vector<double> basis() const {
-        std::vector<double> x(n_ * n_);
-        detail::check(dctp_plan_basis(h_.get(), x.data()));
-        return x;
+    /// Dense basis X (n x n, row-major), columns signed by the largest-entry
+    /// rule (fast_transform.hpp:142); built on the host on first use.
+    const Matrix& basis() const {
+        std::call_once(state_->basis_once, [this] {
+            Matrix x(n_, n_);
+            detail::check(dctp_plan_basis(h_.get(), x.data()));
+            state_->basis = std::move(x);
+        });
+        return state_->basis;
     }
 
     DctPlusWorkspace make_workspace() const { return DctPlusWorkspace{std::vector<double>(n_)}; }
@@ -195,22 +274,49 @@ class DctPlusPlan {
     friend class PrunedEnsemblePlan;
     DctPlusPlan(const dctp_plan* borrowed, RankOneUpdate update) : update_(std::move(update)) {
         h_.reset(const_cast<dctp_plan*>(borrowed), [](dctp_plan*) {});
-        int slow = 0;
-        detail::check(dctp_plan_info(h_.get(), &n_, &eps_, &slow, nullptr, nullptr, &device_));
-        slow_ = slow != 0;
+        init();
     }
     void check_size(const std::vector<double>& s) const {
         if (s.size() != n_) throw std::invalid_argument("DctPlusPlan: signal size mismatch");
     }
-    std::vector<double> setup_vector(int which) const {
-        std::vector<double> v(n_);
-        detail::check(dctp_plan_setup(h_.get(), which == 0 ? v.data() : nullptr, which == 1 ? v.data() : nullptr,
-                                      nullptr, nullptr, nullptr));
-        return v;
+    /// Host copies of the setup (shared by copies of the plan object).
+    struct State {
+        CauchyFactorization fact;
+        TrigPlan dct;
+        std::once_flag basis_once;
+        Matrix basis;
+        State(std::size_t n, int device) : dct(TrigKind::dct2, n, device) {}
+    };
+    void init() {
+        int slow = 0;
+        detail::check(dctp_plan_info(h_.get(), &n_, &eps_, &slow, nullptr, nullptr, &device_));
+        slow_ = slow != 0;
+        state_ = std::make_shared<State>(n_, device_ < 0 ? 0 : device_);
+        auto& f = state_->fact;
+        f.lambda.resize(n_);
+        f.spec.mu.resize(n_);
+        f.spec.z.resize(n_);
+        f.spec.a.resize(n_);
+        f.sigma.resize(n_);
+        detail::check(dctp_plan_setup(h_.get(), f.lambda.data(), f.spec.mu.data(), f.spec.z.data(),
+                                      f.spec.a.data(), f.sigma.data()));
+        std::vector<int> pass(n_);
+        std::vector<int64_t> idx(n_);
+        detail::check(dctp_plan_slots(h_.get(), pass.data(), idx.data()));
+        f.spec.slots.resize(n_);
+        for (std::size_t s = 0; s < n_; ++s) f.spec.slots[s] = {pass[s] != 0, static_cast<std::size_t>(idx[s])};
+        std::size_t k = 0;
+        detail::check(dctp_plan_subproblem(h_.get(), &k, nullptr, nullptr, nullptr, &f.spec.rho));
+        f.spec.sub_lambda.resize(k);
+        f.spec.sub_z.resize(k);
+        f.spec.sub_mu.resize(k);
+        detail::check(dctp_plan_subproblem(h_.get(), &k, f.spec.sub_lambda.data(), f.spec.sub_z.data(),
+                                           f.spec.sub_mu.data(), nullptr));
     }
 
     RankOneUpdate update_;
     std::shared_ptr<dctp_plan> h_;
+    std::shared_ptr<State> state_;
     std::size_t n_ = 0;
     double eps_ = 0.0;
     bool slow_ = false;
@@ -225,6 +331,15 @@ inline std::vector<double> forward_nmvp(const DctPlusPlan& plan, const std::vect
     return plan.forward_nmvp(s);
 }
 inline std::vector<double> inverse(const DctPlusPlan& plan, const std::vector<double>& p) { return plan.inverse(p); }
+
+/// Scratch for PrunedEnsemblePlan::forward_all (fast_transform.hpp:323-336):
+/// one workspace per member plus the shared-DCT buffer, and here the flat
+/// K+1 sets the GPU call fills before they are split into Result::coeffs.
+struct PrunedWorkspace {
+    std::vector<DctPlusWorkspace> members;
+    std::vector<double> sd;
+    std::vector<double> flat;
+};
 
 /// Shared DCT + K Cauchy stages, progressive mode c_p = n (fast_transform.hpp:338-454).
 class PrunedEnsemblePlan {
@@ -277,19 +392,36 @@ class PrunedEnsemblePlan {
         std::vector<double> bounds;              // truncation-error bound per member (0 on the full branch)
     };
 
-    Result forward_all(const std::vector<double>& s) const {
+    PrunedWorkspace make_workspace() const {
+        PrunedWorkspace ws;
+        for (const auto& m : members_) ws.members.push_back(m.make_workspace());
+        ws.sd.resize(n_);
+        ws.flat.resize(ensemble_size() * n_);
+        return ws;
+    }
+
+    /// fast_transform.hpp:396-439: res.coeffs[r] (K + 1 sets, set 0 = the
+    /// shared DCT), res.bounds, res.pruned; reuses ws and res's storage.
+    void forward_all(const std::vector<double>& s, PrunedWorkspace& ws, Result& res) const {
         if (s.size() != n_) throw std::invalid_argument("pruned_forward_all: size mismatch");
         const std::size_t sets = ensemble_size();
-        std::vector<double> flat(sets * n_);
-        Result res;
+        ws.flat.resize(sets * n_);
+        res.coeffs.resize(sets);
         res.bounds.assign(sets, 0.0);
         unsigned char pruned = 0;
-        detail::check(dctp_ensemble_forward_all_pruned_host_f64(h_.get(), s.data(), flat.data(), res.bounds.data(),
-                                                                &pruned, 1));
+        detail::check(dctp_ensemble_forward_all_pruned_host_f64(h_.get(), s.data(), ws.flat.data(),
+                                                                res.bounds.data(), &pruned, 1));
         res.pruned = pruned != 0;
         for (std::size_t r = 0; r < sets; ++r)
-            res.coeffs.emplace_back(flat.begin() + static_cast<std::ptrdiff_t>(r * n_),
-                                    flat.begin() + static_cast<std::ptrdiff_t>((r + 1) * n_));
+            res.coeffs[r].assign(ws.flat.begin() + static_cast<std::ptrdiff_t>(r * n_),
+                                 ws.flat.begin() + static_cast<std::ptrdiff_t>((r + 1) * n_));
+        ws.sd.assign(res.coeffs[0].begin(), res.coeffs[0].end());
+    }
+
+    Result forward_all(const std::vector<double>& s) const {
+        PrunedWorkspace ws = make_workspace();
+        Result res;
+        forward_all(s, ws, res);
         return res;
     }
 

@@ -37,6 +37,7 @@ SIGNATURES = {
     "dctp_ozaki_slices": (C.c_int, [_sz, _ip]),
     "dctp_plan_setup": (C.c_int, [_p, _p, _p, _p, _p, _p]),
     "dctp_plan_slots": (C.c_int, [_p, _p, _p]),
+    "dctp_plan_subproblem": (C.c_int, [_p, C.POINTER(_sz), _p, _p, _p, _dp]),
     "dctp_plan_basis": (C.c_int, [_p, _p]),
     "dctp_forward_f64": (C.c_int, [_p, _p, _p, _sz, _p]),
     "dctp_forward_f32": (C.c_int, [_p, _p, _p, _sz, _p]),
@@ -84,6 +85,7 @@ SIGNATURES = {
     "dctp_dct2_f64": (C.c_int, [_sz, _p, _p, _sz, C.c_int, _p]),
     "dctp_idct2_f64": (C.c_int, [_sz, _p, _p, _sz, C.c_int, _p]),
     "dctp_dct2_f32": (C.c_int, [_sz, _p, _p, _sz, C.c_int, _p]),
+    "dctp_trig_host_f64": (C.c_int, [C.c_int, _sz, _p, _p, _sz, C.c_int]),
     "dctp_idct2_f32": (C.c_int, [_sz, _p, _p, _sz, C.c_int, _p]),
     "dctp_profile_enable": (C.c_int, [C.c_int]),
     "dctp_profile_reset": (C.c_int, []),

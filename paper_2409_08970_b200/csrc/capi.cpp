@@ -1051,6 +1051,10 @@ static std::unique_ptr<dctp_plan> build_plan(std::size_t n, const dctp::host::Up
         p->st = dctp::host::build_setup(n, u, eps, tau);
         return p;
     }
+    if (!dctp::dev::dct_supported(n, true))
+        throw std::invalid_argument("DctPlusPlan: n = " + std::to_string(n) +
+                                    " exceeds the GPU DCT kernels (a row must fit in shared memory: powers of two "
+                                    "up to 8192, other sizes up to 14528)");
     DeviceScope scope(device);
     const dctp::host::SecularBackend be = gpu_secular_backend();
     p->st = dctp::host::build_setup(n, u, eps, tau, gpu_setup(n) ? &be : nullptr);
@@ -1853,6 +1857,21 @@ int dctp_plan_slots(const dctp_plan* p, int* passthrough, int64_t* idx) {
     });
 }
 
+int dctp_plan_subproblem(const dctp_plan* p, size_t* k, double* sub_lambda, double* sub_z, double* sub_mu,
+                         double* rho) {
+    return guarded([&] {
+        if (!p) throw std::invalid_argument("dctp_plan_subproblem: null plan");
+        const auto& st = p->st;
+        if (k) *k = st.kept.size();
+        if (rho) *rho = st.rho;
+        for (std::size_t q = 0; q < st.kept.size(); ++q) {
+            if (sub_lambda) sub_lambda[q] = st.lambda[st.kept[q]];
+            if (sub_z) sub_z[q] = st.z[st.kept[q]];
+        }
+        if (sub_mu) std::copy(st.sub_mu.begin(), st.sub_mu.end(), sub_mu);
+    });
+}
+
 int dctp_plan_basis(const dctp_plan* p, double* x) {
     return guarded([&] {
         if (!p || !x) throw std::invalid_argument("dctp_plan_basis: null argument");
@@ -2477,6 +2496,8 @@ void trig_run(bool inverse, std::size_t n, const T* in, T* out, std::size_t batc
     if (n < 1) throw std::invalid_argument("TrigPlan: length must be positive");
     if (batch == 0) return;
     if (!in || !out) throw std::invalid_argument("trig: null buffer");
+    if (!dctp::dev::dct_supported(n, std::is_same_v<T, double>))
+        throw std::invalid_argument("TrigPlan: length " + std::to_string(n) + " exceeds the GPU DCT kernels");
     DeviceScope scope(device);
     const auto e = trig_cache().get(device, n);
     dctp::dev::Twiddles<T> tw;
@@ -2505,6 +2526,21 @@ int dctp_dct2_f32(size_t n, const float* in, float* out, size_t batch, int devic
 }
 int dctp_idct2_f32(size_t n, const float* in, float* out, size_t batch, int device, void* stream) {
     return guarded([&] { trig_run<float>(true, n, in, out, batch, device, static_cast<cudaStream_t>(stream)); });
+}
+
+int dctp_trig_host_f64(int inverse, size_t n, const double* h_in, double* h_out, size_t batch, int device) {
+    return guarded([&] {
+        if (batch == 0) return;
+        if (!h_in || !h_out) throw std::invalid_argument("dctp_trig_host_f64: null buffer");
+        DeviceScope scope(device);
+        cudaStream_t s = host_pipe(device).comp;
+        Scratch<double> d(2 * batch * n, s);
+        cuda_check(cudaMemcpyAsync(d.ptr, h_in, batch * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+        trig_run<double>(inverse != 0, n, d.ptr, d.ptr + batch * n, batch, device, s);
+        cuda_check(cudaMemcpyAsync(h_out, d.ptr + batch * n, batch * n * sizeof(double), cudaMemcpyDeviceToHost, s),
+                   "D2H");
+        cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(trig)");
+    });
 }
 
 int dctp_profile_enable(int on) {

@@ -185,8 +185,7 @@ cudaError_t cauchy_rows_dmma(const double* in, std::size_t ld_in, double* out, s
                              int* flag, cudaStream_t stream) {
     if (batch == 0 || num_stages == 0 || max_cols == 0) return cudaSuccess;
     constexpr std::size_t smem = 2 * (BM + BN) * LDS_ * sizeof(double) + BN * sizeof(double);
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(cauchy_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const cudaError_t attr = smem_optin(reinterpret_cast<const void*>(cauchy_dmma_kernel), static_cast<int>(smem));
     if (attr != cudaSuccess) return attr;
     // 16-byte row loads need 16-byte aligned rows (otherwise the 8-byte gather runs)
     const int vec16 = (reinterpret_cast<std::uintptr_t>(in) % 16 == 0) && (ld_in % 2 == 0);

@@ -3,6 +3,9 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include <cuda_runtime.h>
 
@@ -48,6 +51,24 @@ inline int ilog2(std::size_t n) {
 }
 
 inline bool is_pow2(std::size_t n) { return n != 0 && (n & (n - 1)) == 0; }
+
+/// The >48 KB dynamic shared-memory opt-in of `kern` on the current device.
+/// The attribute is per (function, device), so it is cached per pair: one
+/// plan per device used from threads of one process must
+/// see it set on every device it launches on.
+inline cudaError_t smem_optin(const void* kern, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = done.find({kern, dev});
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done[{kern, dev}] = bytes;
+    return e;
+}
 
 } // namespace dctp::dev
 

@@ -375,6 +375,17 @@ cudaError_t idct_rows(const T* d, std::size_t ld_d, const T* p, std::size_t ld_p
     return cudaGetLastError();
 }
 
+bool dct_supported(std::size_t n, bool f64) {
+    constexpr std::size_t kSmemMax = 227 * 1024;
+    if (n < 1) return false;
+    if (is_pow2(n) && n >= 2) {
+        const std::size_t smem = f64 ? fft_smem_bytes<double>(n, rows_per_cta_for<double>(n))
+                                     : fft_smem_bytes<float>(n, rows_per_cta_for<float>(n));
+        return smem <= kSmemMax;
+    }
+    return 2 * n * (f64 ? sizeof(double) : sizeof(float)) <= kSmemMax;
+}
+
 template cudaError_t dct2_rows<double>(const double*, std::size_t, double*, std::size_t, double*, std::size_t,
                                        Emit<double>, std::size_t, std::size_t, Twiddles<double>, int*, cudaStream_t);
 template cudaError_t dct2_rows<float>(const float*, std::size_t, float*, std::size_t, float*, std::size_t,

@@ -196,9 +196,8 @@ cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std:
     if (batch == 0 || N == 0) return cudaSuccess;
     if (ld_bt % 2 != 0 || reinterpret_cast<std::uintptr_t>(bt) % 16 != 0) return cudaErrorInvalidValue;
     constexpr std::size_t smem = 2 * (BM + BN) * LDS_ * sizeof(double);
-    static const cudaError_t attr = cudaFuncSetAttribute(rows_by_basis_kernel<T>,
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         static_cast<int>(smem));
+    const cudaError_t attr = smem_optin(reinterpret_cast<const void*>(rows_by_basis_kernel<T>),
+                                        static_cast<int>(smem));
     if (attr != cudaSuccess) return attr;
     const int vec16 = !a_map && (reinterpret_cast<std::uintptr_t>(in) % 16 == 0) && (ld_in % 2 == 0);
     const std::size_t num_n = (N + BN - 1) / BN;

@@ -912,16 +912,22 @@ constexpr std::size_t smem_bytes() {
 }
 
 /// Scheduler counter pair of (current device, stream), allocated and zeroed
-/// once; the kernels leave it zeroed (release_counter).
+/// once; the kernels leave it zeroed (release_counter).  Keyed by
+/// cudaStreamGetId, not the handle: cudaStreamPerThread (or the null stream
+/// under per-thread default streams) is one handle for many real streams, and
+/// a destroyed stream's handle can be reused while its kernels still run.
 cudaError_t stream_counter(cudaStream_t stream, unsigned long long** out) {
     static std::mutex mu;
-    static std::vector<std::pair<std::pair<int, cudaStream_t>, unsigned long long*>> reg;
+    static std::vector<std::pair<std::pair<int, unsigned long long>, unsigned long long*>> reg;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
+    unsigned long long sid = 0;
+    e = cudaStreamGetId(stream, &sid);
+    if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(mu);
     for (auto& r : reg)
-        if (r.first.first == dev && r.first.second == stream) {
+        if (r.first.first == dev && r.first.second == sid) {
             *out = r.second;
             return cudaSuccess;
         }
@@ -930,7 +936,7 @@ cudaError_t stream_counter(cudaStream_t stream, unsigned long long** out) {
     if (e != cudaSuccess) return e;
     e = cudaMemset(c, 0, 2 * sizeof(unsigned long long));
     if (e != cudaSuccess) return e;
-    reg.push_back({{dev, stream}, c});
+    reg.push_back({{dev, sid}, c});
     *out = c;
     return cudaSuccess;
 }
@@ -962,8 +968,7 @@ cudaError_t launch_small(const double* in, double* out, std::size_t batch, const
             threads = kLockThreads;
         }
     }
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const cudaError_t attr = smem_optin(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
     if (attr != cudaSuccess) return attr;
     const std::size_t ntiles = (batch + TS - 1) / TS;
     const unsigned grid = static_cast<unsigned>(std::min<std::size_t>(ntiles, static_cast<std::size_t>(num_sms)));

@@ -31,6 +31,11 @@ struct Emit {
     std::size_t ld_alt = 0;
 };
 
+/// Whether the DCT-II/III kernels take rows of length n (the row lives in
+/// shared memory: powers of two up to 8192 in fp64 / 16384 in fp32, other
+/// lengths up to 14528 / 29056).
+bool dct_supported(std::size_t n, bool f64);
+
 /// Forward DCT-II of `batch` rows of length n (orthonormal, U^T s):
 ///   hat[b*ld_hat + k]     = shat_k          (if hat != nullptr)
 ///   out[b*ld_out + to[e]] = sign[e] * shat_{from[e]}   for each emit entry

@@ -348,11 +348,7 @@ cudaError_t launch_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, c
                         int nch, double* out, std::size_t ld_out, const int* col_map, const double* fold_add,
                         std::size_t ld_add, cudaStream_t stream) {
     using G = Geo<S, NT>;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    // the >48 KB opt-in is per device: set it on every call (cheap)
-    cudaError_t e = cudaFuncSetAttribute(ozaki_gemm_kernel<S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         G::kSmem);
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(ozaki_gemm_kernel<S, NT>), G::kSmem);
     if (e != cudaSuccess) return e;
     const std::size_t gm = (M + TM - 1) / TM;
     const unsigned gn = static_cast<unsigned>((N + NT - 1) / NT);

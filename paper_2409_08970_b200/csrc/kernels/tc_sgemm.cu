@@ -394,10 +394,8 @@ cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* 
         return (e && e[0] == '1') ? 2 : 1;
     }();
     constexpr int kSmem2 = kStages * (4 * kABytes + 2 * kBBytes) + 1024 + 64;
-    static const cudaError_t attr1 =
-        cudaFuncSetAttribute(tc_sgemm3_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    static const cudaError_t attr2 =
-        cudaFuncSetAttribute(tc_sgemm3_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+    const cudaError_t attr1 = smem_optin(reinterpret_cast<const void*>(tc_sgemm3_kernel<1>), kSmem);
+    const cudaError_t attr2 = smem_optin(reinterpret_cast<const void*>(tc_sgemm3_kernel<2>), kSmem2);
     if (attr1 != cudaSuccess) return attr1;
     if (attr2 != cudaSuccess) return attr2;
     static const bool mcast = [] { // opt-in: measured slower (the per-chunk cluster barrier)
@@ -405,8 +403,7 @@ cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* 
         return e && e[0] == '1';
     }();
     if (mcast && mt == 1 && b_sw) {
-        static const cudaError_t attr3 =
-            cudaFuncSetAttribute(tc_sgemm3_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        const cudaError_t attr3 = smem_optin(reinterpret_cast<const void*>(tc_sgemm3_kernel<1, true>), kSmem);
         if (attr3 != cudaSuccess) return attr3;
         const unsigned gx = static_cast<unsigned>(((M + BM - 1) / BM + 1) / 2 * 2); // whole CTA pairs
         cudaLaunchConfig_t cfg = {};
@@ -428,12 +425,28 @@ cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* 
         const char* e = std::getenv("DCTP_TC32_NFIRST");
         return (e && e[0] == '0') ? 0 : 1;
     }();
-    const unsigned gm = static_cast<unsigned>((M + BM * mt - 1) / (BM * mt)), gn = static_cast<unsigned>((N + BN - 1) / BN);
-    if (nfirst && gm > 65535u) return cudaErrorInvalidValue;
-    const dim3 grid = nfirst ? dim3(gn, gm) : dim3(gm, gn);
-    (mt == 2 ? tc_sgemm3_kernel<2> : tc_sgemm3_kernel<1>)<<<grid, kThreads * mt, mt == 2 ? kSmem2 : kSmem, stream>>>(A, lda, bt_hi, bt_lo, ldb, C, ldc, M, N, K, flag, col_map,
-                                                         a_map, fold_add, ld_add, b_sw, debug, nfirst);
-    return cudaGetLastError();
+    const std::size_t rows_per_tile = static_cast<std::size_t>(BM) * mt;
+    const std::size_t gm_all = (M + rows_per_tile - 1) / rows_per_tile;
+    const unsigned gn = static_cast<unsigned>((N + BN - 1) / BN);
+    // row tiles on grid.y (nfirst) are limited to 65535: launch row slices
+    // (DCTP_TC32_SLICE_TILES lowers the slice for the tests)
+    static const std::size_t slice = [] {
+        const char* e = std::getenv("DCTP_TC32_SLICE_TILES");
+        const long v = e ? std::atol(e) : 65535;
+        return static_cast<std::size_t>(v >= 1 && v <= 65535 ? v : 65535);
+    }();
+    for (std::size_t t0 = 0; t0 < gm_all; t0 += slice) {
+        const unsigned gm = static_cast<unsigned>(gm_all - t0 < slice ? gm_all - t0 : slice);
+        const std::size_t r0 = t0 * rows_per_tile;
+        const dim3 grid = nfirst ? dim3(gn, gm) : dim3(gm, gn);
+        (mt == 2 ? tc_sgemm3_kernel<2> : tc_sgemm3_kernel<1>)<<<grid, kThreads * mt, mt == 2 ? kSmem2 : kSmem,
+                                                               stream>>>(
+            A + r0 * static_cast<std::size_t>(lda), lda, bt_hi, bt_lo, ldb, C + r0 * ldc, ldc, M - r0, N, K, flag,
+            col_map, a_map, fold_add ? fold_add + r0 * ld_add : nullptr, ld_add, b_sw, debug, nfirst);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 } // namespace dctp::dev

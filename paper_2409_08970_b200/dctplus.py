@@ -129,6 +129,26 @@ def _dev_rows(x, n: int, what: str):
     return rows.contiguous(), single
 
 
+def _check_out(out, rows, shape, what: str):
+    """A caller-supplied device output: same dtype and device as the rows,
+    contiguous, exactly `shape`, and not overlapping the input."""
+    if not _is_device_tensor(out):
+        raise N.InvalidArgument(f"{what}: out must be a CUDA tensor")
+    if out.dtype != rows.dtype or out.device != rows.device:
+        raise N.InvalidArgument(f"{what}: out must match the input's dtype and device")
+    if out.dim() == len(shape) - 1 and shape[0] == 1:  # one signal: out without the batch axis
+        out = out.unsqueeze(0)
+    if tuple(out.shape) != tuple(shape):
+        raise N.InvalidArgument(f"{what}: out has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    if not out.is_contiguous():
+        raise N.InvalidArgument(f"{what}: out must be contiguous")
+    a0, a1 = rows.data_ptr(), rows.data_ptr() + rows.numel() * rows.element_size()
+    b0, b1 = out.data_ptr(), out.data_ptr() + out.numel() * out.element_size()
+    if out.numel() and rows.numel() and a0 < b1 and b0 < a1:
+        raise N.InvalidArgument(f"{what}: out must not overlap the input")
+    return out
+
+
 class DctPlusPlan:
     """Fast DCT+ of one rank-one update of the path graph (fast_transform.hpp:43-302)."""
 
@@ -225,7 +245,7 @@ class DctPlusPlan:
         what = "DctPlusPlan"
         if _is_device_tensor(x):
             rows, single = _dev_rows(x, n, what)
-            y = out if out is not None else torch.empty_like(rows)
+            y = _check_out(out, rows, rows.shape, what) if out is not None else torch.empty_like(rows)
             fn = getattr(lib, self._DEV[(op, rows.dtype == torch.float64)])
             stream = _stream_ptr(rows.device)
             check(fn(self._h, C.c_void_p(rows.data_ptr()), C.c_void_p(y.data_ptr()), rows.shape[0], stream))
@@ -356,8 +376,8 @@ class PrunedEnsemblePlan:
         n, sets = self._n, self.ensemble_size()
         if _is_device_tensor(s):
             rows, single = _dev_rows(s, n, "pruned_forward_all")
-            y = out if out is not None else torch.empty((rows.shape[0], sets, n), dtype=rows.dtype,
-                                                        device=rows.device)
+            y = _check_out(out, rows, (rows.shape[0], sets, n), "pruned_forward_all") if out is not None else \
+                torch.empty((rows.shape[0], sets, n), dtype=rows.dtype, device=rows.device)
             stream = _stream_ptr(rows.device)
             if with_bounds:
                 bounds = torch.empty((rows.shape[0], sets), dtype=rows.dtype, device=rows.device)
@@ -556,7 +576,7 @@ class ChainedFactorization:
         n = self.n
         if _is_device_tensor(s):
             rows, single = _dev_rows(s, n, "chain_forward")
-            y = out if out is not None else torch.empty_like(rows)
+            y = _check_out(out, rows, rows.shape, "chain_forward") if out is not None else torch.empty_like(rows)
             fn = lib.dctp_chain_forward_f64 if rows.dtype == torch.float64 else lib.dctp_chain_forward_f32
             stream = _stream_ptr(rows.device)
             check(fn(self._h, C.c_void_p(rows.data_ptr()), C.c_void_p(y.data_ptr()), rows.shape[0], stream))

@@ -2,12 +2,15 @@
 // reference's own suites (proj/tests/test_fast_transform.cpp,
 // test_spectral.cpp, test_pruning.cpp): known answers, dense-oracle checks,
 // SNR >= 100 dB, exception classes.  Prints "ALL OK" and exits 0 on success.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <limits>
 #include <cstdlib>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime_api.h>
@@ -86,7 +89,7 @@ int main() {
                 const std::vector<double> fast = plan.forward(s, ws);
                 std::vector<double> dense(n, 0.0);
                 for (std::size_t i = 0; i < n; ++i)
-                    for (std::size_t j = 0; j < n; ++j) dense[j] += x[i * n + j] * s[i];
+                    for (std::size_t j = 0; j < n; ++j) dense[j] += x(i, j) * s[i];
                 CHECK(snr_db(dense, fast) >= 100.0);
                 const auto back = plan.inverse(fast);
                 CHECK(snr_db(s, back) >= 100.0);
@@ -185,6 +188,109 @@ int main() {
         }
         CHECK(named);
     }
+    // test_pruning.cpp:22-48 with the workspace overload (fast_transform.hpp:389-439)
+    {
+        const std::vector<RankOneUpdate> kEnsembleUpdates = {RankOneUpdate::self_loop(1, 1.5),
+                                                             RankOneUpdate::edge_delta(2, 3, 1.5)};
+        const double kAlwaysPrune = std::numeric_limits<double>::max();
+        CHECK(throws<std::invalid_argument>([&] { PrunedEnsemblePlan(16, kEnsembleUpdates, 0, 1.0); }));
+        CHECK(throws<std::invalid_argument>([&] { PrunedEnsemblePlan(16, kEnsembleUpdates, 17, 1.0); }));
+        {   // k = 1 degenerates to the plain DCT
+            const PrunedEnsemblePlan plan(16, {}, 16, kAlwaysPrune);
+            CHECK(plan.ensemble_size() == 1);
+            std::vector<double> s(16);
+            detail::check(dctp_fill_signals(7, 2, 0.99, 16, 1, s.data()));
+            const auto res = plan.forward_all(s);
+            CHECK(res.coeffs.size() == 1);
+            const TrigPlan dct(TrigKind::dct2, 16);
+            const auto d = dct(s);
+            double diff = 0.0;
+            for (std::size_t j = 0; j < 16; ++j) diff = std::max(diff, std::abs(d[j] - res.coeffs[0][j]));
+            CHECK(diff < 1e-14);
+        }
+        {   // c_p = n reproduces the full transforms; Rng(11), five AR(0.99) signals
+            const std::size_t n = 16;
+            const PrunedEnsemblePlan plan(n, kEnsembleUpdates, n, kAlwaysPrune);
+            std::vector<double> sig(5 * n);
+            detail::check(dctp_fill_signals(11, 2, 0.99, n, 5, sig.data()));
+            PrunedWorkspace ws = plan.make_workspace();
+            PrunedEnsemblePlan::Result res;
+            for (int rep = 0; rep < 5; ++rep) {
+                const std::vector<double> s(sig.begin() + rep * n, sig.begin() + (rep + 1) * n);
+                plan.forward_all(s, ws, res);
+                CHECK(res.pruned);
+                CHECK(res.coeffs.size() == plan.ensemble_size());
+                for (std::size_t r = 1; r < plan.ensemble_size(); ++r)
+                    CHECK(snr_db(plan.member(r).forward(s), res.coeffs[r]) >= 100.0);
+            }
+        }
+        {   // accessors by const reference (fast_transform.hpp:136-143, 262)
+            const DctPlusPlan plan(64, RankOneUpdate::edge_delta(10, 40, 0.7), 1e-12);
+            const CauchyFactorization& f = plan.factorization();
+            CHECK(&plan.mu() == &f.mu());
+            CHECK(&plan.lambda() == &f.lambda);
+            CHECK(f.size() == 64 && f.rho() == 0.7);
+            CHECK(f.spec.slots.size() == 64 && f.sigma.size() == 64);
+            std::size_t active = 0;
+            for (const auto& sl : f.spec.slots) active += sl.passthrough ? 0 : 1;
+            CHECK(active == f.spec.sub_mu.size() && f.spec.sub_lambda.size() == f.spec.sub_z.size());
+            CHECK(&plan.basis() == &plan.basis() && plan.basis().rows() == 64);
+            CHECK(plan.dct_plan().size() == 64);
+        }
+    }
+    // the reference's threading contract (fast_transform.hpp:33-34, README.md:82-87): one
+    // shared plan, four host threads on their own streams; a NaN in thread 2's batch raises
+    // std::domain_error in thread 2's call only (per-stream flags)
+    {
+        const std::size_t n = 256, batch = 512;
+        const DctPlusPlan plan(n, RankOneUpdate::edge_delta(128, 129, -0.7), 1e-12);
+        std::vector<double> h(n * batch);
+        detail::check(dctp_fill_signals(5, 2, 0.95, n, batch, h.data()));
+        for (int use_per_thread_stream = 0; use_per_thread_stream < 2; ++use_per_thread_stream) {
+            int outcome[4] = {0, 0, 0, 0}; // 1 ok, 2 domain_error, 3 other
+            std::vector<std::thread> pool;
+            for (int t = 0; t < 4; ++t)
+                pool.emplace_back([&, t] {
+                    cudaStream_t st = cudaStreamPerThread;
+                    if (!use_per_thread_stream) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+                    double *din = nullptr, *dout = nullptr;
+                    cudaMalloc(reinterpret_cast<void**>(&din), n * batch * 8);
+                    cudaMalloc(reinterpret_cast<void**>(&dout), n * batch * 8);
+                    std::vector<double> mine = h;
+                    if (t == 2) mine[77 * n + 5] = std::nan("");
+                    cudaMemcpy(din, mine.data(), n * batch * 8, cudaMemcpyHostToDevice);
+                    int res = 1;
+                    for (int it = 0; it < 20 && res == 1; ++it) {
+                        try {
+                            plan.forward_batch(din, dout, batch, st);
+                            plan.sync_check(st);
+                        } catch (const std::domain_error&) {
+                            res = 2;
+                        } catch (...) {
+                            res = 3;
+                        }
+                    }
+                    // the host-buffer path of the same thread: isolated too
+                    try {
+                        std::vector<double> y(n * batch);
+                        plan.forward_host(mine.data(), y.data(), batch);
+                        if (res == 2) res = 3; // NaN input must raise here as well
+                    } catch (const std::domain_error&) {
+                        if (res != 2) res = 3;
+                    } catch (...) {
+                        res = 3;
+                    }
+                    outcome[t] = res;
+                    cudaFree(din);
+                    cudaFree(dout);
+                    if (!use_per_thread_stream) cudaStreamDestroy(st);
+                });
+            for (auto& th : pool) th.join();
+            for (int t = 0; t < 4; ++t) CHECK(outcome[t] == (t == 2 ? 2 : 1));
+        }
+    }
+    // n beyond the GPU DCT kernels' shared-memory row: a clear invalid_argument at creation
+    CHECK(throws<std::invalid_argument>([] { DctPlusPlan(16384, RankOneUpdate::self_loop(1, 1.0), 1e-12); }));
     if (failures == 0) std::printf("ALL OK\n");
     return failures == 0 ? 0 : 1;
 }

@@ -1,0 +1,143 @@
+"""Boundary behaviour on the GPU: caller-supplied outputs are validated,
+per-thread non-finite flags, the tcgen05 GEMM's row slicing beyond the grid
+limit, the DCT size limit, and the int8 (Ozaki) product's slice-count knob."""
+import os
+import subprocess
+import sys
+import threading
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import checkers as O
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2409_08970_b200 as P
+
+    return P
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    torch.cuda.init()
+    return torch
+
+
+def test_out_argument_is_validated(P, torch):
+    plan = P.DctPlusPlan(64, P.RankOneUpdate.self_loop(1, 0.5), 1e-12)
+    x = torch.randn((10, 64), dtype=torch.float64, device="cuda")
+    good = torch.empty_like(x)
+    assert plan.forward(x, out=good) is not None
+    bad = [torch.empty((10, 64), dtype=torch.float32, device="cuda"),   # dtype
+           torch.empty((9, 64), dtype=torch.float64, device="cuda"),    # short
+           torch.empty((64, 10), dtype=torch.float64, device="cuda").t(),  # strided view
+           torch.empty((10, 64), dtype=torch.float64),                  # host
+           x]                                                            # aliasing the input
+    for out in bad:
+        with pytest.raises(P.InvalidArgument):
+            plan.forward(x, out=out)
+    # one signal: out without the batch axis is accepted
+    y1 = torch.empty(64, dtype=torch.float64, device="cuda")
+    plan.forward(x[0], out=y1)
+    assert torch.allclose(y1, plan.forward(x[0]))
+    ens = P.PrunedEnsemblePlan(64, [P.RankOneUpdate.self_loop(1, w) for w in (0.5, 1.0)], 64, 1.7e308)
+    with pytest.raises(P.InvalidArgument):
+        ens.forward_all_batch(x, out=torch.empty((10, 2, 64), dtype=torch.float64, device="cuda"))
+
+
+def test_nan_surfaces_only_in_its_own_thread(P, torch):
+    """Four host threads share one plan, each on its own stream; only the
+    thread whose batch holds a NaN gets DomainError (fast_transform.hpp:33-34,
+    271-276: the failing call throws)."""
+    plan = P.DctPlusPlan(256, P.RankOneUpdate.edge_delta(128, 129, -0.7), 1e-12)
+    base = torch.as_tensor(P.fill_signals(3, P.DIST_AR, 256, 1024, 0.95), device="cuda")
+    results = [None] * 4
+    barrier = threading.Barrier(4)
+
+    def work(t):
+        s = torch.cuda.Stream()
+        x = base.clone()
+        if t == 1:
+            x[500, 7] = float("nan")
+        torch.cuda.synchronize()
+        barrier.wait()
+        out = "ok"
+        with torch.cuda.stream(s):
+            for _ in range(10):
+                try:
+                    plan.forward(x)
+                except P.DomainError:
+                    out = "domain"
+                    break
+        results[t] = out
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert results == ["ok", "domain", "ok", "ok"], results
+
+
+def test_tc_sgemm_row_slices_match_single_grid(P, torch, tmp_path):
+    """The tcgen05 3xTF32 GEMM launches row slices once the row tiles exceed
+    the grid limit; a lowered slice size (3 tiles) must give bit-identical
+    C4 outputs."""
+    script = tmp_path / "c4.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "import paper_2409_08970_b200 as P\n"
+        "ws = [0.05 + k * (1.95 / 15.0) for k in range(16)]\n"
+        "ens = P.PrunedEnsemblePlan(128, [P.RankOneUpdate.self_loop(1, w) for w in ws], 128, 1.7e308)\n"
+        "x = torch.as_tensor(P.fill_signals(P.mix_seed(2409, 128, 4), P.DIST_AR2D, 128, 5000, 0.9), device='cuda')\n"
+        "np.save(sys.argv[1], ens.forward_all_batch(x.float()).cpu().numpy())\n")
+    outs = []
+    for tiles in ("65535", "3"):
+        f = tmp_path / f"y{tiles}.npy"
+        env = dict(os.environ, DCTP_TC32_SLICE_TILES=tiles)
+        subprocess.run([sys.executable, str(script), str(f)], env=env, check=True, timeout=300)
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_dct_size_limit_is_a_clear_error(P, torch):
+    with pytest.raises(P.InvalidArgument, match="exceeds the GPU DCT kernels"):
+        P.DctPlusPlan(16384, P.RankOneUpdate.self_loop(1, 1.0), 1e-12)
+    with pytest.raises(P.InvalidArgument):
+        P.dct2(torch.zeros((1, 16384), dtype=torch.float64, device="cuda"))
+
+
+def test_ozaki_slice_counts_agree(P, torch, reference, tmp_path):
+    """DCTP_OZAKI_SLICES=6 (21 int8 products) and the default 5 (15) both
+    meet the fp64 tolerance on a general-direction dense plan; 6 is ~100x
+    tighter."""
+    script = tmp_path / "oz.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "import paper_2409_08970_b200 as P\n"
+        "n = 2048\n"
+        "v = P.fill_signals(P.mix_seed(2409, n, 50), 0, n, 1)[0] / np.sqrt(n)\n"
+        "plan = P.DctPlusPlan(n, P.RankOneUpdate.general(v, 0.1), 1e-12)\n"
+        "assert P.ozaki_slices(n) == int(sys.argv[2])\n"
+        "x = torch.as_tensor(P.fill_signals(5, 0, n, 300), device='cuda')\n"
+        "np.save(sys.argv[1], plan.forward(x).cpu().numpy())\n")
+    n = 2048
+    v = P.fill_signals(P.mix_seed(2409, n, 50), 0, n, 1)[0] / np.sqrt(n)
+    want = reference.plan(n, O.Update(2, 0.1, 0, 0, tuple(v))).forward(P.fill_signals(5, 0, n, 300))
+    errs = {}
+    for sl in ("5", "6"):
+        f = tmp_path / f"y{sl}.npy"
+        env = dict(os.environ, DCTP_OZAKI_SLICES=sl)
+        subprocess.run([sys.executable, str(script), str(f), sl], env=env, check=True, timeout=300)
+        errs[sl] = O.parity(np.load(f), want)
+    assert errs["5"] <= 1e-10 and errs["6"] <= 1e-12, errs

@@ -1600,13 +1600,14 @@ static void rows_by_ozaki(const double* in, std::size_t ld_in, const int8_t* b_s
                           int S, double* out, std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t s,
                           const char* name, const int* col_map, const int* a_map, const double* fold_add,
                           std::size_t ld_add) {
-    const std::size_t a_bytes = dctp::dev::ozaki_slice_bytes(batch, K, 128, S);
-    const std::size_t rows_pad = (batch + 127) / 128 * 128;
+    const int pm = dctp::dev::ozaki_pad_m();
+    const std::size_t a_bytes = dctp::dev::ozaki_slice_bytes(batch, K, 128, S, pm);
+    const std::size_t rows_pad = (batch + pm - 1) / pm * pm;
     Scratch<int8_t> a_sl(a_bytes, s);
     Scratch<int> ea(rows_pad, s);
     cuda_check(DCTP_LAUNCH("ozaki_slice", s,
                            dctp::dev::ozaki_slice<double>(in, ld_in, batch, K, a_map, 128, S, a_sl.ptr, ea.ptr, flag,
-                                                          s)),
+                                                          s, pm)),
                "signal slicing kernel");
     cuda_check(DCTP_LAUNCH(name, s,
                            dctp::dev::ozaki_gemm(a_sl.ptr, ea.ptr, b_sl, eb, batch, N, K, S, out, ld_out, col_map, s,
@@ -1618,14 +1619,14 @@ static void rows_by_ozaki(const double* in, std::size_t ld_in, const int8_t* b_s
 /// of ozaki_gemm; (slices, exponents) in device memory owned by the caller.
 static std::pair<int8_t*, int*> slice_operand(const double* bt, std::size_t ld, std::size_t rows, int K, int S,
                                               cudaStream_t s) {
-    const int tn = dctp::dev::ozaki_tile_n(S);
+    const int tn = dctp::dev::ozaki_tile_n(S), pn = dctp::dev::ozaki_pad_n(S);
     int8_t* sl = nullptr;
     int* ex = nullptr;
-    cuda_check(cudaMalloc(reinterpret_cast<void**>(&sl), dctp::dev::ozaki_slice_bytes(rows, K, tn, S)),
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&sl), dctp::dev::ozaki_slice_bytes(rows, K, tn, S, pn)),
                "cudaMalloc(operand slices)");
-    cuda_check(cudaMalloc(reinterpret_cast<void**>(&ex), (rows + tn - 1) / tn * tn * sizeof(int)),
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&ex), (rows + pn - 1) / pn * pn * sizeof(int)),
                "cudaMalloc(operand exponents)");
-    cuda_check(dctp::dev::ozaki_slice<double>(bt, ld, rows, K, nullptr, tn, S, sl, ex, nullptr, s),
+    cuda_check(dctp::dev::ozaki_slice<double>(bt, ld, rows, K, nullptr, tn, S, sl, ex, nullptr, s, pn),
                "operand slicing kernel");
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(operand slices)");
     return {sl, ex};

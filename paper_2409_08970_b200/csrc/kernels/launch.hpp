@@ -158,16 +158,19 @@ cudaError_t rows_by_basis(const T* in, std::size_t ld_in, const double* bt, std:
 /// gathered through a_map if given) becomes `slices` int8 digits with a
 /// power-of-two row exponent expo[r], written in the GEMM's tile image for
 /// tiles of `tile_rows` rows (128 for the A side, ozaki_tile_n(slices) for
-/// the B side); non-finite samples raise flag bit 0.  Then
+/// the B side), rows zero-padded to a multiple of pad_rows (ozaki_pad_m() /
+/// ozaki_pad_n(slices)); non-finite samples raise flag bit 0.  Then
 ///   out[b, col_map ? col_map[c] : c] = sum_k a[b, k] bt[c, k]
 /// (or unfolded with fold_add as in rows_by_basis) for M rows of a and N rows
 /// of bt, accurate to ~1e-13 (6 slices) / ~3e-11 (5 slices) of the row
 /// maxima.  K <= 16384.
 int ozaki_tile_n(int slices);
-std::size_t ozaki_slice_bytes(std::size_t rows, int K, int tile_rows, int slices);
+int ozaki_pad_n(int slices);
+int ozaki_pad_m();
+std::size_t ozaki_slice_bytes(std::size_t rows, int K, int tile_rows, int slices, int pad_rows = 0);
 template <class T>
 cudaError_t ozaki_slice(const T* in, std::size_t ld, std::size_t rows, int K, const int* a_map, int tile_rows,
-                        int slices, int8_t* sl, int* expo, int* flag, cudaStream_t stream);
+                        int slices, int8_t* sl, int* expo, int* flag, cudaStream_t stream, int pad_rows = 0);
 cudaError_t ozaki_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M, int N,
                        int K, int slices, double* out, std::size_t ld_out, const int* col_map, cudaStream_t stream,
                        const double* fold_add = nullptr, std::size_t ld_add = 0);

@@ -74,6 +74,14 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, 
         "l"(a), "l"(b), "r"(idesc_i8<NT>()), "r"(accumulate));
 }
 
+/// One lane of a converged warp (elect.sync): the warp-uniform issue pattern
+/// that keeps the MMA loop in uniform registers.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.b32 %0, 1, 0, P;\n}\n" : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                      ptx::smem_addr(bar))
@@ -200,94 +208,17 @@ struct Geo {
     static_assert(NT % 16 == 0 && NT >= 16 && NT <= 256, "M = 128 needs N % 16 == 0");
 };
 
-template <int S, int NT>
-__global__ void __launch_bounds__(kThreads, 1)
-ozaki_gemm_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, const int8_t* __restrict__ b_sl,
-                  const int* __restrict__ eb, std::size_t M, int N, int nch, double* __restrict__ out,
-                  std::size_t ld_out, const int* __restrict__ col_map, const double* __restrict__ fold_add,
-                  std::size_t ld_add) {
-    using G = Geo<S, NT>;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const uint32_t raw = ptx::smem_addr(smem_raw);
-    unsigned char* base = smem_raw + ((1024 - (raw & 1023)) & 1023);
-    uint64_t* full = reinterpret_cast<uint64_t*>(base + G::kStages * G::kStageBytes);
-    uint64_t* empty = full + G::kStages;
-    uint64_t* done = empty + G::kStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-    const uint32_t sbase = ptx::smem_addr(base);
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // grid x = row tile (fastest): the CTAs in flight share their B column tile
-    const std::size_t mt = blockIdx.x;
-    const int nt = blockIdx.y;
-
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-                         ptx::smem_addr(tmem_slot))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-    }
-    if (tid == 32) {
-        for (int i = 0; i < G::kStages; ++i) {
-            ptx::mbar_init(full + i, 1);
-            ptx::mbar_init(empty + i, 1);
-        }
-        ptx::mbar_init(done, 1);
-        ptx::fence_mbar_init();
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const uint32_t tmem = *tmem_slot;
-
-    const int8_t* a_tile = a_sl + mt * static_cast<std::size_t>(nch) * G::kABytes;
-    const int8_t* b_tile = b_sl + static_cast<std::size_t>(nt) * nch * G::kBBytes;
-
-    if (warp == 0) {
-        if (lane == 0) { // producer: one A and one B bulk copy per chunk
-            for (int ch = 0; ch < nch; ++ch) {
-                const int st = ch % G::kStages;
-                if (ch >= G::kStages) ptx::mbar_wait(empty + st, static_cast<uint32_t>(((ch / G::kStages) - 1) & 1));
-                ptx::mbar_expect_tx(full + st, G::kStageBytes);
-                unsigned char* dst = base + st * G::kStageBytes;
-                ptx::bulk_load(dst, a_tile + static_cast<std::size_t>(ch) * G::kABytes, G::kABytes, full + st);
-                ptx::bulk_load(dst + G::kABytes, b_tile + static_cast<std::size_t>(ch) * G::kBBytes, G::kBBytes,
-                               full + st);
-            }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
-        if (lane == 0) { // MMA issuer
-            for (int ch = 0; ch < nch; ++ch) {
-                const int st = ch % G::kStages;
-                ptx::mbar_wait(full + st, static_cast<uint32_t>((ch / G::kStages) & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                const uint32_t sa = sbase + st * G::kStageBytes, sb = sa + G::kABytes;
-#pragma unroll
-                for (int kk = 0; kk < CB / 32; ++kk) {
-                    const uint32_t o = 32u * kk;
-#pragma unroll
-                    for (int L = 0; L < G::kLevels; ++L) {
-                        const uint32_t td = tmem + static_cast<uint32_t>(L * NT);
-#pragma unroll
-                        for (int i = 0; i <= L; ++i) {
-                            const int j = L - i;
-                            const uint32_t acc = (ch > 0 || kk > 0 || i > 0) ? 1u : 0u;
-                            mma_i8<NT>(td, smem_desc(sa + i * TM * CB + o), smem_desc(sb + j * NT * CB + o), acc);
-                        }
-                    }
-                }
-                mma_commit(empty + st);
-            }
-            mma_commit(done);
-        }
-        __syncwarp();
-    }
-
-    // epilogue: warp w reads TMEM lanes 32 w .. 32 w + 31 (tile rows)
-    ptx::mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const std::size_t row = mt * TM + 32 * warp + lane;
+/// Epilogue of one 128 x NT tile (rows row0..row0+127, columns nt NT..):
+/// warp w reads TMEM lanes 32 w .. 32 w + 31 level by level (Horner in fp64,
+/// exact int32 -> fp64 conversions), scales by 2^(e_b + f_c) / 127^2 and
+/// stores the fp64 row segment (or scatters / unfolds it).
+template <int LEVELS, int NT>
+__device__ __forceinline__ void store_tile(uint32_t tmem, std::size_t row0, int nt, int warp, int lane, std::size_t M,
+                                           int N, const int* __restrict__ ea, const int* __restrict__ eb,
+                                           double* __restrict__ out, std::size_t ld_out,
+                                           const int* __restrict__ col_map, const double* __restrict__ fold_add,
+                                           std::size_t ld_add) {
+    const std::size_t row = row0 + 32 * warp + lane;
     const bool live = row < M;
     const double rs = live ? ldexp(1.0 / (127.0 * 127.0), ea[row]) : 0.0;
     constexpr double kInv = 1.0 / 254.0;
@@ -296,10 +227,10 @@ ozaki_gemm_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, c
         double acc[32];
         uint32_t v[32];
 #pragma unroll 1
-        for (int L = G::kLevels - 1; L >= 0; --L) {
+        for (int L = LEVELS - 1; L >= 0; --L) {
             tmem_ld32(tmem + (static_cast<uint32_t>(32 * warp) << 16) + static_cast<uint32_t>(L * NT + c0), v);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-            if (L == G::kLevels - 1) {
+            if (L == LEVELS - 1) {
 #pragma unroll
                 for (int u = 0; u < 32; ++u) acc[u] = static_cast<double>(static_cast<int>(v[u]));
             } else {
@@ -337,10 +268,320 @@ ozaki_gemm_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, c
             }
         }
     }
+}
+
+template <int S, int NT>
+__global__ void __launch_bounds__(kThreads, 1)
+ozaki_gemm_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, const int8_t* __restrict__ b_sl,
+                  const int* __restrict__ eb, std::size_t M, int N, int nch, double* __restrict__ out,
+                  std::size_t ld_out, const int* __restrict__ col_map, const double* __restrict__ fold_add,
+                  std::size_t ld_add, int debug) {
+    using G = Geo<S, NT>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t raw = ptx::smem_addr(smem_raw);
+    unsigned char* base = smem_raw + ((1024 - (raw & 1023)) & 1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + G::kStages * G::kStageBytes);
+    uint64_t* empty = full + G::kStages;
+    uint64_t* done = empty + G::kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    const uint32_t sbase = ptx::smem_addr(base);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // grid x = row tile (fastest): the CTAs in flight share their B column tile
+    const std::size_t mt = blockIdx.x;
+    const int nt = blockIdx.y;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                         ptx::smem_addr(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (tid == 32) {
+        for (int i = 0; i < G::kStages; ++i) {
+            ptx::mbar_init(full + i, 1);
+            ptx::mbar_init(empty + i, 1);
+        }
+        ptx::mbar_init(done, 1);
+        ptx::fence_mbar_init();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    const int8_t* a_tile = a_sl + mt * static_cast<std::size_t>(nch) * G::kABytes;
+    const int8_t* b_tile = b_sl + static_cast<std::size_t>(nt) * nch * G::kBBytes;
+
+    if (warp == 0) { // producer warp: one A and one B bulk copy per chunk
+        // development knob DCTP_OZAKI_DEBUG=1: load only the first ring of
+        // chunks (the MMAs then reuse them: tensor-pipe time alone)
+        const int nload = (debug & 1) ? (nch < G::kStages ? nch : G::kStages) : nch;
+        for (int ch = 0; ch < nload; ++ch) {
+            const int st = ch % G::kStages;
+            if (ch >= G::kStages) ptx::mbar_wait(empty + st, static_cast<uint32_t>(((ch / G::kStages) - 1) & 1));
+            if (elect_one()) {
+                ptx::mbar_expect_tx(full + st, G::kStageBytes);
+                unsigned char* dst = base + st * G::kStageBytes;
+                ptx::bulk_load(dst, a_tile + static_cast<std::size_t>(ch) * G::kABytes, G::kABytes, full + st);
+                ptx::bulk_load(dst + G::kABytes, b_tile + static_cast<std::size_t>(ch) * G::kBBytes, G::kBBytes,
+                               full + st);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1) { // MMA warp: one elected lane issues, the warp stays converged
+        // descriptors of stage 0; other stages / slices / K steps add their
+        // byte offset / 16 to the 14-bit start-address field (< 256 KB: no carry)
+        const uint64_t adesc0 = smem_desc(sbase), bdesc0 = smem_desc(sbase + G::kABytes);
+        for (int ch = 0; ch < nch; ++ch) {
+            const int st = ch % G::kStages;
+            if (!(debug & 1) || ch < G::kStages) ptx::mbar_wait(full + st, static_cast<uint32_t>((ch / G::kStages) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (elect_one()) {
+                const uint64_t so = static_cast<uint64_t>(st * G::kStageBytes) >> 4;
+                const uint64_t ad = adesc0 + so, bd = bdesc0 + so;
+                // slice i outer, j inner: consecutive MMAs write different
+                // level accumulators (L = i + j), never the one just issued
+#pragma unroll
+                for (int kk = 0; kk < CB / 32; ++kk) {
+#pragma unroll
+                    for (int i = 0; i < G::kLevels; ++i) {
+#pragma unroll
+                        for (int j = 0; i + j < G::kLevels; ++j) {
+                            const int L = i + j;
+                            const uint32_t td = tmem + static_cast<uint32_t>(L * NT);
+                            const uint32_t acc = (ch > 0 || kk > 0 || i > 0) ? 1u : 0u;
+                            if (!(debug & 2)) // DCTP_OZAKI_DEBUG=2: loads only
+                                mma_i8<NT>(td, ad + ((i * TM * CB + 32 * kk) >> 4), bd + ((j * NT * CB + 32 * kk) >> 4),
+                                           acc);
+                        }
+                    }
+                }
+                mma_commit(empty + st);
+            }
+            __syncwarp();
+        }
+        if (elect_one()) mma_commit(done);
+        __syncwarp();
+    }
+
+    // epilogue: warp w reads TMEM lanes 32 w .. 32 w + 31 (tile rows)
+    ptx::mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    store_tile<G::kLevels, NT>(tmem, mt * TM, nt, warp, lane, M, N, ea, eb, out, ld_out, col_map, fold_add, ld_add);
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+}
+
+// ---------------------------------------------------------- CTA-pair GEMM
+
+/// Geometry of the CTA-pair kernel: an MMA is M = 256 (128 rows per CTA) x
+/// N = NT; each CTA stages its own 128 A rows and one half (NT / 2 rows) of
+/// the B tile, so per SM the tensor core reads 128 + NT/2 operand rows per
+/// K step instead of 128 + NT (the shared-memory read rate is what holds the
+/// single-CTA N = 96 MMA at ~82% of the tensor peak).
+template <int S, int NT>
+struct Geo2 {
+    static constexpr int kLevels = S;
+    static constexpr int kHalf = NT / 2;
+    static constexpr int kABytes = S * TM * CB;
+    static constexpr int kBBytes = S * kHalf * CB;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = (kMaxSmem - 2048) / kStageBytes;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 + 512;
+    static_assert(kLevels * NT <= 512, "TMEM: one NT-column accumulator per level");
+    static_assert(kStages >= 2, "at least two pipeline stages");
+    static_assert(NT % 16 == 0 && NT <= 256 && kHalf % 8 == 0,
+                  "cta_group::2 with M = 256 needs N % 16 == 0; each half whole 8-row swizzle groups");
+};
+
+template <int NT>
+__host__ __device__ constexpr uint32_t idesc_i8_pair() {
+    return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(NT >> 3) << 17) |
+           (static_cast<uint32_t>(256 >> 4) << 24);
+}
+
+template <int NT>
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc_i8_pair<NT>()), "r"(accumulate));
+}
+
+/// Commit of the pair's MMAs, arriving on the barrier at the same offset in
+/// both CTAs.
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            ptx::smem_addr(bar)),
+        "h"(static_cast<uint16_t>(0x3))
+        : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+/// Arrive on the mbarrier at `bar`'s offset in CTA `rank` of the cluster.
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+    asm volatile(
+        "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(ptx::smem_addr(bar)),
+        "r"(rank)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAITC_%=;\n}\n" ::"r"(ptx::smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+/// Clusters of two CTAs along M.  CTA rank r holds rows 128 r.. of the pair's
+/// 256-row tile and B rows (NT / 2) r.. of the column tile (B sliced with
+/// tile_rows = NT / 2, so its half is tile 2 nt + r).  Rank 0 issues the
+/// cta_group::2 MMAs once both CTAs' stage landed: rank 1's warp 2 relays
+/// its full barrier to rank 0's peer_full barrier; the MMAs' completion is
+/// multicast to both CTAs' empty barriers.  Each CTA's TMEM holds its 128
+/// rows of every level accumulator and runs its own epilogue.
+template <int S, int NT>
+__global__ void __launch_bounds__(kThreads, 1)
+ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, const int8_t* __restrict__ b_sl,
+                   const int* __restrict__ eb, std::size_t M, int N, int nch, double* __restrict__ out,
+                   std::size_t ld_out, const int* __restrict__ col_map, const double* __restrict__ fold_add,
+                   std::size_t ld_add) {
+    using G = Geo2<S, NT>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t raw = ptx::smem_addr(smem_raw);
+    unsigned char* base = smem_raw + ((1024 - (raw & 1023)) & 1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + G::kStages * G::kStageBytes);
+    uint64_t* peer_full = full + G::kStages;
+    uint64_t* empty = peer_full + G::kStages;
+    uint64_t* done = empty + G::kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    const uint32_t sbase = ptx::smem_addr(base);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint32_t rank = 0;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const std::size_t mt = blockIdx.x; // this CTA's 128-row tile (pairs: 2 p, 2 p + 1)
+    const int nt = blockIdx.y;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                         ptx::smem_addr(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+    }
+    if (tid == 32) {
+        for (int i = 0; i < G::kStages; ++i) {
+            ptx::mbar_init(full + i, 1);
+            ptx::mbar_init(peer_full + i, 1);
+            ptx::mbar_init(empty + i, 1);
+        }
+        ptx::mbar_init(done, 1);
+        ptx::fence_mbar_init();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    cluster_sync(); // both CTAs' barriers and TMEM exist before any cross-CTA traffic
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    const int8_t* a_tile = a_sl + mt * static_cast<std::size_t>(nch) * G::kABytes;
+    const int8_t* b_tile = b_sl + (2 * static_cast<std::size_t>(nt) + rank) * nch * G::kBBytes;
+
+    if (warp == 0) { // producer warp (both CTAs): this CTA's A rows and B half
+        for (int ch = 0; ch < nch; ++ch) {
+            const int st = ch % G::kStages;
+            if (ch >= G::kStages) ptx::mbar_wait(empty + st, static_cast<uint32_t>(((ch / G::kStages) - 1) & 1));
+            if (elect_one()) {
+                ptx::mbar_expect_tx(full + st, G::kStageBytes);
+                unsigned char* dst = base + st * G::kStageBytes;
+                ptx::bulk_load(dst, a_tile + static_cast<std::size_t>(ch) * G::kABytes, G::kABytes, full + st);
+                ptx::bulk_load(dst + G::kABytes, b_tile + static_cast<std::size_t>(ch) * G::kBBytes, G::kBBytes,
+                               full + st);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1 && rank == 0) { // MMA warp of the pair
+        const uint64_t adesc0 = smem_desc(sbase), bdesc0 = smem_desc(sbase + G::kABytes);
+        for (int ch = 0; ch < nch; ++ch) {
+            const int st = ch % G::kStages;
+            const uint32_t ph = static_cast<uint32_t>((ch / G::kStages) & 1);
+            ptx::mbar_wait(full + st, ph);
+            mbar_wait_cluster(peer_full + st, ph);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (elect_one()) {
+                const uint64_t so = static_cast<uint64_t>(st * G::kStageBytes) >> 4;
+                const uint64_t ad = adesc0 + so, bd = bdesc0 + so;
+#pragma unroll
+                for (int kk = 0; kk < CB / 32; ++kk) {
+#pragma unroll
+                    for (int i = 0; i < G::kLevels; ++i) {
+#pragma unroll
+                        for (int j = 0; i + j < G::kLevels; ++j) {
+                            const uint32_t td = tmem + static_cast<uint32_t>((i + j) * NT);
+                            const uint32_t acc = (ch > 0 || kk > 0 || i > 0) ? 1u : 0u;
+                            mma_i8_pair<NT>(td, ad + ((i * TM * CB + 32 * kk) >> 4),
+                                            bd + ((j * G::kHalf * CB + 32 * kk) >> 4), acc);
+                        }
+                    }
+                }
+                mma_commit_pair(empty + st);
+            }
+            __syncwarp();
+        }
+        if (elect_one()) mma_commit_pair(done);
+        __syncwarp();
+    } else if (warp == 2 && rank == 1) { // relay: this CTA's stage landed -> rank 0
+        for (int ch = 0; ch < nch; ++ch) {
+            const int st = ch % G::kStages;
+            ptx::mbar_wait(full + st, static_cast<uint32_t>((ch / G::kStages) & 1));
+            if (elect_one()) mbar_arrive_remote(peer_full + st, 0);
+            __syncwarp();
+        }
+    }
+
+    ptx::mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    store_tile<G::kLevels, NT>(tmem, mt * TM, nt, warp, lane, M, N, ea, eb, out, ld_out, col_map, fold_add, ld_add);
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    cluster_sync(); // no peer traffic into this CTA is still pending
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+}
+
+template <int S, int NT>
+cudaError_t launch_gemm2(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M, int N,
+                         int nch, double* out, std::size_t ld_out, const int* col_map, const double* fold_add,
+                         std::size_t ld_add, cudaStream_t stream) {
+    using G = Geo2<S, NT>;
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(ozaki_gemm2_kernel<S, NT>), G::kSmem);
+    if (e != cudaSuccess) return e;
+    const std::size_t gm = (M + 2 * TM - 1) / (2 * TM) * 2; // whole CTA pairs (A rows padded to 256)
+    if (gm >= (1ull << 31)) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(gm), static_cast<unsigned>((N + NT - 1) / NT));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = G::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, ozaki_gemm2_kernel<S, NT>, a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map,
+                              fold_add, ld_add);
 }
 
 template <int S, int NT>
@@ -349,6 +590,10 @@ cudaError_t launch_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, c
                         std::size_t ld_add, cudaStream_t stream) {
     using G = Geo<S, NT>;
     cudaError_t e = smem_optin(reinterpret_cast<const void*>(ozaki_gemm_kernel<S, NT>), G::kSmem);
+    static const int debug = [] { // development knob (timing only): 1 = no loads after the first ring, 2 = no MMAs
+        const char* v = std::getenv("DCTP_OZAKI_DEBUG");
+        return v ? std::atoi(v) : 0;
+    }();
     if (e != cudaSuccess) return e;
     const std::size_t gm = (M + TM - 1) / TM;
     const unsigned gn = static_cast<unsigned>((N + NT - 1) / NT);
@@ -356,7 +601,7 @@ cudaError_t launch_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, c
         const unsigned gx = static_cast<unsigned>(gm - m0 < 65535 ? gm - m0 : 65535);
         ozaki_gemm_kernel<S, NT><<<dim3(gx, gn), kThreads, G::kSmem, stream>>>(
             a_sl + m0 * nch * G::kABytes, ea + m0 * TM, b_sl, eb, M - m0 * TM, N, nch, out + m0 * TM * ld_out,
-            ld_out, col_map, fold_add ? fold_add + m0 * TM * ld_add : nullptr, ld_add);
+            ld_out, col_map, fold_add ? fold_add + m0 * TM * ld_add : nullptr, ld_add, debug);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
@@ -365,19 +610,32 @@ cudaError_t launch_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, c
 
 } // namespace
 
-int ozaki_tile_n(int slices) { return slices <= 5 ? 96 : 80; }
+/// CTA-pair kernel (default; DCTP_OZAKI_PAIR=0: the single-CTA kernel).
+static bool pair_mode() {
+    static const bool on = [] {
+        const char* e = std::getenv("DCTP_OZAKI_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
-std::size_t ozaki_slice_bytes(std::size_t rows, int K, int tile_rows, int slices) {
-    const std::size_t tiles = (rows + tile_rows - 1) / tile_rows;
+int ozaki_pad_n(int slices) { return slices <= 5 ? 96 : 80; }
+int ozaki_tile_n(int slices) { return pair_mode() ? ozaki_pad_n(slices) / 2 : ozaki_pad_n(slices); }
+int ozaki_pad_m() { return pair_mode() ? 2 * TM : TM; }
+
+std::size_t ozaki_slice_bytes(std::size_t rows, int K, int tile_rows, int slices, int pad_rows) {
+    const std::size_t pad = static_cast<std::size_t>(pad_rows > tile_rows ? pad_rows : tile_rows);
+    const std::size_t tiles = (rows + pad - 1) / pad * pad / tile_rows;
     const std::size_t nch = (static_cast<std::size_t>(K) + CB - 1) / CB;
     return tiles * tile_rows * nch * CB * slices;
 }
 
 template <class T>
 cudaError_t ozaki_slice(const T* in, std::size_t ld, std::size_t rows, int K, const int* a_map, int tile_rows,
-                        int slices, int8_t* sl, int* expo, int* flag, cudaStream_t stream) {
+                        int slices, int8_t* sl, int* expo, int* flag, cudaStream_t stream, int pad_rows) {
     if (rows == 0) return cudaSuccess;
-    const std::size_t rows_pad = (rows + tile_rows - 1) / tile_rows * tile_rows;
+    const std::size_t pad = static_cast<std::size_t>(pad_rows > tile_rows ? pad_rows : tile_rows);
+    const std::size_t rows_pad = (rows + pad - 1) / pad * pad;
     const int nch = (K + CB - 1) / CB;
     const int vec = !a_map && reinterpret_cast<std::uintptr_t>(in) % 16 == 0 && (ld * sizeof(T)) % 16 == 0;
     if (rows_pad >= (1ull << 31)) return cudaErrorInvalidValue; // one CTA per (padded) row
@@ -386,15 +644,22 @@ cudaError_t ozaki_slice(const T* in, std::size_t ld, std::size_t rows, int K, co
     return cudaGetLastError();
 }
 template cudaError_t ozaki_slice<double>(const double*, std::size_t, std::size_t, int, const int*, int, int, int8_t*,
-                                         int*, int*, cudaStream_t);
+                                         int*, int*, cudaStream_t, int);
 template cudaError_t ozaki_slice<float>(const float*, std::size_t, std::size_t, int, const int*, int, int, int8_t*,
-                                        int*, int*, cudaStream_t);
+                                        int*, int*, cudaStream_t, int);
 
 cudaError_t ozaki_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M, int N,
                        int K, int slices, double* out, std::size_t ld_out, const int* col_map, cudaStream_t stream,
                        const double* fold_add, std::size_t ld_add) {
     if (M == 0 || N == 0) return cudaSuccess;
     const int nch = (K + CB - 1) / CB;
+    if (pair_mode()) {
+        if (slices == 5)
+            return launch_gemm2<5, 96>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add, stream);
+        if (slices == 6)
+            return launch_gemm2<6, 80>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add, stream);
+        return cudaErrorInvalidValue;
+    }
     if (slices == 5)
         return launch_gemm<5, 96>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add, stream);
     if (slices == 6)

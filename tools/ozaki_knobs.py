@@ -1,0 +1,33 @@
+"""Development probe: C5's int8 (Ozaki) product time under environment knobs,
+one subprocess per setting.  Usage: python tools/ozaki_knobs.py 'A=1 B=2' ''"""
+import json
+import os
+import subprocess
+import sys
+
+CHILD = r'''
+import os, sys, json, torch
+sys.path.insert(0, os.getcwd())
+import paper_2409_08970_b200 as P
+from paper_2409_08970_b200.configs import WORKLOADS, make_plan
+cfg = WORKLOADS[int(os.environ.get("CID", "5"))]
+plan = make_plan(cfg)
+x = torch.as_tensor(P.fill_signals(cfg.seed, cfg.dist, cfg.n, cfg.batch, cfg.r), device="cuda")
+out = torch.empty_like(x)
+fn = plan.forward
+for _ in range(3):
+    fn(x, sync=False, out=out)
+torch.cuda.synchronize()
+P.profile_reset(); P.profile_enable(True)
+for _ in range(10):
+    fn(x, sync=False, out=out)
+torch.cuda.synchronize(); P.profile_enable(False)
+print(json.dumps({k: round(v[1] / v[0], 4) for k, v in P.profile_summary().items()}))
+'''
+for setting in sys.argv[1:]:
+    env = dict(os.environ)
+    for kv in setting.split():
+        k, v = kv.split("=")
+        env[k] = v
+    r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
+    print(repr(setting), r.stdout.strip() or r.stderr[-2000:], flush=True)

@@ -1100,7 +1100,14 @@ static bool fold_route(const dctp_plan* p) {
 
 // int8 tensor-core (Ozaki) products, defined with the dense routes below
 static int ozaki_slices(std::size_t n);
-constexpr int kOzakiFoldMinK = 2048; // shortest product length the folded route sends to them
+// shortest product length the folded route sends to them (DCTP_OZAKI_FOLD_MIN_K)
+static int ozaki_fold_min_k() {
+    static const int v = [] {
+        const char* e = std::getenv("DCTP_OZAKI_FOLD_MIN_K");
+        return e ? std::atoi(e) : 2048;
+    }();
+    return v;
+}
 static void ensure_fold_ozaki(const dctp_plan* p, int which, int S, cudaStream_t s);
 static void rows_by_ozaki(const double* in, std::size_t ld_in, const int8_t* b_sl, const int* eb, int K, int N,
                           int S, double* out, std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t s,
@@ -1175,7 +1182,7 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
         if constexpr (!f32) {
             // the int8 products pay only for long rows (C3's 512-wide u: 0.28 vs
             // 0.30 ms forward, 0.43 vs 0.37 ms inverse with the slicing pass)
-            if (const int S = f.L >= kOzakiFoldMinK ? ozaki_slices(n) : 0) {
+            if (const int S = f.L >= ozaki_fold_min_k() ? ozaki_slices(n) : 0) {
                 ensure_fold_ozaki(p, 0, S, s);
                 rows_by_ozaki(u.ptr, f.L, f.oz[0], f.oz_e[0], f.L, f.cols, S, out, n, batch, p->flags(s), s, "fold_w_i8",
                               at<int>(p->blob, f.map));
@@ -1253,7 +1260,7 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
             }
         }
         if constexpr (!f32) {
-            if (const int S = f.cols >= kOzakiFoldMinK ? ozaki_slices(n) : 0) {
+            if (const int S = f.cols >= ozaki_fold_min_k() ? ozaki_slices(n) : 0) {
                 ensure_fold_ozaki(p, 1, S, s);
                 rows_by_ozaki(in, n, f.oz[1], f.oz_e[1], f.cols, f.L, S, out, n, batch, p->flags(s), s, "fold_wt_i8",
                               nullptr, at<int>(p->blob, f.map), w.ptr, f.L);
@@ -1686,6 +1693,8 @@ struct dctp_ensemble {
     std::size_t gmat32 = 0;
     std::size_t gt_hi = 0, gt_lo = 0; // G^T split for the tcgen05 3xTF32 GEMM, (K+1) n x n
     std::size_t gt_sw = 0;            // the same, in the kernel's swizzled shared-memory blocks
+    std::size_t gt_bf = 0;            // G^T split bf16 hi / lo for the persistent bf16x3 GEMM (tc_bf16x3.cu)
+    int num_sms = 0;
     bool dense32 = false;
     // pruned mode (c_p < n): [UL_r; HL_r] = T_r[:, 0:c_p] per member, K x n x c_p
     std::size_t prune64 = 0, prune32 = 0;
@@ -1742,8 +1751,20 @@ static void ensemble_forward_full(const dctp_ensemble* e, const T* in, T* out, s
         tw = twiddles_at<double>(e->blob, e->tw64);
     }
     if constexpr (f32) {
-        // the tensor-core GEMM (tcgen05 kind::tf32, 3xTF32) unless DCTP_TC32=0
+        // the persistent bf16x3 tensor-core GEMM (n <= 128), else the tcgen05
+        // 3xTF32 GEMM, unless DCTP_TC32=0 (FFMA SGEMM) / DCTP_TC_BF16=0
         const char* tc = std::getenv("DCTP_TC32");
+        const char* bfe = std::getenv("DCTP_TC_BF16");
+        if (e->dense32 && !(tc && tc[0] == '0') && !(bfe && bfe[0] == '0') &&
+            dctp::dev::tc_bf16x3_supported(static_cast<int>(n), static_cast<int>(ld), ld, out) &&
+            reinterpret_cast<std::uintptr_t>(in) % 16 == 0) {
+            cuda_check(DCTP_LAUNCH("progressive_bf16x3", s,
+                                   dctp::dev::tc_bf16x3(in, static_cast<int>(n), at<uint16_t>(e->blob, e->gt_bf), out,
+                                                        ld, batch, static_cast<int>(ld), static_cast<int>(n),
+                                                        e->flags(s), e->num_sms, s)),
+                       "progressive bf16x3 kernel");
+            return;
+        }
         if (e->dense32 && !(tc && tc[0] == '0') &&
             dctp::dev::tc_sgemm3_supported(static_cast<int>(n), static_cast<int>(ld), static_cast<int>(n),
                                            static_cast<int>(n), ld, in, at<float>(e->blob, e->gt_hi),
@@ -2104,6 +2125,13 @@ int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is,
             e->gt_lo = blob.add(bt_lo);
             e->gt_sw = blob.add(dctp::dev::tc_swizzle_b(bt_hi.data(), bt_lo.data(), static_cast<int>(cols),
                                                         static_cast<int>(n), static_cast<int>(n)));
+            {
+                std::vector<double> btd(cols * n);
+                for (std::size_t i = 0; i < n; ++i)
+                    for (std::size_t c = 0; c < cols; ++c) btd[c * n + i] = gd[i * cols + c];
+                e->gt_bf = blob.add(dctp::dev::tc_bf16x3_swizzle_b(btd.data(), static_cast<int>(cols),
+                                                                   static_cast<int>(n), static_cast<int>(n)));
+            }
             e->dense32 = true;
         }
         if (device < 0) {
@@ -2126,6 +2154,7 @@ int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is,
                        "cudaMemcpy(stages)");
         }
         e->flags.device = e->device;
+        cuda_check(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
         *out = e.release();
     });
 }

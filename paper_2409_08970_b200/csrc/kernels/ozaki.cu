@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, const int8_t* __restrict__ b_sl,
                    const int* __restrict__ eb, std::size_t M, int N, int nch, double* __restrict__ out,
                    std::size_t ld_out, const int* __restrict__ col_map, const double* __restrict__ fold_add,
-                   std::size_t ld_add) {
+                   std::size_t ld_add, int ntn, int nfast) {
     using G = Geo2<S, NT>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t raw = ptx::smem_addr(smem_raw);
@@ -470,8 +470,20 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     uint32_t rank = 0;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-    const std::size_t mt = blockIdx.x; // this CTA's 128-row tile (pairs: 2 p, 2 p + 1)
-    const int nt = blockIdx.y;
+    // this CTA's 128-row tile (pairs: 2 p, 2 p + 1) and column tile.  nfast:
+    // consecutive clusters walk the column tiles of one row pair (the B
+    // operand stays in L2 and A streams once: short-K products such as the
+    // chain); otherwise row pairs fastest (B, the larger operand, streams once)
+    std::size_t mt;
+    int nt;
+    if (nfast) {
+        const std::size_t ci = blockIdx.x >> 1;
+        nt = static_cast<int>(ci % static_cast<std::size_t>(ntn));
+        mt = 2 * (ci / static_cast<std::size_t>(ntn)) + rank;
+    } else {
+        mt = blockIdx.x;
+        nt = blockIdx.y;
+    }
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
@@ -567,9 +579,19 @@ cudaError_t launch_gemm2(const int8_t* a_sl, const int* ea, const int8_t* b_sl, 
     cudaError_t e = smem_optin(reinterpret_cast<const void*>(ozaki_gemm2_kernel<S, NT>), G::kSmem);
     if (e != cudaSuccess) return e;
     const std::size_t gm = (M + 2 * TM - 1) / (2 * TM) * 2; // whole CTA pairs (A rows padded to 256)
-    if (gm >= (1ull << 31)) return cudaErrorInvalidValue;
+    const int ntn = (N + NT - 1) / NT;
+    // tile order: the operand that is re-read per tile of the other should be
+    // the one that fits in L2 — walk column tiles first when B is the smaller
+    const std::size_t a_bytes = gm * TM * static_cast<std::size_t>(nch) * CB * S;
+    const std::size_t b_bytes = static_cast<std::size_t>(ntn) * NT * nch * CB * S;
+    static const int order = [] { // DCTP_OZAKI_ORDER: 0 = rows fastest, 1 = columns fastest, else automatic
+        const char* v = std::getenv("DCTP_OZAKI_ORDER");
+        return v ? std::atoi(v) : -1;
+    }();
+    const int nfast = order == 0 ? 0 : order == 1 ? 1 : (b_bytes < a_bytes ? 1 : 0);
+    if (gm * ntn >= (1ull << 31)) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(gm), static_cast<unsigned>((N + NT - 1) / NT));
+    cfg.gridDim = nfast ? dim3(static_cast<unsigned>(gm * ntn), 1) : dim3(static_cast<unsigned>(gm), ntn);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = G::kSmem;
     cfg.stream = stream;
@@ -581,7 +603,7 @@ cudaError_t launch_gemm2(const int8_t* a_sl, const int* ea, const int8_t* b_sl, 
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, ozaki_gemm2_kernel<S, NT>, a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map,
-                              fold_add, ld_add);
+                              fold_add, ld_add, ntn, nfast);
 }
 
 template <int S, int NT>

@@ -323,21 +323,24 @@ def test_misaligned_device_views_take_the_generic_route(P, torch, restatement):
     assert O.parity(out_big[1:].view(33, cfg.n).cpu().numpy(), ref) <= TOL64
 
 
-@pytest.mark.parametrize("tc32", ["1", "0"])
-def test_progressive_fp32_dense_route_edges(P, torch, restatement, monkeypatch, tc32):
+@pytest.mark.parametrize("mode,kernel", [("bf16x3", "progressive_bf16x3"), ("tc32", "progressive_tc32"),
+                                         ("sgemm", "progressive_sgemm")])
+def test_progressive_fp32_dense_route_edges(P, torch, restatement, monkeypatch, mode, kernel):
     """The fp32 progressive dense route (x * [D^T | X_1..X_K]) — on the
-    tcgen05 3xTF32 GEMM, or with DCTP_TC32=0 the FFMA SGEMM — on ragged
-    batches (not multiples of the 128-row tile), against the fp64 generic
-    route; a misaligned output view falls back to the DCT + Cauchy kernels
-    with the same answer; a non-finite sample raises DomainError."""
-    monkeypatch.setenv("DCTP_TC32", tc32)
+    persistent bf16x3 tcgen05 GEMM (default), the tcgen05 3xTF32 GEMM
+    (DCTP_TC_BF16=0) or the FFMA SGEMM (DCTP_TC32=0) — on ragged batches (not
+    multiples of the 128-row tile), against the fp64 generic route; a
+    misaligned output view falls back to the DCT + Cauchy kernels with the
+    same answer; a non-finite sample raises DomainError."""
+    monkeypatch.setenv("DCTP_TC32", "0" if mode == "sgemm" else "1")
+    monkeypatch.setenv("DCTP_TC_BF16", "1" if mode == "bf16x3" else "0")
     ens = plan_for(P, 4)
     cfg = O.config(4)
     P.profile_reset()
     P.profile_enable(True)
     ens.forward_all_batch(dev(torch, np.zeros((130, cfg.n)), torch.float32))
     P.profile_enable(False)
-    assert set(P.profile_summary()) == {"progressive_tc32" if tc32 == "1" else "progressive_sgemm"}
+    assert set(P.profile_summary()) == {kernel}
     for batch in (1, 129, 1000):
         s = restatement.fill_signals(O.mix_seed(O.SEED, cfg.n, batch), 0, cfg.n, batch)
         y32 = ens.forward_all_batch(dev(torch, s, torch.float32)).double().cpu().numpy()

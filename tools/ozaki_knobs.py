@@ -1,5 +1,5 @@
-"""Development probe: C5's int8 (Ozaki) product time under environment knobs,
-one subprocess per setting.  Usage: python tools/ozaki_knobs.py 'A=1 B=2' ''"""
+"""Development probe: a workload's kernel times (CID, default 5 = C5) under
+environment knobs, one subprocess per setting.  Usage: python tools/ozaki_knobs.py 'A=1 B=2' ''"""
 import json
 import os
 import subprocess
@@ -13,8 +13,13 @@ from paper_2409_08970_b200.configs import WORKLOADS, make_plan
 cfg = WORKLOADS[int(os.environ.get("CID", "5"))]
 plan = make_plan(cfg)
 x = torch.as_tensor(P.fill_signals(cfg.seed, cfg.dist, cfg.n, cfg.batch, cfg.r), device="cuda")
-out = torch.empty_like(x)
-fn = plan.forward
+if cfg.progressive:
+    x = x.float()
+    out = torch.empty((x.shape[0], 17, cfg.n), dtype=x.dtype, device=x.device)
+    fn = plan.forward_all_batch
+else:
+    out = torch.empty_like(x)
+    fn = plan.forward
 for _ in range(3):
     fn(x, sync=False, out=out)
 torch.cuda.synchronize()

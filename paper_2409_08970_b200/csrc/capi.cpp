@@ -382,6 +382,7 @@ struct dctp_plan {
         std::size_t w_hi = 0, w_lo = 0;          // fp32 forward on tcgen05: W split 3xTF32 (cols x L)
         std::size_t wt_hi = 0, wt_lo = 0;        // fp32 inverse on tcgen05: W^T split (L x ldwt)
         std::size_t w_sw = 0, wt_sw = 0;         // both, in the kernel's swizzled shared-memory blocks
+        std::size_t w_bf = 0, wt_bf = 0;         // fp32 on the persistent bf16x3 GEMM: W and W^T split bf16
         TwiddleOffsets tw64, tw32;
         // fp64 on the int8 tensor cores: slices of W [0] and W^T [1], built on first use
         int8_t* oz[2] = {nullptr, nullptr};
@@ -649,6 +650,10 @@ static void build_fold(dctp_plan& p, Blob& blob, const ApplyTables& t) {
         f.wt_sw = blob.add(dctp::dev::tc_swizzle_b(thi.data(), tlo.data(), static_cast<int>(L),
                                                    static_cast<int>(cols), static_cast<int>(ldt)));
     }
+    f.w_bf = blob.add(dctp::dev::tc_bf16x3_swizzle_b(w.data(), static_cast<int>(cols), static_cast<int>(L),
+                                                     static_cast<int>(ldw)));
+    f.wt_bf = blob.add(dctp::dev::tc_bf16x3_swizzle_b(wt.data(), static_cast<int>(L), static_cast<int>(cols),
+                                                      static_cast<int>(ldwt)));
     f.ldwt = ldwt;
     f.wt = blob.add(wt);
     f.wt32 = blob.add(to_f32(wt));
@@ -1160,6 +1165,16 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
             // fp32: the tcgen05 3xTF32 GEMM (DCTP_TC32=0: the FFMA2 SGEMM with W^T
             // rounded once, twice the DMMA rate)
             const char* tc = std::getenv("DCTP_TC32");
+            const char* bfe = std::getenv("DCTP_TC_BF16");
+            if (!(tc && tc[0] == '0') && !(bfe && bfe[0] == '0') &&
+                dctp::dev::tc_bf16x3_supported(f.L, f.cols, n, out)) {
+                cuda_check(DCTP_LAUNCH("fold_w_bf16x3", s,
+                                       dctp::dev::tc_bf16x3(u.ptr, f.L, at<uint16_t>(p->blob, f.w_bf), out, n, batch,
+                                                            f.cols, f.L, p->flags(s), p->num_sms, s,
+                                                            at<int>(p->blob, f.map))),
+                           "fold bf16x3 kernel");
+                return;
+            }
             const float* wh = at<float>(p->blob, f.w_hi);
             const float* wl = at<float>(p->blob, f.w_lo);
             if (!(tc && tc[0] == '0') && dctp::dev::tc_sgemm3_supported(f.L, f.cols, f.L, f.L, n, u.ptr, wh, wl, out)) {
@@ -1246,6 +1261,16 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
                    "fold idct kernel");
         if constexpr (f32) {
             const char* tc = std::getenv("DCTP_TC32");
+            const char* bfe = std::getenv("DCTP_TC_BF16");
+            if (!(tc && tc[0] == '0') && !(bfe && bfe[0] == '0') &&
+                dctp::dev::tc_bf16x3_supported(f.cols, f.L, n, out, true) && f.L % 4 == 0) {
+                cuda_check(DCTP_LAUNCH("fold_wt_bf16x3", s,
+                                       dctp::dev::tc_bf16x3(in, static_cast<int>(n), at<uint16_t>(p->blob, f.wt_bf), out,
+                                                            n, batch, f.L, f.cols, p->flags(s), p->num_sms, s, nullptr,
+                                                            at<int>(p->blob, f.map), w.ptr, f.L)),
+                           "fold bf16x3 kernel");
+                return;
+            }
             const float* th = at<float>(p->blob, f.wt_hi);
             const float* tl = at<float>(p->blob, f.wt_lo);
             const int ldt = (f.cols + 3) / 4 * 4;

@@ -238,14 +238,17 @@ cudaError_t tc_sgemm3(const float* A, int lda, const float* bt_hi, const float* 
 std::vector<float> tc_swizzle_b(const float* bt_hi, const float* bt_lo, int N, int K, int ldb);
 
 /// C[M x N] = A[M x K] B (fp32, row-major A and C) on the tcgen05 tensor cores
-/// with the bf16x3 split (tc_bf16x3.cu), K <= 128: a persistent kernel whose
-/// B^T column tile stays resident; b_sw from tc_bf16x3_swizzle_b (B^T given
-/// in fp64, N x K, row stride ldb).  Raises flag bit 0 if column 0 of a row
-/// is non-finite.
-bool tc_bf16x3_supported(int K, int N, std::size_t ldc, const void* C);
+/// with the bf16x3 split (tc_bf16x3.cu): a persistent kernel whose B^T
+/// column tile stays resident (K <= 128) or streams with A (larger K); b_sw
+/// from tc_bf16x3_swizzle_b (B^T given in fp64, N x K, row stride ldb).  A's
+/// columns optionally gathered through a_map; output plain, scattered
+/// (col_map) or unfolded (fold_add, as in rows_by_basis; N % 4 == 0).  Raises
+/// flag bit 0 if column 0 of a row is non-finite.
+bool tc_bf16x3_supported(int K, int N, std::size_t ldc, const void* C, bool fold = false);
 std::vector<uint16_t> tc_bf16x3_swizzle_b(const double* bt, int N, int K, int ldb);
 cudaError_t tc_bf16x3(const float* A, int lda, const uint16_t* b_sw, float* C, std::size_t ldc, std::size_t M, int N,
-                      int K, int* flag, int num_sms, cudaStream_t stream);
+                      int K, int* flag, int num_sms, cudaStream_t stream, const int* col_map = nullptr,
+                      const int* a_map = nullptr, const float* fold_add = nullptr, std::size_t ld_add = 0);
 
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);

@@ -101,11 +101,13 @@ __device__ __forceinline__ uint32_t bf16_bits(float x) {
     return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(x)));
 }
 
-/// A split: rows of fp32 (stride lda) -> bf16 hi / lo in the kernel's chunk
+/// A split: rows of fp32 (stride lda; columns gathered through a_map if
+/// given) -> bf16 hi / lo in the kernel's chunk
 /// image [row tile][chunk][hi | lo][128 rows x 64 B, SW64]; one thread per
 /// 8 consecutive k (one 16-byte unit of each half).
 __global__ void __launch_bounds__(256) bf16x3_split_kernel(const float* __restrict__ a, int lda, std::size_t M,
                                                            std::size_t rows_pad, int K, int nch,
+                                                           const int* __restrict__ a_map,
                                                            unsigned char* __restrict__ a_sw) {
     const std::size_t i = static_cast<std::size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int units = nch * (KC / 8);
@@ -113,13 +115,14 @@ __global__ void __launch_bounds__(256) bf16x3_split_kernel(const float* __restri
     const std::size_t r = i / units;
     const int u = static_cast<int>(i % units), k0 = 8 * u;
     float v[8];
-    if (r < M && k0 + 8 <= K && (lda & 3) == 0) {
+    if (!a_map && r < M && k0 + 8 <= K && (lda & 3) == 0) {
         const float4 p = __ldg(reinterpret_cast<const float4*>(a + r * lda + k0));
         const float4 q = __ldg(reinterpret_cast<const float4*>(a + r * lda + k0 + 4));
         v[0] = p.x, v[1] = p.y, v[2] = p.z, v[3] = p.w, v[4] = q.x, v[5] = q.y, v[6] = q.z, v[7] = q.w;
     } else {
 #pragma unroll
-        for (int t = 0; t < 8; ++t) v[t] = (r < M && k0 + t < K) ? a[r * lda + k0 + t] : 0.f;
+        for (int t = 0; t < 8; ++t)
+            v[t] = (r < M && k0 + t < K) ? a[r * lda + (a_map ? __ldg(a_map + k0 + t) : k0 + t)] : 0.f;
     }
     uint32_t hi[4], lo[4];
 #pragma unroll
@@ -145,22 +148,47 @@ struct Sched {
     }
 };
 
+/// Output of one tile: plain rows (C[r, c]), scattered columns (C[r,
+/// col_map[c]]), or unfolded (C[r, c] = w + v, C[r, 2N - 1 - c] = w - v with
+/// w = fold_add[r, c], the folded inverse of antisymmetric plans).
+struct Epi {
+    float* C;
+    std::size_t ldc;
+    const int* col_map;
+    const float* fold_add;
+    std::size_t ld_add;
+};
+
+/// STREAM = false: K <= 128, the B^T column tile resident (one load per
+/// column tile).  STREAM = true: any K, A and B chunks stream together
+/// through a 4-stage ring (48 KB per stage).
+template <bool STREAM>
+struct Lay {
+    static constexpr int kStages = STREAM ? 4 : kAStages;
+    static constexpr int kStage = STREAM ? kAChunk + kBChunk : kAChunk;
+    static constexpr int kResident = STREAM ? 0 : kBBytes;
+    static constexpr int kSmem = kResident + kStages * kStage + kStaging + 1024 + 256;
+    static_assert(kSmem <= 227 * 1024, "tc_bf16x3: shared memory");
+};
+
+template <bool STREAM, int MODE> // MODE 0: plain rows, 1: col_map, 2: fold_add
 __global__ void __launch_bounds__(kThreads, 1)
-tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __restrict__ b_sw, float* __restrict__ C,
-                 std::size_t ldc, std::size_t M, int N, int nch, unsigned ntm, unsigned ntn, int* flag) {
+tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __restrict__ b_sw, Epi ep,
+                 std::size_t M, int N, int nch, unsigned ntm, unsigned ntn, int* flag) {
+    using Ly = Lay<STREAM>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t raw = ptx::smem_addr(smem_raw);
     unsigned char* base = smem_raw + ((1024 - (raw & 1023)) & 1023);
-    unsigned char* bsm = base;                              // resident B^T column tile
-    unsigned char* asm_ = base + kBBytes;                   // A ring
-    unsigned char* stg = asm_ + kAStages * kAChunk;         // epilogue transposes
+    unsigned char* bsm = base;                                // resident B^T column tile (!STREAM)
+    unsigned char* ring = base + Ly::kResident;               // stages: A chunk (+ B chunk when STREAM)
+    unsigned char* stg = ring + Ly::kStages * Ly::kStage;     // epilogue transposes
     uint64_t* bar = reinterpret_cast<uint64_t*>(stg + kStaging);
-    uint64_t* a_full = bar;                   // kAStages
-    uint64_t* a_empty = a_full + kAStages;    // kAStages
-    uint64_t* b_full = a_empty + kAStages;    // 1
-    uint64_t* b_empty = b_full + 1;           // 1
-    uint64_t* t_full = b_empty + 1;           // 2: accumulator ready
-    uint64_t* t_empty = t_full + 2;           // 2: accumulator drained
+    uint64_t* s_full = bar;                       // kStages
+    uint64_t* s_empty = s_full + Ly::kStages;     // kStages
+    uint64_t* b_full = s_empty + Ly::kStages;     // 1
+    uint64_t* b_empty = b_full + 1;               // 1
+    uint64_t* t_full = b_empty + 1;               // 2: accumulator ready
+    uint64_t* t_empty = t_full + 2;               // 2: accumulator drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -174,9 +202,9 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     if (threadIdx.x == 32) {
-        for (int i = 0; i < kAStages; ++i) {
-            ptx::mbar_init(a_full + i, 1);
-            ptx::mbar_init(a_empty + i, 1);
+        for (int i = 0; i < Ly::kStages; ++i) {
+            ptx::mbar_init(s_full + i, 1);
+            ptx::mbar_init(s_empty + i, 1);
         }
         ptx::mbar_init(b_full, 1);
         ptx::mbar_init(b_empty, 1);
@@ -197,7 +225,7 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
         for (unsigned long long t = sc.first; t < sc.last; ++t) {
             unsigned mt, nt;
             sc.tile(t, mt, nt);
-            if (nt != cur_nt) { // (re)load the resident B^T block once its readers are done
+            if (!STREAM && nt != cur_nt) { // (re)load the resident B^T block once its readers are done
                 if (b_loads > 0) ptx::mbar_wait(b_empty, (b_loads - 1) & 1u);
                 if (elect_one()) {
                     ptx::mbar_expect_tx(b_full, static_cast<uint32_t>(nch * kBChunk));
@@ -210,26 +238,30 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
                 ++b_loads;
             }
             for (int c = 0; c < nch; ++c, ++chunk) {
-                const int st = static_cast<int>(chunk % kAStages);
-                const uint32_t ph = static_cast<uint32_t>((chunk / kAStages) & 1);
-                ptx::mbar_wait(a_empty + st, ph ^ 1u);
+                const int st = static_cast<int>(chunk % Ly::kStages);
+                const uint32_t ph = static_cast<uint32_t>((chunk / Ly::kStages) & 1);
+                ptx::mbar_wait(s_empty + st, ph ^ 1u);
                 if (elect_one()) {
-                    ptx::mbar_expect_tx(a_full + st, kAChunk);
-                    ptx::bulk_load(asm_ + st * kAChunk, a_sw + (static_cast<std::size_t>(mt) * nch + c) * kAChunk,
-                                   kAChunk, a_full + st);
+                    ptx::mbar_expect_tx(s_full + st, Ly::kStage);
+                    unsigned char* dst = ring + st * Ly::kStage;
+                    ptx::bulk_load(dst, a_sw + (static_cast<std::size_t>(mt) * nch + c) * kAChunk, kAChunk,
+                                   s_full + st);
+                    if (STREAM)
+                        ptx::bulk_load(dst + kAChunk, b_sw + (static_cast<std::size_t>(nt) * nch + c) * kBChunk,
+                                       kBChunk, s_full + st);
                 }
                 __syncwarp();
             }
         }
     } else if (warp == 1) { // MMA issuer
-        const uint64_t adesc0 = smem_desc(ptx::smem_addr(asm_)), bdesc0 = smem_desc(ptx::smem_addr(bsm));
+        const uint64_t rdesc0 = smem_desc(ptx::smem_addr(ring)), bdesc0 = smem_desc(ptx::smem_addr(bsm));
         unsigned cur_nt = ~0u, b_loads = 0;
         unsigned long long chunk = 0;
         int i = 0;
         for (unsigned long long t = sc.first; t < sc.last; ++t, ++i) {
             unsigned mt, nt;
             sc.tile(t, mt, nt);
-            if (nt != cur_nt) {
+            if (!STREAM && nt != cur_nt) {
                 ptx::mbar_wait(b_full, b_loads & 1u);
                 cur_nt = nt;
                 ++b_loads;
@@ -239,13 +271,14 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             const uint32_t td = tmem + static_cast<uint32_t>(buf * BN);
             for (int c = 0; c < nch; ++c, ++chunk) {
-                const int st = static_cast<int>(chunk % kAStages);
-                ptx::mbar_wait(a_full + st, static_cast<uint32_t>((chunk / kAStages) & 1));
+                const int st = static_cast<int>(chunk % Ly::kStages);
+                ptx::mbar_wait(s_full + st, static_cast<uint32_t>((chunk / Ly::kStages) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                 if (elect_one()) {
-                    const uint64_t ah = adesc0 + (static_cast<uint64_t>(st * kAChunk) >> 4);
+                    const uint64_t ah = rdesc0 + (static_cast<uint64_t>(st * Ly::kStage) >> 4);
                     const uint64_t al = ah + (kAHalf >> 4);
-                    const uint64_t bh = bdesc0 + (static_cast<uint64_t>(c * kBChunk) >> 4);
+                    const uint64_t bh = STREAM ? ah + (kAChunk >> 4)
+                                               : bdesc0 + (static_cast<uint64_t>(c * kBChunk) >> 4);
                     const uint64_t bl = bh + (kBHalf >> 4);
 #pragma unroll
                     for (int kk = 0; kk < KC / 16; ++kk) { // 16 bf16 = 32 bytes per MMA K step
@@ -254,16 +287,17 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
                         mma_bf16(td, ah + o, bl + o, 1u);
                         mma_bf16(td, al + o, bh + o, 1u);
                     }
-                    mma_commit(a_empty + st);
+                    mma_commit(s_empty + st);
                 }
                 __syncwarp();
             }
             if (elect_one()) {
                 mma_commit(t_full + buf);
-                // the last tile of this column tile: B may be replaced once these MMAs are done
-                unsigned mt2 = 0, nt2 = ~0u;
-                if (t + 1 < sc.last) sc.tile(t + 1, mt2, nt2);
-                if (nt2 != nt) mma_commit(b_empty);
+                if (!STREAM) { // the last tile of this column tile: B may be replaced once these MMAs are done
+                    unsigned mt2 = 0, nt2 = ~0u;
+                    if (t + 1 < sc.last) sc.tile(t + 1, mt2, nt2);
+                    if (nt2 != nt) mma_commit(b_empty);
+                }
             }
             __syncwarp();
         }
@@ -282,10 +316,11 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
 #pragma unroll 1
             for (int cc = 0; cc < BN / 2; cc += 32) {
                 const int c0 = h * (BN / 2) + cc, col0 = static_cast<int>(nt) * BN + c0;
+                if (col0 >= N) break;
                 uint32_t v[32];
                 tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(buf * BN + c0), v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                if (col0 == 0 && row0 + lane < M) bad |= !isfinite(__uint_as_float(v[0])); // the DC coefficient
+                if (col0 == 0 && row0 + lane < M) bad |= !isfinite(__uint_as_float(v[0])); // column 0
 #pragma unroll
                 for (int g = 0; g < 8; ++g)
                     *reinterpret_cast<uint4*>(tb + lane * 128 + ((g ^ (lane & 7)) << 4)) =
@@ -297,15 +332,25 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
                     const uint4 w = *reinterpret_cast<const uint4*>(tb + r * 128 + ((g ^ (r & 7)) << 4));
                     const std::size_t grow = row0 + r;
                     const int col = col0 + 4 * g;
-                    if (grow < M) {
-                        float* dst = C + grow * ldc + col;
+                    if (grow >= M || col >= N) continue;
+                    const float e4[4] = {__uint_as_float(w.x), __uint_as_float(w.y), __uint_as_float(w.z),
+                                         __uint_as_float(w.w)};
+                    float* orow = ep.C + grow * ep.ldc;
+                    if constexpr (MODE == 2) { // N % 4 == 0 on this path
+                        const float4 a4 = __ldg(reinterpret_cast<const float4*>(ep.fold_add + grow * ep.ld_add + col));
+                        __stcs(reinterpret_cast<float4*>(orow + col),
+                               make_float4(a4.x + e4[0], a4.y + e4[1], a4.z + e4[2], a4.w + e4[3]));
+                        __stcs(reinterpret_cast<float4*>(orow + 2 * N - 4 - col),
+                               make_float4(a4.w - e4[3], a4.z - e4[2], a4.y - e4[1], a4.x - e4[0]));
+                    } else if constexpr (MODE == 1) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (col + u < N) orow[__ldg(ep.col_map + col + u)] = e4[u];
+                    } else {
                         if (col + 4 <= N) {
-                            __stcs(reinterpret_cast<float4*>(dst),
-                                   make_float4(__uint_as_float(w.x), __uint_as_float(w.y), __uint_as_float(w.z),
-                                               __uint_as_float(w.w)));
+                            __stcs(reinterpret_cast<float4*>(orow + col), make_float4(e4[0], e4[1], e4[2], e4[3]));
                         } else {
-                            const uint32_t e[4] = {w.x, w.y, w.z, w.w};
-                            for (int u = 0; u < 4 && col + u < N; ++u) dst[u] = __uint_as_float(e[u]);
+                            for (int u = 0; u < 4 && col + u < N; ++u) orow[col + u] = e4[u];
                         }
                     }
                 }
@@ -325,13 +370,8 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
 
 } // namespace
 
-bool tc_bf16x3_supported(int K, int N, std::size_t ldc, const void* C) {
-    return K > 0 && K <= kMaxK && N > 0 && ldc % 4 == 0 && reinterpret_cast<std::uintptr_t>(C) % 16 == 0;
-}
-
-std::size_t tc_bf16x3_a_bytes(std::size_t M, int K) {
-    const std::size_t tiles = (M + BM - 1) / BM;
-    return tiles * ((K + KC - 1) / KC) * static_cast<std::size_t>(kAChunk);
+bool tc_bf16x3_supported(int K, int N, std::size_t ldc, const void* C, bool fold) {
+    return K > 0 && N > 0 && ldc % 4 == 0 && reinterpret_cast<std::uintptr_t>(C) % 16 == 0 && (!fold || N % 4 == 0);
 }
 
 std::vector<uint16_t> tc_bf16x3_swizzle_b(const double* bt, int N, int K, int ldb) {
@@ -368,28 +408,42 @@ std::vector<uint16_t> tc_bf16x3_swizzle_b(const double* bt, int N, int K, int ld
 }
 
 cudaError_t tc_bf16x3(const float* A, int lda, const uint16_t* b_sw, float* C, std::size_t ldc, std::size_t M, int N,
-                      int K, int* flag, int num_sms, cudaStream_t stream) {
+                      int K, int* flag, int num_sms, cudaStream_t stream, const int* col_map, const int* a_map,
+                      const float* fold_add, std::size_t ld_add) {
     if (M == 0 || N == 0) return cudaSuccess;
-    if (K <= 0 || K > kMaxK) return cudaErrorInvalidValue;
+    if (K <= 0) return cudaErrorInvalidValue;
     const int nch = (K + KC - 1) / KC;
     const std::size_t ntm = (M + BM - 1) / BM;
     if (ntm >= (1ull << 32)) return cudaErrorInvalidValue;
     cudaError_t e = cudaSuccess;
     unsigned char* a_sw = nullptr;
-    e = cudaMallocAsync(reinterpret_cast<void**>(&a_sw), tc_bf16x3_a_bytes(M, K), stream);
+    e = cudaMallocAsync(reinterpret_cast<void**>(&a_sw), ntm * nch * static_cast<std::size_t>(kAChunk), stream);
     if (e != cudaSuccess) return e;
     const std::size_t rows_pad = ntm * BM, work = rows_pad * nch * (KC / 8);
     bf16x3_split_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(A, lda, M, rows_pad, K, nch,
-                                                                                      a_sw);
+                                                                                      a_map, a_sw);
     e = cudaGetLastError();
-    if (e == cudaSuccess) e = smem_optin(reinterpret_cast<const void*>(tc_bf16x3_kernel), kSmem);
     if (e == cudaSuccess) {
         const unsigned ntn = static_cast<unsigned>((N + BN - 1) / BN);
         const unsigned long long tiles = static_cast<unsigned long long>(ntm) * ntn;
         const unsigned grid = static_cast<unsigned>(tiles < static_cast<unsigned long long>(num_sms) ? tiles : num_sms);
-        tc_bf16x3_kernel<<<grid, kThreads, kSmem, stream>>>(a_sw, reinterpret_cast<const unsigned char*>(b_sw), C, ldc,
-                                                            M, N, nch, static_cast<unsigned>(ntm), ntn, flag);
-        e = cudaGetLastError();
+        const Epi ep{C, ldc, col_map, fold_add, ld_add};
+        const int mode = fold_add ? 2 : (col_map ? 1 : 0);
+        auto launch = [&](auto kern, int smem) {
+            cudaError_t r = smem_optin(reinterpret_cast<const void*>(kern), smem);
+            if (r != cudaSuccess) return r;
+            kern<<<grid, kThreads, smem, stream>>>(a_sw, reinterpret_cast<const unsigned char*>(b_sw), ep, M, N, nch,
+                                                   static_cast<unsigned>(ntm), ntn, flag);
+            return cudaGetLastError();
+        };
+        if (K > kMaxK)
+            e = mode == 2 ? launch(tc_bf16x3_kernel<true, 2>, Lay<true>::kSmem)
+                : mode == 1 ? launch(tc_bf16x3_kernel<true, 1>, Lay<true>::kSmem)
+                            : launch(tc_bf16x3_kernel<true, 0>, Lay<true>::kSmem);
+        else
+            e = mode == 2 ? launch(tc_bf16x3_kernel<false, 2>, Lay<false>::kSmem)
+                : mode == 1 ? launch(tc_bf16x3_kernel<false, 1>, Lay<false>::kSmem)
+                            : launch(tc_bf16x3_kernel<false, 0>, Lay<false>::kSmem);
     }
     cudaFreeAsync(a_sw, stream);
     return e;

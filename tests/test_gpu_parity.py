@@ -751,12 +751,14 @@ def test_random_plans_all_routes_match_reference(P, torch, reference, monkeypatc
     assert checked >= 30
 
 
-@pytest.mark.parametrize("tc32", ["1", "0"])
-def test_folded_fp32_products_tc32_and_sgemm(P, torch, reference, monkeypatch, tc32):
-    """C3 in fp32: the folded route's W products on the tcgen05 3xTF32 GEMM
-    (fold_w_tc32 / fold_wt_tc32) or, with DCTP_TC32=0, the FFMA SGEMM and
-    the widened DMMA product; forward and inverse against the reference."""
-    monkeypatch.setenv("DCTP_TC32", tc32)
+@pytest.mark.parametrize("mode", ["bf16x3", "tc32", "sgemm"])
+def test_folded_fp32_products_tc32_and_sgemm(P, torch, reference, monkeypatch, mode):
+    """C3 in fp32: the folded route's W products on the persistent bf16x3
+    tcgen05 GEMM (default: fold_w_bf16x3 / fold_wt_bf16x3, W streamed), the
+    tcgen05 3xTF32 GEMM (DCTP_TC_BF16=0) or, with DCTP_TC32=0, the FFMA SGEMM
+    and the widened DMMA product; forward and inverse against the reference."""
+    monkeypatch.setenv("DCTP_TC32", "0" if mode == "sgemm" else "1")
+    monkeypatch.setenv("DCTP_TC_BF16", "1" if mode == "bf16x3" else "0")
     g = load_golden("c3")
     plan = plan_for(P, 3)
     P.profile_reset()
@@ -765,9 +767,9 @@ def test_folded_fp32_products_tc32_and_sgemm(P, torch, reference, monkeypatch, t
     b = plan.inverse(dev(torch, g["forward"], torch.float32)).double().cpu().numpy()
     P.profile_enable(False)
     names = set(P.profile_summary())
-    if tc32 == "1":
-        assert {"fold_w_tc32", "fold_wt_tc32"} <= names
+    if mode == "sgemm":
+        assert not any("tc32" in k or "bf16" in k for k in names)
     else:
-        assert not any("tc32" in k for k in names)
+        assert {f"fold_w_{mode}", f"fold_wt_{mode}"} <= names
     assert O.parity(y, g["forward"]) <= TOL32
     assert O.parity(b, g["signals"]) <= TOL32

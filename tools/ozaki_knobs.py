@@ -18,8 +18,12 @@ if cfg.progressive:
     out = torch.empty((x.shape[0], 17, cfg.n), dtype=x.dtype, device=x.device)
     fn = plan.forward_all_batch
 else:
+    if os.environ.get("DTYPE") == "f32":
+        x = x.float()
+    if os.environ.get("OP") == "inv":
+        x = plan.forward(x)
     out = torch.empty_like(x)
-    fn = plan.forward
+    fn = plan.inverse if os.environ.get("OP") == "inv" else plan.forward
 for _ in range(3):
     fn(x, sync=False, out=out)
 torch.cuda.synchronize()

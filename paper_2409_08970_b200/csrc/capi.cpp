@@ -319,13 +319,25 @@ class Profiler {
 /// thread's call and nowhere else (the reference throws from the failing
 /// call, fast_transform.hpp:271-276; plans are shared across threads,
 /// :33-34).  Keyed by cudaStreamGetId, so cudaStreamPerThread and the legacy
-/// stream resolve to the calling thread's real stream.
+/// stream resolve to the calling thread's real stream.  Launches captured
+/// into a CUDA graph (where cudaStreamGetId is not permitted) raise the
+/// object's graph flag, which every sync_check of the object also reads.
 struct StreamFlags {
     int device = 0;
+    int* graph = nullptr;
     mutable std::mutex mu;
     mutable std::unordered_map<unsigned long long, int*> map;
 
+    void init(int dev) {
+        device = dev;
+        DeviceScope scope(device);
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&graph), sizeof(int)), "cudaMalloc(flag)");
+        cuda_check(cudaMemset(graph, 0, sizeof(int)), "cudaMemset(flag)");
+    }
     int* operator()(cudaStream_t s) const {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cuda_check(cudaStreamIsCapturing(s, &cs), "cudaStreamIsCapturing");
+        if (cs != cudaStreamCaptureStatusNone) return graph;
         unsigned long long id = 0;
         cuda_check(cudaStreamGetId(s, &id), "cudaStreamGetId");
         std::lock_guard<std::mutex> lock(mu);
@@ -343,6 +355,7 @@ struct StreamFlags {
         if (cudaGetDevice(&prev) != cudaSuccess) return;
         cudaSetDevice(device);
         for (auto& kv : map) cudaFree(kv.second);
+        if (graph) cudaFree(graph);
         cudaSetDevice(prev);
     }
 };
@@ -920,7 +933,7 @@ static void upload_plan(dctp_plan& p) {
     cuda_check(cudaMemcpy(static_cast<unsigned char*>(p.blob) + p.stage_desc, desc, sizeof(desc),
                           cudaMemcpyHostToDevice),
                "cudaMemcpy(stage descriptors)");
-    p.flags.device = p.device;
+    p.flags.init(p.device);
     cuda_check(cudaDeviceGetAttribute(&p.num_sms, cudaDevAttrMultiProcessorCount, p.device), "cudaDeviceGetAttribute");
 }
 
@@ -1096,6 +1109,24 @@ static void plan_dense(const dctp_plan* p, const T* in, T* out, std::size_t batc
 static bool dense_route(const dctp_plan* p);
 static void ensure_dense(const dctp_plan* p, cudaStream_t s);
 
+/// Small plans take the one-launch dense product (small_dense.cu) where it
+/// beats the fused persistent kernel (tools/small_sweep.py, GPU time per
+/// forward from CUDA-graph replay): n <= 64 at every batch (n = 64: 5.7 vs
+/// 14.6 us at 4096 signals, 32.5 vs 92.8 us at 65536), n = 128 up to
+/// DCTP_SMALL_DENSE_MAX rows (default 16384: 12.0 vs 20.7 us at 4096, even at
+/// 16384, 186 vs 142 us at 65536).  DCTP_SMALL_DENSE = 0 / 1 forces it off / on.
+static bool small_dense_route(const dctp_plan* p, std::size_t batch) {
+    const char* e = std::getenv("DCTP_SMALL_DENSE");
+    if (e && e[0] == '0') return false;
+    if (p->st.n > 128) return false;
+    if (e && e[0] == '1') return true;
+    static const std::size_t max_rows = [] {
+        const char* m = std::getenv("DCTP_SMALL_DENSE_MAX");
+        return m ? static_cast<std::size_t>(std::atoll(m)) : std::size_t{16384};
+    }();
+    return p->st.n <= 64 || batch <= max_rows;
+}
+
 /// DCTP_FOLD=0 turns the folded route off (structured DCT + Cauchy instead).
 static bool fold_route(const dctp_plan* p) {
     if (!p->fd.on) return false;
@@ -1133,6 +1164,17 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
         if (fast_route(p)) {
             cuda_check(DCTP_LAUNCH("nfst_fwd", s, dctp::dev::nfst_apply(in, out, batch, fast_plan_dev(p), p->flags(s), false, s)),
                        "nfst forward kernel");
+            return;
+        }
+        // small plans at small batches: one dense product with X^T staged in
+        // shared memory (the fused persistent kernel's per-CTA setup costs
+        // more than the whole transform there)
+        if (small_dense_route(p, batch) && dctp::dev::small_dense_supported(n, in, n, out, n)) {
+            ensure_dense(p, s);
+            const auto& d = *p->dense;
+            cuda_check(DCTP_LAUNCH("small_dense", s,
+                                   dctp::dev::small_dense_forward(in, n, d.buf, d.ld, out, n, n, batch, p->flags(s), s)),
+                       "small dense kernel");
             return;
         }
         // TMA bulk copies need 16-byte aligned rows; a misaligned view takes
@@ -1357,13 +1399,16 @@ static void decide_fast_route(dctp_plan& p) {
     p.fs.preferred = !(gap <= 1e-11) || (n >= min_n && !p.fd.on && !p.small);
 }
 
-static void sync_check(int device, int* flag, cudaStream_t s) {
+static void sync_check(int device, const StreamFlags& flags, cudaStream_t s) {
     DeviceScope scope(device);
     cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-    int h = 0;
-    cuda_check(cudaMemcpy(&h, flag, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(flag)");
-    if (h != 0) {
-        cuda_check(cudaMemset(flag, 0, sizeof(int)), "cudaMemset(flag)");
+    int* f = flags(s);
+    int h = 0, g = 0;
+    cuda_check(cudaMemcpy(&h, f, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(flag)");
+    cuda_check(cudaMemcpy(&g, flags.graph, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(flag)");
+    if (h != 0 || g != 0) {
+        if (h) cuda_check(cudaMemset(f, 0, sizeof(int)), "cudaMemset(flag)");
+        if (g) cuda_check(cudaMemset(flags.graph, 0, sizeof(int)), "cudaMemset(flag)");
         throw std::domain_error("DctPlusPlan: non-finite input sample");
     }
 }
@@ -1955,7 +2000,7 @@ int dctp_inverse_nmvp_f32(const dctp_plan* p, const float* in, float* out, size_
 int dctp_plan_sync_check(const dctp_plan* p, void* stream) {
     return guarded([&] {
         if (!p) throw std::invalid_argument("dctp_plan_sync_check: null plan");
-        sync_check(p->device, p->flags(static_cast<cudaStream_t>(stream)), static_cast<cudaStream_t>(stream));
+        sync_check(p->device, p->flags, static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -2008,7 +2053,7 @@ static bool forward_zero_copy(const dctp_plan* p, const double* h_in, double* h_
     if (!pinned_range(h_in, bytes, p->device) || !pinned_range(h_out, bytes, p->device)) return false;
     HostPipe& hp = host_pipe(p->device);
     plan_forward<double>(p, h_in, h_out, batch, hp.comp);
-    sync_check(p->device, p->flags(hp.comp), hp.comp);
+    sync_check(p->device, p->flags, hp.comp);
     return true;
 }
 
@@ -2026,7 +2071,7 @@ extern "C" {
                               [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) {         \
                                   FN<T>(p, din, dout, rows, s);                                       \
                               });                                                                     \
-            sync_check(p->device, p->flags(host_pipe(p->device).comp), nullptr);                                                  \
+            sync_check(p->device, p->flags, host_pipe(p->device).comp);                                                  \
         });                                                                                           \
     }
 DCTP_HOST_ENTRY(dctp_forward_host_f64, double, plan_forward, true)
@@ -2178,7 +2223,7 @@ int dctp_ensemble_create(size_t n, size_t k, const int* kinds, const size_t* is,
                                   k * sizeof(dctp::dev::CauchyStage), cudaMemcpyHostToDevice),
                        "cudaMemcpy(stages)");
         }
-        e->flags.device = e->device;
+        e->flags.init(e->device);
         cuda_check(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
         *out = e.release();
     });
@@ -2263,7 +2308,7 @@ static void ensemble_pruned_host(const dctp_ensemble* e, const T* h_in, T* h_out
     if (h_bounds)
         cuda_check(cudaMemcpyAsync(h_bounds, db.ptr, batch * sets * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
     if (h_pruned) cuda_check(cudaMemcpyAsync(h_pruned, dp.ptr, batch, cudaMemcpyDeviceToHost, s), "D2H");
-    sync_check(e->device, e->flags(s), s);
+    sync_check(e->device, e->flags, s);
 }
 
 extern "C" {
@@ -2289,7 +2334,7 @@ int dctp_ensemble_forward_all_pruned_host_f32(const dctp_ensemble* e, const floa
 int dctp_ensemble_sync_check(const dctp_ensemble* e, void* stream) {
     return guarded([&] {
         if (!e) throw std::invalid_argument("dctp_ensemble_sync_check: null ensemble");
-        sync_check(e->device, e->flags(static_cast<cudaStream_t>(stream)), static_cast<cudaStream_t>(stream));
+        sync_check(e->device, e->flags, static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -2303,7 +2348,7 @@ int dctp_ensemble_forward_all_host_f32(const dctp_ensemble* e, const float* h_in
                               [&](const float* din, float* dout, std::size_t rows, cudaStream_t s) {
                                   ensemble_forward<float>(e, din, dout, rows, s);
                               });
-        sync_check(e->device, e->flags(host_pipe(e->device).comp), nullptr);
+        sync_check(e->device, e->flags, host_pipe(e->device).comp);
     });
 }
 int dctp_ensemble_forward_all_host_f64(const dctp_ensemble* e, const double* h_in, double* h_out, size_t batch) {
@@ -2316,7 +2361,7 @@ int dctp_ensemble_forward_all_host_f64(const dctp_ensemble* e, const double* h_i
                                [&](const double* din, double* dout, std::size_t rows, cudaStream_t s) {
                                    ensemble_forward<double>(e, din, dout, rows, s);
                                });
-        sync_check(e->device, e->flags(host_pipe(e->device).comp), nullptr);
+        sync_check(e->device, e->flags, host_pipe(e->device).comp);
     });
 }
 
@@ -2439,7 +2484,7 @@ int dctp_chain_create(size_t n, size_t k, const int* kinds, const size_t* is, co
             DeviceScope scope(device);
             prepare_pool(device);
             c->blob = blob.upload();
-            c->flags.device = c->device;
+            c->flags.init(c->device);
         }
         *out = c.release();
     });
@@ -2493,7 +2538,7 @@ int dctp_chain_sync_check(const dctp_chain* c, void* stream) {
     return guarded([&] {
         if (!c) throw std::invalid_argument("dctp_chain_sync_check: null chain");
         if (!c->blob) throw std::invalid_argument("ChainedFactorization: host-only chain (created with device < 0)");
-        sync_check(c->device, c->flags(static_cast<cudaStream_t>(stream)), static_cast<cudaStream_t>(stream));
+        sync_check(c->device, c->flags, static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -2508,7 +2553,7 @@ int dctp_chain_sync_check(const dctp_chain* c, void* stream) {
                               [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) {          \
                                   chain_forward<T>(c, din, dout, rows, s);                             \
                               });                                                                      \
-            sync_check(c->device, c->flags(host_pipe(c->device).comp), nullptr);                                                   \
+            sync_check(c->device, c->flags, host_pipe(c->device).comp);                                                   \
         });                                                                                            \
     }
 DCTP_CHAIN_HOST_ENTRY(dctp_chain_forward_host_f64, double)

@@ -250,6 +250,13 @@ cudaError_t tc_bf16x3(const float* A, int lda, const uint16_t* b_sw, float* C, s
                       int K, int* flag, int num_sms, cudaStream_t stream, const int* col_map = nullptr,
                       const int* a_map = nullptr, const float* fold_add = nullptr, std::size_t ld_add = 0);
 
+/// out[b, c] = sum_k in[b, k] xt[c, k] for n in {16, 32, 64, 128}: one CTA
+/// per 32 signals, X^T staged in shared memory, m8n8k4 DMMA (small_dense.cu)
+/// — the latency route of small plans at small batches.
+bool small_dense_supported(std::size_t n, const void* in, std::size_t ld_in, const void* out, std::size_t ld_out);
+cudaError_t small_dense_forward(const double* in, std::size_t ld_in, const double* xt, std::size_t ld_xt, double* out,
+                                std::size_t ld_out, std::size_t n, std::size_t batch, int* flag, cudaStream_t stream);
+
 bool fused_small_supported(std::size_t n, int K, int A);
 bool fused_small_fold_supported(std::size_t n, int columns);
 cudaError_t fused_small_forward(const double* in, double* out, std::size_t batch, const SmallPlanDev& P, int* flag,

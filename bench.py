@@ -349,6 +349,25 @@ def kernel_roofline(cfg, alg, rows, top, t_ms, ms_per_step, ozaki_products):
     out = {"kernel": top, "launch_ms": t_ms, "kernel_share_of_step": t_ms / ms_per_step,
            "algorithmic_bytes_per_launch": nbytes, "hbm_achieved_gbs": hbm_ach, "hbm_frac": hbm_ach / hbm_peak,
            "traffic": None}
+    if "bf16x3" in top:
+        # fp32 product on the tcgen05 tensor cores with the bf16x3 split: three
+        # bf16 MMAs per algorithmic one (tc_bf16x3.cu)
+        flops = alg["flops_cauchy"] * rows
+        bf = meas.get("bf16_tflops")
+        peak = bf / 3.0 if bf else None
+        ach = flops / (t_ms * 1e-3) / 1e12
+        t_flop = flops / (peak * 1e12) if peak else 0.0
+        t_hbm = nbytes / (hbm_peak * 1e9)
+        if t_hbm >= t_flop:
+            out.update({"bound": "hbm", "unit": "GB/s", "achieved": hbm_ach, "peak": hbm_peak,
+                        "frac": hbm_ach / hbm_peak, "peak_source": hbm_src})
+        else:
+            out.update({"bound": "tensor", "unit": "TFLOP/s", "achieved": ach, "peak": peak,
+                        "frac": ach / peak if peak else None,
+                        "peak_source": "MEASURED_PEAKS.json bf16_tflops / 3 (bf16x3 passes)"})
+        out["algorithmic_flops_per_launch"] = flops
+        out["t_roof_ms"] = max(t_flop, t_hbm) * 1e3
+        return out
     if top.endswith("_i8"):
         # fp64 product on the int8 tensor cores: the kernel's algorithm is
         # P = S(S+1)/2 int8 GEMMs of the same shape (ozaki.cu); peak = the
@@ -489,18 +508,46 @@ class GpuArm:
             ms = e0.elapsed_time(e1)
             l2 = f"inputs {in_bytes / 2**20:.0f} MiB per rank per step > 126 MB L2: no flush"
         else:
-            # inputs fit in L2: flush (write 252 MB) between timed steps, each
-            # step bracketed by its own events
-            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            # inputs fit in L2: the K steps rotate over R copies of the input
+            # and output (R x (in + out) > 2 x L2, so every step reads its
+            # input from DRAM), captured in one CUDA graph so the host-side
+            # launch path is not inside the timed region either
+            out_bytes = y.numel() * y.element_size()
+            reps = max(2, -(-2 * L2_BYTES // (in_bytes + out_bytes)))
+            xs = [x.clone() for _ in range(reps)]
+            ys = [torch.empty_like(y) for _ in range(reps)]
+
+            def step_i(i):
+                xi, yi = xs[i % reps], ys[i % reps]
+                if op == "forward_all":
+                    plan.forward_all_batch(xi, sync=False, out=yi)
+                elif op == "inverse":
+                    plan.inverse(xi, sync=False, out=yi)
+                else:
+                    plan.forward(xi, sync=False, out=yi)
+
+            gs = torch.cuda.Stream(self.dev)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(gs):
+                for i in range(reps):  # first-use allocations outside the capture
+                    step_i(i)
+                torch.cuda.synchronize(self.dev)
+                with torch.cuda.graph(graph, stream=gs):
+                    for i in range(steps):
+                        step_i(i)
+            graph.replay()
             self.barrier()
-            for a, b in ev:
-                self.flush_l2()
-                a.record(stream)
-                step()
-                b.record(stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            graph.replay()
+            e1.record(stream)
             self.barrier()
-            ms = sum(a.elapsed_time(b) for a, b in ev)
-            l2 = f"inputs {in_bytes / 2**20:.1f} MiB per rank fit in L2: 252 MB written between timed steps"
+            ms = e0.elapsed_time(e1)
+            if op != "forward_all":
+                check()
+            l2 = (f"inputs {in_bytes / 2**20:.1f} MiB per rank fit in L2: the {steps} timed steps rotate over {reps} "
+                  f"input/output copies ({reps * (in_bytes + out_bytes) / 2**20:.0f} MiB > 2 x 126 MB L2), "
+                  f"captured in one CUDA graph")
         # per-kernel times (the library's CUDA events around every launch): a
         # separate untimed pass of the same steps right after the timed one
         # (same clocks; the same L2 flush between steps for small inputs)
@@ -513,6 +560,11 @@ class GpuArm:
         torch.cuda.synchronize(self.dev)
         P.profile_enable(False)
         prof = P.profile_summary()
+        if not big:
+            # per-launch events include the launch latency of these short
+            # kernels; scale the kernels' shares to the graph-timed step
+            tot = sum(v[1] for v in prof.values()) / steps
+            prof = {k: (v[0], v[1] * (ms / steps) / tot) for k, v in prof.items()}
         sustain = None
         if clocks:
             # untimed sustained load so the clocks (ours and the driver's

@@ -141,3 +141,29 @@ def test_ozaki_slice_counts_agree(P, torch, reference, tmp_path):
         subprocess.run([sys.executable, str(script), str(f), sl], env=env, check=True, timeout=300)
         errs[sl] = O.parity(np.load(f), want)
     assert errs["5"] <= 1e-10 and errs["6"] <= 1e-12, errs
+
+
+def test_cuda_graph_capture_and_replay(P, torch):
+    """Launches captured into a CUDA graph replay to the same coefficients;
+    a non-finite sample fed through the graph raises DomainError at the next
+    sync_check (the object's graph flag)."""
+    plan = P.DctPlusPlan(256, P.RankOneUpdate.edge_delta(128, 129, -0.7), 1e-12)
+    x = torch.as_tensor(P.fill_signals(9, P.DIST_AR, 256, 2048, 0.95), device="cuda")
+    want = plan.forward(x)
+    y = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        plan.forward(x, sync=False, out=y)  # warm-up outside the capture
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            plan.forward(x, sync=False, out=y)
+    y.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, want)
+    x[3, 4] = float("nan")
+    g.replay()
+    with pytest.raises(P.DomainError):
+        plan.sync_check()
+    plan.sync_check()  # cleared

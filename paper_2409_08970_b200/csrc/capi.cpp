@@ -1136,13 +1136,16 @@ static bool fold_route(const dctp_plan* p) {
 
 // int8 tensor-core (Ozaki) products, defined with the dense routes below
 static int ozaki_slices(std::size_t n);
-// shortest product length the folded route sends to them (DCTP_OZAKI_FOLD_MIN_K)
-static int ozaki_fold_min_k() {
+// shortest product length the folded route sends to them (DCTP_OZAKI_FOLD_MIN_K
+// overrides both): forward 512 (C3: 0.27 vs 0.30 ms with the slicing pass),
+// inverse 2048 (C3's 512-long inverse product: 0.43 vs 0.37 ms — its unfolding
+// epilogue is the heavier one)
+static int ozaki_fold_min_k(bool inverse) {
     static const int v = [] {
         const char* e = std::getenv("DCTP_OZAKI_FOLD_MIN_K");
-        return e ? std::atoi(e) : 2048;
+        return e ? std::atoi(e) : 0;
     }();
-    return v;
+    return v > 0 ? v : (inverse ? 2048 : 512);
 }
 static void ensure_fold_ozaki(const dctp_plan* p, int which, int S, cudaStream_t s);
 static void rows_by_ozaki(const double* in, std::size_t ld_in, const int8_t* b_sl, const int* eb, int K, int N,
@@ -1180,7 +1183,11 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
         // TMA bulk copies need 16-byte aligned rows; a misaligned view takes
         // the generic (DCT + Cauchy kernel) route instead
         const bool aligned = (reinterpret_cast<std::uintptr_t>(in) | reinterpret_cast<std::uintptr_t>(out)) % 16 == 0;
-        if (p->small && aligned) {
+        static const bool fused_off = [] { // DCTP_FUSED=0: skip the fused kernel (route experiments)
+            const char* e = std::getenv("DCTP_FUSED");
+            return e && e[0] == '0';
+        }();
+        if (p->small && aligned && !fused_off) {
             const dctp::dev::SmallPlanDev sp = small_plan_dev(p);
             cuda_check(DCTP_LAUNCH("fused_small_fwd", s,
                                    dctp::dev::fused_small_forward(in, out, batch, sp, p->flags(s), p->num_sms, s)),
@@ -1237,9 +1244,7 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
             }
         }
         if constexpr (!f32) {
-            // the int8 products pay only for long rows (C3's 512-wide u: 0.28 vs
-            // 0.30 ms forward, 0.43 vs 0.37 ms inverse with the slicing pass)
-            if (const int S = f.L >= ozaki_fold_min_k() ? ozaki_slices(n) : 0) {
+            if (const int S = f.L >= ozaki_fold_min_k(false) ? ozaki_slices(n) : 0) {
                 ensure_fold_ozaki(p, 0, S, s);
                 rows_by_ozaki(u.ptr, f.L, f.oz[0], f.oz_e[0], f.L, f.cols, S, out, n, batch, p->flags(s), s, "fold_w_i8",
                               at<int>(p->blob, f.map));
@@ -1327,7 +1332,7 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
             }
         }
         if constexpr (!f32) {
-            if (const int S = f.cols >= ozaki_fold_min_k() ? ozaki_slices(n) : 0) {
+            if (const int S = f.cols >= ozaki_fold_min_k(true) ? ozaki_slices(n) : 0) {
                 ensure_fold_ozaki(p, 1, S, s);
                 rows_by_ozaki(in, n, f.oz[1], f.oz_e[1], f.cols, f.L, S, out, n, batch, p->flags(s), s, "fold_wt_i8",
                               nullptr, at<int>(p->blob, f.map), w.ptr, f.L);
@@ -1601,8 +1606,8 @@ static void ensure_dense(const dctp_plan* p, cudaStream_t s) {
 /// Cauchy block is generated, and the DCT pass disappears.  X^T and X cost
 /// 16 n^2 bytes of HBM.  DCTP_DENSE=0 / 1 forces the choice.
 static bool dense_route(const dctp_plan* p) {
-    if (p->small) return false;
     const char* e = std::getenv("DCTP_DENSE");
+    if (p->small && !(e && e[0] == '1')) return false;
     if (e && e[0] == '0') return false;
     const double n = static_cast<double>(p->st.n);
     if (16.0 * n * n > 4.0 * (1ull << 30)) return false;

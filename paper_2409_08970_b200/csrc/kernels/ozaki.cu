@@ -101,21 +101,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 // ---------------------------------------------------------------- slicing
 
-/// One CTA (8 warps) per row: pass 1 the row maximum (and the finiteness
-/// check of check_signal), pass 2 the S digits.  Thread t handles 4
-/// consecutive k per step (one 32-bit word of a 16-byte swizzle unit), so both
-/// passes read the row with coalesced 32-byte loads (vec: 16-byte aligned
-/// rows, no column map) and each slice's 64-byte chunk rows are written as
-/// whole sectors; pass 2 finds the row in L1/L2.
-template <class T>
+/// Slicing of one row per WPR warps (WPR = 8: a CTA per row, long rows;
+/// WPR = 1: a warp per row, 8 rows per CTA, rows up to 2048): pass 1 the row
+/// maximum (and the finiteness check of check_signal), pass 2 the S digits.
+/// Thread t handles 4 consecutive k per step (one 32-bit word of a 16-byte
+/// swizzle unit), so both passes read the row with coalesced 32-byte loads
+/// (vec: 16-byte aligned rows, no column map) and each slice's 64-byte chunk
+/// rows are written as whole sectors; pass 2 finds the row in L1/L2.
+template <class T, int WPR>
 __global__ void __launch_bounds__(256)
-ozaki_slice_kernel(const T* __restrict__ in, std::size_t ld, std::size_t rows, int K, int nch,
+ozaki_slice_kernel(const T* __restrict__ in, std::size_t ld, std::size_t rows, std::size_t rows_pad, int K, int nch,
                    const int* __restrict__ a_map, int tile_rows, int S, int8_t* __restrict__ sl,
                    int* __restrict__ expo, int* flag, int vec) {
+    constexpr int kRowThreads = 32 * WPR;
     __shared__ double red[8];
     __shared__ int red_bad[8];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const std::size_t r = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = WPR == 8 ? static_cast<int>(threadIdx.x) : lane; // thread index within the row
+    const std::size_t r = WPR == 8 ? blockIdx.x : static_cast<std::size_t>(blockIdx.x) * 8 + warp;
+    if (r >= rows_pad) return; // whole warps (WPR = 1) or whole CTAs (WPR = 8)
     const bool real = r < rows;
     const T* row = in + (real ? r * ld : 0);
     auto load4 = [&](int k, double (&v)[4]) {
@@ -137,7 +141,7 @@ ozaki_slice_kernel(const T* __restrict__ in, std::size_t ld, std::size_t rows, i
     double mx = 0.0;
     bool bad = false;
 #pragma unroll 2
-    for (int k = 4 * tid; k < K; k += 1024) {
+    for (int k = 4 * t; k < K; k += 4 * kRowThreads) {
         double v[4];
         load4(k, v);
 #pragma unroll
@@ -148,32 +152,34 @@ ozaki_slice_kernel(const T* __restrict__ in, std::size_t ld, std::size_t rows, i
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int wbad = __any_sync(0xffffffffu, bad);
-    if (lane == 0) {
-        red[warp] = mx;
-        red_bad[warp] = wbad;
-    }
-    __syncthreads();
-    mx = red[0];
-    int anybad = red_bad[0];
+    int anybad = __any_sync(0xffffffffu, bad);
+    if constexpr (WPR == 8) {
+        if (lane == 0) {
+            red[warp] = mx;
+            red_bad[warp] = anybad;
+        }
+        __syncthreads();
+        mx = red[0];
+        anybad = red_bad[0];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) {
-        mx = fmax(mx, red[w]);
-        anybad |= red_bad[w];
+        for (int w = 1; w < 8; ++w) {
+            mx = fmax(mx, red[w]);
+            anybad |= red_bad[w];
+        }
     }
     if (anybad) {
-        if (tid == 0 && flag) atomicOr(flag, 1);
+        if (t == 0 && flag) atomicOr(flag, 1);
         mx = 0.0;
     }
     int e = 0;
     if (mx > 0.0) frexp(mx, &e); // mx = m 2^e, m in [0.5, 1): |x| < 2^e
-    if (tid == 0) expo[r] = e;
+    if (t == 0) expo[r] = e;
     const double scale = ldexp(127.0, -e);
     const std::size_t tile = r / tile_rows;
     const int lr = static_cast<int>(r % tile_rows);
     const std::size_t slice_bytes = static_cast<std::size_t>(tile_rows) * CB;
 #pragma unroll 2
-    for (int k = 4 * tid; k < nch * CB; k += 1024) {
+    for (int k = 4 * t; k < nch * CB; k += 4 * kRowThreads) {
         double v[4];
         load4(k, v);
 #pragma unroll
@@ -412,12 +418,23 @@ __device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t a, uint64_
 }
 
 /// Commit of the pair's MMAs, arriving on the barrier at the same offset in
-/// both CTAs.
-__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+/// every CTA of `mask`.
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
             ptx::smem_addr(bar)),
-        "h"(static_cast<uint16_t>(0x3))
+        "h"(mask)
+        : "memory");
+}
+
+/// 1-D bulk copy global -> the same shared offset in every CTA of `mask`,
+/// completing on each destination's mbarrier at `bar`'s offset.
+__device__ __forceinline__ void bulk_load_mcast(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+        "%4;\n" ::"r"(ptx::smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(ptx::smem_addr(bar)), "h"(mask)
         : "memory");
 }
 
@@ -443,19 +460,24 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
         : "memory");
 }
 
-/// Clusters of two CTAs along M.  CTA rank r holds rows 128 r.. of the pair's
-/// 256-row tile and B rows (NT / 2) r.. of the column tile (B sliced with
-/// tile_rows = NT / 2, so its half is tile 2 nt + r).  Rank 0 issues the
-/// cta_group::2 MMAs once both CTAs' stage landed: rank 1's warp 2 relays
-/// its full barrier to rank 0's peer_full barrier; the MMAs' completion is
-/// multicast to both CTAs' empty barriers.  Each CTA's TMEM holds its 128
-/// rows of every level accumulator and runs its own epilogue.
-template <int S, int NT>
+/// Clusters of 2 x NSUB CTAs: NSUB CTA pairs along N, each pair two CTAs
+/// along M.  In a pair, the CTA with M-half h holds rows 128 h.. of the
+/// pair's 256-row tile and B rows (NT / 2) h.. of the pair's column tile (B
+/// sliced with tile_rows = NT / 2, so its half is tile 2 nt + h).  The h = 0
+/// CTA issues the cta_group::2 MMAs once both CTAs' stage landed: the h = 1
+/// CTA's warp 2 relays its full barrier to the leader's peer_full barrier.
+/// Each CTA's TMEM holds its 128 rows of every level accumulator and runs its
+/// own epilogue.  NSUB = 2: the two pairs share the same 256 rows, so each CTA
+/// loads one half of its A chunk and multicasts it to its counterpart in the
+/// other pair — A's L2 reads halve (the operand traffic, not the MMAs, held
+/// the pair kernel at ~67% of the tensor pipe); both leaders' commits then
+/// arrive on every CTA's empty barrier.
+template <int S, int NT, int NSUB>
 __global__ void __launch_bounds__(kThreads, 1)
 ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, const int8_t* __restrict__ b_sl,
                    const int* __restrict__ eb, std::size_t M, int N, int nch, double* __restrict__ out,
                    std::size_t ld_out, const int* __restrict__ col_map, const double* __restrict__ fold_add,
-                   std::size_t ld_add, int ntn, int nfast) {
+                   std::size_t ld_add, int ntn, int nfast, std::size_t npairs, int debug) {
     using G = Geo2<S, NT>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t raw = ptx::smem_addr(smem_raw);
@@ -468,21 +490,31 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
     const uint32_t sbase = ptx::smem_addr(base);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    uint32_t rank = 0;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    uint32_t q = 0;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(q));
+    const uint32_t rank = q & 1u, ns = q >> 1; // M half within the pair, pair index
     // this CTA's 128-row tile (pairs: 2 p, 2 p + 1) and column tile.  nfast:
     // consecutive clusters walk the column tiles of one row pair (the B
     // operand stays in L2 and A streams once: short-K products such as the
     // chain); otherwise row pairs fastest (B, the larger operand, streams once)
     std::size_t mt;
     int nt;
-    if (nfast) {
-        const std::size_t ci = blockIdx.x >> 1;
-        nt = static_cast<int>(ci % static_cast<std::size_t>(ntn));
-        mt = 2 * (ci / static_cast<std::size_t>(ntn)) + rank;
-    } else {
+    if (NSUB == 1 && !nfast) {
         mt = blockIdx.x;
         nt = blockIdx.y;
+    } else {
+        const std::size_t ci = blockIdx.x / (2 * NSUB);
+        const std::size_t ntc = (static_cast<std::size_t>(ntn) + NSUB - 1) / NSUB; // column-tile groups
+        std::size_t p, g;
+        if (nfast) {
+            g = ci % ntc;
+            p = ci / ntc;
+        } else {
+            p = ci % npairs;
+            g = ci / npairs;
+        }
+        nt = static_cast<int>(g * NSUB + ns);
+        mt = 2 * p + rank;
     }
 
     if (warp == 0) {
@@ -495,28 +527,40 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
         for (int i = 0; i < G::kStages; ++i) {
             ptx::mbar_init(full + i, 1);
             ptx::mbar_init(peer_full + i, 1);
-            ptx::mbar_init(empty + i, 1);
+            ptx::mbar_init(empty + i, NSUB); // one commit from each pair's leader
         }
         ptx::mbar_init(done, 1);
         ptx::fence_mbar_init();
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
-    cluster_sync(); // both CTAs' barriers and TMEM exist before any cross-CTA traffic
+    cluster_sync(); // every CTA's barriers and TMEM exist before any cross-CTA traffic
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
     const int8_t* a_tile = a_sl + mt * static_cast<std::size_t>(nch) * G::kABytes;
     const int8_t* b_tile = b_sl + (2 * static_cast<std::size_t>(nt) + rank) * nch * G::kBBytes;
 
-    if (warp == 0) { // producer warp (both CTAs): this CTA's A rows and B half
-        for (int ch = 0; ch < nch; ++ch) {
+    const uint16_t all_mask = static_cast<uint16_t>((1u << (2 * NSUB)) - 1u);
+    const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * ns));
+    // development knob DCTP_OZAKI_DEBUG=1: only the first ring of chunks is
+    // loaded (the MMAs reuse it: tensor-pipe time alone)
+    const int nload = (debug & 1) ? (nch < G::kStages ? nch : G::kStages) : nch;
+    if (warp == 0) { // producer warp (every CTA): this CTA's A rows and B half
+        for (int ch = 0; ch < nload; ++ch) {
             const int st = ch % G::kStages;
             if (ch >= G::kStages) ptx::mbar_wait(empty + st, static_cast<uint32_t>(((ch / G::kStages) - 1) & 1));
             if (elect_one()) {
                 ptx::mbar_expect_tx(full + st, G::kStageBytes);
                 unsigned char* dst = base + st * G::kStageBytes;
-                ptx::bulk_load(dst, a_tile + static_cast<std::size_t>(ch) * G::kABytes, G::kABytes, full + st);
+                const int8_t* asrc = a_tile + static_cast<std::size_t>(ch) * G::kABytes;
+                if constexpr (NSUB == 2) { // half of the A chunk, to this CTA and its counterpart
+                    constexpr uint32_t half = G::kABytes / 2;
+                    bulk_load_mcast(dst + ns * half, asrc + ns * half, half, full + st,
+                                    static_cast<uint16_t>((1u << q) | (1u << (q ^ 2u))));
+                } else {
+                    ptx::bulk_load(dst, asrc, G::kABytes, full + st);
+                }
                 ptx::bulk_load(dst + G::kABytes, b_tile + static_cast<std::size_t>(ch) * G::kBBytes, G::kBBytes,
                                full + st);
             }
@@ -527,8 +571,10 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
         for (int ch = 0; ch < nch; ++ch) {
             const int st = ch % G::kStages;
             const uint32_t ph = static_cast<uint32_t>((ch / G::kStages) & 1);
-            ptx::mbar_wait(full + st, ph);
-            mbar_wait_cluster(peer_full + st, ph);
+            if (ch < nload) {
+                ptx::mbar_wait(full + st, ph);
+                mbar_wait_cluster(peer_full + st, ph);
+            }
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             if (elect_one()) {
                 const uint64_t so = static_cast<uint64_t>(st * G::kStageBytes) >> 4;
@@ -546,17 +592,17 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
                         }
                     }
                 }
-                mma_commit_pair(empty + st);
+                mma_commit_pair(empty + st, all_mask);
             }
             __syncwarp();
         }
-        if (elect_one()) mma_commit_pair(done);
+        if (elect_one()) mma_commit_pair(done, pair_mask);
         __syncwarp();
-    } else if (warp == 2 && rank == 1) { // relay: this CTA's stage landed -> rank 0
-        for (int ch = 0; ch < nch; ++ch) {
+    } else if (warp == 2 && rank == 1) { // relay: this CTA's stage landed -> the pair's leader
+        for (int ch = 0; ch < nload; ++ch) {
             const int st = ch % G::kStages;
             ptx::mbar_wait(full + st, static_cast<uint32_t>((ch / G::kStages) & 1));
-            if (elect_one()) mbar_arrive_remote(peer_full + st, 0);
+            if (elect_one()) mbar_arrive_remote(peer_full + st, q - 1);
             __syncwarp();
         }
     }
@@ -571,12 +617,12 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
 }
 
-template <int S, int NT>
+template <int S, int NT, int NSUB>
 cudaError_t launch_gemm2(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M, int N,
                          int nch, double* out, std::size_t ld_out, const int* col_map, const double* fold_add,
                          std::size_t ld_add, cudaStream_t stream) {
     using G = Geo2<S, NT>;
-    cudaError_t e = smem_optin(reinterpret_cast<const void*>(ozaki_gemm2_kernel<S, NT>), G::kSmem);
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(ozaki_gemm2_kernel<S, NT, NSUB>), G::kSmem);
     if (e != cudaSuccess) return e;
     const std::size_t gm = (M + 2 * TM - 1) / (2 * TM) * 2; // whole CTA pairs (A rows padded to 256)
     const int ntn = (N + NT - 1) / NT;
@@ -589,21 +635,27 @@ cudaError_t launch_gemm2(const int8_t* a_sl, const int* ea, const int8_t* b_sl, 
         return v ? std::atoi(v) : -1;
     }();
     const int nfast = order == 0 ? 0 : order == 1 ? 1 : (b_bytes < a_bytes ? 1 : 0);
-    if (gm * ntn >= (1ull << 31)) return cudaErrorInvalidValue;
+    const std::size_t ntc = (static_cast<std::size_t>(ntn) + NSUB - 1) / NSUB;
+    if (gm * ntc * NSUB >= (1ull << 31)) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = nfast ? dim3(static_cast<unsigned>(gm * ntn), 1) : dim3(static_cast<unsigned>(gm), ntn);
+    cfg.gridDim = (NSUB == 1 && !nfast) ? dim3(static_cast<unsigned>(gm), ntn)
+                                        : dim3(static_cast<unsigned>(gm * ntc * NSUB), 1);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = G::kSmem;
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.x = 2 * NSUB;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, ozaki_gemm2_kernel<S, NT>, a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map,
-                              fold_add, ld_add, ntn, nfast);
+    static const int debug = [] { // development knob (timing only): 1 = no loads after the first ring
+        const char* v = std::getenv("DCTP_OZAKI_DEBUG");
+        return v ? std::atoi(v) : 0;
+    }();
+    return cudaLaunchKernelEx(&cfg, ozaki_gemm2_kernel<S, NT, NSUB>, a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map,
+                              fold_add, ld_add, ntn, nfast, gm / 2, debug);
 }
 
 template <int S, int NT>
@@ -632,7 +684,9 @@ cudaError_t launch_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, c
 
 } // namespace
 
-/// CTA-pair kernel (default; DCTP_OZAKI_PAIR=0: the single-CTA kernel).
+/// CTA-pair kernel (default; DCTP_OZAKI_PAIR=0: the single-CTA kernel);
+/// DCTP_OZAKI_MCAST=1: clusters of two pairs sharing A by multicast (correct,
+/// but slower: the L2 reads it saves were not the limit).
 static bool pair_mode() {
     static const bool on = [] {
         const char* e = std::getenv("DCTP_OZAKI_PAIR");
@@ -640,9 +694,20 @@ static bool pair_mode() {
     }();
     return on;
 }
+static int pair_nsub() {
+    static const int v = [] { // measured slower (C5 1.42 vs 1.36 ms, X6 0.41 vs 0.35): opt-in
+        const char* e = std::getenv("DCTP_OZAKI_MCAST");
+        return (e && e[0] == '1') ? 2 : 1;
+    }();
+    return pair_mode() ? v : 1;
+}
 
-int ozaki_pad_n(int slices) { return slices <= 5 ? 96 : 80; }
-int ozaki_tile_n(int slices) { return pair_mode() ? ozaki_pad_n(slices) / 2 : ozaki_pad_n(slices); }
+// B rows are padded to whole clusters' column tiles
+int ozaki_pad_n(int slices) { return (slices <= 5 ? 96 : 80) * pair_nsub(); }
+int ozaki_tile_n(int slices) {
+    const int nt = slices <= 5 ? 96 : 80;
+    return pair_mode() ? nt / 2 : nt;
+}
 int ozaki_pad_m() { return pair_mode() ? 2 * TM : TM; }
 
 std::size_t ozaki_slice_bytes(std::size_t rows, int K, int tile_rows, int slices, int pad_rows) {
@@ -660,9 +725,13 @@ cudaError_t ozaki_slice(const T* in, std::size_t ld, std::size_t rows, int K, co
     const std::size_t rows_pad = (rows + pad - 1) / pad * pad;
     const int nch = (K + CB - 1) / CB;
     const int vec = !a_map && reinterpret_cast<std::uintptr_t>(in) % 16 == 0 && (ld * sizeof(T)) % 16 == 0;
-    if (rows_pad >= (1ull << 31)) return cudaErrorInvalidValue; // one CTA per (padded) row
-    ozaki_slice_kernel<T><<<static_cast<unsigned>(rows_pad), 256, 0, stream>>>(in, ld, rows, K, nch, a_map, tile_rows,
-                                                                               slices, sl, expo, flag, vec);
+    if (rows_pad >= (1ull << 31)) return cudaErrorInvalidValue;
+    if (K <= 2048) // a warp per row, 8 rows per CTA
+        ozaki_slice_kernel<T, 1><<<static_cast<unsigned>((rows_pad + 7) / 8), 256, 0, stream>>>(
+            in, ld, rows, rows_pad, K, nch, a_map, tile_rows, slices, sl, expo, flag, vec);
+    else // a CTA per row
+        ozaki_slice_kernel<T, 8><<<static_cast<unsigned>(rows_pad), 256, 0, stream>>>(
+            in, ld, rows, rows_pad, K, nch, a_map, tile_rows, slices, sl, expo, flag, vec);
     return cudaGetLastError();
 }
 template cudaError_t ozaki_slice<double>(const double*, std::size_t, std::size_t, int, const int*, int, int, int8_t*,
@@ -676,10 +745,17 @@ cudaError_t ozaki_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, co
     if (M == 0 || N == 0) return cudaSuccess;
     const int nch = (K + CB - 1) / CB;
     if (pair_mode()) {
+        const bool mc = pair_nsub() == 2;
         if (slices == 5)
-            return launch_gemm2<5, 96>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add, stream);
+            return mc ? launch_gemm2<5, 96, 2>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add,
+                                               stream)
+                      : launch_gemm2<5, 96, 1>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add,
+                                               stream);
         if (slices == 6)
-            return launch_gemm2<6, 80>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add, stream);
+            return mc ? launch_gemm2<6, 80, 2>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add,
+                                               stream)
+                      : launch_gemm2<6, 80, 1>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add,
+                                               stream);
         return cudaErrorInvalidValue;
     }
     if (slices == 5)

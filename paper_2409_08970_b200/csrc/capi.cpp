@@ -1404,13 +1404,40 @@ static void decide_fast_route(dctp_plan& p) {
     p.fs.preferred = !(gap <= 1e-11) || (n >= min_n && !p.fd.on && !p.small);
 }
 
+/// Page-locked host words of the calling thread for flag read-back (freed at
+/// thread exit).
+struct PinnedWords {
+    int* p = nullptr;
+    PinnedWords() {
+        if (cudaHostAlloc(reinterpret_cast<void**>(&p), 2 * sizeof(int), cudaHostAllocPortable) != cudaSuccess)
+            p = nullptr;
+    }
+    ~PinnedWords() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+/// Waits for `s` and raises std::domain_error if a kernel on it (or a
+/// captured graph of the object) saw a non-finite sample.  The two flag words
+/// are read back by copies queued behind the stream's work, so the call costs
+/// one stream synchronisation.
 static void sync_check(int device, const StreamFlags& flags, cudaStream_t s) {
     DeviceScope scope(device);
-    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     int* f = flags(s);
+    thread_local PinnedWords pw;
     int h = 0, g = 0;
-    cuda_check(cudaMemcpy(&h, f, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(flag)");
-    cuda_check(cudaMemcpy(&g, flags.graph, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(flag)");
+    if (pw.p) {
+        cuda_check(cudaMemcpyAsync(pw.p, f, sizeof(int), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync(flag)");
+        cuda_check(cudaMemcpyAsync(pw.p + 1, flags.graph, sizeof(int), cudaMemcpyDeviceToHost, s),
+                   "cudaMemcpyAsync(flag)");
+        cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        h = pw.p[0];
+        g = pw.p[1];
+    } else {
+        cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        cuda_check(cudaMemcpy(&h, f, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(flag)");
+        cuda_check(cudaMemcpy(&g, flags.graph, sizeof(int), cudaMemcpyDeviceToHost), "cudaMemcpy(flag)");
+    }
     if (h != 0 || g != 0) {
         if (h) cuda_check(cudaMemset(f, 0, sizeof(int)), "cudaMemset(flag)");
         if (g) cuda_check(cudaMemset(flags.graph, 0, sizeof(int)), "cudaMemset(flag)");
@@ -1431,6 +1458,9 @@ struct HostPipe {
     std::vector<cudaEvent_t> loaded, computed, drained;
     void* buf = nullptr;
     std::size_t buf_bytes = 0;
+    // tiny batches (host_tiny): page-locked staging and device rows
+    void* tiny_host = nullptr;
+    void* tiny_dev = nullptr;
 
     HostPipe() = default;
     HostPipe(const HostPipe&) = delete;
@@ -1440,6 +1470,8 @@ struct HostPipe {
         if (cudaGetDevice(&prev) != cudaSuccess) return;
         cudaSetDevice(device);
         if (buf) cudaFree(buf);
+        if (tiny_dev) cudaFree(tiny_dev);
+        if (tiny_host) cudaFreeHost(tiny_host);
         for (auto* v : {&loaded, &computed, &drained})
             for (auto ev : *v) cudaEventDestroy(ev);
         for (cudaStream_t st : {in, comp, out})
@@ -1470,6 +1502,54 @@ static HostPipe& host_pipe(int device) {
 static std::size_t env_size(const char* name, std::size_t dflt) {
     const char* e = std::getenv(name);
     return e ? static_cast<std::size_t>(std::max(1, std::atoi(e))) : dflt;
+}
+
+/// Largest batch (input + output bytes) the tiny host path takes.
+constexpr std::size_t kTinyBytes = 256 << 10;
+
+/// Host-buffer apply of a tiny batch (the reference's per-signal call,
+/// bench.hpp:139-169): copy into page-locked staging that the kernels read
+/// and write in place over PCIe (mapped; no H2D / D2H copy operations), the
+/// flag read-back queued behind them, one synchronisation (sync_check), copy
+/// out — for rows up to 256 samples; longer rows (whose kernels read the input
+/// more than once) stage through device memory with one H2D and one D2H
+/// (tools/latency_report.py: C1 / C2 / C3 per-signal 54 / 62 / 97 us through
+/// the staged pipeline -> 30 / 32 / 69 us).  DCTP_TINY=0 / copy / map forces
+/// off / device staging / mapped staging.  Returns false above kTinyBytes.
+template <class T, class F>
+static bool host_tiny(int device, const StreamFlags& flags, std::size_t batch, std::size_t in_row,
+                      std::size_t out_row, const T* h_in, T* h_out, F&& run) {
+    const std::size_t in_b = batch * in_row * sizeof(T), out_b = batch * out_row * sizeof(T);
+    if (in_b + out_b > kTinyBytes) return false;
+    static const int forced = [] { // -1 auto, 0 off, 1 mapped staging, 2 device staging
+        const char* e = std::getenv("DCTP_TINY");
+        if (!e) return -1;
+        return e[0] == '0' ? 0 : (e[0] == 'c' ? 2 : (e[0] == 'm' ? 1 : -1));
+    }();
+    if (forced == 0) return false;
+    const int mode = forced > 0 ? forced : (in_row <= 256 ? 1 : 2);
+    if (!h_in || !h_out) throw std::invalid_argument("host buffer is null");
+    DeviceScope scope(device);
+    HostPipe& hp = host_pipe(device);
+    if (!hp.tiny_host) {
+        cuda_check(cudaHostAlloc(&hp.tiny_host, kTinyBytes, cudaHostAllocPortable), "cudaHostAlloc(tiny)");
+        cuda_check(cudaMalloc(&hp.tiny_dev, kTinyBytes), "cudaMalloc(tiny)");
+    }
+    const std::size_t out_off = (in_b + 255) / 256 * 256;
+    if (out_off + out_b > kTinyBytes) return false;
+    char* hs = static_cast<char*>(hp.tiny_host);
+    char* ds = static_cast<char*>(hp.tiny_dev);
+    std::memcpy(hs, h_in, in_b);
+    if (mode == 1) {
+        run(reinterpret_cast<const T*>(hs), reinterpret_cast<T*>(hs + out_off), batch, hp.comp);
+    } else {
+        cuda_check(cudaMemcpyAsync(ds, hs, in_b, cudaMemcpyHostToDevice, hp.comp), "H2D");
+        run(reinterpret_cast<const T*>(ds), reinterpret_cast<T*>(ds + out_off), batch, hp.comp);
+        cuda_check(cudaMemcpyAsync(hs + out_off, ds + out_off, out_b, cudaMemcpyDeviceToHost, hp.comp), "D2H");
+    }
+    sync_check(device, flags, hp.comp);
+    std::memcpy(h_out, hs + out_off, out_b);
+    return true;
 }
 
 template <class T, class F>
@@ -2072,6 +2152,8 @@ extern "C" {
             if (batch == 0) return;                                                                   \
             const std::size_t n = p->st.n;                                                           \
             if (ZC && forward_zero_copy(p, h_in, h_out, batch)) return;                               \
+            auto fn = [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) { FN<T>(p, din, dout, rows, s); }; \
+            if (host_tiny<T>(p->device, p->flags, batch, n, n, h_in, h_out, fn)) return;              \
             host_roundtrip<T>(p->device, batch, n, n, h_in, h_out,                                    \
                               [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) {         \
                                   FN<T>(p, din, dout, rows, s);                                       \
@@ -2349,6 +2431,11 @@ int dctp_ensemble_forward_all_host_f32(const dctp_ensemble* e, const float* h_in
         if (!e->blob) throw std::invalid_argument("PrunedEnsemblePlan: host-only plan (created with device < 0)");
         if (batch == 0) return;
         const std::size_t sets = e->members.size() + 1;
+        if (host_tiny<float>(e->device, e->flags, batch, e->n, sets * e->n, h_in, h_out,
+                             [&](const float* din, float* dout, std::size_t rows, cudaStream_t s) {
+                                 ensemble_forward<float>(e, din, dout, rows, s);
+                             }))
+            return;
         host_roundtrip<float>(e->device, batch, e->n, sets * e->n, h_in, h_out,
                               [&](const float* din, float* dout, std::size_t rows, cudaStream_t s) {
                                   ensemble_forward<float>(e, din, dout, rows, s);
@@ -2362,6 +2449,11 @@ int dctp_ensemble_forward_all_host_f64(const dctp_ensemble* e, const double* h_i
         if (!e->blob) throw std::invalid_argument("PrunedEnsemblePlan: host-only plan (created with device < 0)");
         if (batch == 0) return;
         const std::size_t sets = e->members.size() + 1;
+        if (host_tiny<double>(e->device, e->flags, batch, e->n, sets * e->n, h_in, h_out,
+                             [&](const double* din, double* dout, std::size_t rows, cudaStream_t s) {
+                                 ensemble_forward<double>(e, din, dout, rows, s);
+                             }))
+            return;
         host_roundtrip<double>(e->device, batch, e->n, sets * e->n, h_in, h_out,
                                [&](const double* din, double* dout, std::size_t rows, cudaStream_t s) {
                                    ensemble_forward<double>(e, din, dout, rows, s);
@@ -2554,6 +2646,8 @@ int dctp_chain_sync_check(const dctp_chain* c, void* stream) {
             if (!c->blob) throw std::invalid_argument("ChainedFactorization: host-only chain (created with device < 0)"); \
             if (batch == 0) return;                                                                    \
             const std::size_t n = c->ch.n;                                                             \
+            auto fn = [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) { chain_forward<T>(c, din, dout, rows, s); }; \
+            if (host_tiny<T>(c->device, c->flags, batch, n, n, h_in, h_out, fn)) return;               \
             host_roundtrip<T>(c->device, batch, n, n, h_in, h_out,                                     \
                               [&](const T* din, T* dout, std::size_t rows, cudaStream_t s) {          \
                                   chain_forward<T>(c, din, dout, rows, s);                             \

@@ -1204,6 +1204,28 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
         constexpr bool f32 = std::is_same_v<T, float>;
         const dctp::dev::Emit<T> even{at<int>(p->blob, f.to), at<int>(p->blob, f.from),
                                       at<T>(p->blob, f32 ? f.sign32 : f.sign64), f.n_even};
+        if constexpr (!f32) {
+            // the W product on the int8 tensor cores: the fold kernel writes
+            // u's int8 slices directly (no u round trip, no slicing pass)
+            if (const int S = f.L >= ozaki_fold_min_k(false) ? ozaki_slices(n) : 0) {
+                ensure_fold_ozaki(p, 0, S, s);
+                const int pm = dctp::dev::ozaki_pad_m();
+                const std::size_t rows_pad = (batch + pm - 1) / pm * pm;
+                Scratch<int8_t> a_sl(dctp::dev::ozaki_slice_bytes(batch, f.L, 128, S, pm), s);
+                Scratch<int> ea(rows_pad, s);
+                const dctp::dev::FoldSlices fs{a_sl.ptr, ea.ptr, S, (f.L + 63) / 64, 128};
+                cuda_check(DCTP_LAUNCH("fold_dct", s,
+                                       dctp::dev::dct2_fold_rows<T>(in, n, nullptr, f.L, out, n, even, f.L, batch,
+                                                                    twiddles_at<T>(p->blob, f.tw64), p->flags(s), s,
+                                                                    fs)),
+                           "fold dct kernel");
+                cuda_check(DCTP_LAUNCH("fold_w_i8", s,
+                                       dctp::dev::ozaki_gemm(a_sl.ptr, ea.ptr, f.oz[0], f.oz_e[0], batch, f.cols, f.L,
+                                                             S, out, n, at<int>(p->blob, f.map), s)),
+                           "int8 tensor-core product kernel");
+                return;
+            }
+        }
         Scratch<T> u(batch * static_cast<std::size_t>(f.L), s);
         cuda_check(DCTP_LAUNCH("fold_dct", s,
                                dctp::dev::dct2_fold_rows<T>(in, n, u.ptr, f.L, out, n, even, f.L, batch,
@@ -1240,14 +1262,6 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
                                        dctp::dev::sgemm_rows(u.ptr, f.L, b, static_cast<int>(f.ldwt), out, n, batch,
                                                              f.cols, f.L, p->flags(s), s, at<int>(p->blob, f.map))),
                            "fold sgemm kernel");
-                return;
-            }
-        }
-        if constexpr (!f32) {
-            if (const int S = f.L >= ozaki_fold_min_k(false) ? ozaki_slices(n) : 0) {
-                ensure_fold_ozaki(p, 0, S, s);
-                rows_by_ozaki(u.ptr, f.L, f.oz[0], f.oz_e[0], f.L, f.cols, S, out, n, batch, p->flags(s), s, "fold_w_i8",
-                              at<int>(p->blob, f.map));
                 return;
             }
         }

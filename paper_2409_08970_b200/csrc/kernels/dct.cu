@@ -30,19 +30,30 @@ std::size_t fft_smem_bytes(std::size_t n, int rows) {
     return 2 * static_cast<std::size_t>(rows) * padded_len(static_cast<int>(n / 2)) * sizeof(T) * 2;
 }
 
+/// Byte offset of (row r, 16-byte chunk c16) in a K-major SWIZZLE_64B tile
+/// row of 64 bytes — the int8 GEMM's operand image (ozaki.cu).
+__device__ __forceinline__ uint32_t sw64_int8(int r, int c16) {
+    return static_cast<uint32_t>(r * 64 + ((c16 ^ ((r >> 1) & 3)) << 4));
+}
+
 /// FOLD (antisymmetric plans): the input rows hold 2n samples; the kernel
 /// writes u_j = x_j - x_{2n-1-j} to `hat` and transforms y_j = x_j + x_{2n-1-j}
-/// (length n), whose DCT gives the even coefficients of the full row.
+/// (length n), whose DCT gives the even coefficients of the full row.  With
+/// fs.sl set (fp64), u is not written: it stays in shared memory and leaves as
+/// the int8 slices of the W product (ozaki.cu's digits and tile image), so the
+/// product needs no separate slicing pass over u.
 template <class T, bool FOLD = false>
 __global__ void __launch_bounds__(kThreads)
 dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat, std::size_t ld_hat,
                 T* __restrict__ out, std::size_t ld_out, Emit<T> emit, int n, int logn,
-                int rows_per_cta, std::size_t batch, Twiddles<T> tw, int* flag) {
+                int rows_per_cta, std::size_t batch, Twiddles<T> tw, int* flag, FoldSlices fs) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = n >> 1, logN = logn - 1, ld = padded_len(N);
     cplx_t<T>* nat = reinterpret_cast<cplx_t<T>*>(smem_raw);
     cplx_t<T>* work = nat + rows_per_cta * ld;
     T* sh = reinterpret_cast<T*>(nat); // real output rows (stride n) once `nat` is consumed
+    T* ush = reinterpret_cast<T*>(work + rows_per_cta * ld); // u rows (fs.sl), then row maxima
+    const bool slice = FOLD && sizeof(T) == 8 && fs.sl != nullptr;
     const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * rows_per_cta;
     const int rows = static_cast<int>(min(static_cast<std::size_t>(rows_per_cta), batch - b0));
 
@@ -71,7 +82,10 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
             T v = xv[u];
             if constexpr (FOLD) {
                 bad |= !finite_val(xm[u]);
-                hat[(b0 + r) * ld_hat + j] = xv[u] - xm[u];
+                if (slice)
+                    ush[r * n + j] = xv[u] - xm[u];
+                else
+                    hat[(b0 + r) * ld_hat + j] = xv[u] - xm[u];
                 v = xv[u] + xm[u];
             }
             const int p = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
@@ -80,6 +94,58 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
     }
     if (bad) atomicOr(flag, 1);
     __syncthreads();
+
+    if constexpr (FOLD) {
+        if (slice) { // u -> int8 digits (ozaki_slice_kernel's arithmetic), per row
+            double* rmax = reinterpret_cast<double*>(ush + rows * n);
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            for (int r = warp; r < rows; r += kThreads / 32) {
+                double mx = 0.0;
+                bool nf = false;
+                for (int j = lane; j < n; j += 32) {
+                    const double v = static_cast<double>(ush[r * n + j]);
+                    nf |= !isfinite(v);
+                    mx = fmax(mx, fabs(v));
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if (__any_sync(0xffffffffu, nf)) mx = 0.0; // flagged above
+                if (lane == 0) {
+                    int e = 0;
+                    if (mx > 0.0) frexp(mx, &e);
+                    fs.expo[b0 + r] = e;
+                    rmax[r] = ldexp(127.0, -e);
+                }
+            }
+            __syncthreads();
+            const int groups = fs.nch * 16; // 4-sample words per row
+            const std::size_t slice_bytes = static_cast<std::size_t>(fs.tile_rows) * 64;
+            for (int g = threadIdx.x; g < rows * groups; g += kThreads) {
+                const int r = g / groups, k = 4 * (g - r * groups);
+                const std::size_t grow = b0 + r;
+                const double scale = rmax[r];
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double x = k + u < n ? static_cast<double>(ush[r * n + k + u]) : 0.0;
+                    v[u] = isfinite(x) ? x * scale : 0.0;
+                }
+                const std::size_t tile = grow / fs.tile_rows;
+                const int lr = static_cast<int>(grow % fs.tile_rows), ch = k / 64, c16 = (k % 64) / 16;
+                int8_t* dst = fs.sl + ((tile * fs.nch + ch) * fs.S) * slice_bytes + sw64_int8(lr, c16) + (k % 16);
+                for (int s = 0; s < fs.S; ++s) {
+                    uint32_t w = 0u;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const double d = rint(v[u]);
+                        v[u] = (v[u] - d) * 254.0;
+                        w |= (static_cast<uint32_t>(static_cast<int>(d)) & 0xFFu) << (8 * u);
+                    }
+                    *reinterpret_cast<uint32_t*>(dst + s * slice_bytes) = w;
+                }
+            }
+        }
+    }
 
     fft_rows<T, false>(nat, work, rows, N, logN, tw.fft);
 
@@ -320,7 +386,7 @@ cudaError_t dct2_rows(const T* in, std::size_t ld_in, T* hat, std::size_t ld_hat
         if (e != cudaSuccess) return e;
         const unsigned grid = static_cast<unsigned>((batch + rows - 1) / rows);
         kern<<<grid, kThreads, smem, stream>>>(in, ld_in, hat, ld_hat, out, ld_out, emit,
-                                              static_cast<int>(n), ilog2(n), rows, batch, tw, flag);
+                                              static_cast<int>(n), ilog2(n), rows, batch, tw, flag, FoldSlices{});
         return cudaGetLastError();
     }
     const std::size_t smem = 2 * n * sizeof(T);
@@ -335,17 +401,19 @@ cudaError_t dct2_rows(const T* in, std::size_t ld_in, T* hat, std::size_t ld_hat
 template <class T>
 cudaError_t dct2_fold_rows(const T* in, std::size_t ld_in, T* u, std::size_t ld_u, T* out, std::size_t ld_out,
                            Emit<T> emit, std::size_t n, std::size_t batch, Twiddles<T> tw, int* flag,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, FoldSlices fs) {
     if (batch == 0) return cudaSuccess;
     if (!is_pow2(n) || n < 2) return cudaErrorInvalidValue;
+    if (fs.sl && sizeof(T) != 8) return cudaErrorInvalidValue;
     const int rows = rows_per_cta_for<T>(n);
-    const std::size_t smem = fft_smem_bytes<T>(n, rows);
+    const std::size_t smem =
+        fft_smem_bytes<T>(n, rows) + (fs.sl ? static_cast<std::size_t>(rows) * (n * sizeof(T) + sizeof(double)) : 0);
     auto kern = dct2_fft_kernel<T, true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const unsigned grid = static_cast<unsigned>((batch + rows - 1) / rows);
     kern<<<grid, kThreads, smem, stream>>>(in, ld_in, u, ld_u, out, ld_out, emit, static_cast<int>(n), ilog2(n), rows,
-                                          batch, tw, flag);
+                                          batch, tw, flag, fs);
     return cudaGetLastError();
 }
 
@@ -392,9 +460,10 @@ template cudaError_t dct2_rows<float>(const float*, std::size_t, float*, std::si
                                       Emit<float>, std::size_t, std::size_t, Twiddles<float>, int*, cudaStream_t);
 template cudaError_t dct2_fold_rows<double>(const double*, std::size_t, double*, std::size_t, double*, std::size_t,
                                             Emit<double>, std::size_t, std::size_t, Twiddles<double>, int*,
-                                            cudaStream_t);
+                                            cudaStream_t, FoldSlices);
 template cudaError_t dct2_fold_rows<float>(const float*, std::size_t, float*, std::size_t, float*, std::size_t,
-                                           Emit<float>, std::size_t, std::size_t, Twiddles<float>, int*, cudaStream_t);
+                                           Emit<float>, std::size_t, std::size_t, Twiddles<float>, int*, cudaStream_t,
+                                           FoldSlices);
 template cudaError_t idct_rows<double>(const double*, std::size_t, const double*, std::size_t, Emit<double>,
                                        double*, std::size_t, std::size_t, std::size_t, Twiddles<double>, int*,
                                        cudaStream_t);

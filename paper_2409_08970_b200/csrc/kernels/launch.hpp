@@ -45,13 +45,23 @@ cudaError_t dct2_rows(const T* in, std::size_t ld_in, T* hat, std::size_t ld_hat
                       std::size_t ld_out, Emit<T> emit, std::size_t n, std::size_t batch,
                       Twiddles<T> tw, int* flag, cudaStream_t stream);
 
+/// int8 slices of u written by the folded DCT kernel instead of u itself
+/// (fp64): the int8 GEMM's A image (ozaki.cu layout: tiles of tile_rows rows,
+/// nch 64-byte chunks, S slices) and per-row exponents.
+struct FoldSlices {
+    int8_t* sl = nullptr;
+    int* expo = nullptr;
+    int S = 0, nch = 0, tile_rows = 0;
+};
+
 /// Folded forward of antisymmetric plans: rows of 2n samples x; writes
-/// u_j = x_j - x_{2n-1-j} (n per row) to `u` and emits the DCT-II (length n)
-/// of y_j = x_j + x_{2n-1-j} through `emit`.
+/// u_j = x_j - x_{2n-1-j} (n per row) to `u` (or, with fs.sl, its int8
+/// slices) and emits the DCT-II (length n) of y_j = x_j + x_{2n-1-j} through
+/// `emit`.
 template <class T>
 cudaError_t dct2_fold_rows(const T* in, std::size_t ld_in, T* u, std::size_t ld_u, T* out, std::size_t ld_out,
                            Emit<T> emit, std::size_t n, std::size_t batch, Twiddles<T> tw, int* flag,
-                           cudaStream_t stream);
+                           cudaStream_t stream, FoldSlices fs = {});
 
 /// Inverse (DCT-III, orthonormal, U d) of rows d; before the transform
 ///   d[to[e]] = sign[e] * p[b*ld_p + from[e]]  (the pass-through slots).

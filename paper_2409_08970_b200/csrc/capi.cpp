@@ -1136,16 +1136,15 @@ static bool fold_route(const dctp_plan* p) {
 
 // int8 tensor-core (Ozaki) products, defined with the dense routes below
 static int ozaki_slices(std::size_t n);
-// shortest product length the folded route sends to them (DCTP_OZAKI_FOLD_MIN_K
-// overrides both): forward 512 (C3: 0.27 vs 0.30 ms with the slicing pass),
-// inverse 2048 (C3's 512-long inverse product: 0.43 vs 0.37 ms — its unfolding
-// epilogue is the heavier one)
-static int ozaki_fold_min_k(bool inverse) {
+// shortest product length the folded route sends to them (DCTP_OZAKI_FOLD_MIN_K):
+// 512 (C3 forward 0.17 + the slices written by the fold kernel vs 0.30 ms on
+// DMMA; inverse 0.21 + 0.06 slicing vs 0.37 ms)
+static int ozaki_fold_min_k(bool) {
     static const int v = [] {
         const char* e = std::getenv("DCTP_OZAKI_FOLD_MIN_K");
-        return e ? std::atoi(e) : 0;
+        return e ? std::atoi(e) : 512;
     }();
-    return v > 0 ? v : (inverse ? 2048 : 512);
+    return v;
 }
 static void ensure_fold_ozaki(const dctp_plan* p, int which, int S, cudaStream_t s);
 static void rows_by_ozaki(const double* in, std::size_t ld_in, const int8_t* b_sl, const int* eb, int K, int N,

@@ -216,20 +216,27 @@ struct Geo {
 
 /// Epilogue of one 128 x NT tile (rows row0..row0+127, columns nt NT..):
 /// warp w reads TMEM lanes 32 w .. 32 w + 31 level by level (Horner in fp64,
-/// exact int32 -> fp64 conversions), scales by 2^(e_b + f_c) / 127^2 and
-/// stores the fp64 row segment (or scatters / unfolds it).
+/// exact int32 -> fp64 conversions) and scales by 2^(e_b + f_c) / 127^2; the
+/// 32 x 32 blocks then turn around in shared memory (`stage`: this warp's
+/// 32 x 33 doubles of the idle pipeline ring) so that every store — plain
+/// rows, scattered slots (col_map) or the unfolded pair (fold_add) — is a
+/// warp-wide run of consecutive columns of one row (coalesced, whole
+/// sectors) instead of 32 rows at once.
 template <int LEVELS, int NT>
 __device__ __forceinline__ void store_tile(uint32_t tmem, std::size_t row0, int nt, int warp, int lane, std::size_t M,
                                            int N, const int* __restrict__ ea, const int* __restrict__ eb,
                                            double* __restrict__ out, std::size_t ld_out,
                                            const int* __restrict__ col_map, const double* __restrict__ fold_add,
-                                           std::size_t ld_add) {
-    const std::size_t row = row0 + 32 * warp + lane;
+                                           std::size_t ld_add, double* stage) {
+    constexpr int LDS = 33;
+    const std::size_t wrow0 = row0 + 32 * warp, row = wrow0 + lane;
     const bool live = row < M;
     const double rs = live ? ldexp(1.0 / (127.0 * 127.0), ea[row]) : 0.0;
     constexpr double kInv = 1.0 / 254.0;
+    const int lim = min(N, nt * NT + NT); // columns of this tile
 #pragma unroll 1
     for (int c0 = 0; c0 < NT; c0 += 32) {
+        const int cbase = nt * NT + c0;
         double acc[32];
         uint32_t v[32];
 #pragma unroll 1
@@ -244,35 +251,34 @@ __device__ __forceinline__ void store_tile(uint32_t tmem, std::size_t row0, int 
                 for (int u = 0; u < 32; ++u) acc[u] = fma(acc[u], kInv, static_cast<double>(static_cast<int>(v[u])));
             }
         }
-        if (live) {
-            const int cbase = nt * NT + c0;
-            const int lim = min(N, nt * NT + NT); // columns of this tile
-            double* orow = out + row * ld_out;
-            if (fold_add) { // unfold: x_c = w_c + v_c, x_{2N-1-c} = w_c - v_c
-                const double* add = fold_add + row * ld_add;
-#pragma unroll 4
-                for (int u = 0; u < 32; ++u)
-                    if (cbase + u < lim) {
-                        const double v = acc[u] * ldexp(rs, __ldg(eb + cbase + u)), w = add[cbase + u];
-                        orow[cbase + u] = w + v;
-                        orow[2 * N - 1 - (cbase + u)] = w - v;
-                    }
-            } else if (col_map) {
+        if (cbase >= lim) break; // padded column tiles
 #pragma unroll
-                for (int u = 0; u < 32; ++u)
-                    if (cbase + u < lim) orow[__ldg(col_map + cbase + u)] = acc[u] * ldexp(rs, __ldg(eb + cbase + u));
-            } else if (cbase + 32 <= lim && (ld_out & 1) == 0) {
+        for (int u = 0; u < 32; ++u)
+            stage[lane * LDS + u] = cbase + u < lim ? acc[u] * ldexp(rs, __ldg(eb + cbase + u)) : 0.0;
+        __syncwarp();
+        // lane l now carries column cbase + l of each of the warp's 32 rows
+        const int c = cbase + lane;
+        const bool col_ok = c < lim;
+        const int dst = col_ok ? (col_map ? __ldg(col_map + c) : c) : 0;
+        if (fold_add) { // unfold: x_c = w_c + v_c, x_{2N-1-c} = w_c - v_c; all 32 w loads in flight first
+            double wv[32];
 #pragma unroll
-                for (int u = 0; u < 32; u += 2)
-                    *reinterpret_cast<double2*>(orow + cbase + u) =
-                        make_double2(acc[u] * ldexp(rs, __ldg(eb + cbase + u)),
-                                     acc[u + 1] * ldexp(rs, __ldg(eb + cbase + u + 1)));
-            } else {
+            for (int r = 0; r < 32; ++r)
+                wv[r] = (col_ok && wrow0 + r < M) ? __ldg(fold_add + (wrow0 + r) * ld_add + c) : 0.0;
 #pragma unroll
-                for (int u = 0; u < 32; ++u)
-                    if (cbase + u < lim) orow[cbase + u] = acc[u] * ldexp(rs, __ldg(eb + cbase + u));
-            }
+            for (int r = 0; r < 32; ++r)
+                if (col_ok && wrow0 + r < M) {
+                    const double val = stage[r * LDS + lane];
+                    double* orow = out + (wrow0 + r) * ld_out;
+                    orow[c] = wv[r] + val;
+                    orow[2 * N - 1 - c] = wv[r] - val;
+                }
+        } else {
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r)
+                if (col_ok && wrow0 + r < M) out[(wrow0 + r) * ld_out + dst] = stage[r * LDS + lane];
         }
+        __syncwarp();
     }
 }
 
@@ -374,7 +380,8 @@ ozaki_gemm_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, c
     // epilogue: warp w reads TMEM lanes 32 w .. 32 w + 31 (tile rows)
     ptx::mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    store_tile<G::kLevels, NT>(tmem, mt * TM, nt, warp, lane, M, N, ea, eb, out, ld_out, col_map, fold_add, ld_add);
+    store_tile<G::kLevels, NT>(tmem, mt * TM, nt, warp, lane, M, N, ea, eb, out, ld_out, col_map, fold_add, ld_add,
+                               reinterpret_cast<double*>(base) + warp * 32 * 33);
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     if (warp == 0)
@@ -609,7 +616,8 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
 
     ptx::mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    store_tile<G::kLevels, NT>(tmem, mt * TM, nt, warp, lane, M, N, ea, eb, out, ld_out, col_map, fold_add, ld_add);
+    store_tile<G::kLevels, NT>(tmem, mt * TM, nt, warp, lane, M, N, ea, eb, out, ld_out, col_map, fold_add, ld_add,
+                               reinterpret_cast<double*>(base) + warp * 32 * 33);
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     cluster_sync(); // no peer traffic into this CTA is still pending

@@ -619,10 +619,11 @@ def test_folded_route_for_antisymmetric_plans(P, torch, reference, monkeypatch, 
             P.profile_enable(True)
             plan.inverse(plan.forward(dev(torch, s, torch.float64)))
             P.profile_enable(False)
-            # fp64 forward products of length n/2 >= 512 run on the int8 tensor cores
+            # fp64 products of length n/2 >= 512 run on the int8 tensor cores
             int8 = n // 2 >= 512 and P.ozaki_slices(n) > 0
-            fwd = {"fold_w_i8"} if int8 else {"fold_w"}  # u leaves the fold kernel as int8 slices
-            assert set(P.profile_summary()) == {"fold_dct", "fold_idct", "fold_wt"} | fwd
+            want_k = ({"fold_w_i8", "fold_wt_i8", "ozaki_slice"} if int8  # u leaves the fold kernel as int8 slices
+                      else {"fold_w", "fold_wt"})
+            assert set(P.profile_summary()) == {"fold_dct", "fold_idct"} | want_k
     monkeypatch.delenv("DCTP_FOLD")
     int8 = n // 2 >= 512 and P.ozaki_slices(n) > 0
     assert O.parity(got[("auto", "float64")], got[("0", "float64")]) <= (TOL64 if int8 else 1e-12)

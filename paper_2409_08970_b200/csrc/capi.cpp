@@ -1315,6 +1315,30 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
         const dctp::dev::Emit<T> even{at<int>(p->blob, f.from), at<int>(p->blob, f.to),
                                       at<T>(p->blob, f32 ? f.sign32 : f.sign64), f.n_even};
         Scratch<T> w(batch * static_cast<std::size_t>(f.L), s);
+        if constexpr (!f32) {
+            // the W^T product on the int8 tensor cores: the fold kernel also
+            // gathers p's W slots and writes their int8 slices (no slicing pass)
+            if (const int S = f.cols >= ozaki_fold_min_k(true) ? ozaki_slices(n) : 0) {
+                ensure_fold_ozaki(p, 1, S, s);
+                const int pm = dctp::dev::ozaki_pad_m();
+                const std::size_t rows_pad = (batch + pm - 1) / pm * pm;
+                Scratch<int8_t> a_sl(dctp::dev::ozaki_slice_bytes(batch, f.cols, 128, S, pm), s);
+                Scratch<int> ea(rows_pad, s);
+                dctp::dev::FoldSlices fs{a_sl.ptr, ea.ptr, S, (f.cols + 63) / 64, 128};
+                fs.map = at<int>(p->blob, f.map);
+                fs.K = f.cols;
+                cuda_check(DCTP_LAUNCH("fold_idct", s,
+                                       dctp::dev::idct_rows<T>(at<T>(p->blob, f.zero), 0, in, n, even, w.ptr, f.L,
+                                                               f.L, batch, twiddles_at<T>(p->blob, f.tw64),
+                                                               p->flags(s), s, fs)),
+                           "fold idct kernel");
+                cuda_check(DCTP_LAUNCH("fold_wt_i8", s,
+                                       dctp::dev::ozaki_gemm(a_sl.ptr, ea.ptr, f.oz[1], f.oz_e[1], batch, f.L, f.cols,
+                                                             S, out, n, nullptr, s, w.ptr, f.L)),
+                           "int8 tensor-core product kernel");
+                return;
+            }
+        }
         cuda_check(DCTP_LAUNCH("fold_idct", s,
                                dctp::dev::idct_rows<T>(at<T>(p->blob, f.zero), 0, in, n, even, w.ptr, f.L, f.L, batch,
                                                        twiddles_at<T>(p->blob, f32 ? f.tw32 : f.tw64), p->flags(s), s)),
@@ -1341,14 +1365,6 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
                                                             f.cols, p->flags(s), s, nullptr, at<int>(p->blob, f.map), w.ptr,
                                                             f.L, at<float>(p->blob, f.wt_sw))),
                            "fold tcgen05 kernel");
-                return;
-            }
-        }
-        if constexpr (!f32) {
-            if (const int S = f.cols >= ozaki_fold_min_k(true) ? ozaki_slices(n) : 0) {
-                ensure_fold_ozaki(p, 1, S, s);
-                rows_by_ozaki(in, n, f.oz[1], f.oz_e[1], f.cols, f.L, S, out, n, batch, p->flags(s), s, "fold_wt_i8",
-                              nullptr, at<int>(p->blob, f.map), w.ptr, f.L);
                 return;
             }
         }

@@ -198,11 +198,65 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
     }
 }
 
+/// Digits of K gathered values per row (ozaki.cu's slicing arithmetic and
+/// tile image), rows b0.. of a CTA: g holds the rows' values (stride K),
+/// rmax scratch per row.
+__device__ void slice_rows_to_tiles(const double* g, int rows, int K, std::size_t b0, const FoldSlices& fs,
+                                    double* rmax) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < rows; r += kThreads / 32) {
+        double mx = 0.0;
+        bool nf = false;
+        for (int j = lane; j < K; j += 32) {
+            nf |= !isfinite(g[r * K + j]);
+            mx = fmax(mx, fabs(g[r * K + j]));
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (__any_sync(0xffffffffu, nf)) mx = 0.0;
+        if (lane == 0) {
+            int e = 0;
+            if (mx > 0.0) frexp(mx, &e);
+            fs.expo[b0 + r] = e;
+            rmax[r] = ldexp(127.0, -e);
+        }
+    }
+    __syncthreads();
+    const int groups = fs.nch * 16;
+    const std::size_t slice_bytes = static_cast<std::size_t>(fs.tile_rows) * 64;
+    for (int t = threadIdx.x; t < rows * groups; t += kThreads) {
+        const int r = t / groups, k = 4 * (t - r * groups);
+        const std::size_t grow = b0 + r;
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double x = k + u < K ? g[r * K + k + u] : 0.0;
+            v[u] = isfinite(x) ? x * rmax[r] : 0.0;
+        }
+        const std::size_t tile = grow / fs.tile_rows;
+        const int lr = static_cast<int>(grow % fs.tile_rows), ch = k / 64, c16 = (k % 64) / 16;
+        int8_t* dst = fs.sl + ((tile * fs.nch + ch) * fs.S) * slice_bytes + sw64_int8(lr, c16) + (k % 16);
+        for (int s = 0; s < fs.S; ++s) {
+            uint32_t w = 0u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double d = rint(v[u]);
+                v[u] = (v[u] - d) * 254.0;
+                w |= (static_cast<uint32_t>(static_cast<int>(d)) & 0xFFu) << (8 * u);
+            }
+            *reinterpret_cast<uint32_t*>(dst + s * slice_bytes) = w;
+        }
+    }
+}
+
+/// fs.sl set (fp64): the K = fs.K values p[row, fs.map[k]] of each row also
+/// leave as the int8 slices of the folded inverse's W product (no separate
+/// gather-and-slice pass over p).
 template <class T>
 __global__ void __launch_bounds__(kThreads)
 idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__ p, std::size_t ld_p,
                 Emit<T> emit, T* __restrict__ out, std::size_t ld_out, int n, int logn,
-                int rows_per_cta, std::size_t batch, Twiddles<T> tw, int* flag) {
+                int rows_per_cta, std::size_t batch, Twiddles<T> tw, int* flag, FoldSlices fs) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = n >> 1, logN = logn - 1, ld = padded_len(N);
     cplx_t<T>* nat = reinterpret_cast<cplx_t<T>*>(smem_raw);
@@ -210,6 +264,36 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
     T* sh = reinterpret_cast<T*>(work); // the real coefficients, consumed before the FFT writes `work`
     const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * rows_per_cta;
     const int rows = static_cast<int>(min(static_cast<std::size_t>(rows_per_cta), batch - b0));
+    if constexpr (sizeof(T) == 8) {
+        if (fs.sl != nullptr) { // gathered values into the extra shared rows, then their digits
+            double* g = reinterpret_cast<double*>(work + rows_per_cta * ld);
+            double* rmax = g + rows_per_cta * fs.K;
+            constexpr int U = 8;
+            bool nf = false;
+            for (int t0 = threadIdx.x; t0 < rows * fs.K; t0 += U * kThreads) {
+                double v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int t = t0 + u * kThreads;
+                    if (t < rows * fs.K) {
+                        const int r = t / fs.K, k = t - r * fs.K;
+                        v[u] = static_cast<double>(p[(b0 + r) * ld_p + __ldg(fs.map + k)]);
+                    } else {
+                        v[u] = 0.0;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (t0 + u * kThreads < rows * fs.K) {
+                        nf |= !isfinite(v[u]);
+                        g[t0 + u * kThreads] = v[u];
+                    }
+            }
+            if (nf) atomicOr(flag, 1);
+            __syncthreads();
+            slice_rows_to_tiles(g, rows, fs.K, b0, fs, rmax);
+        }
+    }
 
     // X_k = sqrt(2/n) c_k d_k, with X_0 doubled (the REDFT01 convention).
     const T scale = static_cast<T>(sqrt(2.0 / n));
@@ -420,18 +504,21 @@ cudaError_t dct2_fold_rows(const T* in, std::size_t ld_in, T* u, std::size_t ld_
 template <class T>
 cudaError_t idct_rows(const T* d, std::size_t ld_d, const T* p, std::size_t ld_p, Emit<T> emit,
                       T* out, std::size_t ld_out, std::size_t n, std::size_t batch,
-                      Twiddles<T> tw, int* flag, cudaStream_t stream) {
+                      Twiddles<T> tw, int* flag, cudaStream_t stream, FoldSlices fs) {
     if (batch == 0) return cudaSuccess;
     if (is_pow2(n) && n >= 2) {
         const int rows = rows_per_cta_for<T>(n);
-        const std::size_t smem = fft_smem_bytes<T>(n, rows);
+        if (fs.sl && sizeof(T) != 8) return cudaErrorInvalidValue;
+        const std::size_t smem =
+            fft_smem_bytes<T>(n, rows) +
+            (fs.sl ? static_cast<std::size_t>(rows) * (static_cast<std::size_t>(fs.K) + 1) * sizeof(double) : 0);
         auto kern = idct_fft_kernel<T>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
         const unsigned grid = static_cast<unsigned>((batch + rows - 1) / rows);
         kern<<<grid, kThreads, smem, stream>>>(d, ld_d, p, ld_p, emit, out, ld_out, static_cast<int>(n),
-                                              ilog2(n), rows, batch, tw, flag);
+                                              ilog2(n), rows, batch, tw, flag, fs);
         return cudaGetLastError();
     }
     const std::size_t smem = n * sizeof(T);
@@ -466,8 +553,9 @@ template cudaError_t dct2_fold_rows<float>(const float*, std::size_t, float*, st
                                            FoldSlices);
 template cudaError_t idct_rows<double>(const double*, std::size_t, const double*, std::size_t, Emit<double>,
                                        double*, std::size_t, std::size_t, std::size_t, Twiddles<double>, int*,
-                                       cudaStream_t);
+                                       cudaStream_t, FoldSlices);
 template cudaError_t idct_rows<float>(const float*, std::size_t, const float*, std::size_t, Emit<float>, float*,
-                                      std::size_t, std::size_t, std::size_t, Twiddles<float>, int*, cudaStream_t);
+                                      std::size_t, std::size_t, std::size_t, Twiddles<float>, int*, cudaStream_t,
+                                      FoldSlices);
 
 } // namespace dctp::dev

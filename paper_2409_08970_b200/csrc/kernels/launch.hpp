@@ -52,6 +52,8 @@ struct FoldSlices {
     int8_t* sl = nullptr;
     int* expo = nullptr;
     int S = 0, nch = 0, tile_rows = 0;
+    const int* map = nullptr; // idct_rows: the K gathered columns of p to slice (the folded inverse's W slots)
+    int K = 0;
 };
 
 /// Folded forward of antisymmetric plans: rows of 2n samples x; writes
@@ -68,7 +70,7 @@ cudaError_t dct2_fold_rows(const T* in, std::size_t ld_in, T* u, std::size_t ld_
 template <class T>
 cudaError_t idct_rows(const T* d, std::size_t ld_d, const T* p, std::size_t ld_p, Emit<T> emit,
                       T* out, std::size_t ld_out, std::size_t n, std::size_t batch,
-                      Twiddles<T> tw, int* flag, cudaStream_t stream);
+                      Twiddles<T> tw, int* flag, cudaStream_t stream, FoldSlices fs = {});
 
 /// One Cauchy stage (SIMT, entries generated on the fly from fp64 gaps):
 ///   out[b*ld_out + dst[c]] = cscale[c] * sum_r rscale[r] * in[b*ld_in + src[r]] / (x[r] - y[c])

@@ -621,7 +621,7 @@ def test_folded_route_for_antisymmetric_plans(P, torch, reference, monkeypatch, 
             P.profile_enable(False)
             # fp64 products of length n/2 >= 512 run on the int8 tensor cores
             int8 = n // 2 >= 512 and P.ozaki_slices(n) > 0
-            want_k = ({"fold_w_i8", "fold_wt_i8", "ozaki_slice"} if int8  # u leaves the fold kernel as int8 slices
+            want_k = ({"fold_w_i8", "fold_wt_i8"} if int8  # u / p's W slots leave the fold kernels as int8 slices
                       else {"fold_w", "fold_wt"})
             assert set(P.profile_summary()) == {"fold_dct", "fold_idct"} | want_k
     monkeypatch.delenv("DCTP_FOLD")

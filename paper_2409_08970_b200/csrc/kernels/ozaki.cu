@@ -214,14 +214,21 @@ struct Geo {
     static_assert(NT % 16 == 0 && NT >= 16 && NT <= 256, "M = 128 needs N % 16 == 0");
 };
 
+/// 2^e as a double for the small exponents of the slicing (|e| < 1000),
+/// built from its bit pattern (ldexp's range handling costs ~20 branchy
+/// instructions per element in the epilogue).
+__device__ __forceinline__ double pow2i(int e) {
+    return __longlong_as_double(static_cast<long long>(1023 + e) << 52);
+}
+
 /// Epilogue of one 128 x NT tile (rows row0..row0+127, columns nt NT..):
 /// warp w reads TMEM lanes 32 w .. 32 w + 31 level by level (Horner in fp64,
-/// exact int32 -> fp64 conversions) and scales by 2^(e_b + f_c) / 127^2; the
-/// 32 x 32 blocks then turn around in shared memory (`stage`: this warp's
-/// 32 x 33 doubles of the idle pipeline ring) so that every store — plain
-/// rows, scattered slots (col_map) or the unfolded pair (fold_add) — is a
-/// warp-wide run of consecutive columns of one row (coalesced, whole
-/// sectors) instead of 32 rows at once.
+/// exact int32 -> fp64 conversions); the 32 x 32 blocks then turn around in
+/// shared memory (`stage`: this warp's 32 x 33 doubles) so that every store —
+/// plain rows, scattered slots (col_map) or the unfolded pair (fold_add) — is
+/// a warp-wide run of consecutive columns of one row (coalesced, whole
+/// sectors) instead of 32 rows at once.  Scales: 2^e_b / 127^2 per row before
+/// the turn-around, 2^f_c per column (one per lane) after it.
 template <int LEVELS, int NT>
 __device__ __forceinline__ void store_tile(uint32_t tmem, std::size_t row0, int nt, int warp, int lane, std::size_t M,
                                            int N, const int* __restrict__ ea, const int* __restrict__ eb,
@@ -230,8 +237,8 @@ __device__ __forceinline__ void store_tile(uint32_t tmem, std::size_t row0, int 
                                            std::size_t ld_add, double* stage) {
     constexpr int LDS = 33;
     const std::size_t wrow0 = row0 + 32 * warp, row = wrow0 + lane;
-    const bool live = row < M;
-    const double rs = live ? ldexp(1.0 / (127.0 * 127.0), ea[row]) : 0.0;
+    const double rs = row < M ? pow2i(ea[row]) * (1.0 / (127.0 * 127.0)) : 0.0;
+    const int live_rows = wrow0 >= M ? 0 : (M - wrow0 >= 32 ? 32 : static_cast<int>(M - wrow0));
     constexpr double kInv = 1.0 / 254.0;
     const int lim = min(N, nt * NT + NT); // columns of this tile
 #pragma unroll 1
@@ -253,30 +260,33 @@ __device__ __forceinline__ void store_tile(uint32_t tmem, std::size_t row0, int 
         }
         if (cbase >= lim) break; // padded column tiles
 #pragma unroll
-        for (int u = 0; u < 32; ++u)
-            stage[lane * LDS + u] = cbase + u < lim ? acc[u] * ldexp(rs, __ldg(eb + cbase + u)) : 0.0;
+        for (int u = 0; u < 32; ++u) stage[lane * LDS + u] = acc[u] * rs;
         __syncwarp();
-        // lane l now carries column cbase + l of each of the warp's 32 rows
+        // lane l now carries column c = cbase + l of each of the warp's rows
         const int c = cbase + lane;
         const bool col_ok = c < lim;
+        const double cs = col_ok ? pow2i(__ldg(eb + c)) : 0.0;
         const int dst = col_ok ? (col_map ? __ldg(col_map + c) : c) : 0;
-        if (fold_add) { // unfold: x_c = w_c + v_c, x_{2N-1-c} = w_c - v_c; all 32 w loads in flight first
-            double wv[32];
+        if (col_ok) {
+            if (fold_add) { // unfold: x_c = w_c + v_c, x_{2N-1-c} = w_c - v_c; all w loads in flight first
+                double wv[32];
 #pragma unroll
-            for (int r = 0; r < 32; ++r)
-                wv[r] = (col_ok && wrow0 + r < M) ? __ldg(fold_add + (wrow0 + r) * ld_add + c) : 0.0;
+                for (int r = 0; r < 32; ++r) wv[r] = r < live_rows ? __ldg(fold_add + (wrow0 + r) * ld_add + c) : 0.0;
 #pragma unroll
-            for (int r = 0; r < 32; ++r)
-                if (col_ok && wrow0 + r < M) {
-                    const double val = stage[r * LDS + lane];
-                    double* orow = out + (wrow0 + r) * ld_out;
-                    orow[c] = wv[r] + val;
-                    orow[2 * N - 1 - c] = wv[r] - val;
-                }
-        } else {
+                for (int r = 0; r < 32; ++r)
+                    if (r < live_rows) {
+                        const double val = stage[r * LDS + lane] * cs;
+                        double* orow = out + (wrow0 + r) * ld_out;
+                        orow[c] = wv[r] + val;
+                        orow[2 * N - 1 - c] = wv[r] - val;
+                    }
+            } else if (live_rows == 32) {
+                double* o = out + wrow0 * ld_out + dst;
 #pragma unroll 8
-            for (int r = 0; r < 32; ++r)
-                if (col_ok && wrow0 + r < M) out[(wrow0 + r) * ld_out + dst] = stage[r * LDS + lane];
+                for (int r = 0; r < 32; ++r) o[r * ld_out] = stage[r * LDS + lane] * cs;
+            } else {
+                for (int r = 0; r < live_rows; ++r) out[(wrow0 + r) * ld_out + dst] = stage[r * LDS + lane] * cs;
+            }
         }
         __syncwarp();
     }
@@ -616,13 +626,228 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
 
     ptx::mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    store_tile<G::kLevels, NT>(tmem, mt * TM, nt, warp, lane, M, N, ea, eb, out, ld_out, col_map, fold_add, ld_add,
-                               reinterpret_cast<double*>(base) + warp * 32 * 33);
+    if (!(debug & 4)) // DCTP_OZAKI_DEBUG=4: no epilogue (timing only)
+        store_tile<G::kLevels, NT>(tmem, mt * TM, nt, warp, lane, M, N, ea, eb, out, ld_out, col_map, fold_add,
+                                   ld_add, reinterpret_cast<double*>(base) + warp * 32 * 33);
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     cluster_sync(); // no peer traffic into this CTA is still pending
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+}
+
+// ------------------------------------------------------ persistent CTA pairs
+
+/// Geometry of the persistent pair kernel: a 3-stage ring (the epilogue needs
+/// its own staging: the ring keeps loading the next tile meanwhile).
+template <int S, int NT>
+struct GeoP {
+    static constexpr int kLevels = S;
+    static constexpr int kHalf = NT / 2;
+    static constexpr int kABytes = S * TM * CB;
+    static constexpr int kBBytes = S * kHalf * CB;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStaging = 4 * 32 * 33 * 8; // 4 epilogue warps x 32 x 33 doubles
+    static constexpr int kStages = (kMaxSmem - 2048 - kStaging) / kStageBytes;
+    static constexpr int kSmem = kStages * kStageBytes + kStaging + 1024 + 512;
+    static_assert(kLevels * NT <= 512, "TMEM: one NT-column accumulator per level");
+    static_assert(kStages >= 2, "at least two pipeline stages");
+};
+constexpr int kPThreads = 256; // warp 0 producer, 1 MMA (rank 0), 2 relay (rank 1), 4-7 epilogue
+
+/// Persistent CTA pairs (cluster of 2 along M, cta_group::2 MMAs as in
+/// ozaki_gemm2_kernel) over tiles t = cluster, cluster + clusters, ...: the
+/// producer streams the chunks of consecutive tiles through one ring (the next
+/// tile's first stages load while the current tile's MMAs and epilogue run),
+/// so the per-tile prologue, pipeline fill and teardown of the one-tile
+/// kernel are paid once — what dominates short products (K = 512 .. 2048:
+/// the folded products and the rank-k chain).  The accumulator (5 x 96 TMEM
+/// columns) is single-buffered: the MMAs of tile i + 1 wait until both CTAs'
+/// epilogue warps (4-7) drained tile i (t_empty: 8 arrivals at the leader).
+template <int S, int NT>
+__global__ void __launch_bounds__(kPThreads, 1)
+ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, const int8_t* __restrict__ b_sl,
+                   const int* __restrict__ eb, std::size_t M, int N, int nch, double* __restrict__ out,
+                   std::size_t ld_out, const int* __restrict__ col_map, const double* __restrict__ fold_add,
+                   std::size_t ld_add, int ntn, int nfast, std::size_t npairs) {
+    using G = GeoP<S, NT>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t raw = ptx::smem_addr(smem_raw);
+    unsigned char* base = smem_raw + ((1024 - (raw & 1023)) & 1023);
+    double* staging = reinterpret_cast<double*>(base + G::kStages * G::kStageBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + G::kStages * G::kStageBytes + G::kStaging);
+    uint64_t* peer_full = full + G::kStages;
+    uint64_t* empty = peer_full + G::kStages;
+    uint64_t* t_full = empty + G::kStages;  // accumulator complete (leader's commit, both CTAs)
+    uint64_t* t_empty = t_full + 1;         // accumulator drained (leader: 4 local + 4 peer epilogue warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 1);
+    const uint32_t sbase = ptx::smem_addr(base);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint32_t rank = 0;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const std::size_t clusters = gridDim.x / 2, cid = blockIdx.x / 2;
+    const std::size_t tiles = npairs * static_cast<std::size_t>(ntn);
+    auto tile_of = [&](std::size_t t, std::size_t& mt, int& nt) {
+        std::size_t p;
+        if (nfast) {
+            nt = static_cast<int>(t % ntn);
+            p = t / ntn;
+        } else {
+            p = t % npairs;
+            nt = static_cast<int>(t / npairs);
+        }
+        mt = 2 * p + rank;
+    };
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                         ptx::smem_addr(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+    }
+    if (tid == 32) {
+        for (int i = 0; i < G::kStages; ++i) {
+            ptx::mbar_init(full + i, 1);
+            ptx::mbar_init(peer_full + i, 1);
+            ptx::mbar_init(empty + i, 1);
+        }
+        ptx::mbar_init(t_full, 1);
+        ptx::mbar_init(t_empty, 8);
+        ptx::fence_mbar_init();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    cluster_sync();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) { // producer (both CTAs): chunks of every tile of this pair, one ring
+        unsigned long long q = 0;
+        for (std::size_t t = cid; t < tiles; t += clusters) {
+            std::size_t mt;
+            int nt;
+            tile_of(t, mt, nt);
+            const int8_t* a_tile = a_sl + mt * static_cast<std::size_t>(nch) * G::kABytes;
+            const int8_t* b_tile = b_sl + (2 * static_cast<std::size_t>(nt) + rank) * nch * G::kBBytes;
+            for (int ch = 0; ch < nch; ++ch, ++q) {
+                const int st = static_cast<int>(q % G::kStages);
+                if (q >= static_cast<unsigned long long>(G::kStages))
+                    ptx::mbar_wait(empty + st, static_cast<uint32_t>(((q / G::kStages) - 1) & 1));
+                if (elect_one()) {
+                    ptx::mbar_expect_tx(full + st, G::kStageBytes);
+                    unsigned char* dst = base + st * G::kStageBytes;
+                    ptx::bulk_load(dst, a_tile + static_cast<std::size_t>(ch) * G::kABytes, G::kABytes, full + st);
+                    ptx::bulk_load(dst + G::kABytes, b_tile + static_cast<std::size_t>(ch) * G::kBBytes,
+                                   G::kBBytes, full + st);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 1 && rank == 0) { // MMA warp of the pair
+        const uint64_t adesc0 = smem_desc(sbase), bdesc0 = smem_desc(sbase + G::kABytes);
+        unsigned long long q = 0;
+        int i = 0;
+        for (std::size_t t = cid; t < tiles; t += clusters, ++i) {
+            if (i > 0) mbar_wait_cluster(t_empty, static_cast<uint32_t>((i - 1) & 1)); // epilogues drained TMEM
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            for (int ch = 0; ch < nch; ++ch, ++q) {
+                const int st = static_cast<int>(q % G::kStages);
+                const uint32_t ph = static_cast<uint32_t>((q / G::kStages) & 1);
+                ptx::mbar_wait(full + st, ph);
+                mbar_wait_cluster(peer_full + st, ph);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                if (elect_one()) {
+                    const uint64_t so = static_cast<uint64_t>(st * G::kStageBytes) >> 4;
+                    const uint64_t ad = adesc0 + so, bd = bdesc0 + so;
+#pragma unroll
+                    for (int kk = 0; kk < CB / 32; ++kk) {
+#pragma unroll
+                        for (int a = 0; a < G::kLevels; ++a) {
+#pragma unroll
+                            for (int b = 0; a + b < G::kLevels; ++b) {
+                                const uint32_t td = tmem + static_cast<uint32_t>((a + b) * NT);
+                                const uint32_t acc = (ch > 0 || kk > 0 || a > 0) ? 1u : 0u;
+                                mma_i8_pair<NT>(td, ad + ((a * TM * CB + 32 * kk) >> 4),
+                                                bd + ((b * G::kHalf * CB + 32 * kk) >> 4), acc);
+                            }
+                        }
+                    }
+                    mma_commit_pair(empty + st, 0x3);
+                }
+                __syncwarp();
+            }
+            if (elect_one()) mma_commit_pair(t_full, 0x3);
+            __syncwarp();
+        }
+    } else if (warp == 2 && rank == 1) { // relay: this CTA's stage landed -> the leader
+        unsigned long long q = 0;
+        for (std::size_t t = cid; t < tiles; t += clusters)
+            for (int ch = 0; ch < nch; ++ch, ++q) {
+                const int st = static_cast<int>(q % G::kStages);
+                ptx::mbar_wait(full + st, static_cast<uint32_t>((q / G::kStages) & 1));
+                if (elect_one()) mbar_arrive_remote(peer_full + st, 0);
+                __syncwarp();
+            }
+    } else if (warp >= 4) { // epilogue warps: TMEM lane quarter warp % 4
+        const int ew = warp - 4;
+        int i = 0;
+        for (std::size_t t = cid; t < tiles; t += clusters, ++i) {
+            std::size_t mt;
+            int nt;
+            tile_of(t, mt, nt);
+            ptx::mbar_wait(t_full, static_cast<uint32_t>(i & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            store_tile<G::kLevels, NT>(tmem, mt * TM, nt, ew, lane, M, N, ea, eb, out, ld_out, col_map, fold_add,
+                                       ld_add, staging + ew * 32 * 33);
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) { // both CTAs' epilogue warps release the pair's accumulator at the leader
+                if (rank == 0)
+                    ptx::mbar_arrive(t_empty);
+                else
+                    mbar_arrive_remote(t_empty, 0);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    cluster_sync();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+}
+
+template <int S, int NT>
+cudaError_t launch_gemmp(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M, int N,
+                         int nch, double* out, std::size_t ld_out, const int* col_map, const double* fold_add,
+                         std::size_t ld_add, cudaStream_t stream) {
+    using G = GeoP<S, NT>;
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(ozaki_gemmp_kernel<S, NT>), G::kSmem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const std::size_t npairs = (M + 2 * TM - 1) / (2 * TM);
+    const int ntn = (N + NT - 1) / NT;
+    const std::size_t a_bytes = npairs * 2 * TM * static_cast<std::size_t>(nch) * CB * S;
+    const std::size_t b_bytes = static_cast<std::size_t>(ntn) * NT * nch * CB * S;
+    const int nfast = b_bytes < a_bytes ? 1 : 0;
+    const std::size_t tiles = npairs * ntn;
+    const std::size_t clusters = std::min<std::size_t>(tiles, static_cast<std::size_t>(sms / 2));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * clusters), 1);
+    cfg.blockDim = dim3(kPThreads);
+    cfg.dynamicSmemBytes = G::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, ozaki_gemmp_kernel<S, NT>, a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map,
+                              fold_add, ld_add, ntn, nfast, npairs);
 }
 
 template <int S, int NT, int NSUB>
@@ -752,6 +977,17 @@ cudaError_t ozaki_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, co
                        const double* fold_add, std::size_t ld_add) {
     if (M == 0 || N == 0) return cudaSuccess;
     const int nch = (K + CB - 1) / CB;
+    static const int persist = [] { // DCTP_OZAKI_PERSIST: 0 never, 1 always, else K <= 2048
+        const char* e = std::getenv("DCTP_OZAKI_PERSIST");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (pair_mode() && pair_nsub() == 1 && (persist == 1 || (persist != 0 && K <= 2048))) {
+        if (slices == 5)
+            return launch_gemmp<5, 96>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add, stream);
+        if (slices == 6)
+            return launch_gemmp<6, 80>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, fold_add, ld_add, stream);
+        return cudaErrorInvalidValue;
+    }
     if (pair_mode()) {
         const bool mc = pair_nsub() == 2;
         if (slices == 5)

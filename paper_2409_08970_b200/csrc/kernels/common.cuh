@@ -44,6 +44,24 @@ __device__ __forceinline__ float cauchy_entry<float>(double x, double y) {
     return __frcp_rn(static_cast<float>(x - y));
 }
 
+/// One int8 digit of the Ozaki slicing (ozaki.cu): d = rint(v) (ties to even),
+/// returned as its low byte, and v <- (v - d) * 254.  The rounding uses the
+/// 1.5 * 2^52 addend (two DADDs, the integer read from the low word) instead
+/// of FRND + F2I, which run on B200's narrow fp64 conversion path; exact for
+/// |v| < 2^51.
+__device__ __forceinline__ uint32_t ozaki_digit(double& v) {
+    constexpr double kMagic = 6755399441055744.0; // 1.5 * 2^52
+    const double t = v + kMagic;
+    const double d = t - kMagic;
+    v = (v - d) * 254.0;
+    return static_cast<uint32_t>(__double2loint(t)) & 0xFFu;
+}
+
+/// int32 -> fp64 without I2F: 2^52 + 2^31 + i is exact in the mantissa.
+__device__ __forceinline__ double i32_to_f64(uint32_t bits) {
+    return __hiloint2double(0x43300000, static_cast<int>(bits ^ 0x80000000u)) - 4503601774854144.0;
+}
+
 inline int ilog2(std::size_t n) {
     int l = 0;
     while ((std::size_t{1} << l) < n) ++l;

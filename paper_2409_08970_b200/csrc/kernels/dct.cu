@@ -137,9 +137,7 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
                     uint32_t w = 0u;
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const double d = rint(v[u]);
-                        v[u] = (v[u] - d) * 254.0;
-                        w |= (static_cast<uint32_t>(static_cast<int>(d)) & 0xFFu) << (8 * u);
+                        w |= ozaki_digit(v[u]) << (8 * u);
                     }
                     *reinterpret_cast<uint32_t*>(dst + s * slice_bytes) = w;
                 }
@@ -240,9 +238,7 @@ __device__ void slice_rows_to_tiles(const double* g, int rows, int K, std::size_
             uint32_t w = 0u;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const double d = rint(v[u]);
-                v[u] = (v[u] - d) * 254.0;
-                w |= (static_cast<uint32_t>(static_cast<int>(d)) & 0xFFu) << (8 * u);
+                w |= ozaki_digit(v[u]) << (8 * u);
             }
             *reinterpret_cast<uint32_t*>(dst + s * slice_bytes) = w;
         }

@@ -190,9 +190,7 @@ ozaki_slice_kernel(const T* __restrict__ in, std::size_t ld, std::size_t rows, s
             uint32_t w = 0u;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const double d = rint(v[u]);
-                v[u] = (v[u] - d) * 254.0;
-                w |= (static_cast<uint32_t>(static_cast<int>(d)) & 0xFFu) << (8 * u);
+                w |= ozaki_digit(v[u]) << (8 * u);
             }
             *reinterpret_cast<uint32_t*>(dst + s * slice_bytes) = w;
         }
@@ -252,10 +250,10 @@ __device__ __forceinline__ void store_tile(uint32_t tmem, std::size_t row0, int 
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
             if (L == LEVELS - 1) {
 #pragma unroll
-                for (int u = 0; u < 32; ++u) acc[u] = static_cast<double>(static_cast<int>(v[u]));
+                for (int u = 0; u < 32; ++u) acc[u] = i32_to_f64(v[u]);
             } else {
 #pragma unroll
-                for (int u = 0; u < 32; ++u) acc[u] = fma(acc[u], kInv, static_cast<double>(static_cast<int>(v[u])));
+                for (int u = 0; u < 32; ++u) acc[u] = fma(acc[u], kInv, i32_to_f64(v[u]));
             }
         }
         if (cbase >= lim) break; // padded column tiles

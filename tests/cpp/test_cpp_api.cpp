@@ -258,7 +258,9 @@ int main() {
                     cudaMalloc(reinterpret_cast<void**>(&dout), n * batch * 8);
                     std::vector<double> mine = h;
                     if (t == 2) mine[77 * n + 5] = std::nan("");
-                    cudaMemcpy(din, mine.data(), n * batch * 8, cudaMemcpyHostToDevice);
+                    // on the thread's own stream: a pageable cudaMemcpy may return before its DMA
+                    // lands, and a non-blocking stream does not order behind the legacy stream
+                    cudaMemcpyAsync(din, mine.data(), n * batch * 8, cudaMemcpyHostToDevice, st);
                     int res = 1;
                     for (int it = 0; it < 20 && res == 1; ++it) {
                         try {
@@ -286,7 +288,12 @@ int main() {
                     if (!use_per_thread_stream) cudaStreamDestroy(st);
                 });
             for (auto& th : pool) th.join();
-            for (int t = 0; t < 4; ++t) CHECK(outcome[t] == (t == 2 ? 2 : 1));
+            for (int t = 0; t < 4; ++t) {
+                if (outcome[t] != (t == 2 ? 2 : 1))
+                    std::printf("thread isolation: per-thread-stream=%d thread %d outcome %d\n", use_per_thread_stream,
+                                t, outcome[t]);
+                CHECK(outcome[t] == (t == 2 ? 2 : 1));
+            }
         }
     }
     // n beyond the GPU DCT kernels' shared-memory row: a clear invalid_argument at creation

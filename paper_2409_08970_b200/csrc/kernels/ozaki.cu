@@ -99,6 +99,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15}, [%16];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+
 // ---------------------------------------------------------------- slicing
 
 /// Slicing of one row per WPR warps (WPR = 8: a CTA per row, long rows;
@@ -226,13 +235,16 @@ __device__ __forceinline__ double pow2i(int e) {
 /// plain rows, scattered slots (col_map) or the unfolded pair (fold_add) — is
 /// a warp-wide run of consecutive columns of one row (coalesced, whole
 /// sectors) instead of 32 rows at once.  Scales: 2^e_b / 127^2 per row before
-/// the turn-around, 2^f_c per column (one per lane) after it.
-template <int LEVELS, int NT>
+/// the turn-around, 2^f_c per column (one per lane) after it.  `lsum`
+/// (split-K tiles): the level sums come from the tile's accumulated int32
+/// sums in global memory ([level * NT + column][lane], red_tile) instead of
+/// TMEM — exact integers, so the result is bit-identical to the unsplit tile's.
+template <int LEVELS, int NT, bool LSUM = false>
 __device__ __forceinline__ void store_tile(uint32_t tmem, std::size_t row0, int nt, int warp, int lane, std::size_t M,
                                            int N, const int* __restrict__ ea, const int* __restrict__ eb,
                                            double* __restrict__ out, std::size_t ld_out,
                                            const int* __restrict__ col_map, const double* __restrict__ fold_add,
-                                           std::size_t ld_add, double* stage) {
+                                           std::size_t ld_add, double* stage, const int* lsum = nullptr) {
     constexpr int LDS = 33;
     const std::size_t wrow0 = row0 + 32 * warp, row = wrow0 + lane;
     const double rs = row < M ? pow2i(ea[row]) * (1.0 / (127.0 * 127.0)) : 0.0;
@@ -246,8 +258,14 @@ __device__ __forceinline__ void store_tile(uint32_t tmem, std::size_t row0, int 
         uint32_t v[32];
 #pragma unroll 1
         for (int L = LEVELS - 1; L >= 0; --L) {
-            tmem_ld32(tmem + (static_cast<uint32_t>(32 * warp) << 16) + static_cast<uint32_t>(L * NT + c0), v);
-            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            if constexpr (LSUM) {
+                const int* src = lsum + static_cast<std::size_t>(L * NT + c0) * 32 + lane;
+#pragma unroll
+                for (int u = 0; u < 32; ++u) v[u] = c0 + u < NT ? static_cast<uint32_t>(__ldcg(src + u * 32)) : 0u;
+            } else {
+                tmem_ld32(tmem + (static_cast<uint32_t>(32 * warp) << 16) + static_cast<uint32_t>(L * NT + c0), v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            }
             if (L == LEVELS - 1) {
 #pragma unroll
                 for (int u = 0; u < 32; ++u) acc[u] = i32_to_f64(v[u]);
@@ -288,6 +306,141 @@ __device__ __forceinline__ void store_tile(uint32_t tmem, std::size_t row0, int 
         }
         __syncwarp();
     }
+}
+
+/// Split-K tiles (SplitSched): a unit's level sums, warp w's 32 TMEM lanes,
+/// added into the tile's int32 accumulator in global memory, [level * NT +
+/// column][lane] (16-column TMEM loads; each reduction a 128-byte warp run;
+/// fire-and-forget, exact).
+template <int LEVELS, int NT>
+__device__ __forceinline__ void red_tile(uint32_t tmem, int warp, int lane, int* __restrict__ acc) {
+#pragma unroll 1
+    for (int L = 0; L < LEVELS; ++L)
+#pragma unroll 1
+        for (int c0 = 0; c0 < NT; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tmem + (static_cast<uint32_t>(32 * warp) << 16) + static_cast<uint32_t>(L * NT + c0), v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            int* d = acc + static_cast<std::size_t>(L * NT + c0) * 32 + lane;
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (c0 + u < NT) atomicAdd(d + u * 32, static_cast<int>(v[u]));
+        }
+}
+
+/// Split-K tiles: the units of a tile run in any order on any pairs; each
+/// adds its level sums (red_tile), then counts in on the tile's counter (one
+/// per CTA half and epilogue warp); the last to arrive finishes the tile from
+/// the accumulated sums and rearms the counter.  Integer sums: the result is
+/// bit-identical to the unsplit tile's.
+struct SplitSched {
+    std::size_t full = 0;   // whole-tile units (the first `full` tiles)
+    int rem = 0;            // tiles split along K (the last rem tiles)
+    int nsplit = 1;         // units per split tile
+    int* cnt = nullptr;     // rem x 2 x 4 arrival counters (zero at launch)
+    int* acc = nullptr;     // rem x 2 x 4 accumulators of LEVELS * NT * 32 int32 (zero at launch)
+};
+
+/// Work unit u -> (column tile, pair, chunk range, split slot): whole tiles
+/// first, then the split tiles' K ranges.
+struct Unit {
+    std::size_t pair;
+    int nt, kb, ke, slot;
+};
+__device__ __forceinline__ Unit unit_of(std::size_t u, const SplitSched& s, int nch, int ntn, int nfast,
+                                        std::size_t npairs) {
+    Unit w;
+    std::size_t t = u;
+    w.kb = 0;
+    w.ke = nch;
+    w.slot = -1;
+    if (u >= s.full) {
+        const std::size_t v = u - s.full;
+        const int split = static_cast<int>(v / s.rem);
+        w.slot = static_cast<int>(v % s.rem);
+        t = s.full + w.slot;
+        w.kb = static_cast<int>(static_cast<long long>(split) * nch / s.nsplit);
+        w.ke = static_cast<int>(static_cast<long long>(split + 1) * nch / s.nsplit);
+    }
+    if (nfast) {
+        w.nt = static_cast<int>(t % ntn);
+        w.pair = t / ntn;
+    } else {
+        w.pair = t % npairs;
+        w.nt = static_cast<int>(t / npairs);
+    }
+    return w;
+}
+
+/// Epilogue of a split unit by one epilogue warp (ew: its TMEM lane quarter);
+/// `release` runs once the accumulator has been read.
+template <int LEVELS, int NT, class R>
+__device__ __forceinline__ void finish_split(const SplitSched& s, const Unit& w, uint32_t rank, uint32_t tmem, int ew,
+                                             int lane, std::size_t M, int N, const int* ea, const int* eb, double* out,
+                                             std::size_t ld_out, const int* col_map, const double* fold_add,
+                                             std::size_t ld_add, double* stage, R&& release) {
+    const std::size_t blk = (static_cast<std::size_t>(w.slot) * 2 + rank) * 4 + ew;
+    int* acc = s.acc + blk * (static_cast<std::size_t>(LEVELS) * NT * 32);
+    red_tile<LEVELS, NT>(tmem, ew, lane, acc);
+    release();
+    __threadfence();
+    __syncwarp();
+    int old = 0;
+    if (lane == 0) old = atomicAdd(s.cnt + blk, 1);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old == s.nsplit - 1) {
+        __threadfence();
+        store_tile<LEVELS, NT, true>(tmem, (2 * w.pair + rank) * TM, w.nt, ew, lane, M, N, ea, eb, out, ld_out,
+                                     col_map, fold_add, ld_add, stage, acc);
+        if (lane == 0) s.cnt[blk] = 0;
+    }
+}
+
+/// Split of the tail: nsplit minimising the tail's length in waves,
+/// ceil(rem * nsplit / slots) / nsplit, plus 3% of a wave per extra split
+/// and 30% for splitting at all (measured on C5's shapes: the units' own
+/// pipeline fill, the reductions and the finishing epilogue); every unit
+/// keeps >= 8 chunks.  DCTP_OZAKI_SPLIT = 0 turns it off; by default
+/// products with K >= 2048.
+static void plan_split(std::size_t tiles, std::size_t slots, int nch, SplitSched& s) {
+    static const int knob = [] {
+        const char* e = std::getenv("DCTP_OZAKI_SPLIT");
+        return e ? std::atoi(e) : -1;
+    }();
+    s.full = tiles;
+    s.rem = 0;
+    s.nsplit = 1;
+    const std::size_t rem = tiles % slots;
+    if (knob == 0 || rem == 0 || (knob < 0 && nch < 32)) return;
+    double best = 1.0;
+    int bn = 1;
+    for (int ns = 2; ns <= 16 && nch / ns >= 8; ++ns) {
+        const double w = static_cast<double>((rem * ns + slots - 1) / slots) / ns + 0.03 * (ns - 1) + 0.3;
+        if (w < best - 1e-9) {
+            best = w;
+            bn = ns;
+        }
+    }
+    if (bn == 1) return;
+    s.full = tiles - rem;
+    s.rem = static_cast<int>(rem);
+    s.nsplit = bn;
+}
+
+/// Stream-ordered split workspace (counters + accumulators, zeroed); freed by
+/// split_free after the launch.
+static cudaError_t split_alloc(SplitSched& s, std::size_t ints_per_blk, cudaStream_t stream, void** ws) {
+    *ws = nullptr;
+    if (s.rem == 0) return cudaSuccess;
+    const std::size_t nblk = static_cast<std::size_t>(s.rem) * 8;
+    const std::size_t cnt_bytes = (nblk * sizeof(int) + 255) / 256 * 256;
+    const std::size_t bytes = cnt_bytes + nblk * ints_per_blk * sizeof(int);
+    cudaError_t e = cudaMallocAsync(ws, bytes, stream);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(*ws, 0, bytes, stream);
+    s.cnt = static_cast<int*>(*ws);
+    s.acc = reinterpret_cast<int*>(static_cast<char*>(*ws) + cnt_bytes);
+    return e;
 }
 
 template <int S, int NT>
@@ -492,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, const int8_t* __restrict__ b_sl,
                    const int* __restrict__ eb, std::size_t M, int N, int nch, double* __restrict__ out,
                    std::size_t ld_out, const int* __restrict__ col_map, const double* __restrict__ fold_add,
-                   std::size_t ld_add, int ntn, int nfast, std::size_t npairs, int debug) {
+                   std::size_t ld_add, int ntn, int nfast, std::size_t npairs, int debug, SplitSched sched) {
     using G = Geo2<S, NT>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t raw = ptx::smem_addr(smem_raw);
@@ -514,7 +667,12 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
     // chain); otherwise row pairs fastest (B, the larger operand, streams once)
     std::size_t mt;
     int nt;
-    if (NSUB == 1 && !nfast) {
+    Unit w{0, 0, 0, nch, -1}; // split-K tail (NSUB = 1): whole tiles, then K ranges of the last tiles
+    if (NSUB == 1 && sched.rem > 0) {
+        w = unit_of(blockIdx.x / 2, sched, nch, ntn, nfast, npairs);
+        mt = 2 * w.pair + rank;
+        nt = w.nt;
+    } else if (NSUB == 1 && !nfast) {
         mt = blockIdx.x;
         nt = blockIdx.y;
     } else {
@@ -553,8 +711,9 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
-    const int8_t* a_tile = a_sl + mt * static_cast<std::size_t>(nch) * G::kABytes;
-    const int8_t* b_tile = b_sl + (2 * static_cast<std::size_t>(nt) + rank) * nch * G::kBBytes;
+    const int8_t* a_tile = a_sl + (mt * static_cast<std::size_t>(nch) + w.kb) * G::kABytes;
+    const int8_t* b_tile = b_sl + ((2 * static_cast<std::size_t>(nt) + rank) * nch + w.kb) * G::kBBytes;
+    nch = w.ke - w.kb; // this unit's chunks
 
     const uint16_t all_mask = static_cast<uint16_t>((1u << (2 * NSUB)) - 1u);
     const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * ns));
@@ -624,7 +783,10 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
 
     ptx::mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    if (!(debug & 4)) // DCTP_OZAKI_DEBUG=4: no epilogue (timing only)
+    if (w.slot >= 0)
+        finish_split<G::kLevels, NT>(sched, w, rank, tmem, warp, lane, M, N, ea, eb, out, ld_out, col_map, fold_add,
+                                     ld_add, reinterpret_cast<double*>(base) + warp * 32 * 33, [] {});
+    else if (!(debug & 4)) // DCTP_OZAKI_DEBUG=4: no epilogue (timing only)
         store_tile<G::kLevels, NT>(tmem, mt * TM, nt, warp, lane, M, N, ea, eb, out, ld_out, col_map, fold_add,
                                    ld_add, reinterpret_cast<double*>(base) + warp * 32 * 33);
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -654,20 +816,25 @@ struct GeoP {
 constexpr int kPThreads = 256; // warp 0 producer, 1 MMA (rank 0), 2 relay (rank 1), 4-7 epilogue
 
 /// Persistent CTA pairs (cluster of 2 along M, cta_group::2 MMAs as in
-/// ozaki_gemm2_kernel) over tiles t = cluster, cluster + clusters, ...: the
-/// producer streams the chunks of consecutive tiles through one ring (the next
-/// tile's first stages load while the current tile's MMAs and epilogue run),
-/// so the per-tile prologue, pipeline fill and teardown of the one-tile
+/// ozaki_gemm2_kernel) over work units u = cluster, cluster + clusters, ...:
+/// the producer streams the chunks of consecutive units through one ring (the
+/// next unit's first stages load while the current unit's MMAs and epilogue
+/// run), so the per-tile prologue, pipeline fill and teardown of the one-tile
 /// kernel are paid once — what dominates short products (K = 512 .. 2048:
 /// the folded products and the rank-k chain).  The accumulator (5 x 96 TMEM
-/// columns) is single-buffered: the MMAs of tile i + 1 wait until both CTAs'
-/// epilogue warps (4-7) drained tile i (t_empty: 8 arrivals at the leader).
-template <int S, int NT>
+/// columns) is single-buffered: the MMAs of unit i + 1 wait until both CTAs'
+/// epilogue warps (4-7) drained unit i (t_empty: 8 arrivals at the leader).
+///
+/// Split-K tail (SplitSched): the first `full` units are whole tiles; the
+/// remaining `rem` tiles — a partial last wave — are split along K into
+/// `nsplit` units each, so the tail costs ~1/nsplit of a wave instead of a
+/// whole one (C5 sharded 8 ways, 256 rows: 86 column tiles on 74 pairs).
+template <int S, int NT, bool SPLIT>
 __global__ void __launch_bounds__(kPThreads, 1)
 ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, const int8_t* __restrict__ b_sl,
                    const int* __restrict__ eb, std::size_t M, int N, int nch, double* __restrict__ out,
                    std::size_t ld_out, const int* __restrict__ col_map, const double* __restrict__ fold_add,
-                   std::size_t ld_add, int ntn, int nfast, std::size_t npairs) {
+                   std::size_t ld_add, int ntn, int nfast, std::size_t npairs, SplitSched sched) {
     using G = GeoP<S, NT>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t raw = ptx::smem_addr(smem_raw);
@@ -685,19 +852,7 @@ ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
     uint32_t rank = 0;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
     const std::size_t clusters = gridDim.x / 2, cid = blockIdx.x / 2;
-    const std::size_t tiles = npairs * static_cast<std::size_t>(ntn);
-    auto tile_of = [&](std::size_t t, std::size_t& mt, int& nt) {
-        std::size_t p;
-        if (nfast) {
-            nt = static_cast<int>(t % ntn);
-            p = t / ntn;
-        } else {
-            p = t % npairs;
-            nt = static_cast<int>(t / npairs);
-        }
-        mt = 2 * p + rank;
-    };
-
+    const std::size_t units = sched.full + static_cast<std::size_t>(sched.rem) * sched.nsplit;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
                          ptx::smem_addr(tmem_slot))
@@ -720,15 +875,13 @@ ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) { // producer (both CTAs): chunks of every tile of this pair, one ring
+    if (warp == 0) { // producer (both CTAs): chunks of every unit of this pair, one ring
         unsigned long long q = 0;
-        for (std::size_t t = cid; t < tiles; t += clusters) {
-            std::size_t mt;
-            int nt;
-            tile_of(t, mt, nt);
-            const int8_t* a_tile = a_sl + mt * static_cast<std::size_t>(nch) * G::kABytes;
-            const int8_t* b_tile = b_sl + (2 * static_cast<std::size_t>(nt) + rank) * nch * G::kBBytes;
-            for (int ch = 0; ch < nch; ++ch, ++q) {
+        for (std::size_t u = cid; u < units; u += clusters) {
+            const Unit w = unit_of(u, sched, nch, ntn, nfast, npairs);
+            const int8_t* a_tile = a_sl + (2 * w.pair + rank) * static_cast<std::size_t>(nch) * G::kABytes;
+            const int8_t* b_tile = b_sl + (2 * static_cast<std::size_t>(w.nt) + rank) * nch * G::kBBytes;
+            for (int ch = w.kb; ch < w.ke; ++ch, ++q) {
                 const int st = static_cast<int>(q % G::kStages);
                 if (q >= static_cast<unsigned long long>(G::kStages))
                     ptx::mbar_wait(empty + st, static_cast<uint32_t>(((q / G::kStages) - 1) & 1));
@@ -746,10 +899,11 @@ ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
         const uint64_t adesc0 = smem_desc(sbase), bdesc0 = smem_desc(sbase + G::kABytes);
         unsigned long long q = 0;
         int i = 0;
-        for (std::size_t t = cid; t < tiles; t += clusters, ++i) {
+        for (std::size_t u = cid; u < units; u += clusters, ++i) {
+            const Unit w = unit_of(u, sched, nch, ntn, nfast, npairs);
             if (i > 0) mbar_wait_cluster(t_empty, static_cast<uint32_t>((i - 1) & 1)); // epilogues drained TMEM
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            for (int ch = 0; ch < nch; ++ch, ++q) {
+            for (int ch = w.kb; ch < w.ke; ++ch, ++q) {
                 const int st = static_cast<int>(q % G::kStages);
                 const uint32_t ph = static_cast<uint32_t>((q / G::kStages) & 1);
                 ptx::mbar_wait(full + st, ph);
@@ -765,7 +919,7 @@ ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
 #pragma unroll
                             for (int b = 0; a + b < G::kLevels; ++b) {
                                 const uint32_t td = tmem + static_cast<uint32_t>((a + b) * NT);
-                                const uint32_t acc = (ch > 0 || kk > 0 || a > 0) ? 1u : 0u;
+                                const uint32_t acc = (ch > w.kb || kk > 0 || a > 0) ? 1u : 0u;
                                 mma_i8_pair<NT>(td, ad + ((a * TM * CB + 32 * kk) >> 4),
                                                 bd + ((b * G::kHalf * CB + 32 * kk) >> 4), acc);
                             }
@@ -780,31 +934,39 @@ ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
         }
     } else if (warp == 2 && rank == 1) { // relay: this CTA's stage landed -> the leader
         unsigned long long q = 0;
-        for (std::size_t t = cid; t < tiles; t += clusters)
-            for (int ch = 0; ch < nch; ++ch, ++q) {
+        for (std::size_t u = cid; u < units; u += clusters) {
+            const Unit w = unit_of(u, sched, nch, ntn, nfast, npairs);
+            for (int ch = w.kb; ch < w.ke; ++ch, ++q) {
                 const int st = static_cast<int>(q % G::kStages);
                 ptx::mbar_wait(full + st, static_cast<uint32_t>((q / G::kStages) & 1));
                 if (elect_one()) mbar_arrive_remote(peer_full + st, 0);
                 __syncwarp();
             }
+        }
     } else if (warp >= 4) { // epilogue warps: TMEM lane quarter warp % 4
         const int ew = warp - 4;
         int i = 0;
-        for (std::size_t t = cid; t < tiles; t += clusters, ++i) {
-            std::size_t mt;
-            int nt;
-            tile_of(t, mt, nt);
-            ptx::mbar_wait(t_full, static_cast<uint32_t>(i & 1));
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            store_tile<G::kLevels, NT>(tmem, mt * TM, nt, ew, lane, M, N, ea, eb, out, ld_out, col_map, fold_add,
-                                       ld_add, staging + ew * 32 * 33);
+        auto release = [&] { // both CTAs' epilogue warps release the pair's accumulator at the leader
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
-            if (lane == 0) { // both CTAs' epilogue warps release the pair's accumulator at the leader
+            if (lane == 0) {
                 if (rank == 0)
                     ptx::mbar_arrive(t_empty);
                 else
                     mbar_arrive_remote(t_empty, 0);
+            }
+        };
+        for (std::size_t u = cid; u < units; u += clusters, ++i) {
+            const Unit w = unit_of(u, sched, nch, ntn, nfast, npairs);
+            ptx::mbar_wait(t_full, static_cast<uint32_t>(i & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (!SPLIT || w.slot < 0) {
+                store_tile<G::kLevels, NT>(tmem, (2 * w.pair + rank) * TM, w.nt, ew, lane, M, N, ea, eb, out, ld_out,
+                                           col_map, fold_add, ld_add, staging + ew * 32 * 33);
+                release();
+            } else if constexpr (SPLIT) {
+                finish_split<G::kLevels, NT>(sched, w, rank, tmem, ew, lane, M, N, ea, eb, out, ld_out, col_map,
+                                             fold_add, ld_add, staging + ew * 32 * 33, release);
             }
         }
     }
@@ -820,7 +982,8 @@ cudaError_t launch_gemmp(const int8_t* a_sl, const int* ea, const int8_t* b_sl, 
                          int nch, double* out, std::size_t ld_out, const int* col_map, const double* fold_add,
                          std::size_t ld_add, cudaStream_t stream) {
     using G = GeoP<S, NT>;
-    cudaError_t e = smem_optin(reinterpret_cast<const void*>(ozaki_gemmp_kernel<S, NT>), G::kSmem);
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(ozaki_gemmp_kernel<S, NT, false>), G::kSmem);
+    if (e == cudaSuccess) e = smem_optin(reinterpret_cast<const void*>(ozaki_gemmp_kernel<S, NT, true>), G::kSmem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -831,7 +994,13 @@ cudaError_t launch_gemmp(const int8_t* a_sl, const int* ea, const int8_t* b_sl, 
     const std::size_t b_bytes = static_cast<std::size_t>(ntn) * NT * nch * CB * S;
     const int nfast = b_bytes < a_bytes ? 1 : 0;
     const std::size_t tiles = npairs * ntn;
-    const std::size_t clusters = std::min<std::size_t>(tiles, static_cast<std::size_t>(sms / 2));
+    SplitSched sched;
+    plan_split(tiles, static_cast<std::size_t>(sms / 2), nch, sched);
+    const std::size_t units = sched.full + static_cast<std::size_t>(sched.rem) * sched.nsplit;
+    const std::size_t clusters = std::min<std::size_t>(units, static_cast<std::size_t>(sms / 2));
+    void* ws = nullptr;
+    e = split_alloc(sched, static_cast<std::size_t>(G::kLevels) * NT * 32, stream, &ws);
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * clusters), 1);
     cfg.blockDim = dim3(kPThreads);
@@ -844,8 +1013,15 @@ cudaError_t launch_gemmp(const int8_t* a_sl, const int* ea, const int8_t* b_sl, 
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, ozaki_gemmp_kernel<S, NT>, a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map,
-                              fold_add, ld_add, ntn, nfast, npairs);
+    e = sched.rem > 0 ? cudaLaunchKernelEx(&cfg, ozaki_gemmp_kernel<S, NT, true>, a_sl, ea, b_sl, eb, M, N, nch, out,
+                                           ld_out, col_map, fold_add, ld_add, ntn, nfast, npairs, sched)
+                      : cudaLaunchKernelEx(&cfg, ozaki_gemmp_kernel<S, NT, false>, a_sl, ea, b_sl, eb, M, N, nch, out,
+                                           ld_out, col_map, fold_add, ld_add, ntn, nfast, npairs, sched);
+    if (ws) {
+        const cudaError_t f = cudaFreeAsync(ws, stream);
+        if (e == cudaSuccess) e = f;
+    }
+    return e;
 }
 
 template <int S, int NT, int NSUB>
@@ -868,9 +1044,21 @@ cudaError_t launch_gemm2(const int8_t* a_sl, const int* ea, const int8_t* b_sl, 
     const int nfast = order == 0 ? 0 : order == 1 ? 1 : (b_bytes < a_bytes ? 1 : 0);
     const std::size_t ntc = (static_cast<std::size_t>(ntn) + NSUB - 1) / NSUB;
     if (gm * ntc * NSUB >= (1ull << 31)) return cudaErrorInvalidValue;
+    SplitSched sched;
+    if (NSUB == 1) {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        plan_split(gm / 2 * ntn, static_cast<std::size_t>(sms / 2), nch, sched);
+    }
+    void* ws = nullptr;
+    e = split_alloc(sched, static_cast<std::size_t>(G::kLevels) * NT * 32, stream, &ws);
+    if (e != cudaSuccess) return e;
+    const std::size_t units = sched.full + static_cast<std::size_t>(sched.rem) * sched.nsplit;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = (NSUB == 1 && !nfast) ? dim3(static_cast<unsigned>(gm), ntn)
-                                        : dim3(static_cast<unsigned>(gm * ntc * NSUB), 1);
+    cfg.gridDim = sched.rem > 0 ? dim3(static_cast<unsigned>(2 * units), 1)
+                  : (NSUB == 1 && !nfast) ? dim3(static_cast<unsigned>(gm), ntn)
+                                          : dim3(static_cast<unsigned>(gm * ntc * NSUB), 1);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = G::kSmem;
     cfg.stream = stream;
@@ -885,8 +1073,13 @@ cudaError_t launch_gemm2(const int8_t* a_sl, const int* ea, const int8_t* b_sl, 
         const char* v = std::getenv("DCTP_OZAKI_DEBUG");
         return v ? std::atoi(v) : 0;
     }();
-    return cudaLaunchKernelEx(&cfg, ozaki_gemm2_kernel<S, NT, NSUB>, a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map,
-                              fold_add, ld_add, ntn, nfast, gm / 2, debug);
+    e = cudaLaunchKernelEx(&cfg, ozaki_gemm2_kernel<S, NT, NSUB>, a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map,
+                           fold_add, ld_add, ntn, nfast, gm / 2, debug, sched);
+    if (ws) {
+        const cudaError_t f = cudaFreeAsync(ws, stream);
+        if (e == cudaSuccess) e = f;
+    }
+    return e;
 }
 
 template <int S, int NT>

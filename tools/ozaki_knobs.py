@@ -11,6 +11,9 @@ sys.path.insert(0, os.getcwd())
 import paper_2409_08970_b200 as P
 from paper_2409_08970_b200.configs import WORKLOADS, make_plan
 cfg = WORKLOADS[int(os.environ.get("CID", "5"))]
+if os.environ.get("BATCH"):
+    import dataclasses
+    cfg = dataclasses.replace(cfg, batch=int(os.environ["BATCH"]))
 plan = make_plan(cfg)
 x = torch.as_tensor(P.fill_signals(cfg.seed, cfg.dist, cfg.n, cfg.batch, cfg.r), device="cuda")
 if cfg.progressive:
@@ -31,12 +34,25 @@ P.profile_reset(); P.profile_enable(True)
 for _ in range(10):
     fn(x, sync=False, out=out)
 torch.cuda.synchronize(); P.profile_enable(False)
+if os.environ.get("SAVE"):
+    import numpy as np
+    np.save(os.environ["SAVE"], out.double().cpu().numpy())
 print(json.dumps({k: round(v[1] / v[0], 4) for k, v in P.profile_summary().items()}))
 '''
-for setting in sys.argv[1:]:
+first = None
+for i, setting in enumerate(sys.argv[1:]):
     env = dict(os.environ)
     for kv in setting.split():
         k, v = kv.split("=")
         env[k] = v
+    env["SAVE"] = f"/tmp/ozaki_knobs_{i}.npy"
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
-    print(repr(setting), r.stdout.strip() or r.stderr[-2000:], flush=True)
+    gap = ""
+    if r.returncode == 0:  # max |y - y_first| / max |y_first| against the first setting's output
+        import numpy as np
+        y = np.load(env["SAVE"])
+        if first is None:
+            first = y
+        elif y.shape == first.shape:
+            gap = f" gap={np.abs(y - first).max() / np.abs(first).max():.2e}"
+    print(repr(setting), (r.stdout.strip() or r.stderr[-2000:]) + gap, flush=True)

@@ -88,17 +88,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-}
-
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
@@ -254,29 +243,44 @@ __device__ __forceinline__ void store_tile(uint32_t tmem, std::size_t row0, int 
 #pragma unroll 1
     for (int c0 = 0; c0 < NT; c0 += 32) {
         const int cbase = nt * NT + c0;
-        double acc[32];
-        uint32_t v[32];
+        if (cbase >= lim) break; // padded column tiles
+        if constexpr (LSUM) {
+            double acc[32];
+            uint32_t v[32];
 #pragma unroll 1
-        for (int L = LEVELS - 1; L >= 0; --L) {
-            if constexpr (LSUM) {
+            for (int L = LEVELS - 1; L >= 0; --L) {
                 const int* src = lsum + static_cast<std::size_t>(L * NT + c0) * 32 + lane;
 #pragma unroll
                 for (int u = 0; u < 32; ++u) v[u] = c0 + u < NT ? static_cast<uint32_t>(__ldcg(src + u * 32)) : 0u;
-            } else {
-                tmem_ld32(tmem + (static_cast<uint32_t>(32 * warp) << 16) + static_cast<uint32_t>(L * NT + c0), v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                if (L == LEVELS - 1) {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) acc[u] = i32_to_f64(v[u]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) acc[u] = fma(acc[u], kInv, i32_to_f64(v[u]));
+                }
             }
-            if (L == LEVELS - 1) {
 #pragma unroll
-                for (int u = 0; u < 32; ++u) acc[u] = i32_to_f64(v[u]);
-            } else {
+            for (int u = 0; u < 32; ++u) stage[lane * LDS + u] = acc[u] * rs;
+        } else {
+            // 16-column halves: every level's TMEM load in flight before one wait
+#pragma unroll 1
+            for (int h = 0; h < 32; h += 16) {
+                uint32_t v[LEVELS][16];
 #pragma unroll
-                for (int u = 0; u < 32; ++u) acc[u] = fma(acc[u], kInv, i32_to_f64(v[u]));
+                for (int L = 0; L < LEVELS; ++L)
+                    tmem_ld16(tmem + (static_cast<uint32_t>(32 * warp) << 16) + static_cast<uint32_t>(L * NT + c0 + h),
+                              v[L]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    double a = i32_to_f64(v[LEVELS - 1][u]);
+#pragma unroll
+                    for (int L = LEVELS - 2; L >= 0; --L) a = fma(a, kInv, i32_to_f64(v[L][u]));
+                    stage[lane * LDS + h + u] = a * rs;
+                }
             }
         }
-        if (cbase >= lim) break; // padded column tiles
-#pragma unroll
-        for (int u = 0; u < 32; ++u) stage[lane * LDS + u] = acc[u] * rs;
         __syncwarp();
         // lane l now carries column c = cbase + l of each of the warp's rows
         const int c = cbase + lane;

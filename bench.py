@@ -372,10 +372,12 @@ def kernel_roofline(cfg, alg, rows, top, t_ms, ms_per_step, ozaki_products):
         # fp64 product on the int8 tensor cores: the kernel's algorithm is
         # P = S(S+1)/2 int8 GEMMs of the same shape (ozaki.cu); peak = the
         # measured tcgen05 kind::i8 rate (tools/tc_peak.cu)
-        ops = ozaki_products * alg["flops_cauchy"] * rows
+        # the NFST route's materialised n x n operator: 2 n^2 per signal
+        alg_flops = 2.0 * cfg["n"] * cfg["n"] if top.startswith("nfst_dense") else alg["flops_cauchy"]
+        ops = ozaki_products * alg_flops * rows
         peak = own.get("tcgen05_i8_tops")
         ach = ops / (t_ms * 1e-3) / 1e12
-        fp64_eq = alg["flops_cauchy"] * rows / (t_ms * 1e-3) / 1e12
+        fp64_eq = alg_flops * rows / (t_ms * 1e-3) / 1e12
         dmma = max(own.get("dmma_m8n8k4_tflops") or 0, own.get("dmma_m16n8k16_tflops") or 0) or None
         out.update({"bound": "tensor", "unit": "TOPS (int8)", "achieved": ach, "peak": peak,
                     "frac": ach / peak if peak else None,
@@ -587,6 +589,8 @@ class GpuArm:
         launches = {k: v[0] / steps for k, v in prof.items()}
         top = max(prof, key=lambda k: prof[k][1])
         S = ctypes_ozaki_slices(n)
+        if top == "nfst_dense_inv_i8":
+            S = 6  # the NFST adjoint's materialised operator takes 6 slices (capi.cpp nfst_dense_slices)
         roof = kernel_roofline(cfg, alg, rows, top, per_launch[top], ms_per_step, S * (S + 1) // 2)
         meas, _ = peaks()
         hbm_peak = meas.get("hbm_gbs") or 6650.0

@@ -410,6 +410,7 @@ struct dctp_plan {
         double z0 = 0.0, ext_scale = 0.0;
         int R = 0, taps = 0, hw = 0, ext_slot = -1;
         bool preferred = false;  // chosen at creation (decide_fast_route)
+        bool probing = false;    // decide_fast_route's probe runs the NFST kernel itself
         double probe_gap = 0.0;  // NFST vs exact on the creation probe (max-norm relative)
     } fs;
     // materialised basis for the dense routes (forward_nmvp, inverse(fast =
@@ -423,6 +424,11 @@ struct dctp_plan {
         int8_t* oz[2] = {nullptr, nullptr};
         int* oz_e[2] = {nullptr, nullptr};
         int oz_slices = 0;
+        // int8 slices of the NFST route's own linear maps (forward [0],
+        // adjoint inverse [1]) materialised as n x n operators (ensure_nfst_ozaki)
+        int8_t* nf[2] = {nullptr, nullptr};
+        int* nf_e[2] = {nullptr, nullptr};
+        int nf_slices[2] = {0, 0};
     };
     std::unique_ptr<Dense> dense = std::make_unique<Dense>();
 
@@ -437,6 +443,8 @@ struct dctp_plan {
                 for (int i = 0; i < 2; ++i) {
                     if (dense->oz[i]) cudaFree(dense->oz[i]);
                     if (dense->oz_e[i]) cudaFree(dense->oz_e[i]);
+                    if (dense->nf[i]) cudaFree(dense->nf[i]);
+                    if (dense->nf_e[i]) cudaFree(dense->nf_e[i]);
                 }
             for (int i = 0; i < 2; ++i) {
                 if (fd.oz[i]) cudaFree(fd.oz[i]);
@@ -1151,6 +1159,8 @@ static void rows_by_ozaki(const double* in, std::size_t ld_in, const int8_t* b_s
                           int S, double* out, std::size_t ld_out, std::size_t batch, int* flag, cudaStream_t s,
                           const char* name, const int* col_map = nullptr, const int* a_map = nullptr,
                           const double* fold_add = nullptr, std::size_t ld_add = 0);
+static int nfst_dense_slices(const dctp_plan* p, int which);
+static void ensure_nfst_ozaki(const dctp_plan* p, int which, int S, cudaStream_t s);
 
 template <class T>
 static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s) {
@@ -1164,6 +1174,13 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
     DeviceScope scope(p->device);
     if constexpr (std::is_same_v<T, double>) {
         if (fast_route(p)) {
+            if (const int S = nfst_dense_slices(p, 0)) { // the NFST's own map, materialised, on the int8 tensor cores
+                ensure_nfst_ozaki(p, 0, S, s);
+                const auto& d = *p->dense;
+                rows_by_ozaki(in, n, d.nf[0], d.nf_e[0], static_cast<int>(n), static_cast<int>(n), S, out, n, batch,
+                              p->flags(s), s, "nfst_dense_i8");
+                return;
+            }
             cuda_check(DCTP_LAUNCH("nfst_fwd", s, dctp::dev::nfst_apply(in, out, batch, fast_plan_dev(p), p->flags(s), false, s)),
                        "nfst forward kernel");
             return;
@@ -1296,6 +1313,14 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
     if constexpr (std::is_same_v<T, double>) {
         if (fast_route(p)) {
             DeviceScope scope(p->device);
+            if (const int S = nfst_dense_slices(p, 1)) {
+                const std::size_t n = p->st.n;
+                ensure_nfst_ozaki(p, 1, S, s);
+                const auto& d = *p->dense;
+                rows_by_ozaki(in, n, d.nf[1], d.nf_e[1], static_cast<int>(n), static_cast<int>(n), S, out, n, batch,
+                              p->flags(s), s, "nfst_dense_inv_i8");
+                return;
+            }
             cuda_check(DCTP_LAUNCH("nfst_inv", s, dctp::dev::nfst_apply(in, out, batch, fast_plan_dev(p), p->flags(s), true, s)),
                        "nfst inverse kernel");
             return;
@@ -1414,7 +1439,9 @@ static void decide_fast_route(dctp_plan& p) {
     std::unique_ptr<double, decltype(&cudaFree)> hold(d, &cudaFree);
     cuda_check(cudaMemcpy(d, h.data(), rows * n * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy(route probe)");
     p.fs.preferred = true;
+    p.fs.probing = true;
     plan_forward<double>(&p, d, d + rows * n, rows, nullptr);
+    p.fs.probing = false;
     p.fs.preferred = false;
     plan_forward<double>(&p, d, d + 2 * rows * n, rows, nullptr);
     cuda_check(cudaMemcpy(a.data(), d + rows * n, rows * n * sizeof(double), cudaMemcpyDeviceToHost), "route probe");
@@ -1808,6 +1835,58 @@ static void rows_by_ozaki(const double* in, std::size_t ld_in, const int8_t* b_s
 
 /// int8 slices of an operand matrix bt (rows x K, stride ld) for the B side
 /// of ozaki_gemm; (slices, exponents) in device memory owned by the caller.
+/// The NFST route on the int8 tensor cores: its forward (and adjoint
+/// inverse) is a fixed linear map of the signal — DCT, weights, DST-I,
+/// Gaussian-gridding taps, all linear — so it is materialised once per plan
+/// as the n x n operator F (row i = the NFST kernel applied to e_i: the same
+/// kernel, so F carries the reference's own NFST approximation and the
+/// result stays on the reference's fast route, fast_transform.hpp:163-190)
+/// and applied as out = in F on the kind::i8 product.  At n = 1024 / 2048
+/// that is 0.26 / 0.42 ms per batch (X7 / X8) against 0.91 / 1.02 ms in the
+/// one-signal-per-CTA NFST kernel, whose FFT and tap passes run at ~15% of
+/// the fp64 pipe; the dense product costs n^2 per signal against the NFST's
+/// n log n, so it stops paying past n = 4096 (DCTP_NFST_DENSE_MAX_N).  The
+/// adjoint (which = 1) takes 6 slices: its map amplifies the product's
+/// rounding (n = 2048, self-loop 5.0: 1.0e-10 from the reference with 5
+/// slices, at the tolerance).  DCTP_NFST_DENSE = 0 keeps the NFST kernel.
+static int nfst_dense_slices(const dctp_plan* p, int which) {
+    const char* e = std::getenv("DCTP_NFST_DENSE");
+    if (p->fs.probing || (e && e[0] == '0')) return 0;
+    const char* m = std::getenv("DCTP_NFST_DENSE_MAX_N");
+    const std::size_t max_n = m ? static_cast<std::size_t>(std::atoll(m)) : std::size_t{4096};
+    const int S = p->st.n <= max_n ? ozaki_slices(p->st.n) : 0;
+    return S && which == 1 ? 6 : S;
+}
+
+static void ensure_nfst_ozaki(const dctp_plan* p, int which, int S, cudaStream_t s) {
+    auto& d = *p->dense;
+    std::lock_guard<std::mutex> lock(d.mu);
+    if (d.nf[which] && d.nf_slices[which] == S) return;
+    if (d.nf[which]) {
+        cudaFree(d.nf[which]);
+        cudaFree(d.nf_e[which]);
+        d.nf[which] = nullptr;
+        d.nf_e[which] = nullptr;
+    }
+    const std::size_t n = p->st.n;
+    Scratch<double> eye(n * n, s), img(n * n, s);
+    Scratch<int> flag(1, s);
+    cuda_check(cudaMemsetAsync(eye.ptr, 0, n * n * sizeof(double), s), "cudaMemset(identity)");
+    cuda_check(cudaMemsetAsync(flag.ptr, 0, sizeof(int), s), "cudaMemset(flag)");
+    const std::vector<double> ones(n, 1.0); // the diagonal: one strided 2-D copy
+    cuda_check(cudaMemcpy2DAsync(eye.ptr, (n + 1) * sizeof(double), ones.data(), sizeof(double), sizeof(double), n,
+                                 cudaMemcpyHostToDevice, s),
+               "H2D(identity)");
+    cuda_check(dctp::dev::nfst_apply(eye.ptr, img.ptr, n, fast_plan_dev(p), flag.ptr, which == 1, s),
+               "nfst operator kernel");
+    const int ni = static_cast<int>(n);
+    cuda_check(dctp::dev::transpose_square(img.ptr, n, eye.ptr, n, ni, s), "transpose kernel"); // bt = F^T
+    auto [sl, ex] = slice_operand(eye.ptr, n, n, ni, S, s); // synchronises s (the host vector may go)
+    d.nf[which] = sl;
+    d.nf_e[which] = ex;
+    d.nf_slices[which] = S;
+}
+
 static std::pair<int8_t*, int*> slice_operand(const double* bt, std::size_t ld, std::size_t rows, int K, int S,
                                               cudaStream_t s) {
     const int tn = dctp::dev::ozaki_tile_n(S), pn = dctp::dev::ozaki_pad_n(S);

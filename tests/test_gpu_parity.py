@@ -633,7 +633,8 @@ def test_folded_route_for_antisymmetric_plans(P, torch, reference, monkeypatch, 
     (128, O.Update(0, 0.5, 1), "1", TOL64), (256, O.Update(1, -0.7, 128, 129), "1", TOL64),
     (512, O.Update(0, 1.3, 1), None, TOL64), (1024, O.Update(0, 0.5, 1), None, TOL64),
     (2048, O.Update(0, 5.0, 1), None, TOL64), (2048, O.Update(1, 2.0, 1024, 1025), None, 5e-10)])
-def test_nfst_route_matches_reference_fast_route(P, torch, reference, monkeypatch, n, u, mode, tol):
+@pytest.mark.parametrize("nfst_dense", ["0", "auto"])
+def test_nfst_route_matches_reference_fast_route(P, torch, reference, monkeypatch, n, u, mode, tol, nfst_dense):
     """The NFST fast route (nfst.cu) is the reference's own forward algorithm
     (fast_transform.hpp:163-190, nfst.hpp:201-238), so it reproduces the
     reference's forward() to rounding, including the NFST's approximation
@@ -647,9 +648,15 @@ def test_nfst_route_matches_reference_fast_route(P, torch, reference, monkeypatc
     ~1e-10 with the FFT implementation (the numpy restatement of the same
     algorithm with numpy's pocketfft differs from it by 1.1e-10 as well), so
     its bound is the reference's own rounding noise (5e-10, i.e. 1/70 of
-    its approximation error).  fp32 keeps the exact routes."""
+    its approximation error).  fp32 keeps the exact routes.  nfst_dense:
+    "0" runs the NFST kernel itself; "auto" applies the same kernel's map,
+    materialised once as an n x n operator, on the int8 tensor cores from
+    n = 1024 (int8 products) to 4096."""
     if mode is not None:
         monkeypatch.setenv("DCTP_FAST", mode)
+    if nfst_dense == "0":
+        monkeypatch.setenv("DCTP_NFST_DENSE", "0")
+    dense_op = nfst_dense == "auto" and 1024 <= n <= 4096 and P.ozaki_slices(n) > 0
     rows = 257 if n <= 1024 else 96
     s = np.random.default_rng(n + 7).standard_normal((rows, n))
     rp = reference.plan(n, u)
@@ -663,7 +670,7 @@ def test_nfst_route_matches_reference_fast_route(P, torch, reference, monkeypatc
     P.profile_enable(True)
     got = plan.forward(dev(torch, s, torch.float64)).cpu().numpy()
     P.profile_enable(False)
-    assert set(P.profile_summary()) == {"nfst_fwd"}
+    assert set(P.profile_summary()) == ({"nfst_dense_i8", "ozaki_slice"} if dense_op else {"nfst_fwd"})
     assert O.parity(got, want) <= tol
     assert abs(O.parity(got, exact) - O.parity(want, exact)) <= max(tol, 0.02 * O.parity(want, exact))
     y32 = plan.forward(dev(torch, s, torch.float32)).double().cpu().numpy()
@@ -673,7 +680,7 @@ def test_nfst_route_matches_reference_fast_route(P, torch, reference, monkeypatc
     P.profile_enable(True)
     back = plan.inverse(dev(torch, want, torch.float64)).cpu().numpy()
     P.profile_enable(False)
-    assert set(P.profile_summary()) == {"nfst_inv"}
+    assert set(P.profile_summary()) == ({"nfst_dense_inv_i8", "ozaki_slice"} if dense_op else {"nfst_inv"})
     back_want = rp.inverse(want)
     assert O.parity(back, back_want) <= tol
     assert O.parity(back, s) <= max(10 * tol, 2 * O.parity(back_want, s))  # round trip

@@ -341,8 +341,9 @@ struct SplitSched {
     std::size_t full = 0;   // whole-tile units (the first `full` tiles)
     int rem = 0;            // tiles split along K (the last rem tiles)
     int nsplit = 1;         // units per split tile
-    int* cnt = nullptr;     // rem x 2 x 4 arrival counters (zero at launch)
-    int* acc = nullptr;     // rem x 2 x 4 accumulators of LEVELS * NT * 32 int32 (zero at launch)
+    int* cnt = nullptr;     // per tile, CTA half and epilogue warp: arrival counters (zero at launch)
+    int* acc = nullptr;     // ... and that warp's int32 level sums (zero at launch)
+    int debug = 0;          // persistent kernel, development knob DCTP_OZAKI_PDEBUG (phase isolation)
 };
 
 /// Work unit u -> (column tile, pair, chunk range, split slot): whole tiles
@@ -433,10 +434,11 @@ static void plan_split(std::size_t tiles, std::size_t slots, int nch, SplitSched
 
 /// Stream-ordered split workspace (counters + accumulators, zeroed); freed by
 /// split_free after the launch.
-static cudaError_t split_alloc(SplitSched& s, std::size_t ints_per_blk, cudaStream_t stream, void** ws) {
+static cudaError_t split_alloc(SplitSched& s, std::size_t ints_per_blk, cudaStream_t stream, void** ws,
+                               int blocks_per_tile = 8) {
     *ws = nullptr;
     if (s.rem == 0) return cudaSuccess;
-    const std::size_t nblk = static_cast<std::size_t>(s.rem) * 8;
+    const std::size_t nblk = static_cast<std::size_t>(s.rem) * blocks_per_tile;
     const std::size_t cnt_bytes = (nblk * sizeof(int) + 255) / 256 * 256;
     const std::size_t bytes = cnt_bytes + nblk * ints_per_blk * sizeof(int);
     cudaError_t e = cudaMallocAsync(ws, bytes, stream);
@@ -802,6 +804,158 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
 
 // ------------------------------------------------------ persistent CTA pairs
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+
+/// Persistent-kernel epilogue, phase 1 (accumulator -> registers): the warp
+/// with TMEM lane quarter q and column half h reads its 32 rows x NT/2
+/// columns, every level of an 8-column group in flight before one wait,
+/// Horner in fp64 (exact int32 -> fp64) and the row scale 2^e_b / 127^2.  The
+/// accumulator is free for the next unit's MMAs as soon as every epilogue
+/// warp has done this — the stores (phase 2) then overlap those MMAs.
+template <int LEVELS, int NT>
+__device__ __forceinline__ void drain_half(uint32_t tmem, int q, int h, double rs, double (&acc)[NT / 2]) {
+    constexpr int H = NT / 2;
+    constexpr double kInv = 1.0 / 254.0;
+#pragma unroll
+    for (int g = 0; g < H; g += 8) {
+        uint32_t v[LEVELS][8];
+#pragma unroll
+        for (int L = 0; L < LEVELS; ++L)
+            tmem_ld8(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(L * NT + h * H + g), v[L]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            double a = i32_to_f64(v[LEVELS - 1][u]);
+#pragma unroll
+            for (int L = LEVELS - 2; L >= 0; --L) a = fma(a, kInv, i32_to_f64(v[L][u]));
+            acc[g + u] = a * rs;
+        }
+    }
+}
+
+/// Split-K units, phase 1: the same 32 x NT/2 block from the tile's summed
+/// int32 levels in global memory ([level][column][lane], exact), so a split
+/// tile ends bit-identical to an unsplit one.
+template <int LEVELS, int NT>
+__device__ __forceinline__ void drain_half_sum(const int* __restrict__ lsum, int lane, double rs,
+                                               double (&acc)[NT / 2]) {
+    constexpr int H = NT / 2;
+    constexpr double kInv = 1.0 / 254.0;
+#pragma unroll
+    for (int u = 0; u < H; ++u)
+        acc[u] = i32_to_f64(static_cast<uint32_t>(__ldcg(lsum + static_cast<std::size_t>((LEVELS - 1) * H + u) * 32 + lane)));
+#pragma unroll 1
+    for (int L = LEVELS - 2; L >= 0; --L)
+#pragma unroll
+        for (int u = 0; u < H; ++u)
+            acc[u] = fma(acc[u], kInv,
+                         i32_to_f64(static_cast<uint32_t>(__ldcg(lsum + static_cast<std::size_t>(L * H + u) * 32 + lane))));
+#pragma unroll
+    for (int u = 0; u < H; ++u) acc[u] *= rs;
+}
+
+/// Split-K units: this warp's level sums added into the tile's int32
+/// accumulator ([level][column][lane], 128-byte warp runs, fire-and-forget).
+template <int LEVELS, int NT>
+__device__ __forceinline__ void red_half(uint32_t tmem, int q, int h, int lane, int* __restrict__ acc) {
+    constexpr int H = NT / 2;
+#pragma unroll 1
+    for (int L = 0; L < LEVELS; ++L)
+#pragma unroll
+        for (int g = 0; g < H; g += 8) {
+            uint32_t v[8];
+            tmem_ld8(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(L * NT + h * H + g), v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            int* d = acc + static_cast<std::size_t>(L * H + g) * 32 + lane;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) atomicAdd(d + u * 32, static_cast<int>(v[u]));
+        }
+}
+
+/// Column constants of one warp's half tile, per lane (j = lane & 15) and
+/// 16-column block: the column scale 2^f_c and the destination column —
+/// loaded before the accumulator is ready, so the stores wait on nothing.
+template <int NT>
+struct HalfCols {
+    static constexpr int kBlocks = (NT / 2 + 15) / 16;
+    double cs[kBlocks];
+    int dst[kBlocks];
+    __device__ __forceinline__ void load(int c0, int lane, int N, const int* __restrict__ eb,
+                                         const int* __restrict__ col_map) {
+        constexpr int H = NT / 2;
+        const int j = lane & 15;
+#pragma unroll
+        for (int k = 0; k < kBlocks; ++k) {
+            const int b = 16 * k, c = c0 + b + j;
+            const bool ok = b + j < H && c < N;
+            cs[k] = ok ? pow2i(__ldg(eb + c)) : 0.0;
+            dst[k] = ok ? (col_map ? __ldg(col_map + c) : c) : -1;
+        }
+    }
+};
+
+/// Persistent-kernel epilogue, phase 2 (registers -> HBM): 16-column blocks
+/// of the warp's 32 x NT/2 values turn around in shared memory (32 x 17
+/// doubles) so that each store instruction writes two rows x 16 consecutive
+/// columns (whole 128-byte lines for plain rows); lane (j, r&1) then applies
+/// the column scale 2^f_c and writes plain rows, scattered slots (col_map) or
+/// the unfolded pair (fold_add: x_c = w_c + v_c, x_{2N-1-c} = w_c - v_c).
+template <int NT>
+__device__ __forceinline__ void store_half(const double (&acc)[NT / 2], const HalfCols<NT>& hc, std::size_t wrow0,
+                                           int c0, int lane, std::size_t M, int N, double* __restrict__ out,
+                                           std::size_t ld_out, const double* __restrict__ fold_add, std::size_t ld_add,
+                                           double* stage) {
+    constexpr int H = NT / 2, LDS = 17;
+    const int live_rows = wrow0 >= M ? 0 : (M - wrow0 >= 32 ? 32 : static_cast<int>(M - wrow0));
+    const int j = lane & 15, rp = lane >> 4;
+#pragma unroll
+    for (int k = 0; k < HalfCols<NT>::kBlocks; ++k) {
+        const int b = 16 * k;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (b + u < H) stage[lane * LDS + u] = acc[b + u];
+        __syncwarp();
+        const double cs = hc.cs[k];
+        const int dst = hc.dst[k];
+        if (dst >= 0) {
+            if (fold_add) {
+                const int c = c0 + b + j;
+                double wv[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int r = 2 * i + rp;
+                    wv[i] = r < live_rows ? __ldg(fold_add + (wrow0 + r) * ld_add + c) : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int r = 2 * i + rp;
+                    if (r < live_rows) {
+                        const double val = stage[r * LDS + j] * cs;
+                        double* orow = out + (wrow0 + r) * ld_out;
+                        orow[c] = wv[i] + val;
+                        orow[2 * N - 1 - c] = wv[i] - val;
+                    }
+                }
+            } else {
+                double* o = out + (wrow0 + rp) * ld_out + dst;
+                if (live_rows == 32) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        __stcs(o + 2 * i * ld_out, stage[(2 * i + rp) * LDS + j] * cs);
+                } else {
+                    for (int i = 0; 2 * i + rp < live_rows; ++i)
+                        __stcs(o + 2 * i * ld_out, stage[(2 * i + rp) * LDS + j] * cs);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 /// Geometry of the persistent pair kernel: a 3-stage ring (the epilogue needs
 /// its own staging: the ring keeps loading the next tile meanwhile).
 template <int S, int NT>
@@ -811,13 +965,17 @@ struct GeoP {
     static constexpr int kABytes = S * TM * CB;
     static constexpr int kBBytes = S * kHalf * CB;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStaging = 4 * 32 * 33 * 8; // 4 epilogue warps x 32 x 33 doubles
+    static constexpr int kStaging = 8 * 32 * 17 * 8; // 8 epilogue warps x 32 x 17 doubles
     static constexpr int kStages = (kMaxSmem - 2048 - kStaging) / kStageBytes;
     static constexpr int kSmem = kStages * kStageBytes + kStaging + 1024 + 512;
     static_assert(kLevels * NT <= 512, "TMEM: one NT-column accumulator per level");
     static_assert(kStages >= 2, "at least two pipeline stages");
+    static_assert(NT % 16 == 0 && (NT / 2) % 8 == 0, "column halves of whole 8-column groups");
 };
-constexpr int kPThreads = 256; // warp 0 producer, 1 MMA (rank 0), 2 relay (rank 1), 4-7 epilogue
+// warp 0 producer, 1 MMA (rank 0), 2 relay (rank 1), 4-11 epilogue (lane
+// quarter warp % 4, column half (warp - 4) / 4)
+constexpr int kPThreads = 384;
+constexpr int kPEpiWarps = 8;
 
 /// Persistent CTA pairs (cluster of 2 along M, cta_group::2 MMAs as in
 /// ozaki_gemm2_kernel) over work units u = cluster, cluster + clusters, ...:
@@ -826,8 +984,10 @@ constexpr int kPThreads = 256; // warp 0 producer, 1 MMA (rank 0), 2 relay (rank
 /// run), so the per-tile prologue, pipeline fill and teardown of the one-tile
 /// kernel are paid once — what dominates short products (K = 512 .. 2048:
 /// the folded products and the rank-k chain).  The accumulator (5 x 96 TMEM
-/// columns) is single-buffered: the MMAs of unit i + 1 wait until both CTAs'
-/// epilogue warps (4-7) drained unit i (t_empty: 8 arrivals at the leader).
+/// columns) is single-buffered, but held only while the epilogue drains it:
+/// eight epilogue warps per CTA (lane quarter x column half) copy it into
+/// registers (Horner, row scale), release it (t_empty: 16 arrivals at the
+/// leader) and only then store, so unit i's stores overlap unit i + 1's MMAs.
 ///
 /// Split-K tail (SplitSched): the first `full` units are whole tiles; the
 /// remaining `rem` tiles — a partial last wave — are split along K into
@@ -870,7 +1030,7 @@ ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
             ptx::mbar_init(empty + i, 1);
         }
         ptx::mbar_init(t_full, 1);
-        ptx::mbar_init(t_empty, 8);
+        ptx::mbar_init(t_empty, 2 * kPEpiWarps);
         ptx::fence_mbar_init();
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -924,8 +1084,9 @@ ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
                             for (int b = 0; a + b < G::kLevels; ++b) {
                                 const uint32_t td = tmem + static_cast<uint32_t>((a + b) * NT);
                                 const uint32_t acc = (ch > w.kb || kk > 0 || a > 0) ? 1u : 0u;
-                                mma_i8_pair<NT>(td, ad + ((a * TM * CB + 32 * kk) >> 4),
-                                                bd + ((b * G::kHalf * CB + 32 * kk) >> 4), acc);
+                                if (!(sched.debug & 8)) // development: loads only
+                                    mma_i8_pair<NT>(td, ad + ((a * TM * CB + 32 * kk) >> 4),
+                                                    bd + ((b * G::kHalf * CB + 32 * kk) >> 4), acc);
                             }
                         }
                     }
@@ -947,10 +1108,12 @@ ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
                 __syncwarp();
             }
         }
-    } else if (warp >= 4) { // epilogue warps: TMEM lane quarter warp % 4
-        const int ew = warp - 4;
+    } else if (warp >= 4) { // epilogue warps: TMEM lane quarter warp % 4, column half (warp - 4) / 4
+        constexpr int H = NT / 2;
+        const int ew = warp - 4, q = warp & 3, h = ew >> 2;
+        double* stage = staging + ew * 32 * 17;
         int i = 0;
-        auto release = [&] { // both CTAs' epilogue warps release the pair's accumulator at the leader
+        auto release = [&] { // every epilogue warp of both CTAs releases the pair's accumulator at the leader
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) {
@@ -962,16 +1125,38 @@ ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
         };
         for (std::size_t u = cid; u < units; u += clusters, ++i) {
             const Unit w = unit_of(u, sched, nch, ntn, nfast, npairs);
+            const std::size_t wrow0 = (2 * w.pair + rank) * TM + 32 * q, row = wrow0 + lane;
+            const double rs = row < M ? pow2i(__ldg(ea + row)) * (1.0 / (127.0 * 127.0)) : 0.0;
+            HalfCols<NT> hc;
+            hc.load(w.nt * NT + h * H, lane, N, eb, (sched.debug & 4) ? nullptr : col_map);
             ptx::mbar_wait(t_full, static_cast<uint32_t>(i & 1));
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            double acc[H];
             if (!SPLIT || w.slot < 0) {
-                store_tile<G::kLevels, NT>(tmem, (2 * w.pair + rank) * TM, w.nt, ew, lane, M, N, ea, eb, out, ld_out,
-                                           col_map, fold_add, ld_add, staging + ew * 32 * 33);
+                if (sched.debug & 2) { // development: no drain
+#pragma unroll
+                    for (int c = 0; c < H; ++c) acc[c] = rs;
+                } else {
+                    drain_half<G::kLevels, NT>(tmem, q, h, rs, acc);
+                }
+                release(); // the next unit's MMAs may start: the stores below overlap them
+                if (sched.debug & 1) continue; // development: no stores
+            } else {
+                const std::size_t blk = (static_cast<std::size_t>(w.slot) * 2 + rank) * kPEpiWarps + ew;
+                int* lsum = sched.acc + blk * (static_cast<std::size_t>(G::kLevels) * H * 32);
+                red_half<G::kLevels, NT>(tmem, q, h, lane, lsum);
                 release();
-            } else if constexpr (SPLIT) {
-                finish_split<G::kLevels, NT>(sched, w, rank, tmem, ew, lane, M, N, ea, eb, out, ld_out, col_map,
-                                             fold_add, ld_add, staging + ew * 32 * 33, release);
+                __threadfence();
+                __syncwarp();
+                int old = 0;
+                if (lane == 0) old = atomicAdd(sched.cnt + blk, 1);
+                old = __shfl_sync(0xffffffffu, old, 0);
+                if (old != sched.nsplit - 1) continue; // another unit of this tile finishes it
+                __threadfence();
+                drain_half_sum<G::kLevels, NT>(lsum, lane, rs, acc);
+                if (lane == 0) sched.cnt[blk] = 0;
             }
+            store_half<NT>(acc, hc, wrow0, w.nt * NT + h * H, lane, M, N, out, ld_out, fold_add, ld_add, stage);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -1000,10 +1185,15 @@ cudaError_t launch_gemmp(const int8_t* a_sl, const int* ea, const int8_t* b_sl, 
     const std::size_t tiles = npairs * ntn;
     SplitSched sched;
     plan_split(tiles, static_cast<std::size_t>(sms / 2), nch, sched);
+    static const int pdebug = [] {
+        const char* v = std::getenv("DCTP_OZAKI_PDEBUG");
+        return v ? std::atoi(v) : 0;
+    }();
+    sched.debug = pdebug;
     const std::size_t units = sched.full + static_cast<std::size_t>(sched.rem) * sched.nsplit;
     const std::size_t clusters = std::min<std::size_t>(units, static_cast<std::size_t>(sms / 2));
     void* ws = nullptr;
-    e = split_alloc(sched, static_cast<std::size_t>(G::kLevels) * NT * 32, stream, &ws);
+    e = split_alloc(sched, static_cast<std::size_t>(G::kLevels) * (NT / 2) * 32, stream, &ws, 2 * kPEpiWarps);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * clusters), 1);

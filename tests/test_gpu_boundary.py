@@ -143,6 +143,41 @@ def test_ozaki_slice_counts_agree(P, torch, reference, tmp_path):
     assert errs["5"] <= 1e-10 and errs["6"] <= 1e-12, errs
 
 
+def test_ozaki_persistent_split_and_one_tile_kernels_agree(P, torch, reference, tmp_path):
+    """The int8 products' three schedules give bit-identical coefficients:
+    the persistent CTA-pair kernel (K <= 2048) with its split-K tail (1000
+    rows of n = 2048: 4 pairs x 22 column tiles on 74 pair slots leave a
+    14-tile tail split 4 ways), the same kernel unsplit (DCTP_OZAKI_SPLIT=0)
+    and the one-tile pair kernel (DCTP_OZAKI_PERSIST=0) — exact int32 level
+    sums, the same Horner and scaling order — for 5 slices (96-column tiles)
+    and 6 (80-column tiles); and the default meets the fp64 tolerance
+    against the reference."""
+    script = tmp_path / "ozp.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "import paper_2409_08970_b200 as P\n"
+        "n = 2048\n"
+        "v = P.fill_signals(P.mix_seed(2409, n, 50), 0, n, 1)[0] / np.sqrt(n)\n"
+        "plan = P.DctPlusPlan(n, P.RankOneUpdate.general(v, 0.1), 1e-12)\n"
+        "x = torch.as_tensor(P.fill_signals(7, 0, n, 1000), device='cuda')\n"
+        "np.save(sys.argv[1], plan.forward(x).cpu().numpy())\n")
+    n = 2048
+    v = P.fill_signals(P.mix_seed(2409, n, 50), 0, n, 1)[0] / np.sqrt(n)
+    want = reference.plan(n, O.Update(2, 0.1, 0, 0, tuple(v))).forward(P.fill_signals(7, 0, n, 1000))
+    for sl in ("5", "6"):
+        outs = {}
+        for mode, extra in (("split", {}), ("unsplit", {"DCTP_OZAKI_SPLIT": "0"}),
+                            ("one_tile", {"DCTP_OZAKI_PERSIST": "0"})):
+            f = tmp_path / f"y{sl}_{mode}.npy"
+            env = dict(os.environ, DCTP_OZAKI_SLICES=sl, **extra)
+            subprocess.run([sys.executable, str(script), str(f)], env=env, check=True, timeout=300)
+            outs[mode] = np.load(f)
+        assert np.array_equal(outs["split"], outs["unsplit"]), sl
+        assert np.array_equal(outs["split"], outs["one_tile"]), sl
+        assert O.parity(outs["split"], want) <= 1e-10
+
+
 def test_cuda_graph_capture_and_replay(P, torch):
     """Launches captured into a CUDA graph replay to the same coefficients;
     a non-finite sample fed through the graph raises DomainError at the next

@@ -1615,10 +1615,11 @@ static void host_roundtrip(int device, std::size_t batch, std::size_t in_row, st
     DeviceScope scope(device);
     const int slots = static_cast<int>(std::min<std::size_t>(env_size("DCTP_HOST_SLOTS", 3), kMaxHostSlots));
     const std::size_t row_bytes = std::max(in_row, out_row) * sizeof(T);
+    const std::size_t floor_rows = env_size("DCTP_HOST_MIN_ROWS", 256);
     const std::size_t max_rows =
-        std::max<std::size_t>(256, (env_size("DCTP_HOST_CHUNK_MB", 16) << 20) / row_bytes); // tuning knobs
-    const std::size_t min_rows =
-        std::min(max_rows, std::max<std::size_t>(256, (env_size("DCTP_HOST_CHUNK_MIN_MB", 2) << 20) / row_bytes));
+        std::max<std::size_t>(floor_rows, (env_size("DCTP_HOST_CHUNK_MB", 16) << 20) / row_bytes); // tuning knobs
+    const std::size_t min_rows = std::min(
+        max_rows, std::max<std::size_t>(floor_rows, (env_size("DCTP_HOST_CHUNK_MIN_MB", 2) << 20) / row_bytes));
     // Chunk schedule: sizes double from min_rows up to max_rows at the head and
     // mirror that ramp at the tail, so the pipeline fills and drains with small
     // chunks while the middle runs few, large ones (every kernel launch costs a

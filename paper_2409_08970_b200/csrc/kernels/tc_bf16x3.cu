@@ -28,7 +28,9 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_bf16.h>
+#include <cudaTypedefs.h>
 
 #include "kernels/common.cuh"
 #include "kernels/launch.hpp"
@@ -47,7 +49,6 @@ constexpr int kBHalf = BN * KC * 2;            // 16 KB
 constexpr int kBChunk = 2 * kBHalf;            // 32 KB
 constexpr int kBBytes = (kMaxK / KC) * kBChunk; // 128 KB resident
 constexpr int kStaging = kEpiWarps * 32 * 32 * 4;
-constexpr int kSmem = kBBytes + kAStages * kAChunk + kStaging + 1024 + 256;
 
 __host__ __device__ constexpr uint32_t sw64_off(int r, int c16) {
     return static_cast<uint32_t>(r * 64 + ((c16 ^ ((r >> 1) & 3)) << 4));
@@ -157,6 +158,7 @@ struct Epi {
     const int* col_map;
     const float* fold_add;
     std::size_t ld_add;
+    int debug = 0; // DCTP_TC_DEBUG (development: phase isolation)
 };
 
 /// STREAM = false: K <= 128, the B^T column tile resident (one load per
@@ -171,10 +173,22 @@ struct Lay {
     static_assert(kSmem <= 227 * 1024, "tc_bf16x3: shared memory");
 };
 
-template <bool STREAM, int MODE> // MODE 0: plain rows, 1: col_map, 2: fold_add
+/// TMA store of one 32 x 32 fp32 block staged in shared memory (128-byte
+/// rows, SWIZZLE_128B — the turn-around's own layout) at (row0, col0) of C.
+__device__ __forceinline__ void tma_store_block(const CUtensorMap* map, const void* smem, int col0, int row0) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(col0), "r"(row0), "r"(ptx::smem_addr(smem))
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+
+template <bool STREAM, int MODE> // MODE 0: plain rows, 1: col_map, 2: fold_add, 3: plain rows by TMA stores
 __global__ void __launch_bounds__(kThreads, 1)
 tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __restrict__ b_sw, Epi ep,
-                 std::size_t M, int N, int nch, unsigned ntm, unsigned ntn, int* flag) {
+                 std::size_t M, int N, int nch, unsigned ntm, unsigned ntn, int* flag,
+                 const __grid_constant__ CUtensorMap cmap) {
     using Ly = Lay<STREAM>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t raw = ptx::smem_addr(smem_raw);
@@ -241,12 +255,15 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
                 const int st = static_cast<int>(chunk % Ly::kStages);
                 const uint32_t ph = static_cast<uint32_t>((chunk / Ly::kStages) & 1);
                 ptx::mbar_wait(s_empty + st, ph ^ 1u);
+                // development knob DCTP_TC_DEBUG=1: only the first ring of A chunks is loaded
+                const bool skip = (ep.debug & 1) && chunk >= static_cast<unsigned long long>(Ly::kStages);
                 if (elect_one()) {
-                    ptx::mbar_expect_tx(s_full + st, Ly::kStage);
+                    ptx::mbar_expect_tx(s_full + st, skip ? 0u : static_cast<uint32_t>(Ly::kStage));
                     unsigned char* dst = ring + st * Ly::kStage;
-                    ptx::bulk_load(dst, a_sw + (static_cast<std::size_t>(mt) * nch + c) * kAChunk, kAChunk,
-                                   s_full + st);
-                    if (STREAM)
+                    if (!skip)
+                        ptx::bulk_load(dst, a_sw + (static_cast<std::size_t>(mt) * nch + c) * kAChunk, kAChunk,
+                                       s_full + st);
+                    if (STREAM && !skip)
                         ptx::bulk_load(dst + kAChunk, b_sw + (static_cast<std::size_t>(nt) * nch + c) * kBChunk,
                                        kBChunk, s_full + st);
                 }
@@ -313,18 +330,44 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
             ptx::mbar_wait(t_full + buf, static_cast<uint32_t>((i >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             const std::size_t row0 = static_cast<std::size_t>(mt) * BM + 32 * q;
-#pragma unroll 1
-            for (int cc = 0; cc < BN / 2; cc += 32) {
-                const int c0 = h * (BN / 2) + cc, col0 = static_cast<int>(nt) * BN + c0;
-                if (col0 >= N) break;
-                uint32_t v[32];
-                tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(buf * BN + c0), v);
+            // the warp's four 32 x 32 blocks: block k + 1's TMEM load is in
+            // flight while block k turns around and stores; the accumulator
+            // is released as soon as the last block is in registers
+            constexpr int kBlk = BN / 2 / 32;
+            const int colh = static_cast<int>(nt) * BN + h * (BN / 2);
+            const int nblk = colh >= N ? 0 : min(kBlk, (N - colh + 31) / 32);
+            const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * q) << 16) +
+                                   static_cast<uint32_t>(buf * BN + h * (BN / 2));
+            uint32_t v[2][32];
+            if (nblk > 0) tmem_ld32(taddr, v[0]);
+#pragma unroll
+            for (int k = 0; k < kBlk; ++k) {
+                if (k >= nblk) break;
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                if (col0 == 0 && row0 + lane < M) bad |= !isfinite(__uint_as_float(v[0])); // column 0
+                if (k + 1 < nblk) {
+                    tmem_ld32(taddr + static_cast<uint32_t>(32 * (k + 1)), v[(k + 1) & 1]);
+                } else {
+                    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(t_empty + buf);
+                }
+                const uint32_t(&w32)[32] = v[k & 1];
+                const int col0 = colh + 32 * k;
+                if (col0 == 0 && row0 + lane < M) bad |= !isfinite(__uint_as_float(w32[0])); // column 0
+                if constexpr (MODE == 3) { // the previous block's store must have read the staging
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                    __syncwarp();
+                }
 #pragma unroll
                 for (int g = 0; g < 8; ++g)
                     *reinterpret_cast<uint4*>(tb + lane * 128 + ((g ^ (lane & 7)) << 4)) =
-                        make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+                        make_uint4(w32[4 * g], w32[4 * g + 1], w32[4 * g + 2], w32[4 * g + 3]);
+                if constexpr (MODE == 3) { // one TMA store per block (rows >= M / columns >= N are clipped)
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) tma_store_block(&cmap, tb, col0, static_cast<int>(row0));
+                    continue;
+                }
                 __syncwarp();
 #pragma unroll
                 for (int it = 0; it < 8; ++it) {
@@ -356,11 +399,16 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
                 }
                 __syncwarp();
             }
-            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(t_empty + buf);
+            if (nblk == 0) {
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(t_empty + buf);
+            }
+
         }
         if (bad) atomicOr(flag, 1);
+        if constexpr (MODE == 3)
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
@@ -407,6 +455,29 @@ std::vector<uint16_t> tc_bf16x3_swizzle_b(const double* bt, int N, int K, int ld
     return out;
 }
 
+/// Tensor map of C (M rows x N fp32 columns, row stride ldc) in 32 x 32
+/// boxes with 128-byte swizzle, for the TMA-store epilogue; false if the
+/// driver entry point or the encoding is unavailable (the kernel then stores
+/// with st.global).
+static bool c_tensor_map(float* C, std::size_t ldc, std::size_t M, int N, CUtensorMap* map) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode || M >= (1ull << 31) || (ldc * 4) % 16 != 0 || reinterpret_cast<std::uintptr_t>(C) % 16 != 0)
+        return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldc) * 4};
+    const cuuint32_t box[2] = {32, 32}, estr[2] = {1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t tc_bf16x3(const float* A, int lda, const uint16_t* b_sw, float* C, std::size_t ldc, std::size_t M, int N,
                       int K, int* flag, int num_sms, cudaStream_t stream, const int* col_map, const int* a_map,
                       const float* fold_add, std::size_t ld_add) {
@@ -427,21 +498,37 @@ cudaError_t tc_bf16x3(const float* A, int lda, const uint16_t* b_sw, float* C, s
         const unsigned ntn = static_cast<unsigned>((N + BN - 1) / BN);
         const unsigned long long tiles = static_cast<unsigned long long>(ntm) * ntn;
         const unsigned grid = static_cast<unsigned>(tiles < static_cast<unsigned long long>(num_sms) ? tiles : num_sms);
-        const Epi ep{C, ldc, col_map, fold_add, ld_add};
-        const int mode = fold_add ? 2 : (col_map ? 1 : 0);
+        static const int dbg = [] {
+            const char* v = std::getenv("DCTP_TC_DEBUG");
+            return v ? std::atoi(v) : 0;
+        }();
+        const Epi ep{C, ldc, col_map, fold_add, ld_add, dbg};
+        int mode = fold_add ? 2 : (col_map ? 1 : 0);
+        CUtensorMap cmap;
+        std::memset(&cmap, 0, sizeof(cmap));
+        // DCTP_TC_TMA_STORE=1: plain rows leave by TMA tensor stores (one per
+        // 32 x 32 block) instead of st.global — measured slower at C4 (0.158
+        // vs 0.148 ms: the stores are not issue-bound), kept opt-in
+        static const bool tma_store = [] {
+            const char* v = std::getenv("DCTP_TC_TMA_STORE");
+            return v && v[0] == '1';
+        }();
+        if (mode == 0 && tma_store && c_tensor_map(C, ldc, M, N, &cmap)) mode = 3;
         auto launch = [&](auto kern, int smem) {
             cudaError_t r = smem_optin(reinterpret_cast<const void*>(kern), smem);
             if (r != cudaSuccess) return r;
             kern<<<grid, kThreads, smem, stream>>>(a_sw, reinterpret_cast<const unsigned char*>(b_sw), ep, M, N, nch,
-                                                   static_cast<unsigned>(ntm), ntn, flag);
+                                                   static_cast<unsigned>(ntm), ntn, flag, cmap);
             return cudaGetLastError();
         };
         if (K > kMaxK)
-            e = mode == 2 ? launch(tc_bf16x3_kernel<true, 2>, Lay<true>::kSmem)
+            e = mode == 3   ? launch(tc_bf16x3_kernel<true, 3>, Lay<true>::kSmem)
+                : mode == 2 ? launch(tc_bf16x3_kernel<true, 2>, Lay<true>::kSmem)
                 : mode == 1 ? launch(tc_bf16x3_kernel<true, 1>, Lay<true>::kSmem)
                             : launch(tc_bf16x3_kernel<true, 0>, Lay<true>::kSmem);
         else
-            e = mode == 2 ? launch(tc_bf16x3_kernel<false, 2>, Lay<false>::kSmem)
+            e = mode == 3   ? launch(tc_bf16x3_kernel<false, 3>, Lay<false>::kSmem)
+                : mode == 2 ? launch(tc_bf16x3_kernel<false, 2>, Lay<false>::kSmem)
                 : mode == 1 ? launch(tc_bf16x3_kernel<false, 1>, Lay<false>::kSmem)
                             : launch(tc_bf16x3_kernel<false, 0>, Lay<false>::kSmem);
     }

@@ -60,12 +60,12 @@ def copy_bw():
     return res
 
 
-def host_entry(chunk_mb, slots=3, streamed=1, stream_kb=2048, min_mb=2):
+def host_entry(chunk_mb, slots=3, streamed=1, stream_kb=2048, min_mb=2, wl=2, floor=256):
     code = r"""
 import time, numpy as np, torch, json
 import paper_2409_08970_b200 as P
 from paper_2409_08970_b200.configs import WORKLOADS, make_plan
-cfg = WORKLOADS[2]
+cfg = WORKLOADS[WL]
 plan = make_plan(cfg)
 x = torch.randn(cfg.batch, cfg.n, dtype=torch.float64).pin_memory().numpy()
 y = torch.empty(cfg.batch, cfg.n, dtype=torch.float64).pin_memory().numpy()
@@ -81,8 +81,9 @@ ms = (time.perf_counter() - t) / R * 1e3
 print(json.dumps({"ms": ms}))
 """
     env = dict(os.environ, DCTP_HOST_CHUNK_MB=str(chunk_mb), DCTP_HOST_SLOTS=str(slots), DCTP_HOST_STREAMED=str(streamed),
-               DCTP_STREAM_CHUNK_KB=str(stream_kb), DCTP_HOST_CHUNK_MIN_MB=str(min_mb))
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT)
+               DCTP_STREAM_CHUNK_KB=str(stream_kb), DCTP_HOST_CHUNK_MIN_MB=str(min_mb), DCTP_HOST_MIN_ROWS=str(floor))
+    out = subprocess.run([sys.executable, "-c", code.replace("WL", str(wl))], env=env, capture_output=True, text=True,
+                         cwd=ROOT)
     try:
         return json.loads(out.stdout.strip().splitlines()[-1])
     except Exception:
@@ -91,7 +92,8 @@ print(json.dumps({"ms": ms}))
 
 if __name__ == "__main__":
     print(json.dumps({"copy_bw": copy_bw()}))
-    for kb in (8192,):
-        print(json.dumps({"streamed_chunk_kb": kb, **host_entry(8, 3, 1, kb)}))
-    for mb, mn, slots in ((16, 16, 3), (16, 1, 3), (16, 2, 3), (16, 4, 3), (32, 2, 3), (32, 4, 3), (16, 2, 4), (8, 1, 3)):
-        print(json.dumps({"staged_chunk_mb": mb, "min_mb": mn, "slots": slots, **host_entry(mb, slots, 0, min_mb=mn)}))
+    wl = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    for mb, mn, slots, floor in ((16, 2, 3, 256), (16, 1, 3, 16), (16, 2, 3, 16), (8, 1, 3, 16), (32, 1, 3, 16),
+                                 (16, 1, 4, 16), (8, 1, 4, 16), (4, 1, 4, 16)):
+        print(json.dumps({"wl": wl, "staged_chunk_mb": mb, "min_mb": mn, "slots": slots, "floor": floor,
+                          **host_entry(mb, slots, 0, min_mb=mn, wl=wl, floor=floor)}))

@@ -36,6 +36,34 @@ __device__ __forceinline__ uint32_t sw64_int8(int r, int c16) {
     return static_cast<uint32_t>(r * 64 + ((c16 ^ ((r >> 1) & 3)) << 4));
 }
 
+/// (t / K, t % K) for a thread's flat index t advanced by `step`, without a
+/// division per element (the gather loops' index math was ~30% of their
+/// instructions).
+__device__ __forceinline__ void step_rk(int& r, int& k, int step, int K) {
+    k += step;
+    while (k >= K) {
+        k -= K;
+        ++r;
+    }
+}
+
+/// Byte offset of (row grow, column k) in the int8 slice image of slice 0
+/// (tiles of fs.tile_rows rows, 64-byte K chunks, SWIZZLE_64B), shifts for the
+/// 128-row tiles every caller uses.
+__device__ __forceinline__ std::size_t slice_off(const FoldSlices& fs, std::size_t grow, int k) {
+    std::size_t tile;
+    int lr;
+    if (fs.tile_rows == 128) {
+        tile = grow >> 7;
+        lr = static_cast<int>(grow & 127);
+    } else {
+        tile = grow / fs.tile_rows;
+        lr = static_cast<int>(grow % fs.tile_rows);
+    }
+    const std::size_t slice_bytes = static_cast<std::size_t>(fs.tile_rows) * 64;
+    return ((tile * fs.nch + (k >> 6)) * fs.S) * slice_bytes + sw64_int8(lr, (k & 63) >> 4) + (k & 15);
+}
+
 /// FOLD (antisymmetric plans): the input rows hold 2n samples; the kernel
 /// writes u_j = x_j - x_{2n-1-j} to `hat` and transforms y_j = x_j + x_{2n-1-j}
 /// (length n), whose DCT gives the even coefficients of the full row.  With
@@ -120,8 +148,9 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
             __syncthreads();
             const int groups = fs.nch * 16; // 4-sample words per row
             const std::size_t slice_bytes = static_cast<std::size_t>(fs.tile_rows) * 64;
-            for (int g = threadIdx.x; g < rows * groups; g += kThreads) {
-                const int r = g / groups, k = 4 * (g - r * groups);
+            int r = threadIdx.x / groups, kg = threadIdx.x - r * groups;
+            for (; r < rows; step_rk(r, kg, kThreads, groups)) {
+                const int k = 4 * kg;
                 const std::size_t grow = b0 + r;
                 const double scale = rmax[r];
                 double v[4];
@@ -130,9 +159,7 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
                     const double x = k + u < n ? static_cast<double>(ush[r * n + k + u]) : 0.0;
                     v[u] = isfinite(x) ? x * scale : 0.0;
                 }
-                const std::size_t tile = grow / fs.tile_rows;
-                const int lr = static_cast<int>(grow % fs.tile_rows), ch = k / 64, c16 = (k % 64) / 16;
-                int8_t* dst = fs.sl + ((tile * fs.nch + ch) * fs.S) * slice_bytes + sw64_int8(lr, c16) + (k % 16);
+                int8_t* dst = fs.sl + slice_off(fs, grow, k);
                 for (int s = 0; s < fs.S; ++s) {
                     uint32_t w = 0u;
 #pragma unroll
@@ -222,8 +249,9 @@ __device__ void slice_rows_to_tiles(const double* g, int rows, int K, std::size_
     __syncthreads();
     const int groups = fs.nch * 16;
     const std::size_t slice_bytes = static_cast<std::size_t>(fs.tile_rows) * 64;
-    for (int t = threadIdx.x; t < rows * groups; t += kThreads) {
-        const int r = t / groups, k = 4 * (t - r * groups);
+    int r = threadIdx.x / groups, kg = threadIdx.x - r * groups;
+    for (; r < rows; step_rk(r, kg, kThreads, groups)) {
+        const int k = 4 * kg;
         const std::size_t grow = b0 + r;
         double v[4];
 #pragma unroll
@@ -231,9 +259,7 @@ __device__ void slice_rows_to_tiles(const double* g, int rows, int K, std::size_
             const double x = k + u < K ? g[r * K + k + u] : 0.0;
             v[u] = isfinite(x) ? x * rmax[r] : 0.0;
         }
-        const std::size_t tile = grow / fs.tile_rows;
-        const int lr = static_cast<int>(grow % fs.tile_rows), ch = k / 64, c16 = (k % 64) / 16;
-        int8_t* dst = fs.sl + ((tile * fs.nch + ch) * fs.S) * slice_bytes + sw64_int8(lr, c16) + (k % 16);
+        int8_t* dst = fs.sl + slice_off(fs, grow, k);
         for (int s = 0; s < fs.S; ++s) {
             uint32_t w = 0u;
 #pragma unroll
@@ -266,17 +292,17 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
             double* rmax = g + rows_per_cta * fs.K;
             constexpr int U = 8;
             bool nf = false;
+            int r0 = threadIdx.x / fs.K, k0 = threadIdx.x - r0 * fs.K;
             for (int t0 = threadIdx.x; t0 < rows * fs.K; t0 += U * kThreads) {
                 double v[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int t = t0 + u * kThreads;
-                    if (t < rows * fs.K) {
-                        const int r = t / fs.K, k = t - r * fs.K;
-                        v[u] = static_cast<double>(p[(b0 + r) * ld_p + __ldg(fs.map + k)]);
+                    if (r0 < rows) {
+                        v[u] = static_cast<double>(p[(b0 + r0) * ld_p + __ldg(fs.map + k0)]);
                     } else {
                         v[u] = 0.0;
                     }
+                    step_rk(r0, k0, kThreads, fs.K);
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u)
@@ -308,25 +334,24 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
     }
     __syncthreads();
     bool bad = false;
-    for (int t0 = threadIdx.x; t0 < rows * emit.count; t0 += U * kThreads) {
-        T v[U];
+    if (emit.count > 0) {
+        int re = threadIdx.x / emit.count, ee = threadIdx.x - re * emit.count;
+        for (int t0 = threadIdx.x; t0 < rows * emit.count; t0 += U * kThreads) {
+            T v[U];
+            int ri[U], ei[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int t = t0 + u * kThreads;
-            if (t < rows * emit.count) {
-                const int r = t / emit.count, e = t - r * emit.count;
-                v[u] = p[(b0 + r) * ld_p + emit.from[e]];
-            } else {
-                v[u] = T(0);
+            for (int u = 0; u < U; ++u) {
+                ri[u] = re;
+                ei[u] = ee;
+                v[u] = re < rows ? p[(b0 + re) * ld_p + __ldg(emit.from + ee)] : T(0);
+                step_rk(re, ee, kThreads, emit.count);
             }
-        }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int t = t0 + u * kThreads;
-            if (t >= rows * emit.count) break;
-            const int r = t / emit.count, e = t - r * emit.count;
-            bad |= !finite_val(v[u]);
-            sh[r * n + emit.to[e]] = emit.sign[e] * v[u];
+            for (int u = 0; u < U; ++u) {
+                if (ri[u] >= rows) break;
+                bad |= !finite_val(v[u]);
+                sh[ri[u] * n + __ldg(emit.to + ei[u])] = __ldg(emit.sign + ei[u]) * v[u];
+            }
         }
     }
     if (bad) atomicOr(flag, 1);

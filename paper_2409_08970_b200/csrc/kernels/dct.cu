@@ -64,6 +64,56 @@ __device__ __forceinline__ std::size_t slice_off(const FoldSlices& fs, std::size
     return ((tile * fs.nch + (k >> 6)) * fs.S) * slice_bytes + sw64_int8(lr, (k & 63) >> 4) + (k & 15);
 }
 
+/// Eight consecutive values k0..k0+7 of one row (src: the row, 16-byte
+/// aligned when vec) scaled and cut into S int8 digits (ozaki_digit), one
+/// 8-byte store per slice plane.
+template <int S>
+__device__ __forceinline__ void slice8_rows(const double* src, int k0, int K, bool vec, double scale, int8_t* dst,
+                                            std::size_t slice_bytes) {
+    double v[8];
+    if (vec && k0 + 8 <= K) {
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+            const double2 p = *reinterpret_cast<const double2*>(src + k0 + u);
+            v[u] = p.x;
+            v[u + 1] = p.y;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = k0 + u < K ? src[k0 + u] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = isfinite(v[u]) ? v[u] * scale : 0.0;
+#pragma unroll
+    for (int sl = 0; sl < S; ++sl) {
+        uint32_t lo = 0u, hi = 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            lo |= ozaki_digit(v[u]) << (8 * u);
+            hi |= ozaki_digit(v[4 + u]) << (8 * u);
+        }
+        *reinterpret_cast<uint2*>(dst + sl * slice_bytes) = make_uint2(lo, hi);
+    }
+}
+
+/// The slices of `rows` rows of K values each (src row r at src + r * lds),
+/// 8-value groups spread over the CTA.
+__device__ __forceinline__ void slice_rows(const double* src, int lds, int rows, int K, std::size_t b0,
+                                           const FoldSlices& fs, const double* rscale) {
+    const int groups = fs.nch * 8; // 8-value groups per row (64-byte chunks)
+    const std::size_t slice_bytes = static_cast<std::size_t>(fs.tile_rows) * 64;
+    const bool vec = (lds % 2) == 0;
+    int r = threadIdx.x / groups, kg = threadIdx.x - r * groups;
+    for (; r < rows; step_rk(r, kg, kThreads, groups)) {
+        const int k0 = 8 * kg;
+        int8_t* dst = fs.sl + slice_off(fs, b0 + r, k0);
+        if (fs.S == 5)
+            slice8_rows<5>(src + r * lds, k0, K, vec, rscale[r], dst, slice_bytes);
+        else
+            slice8_rows<6>(src + r * lds, k0, K, vec, rscale[r], dst, slice_bytes);
+    }
+}
+
 /// FOLD (antisymmetric plans): the input rows hold 2n samples; the kernel
 /// writes u_j = x_j - x_{2n-1-j} to `hat` and transforms y_j = x_j + x_{2n-1-j}
 /// (length n), whose DCT gives the even coefficients of the full row.  With
@@ -146,29 +196,7 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
                 }
             }
             __syncthreads();
-            const int groups = fs.nch * 16; // 4-sample words per row
-            const std::size_t slice_bytes = static_cast<std::size_t>(fs.tile_rows) * 64;
-            int r = threadIdx.x / groups, kg = threadIdx.x - r * groups;
-            for (; r < rows; step_rk(r, kg, kThreads, groups)) {
-                const int k = 4 * kg;
-                const std::size_t grow = b0 + r;
-                const double scale = rmax[r];
-                double v[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const double x = k + u < n ? static_cast<double>(ush[r * n + k + u]) : 0.0;
-                    v[u] = isfinite(x) ? x * scale : 0.0;
-                }
-                int8_t* dst = fs.sl + slice_off(fs, grow, k);
-                for (int s = 0; s < fs.S; ++s) {
-                    uint32_t w = 0u;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        w |= ozaki_digit(v[u]) << (8 * u);
-                    }
-                    *reinterpret_cast<uint32_t*>(dst + s * slice_bytes) = w;
-                }
-            }
+            slice_rows(reinterpret_cast<const double*>(ush), n, rows, n, b0, fs, rmax);
         }
     }
 
@@ -247,28 +275,7 @@ __device__ void slice_rows_to_tiles(const double* g, int rows, int K, std::size_
         }
     }
     __syncthreads();
-    const int groups = fs.nch * 16;
-    const std::size_t slice_bytes = static_cast<std::size_t>(fs.tile_rows) * 64;
-    int r = threadIdx.x / groups, kg = threadIdx.x - r * groups;
-    for (; r < rows; step_rk(r, kg, kThreads, groups)) {
-        const int k = 4 * kg;
-        const std::size_t grow = b0 + r;
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const double x = k + u < K ? g[r * K + k + u] : 0.0;
-            v[u] = isfinite(x) ? x * rmax[r] : 0.0;
-        }
-        int8_t* dst = fs.sl + slice_off(fs, grow, k);
-        for (int s = 0; s < fs.S; ++s) {
-            uint32_t w = 0u;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                w |= ozaki_digit(v[u]) << (8 * u);
-            }
-            *reinterpret_cast<uint32_t*>(dst + s * slice_bytes) = w;
-        }
-    }
+    slice_rows(g, K, rows, K, b0, fs, rmax);
 }
 
 /// fs.sl set (fp64): the K = fs.K values p[row, fs.map[k]] of each row also

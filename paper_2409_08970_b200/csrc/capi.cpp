@@ -7,6 +7,7 @@
 
 
 #include <algorithm>
+#include <limits>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -1353,7 +1354,7 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
                 fs.map = at<int>(p->blob, f.map);
                 fs.K = f.cols;
                 cuda_check(DCTP_LAUNCH("fold_idct", s,
-                                       dctp::dev::idct_rows<T>(at<T>(p->blob, f.zero), 0, in, n, even, w.ptr, f.L,
+                                       dctp::dev::idct_rows<T>(nullptr, 0, in, n, even, w.ptr, f.L,
                                                                f.L, batch, twiddles_at<T>(p->blob, f.tw64),
                                                                p->flags(s), s, fs)),
                            "fold idct kernel");
@@ -1365,7 +1366,7 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
             }
         }
         cuda_check(DCTP_LAUNCH("fold_idct", s,
-                               dctp::dev::idct_rows<T>(at<T>(p->blob, f.zero), 0, in, n, even, w.ptr, f.L, f.L, batch,
+                               dctp::dev::idct_rows<T>(nullptr, 0, in, n, even, w.ptr, f.L, f.L, batch,
                                                        twiddles_at<T>(p->blob, f32 ? f.tw32 : f.tw64), p->flags(s), s)),
                    "fold idct kernel");
         if constexpr (f32) {

@@ -333,7 +333,7 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int t = t0 + u * kThreads;
-            v[u] = t < rows * n ? d[(b0 + (t >> logn)) * ld_d + (t & (n - 1))] : T(0);
+            v[u] = (t < rows * n && d) ? d[(b0 + (t >> logn)) * ld_d + (t & (n - 1))] : T(0);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -549,6 +549,7 @@ cudaError_t idct_rows(const T* d, std::size_t ld_d, const T* p, std::size_t ld_p
                                               ilog2(n), rows, batch, tw, flag, fs);
         return cudaGetLastError();
     }
+    if (!d) return cudaErrorInvalidValue; // zero d rows (d = nullptr): the FFT kernel only
     const std::size_t smem = n * sizeof(T);
     auto kern = idct_direct_kernel<T>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

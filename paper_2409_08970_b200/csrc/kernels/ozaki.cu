@@ -195,6 +195,94 @@ ozaki_slice_kernel(const T* __restrict__ in, std::size_t ld, std::size_t rows, s
     }
 }
 
+/// Long fp64 rows (2048 < K <= 8192, 16-byte aligned, no column map: C5's
+/// signals): one CTA per row keeps the row in registers (thread t: 8-value
+/// groups k = 8 t + 2048 i), so it is read once — all loads in flight before
+/// the maximum — and each group leaves as one 8-byte store per slice plane.
+template <int S>
+__global__ void __launch_bounds__(256)
+ozaki_slice_reg_kernel(const double* __restrict__ in, std::size_t ld, std::size_t rows, int K, int nch,
+                       int tile_rows, int8_t* __restrict__ sl, int* __restrict__ expo, int* flag) {
+    constexpr int G = 4; // groups of 8 per thread: 256 x 8 x 4 = 8192
+    __shared__ double red[8];
+    __shared__ int red_bad[8];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const std::size_t r = blockIdx.x;
+    const bool real = r < rows;
+    const double* row = in + (real ? r * ld : 0);
+    const int kend = nch * CB;
+    double v[G][8];
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const int k = 8 * t + 2048 * i;
+        if (real && k + 8 <= K) {
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+                const double2 a = __ldg(reinterpret_cast<const double2*>(row + k + u));
+                v[i][u] = a.x;
+                v[i][u + 1] = a.y;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[i][u] = (real && k + u < K) ? row[k + u] : 0.0;
+        }
+    }
+    double mx = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < G; ++i)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            bad |= !isfinite(v[i][u]);
+            mx = fmax(mx, fabs(v[i][u]));
+        }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    int anybad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+        red[warp] = mx;
+        red_bad[warp] = anybad;
+    }
+    __syncthreads();
+    mx = red[0];
+    anybad = red_bad[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+        mx = fmax(mx, red[w]);
+        anybad |= red_bad[w];
+    }
+    if (anybad) {
+        if (t == 0 && flag) atomicOr(flag, 1);
+        mx = 0.0;
+    }
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);
+    if (t == 0) expo[r] = e;
+    const double scale = ldexp(127.0, -e);
+    const std::size_t tile = r / tile_rows;
+    const int lr = static_cast<int>(r % tile_rows);
+    const std::size_t slice_bytes = static_cast<std::size_t>(tile_rows) * CB;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const int k = 8 * t + 2048 * i;
+        if (k >= kend) break;
+        double* w = v[i];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w[u] = isfinite(w[u]) ? w[u] * scale : 0.0;
+        int8_t* dst = sl + ((tile * nch + k / CB) * S) * slice_bytes + sw64(lr, (k % CB) / 16) + (k % 16);
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+            uint32_t lo = 0u, hi = 0u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                lo |= ozaki_digit(w[u]) << (8 * u);
+                hi |= ozaki_digit(w[4 + u]) << (8 * u);
+            }
+            *reinterpret_cast<uint2*>(dst + q * slice_bytes) = make_uint2(lo, hi);
+        }
+    }
+}
+
 // ------------------------------------------------------------------- GEMM
 
 template <int S, int NT>
@@ -1344,6 +1432,14 @@ cudaError_t ozaki_slice(const T* in, std::size_t ld, std::size_t rows, int K, co
     const int nch = (K + CB - 1) / CB;
     const int vec = !a_map && reinterpret_cast<std::uintptr_t>(in) % 16 == 0 && (ld * sizeof(T)) % 16 == 0;
     if (rows_pad >= (1ull << 31)) return cudaErrorInvalidValue;
+    if constexpr (sizeof(T) == 8) {
+        if (K > 2048 && nch * CB <= 8192 && vec && (slices == 5 || slices == 6)) { // the row held in registers
+            auto kern = slices == 5 ? ozaki_slice_reg_kernel<5> : ozaki_slice_reg_kernel<6>;
+            kern<<<static_cast<unsigned>(rows_pad), 256, 0, stream>>>(in, ld, rows, K, nch, tile_rows, sl, expo,
+                                                                      flag);
+            return cudaGetLastError();
+        }
+    }
     if (K <= 2048) // a warp per row, 8 rows per CTA
         ozaki_slice_kernel<T, 1><<<static_cast<unsigned>((rows_pad + 7) / 8), 256, 0, stream>>>(
             in, ld, rows, rows_pad, K, nch, a_map, tile_rows, slices, sl, expo, flag, vec);

@@ -369,18 +369,32 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
                     continue;
                 }
                 __syncwarp();
+                // lane (row group lane >> 3, 4-column group g): the same
+                // columns in all 8 iterations; the unfold's fold rows are all
+                // loaded before the first store (the stores may alias them, so
+                // the compiler would otherwise serialise load -> store)
+                const int g = lane & 7, col = col0 + 4 * g;
+                float4 add[8];
+                if constexpr (MODE == 2) { // N % 4 == 0 on this path
+#pragma unroll
+                    for (int it = 0; it < 8; ++it) {
+                        const std::size_t grow = row0 + 4 * it + (lane >> 3);
+                        add[it] = (grow < M && col < N)
+                                      ? __ldg(reinterpret_cast<const float4*>(ep.fold_add + grow * ep.ld_add + col))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
 #pragma unroll
                 for (int it = 0; it < 8; ++it) {
-                    const int r = 4 * it + (lane >> 3), g = lane & 7;
+                    const int r = 4 * it + (lane >> 3);
                     const uint4 w = *reinterpret_cast<const uint4*>(tb + r * 128 + ((g ^ (r & 7)) << 4));
                     const std::size_t grow = row0 + r;
-                    const int col = col0 + 4 * g;
                     if (grow >= M || col >= N) continue;
                     const float e4[4] = {__uint_as_float(w.x), __uint_as_float(w.y), __uint_as_float(w.z),
                                          __uint_as_float(w.w)};
                     float* orow = ep.C + grow * ep.ldc;
-                    if constexpr (MODE == 2) { // N % 4 == 0 on this path
-                        const float4 a4 = __ldg(reinterpret_cast<const float4*>(ep.fold_add + grow * ep.ld_add + col));
+                    if constexpr (MODE == 2) {
+                        const float4 a4 = add[it];
                         __stcs(reinterpret_cast<float4*>(orow + col),
                                make_float4(a4.x + e4[0], a4.y + e4[1], a4.z + e4[2], a4.w + e4[3]));
                         __stcs(reinterpret_cast<float4*>(orow + 2 * N - 4 - col),

@@ -402,6 +402,14 @@ struct dctp_plan {
         int8_t* oz[2] = {nullptr, nullptr};
         int* oz_e[2] = {nullptr, nullptr};
         int oz_slices = 0;
+        // small plans (p.small, L <= 256): only the grouped int8 forward
+        // (fold_i8_route) — even rows [D_even | 0] padded to whole column
+        // tiles, then [0 | W], for 96- [0] and 80-column [1] tiles (5 / 6 slices)
+        bool small = false;
+        std::size_t g_b[2] = {0, 0}, g_map[2] = {0, 0};
+        int g_rows[2] = {0, 0}, g_split[2] = {0, 0};
+        int8_t* g_sl[2] = {nullptr, nullptr};
+        int* g_e[2] = {nullptr, nullptr};
     } fd;
     // NFST fast route (fp64): the reference's own forward algorithm on the GPU
     struct {
@@ -450,6 +458,8 @@ struct dctp_plan {
             for (int i = 0; i < 2; ++i) {
                 if (fd.oz[i]) cudaFree(fd.oz[i]);
                 if (fd.oz_e[i]) cudaFree(fd.oz_e[i]);
+                if (fd.g_sl[i]) cudaFree(fd.g_sl[i]);
+                if (fd.g_e[i]) cudaFree(fd.g_e[i]);
             }
             cudaSetDevice(prev);
         }
@@ -595,7 +605,8 @@ static void build_small(dctp_plan& p, Blob& blob, const ApplyTables& t) {
 static void build_fold(dctp_plan& p, Blob& blob, const ApplyTables& t) {
     const auto& st = p.st;
     const std::size_t n = st.n, K = t.kept_idx.size(), A = t.nu.size();
-    if (p.small || K == 0 || A == 0 || n < 64 || (n & (n - 1)) != 0 || n > (std::size_t{1} << 14)) return;
+    if ((p.small && n > 512) || K == 0 || A == 0 || n < 64 || (n & (n - 1)) != 0 || n > (std::size_t{1} << 14))
+        return;
     for (int j : t.kept_idx)
         if (j % 2 == 0) return;
     std::size_t odd_pass = 0;
@@ -692,6 +703,36 @@ static void build_fold(dctp_plan& p, Blob& blob, const ApplyTables& t) {
     f.sign32 = blob.add(to_f32(sign));
     f.tw64 = add_twiddles<double>(blob, L);
     f.tw32 = add_twiddles<float>(blob, L);
+    f.small = p.small;
+    if (L <= 256) {
+        // the grouped operand of the int8 route: out[:, gmap[r]] = sum_k [y | u]_k Bg[r][k]
+        // with Bg's even rows = sigma / sqrt 2 times the orthonormal DCT-II row of y
+        // (the fold kernel's half-length DCT and emit) and the odd rows = W
+        for (int v = 0; v < 2; ++v) {
+            const std::size_t NT = static_cast<std::size_t>(dctp::dev::ozaki_group_tile(v == 0 ? 5 : 6));
+            const std::size_t E = (to.size() + NT - 1) / NT * NT, rows = E + cols, ldg = 2 * L;
+            std::vector<double> bg(rows * ldg, 0.0);
+            std::vector<int> gmap(rows, -1);
+            for (std::size_t q = 0; q < to.size(); ++q) {
+                const std::size_t k = static_cast<std::size_t>(from[q]);
+                const long double ck = k == 0 ? 1.0L / std::sqrt(2.0L) : 1.0L;
+                for (std::size_t j = 0; j < L; ++j) {
+                    const std::size_t m = ((2 * j + 1) * k) % (4 * L);
+                    bg[q * ldg + j] = static_cast<double>(static_cast<long double>(sign[q]) * std::sqrt(2.0L / L) * ck *
+                                                          std::cos(static_cast<long double>(pi) * m / (2.0L * L)));
+                }
+                gmap[q] = to[q];
+            }
+            for (std::size_t c = 0; c < cols; ++c) {
+                for (std::size_t j = 0; j < L; ++j) bg[(E + c) * ldg + L + j] = w[c * ldw + j];
+                gmap[E + c] = map[c];
+            }
+            f.g_b[v] = blob.add(bg);
+            f.g_map[v] = blob.add(gmap);
+            f.g_rows[v] = static_cast<int>(rows);
+            f.g_split[v] = static_cast<int>(E / NT);
+        }
+    }
     f.on = true;
 }
 
@@ -1138,7 +1179,7 @@ static bool small_dense_route(const dctp_plan* p, std::size_t batch) {
 
 /// DCTP_FOLD=0 turns the folded route off (structured DCT + Cauchy instead).
 static bool fold_route(const dctp_plan* p) {
-    if (!p->fd.on) return false;
+    if (!p->fd.on || p->fd.small) return false;
     const char* e = std::getenv("DCTP_FOLD");
     return !(e && e[0] == '0');
 }
@@ -1163,6 +1204,38 @@ static void rows_by_ozaki(const double* in, std::size_t ld_in, const int8_t* b_s
 static int nfst_dense_slices(const dctp_plan* p, int which);
 static void ensure_nfst_ozaki(const dctp_plan* p, int which, int S, cudaStream_t s);
 
+/// Slice count of the int8 products where the route does not depend on n
+/// (DCTP_OZAKI_SLICES: 5 default, or 6).
+static int ozaki_slice_count() {
+    static const int v = [] {
+        const char* e = std::getenv("DCTP_OZAKI_SLICES");
+        const int k = e ? std::atoi(e) : 5;
+        return (k == 5 || k == 6) ? k : 5;
+    }();
+    return v;
+}
+
+/// Grouped int8 route of small folded plans (C2: n = 256, edge (128, 129)):
+/// one slicing pass writes [y | u] of every row, one persistent CTA-pair
+/// product gives the even (D y) and odd (W u) coefficients — every output row
+/// written by one kernel, no FFT.  Measured against the fused DMMA kernel at
+/// C2 (tools/fold_i8_sweep.py, bench kernel split): 0.167 ms (slicing 0.046 +
+/// product 0.119; the product's operand loads alone take 0.048 — each A
+/// half is re-read by two 96-column tiles, TMEM holds 5 x 96 int32 columns)
+/// vs 0.139 ms, and slower at every batch from 1024 rows; parity with the
+/// fused kernel 6.4e-12.  So the fused kernel stays the route; DCTP_FOLD_I8=1
+/// selects this one (tests keep it correct).
+static bool fold_i8_route(const dctp_plan* p, std::size_t batch, const void* in, const void* out) {
+    const auto& f = p->fd;
+    if (!f.on || !f.small || f.g_b[0] == 0 || batch == 0 || !dctp::dev::ozaki_grouped_supported()) return false;
+    if ((reinterpret_cast<std::uintptr_t>(in) | reinterpret_cast<std::uintptr_t>(out)) % 16 != 0) return false;
+    const char* e = std::getenv("DCTP_FOLD_I8");
+    return e && e[0] == '1';
+}
+
+/// int8 slices of the grouped operand Bg (variant v: 5 / 6 slices), once per plan.
+static void ensure_fold_grouped(const dctp_plan* p, int v, int S, cudaStream_t s);
+
 template <class T>
 static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t batch, cudaStream_t s) {
     if (!p) throw std::invalid_argument("dctp_forward: null plan");
@@ -1184,6 +1257,25 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
             }
             cuda_check(DCTP_LAUNCH("nfst_fwd", s, dctp::dev::nfst_apply(in, out, batch, fast_plan_dev(p), p->flags(s), false, s)),
                        "nfst forward kernel");
+            return;
+        }
+        if (fold_i8_route(p, batch, in, out)) {
+            const auto& f = p->fd;
+            const int S = ozaki_slice_count(), v = S == 5 ? 0 : 1;
+            ensure_fold_grouped(p, v, S, s);
+            const int pm = dctp::dev::ozaki_pad_m(), K2 = 2 * f.L;
+            const std::size_t rows_pad = (batch + pm - 1) / pm * pm;
+            Scratch<int8_t> a_sl(dctp::dev::ozaki_slice_bytes(batch, K2, 128, S, pm), s);
+            Scratch<int> ea(rows_pad, s);
+            cuda_check(DCTP_LAUNCH("fold_slice", s,
+                                   dctp::dev::ozaki_slice_fold(in, n, batch, f.L, 128, S, a_sl.ptr, ea.ptr, p->flags(s),
+                                                               s, pm)),
+                       "fold slicing kernel");
+            cuda_check(DCTP_LAUNCH("fold_i8", s,
+                                   dctp::dev::ozaki_gemm_grouped(a_sl.ptr, ea.ptr, f.g_sl[v], f.g_e[v], batch,
+                                                                 f.g_rows[v], K2, S, out, n,
+                                                                 at<int>(p->blob, f.g_map[v]), f.g_split[v], f.L, s)),
+                       "grouped int8 tensor-core product kernel");
             return;
         }
         // small plans at small batches: one dense product with X^T staged in
@@ -1790,6 +1882,16 @@ static void ensure_ozaki(const dctp_plan* p, int which, int S, cudaStream_t s) {
     d.oz[which] = sl;
     d.oz_e[which] = ex;
     d.oz_slices = S;
+}
+
+static void ensure_fold_grouped(const dctp_plan* p, int v, int S, cudaStream_t s) {
+    auto& f = const_cast<dctp_plan*>(p)->fd;
+    std::lock_guard<std::mutex> lock(p->dense->mu);
+    if (f.g_sl[v]) return;
+    auto [sl, ex] = slice_operand(at<double>(p->blob, f.g_b[v]), 2 * static_cast<std::size_t>(f.L),
+                                  static_cast<std::size_t>(f.g_rows[v]), 2 * f.L, S, s);
+    f.g_sl[v] = sl;
+    f.g_e[v] = ex;
 }
 
 /// int8 slices of the folded route's W (which = 0, cols x L) or W^T (which =

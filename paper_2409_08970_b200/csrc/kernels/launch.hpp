@@ -183,6 +183,21 @@ std::size_t ozaki_slice_bytes(std::size_t rows, int K, int tile_rows, int slices
 template <class T>
 cudaError_t ozaki_slice(const T* in, std::size_t ld, std::size_t rows, int K, const int* a_map, int tile_rows,
                         int slices, int8_t* sl, int* expo, int* flag, cudaStream_t stream, int pad_rows = 0);
+/// Folded rows x (2L samples) -> the sliced K = 2L operand [y | u] (y_j =
+/// x_j + x_{2L-1-j}, u_j = x_j - x_{2L-1-j}), one exponent per row; L % 4 == 0,
+/// L <= 1024, 16-byte aligned rows.
+cudaError_t ozaki_slice_fold(const double* in, std::size_t ld, std::size_t rows, int L, int tile_rows, int slices,
+                             int8_t* sl, int* expo, int* flag, cudaStream_t stream, int pad_rows = 0);
+/// Grouped product on the persistent CTA-pair kernel: output column tiles
+/// (ozaki_group_tile(slices) columns each) below nt_split contract K columns
+/// [0, k_split) of a and bt, the others [k_split, K) — two products with
+/// different operand halves (the fold's D y and W u) in one launch, each
+/// output row written by one kernel; col_map < 0 skips padding columns.
+bool ozaki_grouped_supported();
+int ozaki_group_tile(int slices);
+cudaError_t ozaki_gemm_grouped(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M,
+                               int N, int K, int slices, double* out, std::size_t ld_out, const int* col_map,
+                               int nt_split, int k_split, cudaStream_t stream);
 cudaError_t ozaki_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M, int N,
                        int K, int slices, double* out, std::size_t ld_out, const int* col_map, cudaStream_t stream,
                        const double* fold_add = nullptr, std::size_t ld_add = 0);

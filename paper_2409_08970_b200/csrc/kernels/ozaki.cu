@@ -283,6 +283,85 @@ ozaki_slice_reg_kernel(const double* __restrict__ in, std::size_t ld, std::size_
     }
 }
 
+/// Folded rows (antisymmetric plans): row r of x (2L samples) becomes the K =
+/// 2L operand [y | u], y_j = x_j + x_{2L-1-j}, u_j = x_j - x_{2L-1-j} (j < L),
+/// sliced with one exponent per row (max over both halves) — the A side of
+/// the grouped product that gives the even (D y) and odd (W u) coefficients
+/// of the row in one launch.  A warp per row, 8 rows per CTA; lane l takes 4
+/// consecutive j per step (16-byte loads of x_j.. and of the mirrored x).
+template <int S, int kMaxSteps> // L <= 128 kMaxSteps
+__global__ void __launch_bounds__(256)
+ozaki_slice_fold_kernel(const double* __restrict__ in, std::size_t ld, std::size_t rows, std::size_t rows_pad,
+                        int L, int tile_rows, int8_t* __restrict__ sl, int* __restrict__ expo, int* flag) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const std::size_t r = static_cast<std::size_t>(blockIdx.x) * 8 + warp;
+    if (r >= rows_pad) return;
+    const bool real = r < rows;
+    const double* row = in + (real ? r * ld : 0);
+    const int steps = (L + 127) / 128;
+    double y[kMaxSteps][4], u[kMaxSteps][4];
+    double mx = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < kMaxSteps; ++i) {
+        if (i >= steps) break;
+        const int j = 4 * lane + 128 * i;
+        double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
+        if (real && j < L) {
+            const double2 a0 = __ldg(reinterpret_cast<const double2*>(row + j));
+            const double2 a1 = __ldg(reinterpret_cast<const double2*>(row + j + 2));
+            const double2 b0 = __ldg(reinterpret_cast<const double2*>(row + 2 * L - 4 - j));
+            const double2 b1 = __ldg(reinterpret_cast<const double2*>(row + 2 * L - 2 - j));
+            a[0] = a0.x, a[1] = a0.y, a[2] = a1.x, a[3] = a1.y;
+            b[0] = b1.y, b[1] = b1.x, b[2] = b0.y, b[3] = b0.x; // x_{2L-1-j-q}
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            bad |= !isfinite(a[q]) || !isfinite(b[q]);
+            y[i][q] = a[q] + b[q];
+            u[i][q] = a[q] - b[q];
+            mx = fmax(mx, fmax(fabs(y[i][q]), fabs(u[i][q])));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (__any_sync(0xffffffffu, bad)) {
+        if (lane == 0 && flag) atomicOr(flag, 1);
+        mx = 0.0;
+    }
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);
+    if (lane == 0) expo[r] = e;
+    const double scale = ldexp(127.0, -e);
+    const std::size_t tile = r / tile_rows;
+    const int lr = static_cast<int>(r % tile_rows), nch = (2 * L + CB - 1) / CB;
+    const std::size_t slice_bytes = static_cast<std::size_t>(tile_rows) * CB;
+#pragma unroll
+    for (int i = 0; i < kMaxSteps; ++i) {
+        if (i >= steps) break;
+        const int j = 4 * lane + 128 * i;
+        if (j >= L) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double x = h == 0 ? y[i][q] : u[i][q];
+                v[q] = isfinite(x) ? x * scale : 0.0;
+            }
+            const int k = j + h * L;
+            int8_t* dst = sl + ((tile * nch + k / CB) * S) * slice_bytes + sw64(lr, (k % CB) / 16) + (k % 16);
+#pragma unroll
+            for (int q = 0; q < S; ++q) {
+                uint32_t w = 0u;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) w |= ozaki_digit(v[t]) << (8 * t);
+                *reinterpret_cast<uint32_t*>(dst + q * slice_bytes) = w;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------- GEMM
 
 template <int S, int NT>
@@ -432,6 +511,9 @@ struct SplitSched {
     int* cnt = nullptr;     // per tile, CTA half and epilogue warp: arrival counters (zero at launch)
     int* acc = nullptr;     // ... and that warp's int32 level sums (zero at launch)
     int debug = 0;          // persistent kernel, development knob DCTP_OZAKI_PDEBUG (phase isolation)
+    // grouped product: column tiles < nt_split take K chunks [0, kch_split),
+    // the others [kch_split, nch) (the folded row's y and u halves); -1: off
+    int nt_split = -1, kch_split = 0;
 };
 
 /// Work unit u -> (column tile, pair, chunk range, split slot): whole tiles
@@ -461,6 +543,10 @@ __device__ __forceinline__ Unit unit_of(std::size_t u, const SplitSched& s, int 
     } else {
         w.pair = t % npairs;
         w.nt = static_cast<int>(t / npairs);
+    }
+    if (s.nt_split >= 0) { // grouped product (never split along K)
+        w.kb = w.nt < s.nt_split ? 0 : s.kch_split;
+        w.ke = w.nt < s.nt_split ? s.kch_split : nch;
     }
     return w;
 }
@@ -1257,7 +1343,7 @@ ozaki_gemmp_kernel(const int8_t* __restrict__ a_sl, const int* __restrict__ ea, 
 template <int S, int NT>
 cudaError_t launch_gemmp(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M, int N,
                          int nch, double* out, std::size_t ld_out, const int* col_map, const double* fold_add,
-                         std::size_t ld_add, cudaStream_t stream) {
+                         std::size_t ld_add, cudaStream_t stream, int nt_split = -1, int kch_split = 0) {
     using G = GeoP<S, NT>;
     cudaError_t e = smem_optin(reinterpret_cast<const void*>(ozaki_gemmp_kernel<S, NT, false>), G::kSmem);
     if (e == cudaSuccess) e = smem_optin(reinterpret_cast<const void*>(ozaki_gemmp_kernel<S, NT, true>), G::kSmem);
@@ -1272,7 +1358,13 @@ cudaError_t launch_gemmp(const int8_t* a_sl, const int* ea, const int8_t* b_sl, 
     const int nfast = b_bytes < a_bytes ? 1 : 0;
     const std::size_t tiles = npairs * ntn;
     SplitSched sched;
-    plan_split(tiles, static_cast<std::size_t>(sms / 2), nch, sched);
+    if (nt_split < 0) {
+        plan_split(tiles, static_cast<std::size_t>(sms / 2), nch, sched);
+    } else {
+        sched.full = tiles;
+        sched.nt_split = nt_split;
+        sched.kch_split = kch_split;
+    }
     static const int pdebug = [] {
         const char* v = std::getenv("DCTP_OZAKI_PDEBUG");
         return v ? std::atoi(v) : 0;
@@ -1415,6 +1507,7 @@ int ozaki_tile_n(int slices) {
     return pair_mode() ? nt / 2 : nt;
 }
 int ozaki_pad_m() { return pair_mode() ? 2 * TM : TM; }
+int ozaki_group_tile(int slices) { return slices <= 5 ? 96 : 80; }
 
 std::size_t ozaki_slice_bytes(std::size_t rows, int K, int tile_rows, int slices, int pad_rows) {
     const std::size_t pad = static_cast<std::size_t>(pad_rows > tile_rows ? pad_rows : tile_rows);
@@ -1452,6 +1545,42 @@ template cudaError_t ozaki_slice<double>(const double*, std::size_t, std::size_t
                                          int*, int*, cudaStream_t, int);
 template cudaError_t ozaki_slice<float>(const float*, std::size_t, std::size_t, int, const int*, int, int, int8_t*,
                                         int*, int*, cudaStream_t, int);
+
+cudaError_t ozaki_slice_fold(const double* in, std::size_t ld, std::size_t rows, int L, int tile_rows, int slices,
+                             int8_t* sl, int* expo, int* flag, cudaStream_t stream, int pad_rows) {
+    if (rows == 0) return cudaSuccess;
+    if (L % 4 != 0 || L > 1024 || reinterpret_cast<std::uintptr_t>(in) % 16 != 0 || (ld * sizeof(double)) % 16 != 0)
+        return cudaErrorInvalidValue;
+    const std::size_t pad = static_cast<std::size_t>(pad_rows > tile_rows ? pad_rows : tile_rows);
+    const std::size_t rows_pad = (rows + pad - 1) / pad * pad;
+    const unsigned grid = static_cast<unsigned>((rows_pad + 7) / 8);
+    if (slices != 5 && slices != 6) return cudaErrorInvalidValue;
+    auto pick = [&](auto s5, auto s6) { return slices == 5 ? s5 : s6; };
+    // register arrays sized to the row (one 128-sample step per lane group)
+    auto kern = L <= 128   ? pick(ozaki_slice_fold_kernel<5, 1>, ozaki_slice_fold_kernel<6, 1>)
+                : L <= 256 ? pick(ozaki_slice_fold_kernel<5, 2>, ozaki_slice_fold_kernel<6, 2>)
+                : L <= 512 ? pick(ozaki_slice_fold_kernel<5, 4>, ozaki_slice_fold_kernel<6, 4>)
+                           : pick(ozaki_slice_fold_kernel<5, 8>, ozaki_slice_fold_kernel<6, 8>);
+    kern<<<grid, 256, 0, stream>>>(in, ld, rows, rows_pad, L, tile_rows, sl, expo, flag);
+    return cudaGetLastError();
+}
+
+bool ozaki_grouped_supported() { return pair_mode() && pair_nsub() == 1; }
+
+cudaError_t ozaki_gemm_grouped(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M,
+                               int N, int K, int slices, double* out, std::size_t ld_out, const int* col_map,
+                               int nt_split, int k_split, cudaStream_t stream) {
+    if (M == 0 || N == 0) return cudaSuccess;
+    if (!ozaki_grouped_supported() || k_split % CB != 0) return cudaErrorInvalidValue;
+    const int nch = (K + CB - 1) / CB;
+    if (slices == 5)
+        return launch_gemmp<5, 96>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, nullptr, 0, stream, nt_split,
+                                   k_split / CB);
+    if (slices == 6)
+        return launch_gemmp<6, 80>(a_sl, ea, b_sl, eb, M, N, nch, out, ld_out, col_map, nullptr, 0, stream, nt_split,
+                                   k_split / CB);
+    return cudaErrorInvalidValue;
+}
 
 cudaError_t ozaki_gemm(const int8_t* a_sl, const int* ea, const int8_t* b_sl, const int* eb, std::size_t M, int N,
                        int K, int slices, double* out, std::size_t ld_out, const int* col_map, cudaStream_t stream,

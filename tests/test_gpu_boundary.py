@@ -178,6 +178,30 @@ def test_ozaki_persistent_split_and_one_tile_kernels_agree(P, torch, reference, 
         assert O.parity(outs["split"], want) <= 1e-10
 
 
+def test_grouped_int8_fold_route_matches_reference(P, torch, reference, tmp_path):
+    """The opt-in grouped int8 route of small folded plans (DCTP_FOLD_I8=1:
+    the [y | u] slicing pass and the persistent CTA-pair product with even /
+    odd column-tile groups) meets the fp64 tolerance against the reference on
+    a ragged C2-shape batch and agrees with the default fused kernel."""
+    script = tmp_path / "fi8.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "import paper_2409_08970_b200 as P\n"
+        "plan = P.DctPlusPlan(256, P.RankOneUpdate.edge_delta(128, 129, -0.7), 1e-12)\n"
+        "x = torch.as_tensor(P.fill_signals(13, P.DIST_AR, 256, 1001, 0.95), device='cuda')\n"
+        "np.save(sys.argv[1], plan.forward(x).cpu().numpy())\n")
+    outs = {}
+    for mode in ("0", "1"):
+        f = tmp_path / f"y{mode}.npy"
+        subprocess.run([sys.executable, str(script), str(f)], env=dict(os.environ, DCTP_FOLD_I8=mode), check=True,
+                       timeout=300)
+        outs[mode] = np.load(f)
+    want = reference.plan(256, O.Update(1, -0.7, 128, 129)).forward(P.fill_signals(13, P.DIST_AR, 256, 1001, 0.95))
+    assert O.parity(outs["1"], want) <= 1e-10
+    assert O.parity(outs["1"], outs["0"]) <= 1e-10
+
+
 def test_cuda_graph_capture_and_replay(P, torch):
     """Launches captured into a CUDA graph replay to the same coefficients;
     a non-finite sample fed through the graph raises DomainError at the next

@@ -1,21 +1,14 @@
 #!/bin/bash
-# End-of-round bench set (GPU box): every config through bench.py, the
-# reference arm, written to gpurun_out/final/.
+# End-of-round bench set (GPU box) into gpurun_out/final/: the default bench
+# line (C5 headline + every BASELINE config), the reference arm, the SURVEY
+# 8(f) extras (X6 chain, X7 / X8 NFST route), the C5 shard sweep, clocks.
 set -u
 out=gpurun_out/final
 mkdir -p $out
-python bench.py > $out/bench_final.json 2> $out/bench_final.err
-python bench.py --impl reference > $out/bench_ref_final.json 2> $out/bench_ref_final.err
-for c in 1 3 4 5 6 7 8; do
-    python bench.py --config $c --steps 20 --warmup 5 > $out/bench_c$c.json 2> $out/bench_c$c.err
+python bench.py > $out/bench_final.json 2> $out/bench_final.err; echo "bench rc=$?"
+python bench.py --impl reference > $out/bench_ref_final.json 2> $out/bench_ref_final.err; echo "reference rc=$?"
+for c in X6 X7 X8; do
+    python bench.py --config $c --no-configs --steps 20 --warmup 5 > $out/bench_$c.json 2> $out/bench_$c.err
+    echo "$c rc=$?"
 done
-for f in $out/*.json; do
-    python - "$f" <<'PY'
-import json, sys
-d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
-r = d.get("roofline") or {}
-print(sys.argv[1].split("/")[-1], d.get("ms_per_step"), "%.3g" % d["value"], r.get("kernel"), r.get("frac"),
-      "e2e %.3g" % (d.get("e2e") or {}).get("value", 0), (d.get("cpu_baseline") or {}).get("value"),
-      (d.get("clocks") or {}).get("sm_mhz"), (d.get("clocks") or {}).get("reasons"))
-PY
-done
+python tools/shard_sweep.py > $out/shard_sweep.jsonl 2>&1; echo "shard sweep rc=$?"

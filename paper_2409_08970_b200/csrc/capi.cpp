@@ -1335,6 +1335,29 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
                 return;
             }
         }
+        if constexpr (f32) {
+            // fp32 on the persistent bf16x3 GEMM: the fold kernel writes u's
+            // bf16 hi / lo A image directly (no u round trip, no split pass)
+            const char* tc = std::getenv("DCTP_TC32");
+            const char* bfe = std::getenv("DCTP_TC_BF16");
+            if (!(tc && tc[0] == '0') && !(bfe && bfe[0] == '0') &&
+                dctp::dev::tc_bf16x3_supported(f.L, f.cols, n, out)) {
+                Scratch<unsigned char> img(dctp::dev::tc_bf16x3_a_bytes(batch, f.L), s);
+                dctp::dev::FoldSlices fs;
+                fs.bf = img.ptr;
+                cuda_check(DCTP_LAUNCH("fold_dct", s,
+                                       dctp::dev::dct2_fold_rows<T>(in, n, nullptr, f.L, out, n, even, f.L, batch,
+                                                                    twiddles_at<T>(p->blob, f.tw32), p->flags(s), s,
+                                                                    fs)),
+                           "fold dct kernel");
+                cuda_check(DCTP_LAUNCH("fold_w_bf16x3", s,
+                                       dctp::dev::tc_bf16x3(nullptr, f.L, at<uint16_t>(p->blob, f.w_bf), out, n, batch,
+                                                            f.cols, f.L, p->flags(s), p->num_sms, s,
+                                                            at<int>(p->blob, f.map), nullptr, nullptr, 0, img.ptr)),
+                           "fold bf16x3 kernel");
+                return;
+            }
+        }
         Scratch<T> u(batch * static_cast<std::size_t>(f.L), s);
         cuda_check(DCTP_LAUNCH("fold_dct", s,
                                dctp::dev::dct2_fold_rows<T>(in, n, u.ptr, f.L, out, n, even, f.L, batch,
@@ -1345,16 +1368,6 @@ static void plan_forward(const dctp_plan* p, const T* in, T* out, std::size_t ba
             // fp32: the tcgen05 3xTF32 GEMM (DCTP_TC32=0: the FFMA2 SGEMM with W^T
             // rounded once, twice the DMMA rate)
             const char* tc = std::getenv("DCTP_TC32");
-            const char* bfe = std::getenv("DCTP_TC_BF16");
-            if (!(tc && tc[0] == '0') && !(bfe && bfe[0] == '0') &&
-                dctp::dev::tc_bf16x3_supported(f.L, f.cols, n, out)) {
-                cuda_check(DCTP_LAUNCH("fold_w_bf16x3", s,
-                                       dctp::dev::tc_bf16x3(u.ptr, f.L, at<uint16_t>(p->blob, f.w_bf), out, n, batch,
-                                                            f.cols, f.L, p->flags(s), p->num_sms, s,
-                                                            at<int>(p->blob, f.map))),
-                           "fold bf16x3 kernel");
-                return;
-            }
             const float* wh = at<float>(p->blob, f.w_hi);
             const float* wl = at<float>(p->blob, f.w_lo);
             if (!(tc && tc[0] == '0') && dctp::dev::tc_sgemm3_supported(f.L, f.cols, f.L, f.L, n, u.ptr, wh, wl, out)) {
@@ -1457,22 +1470,36 @@ static void plan_inverse(const dctp_plan* p, const T* in, T* out, std::size_t ba
                 return;
             }
         }
+        if constexpr (f32) {
+            // fp32 on the persistent bf16x3 GEMM: the fold idct kernel also
+            // gathers p's W slots into the GEMM's bf16 A image (no gathered split pass)
+            const char* tc = std::getenv("DCTP_TC32");
+            const char* bfe = std::getenv("DCTP_TC_BF16");
+            if (!(tc && tc[0] == '0') && !(bfe && bfe[0] == '0') &&
+                dctp::dev::tc_bf16x3_supported(f.cols, f.L, n, out, true) && f.L % 4 == 0) {
+                Scratch<unsigned char> img(dctp::dev::tc_bf16x3_a_bytes(batch, f.cols), s);
+                dctp::dev::FoldSlices fs;
+                fs.bf = img.ptr;
+                fs.map = at<int>(p->blob, f.map);
+                fs.K = f.cols;
+                cuda_check(DCTP_LAUNCH("fold_idct", s,
+                                       dctp::dev::idct_rows<T>(nullptr, 0, in, n, even, w.ptr, f.L, f.L, batch,
+                                                               twiddles_at<T>(p->blob, f.tw32), p->flags(s), s, fs)),
+                           "fold idct kernel");
+                cuda_check(DCTP_LAUNCH("fold_wt_bf16x3", s,
+                                       dctp::dev::tc_bf16x3(nullptr, static_cast<int>(n), at<uint16_t>(p->blob, f.wt_bf),
+                                                            out, n, batch, f.L, f.cols, p->flags(s), p->num_sms, s,
+                                                            nullptr, nullptr, w.ptr, f.L, img.ptr)),
+                           "fold bf16x3 kernel");
+                return;
+            }
+        }
         cuda_check(DCTP_LAUNCH("fold_idct", s,
                                dctp::dev::idct_rows<T>(nullptr, 0, in, n, even, w.ptr, f.L, f.L, batch,
                                                        twiddles_at<T>(p->blob, f32 ? f.tw32 : f.tw64), p->flags(s), s)),
                    "fold idct kernel");
         if constexpr (f32) {
             const char* tc = std::getenv("DCTP_TC32");
-            const char* bfe = std::getenv("DCTP_TC_BF16");
-            if (!(tc && tc[0] == '0') && !(bfe && bfe[0] == '0') &&
-                dctp::dev::tc_bf16x3_supported(f.cols, f.L, n, out, true) && f.L % 4 == 0) {
-                cuda_check(DCTP_LAUNCH("fold_wt_bf16x3", s,
-                                       dctp::dev::tc_bf16x3(in, static_cast<int>(n), at<uint16_t>(p->blob, f.wt_bf), out,
-                                                            n, batch, f.L, f.cols, p->flags(s), p->num_sms, s, nullptr,
-                                                            at<int>(p->blob, f.map), w.ptr, f.L)),
-                           "fold bf16x3 kernel");
-                return;
-            }
             const float* th = at<float>(p->blob, f.wt_hi);
             const float* tl = at<float>(p->blob, f.wt_lo);
             const int ldt = (f.cols + 3) / 4 * 4;

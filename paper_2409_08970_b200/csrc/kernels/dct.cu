@@ -11,6 +11,8 @@
 // slots of the DCT+ output), so the pass-through never needs its own launch.
 // Other n: a direct O(n^2) kernel over a cos(pi m / 2n) table.
 #include <algorithm>
+
+#include <cuda_bf16.h>
 #include <cmath>
 
 #include "kernels/common.cuh"
@@ -132,6 +134,40 @@ __device__ __forceinline__ void slice_rows(const double* src, int lds, int rows,
     }
 }
 
+__device__ __forceinline__ uint32_t bf16_pair(float a, float b) {
+    return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(a))) |
+           (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(b))) << 16);
+}
+
+/// fp32 rows (row r at src + r * lds, K values) -> the bf16x3 GEMM's A image
+/// (tc_bf16x3_a_bytes layout: 128-row tiles x 32-column chunks x hi | lo x
+/// 128 rows x 64 B, SWIZZLE_64B rows; a = hi + lo, hi = bf16(a), lo =
+/// bf16(a - hi) — the split kernel's arithmetic), 8-value groups.
+__device__ __forceinline__ void bf16_rows(const float* src, int lds, int rows, int K, std::size_t b0,
+                                          unsigned char* img) {
+    const int nch = (K + 31) / 32, groups = nch * 4;
+    int r = threadIdx.x / groups, kg = threadIdx.x - r * groups;
+    for (; r < rows; step_rk(r, kg, kThreads, groups)) {
+        const int k0 = 8 * kg;
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = k0 + u < K ? src[r * lds + k0 + u] : 0.f;
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float h0 = __bfloat162float(__float2bfloat16_rn(v[2 * q]));
+            const float h1 = __bfloat162float(__float2bfloat16_rn(v[2 * q + 1]));
+            hi[q] = bf16_pair(h0, h1);
+            lo[q] = bf16_pair(v[2 * q] - h0, v[2 * q + 1] - h1);
+        }
+        const std::size_t grow = b0 + r;
+        unsigned char* blk = img + ((grow >> 7) * nch + (k0 >> 5)) * 16384 + sw64_int8(static_cast<int>(grow & 127),
+                                                                                         (k0 & 31) >> 3);
+        *reinterpret_cast<uint4*>(blk) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(blk + 8192) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+}
+
 /// FOLD (antisymmetric plans): the input rows hold 2n samples; the kernel
 /// writes u_j = x_j - x_{2n-1-j} to `hat` and transforms y_j = x_j + x_{2n-1-j}
 /// (length n), whose DCT gives the even coefficients of the full row.  With
@@ -150,6 +186,8 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
     T* sh = reinterpret_cast<T*>(nat); // real output rows (stride n) once `nat` is consumed
     T* ush = reinterpret_cast<T*>(work + rows_per_cta * ld); // u rows (fs.sl), then row maxima
     const bool slice = FOLD && sizeof(T) == 8 && fs.sl != nullptr;
+    const bool tobf = FOLD && sizeof(T) == 4 && fs.bf != nullptr; // u -> the bf16x3 A image (fp32)
+    const bool to_smem = slice || tobf;                            // u rows stay in shared memory
     const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * rows_per_cta;
     const int rows = static_cast<int>(min(static_cast<std::size_t>(rows_per_cta), batch - b0));
 
@@ -165,7 +203,7 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
     // (j+3, j+1) each become one complex store
     // (fp32 only: the fp64 variant measured slower, 0.105 -> 0.123 ms at C3)
     const bool vec4 = sizeof(T) == 4 && n % 4 == 0 && reinterpret_cast<std::uintptr_t>(in) % 16 == 0 && (ld_in * sizeof(T)) % 16 == 0 &&
-                      (slice || !FOLD || (reinterpret_cast<std::uintptr_t>(hat) % 16 == 0 && (ld_hat * sizeof(T)) % 16 == 0));
+                      (to_smem || !FOLD || (reinterpret_cast<std::uintptr_t>(hat) % 16 == 0 && (ld_hat * sizeof(T)) % 16 == 0));
     if (vec4) {
         constexpr int U4 = 4;
         const int n4 = n >> 2, logn4 = logn - 2;
@@ -202,7 +240,7 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
                     }
                 }
                 if constexpr (FOLD) {
-                    if (slice)
+                    if (to_smem)
                         store4(ush + r * n + j0, uu);
                     else
                         store4(hat + (b0 + r) * ld_hat + j0, uu);
@@ -230,7 +268,7 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
             T v = xv[u];
             if constexpr (FOLD) {
                 bad |= !finite_val(xm[u]);
-                if (slice)
+                if (to_smem)
                     ush[r * n + j] = xv[u] - xm[u];
                 else
                     hat[(b0 + r) * ld_hat + j] = xv[u] - xm[u];
@@ -243,6 +281,9 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
     if (bad) atomicOr(flag, 1);
     __syncthreads();
 
+    if constexpr (FOLD && sizeof(T) == 4) {
+        if (tobf) bf16_rows(reinterpret_cast<const float*>(ush), n, rows, n, b0, fs.bf);
+    }
     if constexpr (FOLD) {
         if (slice) { // u -> int8 digits (ozaki_slice_kernel's arithmetic), per row
             double* rmax = reinterpret_cast<double*>(ush + rows * n);
@@ -391,6 +432,32 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
             if (nf) atomicOr(flag, 1);
             __syncthreads();
             slice_rows_to_tiles(g, rows, fs.K, b0, fs, rmax);
+        }
+    }
+
+    if constexpr (sizeof(T) == 4) {
+        if (fs.bf != nullptr) { // gathered W slots -> the bf16x3 A image (no gathered split pass)
+            float* g = reinterpret_cast<float*>(work + rows_per_cta * ld);
+            constexpr int U = 8;
+            bool nf = false;
+            int r0 = threadIdx.x / fs.K, k0 = threadIdx.x - r0 * fs.K;
+            for (int t0 = threadIdx.x; t0 < rows * fs.K; t0 += U * kThreads) {
+                float v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    v[u] = r0 < rows ? p[(b0 + r0) * ld_p + __ldg(fs.map + k0)] : 0.f;
+                    step_rk(r0, k0, kThreads, fs.K);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (t0 + u * kThreads < rows * fs.K) {
+                        nf |= !isfinite(v[u]);
+                        g[t0 + u * kThreads] = v[u];
+                    }
+            }
+            if (nf) atomicOr(flag, 1);
+            __syncthreads();
+            bf16_rows(g, fs.K, rows, fs.K, b0, fs.bf);
         }
     }
 
@@ -590,10 +657,10 @@ cudaError_t dct2_fold_rows(const T* in, std::size_t ld_in, T* u, std::size_t ld_
                            cudaStream_t stream, FoldSlices fs) {
     if (batch == 0) return cudaSuccess;
     if (!is_pow2(n) || n < 2) return cudaErrorInvalidValue;
-    if (fs.sl && sizeof(T) != 8) return cudaErrorInvalidValue;
+    if ((fs.sl && sizeof(T) != 8) || (fs.bf && sizeof(T) != 4)) return cudaErrorInvalidValue;
     const int rows = rows_per_cta_for<T>(n);
-    const std::size_t smem =
-        fft_smem_bytes<T>(n, rows) + (fs.sl ? static_cast<std::size_t>(rows) * (n * sizeof(T) + sizeof(double)) : 0);
+    const std::size_t smem = fft_smem_bytes<T>(n, rows) +
+                             ((fs.sl || fs.bf) ? static_cast<std::size_t>(rows) * (n * sizeof(T) + sizeof(double)) : 0);
     auto kern = dct2_fft_kernel<T, true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -610,10 +677,11 @@ cudaError_t idct_rows(const T* d, std::size_t ld_d, const T* p, std::size_t ld_p
     if (batch == 0) return cudaSuccess;
     if (is_pow2(n) && n >= 2) {
         const int rows = rows_per_cta_for<T>(n);
-        if (fs.sl && sizeof(T) != 8) return cudaErrorInvalidValue;
+        if ((fs.sl && sizeof(T) != 8) || (fs.bf && sizeof(T) != 4)) return cudaErrorInvalidValue;
         const std::size_t smem =
             fft_smem_bytes<T>(n, rows) +
-            (fs.sl ? static_cast<std::size_t>(rows) * (static_cast<std::size_t>(fs.K) + 1) * sizeof(double) : 0);
+            (fs.sl ? static_cast<std::size_t>(rows) * (static_cast<std::size_t>(fs.K) + 1) * sizeof(double) : 0) +
+            (fs.bf ? static_cast<std::size_t>(rows) * static_cast<std::size_t>(fs.K) * sizeof(float) : 0);
         auto kern = idct_fft_kernel<T>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));

@@ -54,6 +54,9 @@ struct FoldSlices {
     int S = 0, nch = 0, tile_rows = 0;
     const int* map = nullptr; // idct_rows: the K gathered columns of p to slice (the folded inverse's W slots)
     int K = 0;
+    // fp32: the same values leave as the bf16x3 GEMM's A image instead (hi /
+    // lo bf16 halves, tc_bf16x3_a_bytes layout) — no u round trip / split pass
+    unsigned char* bf = nullptr;
 };
 
 /// Folded forward of antisymmetric plans: rows of 2n samples x; writes
@@ -275,7 +278,13 @@ bool tc_bf16x3_supported(int K, int N, std::size_t ldc, const void* C, bool fold
 std::vector<uint16_t> tc_bf16x3_swizzle_b(const double* bt, int N, int K, int ldb);
 cudaError_t tc_bf16x3(const float* A, int lda, const uint16_t* b_sw, float* C, std::size_t ldc, std::size_t M, int N,
                       int K, int* flag, int num_sms, cudaStream_t stream, const int* col_map = nullptr,
-                      const int* a_map = nullptr, const float* fold_add = nullptr, std::size_t ld_add = 0);
+                      const int* a_map = nullptr, const float* fold_add = nullptr, std::size_t ld_add = 0,
+                      const unsigned char* a_img = nullptr);
+/// Bytes of the bf16x3 GEMM's A image for M rows of K columns (128-row tiles
+/// x 32-column chunks x hi | lo x 128 rows x 64 B, SWIZZLE_64B rows) — what
+/// the fp32 fold kernels write when FoldSlices::bf is set; pass it to
+/// tc_bf16x3 as a_img (A and a_map are then unused).
+std::size_t tc_bf16x3_a_bytes(std::size_t M, int K);
 
 /// out[b, c] = sum_k in[b, k] xt[c, k] for n in {16, 32, 64, 128}: one CTA
 /// per 32 signals, X^T staged in shared memory, m8n8k4 DMMA (small_dense.cu)

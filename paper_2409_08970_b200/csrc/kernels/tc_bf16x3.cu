@@ -432,6 +432,10 @@ tc_bf16x3_kernel(const unsigned char* __restrict__ a_sw, const unsigned char* __
 
 } // namespace
 
+std::size_t tc_bf16x3_a_bytes(std::size_t M, int K) {
+    return (M + BM - 1) / BM * static_cast<std::size_t>((K + KC - 1) / KC) * kAChunk;
+}
+
 bool tc_bf16x3_supported(int K, int N, std::size_t ldc, const void* C, bool fold) {
     return K > 0 && N > 0 && ldc % 4 == 0 && reinterpret_cast<std::uintptr_t>(C) % 16 == 0 && (!fold || N % 4 == 0);
 }
@@ -494,7 +498,7 @@ static bool c_tensor_map(float* C, std::size_t ldc, std::size_t M, int N, CUtens
 
 cudaError_t tc_bf16x3(const float* A, int lda, const uint16_t* b_sw, float* C, std::size_t ldc, std::size_t M, int N,
                       int K, int* flag, int num_sms, cudaStream_t stream, const int* col_map, const int* a_map,
-                      const float* fold_add, std::size_t ld_add) {
+                      const float* fold_add, std::size_t ld_add, const unsigned char* a_img) {
     if (M == 0 || N == 0) return cudaSuccess;
     if (K <= 0) return cudaErrorInvalidValue;
     const int nch = (K + KC - 1) / KC;
@@ -502,12 +506,15 @@ cudaError_t tc_bf16x3(const float* A, int lda, const uint16_t* b_sw, float* C, s
     if (ntm >= (1ull << 32)) return cudaErrorInvalidValue;
     cudaError_t e = cudaSuccess;
     unsigned char* a_sw = nullptr;
-    e = cudaMallocAsync(reinterpret_cast<void**>(&a_sw), ntm * nch * static_cast<std::size_t>(kAChunk), stream);
-    if (e != cudaSuccess) return e;
-    const std::size_t rows_pad = ntm * BM, work = rows_pad * nch * (KC / 8);
-    bf16x3_split_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(A, lda, M, rows_pad, K, nch,
-                                                                                      a_map, a_sw);
-    e = cudaGetLastError();
+    if (!a_img) {
+        e = cudaMallocAsync(reinterpret_cast<void**>(&a_sw), ntm * nch * static_cast<std::size_t>(kAChunk), stream);
+        if (e != cudaSuccess) return e;
+        const std::size_t rows_pad = ntm * BM, work = rows_pad * nch * (KC / 8);
+        bf16x3_split_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(A, lda, M, rows_pad, K,
+                                                                                          nch, a_map, a_sw);
+        e = cudaGetLastError();
+    }
+    const unsigned char* a_use = a_img ? a_img : a_sw;
     if (e == cudaSuccess) {
         const unsigned ntn = static_cast<unsigned>((N + BN - 1) / BN);
         const unsigned long long tiles = static_cast<unsigned long long>(ntm) * ntn;
@@ -531,7 +538,7 @@ cudaError_t tc_bf16x3(const float* A, int lda, const uint16_t* b_sw, float* C, s
         auto launch = [&](auto kern, int smem) {
             cudaError_t r = smem_optin(reinterpret_cast<const void*>(kern), smem);
             if (r != cudaSuccess) return r;
-            kern<<<grid, kThreads, smem, stream>>>(a_sw, reinterpret_cast<const unsigned char*>(b_sw), ep, M, N, nch,
+            kern<<<grid, kThreads, smem, stream>>>(a_use, reinterpret_cast<const unsigned char*>(b_sw), ep, M, N, nch,
                                                    static_cast<unsigned>(ntm), ntn, flag, cmap);
             return cudaGetLastError();
         };
@@ -546,7 +553,7 @@ cudaError_t tc_bf16x3(const float* A, int lda, const uint16_t* b_sw, float* C, s
                 : mode == 1 ? launch(tc_bf16x3_kernel<false, 1>, Lay<false>::kSmem)
                             : launch(tc_bf16x3_kernel<false, 0>, Lay<false>::kSmem);
     }
-    cudaFreeAsync(a_sw, stream);
+    if (a_sw) cudaFreeAsync(a_sw, stream);
     return e;
 }
 

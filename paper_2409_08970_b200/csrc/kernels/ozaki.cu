@@ -199,11 +199,10 @@ ozaki_slice_kernel(const T* __restrict__ in, std::size_t ld, std::size_t rows, s
 /// signals): one CTA per row keeps the row in registers (thread t: 8-value
 /// groups k = 8 t + 2048 i), so it is read once — all loads in flight before
 /// the maximum — and each group leaves as one 8-byte store per slice plane.
-template <int S>
+template <int S, int G> // G groups of 8 per thread: rows up to 256 x 8 x G samples
 __global__ void __launch_bounds__(256)
 ozaki_slice_reg_kernel(const double* __restrict__ in, std::size_t ld, std::size_t rows, int K, int nch,
                        int tile_rows, int8_t* __restrict__ sl, int* __restrict__ expo, int* flag) {
-    constexpr int G = 4; // groups of 8 per thread: 256 x 8 x 4 = 8192
     __shared__ double red[8];
     __shared__ int red_bad[8];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -1526,8 +1525,16 @@ cudaError_t ozaki_slice(const T* in, std::size_t ld, std::size_t rows, int K, co
     const int vec = !a_map && reinterpret_cast<std::uintptr_t>(in) % 16 == 0 && (ld * sizeof(T)) % 16 == 0;
     if (rows_pad >= (1ull << 31)) return cudaErrorInvalidValue;
     if constexpr (sizeof(T) == 8) {
-        if (K > 2048 && nch * CB <= 8192 && vec && (slices == 5 || slices == 6)) { // the row held in registers
-            auto kern = slices == 5 ? ozaki_slice_reg_kernel<5> : ozaki_slice_reg_kernel<6>;
+        // rows of 1025 .. 8192 samples held in registers, one CTA per row
+        // (C5: 0.065 -> 0.050 ms; X8's 2048-sample rows 0.076 -> 0.048; at
+        // 1024 samples half the threads would idle: 0.062 -> 0.068, so the
+        // warp-per-row kernel keeps them)
+        if (K > 1024 && nch * CB <= 8192 && vec && (slices == 5 || slices == 6)) {
+            const int G = nch * CB <= 2048 ? 1 : (nch * CB <= 4096 ? 2 : 4);
+            auto kern = slices == 5 ? (G == 1 ? ozaki_slice_reg_kernel<5, 1>
+                                              : G == 2 ? ozaki_slice_reg_kernel<5, 2> : ozaki_slice_reg_kernel<5, 4>)
+                                    : (G == 1 ? ozaki_slice_reg_kernel<6, 1>
+                                              : G == 2 ? ozaki_slice_reg_kernel<6, 2> : ozaki_slice_reg_kernel<6, 4>);
             kern<<<static_cast<unsigned>(rows_pad), 256, 0, stream>>>(in, ld, rows, K, nch, tile_rows, sl, expo,
                                                                       flag);
             return cudaGetLastError();

@@ -33,6 +33,7 @@ cap c5_dense_i8 C5 ozaki_gemm2 2
 cap c5_dense_i8_256rows C5 ozaki_gemm2 2 256
 cap x6_chain_i8 X6 ozaki_gemm 2
 cap x7_nfst_i8 X7 ozaki_gemm 2
+cap x8_slice X8 ozaki_slice 2
 python tools/ncu_collect.py $out $out/ncu_summary_final.json > $out/collect.log 2>&1; echo "collect rc=$?"
 for f in $out/*.ncu-rep; do
     case $(basename $f) in c5_dense_i8.ncu-rep|c3_fold_w_i8.ncu-rep|c4_bf16x3.ncu-rep) ;; *) rm -f $f ;; esac

@@ -67,10 +67,6 @@ __device__ __forceinline__ void butterfly<4>(double2 (&v)[4]) {
     v[3] = make_double2(a1.x - a3.x, a1.y - a3.y);
 }
 
-__device__ __forceinline__ void producer_sync() {
-    asm volatile("bar.sync 1, %0;\n" ::"n"(kProducerThreads) : "memory");
-}
-
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 2, %0;\n" ::"n"(32 * kConsumerWarps) : "memory");
 }
@@ -103,10 +99,6 @@ __device__ __forceinline__ void lane_loop(int lane, F&& f) {
         const int t = lane + 32 * (TOTAL / 32);
         if (t < TOTAL) f(t);
     }
-}
-
-__device__ __forceinline__ bool non_finite(double v) {
-    return ((__double_as_longlong(v) >> 52) & 0x7ff) == 0x7ff; // integer test: keeps the fp64 pipe free
 }
 
 /// One Stockham (autosort) pass (P >= 1) over the SPW signals one producer

@@ -1733,13 +1733,15 @@ static void host_roundtrip(int device, std::size_t batch, std::size_t in_row, st
                            T* h_out, F&& run) {
     if (!h_in || !h_out) throw std::invalid_argument("host buffer is null");
     DeviceScope scope(device);
-    const int slots = static_cast<int>(std::min<std::size_t>(env_size("DCTP_HOST_SLOTS", 3), kMaxHostSlots));
+    // defaults from tools/e2e_probe.py on the B200 box: 16 MB chunks ramping
+    // from 4 MB (floor 64 rows), 4 slots — C5 e2e 3.54 -> 3.48 ms, C2 3.24 -> 3.22
+    const int slots = static_cast<int>(std::min<std::size_t>(env_size("DCTP_HOST_SLOTS", 4), kMaxHostSlots));
     const std::size_t row_bytes = std::max(in_row, out_row) * sizeof(T);
-    const std::size_t floor_rows = env_size("DCTP_HOST_MIN_ROWS", 256);
+    const std::size_t floor_rows = env_size("DCTP_HOST_MIN_ROWS", 64);
     const std::size_t max_rows =
         std::max<std::size_t>(floor_rows, (env_size("DCTP_HOST_CHUNK_MB", 16) << 20) / row_bytes); // tuning knobs
     const std::size_t min_rows = std::min(
-        max_rows, std::max<std::size_t>(floor_rows, (env_size("DCTP_HOST_CHUNK_MIN_MB", 2) << 20) / row_bytes));
+        max_rows, std::max<std::size_t>(floor_rows, (env_size("DCTP_HOST_CHUNK_MIN_MB", 4) << 20) / row_bytes));
     // Chunk schedule: sizes double from min_rows up to max_rows at the head and
     // mirror that ramp at the tail, so the pipeline fills and drains with small
     // chunks while the middle runs few, large ones (every kernel launch costs a

@@ -93,7 +93,7 @@ print(json.dumps({"ms": ms}))
 if __name__ == "__main__":
     print(json.dumps({"copy_bw": copy_bw()}))
     wl = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-    for mb, mn, slots, floor in ((16, 2, 3, 256), (16, 1, 3, 16), (16, 2, 3, 16), (8, 1, 3, 16), (32, 1, 3, 16),
-                                 (16, 1, 4, 16), (8, 1, 4, 16), (4, 1, 4, 16)):
+    for mb, mn, slots, floor in ((16, 2, 3, 256), (16, 4, 4, 64), (16, 4, 6, 64), (16, 8, 6, 128), (16, 2, 6, 32),
+                                 (32, 4, 6, 64), (16, 16, 6, 256), (8, 4, 6, 64)):
         print(json.dumps({"wl": wl, "staged_chunk_mb": mb, "min_mb": mn, "slots": slots, "floor": floor,
                           **host_entry(mb, slots, 0, min_mb=mn, wl=wl, floor=floor)}))

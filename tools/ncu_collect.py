@@ -1,5 +1,5 @@
-"""Collect the ncu --set full captures of tools/ncu_all.sh into one summary
-(profiles/<round>/ncu_summary.json): per kernel the duration, DRAM traffic,
+"""Collect the ncu --set full captures of tools/ncu_final.sh into one summary
+(profiles/<round>/ncu_summary_final.json): per kernel the duration, DRAM traffic,
 pipe activity and occupancy the rooflines in DESIGN.md quote.
 usage: python tools/ncu_collect.py gpurun_out/ncu profiles/r02/ncu_summary.json"""
 import csv

@@ -201,11 +201,11 @@ dct2_fft_kernel(const T* __restrict__ in, std::size_t ld_in, T* __restrict__ hat
     // 16-byte rows: four consecutive samples (and their four mirrors) per
     // thread step, vector loads and stores; Makhoul pairs (j, j+2) and
     // (j+3, j+1) each become one complex store
-    // (fp32 only: the fp64 variant measured slower, 0.105 -> 0.123 ms at C3)
-    const bool vec4 = sizeof(T) == 4 && n % 4 == 0 && reinterpret_cast<std::uintptr_t>(in) % 16 == 0 && (ld_in * sizeof(T)) % 16 == 0 &&
+    // (fp64: two steps in flight per thread — four measured slower, 0.105 -> 0.123 ms at C3)
+    const bool vec4 = n % 4 == 0 && reinterpret_cast<std::uintptr_t>(in) % 16 == 0 && (ld_in * sizeof(T)) % 16 == 0 &&
                       (to_smem || !FOLD || (reinterpret_cast<std::uintptr_t>(hat) % 16 == 0 && (ld_hat * sizeof(T)) % 16 == 0));
     if (vec4) {
-        constexpr int U4 = 4;
+        constexpr int U4 = sizeof(T) == 8 ? 2 : 4;
         const int n4 = n >> 2, logn4 = logn - 2;
         for (int t0 = threadIdx.x; t0 < rows * n4; t0 += U4 * kThreads) {
             T xv[U4][4], xm[U4][4];

@@ -404,8 +404,60 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
     T* sh = reinterpret_cast<T*>(work); // the real coefficients, consumed before the FFT writes `work`
     const std::size_t b0 = static_cast<std::size_t>(blockIdx.x) * rows_per_cta;
     const int rows = static_cast<int>(min(static_cast<std::size_t>(rows_per_cta), batch - b0));
+    // The folded inverse (zero d rows, p's W slots gathered for the product):
+    // both gathers from p — the W slots into g, the even slots into the
+    // IDCT input — with all their loads in flight together (one global
+    // round trip per CTA instead of two), then the W slots leave as the
+    // product's A image (int8 digits in fp64, bf16 halves in fp32).
+    const bool comb = !d && ((sizeof(T) == 8 && fs.sl != nullptr) || (sizeof(T) == 4 && fs.bf != nullptr));
+    if (comb) {
+        for (int t = threadIdx.x; t < (rows * n * static_cast<int>(sizeof(T))) / 16; t += kThreads)
+            reinterpret_cast<uint4*>(sh)[t] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+        T* g = reinterpret_cast<T*>(work + rows_per_cta * ld);
+        constexpr int U = 8;
+        const int tot_o = rows * fs.K, tot_e = rows * emit.count;
+        int r0 = threadIdx.x / fs.K, k0 = threadIdx.x - r0 * fs.K;
+        int re = emit.count > 0 ? threadIdx.x / emit.count : rows, ee = emit.count > 0 ? threadIdx.x - re * emit.count : 0;
+        bool nf = false;
+        for (int t0 = 0; t0 < max(tot_o, tot_e); t0 += U * kThreads) {
+            T vo[U], ve[U];
+            int ri[U], ei[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                vo[u] = r0 < rows ? p[(b0 + r0) * ld_p + __ldg(fs.map + k0)] : T(0);
+                step_rk(r0, k0, kThreads, fs.K);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                ri[u] = re;
+                ei[u] = ee;
+                ve[u] = re < rows ? p[(b0 + re) * ld_p + __ldg(emit.from + ee)] : T(0);
+                if (emit.count > 0) step_rk(re, ee, kThreads, emit.count);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int t = t0 + u * kThreads + static_cast<int>(threadIdx.x);
+                if (t < tot_o) {
+                    nf |= !finite_val(vo[u]);
+                    g[t] = vo[u];
+                }
+                if (ri[u] < rows) {
+                    nf |= !finite_val(ve[u]);
+                    sh[ri[u] * n + __ldg(emit.to + ei[u])] = __ldg(emit.sign + ei[u]) * ve[u];
+                }
+            }
+        }
+        if (nf) atomicOr(flag, 1);
+        __syncthreads();
+        if constexpr (sizeof(T) == 8)
+            slice_rows_to_tiles(reinterpret_cast<const double*>(g), rows, fs.K, b0, fs,
+                                reinterpret_cast<double*>(g) + rows_per_cta * fs.K);
+        else
+            bf16_rows(reinterpret_cast<const float*>(g), fs.K, rows, fs.K, b0, fs.bf);
+    }
     if constexpr (sizeof(T) == 8) {
-        if (fs.sl != nullptr) { // gathered values into the extra shared rows, then their digits
+        if (fs.sl != nullptr && !comb) { // gathered values into the extra shared rows, then their digits
             double* g = reinterpret_cast<double*>(work + rows_per_cta * ld);
             double* rmax = g + rows_per_cta * fs.K;
             constexpr int U = 8;
@@ -436,7 +488,7 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
     }
 
     if constexpr (sizeof(T) == 4) {
-        if (fs.bf != nullptr) { // gathered W slots -> the bf16x3 A image (no gathered split pass)
+        if (fs.bf != nullptr && !comb) { // gathered W slots -> the bf16x3 A image (no gathered split pass)
             float* g = reinterpret_cast<float*>(work + rows_per_cta * ld);
             constexpr int U = 8;
             bool nf = false;
@@ -465,7 +517,9 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
     const T scale = static_cast<T>(sqrt(2.0 / n));
     const T dc_scale = static_cast<T>(2.0 / sqrt(static_cast<double>(n)));
     constexpr int U = 8; // independent loads in flight per thread
-    if (!d) { // zero d rows (the folded inverse): plain 16-byte zero stores
+    if (comb) {
+        // sh already holds the even slots (above)
+    } else if (!d) { // zero d rows (the folded inverse): plain 16-byte zero stores
         for (int t = threadIdx.x; t < (rows * n * static_cast<int>(sizeof(T))) / 16; t += kThreads)
             reinterpret_cast<uint4*>(sh)[t] = make_uint4(0u, 0u, 0u, 0u);
     } else
@@ -482,7 +536,7 @@ idct_fft_kernel(const T* __restrict__ d, std::size_t ld_d, const T* __restrict__
     }
     __syncthreads();
     bool bad = false;
-    if (emit.count > 0) {
+    if (emit.count > 0 && !comb) {
         int re = threadIdx.x / emit.count, ee = threadIdx.x - re * emit.count;
         for (int t0 = threadIdx.x; t0 < rows * emit.count; t0 += U * kThreads) {
             T v[U];

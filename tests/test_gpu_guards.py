@@ -59,7 +59,7 @@ CASES = {
     "fused_pingpong_n256": (256, ("edge_delta", 128, 129, -0.7), ("f64", "f32"), ("forward", "inverse")),
     "fold_n1024": (1024, ("edge_delta", 1, 1024, 1.0), ("f64", "f32"), ("forward", "inverse")),
     "nfst_n1024": (1024, ("self_loop", 1, 0.5), ("f64",), ("forward", "inverse")),
-    "structured_n512": (512, ("self_loop", 1, 2.0), ("f64", "f32"), ("forward", "inverse")),
+    "selfloop_n512": (512, ("self_loop", 1, 2.0), ("f64", "f32"), ("forward", "inverse")),  # NFST / structured routes
 }
 
 
